@@ -1,0 +1,257 @@
+/*
+ * fp8train.h -- C-ABI of the B200-native dynamically scaled Float8Linear step.
+ *
+ * Source of the operations: TorchAO (arXiv 2507.16099) §2.1 "FP8 Training"
+ * and Appendix A "TorchAO FP8 Scaling Recipes"
+ * (PAPER.md:592-599); MX formats from Appendix E.  The paper
+ * defines the recipes in prose; the exact arithmetic each call performs is
+ * written out in DESIGN.md "Readings" (mirrors SURVEY.md §8c) and
+ * cross-referenced below as R-cN.
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ *  - All tensor pointers are DEVICE pointers (except where a parameter is
+ *    documented as host).  Every compute call is asynchronous on `stream`
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream) and never
+ *    synchronises the host.  amax and scales live in device memory only
+ *    (dynamic scaling).
+ *  - Ownership: the caller owns every buffer.  The library never allocates or
+ *    frees device memory inside these calls; temporaries come from the
+ *    caller's workspace, sized by the *_bytes() helpers.
+ *  - Errors: argument, shape and alignment checks run BEFORE any launch and
+ *    return a status with no partial work.  Launch failures -> FP8_ECUDA,
+ *    NCCL failures -> FP8_ENCCL.  Asynchronous device faults surface at the
+ *    caller's next synchronisation, as usual in CUDA.  fp8_last_error()
+ *    returns a thread-local message for the last non-OK status.
+ *  - Layout: every matrix is row-major with a leading dimension `ld` in
+ *    elements.  FP8 code buffers (`q`, `q_t`) are dense (ld = cols, resp.
+ *    ld = rows for the transposed copy).
+ *  - Alignment: pointers 16-byte aligned; rows, cols >= 16 and multiples of
+ *    16; ld * element_size a multiple of 16.  MX (block-32) operands need
+ *    rows and cols multiples of 128 (the E8M0 blocked layout below).
+ *    Violations -> FP8_EALIGN.
+ *  - Inputs must be finite (PAPER.md:281 recipes assume it; R-c9).  NaN
+ *    propagates through amax; it is not detected.
+ *  - Thread safety: re-entrant; no mutable global state beyond cached device
+ *    attributes, the lazily resolved cuTensorMapEncodeTiled entry point and
+ *    the thread-local error string.
+ *
+ * Number formats (R-c1, R-c2, R-c10, R-c11)
+ *  - FP8_E4M3: "FN" variant, no inf, NaN 0x7F/0xFF, max 448.
+ *  - FP8_E5M2: IEEE-like, inf 0x7C/0xFC, max 57344.
+ *  - cast = satRNE(RN32(x * s)): the fp32 product rounded first, then round to
+ *    nearest even with saturation to +-max; sign preserved (-0 -> 0x80);
+ *    subnormals kept.
+ *  - scale s = RN32(fmax / max(amax, 1e-12f)) (multiplicative, fp8 ~= x*s;
+ *    R-c3, R-c5, R-c6).  GEMM epilogues multiply by 1/s.
+ *  - E8M0 (MX): code c -> 2^(c-127).  FLOOR: c = clamp(floor(log2 amax) -
+ *    emax + 127, 0, 254) (emax 8 for e4m3, 15 for e5m2); RCEIL: c =
+ *    clamp(127 + ceil(log2(amax / fmax)), 0, 254); zero block -> 0
+ *    (R-c12, R-c13).  Elements: satRNE(RN32(x * 2^(127-c))).
+ *
+ * E8M0 blocked scale layout (MX operands)
+ *  The codes of an MX operand with R rows and C columns (blocks of 32 along
+ *  the columns) form a logical [R, C/32] byte matrix.  It is stored tiled in
+ *  128 x 4 tiles, tiles row-major: tile (rb, cb) starts at byte
+ *  (rb * (C/128) + cb) * 512, and inside a tile logical (r, c) sits at byte
+ *  (r % 32) * 16 + (r / 32) * 4 + c, r in [0,128), c in [0,4).  This is the
+ *  scale-factor atom tcgen05.mma.kind::mxf8f6f4.block_scale consumes from
+ *  TMEM (32 lanes x 4 words, replicated per lane quadrant), so the GEMM can
+ *  stream it with one bulk copy per tile.  Size: R * C / 32 bytes.
+ */
+#ifndef FP8TRAIN_H_
+#define FP8TRAIN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FP8TRAIN_ABI_VERSION 1
+
+typedef enum {
+  FP8_OK = 0,
+  FP8_EINVAL = 1,        /* bad argument or shape */
+  FP8_EALIGN = 2,        /* alignment / divisibility rule violated */
+  FP8_EUNSUPPORTED = 3,  /* valid request this build does not implement */
+  FP8_ECUDA = 4,         /* a CUDA runtime/driver call or launch failed */
+  FP8_ENCCL = 5,         /* an NCCL call failed */
+  FP8_EWORKSPACE = 6     /* workspace smaller than *_workspace_bytes() */
+} fp8_status_t;
+
+typedef enum { FP8_DT_F32 = 0, FP8_DT_BF16 = 1 } fp8_dtype_t;
+typedef enum { FP8_E4M3 = 0, FP8_E5M2 = 1 } fp8_format_t;
+
+/* Scaling granularity (Appendix A; MX: PAPER.md:735). */
+typedef enum {
+  FP8_GRAN_TENSOR = 0,   /* one scale for the tensor (tensorwise recipe) */
+  FP8_GRAN_ROW = 1,      /* one scale per row, reduced over the columns */
+  FP8_GRAN_COL = 2,      /* one scale per column, reduced over the rows */
+  FP8_GRAN_ROW_COL = 3,  /* rowwise recipe dual cast from one input: q with per-row
+                            scales, q_t with per-column scales */
+  FP8_GRAN_MX32 = 4      /* MXFP8: q = blocks of 32 along columns ("dim0"),
+                            q_t = blocks of 32 along rows ("dim1"), E8M0 scales */
+} fp8_gran_t;
+
+typedef enum { FP8_MX_FLOOR = 0, FP8_MX_RCEIL = 1 } fp8_mx_round_t;
+
+typedef enum {
+  FP8_RECIPE_TENSORWISE = 0,
+  FP8_RECIPE_ROWWISE = 1,
+  FP8_RECIPE_MXFP8 = 2        /* PAPER.md:735 (MX formats for training) */
+} fp8_recipe_t;
+
+/* High-precision input matrix: row-major, `ld` in elements (>= cols). */
+typedef struct {
+  const void* ptr;
+  fp8_dtype_t dtype;
+  int64_t rows, cols, ld;
+} fp8_hp_t;
+
+/* A quantised tensor produced by fp8_cast_scaled (caller-owned buffers).
+ *   q      : codes [rows, cols] row-major, or NULL
+ *   q_t    : codes of the transposed copy [cols, rows] row-major, or NULL
+ *   scale  : scales that go with q:
+ *              TENSOR float[1], ROW float[rows], COL float[cols],
+ *              ROW_COL float[rows] (row scales), MX32 E8M0 blocked [rows x cols/32]
+ *   scale_t: scales that go with q_t:
+ *              TENSOR/ROW/COL: may alias `scale` or be NULL (same values),
+ *              ROW_COL float[cols] (column scales),
+ *              MX32 E8M0 blocked [cols x rows/32]
+ *   amax   : float[ ] amax behind `scale` (same shape), or NULL
+ *   amax_t : float[ ] amax behind `scale_t` (ROW_COL: [cols]), or NULL
+ * For MX32 amax/amax_t are unused (the block amax is fused into the cast). */
+typedef struct {
+  uint8_t* q;
+  uint8_t* q_t;
+  void* scale;
+  void* scale_t;
+  float* amax;
+  float* amax_t;
+  fp8_format_t fmt;
+  fp8_gran_t gran;
+  int64_t rows, cols;
+} fp8_tensor_t;
+
+/* Linear configuration (Appendix A recipes). */
+typedef struct {
+  fp8_recipe_t recipe;
+  fp8_format_t fmt_fwd;   /* X and W codes: FP8_E4M3 by default (R-c8) */
+  fp8_format_t fmt_grad;  /* dY codes: FP8_E5M2 by default (R-c8, R-c14) */
+  fp8_mx_round_t mx_round;/* MXFP8 shared-exponent rule (R-c12) */
+  fp8_dtype_t out_dtype;  /* FP8_DT_BF16 (north star) or FP8_DT_F32 */
+} fp8_linear_cfg_t;
+
+/* ---------------------------------------------------------------------------
+ * fp8_amax -- amax = max |x| over the scaling unit (R-c step 3).
+ *   gran TENSOR -> amax_out float[1]; ROW -> float[rows]; COL -> float[cols].
+ *   (ROW_COL / MX32 -> FP8_EINVAL: their amax is fused into the cast.)
+ *   Exact: computed as an unsigned max over |x| bit patterns.
+ *   `ws` must hold fp8_amax_workspace_bytes() bytes (u32 accumulators).
+ * ------------------------------------------------------------------------- */
+size_t fp8_amax_workspace_bytes(fp8_hp_t x, fp8_gran_t gran);
+fp8_status_t fp8_amax(fp8_hp_t x, fp8_gran_t gran, float* amax_out,
+                      void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * fp8_cast_scaled -- scale from amax, then saturating RNE cast (PAPER.md:281-287,
+ * Appendix A).  Writes out->q and/or out->q_t (at least one non-NULL), the
+ * scales and (optionally) the amax, per out->gran (see fp8_tensor_t).
+ *   amax_in: optional precomputed amax (device, TENSOR float[1] only -- e.g. the
+ *            all-reduced global weight amax of fp8_fsdp_allgather); NULL = compute.
+ *   mx_round: used for FP8_GRAN_MX32 only.
+ *   `ws` must hold fp8_cast_workspace_bytes() bytes.
+ * out->rows/cols must equal x.rows/cols.
+ * ------------------------------------------------------------------------- */
+size_t fp8_cast_workspace_bytes(fp8_hp_t x, fp8_gran_t gran);
+fp8_status_t fp8_cast_scaled(fp8_hp_t x, fp8_mx_round_t mx_round, const float* amax_in,
+                             fp8_tensor_t* out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * fp8_gemm -- the scaled FP8 GEMM on tcgen05 tensor cores:
+ *   D[m,n] = sum_k dec(A[m,k]) dec(B[n,k]) * (1/sa) * (1/sb)   fp32 accumulate
+ * A [M,K] and B [N,K] are FP8 codes, both K-contiguous ("K-major"); ld in bytes
+ * == elements.  Scale modes:
+ *   gran TENSOR: sa, sb float[1] (multiplicative scales, device)
+ *   gran ROW   : sa float[M], sb float[N]
+ *   gran MX32  : sa, sb E8M0 blocked codes of A [M x K/32] and B [N x K/32];
+ *                the per-32-block 2^(c-127) factors are applied inside the MMA.
+ * D is [M,N] row-major with leading dimension ldd elements, dtype out_dtype
+ * (BF16 = RN of the fp32 result; F32 = the fp32 result).  Order of the fp32
+ * accumulation and of the epilogue products is unspecified (R-c16).
+ * ------------------------------------------------------------------------- */
+fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, const void* sa,
+                      const uint8_t* B, fp8_format_t fmt_b, const void* sb,
+                      fp8_gran_t gran, int64_t M, int64_t N, int64_t K,
+                      int64_t lda, int64_t ldb, void* D, fp8_dtype_t out_dtype, int64_t ldd,
+                      void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Float8Linear forward: Y = X W^T with the recipe's casts (Appendix A):
+ *   tensorwise: X, W one scale each;  rowwise: X per row, W per row (over K);
+ *   mxfp8: X, W blocks of 32 along K.
+ * x [M,K], w [N,K] high precision; y [M,N] out_dtype, dense (ld = N).
+ * w_fp8 (nullable): pre-cast tensorwise weight (e.g. from fp8_fsdp_allgather):
+ *   w_fp8->q [N,K] codes + w_fp8->scale float[1]; then `w` may have ptr NULL
+ *   (its rows/cols still give the shape).
+ * saved: caller buffer of fp8_linear_saved_bytes() bytes; the forward writes
+ *   the FP8 operands the backward needs (the X operand of dW and the W operand
+ *   of dX with their scales, per the operand plan of DESIGN.md §2).
+ * ws: fp8_linear_workspace_bytes() bytes of scratch.
+ * ------------------------------------------------------------------------- */
+size_t fp8_linear_saved_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K);
+size_t fp8_linear_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K);
+fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
+                            const fp8_tensor_t* w_fp8, void* y, void* saved,
+                            void* ws, size_t ws_bytes, void* stream);
+
+/* Float8Linear backward: dX = dY W and dW = dY^T X (S:289-299 notation):
+ *   tensorwise: dY one scale, reuse X/W scales; rowwise: dY per row for dX and
+ *   per column for dW, W per column, X per column ("rows of the left
+ *   operand, columns of the right"); mxfp8: dY blocks along N (dX) and along M
+ *   (dW), W along N, X along M.
+ * dy [M,N]; dx [M,K] and dw [N,K] out_dtype dense, either may be NULL.
+ * `saved` must be the buffer the matching fp8_linear_fwd wrote. */
+fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K,
+                            const void* saved, void* dx, void* dw,
+                            void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * FSDP2-style FP8 weight all-gather (PAPER.md:596 enable_fp8_all_gather;
+ * reading R-c18): per rank, amax of the local shard -> NCCL all-reduce MAX ->
+ * s = RN32(fmax / max(amax, eps)) -> cast the shard into slot `rank` of
+ * w_full -> NCCL all-gather of the bytes.  The result is bit-identical on
+ * every rank and equal to the unsharded tensorwise cast.
+ *   w_shard  [rows_local, cols] high precision (this rank's rows)
+ *   w_full   [nranks * rows_local, cols] u8 codes (device)
+ *   scale_out float[1], amax_out float[1] (device; the global amax)
+ *   ws: fp8_fsdp_workspace_bytes() bytes.
+ * ------------------------------------------------------------------------- */
+typedef struct fp8_comm_s* fp8_comm_t;
+/* Host: fill id[128] on one rank (ncclGetUniqueId); broadcast it yourself. */
+fp8_status_t fp8_comm_get_unique_id(uint8_t id[128]);
+/* Host, collective over nranks processes; binds the communicator to the
+ * current CUDA device. */
+fp8_status_t fp8_comm_init(fp8_comm_t* comm, const uint8_t id[128], int nranks, int rank);
+fp8_status_t fp8_comm_destroy(fp8_comm_t comm);
+size_t fp8_fsdp_workspace_bytes(fp8_hp_t w_shard);
+fp8_status_t fp8_fsdp_allgather(fp8_comm_t comm, fp8_hp_t w_shard, fp8_format_t fmt,
+                                uint8_t* w_full, float* scale_out, float* amax_out,
+                                void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Helpers
+ * ------------------------------------------------------------------------- */
+int fp8_abi_version(void);
+/* Thread-local message describing the last non-OK status of this thread. */
+const char* fp8_last_error(void);
+/* Number of kernels this library has launched in the calling process (all
+ * threads); for launch accounting in benchmarks. */
+uint64_t fp8_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FP8TRAIN_H_ */

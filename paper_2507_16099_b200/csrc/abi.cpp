@@ -1,0 +1,470 @@
+// C-ABI implementation (include/fp8train.h): validation, workspace carving and the
+// per-recipe orchestration of the Float8Linear forward/backward (Appendix A,
+// PAPER.md:594-598).  Every compute step runs in the kernels of cast_kernels.cu /
+// gemm_kernels.cu; this file only checks arguments and enqueues work.
+#include "fp8train.h"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "kernels.h"
+
+namespace fp8t {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static thread_local std::string g_err;
+
+fp8_status_t fail(fp8_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+fp8_status_t cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return FP8_OK;
+  return fail(FP8_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define FP8T_TRY(expr)                         \
+  do {                                         \
+    fp8_status_t _s = (expr);                  \
+    if (_s != FP8_OK) return _s;               \
+  } while (0)
+#define FP8T_CUDA(expr, what) FP8T_TRY(cuda_check((expr), (what)))
+
+static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+static inline size_t al(size_t b) { return (b + 255) & ~size_t(255); }
+static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+static inline size_t esize(fp8_dtype_t d) { return d == FP8_DT_F32 ? 4 : 2; }
+
+static fp8_status_t check_hp(const fp8_hp_t& x, const char* name, bool need_ptr = true) {
+  if (x.dtype != FP8_DT_F32 && x.dtype != FP8_DT_BF16) return fail(FP8_EINVAL, "%s: bad dtype", name);
+  if (x.rows < 16 || x.cols < 16) return fail(FP8_EINVAL, "%s: rows/cols must be >= 16", name);
+  if (x.rows % 16 || x.cols % 16) return fail(FP8_EALIGN, "%s: rows and cols must be multiples of 16", name);
+  if (x.ld < x.cols) return fail(FP8_EINVAL, "%s: ld < cols", name);
+  if ((x.ld * (int64_t)esize(x.dtype)) % 16) return fail(FP8_EALIGN, "%s: ld*elem_size must be a multiple of 16", name);
+  if (x.rows > (int64_t)1 << 31 || x.cols > (int64_t)1 << 31) return fail(FP8_EINVAL, "%s: dims too large", name);
+  if (need_ptr && !x.ptr) return fail(FP8_EINVAL, "%s: null pointer", name);
+  if (x.ptr && !aligned16(x.ptr)) return fail(FP8_EALIGN, "%s: pointer not 16-byte aligned", name);
+  return FP8_OK;
+}
+static fp8_status_t check_ptr(const void* p, const char* name) {
+  if (!p) return fail(FP8_EINVAL, "%s: null pointer", name);
+  if (!aligned16(p)) return fail(FP8_EALIGN, "%s: pointer not 16-byte aligned", name);
+  return FP8_OK;
+}
+static fp8_status_t check_fmt(int f) {
+  return (f == FP8_E4M3 || f == FP8_E5M2) ? FP8_OK : fail(FP8_EINVAL, "bad fp8 format");
+}
+
+// Bump allocator over a caller buffer (256-byte aligned regions).
+struct Carve {
+  uint8_t* base;
+  size_t off = 0;
+  explicit Carve(void* b) : base(static_cast<uint8_t*>(b)) {}
+  template <typename T> T* take(size_t bytes) {
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += al(bytes);
+    return p;
+  }
+};
+
+}  // namespace fp8t
+
+using namespace fp8t;
+
+extern "C" {
+
+int fp8_abi_version(void) { return FP8TRAIN_ABI_VERSION; }
+const char* fp8_last_error(void) { return g_err.c_str(); }
+uint64_t fp8_launch_count(void) { return g_launches.load(); }
+
+// ---------------------------------------------------------------------------
+// amax
+// ---------------------------------------------------------------------------
+size_t fp8_amax_workspace_bytes(fp8_hp_t, fp8_gran_t) { return 0; }
+
+fp8_status_t fp8_amax(fp8_hp_t x, fp8_gran_t gran, float* amax_out, void*, size_t, void* stream) {
+  FP8T_TRY(check_hp(x, "x"));
+  if (!amax_out) return fail(FP8_EINVAL, "amax_out: null pointer");
+  int mode;
+  size_t n;
+  switch (gran) {
+    case FP8_GRAN_TENSOR: mode = 1; n = 1; break;
+    case FP8_GRAN_ROW: mode = 2; n = x.rows; break;
+    case FP8_GRAN_COL: mode = 4; n = x.cols; break;
+    default: return fail(FP8_EINVAL, "fp8_amax: gran must be TENSOR, ROW or COL");
+  }
+  uint32_t* acc = reinterpret_cast<uint32_t*>(amax_out);
+  FP8T_CUDA(cudaMemsetAsync(acc, 0, n * 4, S(stream)), "memset amax");
+  FP8T_CUDA(launch_amax(x.ptr, x.dtype == FP8_DT_BF16, x.rows, x.cols, x.ld, mode, acc, acc, acc, S(stream)),
+            "amax kernel");
+  return FP8_OK;
+}
+
+// ---------------------------------------------------------------------------
+// cast
+// ---------------------------------------------------------------------------
+size_t fp8_cast_workspace_bytes(fp8_hp_t x, fp8_gran_t gran) {
+  switch (gran) {
+    case FP8_GRAN_TENSOR: return al(4);
+    case FP8_GRAN_ROW: return al(4 * x.rows);
+    case FP8_GRAN_COL: return al(4 * x.cols);
+    case FP8_GRAN_ROW_COL: return al(4 * x.rows) + al(4 * x.cols);
+    default: return 0;
+  }
+}
+
+fp8_status_t fp8_cast_scaled(fp8_hp_t x, fp8_mx_round_t mx_round, const float* amax_in, fp8_tensor_t* out,
+                             void* ws, size_t ws_bytes, void* stream) {
+  FP8T_TRY(check_hp(x, "x"));
+  if (!out) return fail(FP8_EINVAL, "out: null pointer");
+  FP8T_TRY(check_fmt(out->fmt));
+  if (out->rows != x.rows || out->cols != x.cols) return fail(FP8_EINVAL, "out shape != x shape");
+  if (!out->q && !out->q_t) return fail(FP8_EINVAL, "out->q and out->q_t are both NULL");
+  if (out->q) FP8T_TRY(check_ptr(out->q, "out->q"));
+  if (out->q_t) FP8T_TRY(check_ptr(out->q_t, "out->q_t"));
+  if (amax_in && out->gran != FP8_GRAN_TENSOR) return fail(FP8_EINVAL, "amax_in is only valid for TENSOR");
+  const bool bf16 = x.dtype == FP8_DT_BF16;
+  cudaStream_t st = S(stream);
+  const int fmt = out->fmt;
+
+  if (out->gran == FP8_GRAN_MX32) {
+    if (x.rows % 128 || x.cols % 128) return fail(FP8_EALIGN, "MX32 needs rows and cols multiples of 128");
+    if (mx_round != FP8_MX_FLOOR && mx_round != FP8_MX_RCEIL) return fail(FP8_EINVAL, "bad mx_round");
+    if (out->q && !out->scale) return fail(FP8_EINVAL, "MX32: q needs scale");
+    if (out->q_t && !out->scale_t) return fail(FP8_EINVAL, "MX32: q_t needs scale_t");
+    FP8T_CUDA(launch_mx_cast(x.ptr, bf16, fmt, mx_round == FP8_MX_RCEIL, x.rows, x.cols, x.ld, out->q,
+                             static_cast<uint8_t*>(out->scale), out->q_t, static_cast<uint8_t*>(out->scale_t), st),
+              "mx cast kernel");
+    return FP8_OK;
+  }
+  if (out->gran < FP8_GRAN_TENSOR || out->gran > FP8_GRAN_ROW_COL) return fail(FP8_EINVAL, "bad gran");
+  {
+    // amax accumulators come from out->amax / out->amax_t when given, else from ws
+    size_t need = 0;
+    if (out->gran == FP8_GRAN_ROW_COL) {
+      if (!out->amax) need += al(4 * x.rows);
+      if (!out->amax_t) need += al(4 * x.cols);
+    } else if (!out->amax && !amax_in) {
+      need = fp8_cast_workspace_bytes(x, out->gran);
+    }
+    if (need && (!ws || ws_bytes < need)) return fail(FP8_EWORKSPACE, "workspace too small (%zu < %zu)", ws_bytes, need);
+  }
+  Carve c(ws);
+
+  if (out->gran == FP8_GRAN_ROW_COL) {
+    if (!out->scale || (out->q_t && !out->scale_t)) return fail(FP8_EINVAL, "ROW_COL needs scale (and scale_t)");
+    float* ar = out->amax ? out->amax : c.take<float>(4 * x.rows);
+    float* ac = out->amax_t ? out->amax_t : c.take<float>(4 * x.cols);
+    FP8T_CUDA(cudaMemsetAsync(ar, 0, 4 * x.rows, st), "memset");
+    FP8T_CUDA(cudaMemsetAsync(ac, 0, 4 * x.cols, st), "memset");
+    FP8T_CUDA(launch_amax(x.ptr, bf16, x.rows, x.cols, x.ld, 6, nullptr, reinterpret_cast<uint32_t*>(ar),
+                          reinterpret_cast<uint32_t*>(ac), st),
+              "amax kernel");
+    FP8T_CUDA(launch_cast(x.ptr, bf16, fmt, x.rows, x.cols, x.ld, out->q ? 2 : 0, out->q_t ? 3 : 0, ar, ac, out->q,
+                          out->q_t, static_cast<float*>(out->scale), static_cast<float*>(out->scale_t), st),
+              "cast kernel");
+    return FP8_OK;
+  }
+
+  // TENSOR / ROW / COL: one scale vector shared by q and q_t
+  if (!out->scale && !out->scale_t) return fail(FP8_EINVAL, "scale: null pointer");
+  const int mode = out->gran == FP8_GRAN_TENSOR ? 1 : (out->gran == FP8_GRAN_ROW ? 2 : 3);
+  const int amode = out->gran == FP8_GRAN_TENSOR ? 1 : (out->gran == FP8_GRAN_ROW ? 2 : 4);
+  const size_t n = out->gran == FP8_GRAN_TENSOR ? 1 : (out->gran == FP8_GRAN_ROW ? x.rows : x.cols);
+  const float* a = amax_in;
+  if (!a) {
+    float* acc = out->amax ? out->amax : c.take<float>(4 * n);
+    FP8T_CUDA(cudaMemsetAsync(acc, 0, 4 * n, st), "memset");
+    uint32_t* u = reinterpret_cast<uint32_t*>(acc);
+    FP8T_CUDA(launch_amax(x.ptr, bf16, x.rows, x.cols, x.ld, amode, u, u, u, st), "amax kernel");
+    a = acc;
+  } else if (out->amax && out->amax != amax_in) {
+    FP8T_CUDA(cudaMemcpyAsync(out->amax, amax_in, 4, cudaMemcpyDeviceToDevice, st), "copy amax");
+  }
+  float* sq = static_cast<float*>(out->scale ? out->scale : out->scale_t);
+  float* stt = static_cast<float*>(out->scale_t ? out->scale_t : out->scale);
+  FP8T_CUDA(launch_cast(x.ptr, bf16, fmt, x.rows, x.cols, x.ld, out->q ? mode : 0, out->q_t ? mode : 0, a, a,
+                        out->q, out->q_t, out->q ? sq : nullptr, stt, st),
+            "cast kernel");
+  return FP8_OK;
+}
+
+// ---------------------------------------------------------------------------
+// GEMM
+// ---------------------------------------------------------------------------
+fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, const void* sa, const uint8_t* B, fp8_format_t fmt_b,
+                      const void* sb, fp8_gran_t gran, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
+                      void* D, fp8_dtype_t out_dtype, int64_t ldd, void* stream) {
+  FP8T_TRY(check_ptr(A, "A"));
+  FP8T_TRY(check_ptr(B, "B"));
+  FP8T_TRY(check_ptr(D, "D"));
+  FP8T_TRY(check_fmt(fmt_a));
+  FP8T_TRY(check_fmt(fmt_b));
+  if (!sa || !sb) return fail(FP8_EINVAL, "scales: null pointer");
+  if (M < 16 || N < 16 || K < 16) return fail(FP8_EINVAL, "M, N, K must be >= 16");
+  if (M % 16 || N % 16 || K % 16) return fail(FP8_EALIGN, "M, N, K must be multiples of 16");
+  if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return fail(FP8_EINVAL, "dims too large");
+  if (lda < K || ldb < K || ldd < N) return fail(FP8_EINVAL, "leading dimension too small");
+  if (lda % 16 || ldb % 16) return fail(FP8_EALIGN, "lda/ldb must be multiples of 16 bytes");
+  if (out_dtype != FP8_DT_BF16 && out_dtype != FP8_DT_F32) return fail(FP8_EINVAL, "bad out_dtype");
+  if ((ldd * (int64_t)esize(out_dtype)) % 16) return fail(FP8_EALIGN, "ldd*elem_size must be a multiple of 16");
+  int mode;
+  if (gran == FP8_GRAN_TENSOR) mode = 0;
+  else if (gran == FP8_GRAN_ROW) mode = 1;
+  else if (gran == FP8_GRAN_MX32) {
+    mode = 2;
+    if (M % 128 || N % 128 || K % 128) return fail(FP8_EALIGN, "MX32 GEMM needs M, N, K multiples of 128");
+    FP8T_TRY(check_ptr(sa, "sfa"));
+    FP8T_TRY(check_ptr(sb, "sfb"));
+  } else return fail(FP8_EINVAL, "fp8_gemm: gran must be TENSOR, ROW or MX32");
+  GemmProblem p{A, B, (int)fmt_a, (int)fmt_b, sa, sb, mode, M, N, K, lda, ldb, D, out_dtype == FP8_DT_F32, ldd};
+  FP8T_CUDA(launch_gemm(p, S(stream)), "gemm kernel");
+  return FP8_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Float8Linear forward / backward
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Saved {          // written by fwd, read by bwd
+  uint8_t* xT;          // [K, M]  X operand of dW (K-major over M)
+  uint8_t* wT;          // [K, N]  W operand of dX (K-major over N)
+  void* sx;             // tensorwise float[1] | rowwise float[K] | mx E8M0 [K x M/32]
+  void* sw;             // tensorwise float[1] | rowwise float[K] | mx E8M0 [K x N/32]
+};
+Saved carve_saved(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K, void* base, size_t* bytes) {
+  Carve c(base);
+  Saved s;
+  s.xT = c.take<uint8_t>((size_t)K * M);
+  s.wT = c.take<uint8_t>((size_t)K * N);
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    s.sx = c.take<float>(4);
+    s.sw = c.take<float>(4);
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+    s.sx = c.take<float>(4 * K);
+    s.sw = c.take<float>(4 * K);
+  } else {
+    s.sx = c.take<uint8_t>((size_t)K * M / 32);
+    s.sw = c.take<uint8_t>((size_t)K * N / 32);
+  }
+  if (bytes) *bytes = c.off;
+  return s;
+}
+
+struct FwdWs {
+  uint8_t* xq; uint8_t* wq;
+  float* amax;       // tensorwise [2] | rowwise [M + K + N + K]
+  float* sxr; float* swr;      // rowwise row scales
+  uint8_t* sfx; uint8_t* sfw;  // mx dim0 scales
+};
+FwdWs carve_fwd(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K, void* base, size_t* bytes) {
+  Carve c(base);
+  FwdWs w{};
+  w.xq = c.take<uint8_t>((size_t)M * K);
+  w.wq = c.take<uint8_t>((size_t)N * K);
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    w.amax = c.take<float>(8);
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+    w.amax = c.take<float>(4 * (M + K + N + K));
+    w.sxr = c.take<float>(4 * M);
+    w.swr = c.take<float>(4 * N);
+  } else {
+    w.sfx = c.take<uint8_t>((size_t)M * K / 32);
+    w.sfw = c.take<uint8_t>((size_t)N * K / 32);
+  }
+  if (bytes) *bytes = c.off;
+  return w;
+}
+
+struct BwdWs {
+  uint8_t* g; uint8_t* gT;   // [M,N], [N,M]
+  float* amax;               // tensorwise [1] | rowwise [M + N]
+  void* sg; void* sgT;       // tensorwise float[1] | rowwise float[M], float[N] | mx E8M0
+};
+BwdWs carve_bwd(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, void* base, size_t* bytes) {
+  Carve c(base);
+  BwdWs w{};
+  w.g = c.take<uint8_t>((size_t)M * N);
+  w.gT = c.take<uint8_t>((size_t)M * N);
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    w.amax = c.take<float>(4);
+    w.sg = c.take<float>(4);
+    w.sgT = w.sg;
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+    w.amax = c.take<float>(4 * (M + N));
+    w.sg = c.take<float>(4 * M);
+    w.sgT = c.take<float>(4 * N);
+  } else {
+    w.sg = c.take<uint8_t>((size_t)M * N / 32);
+    w.sgT = c.take<uint8_t>((size_t)M * N / 32);
+  }
+  if (bytes) *bytes = c.off;
+  return w;
+}
+
+fp8_status_t check_cfg(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K) {
+  if (!cfg) return fail(FP8_EINVAL, "cfg: null pointer");
+  if (cfg->recipe < FP8_RECIPE_TENSORWISE || cfg->recipe > FP8_RECIPE_MXFP8) return fail(FP8_EINVAL, "bad recipe");
+  FP8T_TRY(check_fmt(cfg->fmt_fwd));
+  FP8T_TRY(check_fmt(cfg->fmt_grad));
+  if (cfg->out_dtype != FP8_DT_BF16 && cfg->out_dtype != FP8_DT_F32) return fail(FP8_EINVAL, "bad out_dtype");
+  if (cfg->mx_round != FP8_MX_FLOOR && cfg->mx_round != FP8_MX_RCEIL) return fail(FP8_EINVAL, "bad mx_round");
+  if (M < 16 || N < 16 || K < 16) return fail(FP8_EINVAL, "M, N, K must be >= 16");
+  if (M % 16 || N % 16 || K % 16) return fail(FP8_EALIGN, "M, N, K must be multiples of 16");
+  if (cfg->recipe == FP8_RECIPE_MXFP8 && (M % 128 || N % 128 || K % 128))
+    return fail(FP8_EALIGN, "mxfp8 needs M, N, K multiples of 128");
+  return FP8_OK;
+}
+
+}  // namespace
+
+size_t fp8_linear_saved_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K) {
+  if (!cfg) return 0;
+  size_t b = 0;
+  carve_saved(cfg, M, N, K, nullptr, &b);
+  return b;
+}
+
+size_t fp8_linear_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K) {
+  if (!cfg) return 0;
+  size_t f = 0, b = 0;
+  carve_fwd(cfg, M, N, K, nullptr, &f);
+  carve_bwd(cfg, M, N, nullptr, &b);
+  return f > b ? f : b;
+}
+
+fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w, const fp8_tensor_t* w_fp8,
+                            void* y, void* saved, void* ws, size_t ws_bytes, void* stream) {
+  FP8T_TRY(check_hp(x, "x"));
+  FP8T_TRY(check_hp(w, "w", w_fp8 == nullptr));
+  const int64_t M = x.rows, K = x.cols, N = w.rows;
+  if (w.cols != K) return fail(FP8_EINVAL, "w.cols != x.cols");
+  FP8T_TRY(check_cfg(cfg, M, N, K));
+  FP8T_TRY(check_ptr(y, "y"));
+  FP8T_TRY(check_ptr(saved, "saved"));
+  FP8T_TRY(check_ptr(ws, "ws"));
+  if (ws_bytes < fp8_linear_workspace_bytes(cfg, M, N, K)) return fail(FP8_EWORKSPACE, "workspace too small");
+  if (w_fp8) {
+    if (cfg->recipe != FP8_RECIPE_TENSORWISE) return fail(FP8_EUNSUPPORTED, "w_fp8 needs the tensorwise recipe");
+    if (w_fp8->rows != N || w_fp8->cols != K) return fail(FP8_EINVAL, "w_fp8 shape");
+    if (w_fp8->fmt != cfg->fmt_fwd) return fail(FP8_EINVAL, "w_fp8 format != cfg->fmt_fwd");
+    FP8T_TRY(check_ptr(w_fp8->q, "w_fp8->q"));
+    if (!w_fp8->scale) return fail(FP8_EINVAL, "w_fp8->scale: null pointer");
+  }
+  cudaStream_t st = S(stream);
+  const bool xb = x.dtype == FP8_DT_BF16, wb = w.dtype == FP8_DT_BF16;
+  const int ff = cfg->fmt_fwd;
+  Saved sv = carve_saved(cfg, M, N, K, saved, nullptr);
+  FwdWs fw = carve_fwd(cfg, M, N, K, ws, nullptr);
+  const int of32 = cfg->out_dtype == FP8_DT_F32;
+
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    uint32_t* ax = reinterpret_cast<uint32_t*>(fw.amax);
+    uint32_t* aw = ax + 1;
+    FP8T_CUDA(cudaMemsetAsync(ax, 0, 8, st), "memset");
+    FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
+    FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 1, 1, fw.amax, fw.amax, fw.xq, sv.xT, (float*)sv.sx,
+                          (float*)sv.sx, st),
+              "cast x");
+    const uint8_t* wq = fw.wq;
+    if (w_fp8) {
+      wq = w_fp8->q;
+      FP8T_CUDA(launch_transpose_u8(w_fp8->q, N, K, sv.wT, st), "transpose w");
+      FP8T_CUDA(cudaMemcpyAsync(sv.sw, w_fp8->scale, 4, cudaMemcpyDeviceToDevice, st), "copy w scale");
+    } else {
+      FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 1, aw, nullptr, nullptr, st), "amax w");
+      FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 1, 1, fw.amax + 1, fw.amax + 1, fw.wq, sv.wT, (float*)sv.sw,
+                            (float*)sv.sw, st),
+                "cast w");
+    }
+    GemmProblem p{fw.xq, wq, ff, ff, sv.sx, sv.sw, 0, M, N, K, K, K, y, of32, N};
+    FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+    float* axr = fw.amax;
+    float* axc = axr + M;
+    float* awr = axc + K;
+    float* awc = awr + N;
+    FP8T_CUDA(cudaMemsetAsync(fw.amax, 0, 4 * (M + K + N + K), st), "memset");
+    FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 6, nullptr, (uint32_t*)axr, (uint32_t*)axc, st), "amax x");
+    FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 6, nullptr, (uint32_t*)awr, (uint32_t*)awc, st), "amax w");
+    FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 2, 3, axr, axc, fw.xq, sv.xT, fw.sxr, (float*)sv.sx, st),
+              "cast x");
+    FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 3, awr, awc, fw.wq, sv.wT, fw.swr, (float*)sv.sw, st),
+              "cast w");
+    GemmProblem p{fw.xq, fw.wq, ff, ff, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N};
+    FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+  } else {
+    const bool rc = cfg->mx_round == FP8_MX_RCEIL;
+    FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, fw.xq, fw.sfx, sv.xT, (uint8_t*)sv.sx, st), "mx cast x");
+    FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, fw.wq, fw.sfw, sv.wT, (uint8_t*)sv.sw, st), "mx cast w");
+    GemmProblem p{fw.xq, fw.wq, ff, ff, fw.sfx, fw.sfw, 2, M, N, K, K, K, y, of32, N};
+    FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+  }
+  return FP8_OK;
+}
+
+fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K, const void* saved, void* dx,
+                            void* dw, void* ws, size_t ws_bytes, void* stream) {
+  FP8T_TRY(check_hp(dy, "dy"));
+  const int64_t M = dy.rows, N = dy.cols;
+  FP8T_TRY(check_cfg(cfg, M, N, K));
+  FP8T_TRY(check_ptr(saved, "saved"));
+  FP8T_TRY(check_ptr(ws, "ws"));
+  if (dx) FP8T_TRY(check_ptr(dx, "dx"));
+  if (dw) FP8T_TRY(check_ptr(dw, "dw"));
+  if (ws_bytes < fp8_linear_workspace_bytes(cfg, M, N, K)) return fail(FP8_EWORKSPACE, "workspace too small");
+  cudaStream_t st = S(stream);
+  const bool gb = dy.dtype == FP8_DT_BF16;
+  const int ff = cfg->fmt_fwd, fg = cfg->fmt_grad;
+  Saved sv = carve_saved(cfg, M, N, K, const_cast<void*>(saved), nullptr);
+  BwdWs bw = carve_bwd(cfg, M, N, ws, nullptr);
+  const int of32 = cfg->out_dtype == FP8_DT_F32;
+  int mode;
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    mode = 0;
+    FP8T_CUDA(cudaMemsetAsync(bw.amax, 0, 4, st), "memset");
+    FP8T_CUDA(launch_amax(dy.ptr, gb, M, N, dy.ld, 1, (uint32_t*)bw.amax, nullptr, nullptr, st), "amax dy");
+    FP8T_CUDA(launch_cast(dy.ptr, gb, fg, M, N, dy.ld, dx ? 1 : 0, dw ? 1 : 0, bw.amax, bw.amax, bw.g, bw.gT,
+                          (float*)bw.sg, (float*)bw.sg, st),
+              "cast dy");
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+    mode = 1;
+    float* ar = bw.amax;
+    float* ac = ar + M;
+    FP8T_CUDA(cudaMemsetAsync(bw.amax, 0, 4 * (M + N), st), "memset");
+    FP8T_CUDA(launch_amax(dy.ptr, gb, M, N, dy.ld, 6, nullptr, (uint32_t*)ar, (uint32_t*)ac, st), "amax dy");
+    FP8T_CUDA(launch_cast(dy.ptr, gb, fg, M, N, dy.ld, dx ? 2 : 0, dw ? 3 : 0, ar, ac, bw.g, bw.gT, (float*)bw.sg,
+                          (float*)bw.sgT, st),
+              "cast dy");
+  } else {
+    mode = 2;
+    FP8T_CUDA(launch_mx_cast(dy.ptr, gb, fg, cfg->mx_round == FP8_MX_RCEIL, M, N, dy.ld, dx ? bw.g : nullptr,
+                             (uint8_t*)bw.sg, dw ? bw.gT : nullptr, (uint8_t*)bw.sgT, st),
+              "mx cast dy");
+  }
+  if (!dx && !dw) return FP8_OK;
+  if (dx) {  // dX[M,K] = dY[M,N] . W  : A = dY (K-major over N), B = W^T [K,N]
+    GemmProblem p{bw.g, sv.wT, fg, ff, bw.sg, sv.sw, mode, M, K, N, N, N, dx, of32, K};
+    FP8T_CUDA(launch_gemm(p, st), "gemm dx");
+  }
+  if (dw) {  // dW[N,K] = dY^T[N,M] . X : A = dY^T [N,M], B = X^T [K,M]
+    GemmProblem p{bw.gT, sv.xT, fg, ff, bw.sgT, sv.sx, mode, N, K, M, M, M, dw, of32, K};
+    FP8T_CUDA(launch_gemm(p, st), "gemm dw");
+  }
+  return FP8_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,459 @@
+// Memory-bound kernels of the Float8Linear step (HBM roofline):
+//   amax_tile   : max|x| per tensor / row / column  (Appendix A)
+//   cast_tile   : s = RN32(fmax/max(amax,eps)); q = satRNE(RN32(x*s)); row-major and/or
+//                 transposed FP8 output from one read (tensorwise / rowwise casts)
+//   mx_cast     : MXFP8 dim0 + dim1 casts with E8M0 block-32 scales from one read
+//   transpose_u8: FP8 byte transpose (pre-gathered FSDP weight -> the dX operand)
+// All kernels read 128 x 128 tiles with 16-byte vector loads; transposed outputs go
+// through a 16 KB XOR-swizzled shared-memory tile and leave as 16-byte stores.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace fp8t {
+
+// eps = fp32(1e-12) (DESIGN.md R-c5), written as its bit pattern.
+__device__ __forceinline__ float kEps() { return __int_as_float(0x2B8CBCCC); }
+template <int FMT> __device__ __forceinline__ float kFmax() { return FMT == 0 ? 448.0f : 57344.0f; }
+template <int FMT> __device__ __forceinline__ int kEmax() { return FMT == 0 ? 8 : 15; }
+
+// s = RN32(fmax / max(amax, eps)), IEEE division (R-c3, R-c6).
+template <int FMT>
+__device__ __forceinline__ float scale_of(float amax) {
+  return __fdiv_rn(kFmax<FMT>(), fmaxf(amax, kEps()));
+}
+
+// ---------------------------------------------------------------------------
+// 8-element loads as fp32 (exact widening) and |x| bit patterns
+// ---------------------------------------------------------------------------
+template <typename T> struct Ld8;
+template <> struct Ld8<float> {
+  static __device__ __forceinline__ void load(const float* p, float (&v)[8]) {
+    float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+};
+template <> struct Ld8<__nv_bfloat16> {
+  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float (&v)[8]) {
+    uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+};
+__device__ __forceinline__ int imin128(int64_t v) { return v < 128 ? (int)v : 128; }
+__device__ __forceinline__ uint32_t abs_bits(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
+
+template <int FMT>
+__device__ __forceinline__ uint2 cast8(const float (&v)[8], float s) {
+  float p[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = __fmul_rn(v[i], s);
+  return make_uint2(cvt_x4<FMT>(p[0], p[1], p[2], p[3]), cvt_x4<FMT>(p[4], p[5], p[6], p[7]));
+}
+template <int FMT>
+__device__ __forceinline__ uint2 cast8v(const float (&v)[8], const float* s) {
+  float p[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = __fmul_rn(v[i], s[i]);
+  return make_uint2(cvt_x4<FMT>(p[0], p[1], p[2], p[3]), cvt_x4<FMT>(p[4], p[5], p[6], p[7]));
+}
+
+// ---------------------------------------------------------------------------
+// Transposed-tile staging.  Tile = 128 rows x 128 bytes; word w of row r lives at
+// word position w ^ (((r >> 4) & 7) << 2), which makes both the row-wise writes
+// and the 16-row column reads below bank-conflict free.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int swz(int r, int w) { return r * 32 + (w ^ (((r >> 4) & 7) << 2)); }
+
+// 4x4 byte transpose: in a,b,c,d = rows (4 column bytes each) -> out[j] = column j (4 row bytes).
+__device__ __forceinline__ void transpose4x4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t (&o)[4]) {
+  uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+  uint32_t t2 = __byte_perm(c, d, 0x5140), t3 = __byte_perm(c, d, 0x7362);
+  o[0] = __byte_perm(t0, t2, 0x5410);
+  o[1] = __byte_perm(t0, t2, 0x7632);
+  o[2] = __byte_perm(t1, t3, 0x5410);
+  o[3] = __byte_perm(t1, t3, 0x7632);
+}
+
+// Phase 2: each thread reads a 16-row x 4-column block of the staged tile and writes
+// the 4 transposed rows (16 bytes each).  Threads t..t+7 cover 128 contiguous bytes.
+__device__ __forceinline__ void store_transposed(const uint32_t* tile, uint8_t* qt, int64_t ldt, int64_t r0,
+                                                 int64_t c0, int vrows, int vcols) {
+  const int t = threadIdx.x;
+  const int rg = t & 7, w = t >> 3;
+  if (16 * rg >= vrows || 4 * w >= vcols) return;
+  uint32_t W[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) W[i] = tile[swz(16 * rg + i, w)];
+  uint32_t o[4][4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    uint32_t col[4];
+    transpose4x4(W[4 * g], W[4 * g + 1], W[4 * g + 2], W[4 * g + 3], col);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j][g] = col[j];
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint8_t* dst = qt + (c0 + 4 * w + j) * ldt + r0 + 16 * rg;
+    *reinterpret_cast<uint4*>(dst) = make_uint4(o[j][0], o[j][1], o[j][2], o[j][3]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// amax over a 128 x 128 tile: tensor / per-row / per-column maxima, merged with
+// u32 atomicMax on |x| bit patterns (exact, order independent).  Output buffers
+// must be zeroed beforehand.
+// ---------------------------------------------------------------------------
+template <typename T, int MODE>  // MODE bit0: tensor, bit1: row, bit2: col
+__global__ void __launch_bounds__(256) amax_tile_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
+                                                        uint32_t* amax_tensor, uint32_t* amax_row,
+                                                        uint32_t* amax_col) {
+  __shared__ uint32_t colred[8][128];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t r0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 128;
+  const int cc = (t & 15) * 8;
+  const bool cvalid = c0 + cc < C;
+  uint32_t tmax = 0;
+  uint32_t cmax[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  float v[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t r = r0 + (t >> 4) + 16 * i;
+    if (cvalid && r < R) {
+      Ld8<T>::load(x + r * ld + c0 + cc, v[i]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[i][e] = 0.f;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t rmax = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t a = abs_bits(v[i][e]);
+      rmax = max(rmax, a);
+      cmax[e] = max(cmax[e], a);
+    }
+    tmax = max(tmax, rmax);
+    if (MODE & 2) {
+      rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, 1));
+      rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, 2));
+      rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, 4));
+      rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, 8));
+      const int64_t r = r0 + (t >> 4) + 16 * i;
+      if ((t & 15) == 0 && r < R) atomicMax(amax_row + r, rmax);
+    }
+  }
+  if (MODE & 1) {
+    tmax = __reduce_max_sync(0xffffffffu, tmax);
+    __shared__ uint32_t wred[8];
+    if (lane == 0) wred[warp] = tmax;
+    __syncthreads();
+    if (t == 0) {
+      uint32_t m = wred[0];
+#pragma unroll
+      for (int i = 1; i < 8; ++i) m = max(m, wred[i]);
+      atomicMax(amax_tensor, m);
+    }
+  }
+  if (MODE & 4) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      cmax[e] = max(cmax[e], __shfl_xor_sync(0xffffffffu, cmax[e], 16));
+    }
+    if (lane < 16) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) colred[warp][cc + e] = cmax[e];
+    }
+    __syncthreads();
+    if (t < 128 && c0 + t < C) {
+      uint32_t m = colred[0][t];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) m = max(m, colred[w][t]);
+      atomicMax(amax_col + c0 + t, m);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// cast_tile: q (row-major) with scale mode QM, q_t (transposed) with scale mode TM.
+// Modes: 0 none, 1 tensor (amax[1]), 2 per row (amax[R]), 3 per column (amax[C]).
+// Scale outputs are written by the tiles on the first tile row / column.
+// ---------------------------------------------------------------------------
+template <typename T, int FMT, int QM, int TM>
+__global__ void __launch_bounds__(256) cast_tile_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
+                                                        const float* __restrict__ amax_q,
+                                                        const float* __restrict__ amax_t, uint8_t* __restrict__ q,
+                                                        uint8_t* __restrict__ qt, float* scale_q, float* scale_t) {
+  __shared__ __align__(16) uint32_t tile[128 * 32];
+  __shared__ float sq[128];
+  __shared__ float st[128];
+  const int t = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 128;
+  const int vrows = imin128(R - r0), vcols = imin128(C - c0);
+
+  // Per-tile scale vectors (and the scale outputs).
+  auto fill = [&](int mode, const float* amax, float* sv, float* out) {
+    if (mode == 1) {
+      if (t == 0) {
+        const float s = scale_of<FMT>(amax[0]);
+        sv[0] = s;
+        if (out && blockIdx.x == 0 && blockIdx.y == 0) out[0] = s;
+      }
+    } else if (mode == 2) {
+      if (t < vrows) {
+        const float s = scale_of<FMT>(amax[r0 + t]);
+        sv[t] = s;
+        if (out && blockIdx.x == 0) out[r0 + t] = s;
+      }
+    } else if (mode == 3) {
+      if (t < vcols) {
+        const float s = scale_of<FMT>(amax[c0 + t]);
+        sv[t] = s;
+        if (out && blockIdx.y == 0) out[c0 + t] = s;
+      }
+    }
+  };
+  fill(QM, amax_q, sq, scale_q);
+  fill(TM, amax_t, st, scale_t);
+  __syncthreads();
+
+  const int cc = (t & 15) * 8;
+  const bool cvalid = cc < vcols;
+#pragma unroll 2
+  for (int i = 0; i < 8; ++i) {
+    const int rr = (t >> 4) + 16 * i;
+    if (!cvalid || rr >= vrows) continue;
+    float v[8];
+    Ld8<T>::load(x + (r0 + rr) * ld + c0 + cc, v);
+    uint2 bq = make_uint2(0, 0), bt = make_uint2(0, 0);
+    if (QM != 0) {
+      if (QM == 1) bq = cast8<FMT>(v, sq[0]);
+      if (QM == 2) bq = cast8<FMT>(v, sq[rr]);
+      if (QM == 3) bq = cast8v<FMT>(v, &sq[cc]);
+      *reinterpret_cast<uint2*>(q + (r0 + rr) * C + c0 + cc) = bq;
+    }
+    if (TM != 0) {
+      if (TM == QM) bt = bq;
+      else if (TM == 1) bt = cast8<FMT>(v, st[0]);
+      else if (TM == 2) bt = cast8<FMT>(v, st[rr]);
+      else bt = cast8v<FMT>(v, &st[cc]);
+      *reinterpret_cast<uint2*>(&tile[swz(rr, cc >> 2)]) = bt;
+    }
+  }
+  if (TM != 0) {
+    __syncthreads();
+    store_transposed(tile, qt, R, r0, c0, vrows, vcols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// MXFP8 cast, dim0 (blocks of 32 along columns, row-major out) and dim1 (blocks
+// of 32 along rows, transposed out) from one read of a 128 x 128 tile.
+// E8M0 codes by integer exponent arithmetic (R-c12):
+//   FLOOR: c = clamp(E - emax, 0, 254)              E = fp32 exponent field of amax
+//   RCEIL: c = clamp(E - emax + (mant > 0x600000), 0, 254), E == 0 -> 0
+// (mant > 0x600000  <=>  amax mantissa > 1.75 = fmax mantissa)
+// Elements: satRNE(RN32(x * 2^(127-c))), no flush-to-zero (R-c11).
+// Scales are written in the blocked 128x4 layout of fp8train.h.
+// ---------------------------------------------------------------------------
+template <int FMT, bool RCEIL>
+__device__ __forceinline__ uint32_t e8m0_code(uint32_t amax_bits) {
+  const int E = (int)(amax_bits >> 23);
+  if (E == 0) return 0;
+  int c = E - kEmax<FMT>();
+  if (RCEIL && (amax_bits & 0x7FFFFFu) > 0x600000u) c += 1;
+  return (uint32_t)min(max(c, 0), 254);
+}
+// 2^(127 - c) as fp32 (c = 254 -> 2^-127, a subnormal).
+__device__ __forceinline__ float e8m0_mult(uint32_t c) {
+  return c < 254 ? __uint_as_float((254u - c) << 23) : __uint_as_float(0x00400000u);
+}
+__device__ __forceinline__ int64_t sf_offset(int64_t r, int64_t cblk, int64_t ncol_tiles) {
+  // logical (row r, 32-block column cblk) of a [R, C/32] code matrix, 128x4 tiles
+  return ((r >> 7) * ncol_tiles + (cblk >> 2)) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (cblk & 3);
+}
+
+template <typename T, int FMT, bool RCEIL, bool DIM0, bool DIM1>
+__global__ void __launch_bounds__(256) mx_cast_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
+                                                      uint8_t* __restrict__ q0, uint8_t* __restrict__ sf0,
+                                                      uint8_t* __restrict__ q1, uint8_t* __restrict__ sf1) {
+  __shared__ __align__(16) uint32_t tile[128 * 32];
+  __shared__ uint32_t red[8][4][128];
+  __shared__ float mult1[4][128];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t r0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 128;
+  const int cc = (t & 15) * 8;
+  float v[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) Ld8<T>::load(x + (r0 + (t >> 4) + 16 * i) * ld + c0 + cc, v[i]);
+
+  if (DIM0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t m = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m = max(m, abs_bits(v[i][e]));
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+      const uint32_t code = e8m0_code<FMT, RCEIL>(m);
+      const int64_t r = r0 + (t >> 4) + 16 * i;
+      *reinterpret_cast<uint2*>(q0 + r * C + c0 + cc) = cast8<FMT>(v[i], e8m0_mult(code));
+      if ((t & 3) == 0) sf0[sf_offset(r, (c0 + cc) >> 5, C >> 7)] = (uint8_t)code;
+    }
+  }
+  if (DIM1) {
+    // per-column maxima over the 2 rows-per-block this thread holds, for each 32-row block j
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        uint32_t m = max(abs_bits(v[2 * j][e]), abs_bits(v[2 * j + 1][e]));
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, 16));
+        if (lane < 16) red[warp][j][cc + e] = m;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int idx = t + 256 * k;  // (j, col) pairs, 4 x 128
+      const int j = idx >> 7, col = idx & 127;
+      uint32_t m = red[0][j][col];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) m = max(m, red[w][j][col]);
+      const uint32_t code = e8m0_code<FMT, RCEIL>(m);
+      mult1[j][col] = e8m0_mult(code);
+      sf1[sf_offset(c0 + col, (r0 >> 5) + j, R >> 7)] = (uint8_t)code;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int rr = (t >> 4) + 16 * i;
+      const int j = i >> 1;  // rows 16i..16i+15 (+t>>4) lie in 32-row block i/2
+      float s[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s[e] = mult1[j][cc + e];
+      *reinterpret_cast<uint2*>(&tile[swz(rr, cc >> 2)]) = cast8v<FMT>(v[i], s);
+    }
+    __syncthreads();
+    store_transposed(tile, q1, R, r0, c0, 128, 128);
+  }
+}
+
+// FP8 byte transpose [R, C] -> [C, R] (R, C multiples of 16).
+__global__ void __launch_bounds__(256) transpose_u8_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C,
+                                                           uint8_t* __restrict__ out) {
+  __shared__ __align__(16) uint32_t tile[128 * 32];
+  const int t = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 128;
+  const int vrows = imin128(R - r0), vcols = imin128(C - c0);
+  const int cc = (t & 15) * 8;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int rr = (t >> 4) + 16 * i;
+    if (cc < vcols && rr < vrows)
+      *reinterpret_cast<uint2*>(&tile[swz(rr, cc >> 2)]) =
+          __ldg(reinterpret_cast<const uint2*>(in + (r0 + rr) * C + c0 + cc));
+  }
+  __syncthreads();
+  store_transposed(tile, out, R, r0, c0, vrows, vcols);
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers
+// ---------------------------------------------------------------------------
+static inline dim3 tile_grid(int64_t R, int64_t C) { return dim3((unsigned)((C + 127) / 128), (unsigned)((R + 127) / 128)); }
+
+template <typename T>
+static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, int mode, uint32_t* at,
+                                 uint32_t* ar, uint32_t* ac, cudaStream_t st) {
+  const T* p = static_cast<const T*>(x);
+  dim3 g = tile_grid(R, C);
+  switch (mode) {
+    case 1: amax_tile_kernel<T, 1><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac); break;
+    case 2: amax_tile_kernel<T, 2><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac); break;
+    case 4: amax_tile_kernel<T, 4><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac); break;
+    case 6: amax_tile_kernel<T, 6><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac); break;
+    default: return cudaErrorInvalidValue;
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_amax(const void* x, bool bf16, int64_t R, int64_t C, int64_t ld, int mode, uint32_t* at,
+                        uint32_t* ar, uint32_t* ac, cudaStream_t st) {
+  return bf16 ? amax_launch_t<__nv_bfloat16>(x, R, C, ld, mode, at, ar, ac, st)
+              : amax_launch_t<float>(x, R, C, ld, mode, at, ar, ac, st);
+}
+
+template <typename T, int FMT>
+static cudaError_t cast_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, int qm, int tm,
+                                 const float* aq, const float* at, uint8_t* q, uint8_t* qt, float* sq, float* st,
+                                 cudaStream_t s) {
+  const T* p = static_cast<const T*>(x);
+  dim3 g = tile_grid(R, C);
+#define FP8T_CAST(QM, TM)                                                                       \
+  if (qm == QM && tm == TM) {                                                                   \
+    cast_tile_kernel<T, FMT, QM, TM><<<g, 256, 0, s>>>(p, R, C, ld, aq, at, q, qt, sq, st);     \
+    count_launch();                                                                             \
+    return cudaGetLastError();                                                                  \
+  }
+  FP8T_CAST(1, 0) FP8T_CAST(0, 1) FP8T_CAST(1, 1)
+  FP8T_CAST(2, 0) FP8T_CAST(0, 2) FP8T_CAST(2, 2)
+  FP8T_CAST(3, 0) FP8T_CAST(0, 3) FP8T_CAST(3, 3)
+  FP8T_CAST(2, 3)
+#undef FP8T_CAST
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_cast(const void* x, bool bf16, int fmt, int64_t R, int64_t C, int64_t ld, int qm, int tm,
+                        const float* aq, const float* at, uint8_t* q, uint8_t* qt, float* sq, float* st,
+                        cudaStream_t s) {
+  if (bf16)
+    return fmt == 0 ? cast_launch_t<__nv_bfloat16, 0>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s)
+                    : cast_launch_t<__nv_bfloat16, 1>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s);
+  return fmt == 0 ? cast_launch_t<float, 0>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s)
+                  : cast_launch_t<float, 1>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s);
+}
+
+template <typename T, int FMT, bool RC>
+static cudaError_t mx_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, uint8_t* q0, uint8_t* sf0,
+                               uint8_t* q1, uint8_t* sf1, cudaStream_t s) {
+  const T* p = static_cast<const T*>(x);
+  dim3 g = tile_grid(R, C);
+  if (q0 && q1) mx_cast_kernel<T, FMT, RC, true, true><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
+  else if (q0) mx_cast_kernel<T, FMT, RC, true, false><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
+  else mx_cast_kernel<T, FMT, RC, false, true><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mx_cast(const void* x, bool bf16, int fmt, bool rceil, int64_t R, int64_t C, int64_t ld,
+                           uint8_t* q0, uint8_t* sf0, uint8_t* q1, uint8_t* sf1, cudaStream_t s) {
+#define FP8T_MX(T)                                                                                  \
+  if (fmt == 0) return rceil ? mx_launch_t<T, 0, true>(x, R, C, ld, q0, sf0, q1, sf1, s)            \
+                             : mx_launch_t<T, 0, false>(x, R, C, ld, q0, sf0, q1, sf1, s);          \
+  return rceil ? mx_launch_t<T, 1, true>(x, R, C, ld, q0, sf0, q1, sf1, s)                          \
+               : mx_launch_t<T, 1, false>(x, R, C, ld, q0, sf0, q1, sf1, s);
+  if (bf16) { FP8T_MX(__nv_bfloat16) }
+  FP8T_MX(float)
+#undef FP8T_MX
+}
+
+cudaError_t launch_transpose_u8(const uint8_t* in, int64_t R, int64_t C, uint8_t* out, cudaStream_t s) {
+  transpose_u8_kernel<<<tile_grid(R, C), 256, 0, s>>>(in, R, C, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace fp8t

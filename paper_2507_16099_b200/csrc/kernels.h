@@ -1,0 +1,34 @@
+// Internal launcher declarations (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace fp8t {
+
+void count_launch();
+
+// amax_tile: mode bit0 tensor -> at[1], bit1 rows -> ar[R], bit2 cols -> ac[C] (u32 |x| bits, pre-zeroed)
+cudaError_t launch_amax(const void* x, bool bf16, int64_t R, int64_t C, int64_t ld, int mode, uint32_t* at,
+                        uint32_t* ar, uint32_t* ac, cudaStream_t st);
+// cast_tile: scale modes 0 none / 1 tensor / 2 row / 3 col for q (row-major) and qt (transposed)
+cudaError_t launch_cast(const void* x, bool bf16, int fmt, int64_t R, int64_t C, int64_t ld, int qm, int tm,
+                        const float* aq, const float* at, uint8_t* q, uint8_t* qt, float* sq, float* st,
+                        cudaStream_t s);
+// MXFP8 dim0 (q0, sf0) and/or dim1 (q1, sf1) casts, blocked E8M0 layout
+cudaError_t launch_mx_cast(const void* x, bool bf16, int fmt, bool rceil, int64_t R, int64_t C, int64_t ld,
+                           uint8_t* q0, uint8_t* sf0, uint8_t* q1, uint8_t* sf1, cudaStream_t s);
+cudaError_t launch_transpose_u8(const uint8_t* in, int64_t R, int64_t C, uint8_t* out, cudaStream_t s);
+
+// tcgen05 GEMM: D[M,N] = A[M,K] B[N,K]^T with scales.
+//   scale_mode 0: tensor (sa[1], sb[1] float), 1: row (sa[M], sb[N] float), 2: MX (E8M0 blocked)
+struct GemmProblem {
+  const uint8_t* A; const uint8_t* B;
+  int fmt_a, fmt_b;
+  const void* sa; const void* sb;
+  int scale_mode;
+  int64_t M, N, K, lda, ldb;
+  void* D; int out_f32; int64_t ldd;
+};
+cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st);
+
+}  // namespace fp8t

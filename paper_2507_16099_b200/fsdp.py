@@ -1,0 +1,60 @@
+"""FSDP2-style FP8 weight all-gather (enable_fp8_all_gather) over the C-ABI.
+
+One process per GPU.  torch.distributed (NCCL or gloo) is used only to broadcast the
+NCCL unique id; the amax all-reduce and the FP8 all-gather are NCCL calls issued by
+libfp8train.so on the caller's stream.
+"""
+
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+from .ops import FORMATS, _ptr, _stream, hp
+
+
+def shard_rows(N, world, rank):
+    """Contiguous row shard [r*N/P, (r+1)*N/P) of an [N, K] weight (FSDP2 dim-0 sharding)."""
+    if N % world:
+        raise ValueError(f"N={N} not divisible by world size {world}")
+    n = N // world
+    return rank * n, (rank + 1) * n
+
+
+class Comm:
+    """NCCL communicator owned by libfp8train.so, bootstrapped over a torch process group."""
+
+    def __init__(self, group=None):
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if self.rank == 0:
+            buf = (ctypes.c_uint8 * 128)()
+            L.check(L.lib.fp8_comm_get_unique_id(buf), "fp8_comm_get_unique_id")
+            uid = torch.tensor(list(buf), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            uid = uid.cuda()
+        dist.broadcast(uid, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        raw = (ctypes.c_uint8 * 128)(*uid.cpu().tolist())
+        self._h = ctypes.c_void_p()
+        L.check(L.lib.fp8_comm_init(ctypes.byref(self._h), raw, self.world, self.rank), "fp8_comm_init")
+
+    def allgather_fp8(self, w_shard, fmt="e4m3", out=None, scale=None, amax=None, stream=None):
+        """Returns (w_full uint8 [P*rows, cols], scale float[1], global amax float[1])."""
+        rows, cols = w_shard.shape
+        dev = w_shard.device
+        if out is None:
+            out = torch.empty((self.world * rows, cols), dtype=torch.uint8, device=dev)
+        if scale is None:
+            scale = torch.empty(1, dtype=torch.float32, device=dev)
+        if amax is None:
+            amax = torch.empty(1, dtype=torch.float32, device=dev)
+        L.check(L.lib.fp8_fsdp_allgather(self._h, hp(w_shard), FORMATS[fmt], _ptr(out), _ptr(scale), _ptr(amax),
+                                         None, 0, _stream(stream)), "fp8_fsdp_allgather")
+        return out, scale, amax
+
+    def close(self):
+        if self._h:
+            L.check(L.lib.fp8_comm_destroy(self._h), "fp8_comm_destroy")
+            self._h = ctypes.c_void_p()

@@ -1,0 +1,92 @@
+"""Float8Linear: the paper's user surface over the C-ABI.
+
+    convert(model, recipe="tensorwise")     # analog of convert_to_float8_training(model),
+                                            # PAPER.md:614-615 (Appendix B, Listing)
+
+swaps every eligible nn.Linear for a Float8Linear whose forward/backward run the
+dynamically scaled FP8 step of §2.1 in libfp8train.so:
+amax -> scale -> saturating RNE cast -> tcgen05 scaled GEMM, for Y, dX and dW.
+"""
+
+import torch
+from torch import nn
+
+from .ops import LinearPlan
+
+
+class _Plans:
+    def __init__(self):
+        self._p = {}
+
+    def get(self, M, N, K, recipe, out_dtype, device):
+        key = (M, N, K, recipe, out_dtype, str(device))
+        if key not in self._p:
+            self._p[key] = LinearPlan(M, N, K, recipe=recipe, out_dtype=out_dtype, device=device)
+        return self._p[key]
+
+
+_PLANS = _Plans()
+
+
+class _Float8LinearFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x2d, w, recipe):
+        M, K = x2d.shape
+        N = w.shape[0]
+        plan = _PLANS.get(M, N, K, recipe, torch.bfloat16, x2d.device)
+        saved = plan.new_saved(x2d.device)
+        y = plan.forward(x2d.contiguous(), w.contiguous(), saved)
+        ctx.plan, ctx.buf, ctx.wdtype = plan, saved, w.dtype
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        dx, dw = ctx.plan.backward(dy.contiguous(), ctx.buf, want_dx=ctx.needs_input_grad[0],
+                                   want_dw=ctx.needs_input_grad[1])
+        if dw is not None and dw.dtype != ctx.wdtype:
+            dw = dw.to(ctx.wdtype)
+        return dx, dw, None
+
+
+class Float8Linear(nn.Linear):
+    """nn.Linear whose matmuls run as dynamically scaled FP8 (Appendix A recipes)."""
+
+    def __init__(self, in_features, out_features, bias=False, recipe="tensorwise", device=None, dtype=None):
+        super().__init__(in_features, out_features, bias=bias, device=device, dtype=dtype)
+        self.recipe = recipe
+
+    def forward(self, x):
+        shp = x.shape
+        x2d = x.reshape(-1, shp[-1])
+        if x2d.dtype != torch.bfloat16 and x2d.dtype != torch.float32:
+            x2d = x2d.to(torch.bfloat16)
+        y = _Float8LinearFn.apply(x2d, self.weight, self.recipe)
+        if self.bias is not None:
+            y = y + self.bias.to(y.dtype)
+        return y.reshape(*shp[:-1], self.out_features)
+
+    @classmethod
+    def from_linear(cls, lin, recipe):
+        new = cls(lin.in_features, lin.out_features, bias=lin.bias is not None, recipe=recipe,
+                  device=lin.weight.device, dtype=lin.weight.dtype)
+        with torch.no_grad():
+            new.weight.copy_(lin.weight)
+            if lin.bias is not None:
+                new.bias.copy_(lin.bias)
+        return new
+
+
+def _eligible(lin, recipe):
+    q = 128 if recipe == "mxfp8" else 16
+    return lin.in_features % q == 0 and lin.out_features % q == 0
+
+
+def convert(model, recipe="tensorwise", module_filter_fn=None):
+    """Swap nn.Linear -> Float8Linear in place (dims must be multiples of 16, 128 for mxfp8)."""
+    for name, child in list(model.named_children()):
+        if isinstance(child, nn.Linear) and not isinstance(child, Float8Linear):
+            if _eligible(child, recipe) and (module_filter_fn is None or module_filter_fn(child, name)):
+                setattr(model, name, Float8Linear.from_linear(child, recipe))
+        else:
+            convert(child, recipe, module_filter_fn)
+    return model

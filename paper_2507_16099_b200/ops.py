@@ -1,0 +1,149 @@
+"""Torch-facing wrappers of the C-ABI: argument marshalling only.
+
+Every step of the path runs in libfp8train.so; torch provides device memory and
+the current CUDA stream.  Names follow the paper's recipe vocabulary (Appendix A,
+PAPER.md:594-598): tensorwise / rowwise / mxfp8, e4m3 forward / e5m2 gradients.
+"""
+
+import ctypes
+
+import torch
+
+from . import _lib as L
+
+FORMATS = {"e4m3": L.E4M3, "e5m2": L.E5M2}
+GRANS = {"tensor": L.GRAN_TENSOR, "row": L.GRAN_ROW, "col": L.GRAN_COL, "row_col": L.GRAN_ROW_COL,
+         "mx32": L.GRAN_MX32}
+RECIPES = {"tensorwise": L.RECIPE_TENSORWISE, "rowwise": L.RECIPE_ROWWISE, "mxfp8": L.RECIPE_MXFP8}
+MX_ROUND = {"floor": L.MX_FLOOR, "rceil": L.MX_RCEIL}
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def hp(x):
+    """fp8_hp_t view of a 2-D row-major fp32/bf16 CUDA tensor (unit column stride)."""
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ValueError("expected a 2-D tensor with unit column stride")
+    if x.dtype == torch.bfloat16:
+        dt = L.DT_BF16
+    elif x.dtype == torch.float32:
+        dt = L.DT_F32
+    else:
+        raise TypeError(f"unsupported dtype {x.dtype}")
+    if not x.is_cuda:
+        raise ValueError("tensor must be on a CUDA device (no CPU fallback)")
+    return L.HP(x.data_ptr(), dt, x.shape[0], x.shape[1], x.stride(0))
+
+
+def sf_bytes(rows, cols):
+    """Bytes of an E8M0 blocked scale buffer for an MX operand [rows, cols]."""
+    return rows * cols // 32
+
+
+def amax(x, gran="tensor", stream=None):
+    n = {"tensor": 1, "row": x.shape[0], "col": x.shape[1]}[gran]
+    out = torch.empty(n, dtype=torch.float32, device=x.device)
+    L.check(L.lib.fp8_amax(hp(x), GRANS[gran], _ptr(out), None, 0, _stream(stream)), "fp8_amax")
+    return out
+
+
+def cast(x, fmt="e4m3", gran="tensor", want_q=True, want_qt=False, mx_round="floor", amax_in=None,
+         stream=None):
+    """fp8_cast_scaled.  Returns a dict with q [R,C] / q_t [C,R] (uint8), scale(s), amax."""
+    R, C = x.shape
+    dev = x.device
+    out = {"q": None, "q_t": None, "scale": None, "scale_t": None, "amax": None, "amax_t": None}
+    if want_q:
+        out["q"] = torch.empty((R, C), dtype=torch.uint8, device=dev)
+    if want_qt:
+        out["q_t"] = torch.empty((C, R), dtype=torch.uint8, device=dev)
+    f32 = dict(dtype=torch.float32, device=dev)
+    if gran == "mx32":
+        if want_q:
+            out["scale"] = torch.empty(sf_bytes(R, C), dtype=torch.uint8, device=dev)
+        if want_qt:
+            out["scale_t"] = torch.empty(sf_bytes(C, R), dtype=torch.uint8, device=dev)
+    elif gran == "row_col":
+        out["scale"], out["amax"] = torch.empty(R, **f32), torch.empty(R, **f32)
+        out["scale_t"], out["amax_t"] = torch.empty(C, **f32), torch.empty(C, **f32)
+    else:
+        n = {"tensor": 1, "row": R, "col": C}[gran]
+        out["scale"], out["amax"] = torch.empty(n, **f32), torch.empty(n, **f32)
+        if amax_in is not None:
+            out["amax"] = None
+    t = L.Tensor8(*[(out[k].data_ptr() if out[k] is not None else None)
+                    for k in ("q", "q_t", "scale", "scale_t", "amax", "amax_t")],
+                  FORMATS[fmt], GRANS[gran], R, C)
+    h = hp(x)
+    wsb = L.lib.fp8_cast_workspace_bytes(h, GRANS[gran])
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    L.check(L.lib.fp8_cast_scaled(h, MX_ROUND[mx_round], _ptr(amax_in), ctypes.byref(t), _ptr(ws), wsb,
+                                  _stream(stream)), "fp8_cast_scaled")
+    return out
+
+
+def gemm(A, fmt_a, sa, B, fmt_b, sb, gran="tensor", out_dtype=torch.bfloat16, M=None, N=None, K=None,
+         stream=None):
+    """D = A B^T with scales (fp8_gemm).  A [M,K], B [N,K] uint8 codes."""
+    M = A.shape[0] if M is None else M
+    N = B.shape[0] if N is None else N
+    K = A.shape[1] if K is None else K
+    D = torch.empty((M, N), dtype=out_dtype, device=A.device)
+    od = L.DT_F32 if out_dtype == torch.float32 else L.DT_BF16
+    L.check(L.lib.fp8_gemm(_ptr(A), FORMATS[fmt_a], _ptr(sa), _ptr(B), FORMATS[fmt_b], _ptr(sb), GRANS[gran],
+                           M, N, K, A.stride(0), B.stride(0), _ptr(D), od, D.stride(0), _stream(stream)),
+            "fp8_gemm")
+    return D
+
+
+class LinearPlan:
+    """Sizes and buffers for one Float8Linear shape (caller-owned, as the ABI requires)."""
+
+    def __init__(self, M, N, K, recipe="tensorwise", fmt_fwd="e4m3", fmt_grad="e5m2", mx_round="floor",
+                 out_dtype=torch.bfloat16, device="cuda"):
+        self.M, self.N, self.K = M, N, K
+        self.out_dtype = out_dtype
+        self.cfg = L.LinearCfg(RECIPES[recipe], FORMATS[fmt_fwd], FORMATS[fmt_grad], MX_ROUND[mx_round],
+                               L.DT_F32 if out_dtype == torch.float32 else L.DT_BF16)
+        self.saved_bytes = L.lib.fp8_linear_saved_bytes(ctypes.byref(self.cfg), M, N, K)
+        self.ws_bytes = L.lib.fp8_linear_workspace_bytes(ctypes.byref(self.cfg), M, N, K)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
+
+    def new_saved(self, device="cuda"):
+        return torch.empty(self.saved_bytes, dtype=torch.uint8, device=device)
+
+    def forward(self, x, w, saved, y=None, w_fp8=None, stream=None):
+        if y is None:
+            y = torch.empty((self.M, self.N), dtype=self.out_dtype, device=x.device)
+        wq = None
+        if w_fp8 is not None:
+            q, s = w_fp8
+            wq = L.Tensor8(q.data_ptr(), None, s.data_ptr(), None, None, None, self.cfg.fmt_fwd,
+                           L.GRAN_TENSOR, self.N, self.K)
+        wh = hp(w) if w is not None else L.HP(None, L.DT_BF16, self.N, self.K, self.K)
+        L.check(L.lib.fp8_linear_fwd(ctypes.byref(self.cfg), hp(x), wh, ctypes.byref(wq) if wq else None,
+                                     _ptr(y), _ptr(saved), _ptr(self.ws), self.ws_bytes, _stream(stream)),
+                "fp8_linear_fwd")
+        return y
+
+    def backward(self, dy, saved, dx=None, dw=None, want_dx=True, want_dw=True, stream=None):
+        dev = dy.device
+        if want_dx and dx is None:
+            dx = torch.empty((self.M, self.K), dtype=self.out_dtype, device=dev)
+        if want_dw and dw is None:
+            dw = torch.empty((self.N, self.K), dtype=self.out_dtype, device=dev)
+        L.check(L.lib.fp8_linear_bwd(ctypes.byref(self.cfg), hp(dy), self.K, _ptr(saved),
+                                     _ptr(dx) if want_dx else None, _ptr(dw) if want_dw else None,
+                                     _ptr(self.ws), self.ws_bytes, _stream(stream)), "fp8_linear_bwd")
+        return dx, dw
+
+
+def launch_count():
+    return int(L.lib.fp8_launch_count())

@@ -1,0 +1,360 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north star): amax, scales, FP8 bytes and E8M0 codes bit-exact;
+GEMM outputs within |err| <= 1e-2 * sum_k |a||b| / (s_a s_b) per element; integer-grid
+GEMMs bit-exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import codecs, fp8, gemm as ogemm, linear as olin, mx as omx
+from oracle.codecs import E4M3, E5M2
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2507_16099_b200 as fp8t
+    from paper_2507_16099_b200 import ops
+
+
+def _dev(a, dtype):
+    """numpy float32 (bf16-valued when dtype is bf16) -> CUDA tensor."""
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
+    return t.to(dtype).cuda()
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _unblock(buf, R, C):
+    """E8M0 blocked layout (fp8train.h) -> logical [R, C/32] codes (pure index permutation)."""
+    C32 = C // 32
+    b = _np(buf).reshape(R // 128, C32 // 4, 32, 4, 4)
+    return b.transpose(0, 3, 2, 1, 4).reshape(R, C32)
+
+
+def _bits(a):
+    return np.asarray(a, dtype=np.float32).view(np.uint32)
+
+
+FMTNAME = {E4M3: "e4m3", E5M2: "e5m2"}
+
+
+# ----------------------------------------------------------------------------- casts
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("fmt", [E4M3, E5M2])
+@pytest.mark.parametrize("shape", [(256, 256), (384, 320), (16, 48), (1040, 528)])
+def test_cast_tensorwise(dtype, fmt, shape):
+    x = synth.tensor_c2("x", shape, seed=0) if dtype == torch.bfloat16 else synth.tensor_c1("x", shape, seed=0)
+    q, s, a = fp8.cast_tensorwise(x, fmt)
+    out = ops.cast(_dev(x, dtype), FMTNAME[fmt], "tensor", want_q=True, want_qt=True)
+    assert _bits(_np(out["amax"]))[0] == _bits(a).reshape(-1)[0]
+    assert _bits(_np(out["scale"]))[0] == _bits(s).reshape(-1)[0]
+    assert np.array_equal(_np(out["q"]), q)
+    assert np.array_equal(_np(out["q_t"]), q.T)
+
+
+@pytest.mark.parametrize("gran", ["row", "col"])
+@pytest.mark.parametrize("fmt", [E4M3, E5M2])
+def test_cast_row_col(gran, fmt):
+    x = synth.tensor_c3("x", (400, 272), seed=1)
+    q, s, a = (fp8.cast_rowwise if gran == "row" else fp8.cast_colwise)(x, fmt)
+    out = ops.cast(_dev(x, torch.bfloat16), FMTNAME[fmt], gran, want_q=True, want_qt=True)
+    assert np.array_equal(_bits(_np(out["amax"])), _bits(a))
+    assert np.array_equal(_bits(_np(out["scale"])), _bits(s))
+    assert np.array_equal(_np(out["q"]), q)
+    assert np.array_equal(_np(out["q_t"]), q.T)
+
+
+@pytest.mark.parametrize("fmt", [E4M3, E5M2])
+def test_cast_row_col_dual(fmt):
+    # rowwise recipe dual cast: q row-scaled, q_t column-scaled, one call
+    x = synth.tensor_c3("dy", (528, 400), seed=2)
+    qr, sr, ar = fp8.cast_rowwise(x, fmt)
+    qc, sc, ac = fp8.cast_colwise(x, fmt)
+    out = ops.cast(_dev(x, torch.bfloat16), FMTNAME[fmt], "row_col", want_q=True, want_qt=True)
+    assert np.array_equal(_bits(_np(out["amax"])), _bits(ar))
+    assert np.array_equal(_bits(_np(out["amax_t"])), _bits(ac))
+    assert np.array_equal(_bits(_np(out["scale"])), _bits(sr))
+    assert np.array_equal(_bits(_np(out["scale_t"])), _bits(sc))
+    assert np.array_equal(_np(out["q"]), qr)
+    assert np.array_equal(_np(out["q_t"]), qc.T)
+
+
+def _special_tensors():
+    rng = np.random.default_rng(0)
+    z = np.zeros((128, 128), np.float32)
+    out = rng.standard_normal((128, 128)).astype(np.float32)
+    out[0, 0] = 1e4
+    tiny = (rng.standard_normal((128, 128)) * 1e-30).astype(np.float32)
+    grid = synth.integer_grid(synth.stream_key("g"), (128, 128), np.arange(-14, 15))
+    sub = (rng.standard_normal((128, 128)) * 2.0 ** -140).astype(np.float32)   # fp32 subnormals
+    signed_zero = np.where(rng.random((128, 128)) < 0.5, -0.0, 0.0).astype(np.float32)
+    signed_zero[5, 5] = 1.0
+    return {"zeros": z, "outlier": out, "tiny": tiny, "grid": grid, "subnormal": sub, "signed_zero": signed_zero}
+
+
+@pytest.mark.parametrize("name", list(_special_tensors().keys()))
+@pytest.mark.parametrize("fmt", [E4M3, E5M2])
+def test_cast_special(name, fmt):
+    x = _special_tensors()[name]
+    q, s, a = fp8.cast_tensorwise(x, fmt)
+    out = ops.cast(_dev(x, torch.float32), FMTNAME[fmt], "tensor", want_q=True, want_qt=True)
+    assert _bits(_np(out["scale"]))[0] == _bits(s).reshape(-1)[0]
+    assert np.array_equal(_np(out["q"]), q)
+    assert np.array_equal(_np(out["q_t"]), q.T)
+
+
+def _amax_for_scale(s_bits, fmt):
+    """An fp32 amax with RN32(fmax/amax) == s (searched test-side around fmax/s)."""
+    s = np.array([s_bits], np.uint32).view(np.float32)[0]
+    a0 = np.float32(codecs.FMAX[fmt] / np.float64(s))
+    for d in range(-64, 65):
+        a = (np.array([a0], np.float32).view(np.int32) + d).view(np.float32)[0]
+        if fp8.scale_from_amax(a, fmt) == s:
+            return a
+    return None
+
+
+def test_cast_double_rounding_vectors(golden):
+    # the product must be rounded to fp32 before the FP8 rounding.
+    for fmt, kind, xb, sb, want, _ in golden("cast.txt"):
+        bits = int(xb, 16) if kind == "f32" else int(xb, 16) << 16
+        x = np.array([bits], np.uint32).view(np.float32)[0]
+        a = _amax_for_scale(int(sb, 16), fmt)
+        if a is None or abs(x) > a:
+            continue
+        t = np.zeros((16, 16), np.float32)
+        t[0, 0], t[1, 1] = x, a
+        out = ops.cast(_dev(t, torch.float32), fmt, "tensor")
+        assert _bits(_np(out["scale"]))[0] == int(sb, 16)
+        assert int(_np(out["q"])[0, 0]) == int(want, 16), (xb, hex(int(_np(out["q"])[0, 0])))
+
+
+@pytest.mark.parametrize("fmt", [E4M3, E5M2])
+def test_cast_all_bf16_patterns_unit_scale(fmt):
+    # every bf16 bit pattern (NaN excluded) through the cast at s = 1 (amax_in = fmax)
+    bits = (np.arange(1 << 16, dtype=np.uint32) << 16).view(np.float32)
+    bits = bits[~np.isnan(bits)]
+    x = np.zeros(1 << 16, np.float32)
+    x[:len(bits)] = bits
+    x = x.reshape(-1, 256)
+    amax_in = torch.tensor([codecs.FMAX[fmt]], dtype=torch.float32, device="cuda")
+    out = ops.cast(_dev(x, torch.bfloat16), FMTNAME[fmt], "tensor", amax_in=amax_in)
+    assert _np(out["scale"])[0] == 1.0
+    assert np.array_equal(_np(out["q"]), codecs.encode(x, fmt))
+
+
+@pytest.mark.parametrize("fmt", [E4M3, E5M2])
+def test_cast_random_fp32_patterns(fmt):
+    rng = np.random.default_rng(5)
+    x = rng.integers(0, 2 ** 32, size=1 << 22, dtype=np.uint64).astype(np.uint32).view(np.float32)
+    x = np.where(np.isnan(x), np.float32(1.0), x).reshape(-1, 1024)
+    for amax in (codecs.FMAX[fmt], 1.0, 3.0e-20):
+        amax_in = torch.tensor([amax], dtype=torch.float32, device="cuda")
+        s = fp8.scale_from_amax(np.float32(amax), fmt)
+        out = ops.cast(_dev(x, torch.float32), FMTNAME[fmt], "tensor", amax_in=amax_in)
+        assert _bits(_np(out["scale"]))[0] == _bits(s).reshape(-1)[0]
+        assert np.array_equal(_np(out["q"]), fp8.cast_scaled(x, s, fmt))
+
+
+@pytest.mark.parametrize("gran", ["tensor", "row", "col"])
+def test_amax_entry(gran):
+    x = synth.tensor_c3("w", (272, 400), seed=3)
+    want = {"tensor": fp8.amax(x).reshape(1), "row": fp8.amax(x, 1), "col": fp8.amax(x, 0)}[gran]
+    got = ops.amax(_dev(x, torch.bfloat16), gran)
+    assert np.array_equal(_bits(_np(got)), _bits(want))
+
+
+# ----------------------------------------------------------------------------- MX casts
+
+@pytest.mark.parametrize("mode", [omx.FLOOR, omx.RCEIL])
+@pytest.mark.parametrize("fmt", [E4M3, E5M2])
+@pytest.mark.parametrize("shape", [(128, 128), (256, 384)])
+def test_mx_cast(mode, fmt, shape):
+    x = synth.tensor_c4("x", shape, seed=0)
+    q0, s0 = omx.quantize_dim0(x, fmt, mode)
+    q1, s1 = omx.quantize_dim1(x, fmt, mode)
+    out = ops.cast(_dev(x, torch.bfloat16), FMTNAME[fmt], "mx32", want_q=True, want_qt=True, mx_round=mode)
+    R, C = shape
+    assert np.array_equal(_unblock(out["scale"], R, C), s0)
+    assert np.array_equal(_unblock(out["scale_t"], C, R), s1)
+    assert np.array_equal(_np(out["q"]), q0)
+    assert np.array_equal(_np(out["q_t"]), q1)
+
+
+def test_mx_cast_fp32_subnormal_block():
+    # SURVEY App. A.8 2^-130 case: needs no flush-to-zero
+    x = np.zeros((128, 128), np.float32)
+    x[0, :32] = np.float32(2.0 ** -130)
+    x[3, 64:96] = np.float32(-(2.0 ** -135))
+    q0, s0 = omx.quantize_dim0(x, E4M3)
+    out = ops.cast(_dev(x, torch.float32), "e4m3", "mx32", want_q=True, want_qt=False)
+    assert np.array_equal(_unblock(out["scale"], 128, 128), s0)
+    assert np.array_equal(_np(out["q"]), q0)
+    assert int(_np(out["q"])[0, 0]) == 0x20
+
+
+# ----------------------------------------------------------------------------- GEMM
+
+def _grid_operands(M, N, K, seed=0):
+    vals4 = np.arange(-14, 15)
+    a = synth.integer_grid(synth.stream_key("ga", seed), (M, K), vals4)
+    b = synth.integer_grid(synth.stream_key("gb", seed), (N, K), vals4)
+    a[0, 0] = b[0, 0] = 14.0
+    return a, b
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (272, 400, 272), (1024, 768, 512), (16, 16, 16)])
+@pytest.mark.parametrize("out", [torch.float32, torch.bfloat16])
+def test_gemm_integer_grid_exact(M, N, K, out):
+    a, b = _grid_operands(M, N, K)
+    qa, sa, _ = fp8.cast_tensorwise(a, E4M3)
+    qb, sb, _ = fp8.cast_tensorwise(b, E4M3)
+    want = ogemm.gemm_ref(qa, E4M3, sa, qb, E4M3, sb)
+    assert np.array_equal(want, a.astype(np.float64) @ b.astype(np.float64).T)
+    A = torch.from_numpy(qa).cuda()
+    B = torch.from_numpy(qb).cuda()
+    SA = torch.tensor([sa], device="cuda")
+    SB = torch.tensor([sb], device="cuda")
+    D = ops.gemm(A, "e4m3", SA, B, "e4m3", SB, "tensor", out_dtype=out)
+    got = _np(D.float()).astype(np.float64)
+    exp = want.astype(np.float32).astype(np.float64) if out == torch.float32 else \
+        torch.from_numpy(want.astype(np.float32)).to(torch.bfloat16).float().numpy().astype(np.float64)
+    assert np.array_equal(got, exp)
+
+
+def _tol_check(got, ref, bound, tol=1e-2):
+    err = np.abs(got - ref)
+    ok = err <= tol * bound + 1e-30
+    assert ok.all(), f"max err ratio {np.max(err / (bound + 1e-30)):.3e} at {np.argwhere(~ok)[:4]}"
+
+
+@pytest.mark.parametrize("fa,fb", [(E4M3, E4M3), (E5M2, E4M3)])
+@pytest.mark.parametrize("M,N,K", [(256, 512, 384), (400, 272, 528)])
+def test_gemm_tensorwise_tolerance(fa, fb, M, N, K):
+    a = synth.tensor_c2("x", (M, K), seed=4)
+    b = synth.tensor_c2("w", (N, K), seed=4)
+    qa, sa, _ = fp8.cast_tensorwise(a, fa)
+    qb, sb, _ = fp8.cast_tensorwise(b, fb)
+    ref = ogemm.gemm_ref(qa, fa, sa, qb, fb, sb)
+    bd = ogemm.abs_bound(qa, fa, sa, qb, fb, sb)
+    D = ops.gemm(torch.from_numpy(qa).cuda(), FMTNAME[fa], torch.tensor([sa], device="cuda"),
+                 torch.from_numpy(qb).cuda(), FMTNAME[fb], torch.tensor([sb], device="cuda"), "tensor")
+    _tol_check(_np(D.float()).astype(np.float64), ref, bd)
+
+
+def test_gemm_rowwise_tolerance():
+    M, N, K = 384, 400, 272
+    a = synth.tensor_c3("x", (M, K), seed=5)
+    b = synth.tensor_c3("w", (N, K), seed=5)
+    qa, sa, _ = fp8.cast_rowwise(a, E4M3)
+    qb, sb, _ = fp8.cast_rowwise(b, E4M3)
+    ref = ogemm.gemm_ref(qa, E4M3, sa, qb, E4M3, sb)
+    bd = ogemm.abs_bound(qa, E4M3, sa, qb, E4M3, sb)
+    D = ops.gemm(torch.from_numpy(qa).cuda(), "e4m3", torch.from_numpy(sa).cuda(),
+                 torch.from_numpy(qb).cuda(), "e4m3", torch.from_numpy(sb).cuda(), "row")
+    _tol_check(_np(D.float()).astype(np.float64), ref, bd)
+
+
+def _block(codes_logical):
+    """logical [R, C/32] E8M0 codes -> blocked layout bytes (inverse of _unblock)."""
+    R, C32 = codes_logical.shape
+    t = codes_logical.reshape(R // 128, 4, 32, C32 // 4, 4).transpose(0, 3, 2, 1, 4)
+    return np.ascontiguousarray(t).reshape(-1)
+
+
+@pytest.mark.parametrize("fa,fb", [(E4M3, E4M3), (E5M2, E4M3)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (256, 384, 512)])
+def test_gemm_mx_tolerance(fa, fb, M, N, K):
+    a = synth.tensor_c4("x", (M, K), seed=6)
+    b = synth.tensor_c4("w", (N, K), seed=6)
+    qa, sa = omx.quantize_dim0(a, fa)
+    qb, sb = omx.quantize_dim0(b, fb)
+    ref = ogemm.mx_gemm_ref(qa, sa, fa, qb, sb, fb)
+    bd = ogemm.mx_abs_bound(qa, sa, fa, qb, sb, fb)
+    D = ops.gemm(torch.from_numpy(qa).cuda(), FMTNAME[fa], torch.from_numpy(_block(sa)).cuda(),
+                 torch.from_numpy(qb).cuda(), FMTNAME[fb], torch.from_numpy(_block(sb)).cuda(), "mx32",
+                 out_dtype=torch.float32)
+    _tol_check(_np(D).astype(np.float64), ref, bd)
+
+
+def test_gemm_mx_integer_grid_exact():
+    M, N, K = 256, 256, 256
+    a, b = _grid_operands(M, N, K, seed=1)
+    # unit-ish blocks: scale codes chosen so the grid is lossless (amax 14 -> FLOOR code 127+3-8)
+    qa, sa = omx.quantize_dim0(a, E4M3)
+    qb, sb = omx.quantize_dim0(b, E4M3)
+    ref = ogemm.mx_gemm_ref(qa, sa, E4M3, qb, sb, E4M3)
+    D = ops.gemm(torch.from_numpy(qa).cuda(), "e4m3", torch.from_numpy(_block(sa)).cuda(),
+                 torch.from_numpy(qb).cuda(), "e4m3", torch.from_numpy(_block(sb)).cuda(), "mx32",
+                 out_dtype=torch.float32)
+    assert np.array_equal(_np(D).astype(np.float64), ref)
+
+
+# ----------------------------------------------------------------------------- linear
+
+@pytest.mark.parametrize("recipe,cfg,M,N,K", [
+    ("tensorwise", "c1", 256, 256, 256),
+    ("tensorwise", "c2", 400, 272, 528),
+    ("rowwise", "c3", 384, 400, 272),
+    ("mxfp8", "c4", 256, 384, 512),
+])
+def test_linear_fwd_bwd(recipe, cfg, M, N, K):
+    x, w, dy = synth.linear_inputs(cfg, M, N, K, seed=0)
+    dt = torch.float32 if cfg == "c1" else torch.bfloat16
+    y, yb, _ = olin.forward(x, w, recipe)
+    dx, dxb, dw, dwb, _ = olin.backward(x, w, dy, recipe)
+    plan = ops.LinearPlan(M, N, K, recipe=recipe, out_dtype=torch.float32)
+    saved = plan.new_saved()
+    Y = plan.forward(_dev(x, dt), _dev(w, dt), saved)
+    DX, DW = plan.backward(_dev(dy, dt), saved)
+    torch.cuda.synchronize()
+    _tol_check(_np(Y).astype(np.float64), y, yb)
+    _tol_check(_np(DX).astype(np.float64), dx, dxb)
+    _tol_check(_np(DW).astype(np.float64), dw, dwb)
+
+
+def test_linear_bf16_out_and_autograd_module():
+    M, N, K = 256, 384, 256
+    x, w, dy = synth.linear_inputs("c2", M, N, K, seed=3)
+    y, yb, _ = olin.forward(x, w, "tensorwise")
+    dx, dxb, dw, dwb, _ = olin.backward(x, w, dy, "tensorwise")
+    lin = torch.nn.Linear(K, N, bias=False).cuda().to(torch.bfloat16)
+    with torch.no_grad():
+        lin.weight.copy_(_dev(w, torch.bfloat16))
+    model = fp8t.convert(torch.nn.Sequential(lin), "tensorwise")
+    X = _dev(x, torch.bfloat16).requires_grad_(True)
+    Y = model(X)
+    Y.backward(_dev(dy, torch.bfloat16))
+    # bf16 output adds one RN to bf16 (relative 2^-9) on top of the fp32 tolerance
+    _tol_check(_np(Y.float()).astype(np.float64), y, yb)
+    _tol_check(_np(X.grad.float()).astype(np.float64), dx, dxb)
+    _tol_check(_np(model[0].weight.grad.float()).astype(np.float64), dw, dwb)
+
+
+def test_linear_zero_grad():
+    M, N, K = 256, 256, 256
+    x, w, _ = synth.linear_inputs("c2", M, N, K, seed=0)
+    for recipe in ("tensorwise", "rowwise", "mxfp8"):
+        plan = ops.LinearPlan(M, N, K, recipe=recipe)
+        saved = plan.new_saved()
+        plan.forward(_dev(x, torch.bfloat16), _dev(w, torch.bfloat16), saved)
+        DX, DW = plan.backward(torch.zeros((M, N), dtype=torch.bfloat16, device="cuda"), saved)
+        assert torch.all(DX == 0) and torch.all(DW == 0)
+
+
+def test_errors_before_launch():
+    x = torch.zeros((100, 64), dtype=torch.bfloat16, device="cuda")   # rows % 16 != 0
+    with pytest.raises(fp8t._lib.Fp8Error) as e:
+        ops.cast(x, "e4m3", "tensor")
+    assert e.value.status == fp8t._lib.FP8_EALIGN
+    x = torch.zeros((128, 96), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(fp8t._lib.Fp8Error) as e:
+        ops.cast(x, "e4m3", "mx32", want_q=True)
+    assert e.value.status == fp8t._lib.FP8_EALIGN
