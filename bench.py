@@ -1,0 +1,453 @@
+#!/usr/bin/env python
+"""bench.py -- dynamically scaled Float8Linear fwd+bwd step on B200 (TorchAO §2.1, Appendix A).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c4|c3w1] [--impl ours|reference]
+
+One step = one pass of the whole hot path (plus a7 at N>1) over
+one batch: amax -> scale -> cast (X, W, dY) -> Y = X W^T, dX = dY W, dW = dY^T X, all
+in libfp8train.so through the C-ABI (fp8_linear_fwd / fp8_linear_bwd).
+  N = 1 : config c2 = BASELINE.json configs[1] (Llama-3-8B MLP w1, M=16384 K=4096
+          N=14336, tensorwise e4m3/e5m2, bf16 in/out).
+  N > 1 : FSDP2-style weak scaling: each rank owns N/P weight rows and M local tokens;
+          a step adds fp8_fsdp_allgather (amax all-reduce MAX + FP8 all-gather over
+          NCCL) before the forward and a bf16 reduce-scatter of dW after the backward.
+Prints ONE JSON line on rank 0 (contract: DESIGN.md §7).  --impl reference times the
+CPU oracle (oracle/) on a bounded sample of the same workload on the host cores.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP8 linear fwd+bwd TFLOPS/GPU vs FP8 peak & BF16; cast GB/s vs HBM; 1-8 GPU"
+
+CONFIGS = {
+    "c2": dict(M=16384, N=14336, K=4096, recipe="tensorwise", cfg="c2",
+               workload="c2: Llama-3-8B MLP w1 linear fwd+bwd, M=16384 tokens, K=4096, N=14336, "
+                        "tensorwise e4m3 fwd / e5m2 grad, bf16 in/out (BASELINE.json configs[1])"),
+    "c4": dict(M=16384, N=28672, K=8192, recipe="mxfp8", cfg="c4",
+               workload="c4: Llama-3-70B MLP w1 linear fwd+bwd, M=16384, K=8192, N=28672, "
+                        "MXFP8 block-32 E8M0 FLOOR, bf16 in/out (BASELINE.json configs[3])"),
+    "c3w1": dict(M=16384, N=14336, K=4096, recipe="rowwise", cfg="c3",
+                 workload="c3 (w1 linear): Llama-3-8B MLP w1 fwd+bwd, rowwise scaling, bf16 in/out "
+                          "(BASELINE.json configs[2])"),
+}
+# oracle sample for the CPU baseline / reference arm: same K and value recipe, fewer rows
+CPU_SAMPLE = dict(M=128, N=2048)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-bf16", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- oracle arm
+
+def _threads_used():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return int(max(n)) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_step_fn(cfg):
+    """One oracle fwd+bwd on the bounded sample (CPU).  Returns (fn, flops, sample_desc)."""
+    import synth
+    from oracle import linear as olin
+    Ms, Ns, K = CPU_SAMPLE["M"], CPU_SAMPLE["N"], cfg["K"]
+    f = synth.RECIPES[cfg["cfg"]]
+    x, w, dy = f("x", (Ms, K), 0, cfg["cfg"]), f("w", (Ns, K), 0, cfg["cfg"]), f("dy", (Ms, Ns), 0, cfg["cfg"])
+    recipe = cfg["recipe"]
+
+    def step():
+        olin.forward(x, w, recipe)
+        olin.backward(x, w, dy, recipe)
+
+    desc = (f"oracle/linear forward+backward ({recipe}) on a {Ms}x{Ns}x{K} (MxNxK) sample of the "
+            f"{cfg['cfg']} workload (same K and value recipe, {Ms} of {cfg['M']} tokens, {Ns} of {cfg['N']} "
+            f"weight rows); numpy fp64 GEMMs + fp32/numpy encodes")
+    return step, 6.0 * Ms * Ns * K, desc
+
+
+def cpu_baseline(cfg):
+    step, flops, desc = oracle_step_fn(cfg)
+    step()  # untimed warm run
+    t0 = time.perf_counter()
+    step()
+    dt = time.perf_counter() - t0
+    return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": _threads_used(), "kind": "oracle",
+            "sample": desc, "seconds": dt}
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # N > 1: rank 0 alone runs the oracle
+    cfg = CONFIGS[a.config]
+    step, flops, desc = oracle_step_fn(cfg)
+    for _ in range(a.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        step()
+    dt = time.perf_counter() - t0
+    v = flops * a.steps / dt / 1e12
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle GEMMs) / fp32 casts", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "sample": f"{CPU_SAMPLE['M']}x{CPU_SAMPLE['N']}x{cfg['K']}"},
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": _threads_used(), "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons while the timed region runs."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.ok = False
+        self.samples, self.reasons = [], set()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def _peaks():
+    """Roofline denominators: driver-measured MEASURED_PEAKS.json, else the guide's fallback."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm": d["hbm_gbs"], "bf16": d["bf16_tflops"], "bf16_sus": d.get("bf16_tflops_sustained",
+                                                                              d["bf16_tflops"]),
+                "src": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+def _traffic(workload_key):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(workload_key)
+    return None
+
+
+def make_inputs(cfg, M_local, N, K, rank, world, dev):
+    """Seeded synthetic inputs generated on the device with the config's value recipe
+    (SURVEY §8d / DESIGN.md "Input recipe"): X ~ N(0,1) with 8 outlier channels x20,
+    W ~ N(0, 0.02^2), dY ~ N(0, 1e-3^2) (c3: rows x 2^U(-8,8) / 2^U(-4,4); c4: per-32-block
+    magnitudes 2^U(-20,10) with 1% zero blocks)."""
+    import torch
+    g = torch.Generator(device=dev)
+
+    def randn(shape, key):
+        g.manual_seed(1000003 * key + 17)
+        return torch.randn(shape, generator=g, device=dev, dtype=torch.float32)
+
+    def unif(shape, key):
+        g.manual_seed(1000003 * key + 29)
+        return torch.rand(shape, generator=g, device=dev, dtype=torch.float32)
+
+    x = randn((M_local, K), 1 + 7 * rank)
+    ch = (unif((8,), 99) * K).long()
+    x[:, ch] *= 20.0
+    w_full = randn((N, K), 2) * 0.02          # identical on every rank, then sharded
+    dy = randn((M_local, N), 3 + 7 * rank) * 1e-3
+    if cfg["cfg"] == "c3":
+        x *= torch.exp2((2 * unif((M_local, 1), 4 + rank) - 1) * 8)
+        dy *= torch.exp2((2 * unif((M_local, 1), 5 + rank) - 1) * 8)
+        w_full *= torch.exp2((2 * unif((N, 1), 6) - 1) * 4)
+    if cfg["cfg"] == "c4":
+        def blocks(t, key):
+            R, C = t.shape
+            mag = torch.exp2(-20 + 30 * unif((R, C // 32, 1), key))
+            mag = torch.where(unif((R, C // 32, 1), key + 1) < 0.01, torch.zeros_like(mag), mag)
+            return (t.view(R, C // 32, 32) * mag).view(R, C)
+        x, w_full, dy = blocks(x, 40 + rank), blocks(w_full, 50), blocks(dy, 60 + rank)
+    r0, r1 = rank * N // world, (rank + 1) * N // world
+    w = w_full[r0:r1].contiguous()
+    return x.to(torch.bfloat16), w.to(torch.bfloat16), dy.to(torch.bfloat16), w_full.to(torch.bfloat16)
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2507_16099_b200 as fp8t  # noqa: F401  (loads libfp8train.so; raises if missing)
+    from paper_2507_16099_b200 import _lib as L, ops
+    from paper_2507_16099_b200.fsdp import Comm
+
+    cfg = CONFIGS[a.config]
+    M, N, K = cfg["M"], cfg["N"], cfg["K"]
+    fsdp = world > 1
+    if fsdp and cfg["recipe"] != "tensorwise":
+        raise SystemExit("FP8 all-gather is tensorwise-only (PAPER.md:596)")
+    x, w_shard, dy, w_full_hp = make_inputs(cfg, M, N, K, rank, world, dev)
+    if not fsdp:
+        w_shard = w_full_hp
+    del w_full_hp
+    plan = ops.LinearPlan(M, N, K, recipe=cfg["recipe"], out_dtype=torch.bfloat16, device=dev)
+    saved = plan.new_saved(dev)
+    y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+    dx = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
+    dw = torch.empty((N, K), dtype=torch.bfloat16, device=dev)
+    comm = Comm() if fsdp else None
+    if fsdp:
+        w_full = torch.empty((N, K), dtype=torch.uint8, device=dev)
+        w_scale = torch.empty(1, dtype=torch.float32, device=dev)
+        w_amax = torch.empty(1, dtype=torch.float32, device=dev)
+        dw_shard = torch.empty((N // world, K), dtype=torch.bfloat16, device=dev)
+
+    def step(xx=x, ww=w_shard, gg=dy):
+        if fsdp:
+            comm.allgather_fp8(ww, "e4m3", out=w_full, scale=w_scale, amax=w_amax)
+            plan.forward(xx, None, saved, y=y, w_fp8=(w_full, w_scale))
+            plan.backward(gg, saved, dx=dx, dw=dw)
+            dist.reduce_scatter_tensor(dw_shard, dw)
+        else:
+            plan.forward(xx, ww, saved, y=y)
+            plan.backward(gg, saved, dx=dx, dw=dw)
+
+    def barrier():
+        if fsdp:
+            dist.barrier()
+
+    for _ in range(max(a.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device events, max over ranks) ----------------
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    L.lib.fp8_profile_collect(None, None, 0)
+    L.lib.fp8_profile_enable(1)
+    n0 = ops.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(a.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = ops.launch_count() - n0
+    L.lib.fp8_profile_enable(0)
+    import ctypes
+    cap = launches + 16
+    kinds = (ctypes.c_int * cap)()
+    durs = (ctypes.c_float * cap)()
+    nrec = L.lib.fp8_profile_collect(kinds, durs, cap)
+    ms = ev0.elapsed_time(ev1)
+    if fsdp:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / a.steps
+
+    flops_step = 6.0 * M * N * K            # three GEMMs of 2*M*N*K each (per rank)
+    total_flops = flops_step * a.steps * world
+    value = total_flops / (ms / 1e3) / 1e12
+
+    # per-kernel durations from the live events
+    by = {}
+    for i in range(max(nrec, 0)):
+        by.setdefault(kinds[i], []).append(durs[i])
+    gemm_kind = 5 if cfg["recipe"] == "mxfp8" else 4
+    gemm_ms = by.get(gemm_kind, [float("nan")])
+    gemm_avg = sum(gemm_ms) / len(gemm_ms)
+    gemm_tflops = 2.0 * M * N * K / (gemm_avg / 1e3) / 1e12
+    peaks = _peaks()
+    fp8_peak = 2.0 * peaks["bf16_sus"]      # dense FP8 = 2 x bf16 (guide's nominal ratio), sustained
+    # algorithmic cast bytes per step: per hp element read by amax 2 B, by the cast 2 B,
+    # plus 1 B per FP8 layout written (X, W, dY each written in 2 layouts)
+    if cfg["recipe"] == "mxfp8":          # one fused dim0+dim1 read, 2 FP8 layouts + E8M0 scales
+        cast_bytes = (M * K + N * K + M * N) * (2 + 2 + 2 / 32.0)
+        cast_kinds = (2,)
+    elif not fsdp:                         # amax read 2 + cast read 2 + two FP8 layouts 1 + 1
+        cast_bytes = (M * K + N * K + M * N) * 6
+        cast_kinds = (0, 1)
+    else:                                  # X, dY as above; W shard: amax 2 + cast 2 + slot 1;
+        cast_bytes = (M * K + M * N) * 6 + (N // world) * K * 5 + N * K * 2   # + u8 transpose 1 + 1
+        cast_kinds = (0, 1, 3)
+    cast_ms = sum(sum(by.get(k, [])) for k in cast_kinds) / a.steps
+    cast_gbps = cast_bytes / (cast_ms / 1e3) / 1e9 if cast_ms > 0 else None
+    step_gemm_share = sum(gemm_ms) / a.steps / ms_step if ms_step > 0 else None
+
+    # ---------------- end-to-end through the public API with host buffers ----------------
+    e2e = None
+    if a.e2e_steps > 0:
+        xh = x.cpu().pin_memory()
+        wh = w_shard.cpu().pin_memory()
+        gh = dy.cpu().pin_memory()
+        yh = torch.empty_like(y, device="cpu").pin_memory()
+        dxh = torch.empty_like(dx, device="cpu").pin_memory()
+        dwh = torch.empty_like(dw if not fsdp else dw_shard, device="cpu").pin_memory()
+        xd, wd, gd = torch.empty_like(x), torch.empty_like(w_shard), torch.empty_like(dy)
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            wd.copy_(wh, non_blocking=True)
+            gd.copy_(gh, non_blocking=True)
+            step(xd, wd, gd)
+            yh.copy_(y, non_blocking=True)
+            dxh.copy_(dx, non_blocking=True)
+            dwh.copy_(dw if not fsdp else dw_shard, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if fsdp:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        h2d = (x.numel() + w_shard.numel() + dy.numel()) * 2
+        d2h = (y.numel() + dx.numel() + dwh.numel()) * 2
+        e2e = {"value": flops_step * a.e2e_steps * world / (ems / 1e3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ems / a.e2e_steps,
+               "path": "pinned host -> device copies + fp8_linear_fwd/bwd (C-ABI) + device -> host copies"}
+
+    # ---------------- cuBLAS BF16 linear of the same shape (context) ----------------
+    bf16 = None
+    if not a.no_bf16 and not fsdp:
+        wb = w_shard
+
+        def bstep():
+            torch.matmul(x, wb.t(), out=y)
+            torch.matmul(dy, wb, out=dx)
+            torch.matmul(dy.t(), x, out=dw)
+
+        for _ in range(3):
+            bstep()
+        torch.cuda.synchronize()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(a.steps):
+            bstep()
+        b1.record(stream)
+        torch.cuda.synchronize()
+        bms = b0.elapsed_time(b1) / a.steps
+        bf16 = {"ms_per_step": bms, "tflops": flops_step / (bms / 1e3) / 1e12,
+                "speedup_fp8_vs_bf16": bms / ms_step, "impl": "torch.matmul (cuBLAS) bf16, same 3 GEMMs"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(cfg)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
+            "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp8 (e4m3 x e5m2 codes, fp32 accumulate, bf16 out)",
+            "data": "synthetic (seeded, device-generated, config value recipe)",
+            "config": {"workload": cfg["workload"], "M_per_gpu": M, "N": N, "K": K, "recipe": cfg["recipe"],
+                       "parallelism": f"fsdp{world} (fp8 all-gather + amax all-reduce)" if fsdp else "single GPU",
+                       "l2": "inputs larger than L2: X 128 MiB, dY 448 MiB, ~1.2 GB streamed per step; no flush"},
+            "roofline": {"bound": "tensor", "kernel": "fp8_gemm_kernel (tcgen05 kind::%s)" %
+                         ("mxf8f6f4.block_scale" if cfg["recipe"] == "mxfp8" else "f8f6f4"),
+                         "achieved": gemm_tflops, "peak": fp8_peak, "unit": "TFLOP/s",
+                         "frac": gemm_tflops / fp8_peak, "traffic": _traffic(a.config),
+                         "peak_source": f"{peaks['src']}: bf16_tflops_sustained x 2 (dense FP8/BF16 ratio)",
+                         "algorithmic": f"2*M*N*K = {2.0 * M * N * K:.4g} flop per GEMM launch",
+                         "avg_launch_ms": gemm_avg, "share_of_step": step_gemm_share},
+            "cast": {"gbps": cast_gbps, "peak_gbps": peaks["hbm"], "frac": (cast_gbps / peaks["hbm"])
+                     if cast_gbps else None, "ms_per_step": cast_ms, "algorithmic_bytes_per_step": cast_bytes},
+            "bf16": bf16,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if fsdp:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

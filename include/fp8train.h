@@ -251,6 +251,15 @@ const char* fp8_last_error(void);
  * threads); for launch accounting in benchmarks. */
 uint64_t fp8_launch_count(void);
 
+/* Per-launch device timing for benchmarks.  While enabled, every kernel this library
+ * launches is bracketed by two CUDA events recorded on its own stream.
+ * fp8_profile_collect() waits for the recorded events, writes up to max_n records
+ * (kind, duration in ms) in launch order and clears the list; returns the number of
+ * records written (or -1 on a CUDA error).  Kinds: 0 amax, 1 cast, 2 mx_cast,
+ * 3 transpose_u8, 4 gemm (FP8), 5 gemm (MXFP8). */
+void fp8_profile_enable(int on);
+int fp8_profile_collect(int* kinds, float* ms, int max_n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -44,6 +44,8 @@ SIGNATURES = {
     "fp8_abi_version": (_c.c_int, []),
     "fp8_last_error": (_c.c_char_p, []),
     "fp8_launch_count": (_c.c_uint64, []),
+    "fp8_profile_enable": (None, [_c.c_int]),
+    "fp8_profile_collect": (_c.c_int, [_c.POINTER(_c.c_int), _c.POINTER(_c.c_float), _c.c_int]),
     "fp8_amax_workspace_bytes": (_c.c_size_t, [HP, _c.c_int]),
     "fp8_amax": (_c.c_int, [HP, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
     "fp8_cast_workspace_bytes": (_c.c_size_t, [HP, _c.c_int]),
@@ -76,7 +78,7 @@ class Fp8Error(RuntimeError):
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} not built: run `python -m paper_2507_16099_b200.build` "
+            f"{LIB_PATH} not built: run `python paper_2507_16099_b200/build.py` "
             "(there is no CPU fallback for the FP8 path)")
     lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
     for name, (res, args) in SIGNATURES.items():

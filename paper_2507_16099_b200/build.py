@@ -1,6 +1,6 @@
 """Build libfp8train.so in-tree with nvcc for sm_100a (no torch JIT, no caches).
 
-    python -m paper_2507_16099_b200.build          # or __graft_entry__.build()
+    python paper_2507_16099_b200/build.py [-v] [-f]     # or __graft_entry__.build()
 
 Flags: -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo, IEEE fp32 semantics
 (-ftz=false -prec-div=true -prec-sqrt=true, never --use_fast_math: the casts must be

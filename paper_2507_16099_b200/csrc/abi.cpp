@@ -9,7 +9,9 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "kernels.h"
 
@@ -17,6 +19,39 @@ namespace fp8t {
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// ---- optional per-launch event timing (fp8_profile_enable / fp8_profile_collect) ----
+struct ProfRec { int kind; cudaEvent_t a, b; };
+static std::atomic<int> g_prof_on{0};
+static std::mutex g_prof_mu;
+static std::vector<ProfRec> g_prof;          // recorded, not yet collected
+static std::vector<cudaEvent_t> g_prof_free;  // event pool
+
+static cudaEvent_t prof_event() {
+  if (!g_prof_free.empty()) {
+    cudaEvent_t e = g_prof_free.back();
+    g_prof_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+LaunchScope::LaunchScope(int kind, cudaStream_t s) : slot(-1), st(s) {
+  if (!g_prof_on.load(std::memory_order_relaxed)) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  ProfRec r{kind, prof_event(), prof_event()};
+  cudaEventRecord(r.a, s);
+  g_prof.push_back(r);
+  slot = (int)g_prof.size() - 1;
+}
+LaunchScope::~LaunchScope() {
+  count_launch();
+  if (slot < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (slot < (int)g_prof.size()) cudaEventRecord(g_prof[slot].b, st);
+}
 
 static thread_local std::string g_err;
 
@@ -88,6 +123,26 @@ extern "C" {
 int fp8_abi_version(void) { return FP8TRAIN_ABI_VERSION; }
 const char* fp8_last_error(void) { return g_err.c_str(); }
 uint64_t fp8_launch_count(void) { return g_launches.load(); }
+
+void fp8_profile_enable(int on) { g_prof_on.store(on ? 1 : 0); }
+
+int fp8_profile_collect(int* kinds, float* ms, int max_n) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  int n = 0, rc = 0;
+  for (auto& r : g_prof) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) rc = -1;
+    if (n < max_n) {
+      if (kinds) kinds[n] = r.kind;
+      if (ms) ms[n] = t;
+      ++n;
+    }
+    g_prof_free.push_back(r.a);
+    g_prof_free.push_back(r.b);
+  }
+  g_prof.clear();
+  return rc < 0 ? -1 : n;
+}
 
 // ---------------------------------------------------------------------------
 // amax

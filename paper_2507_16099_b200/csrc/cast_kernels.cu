@@ -379,6 +379,7 @@ static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
                                  uint32_t* ar, uint32_t* ac, cudaStream_t st) {
   const T* p = static_cast<const T*>(x);
   dim3 g = tile_grid(R, C);
+  LaunchScope ls(K_AMAX, st);
   switch (mode) {
     case 1: amax_tile_kernel<T, 1><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac); break;
     case 2: amax_tile_kernel<T, 2><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac); break;
@@ -386,7 +387,6 @@ static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
     case 6: amax_tile_kernel<T, 6><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac); break;
     default: return cudaErrorInvalidValue;
   }
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -404,8 +404,8 @@ static cudaError_t cast_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
   dim3 g = tile_grid(R, C);
 #define FP8T_CAST(QM, TM)                                                                       \
   if (qm == QM && tm == TM) {                                                                   \
+    LaunchScope ls(K_CAST, s);                                                                  \
     cast_tile_kernel<T, FMT, QM, TM><<<g, 256, 0, s>>>(p, R, C, ld, aq, at, q, qt, sq, st);     \
-    count_launch();                                                                             \
     return cudaGetLastError();                                                                  \
   }
   FP8T_CAST(1, 0) FP8T_CAST(0, 1) FP8T_CAST(1, 1)
@@ -431,10 +431,10 @@ static cudaError_t mx_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, 
                                uint8_t* q1, uint8_t* sf1, cudaStream_t s) {
   const T* p = static_cast<const T*>(x);
   dim3 g = tile_grid(R, C);
+  LaunchScope ls(K_MX, s);
   if (q0 && q1) mx_cast_kernel<T, FMT, RC, true, true><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
   else if (q0) mx_cast_kernel<T, FMT, RC, true, false><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
   else mx_cast_kernel<T, FMT, RC, false, true><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -451,8 +451,8 @@ cudaError_t launch_mx_cast(const void* x, bool bf16, int fmt, bool rceil, int64_
 }
 
 cudaError_t launch_transpose_u8(const uint8_t* in, int64_t R, int64_t C, uint8_t* out, cudaStream_t s) {
+  LaunchScope ls(K_TRANSPOSE, s);
   transpose_u8_kernel<<<tile_grid(R, C), 256, 0, s>>>(in, R, C, out);
-  count_launch();
   return cudaGetLastError();
 }
 

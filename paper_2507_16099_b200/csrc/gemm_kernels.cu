@@ -312,8 +312,8 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
   }
   a.D = p.D; a.ldd = p.ldd; a.out_f32 = p.out_f32;
   const int grid = a.num_tiles < num_sms() ? a.num_tiles : num_sms();
+  LaunchScope ls(MX ? K_GEMM_MX : K_GEMM, st);
   fp8_gemm_kernel<MX><<<grid, 256, L::bytes, st>>>(ta, tb, a);
-  count_launch();
   return cudaGetLastError();
 }
 

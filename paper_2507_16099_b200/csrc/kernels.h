@@ -7,6 +7,15 @@ namespace fp8t {
 
 void count_launch();
 
+// Launch accounting + optional per-launch CUDA-event timing (fp8_profile_enable).
+enum { K_AMAX = 0, K_CAST = 1, K_MX = 2, K_TRANSPOSE = 3, K_GEMM = 4, K_GEMM_MX = 5 };
+struct LaunchScope {
+  int slot;
+  cudaStream_t st;
+  LaunchScope(int kind, cudaStream_t s);
+  ~LaunchScope();
+};
+
 // amax_tile: mode bit0 tensor -> at[1], bit1 rows -> ar[R], bit2 cols -> ac[C] (u32 |x| bits, pre-zeroed)
 cudaError_t launch_amax(const void* x, bool bf16, int64_t R, int64_t C, int64_t ld, int mode, uint32_t* at,
                         uint32_t* ar, uint32_t* ac, cudaStream_t st);

@@ -14,8 +14,8 @@ HEADER = os.path.join(ROOT, "include", "fp8train.h")
 
 @pytest.fixture(scope="module")
 def L():
-    from paper_2507_16099_b200 import build
-    build.build()
+    import __graft_entry__
+    __graft_entry__._build_module().build()
     from paper_2507_16099_b200 import _lib
     return _lib
 
