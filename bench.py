@@ -428,6 +428,9 @@ def run_ours(a):
                          "avg_launch_ms": gemm_avg, "share_of_step": step_gemm_share},
             "cast": {"gbps": cast_gbps, "peak_gbps": peaks["hbm"], "frac": (cast_gbps / peaks["hbm"])
                      if cast_gbps else None, "ms_per_step": cast_ms, "algorithmic_bytes_per_step": cast_bytes},
+            "kernels_ms_per_step": {name: round(sum(by.get(k, [])) / a.steps, 4)
+                                    for k, name in ((0, "amax"), (1, "cast"), (2, "mx_cast"), (3, "transpose_u8"),
+                                                    (4, "gemm_fp8"), (5, "gemm_mxfp8"))},
             "bf16": bf16,
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -48,6 +48,34 @@ template <> struct Ld8<__nv_bfloat16> {
     }
   }
 };
+// Raw (undecoded) 8-element loads: issue all of a tile's loads before decoding so each
+// thread keeps 8 independent 16-32 B requests in flight with few registers.
+template <typename T> struct Raw8;
+template <> struct Raw8<float> {
+  float4 a, b;
+  __device__ __forceinline__ void load(const float* p) {
+    a = __ldg(reinterpret_cast<const float4*>(p));
+    b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  }
+  __device__ __forceinline__ void zero() { a = b = make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ __forceinline__ void get(float (&v)[8]) const {
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+};
+template <> struct Raw8<__nv_bfloat16> {
+  uint4 u;
+  __device__ __forceinline__ void load(const __nv_bfloat16* p) { u = __ldg(reinterpret_cast<const uint4*>(p)); }
+  __device__ __forceinline__ void zero() { u = make_uint4(0, 0, 0, 0); }
+  __device__ __forceinline__ void get(float (&v)[8]) const {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+};
+
 __device__ __forceinline__ int imin128(int64_t v) { return v < 128 ? (int)v : 128; }
 __device__ __forceinline__ uint32_t abs_bits(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
 
@@ -117,46 +145,66 @@ template <typename T, int MODE>  // MODE bit0: tensor, bit1: row, bit2: col
 __global__ void __launch_bounds__(256) amax_tile_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
                                                         uint32_t* amax_tensor, uint32_t* amax_row,
                                                         uint32_t* amax_col) {
+  // Persistent over 128 x 128 tiles in increasing linear order (the cast kernel walks them in
+  // decreasing order, so its first reads hit the tiles this kernel touched last, still in L2).
   __shared__ uint32_t colred[8][128];
+  __shared__ uint32_t wred[8];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int64_t r0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 128;
+  const int tiles_x = (int)((C + 127) >> 7);
+  const int num_tiles = tiles_x * (int)((R + 127) >> 7);
   const int cc = (t & 15) * 8;
-  const bool cvalid = c0 + cc < C;
   uint32_t tmax = 0;
-  uint32_t cmax[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  float v[8][8];
+  for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    const int64_t r0 = (int64_t)(tile / tiles_x) * 128, c0 = (int64_t)(tile % tiles_x) * 128;
+    const bool cvalid = c0 + cc < C;
+    uint32_t cmax[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    Raw8<T> raw[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t r = r0 + (t >> 4) + 16 * i;
-    if (cvalid && r < R) {
-      Ld8<T>::load(x + r * ld + c0 + cc, v[i]);
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) v[i][e] = 0.f;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    uint32_t rmax = 0;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const uint32_t a = abs_bits(v[i][e]);
-      rmax = max(rmax, a);
-      cmax[e] = max(cmax[e], a);
-    }
-    tmax = max(tmax, rmax);
-    if (MODE & 2) {
-      rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, 1));
-      rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, 2));
-      rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, 4));
-      rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, 8));
+    for (int i = 0; i < 8; ++i) {
       const int64_t r = r0 + (t >> 4) + 16 * i;
-      if ((t & 15) == 0 && r < R) atomicMax(amax_row + r, rmax);
+      if (cvalid && r < R) raw[i].load(x + r * ld + c0 + cc);
+      else raw[i].zero();
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t rmax = 0;
+      float vi[8];
+      raw[i].get(vi);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t a = abs_bits(vi[e]);
+        rmax = max(rmax, a);
+        cmax[e] = max(cmax[e], a);
+      }
+      tmax = max(tmax, rmax);
+      if (MODE & 2) {
+        rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, 1));
+        rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, 2));
+        rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, 4));
+        rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, 8));
+        const int64_t r = r0 + (t >> 4) + 16 * i;
+        if ((t & 15) == 0 && r < R) atomicMax(amax_row + r, rmax);
+      }
+    }
+    if (MODE & 4) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) cmax[e] = max(cmax[e], __shfl_xor_sync(0xffffffffu, cmax[e], 16));
+      if (lane < 16) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) colred[warp][cc + e] = cmax[e];
+      }
+      __syncthreads();
+      if (t < 128 && c0 + t < C) {
+        uint32_t m = colred[0][t];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) m = max(m, colred[w][t]);
+        atomicMax(amax_col + c0 + t, m);
+      }
+      __syncthreads();
     }
   }
-  if (MODE & 1) {
+  if (MODE & 1) {  // one atomic per CTA for the tensor amax
     tmax = __reduce_max_sync(0xffffffffu, tmax);
-    __shared__ uint32_t wred[8];
     if (lane == 0) wred[warp] = tmax;
     __syncthreads();
     if (t == 0) {
@@ -166,22 +214,43 @@ __global__ void __launch_bounds__(256) amax_tile_kernel(const T* __restrict__ x,
       atomicMax(amax_tensor, m);
     }
   }
-  if (MODE & 4) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      cmax[e] = max(cmax[e], __shfl_xor_sync(0xffffffffu, cmax[e], 16));
+}
+
+// Tensorwise amax of a contiguous tensor: persistent grid-stride stream of 16-byte vectors,
+// 8 independent loads in flight per thread, |x| max on raw bit patterns (bf16: two 16-bit
+// lanes per word via __vmaxu2), one atomicMax per CTA.
+template <typename T>
+__global__ void __launch_bounds__(256) amax_flat_kernel(const uint4* __restrict__ x, int64_t n16, uint32_t* out) {
+  __shared__ uint32_t wred[8];
+  constexpr bool BF = sizeof(T) == 2;
+  const uint32_t mask = BF ? 0x7FFF7FFFu : 0x7FFFFFFFu;
+  uint32_t m = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  auto fold = [&](const uint4& v) {
+    if (BF) {
+      m = __vmaxu2(m, v.x & mask); m = __vmaxu2(m, v.y & mask);
+      m = __vmaxu2(m, v.z & mask); m = __vmaxu2(m, v.w & mask);
+    } else {
+      m = max(m, v.x & mask); m = max(m, v.y & mask); m = max(m, v.z & mask); m = max(m, v.w & mask);
     }
-    if (lane < 16) {
+  };
+  for (; i + 7 * stride < n16; i += 8 * stride) {
+    uint4 v[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) colred[warp][cc + e] = cmax[e];
-    }
-    __syncthreads();
-    if (t < 128 && c0 + t < C) {
-      uint32_t m = colred[0][t];
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(x + i + u * stride);
 #pragma unroll
-      for (int w = 1; w < 8; ++w) m = max(m, colred[w][t]);
-      atomicMax(amax_col + c0 + t, m);
-    }
+    for (int u = 0; u < 8; ++u) fold(v[u]);
+  }
+  for (; i < n16; i += stride) fold(__ldg(x + i));
+  if (BF) m = max(m & 0xFFFFu, m >> 16) << 16;   // bf16 |x| bits -> fp32 bit pattern
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) wred[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t r = wred[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = max(r, wred[w]);
+    atomicMax(out, r);
   }
 }
 
@@ -199,7 +268,10 @@ __global__ void __launch_bounds__(256) cast_tile_kernel(const T* __restrict__ x,
   __shared__ float sq[128];
   __shared__ float st[128];
   const int t = threadIdx.x;
-  const int64_t r0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 128;
+  // tiles in decreasing linear order: the first tiles read are the ones amax_tile read last
+  const int rtile = (int)(gridDim.x * gridDim.y - 1 - (blockIdx.y * gridDim.x + blockIdx.x));
+  const int bx = rtile % (int)gridDim.x, by = rtile / (int)gridDim.x;
+  const int64_t r0 = (int64_t)by * 128, c0 = (int64_t)bx * 128;
   const int vrows = imin128(R - r0), vcols = imin128(C - c0);
 
   // Per-tile scale vectors (and the scale outputs).
@@ -208,34 +280,40 @@ __global__ void __launch_bounds__(256) cast_tile_kernel(const T* __restrict__ x,
       if (t == 0) {
         const float s = scale_of<FMT>(amax[0]);
         sv[0] = s;
-        if (out && blockIdx.x == 0 && blockIdx.y == 0) out[0] = s;
+        if (out && bx == 0 && by == 0) out[0] = s;
       }
     } else if (mode == 2) {
       if (t < vrows) {
         const float s = scale_of<FMT>(amax[r0 + t]);
         sv[t] = s;
-        if (out && blockIdx.x == 0) out[r0 + t] = s;
+        if (out && bx == 0) out[r0 + t] = s;
       }
     } else if (mode == 3) {
       if (t < vcols) {
         const float s = scale_of<FMT>(amax[c0 + t]);
         sv[t] = s;
-        if (out && blockIdx.y == 0) out[c0 + t] = s;
+        if (out && by == 0) out[c0 + t] = s;
       }
     }
   };
+  const int cc = (t & 15) * 8;
+  const bool cvalid = cc < vcols;
+  Raw8<T> raw[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int rr = (t >> 4) + 16 * i;
+    if (cvalid && rr < vrows) raw[i].load(x + (r0 + rr) * ld + c0 + cc);
+  }
   fill(QM, amax_q, sq, scale_q);
   fill(TM, amax_t, st, scale_t);
   __syncthreads();
 
-  const int cc = (t & 15) * 8;
-  const bool cvalid = cc < vcols;
-#pragma unroll 2
+#pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int rr = (t >> 4) + 16 * i;
     if (!cvalid || rr >= vrows) continue;
     float v[8];
-    Ld8<T>::load(x + (r0 + rr) * ld + c0 + cc, v);
+    raw[i].get(v);
     uint2 bq = make_uint2(0, 0), bt = make_uint2(0, 0);
     if (QM != 0) {
       if (QM == 1) bq = cast8<FMT>(v, sq[0]);
@@ -372,13 +450,33 @@ __global__ void __launch_bounds__(256) transpose_u8_kernel(const uint8_t* __rest
 // ---------------------------------------------------------------------------
 // Host launchers
 // ---------------------------------------------------------------------------
+static int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
 static inline dim3 tile_grid(int64_t R, int64_t C) { return dim3((unsigned)((C + 127) / 128), (unsigned)((R + 127) / 128)); }
 
 template <typename T>
 static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, int mode, uint32_t* at,
                                  uint32_t* ar, uint32_t* ac, cudaStream_t st) {
   const T* p = static_cast<const T*>(x);
-  dim3 g = tile_grid(R, C);
+  if (mode == 1 && ld == C) {
+    const int64_t n16 = R * C * (int64_t)sizeof(T) / 16;
+    const int64_t cap = (int64_t)sm_count() * 4;
+    const int64_t want = (n16 + 255) / 256;
+    LaunchScope ls(K_AMAX, st);
+    amax_flat_kernel<T><<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(reinterpret_cast<const uint4*>(x), n16, at);
+    return cudaGetLastError();
+  }
+  const int64_t tiles = ((R + 127) / 128) * ((C + 127) / 128);
+  const int64_t cap = (int64_t)sm_count() * 8;   // persistent: up to 8 resident CTAs per SM
+  dim3 g((unsigned)(tiles < cap ? tiles : cap));
   LaunchScope ls(K_AMAX, st);
   switch (mode) {
     case 1: amax_tile_kernel<T, 1><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac); break;

@@ -3,23 +3,30 @@
 //   D[m,n] = sum_k dec(A[m,k]) dec(B[n,k]) * epilogue scales
 //
 // Persistent, warp-specialised, one CTA per SM:
-//   warp 0      TMA producer: A/B tiles (SWIZZLE_128B) into a 4-stage smem ring; MX: E8M0
+//   warp 0      TMA producer: A/B tiles (SWIZZLE_128B, K-major) into an smem ring; MX: E8M0
 //               scale-factor tiles by 1-D bulk copy
-//   warp 1      MMA issuer: one thread issues tcgen05.mma.kind::f8f6f4 (or
-//               kind::mxf8f6f4.block_scale) 128x256x32 per instruction into a TMEM
-//               accumulator; tcgen05.commit frees smem stages / publishes accumulators
+//   warp 1      MMA issuer: one thread issues tcgen05.mma (kind::f8f6f4 or
+//               kind::mxf8f6f4.block_scale) into a TMEM accumulator; tcgen05.commit frees smem
+//               stages and publishes finished accumulators
 //   warp 2      TMEM allocator
 //   warps 4..7  epilogue: tcgen05.ld 32 lanes x 32 columns -> fp32 -> * (1/sa)(1/sb) ->
 //               bf16/fp32 -> global
-// Accumulators are double-buffered in TMEM (2 x 256 columns) for the plain FP8 kinds so
-// the epilogue of tile i overlaps the mainloop of tile i+1; the MX kind keeps one
-// accumulator (256 columns) plus the scale-factor columns.
+//
+// CG = 2 (default for the plain FP8 kinds): a CTA pair (cluster of 2) computes a 256 x 256
+// tile with tcgen05.mma.cta_group::2 (M = 256): each CTA stages its own 128 rows of A and
+// half (128 rows) of B, so per-SM operand traffic is 32 KB per 128-deep K block instead of
+// 48 KB; the leader CTA issues the MMAs, both CTAs hold 128 accumulator lanes.
+// CG = 1: a single CTA computes 128 x 256 (used by the MX kind and for tiny problems).
+// Accumulators are double-buffered in TMEM (2 x 256 columns) for the plain FP8 kinds so the
+// epilogue of tile i overlaps the mainloop of tile i+1; the MX kind keeps one accumulator
+// (256 columns) plus the scale-factor columns.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -27,12 +34,10 @@
 
 namespace fp8t {
 
-constexpr int BM = 128, BN = 256, BK = 128, STAGES = 4;
-constexpr int A_STAGE = BM * BK;        // 16 KB
-constexpr int B_STAGE = BN * BK;        // 32 KB
-constexpr int SFA_STAGE = 512;          // 128 rows x 4 K-blocks of E8M0
-constexpr int SFB_STAGE = 1024;         // 256 rows x 4
-constexpr int GROUP_M = 16;             // tile raster: 16 M-tiles share the N sweep (L2 reuse)
+constexpr int BM = 128, BN = 256, BK = 128;   // per-CTA M rows, MMA N, K block (bytes)
+constexpr int SFA_STAGE = 512;                // 128 rows x 4 K-blocks of E8M0
+constexpr int SFB_STAGE = 1024;               // 256 rows x 4
+constexpr int GROUP_M = 16;                   // tile raster: 16 M-tiles share the N sweep (L2 reuse)
 
 struct GemmArgs {
   int M, N, K;
@@ -44,8 +49,11 @@ struct GemmArgs {
   void* D; int64_t ldd; int out_f32; int row_scales;
 };
 
-template <bool MX> struct Layout {
+template <bool MX, int CG> struct Layout {
+  static constexpr int STAGES = CG == 2 ? 6 : 4;
   static constexpr int ACC = MX ? 1 : 2;
+  static constexpr uint32_t A_STAGE = BM * BK;              // 16 KB
+  static constexpr uint32_t B_STAGE = (BN / CG) * BK;       // 32 KB (CG=1) / 16 KB (CG=2)
   static constexpr uint32_t off_a = 0;
   static constexpr uint32_t off_b = off_a + STAGES * A_STAGE;
   static constexpr uint32_t off_sfa = off_b + STAGES * B_STAGE;
@@ -56,6 +64,7 @@ template <bool MX> struct Layout {
   static constexpr uint32_t bytes = off_tmem + 16 + 1024;  // + alignment slack
   static constexpr uint32_t tmem_cols = 512;
   static constexpr uint32_t sfa_col = 256, sfb_col = 260;  // MX only (after one accumulator)
+  static constexpr uint32_t tx_bytes = CG * (A_STAGE + B_STAGE);  // per stage, counted on the leader
 };
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
@@ -67,81 +76,101 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nb = local / gsz;
 }
 
-template <bool MX>
+template <bool MX, int CG>
 __global__ void __launch_bounds__(256, 1)
     fp8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmArgs args) {
-  using L = Layout<MX>;
+  using L = Layout<MX, CG>;
+  constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const uint32_t full_bar = base + L::off_bar;                 // [STAGES]
+  const uint32_t full_bar = base + L::off_bar;                 // [STAGES]  (leader counts both CTAs)
   const uint32_t empty_bar = full_bar + 8 * STAGES;            // [STAGES]
   const uint32_t tfull_bar = empty_bar + 8 * STAGES;           // [ACC]
-  const uint32_t tempty_bar = tfull_bar + 8 * L::ACC;          // [ACC]
+  const uint32_t tempty_bar = tfull_bar + 8 * L::ACC;          // [ACC]    (leader counts both CTAs)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L::off_tmem);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;
+  const bool leader = crank == 0;
+  const int cta_slot = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // pair / CTA index
+  const int cta_stride = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar + 8 * s, 1);
+      mbar_init(full_bar + 8 * s, CG);
       mbar_init(empty_bar + 8 * s, 1);
     }
     for (int a = 0; a < L::ACC; ++a) {
       mbar_init(tfull_bar + 8 * a, 1);
-      mbar_init(tempty_bar + 8 * a, 128);
+      mbar_init(tempty_bar + 8 * a, CG * 128);
     }
     fence_mbar_init();
   }
   if (warp == 2) {
-    tmem_alloc(smem_u32(tmem_slot), L::tmem_cols);
-    tmem_relinquish();
+    if (CG == 2) {
+      tmem_alloc_cg2(smem_u32(tmem_slot), L::tmem_cols);
+      tmem_relinquish_cg2();
+    } else {
+      tmem_alloc(smem_u32(tmem_slot), L::tmem_cols);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- TMA producer (both CTAs) ----------------
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+    for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
       int mb, nb;
       tile_coords(tile, args.tiles_m, args.tiles_n, mb, nb);
+      const int m0 = mb * BM * CG + (int)crank * BM;
+      const int n0 = nb * BN + (int)crank * (BN / CG);
       const bool sfb_hi = MX && (2 * nb + 1) * 128 < args.N;
-      const uint32_t tx = A_STAGE + B_STAGE + (MX ? SFA_STAGE + (sfb_hi ? SFB_STAGE : SFB_STAGE / 2) : 0);
+      const uint32_t tx = L::tx_bytes + (MX ? SFA_STAGE + (sfb_hi ? SFB_STAGE : SFB_STAGE / 2) : 0);
       for (int kb = 0; kb < args.num_kb; ++kb) {
         mbar_wait(empty_bar + 8 * stage, phase ^ 1);
         if (lane == 0) {
           const uint32_t fb = full_bar + 8 * stage;
-          mbar_arrive_expect_tx(fb, tx);
-          tma_load_2d(base + L::off_a + stage * A_STAGE, &tmA, kb * BK, mb * BM, fb, 0);
-          tma_load_2d(base + L::off_b + stage * B_STAGE, &tmB, kb * BK, nb * BN, fb, 0);
-          if (MX) {
-            const uint8_t* sa = args.sfa + ((int64_t)mb * args.sf_tiles_k + kb) * 512;
-            const uint8_t* sb = args.sfb + ((int64_t)(2 * nb) * args.sf_tiles_k + kb) * 512;
-            bulk_load(base + L::off_sfa + stage * SFA_STAGE, sa, 512, fb);
-            bulk_load(base + L::off_sfb + stage * SFB_STAGE, sb, 512, fb);
-            if (sfb_hi) bulk_load(base + L::off_sfb + stage * SFB_STAGE + 512, sb + (int64_t)args.sf_tiles_k * 512, 512, fb);
+          if (CG == 2) {
+            if (leader) mbar_arrive_expect_tx(fb, tx);
+            else mbar_arrive_cluster(mapa_shared(fb, 0));
+            tma_load_2d_2sm(base + L::off_a + stage * L::A_STAGE, &tmA, kb * BK, m0, fb);
+            tma_load_2d_2sm(base + L::off_b + stage * L::B_STAGE, &tmB, kb * BK, n0, fb);
+          } else {
+            mbar_arrive_expect_tx(fb, tx);
+            tma_load_2d(base + L::off_a + stage * L::A_STAGE, &tmA, kb * BK, m0, fb, 0);
+            tma_load_2d(base + L::off_b + stage * L::B_STAGE, &tmB, kb * BK, n0, fb, 0);
+            if (MX) {
+              const uint8_t* sa = args.sfa + ((int64_t)mb * args.sf_tiles_k + kb) * 512;
+              const uint8_t* sb = args.sfb + ((int64_t)(2 * nb) * args.sf_tiles_k + kb) * 512;
+              bulk_load(base + L::off_sfa + stage * SFA_STAGE, sa, 512, fb);
+              bulk_load(base + L::off_sfb + stage * SFB_STAGE, sb, 512, fb);
+              if (sfb_hi)
+                bulk_load(base + L::off_sfb + stage * SFB_STAGE + 512, sb + (int64_t)args.sf_tiles_k * 512, 512, fb);
+            }
           }
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
+  } else if (warp == 1 && leader) {
+    // ---------------- MMA issuer (leader CTA) ----------------
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+    for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
       mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -155,8 +184,8 @@ __global__ void __launch_bounds__(256, 1)
             tmem_cp_32x128b_warpx4(tmem_base + L::sfb_col + 4,
                                    make_sf_desc(base + L::off_sfb + stage * SFB_STAGE + 512));
           }
-          const uint64_t adesc = make_sw128_kmajor_desc(base + L::off_a + stage * A_STAGE);
-          const uint64_t bdesc = make_sw128_kmajor_desc(base + L::off_b + stage * B_STAGE);
+          const uint64_t adesc = make_sw128_kmajor_desc(base + L::off_a + stage * L::A_STAGE);
+          const uint64_t bdesc = make_sw128_kmajor_desc(base + L::off_b + stage * L::B_STAGE);
 #pragma unroll
           for (int k = 0; k < BK / 32; ++k) {
             // advance 32 bytes along K inside the 128-byte swizzle atom (start address >> 4)
@@ -164,11 +193,18 @@ __global__ void __launch_bounds__(256, 1)
             if (MX)
               mma_mxf8f6f4(d_tmem, adesc + koff, bdesc + koff, idesc_with_sf_id(args.idesc, k, k),
                            (kb | k) != 0, tmem_base + L::sfa_col, tmem_base + L::sfb_col);
+            else if (CG == 2)
+              mma_f8f6f4_cg2(d_tmem, adesc + koff, bdesc + koff, args.idesc, (kb | k) != 0);
             else
               mma_f8f6f4(d_tmem, adesc + koff, bdesc + koff, args.idesc, (kb | k) != 0);
           }
-          mma_commit(empty_bar + 8 * stage);
-          if (kb == args.num_kb - 1) mma_commit(tfull_bar + 8 * acc);
+          if (CG == 2) {
+            mma_commit_cg2_mc(empty_bar + 8 * stage, 0x3);
+            if (kb == args.num_kb - 1) mma_commit_cg2_mc(tfull_bar + 8 * acc, 0x3);
+          } else {
+            mma_commit(empty_bar + 8 * stage);
+            if (kb == args.num_kb - 1) mma_commit(tfull_bar + 8 * acc);
+          }
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -176,16 +212,17 @@ __global__ void __launch_bounds__(256, 1)
       if (++acc == L::ACC) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue ----------------
+    // ---------------- epilogue (both CTAs, own 128 accumulator lanes) ----------------
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
     float ts = 1.f;
     if (!args.row_scales && args.sa) ts = __frcp_rn(args.sa[0]) * __frcp_rn(args.sb[0]);
-    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+    const uint32_t tempty_leader = CG == 2 ? mapa_shared(tempty_bar, 0) : tempty_bar;
+    for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
       int mb, nb;
       tile_coords(tile, args.tiles_m, args.tiles_n, mb, nb);
-      const int row = mb * BM + q * 32 + (int)lane;
+      const int row = mb * BM * CG + (int)crank * BM + q * 32 + (int)lane;
       const bool rvalid = row < args.M;
       float rs = ts;
       if (args.row_scales && rvalid) rs = __frcp_rn(args.sa[row]);
@@ -214,7 +251,8 @@ __global__ void __launch_bounds__(256, 1)
           float* dst = reinterpret_cast<float*>(args.D) + (int64_t)row * args.ldd + col0;
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            if (4 * j < nvalid) reinterpret_cast<float4*>(dst)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            if (4 * j < nvalid)
+              reinterpret_cast<float4*>(dst)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         } else {
           uint32_t pk[16];
 #pragma unroll
@@ -225,20 +263,23 @@ __global__ void __launch_bounds__(256, 1)
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.D) + (int64_t)row * args.ldd + col0;
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (8 * j < nvalid) reinterpret_cast<uint4*>(dst)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            if (8 * j < nvalid)
+              reinterpret_cast<uint4*>(dst)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         }
       }
       tc_fence_before();
-      mbar_arrive(tempty_bar + 8 * acc);
+      if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * acc);
+      else mbar_arrive(tempty_bar + 8 * acc);
       if (++acc == L::ACC) { acc = 0; acc_phase ^= 1; }
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, L::tmem_cols);
+    if (CG == 2) tmem_dealloc_cg2(tmem_base, L::tmem_cols);
+    else tmem_dealloc(tmem_base, L::tmem_cols);
   }
 }
 
@@ -282,25 +323,33 @@ static int num_sms() {
   return n;
 }
 
-template <bool MX>
+// CTA-pair mode for the plain FP8 kinds; FP8T_GEMM_CTA_GROUP=1 forces single-CTA tiles
+// (used by the tests to cover both code paths).
+static int cta_group_for(bool mx) {
+  if (mx) return 1;
+  const char* e = getenv("FP8T_GEMM_CTA_GROUP");
+  return (e && e[0] == '1') ? 1 : 2;
+}
+
+template <bool MX, int CG>
 static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
-  using L = Layout<MX>;
+  using L = Layout<MX, CG>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(fp8_gemm_kernel<MX>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
+    attr_err = cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
   });
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap ta, tb;
-  if (!make_kmajor_map(&ta, p.A, p.M, p.K, p.lda, BM) || !make_kmajor_map(&tb, p.B, p.N, p.K, p.ldb, BN))
+  if (!make_kmajor_map(&ta, p.A, p.M, p.K, p.lda, BM) || !make_kmajor_map(&tb, p.B, p.N, p.K, p.ldb, BN / CG))
     return cudaErrorInvalidValue;
   GemmArgs a{};
   a.M = (int)p.M; a.N = (int)p.N; a.K = (int)p.K;
-  a.tiles_m = (int)((p.M + BM - 1) / BM);
+  a.tiles_m = (int)((p.M + BM * CG - 1) / (BM * CG));
   a.tiles_n = (int)((p.N + BN - 1) / BN);
   a.num_tiles = a.tiles_m * a.tiles_n;
   a.num_kb = (int)((p.K + BK - 1) / BK);
-  a.idesc = MX ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM, BN) : make_idesc_f8f6f4(p.fmt_a, p.fmt_b, BM, BN);
+  a.idesc = MX ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM, BN) : make_idesc_f8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN);
   if (MX) {
     a.sfa = static_cast<const uint8_t*>(p.sa);
     a.sfb = static_cast<const uint8_t*>(p.sb);
@@ -311,14 +360,33 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
     a.row_scales = p.scale_mode == 1;
   }
   a.D = p.D; a.ldd = p.ldd; a.out_f32 = p.out_f32;
-  const int grid = a.num_tiles < num_sms() ? a.num_tiles : num_sms();
+  const int slots = num_sms() / CG;
+  const int grid = CG * (a.num_tiles < slots ? a.num_tiles : slots);
   LaunchScope ls(MX ? K_GEMM_MX : K_GEMM, st);
-  fp8_gemm_kernel<MX><<<grid, 256, L::bytes, st>>>(ta, tb, a);
+  if (CG == 1) {
+    fp8_gemm_kernel<MX, CG><<<grid, 256, L::bytes, st>>>(ta, tb, a);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = L::bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG>, ta, tb, a);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st) {
-  return p.scale_mode == 2 ? launch_t<true>(p, st) : launch_t<false>(p, st);
+  if (p.scale_mode == 2) return launch_t<true, 1>(p, st);
+  return cta_group_for(false) == 2 ? launch_t<false, 2>(p, st) : launch_t<false, 1>(p, st);
 }
 
 }  // namespace fp8t

@@ -210,9 +210,16 @@ def _grid_operands(M, N, K, seed=0):
     return a, b
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (272, 400, 272), (1024, 768, 512), (16, 16, 16)])
+@pytest.fixture(params=["2", "1"], ids=["cta_pair", "single_cta"])
+def cta_group(request, monkeypatch):
+    """Run a GEMM test with the CTA-pair (cta_group::2) kernel and the single-CTA kernel."""
+    monkeypatch.setenv("FP8T_GEMM_CTA_GROUP", request.param)
+    return request.param
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (272, 400, 272), (1024, 768, 512), (16, 16, 16), (768, 1280, 384)])
 @pytest.mark.parametrize("out", [torch.float32, torch.bfloat16])
-def test_gemm_integer_grid_exact(M, N, K, out):
+def test_gemm_integer_grid_exact(M, N, K, out, cta_group):
     a, b = _grid_operands(M, N, K)
     qa, sa, _ = fp8.cast_tensorwise(a, E4M3)
     qb, sb, _ = fp8.cast_tensorwise(b, E4M3)
@@ -237,7 +244,7 @@ def _tol_check(got, ref, bound, tol=1e-2):
 
 @pytest.mark.parametrize("fa,fb", [(E4M3, E4M3), (E5M2, E4M3)])
 @pytest.mark.parametrize("M,N,K", [(256, 512, 384), (400, 272, 528)])
-def test_gemm_tensorwise_tolerance(fa, fb, M, N, K):
+def test_gemm_tensorwise_tolerance(fa, fb, M, N, K, cta_group):
     a = synth.tensor_c2("x", (M, K), seed=4)
     b = synth.tensor_c2("w", (N, K), seed=4)
     qa, sa, _ = fp8.cast_tensorwise(a, fa)
@@ -249,7 +256,7 @@ def test_gemm_tensorwise_tolerance(fa, fb, M, N, K):
     _tol_check(_np(D.float()).astype(np.float64), ref, bd)
 
 
-def test_gemm_rowwise_tolerance():
+def test_gemm_rowwise_tolerance(cta_group):
     M, N, K = 384, 400, 272
     a = synth.tensor_c3("x", (M, K), seed=5)
     b = synth.tensor_c3("w", (N, K), seed=5)

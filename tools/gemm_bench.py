@@ -1,0 +1,61 @@
+"""GEMM-only microbenchmark: our tcgen05 kernel (both CTA-group modes) vs cuBLASLt FP8
+(torch._scaled_mm) on the C2 GEMM shapes.  Context for tuning; not part of the contract."""
+
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2507_16099_b200 import ops  # noqa: E402
+
+SHAPES = [(16384, 14336, 4096), (16384, 4096, 14336), (14336, 4096, 16384), (8192, 8192, 8192),
+          (16384, 28672, 8192)]
+
+
+def timeit(fn, iters=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
+def main():
+    out = []
+    for M, N, K in SHAPES:
+        A = torch.randint(0, 0x70, (M, K), dtype=torch.uint8, device="cuda")
+        B = torch.randint(0, 0x70, (N, K), dtype=torch.uint8, device="cuda")
+        s = torch.ones(1, device="cuda")
+        D = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+        flops = 2.0 * M * N * K
+        row = {"M": M, "N": N, "K": K}
+        for cg in ("1", "2"):
+            os.environ["FP8T_GEMM_CTA_GROUP"] = cg
+            ms = timeit(lambda: ops.gemm(A, "e4m3", s, B, "e4m3", s, "tensor"))
+            row[f"ours_cg{cg}_tflops"] = flops / ms / 1e9
+        try:
+            a8 = A.view(torch.float8_e4m3fn)
+            b8 = B.view(torch.float8_e4m3fn)
+            ms = timeit(lambda: torch._scaled_mm(a8, b8.t(), scale_a=s, scale_b=s, out_dtype=torch.bfloat16))
+            row["cublaslt_fp8_tflops"] = flops / ms / 1e9
+        except Exception as e:  # noqa: BLE001
+            row["cublaslt_fp8_tflops"] = f"n/a: {e}"[:80]
+        Ab = torch.randn((M, K), dtype=torch.bfloat16, device="cuda")
+        Bb = torch.randn((N, K), dtype=torch.bfloat16, device="cuda")
+        ms = timeit(lambda: torch.matmul(Ab, Bb.t()), iters=10)
+        row["cublas_bf16_tflops"] = flops / ms / 1e9
+        out.append(row)
+        print(json.dumps(row), flush=True)
+        del A, B, D, Ab, Bb
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
