@@ -22,21 +22,28 @@ def shard_rows(N, world, rank):
     return rank * n, (rank + 1) * n
 
 
+def bootstrap_unique_id(group=None):
+    """ncclUniqueId from rank 0 of `group`, broadcast over the torch process group (host logic;
+    works over gloo or nccl).  Returns 128 bytes, identical on every rank."""
+    rank = dist.get_rank(group)
+    uid = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        buf = (ctypes.c_uint8 * 128)()
+        L.check(L.lib.fp8_comm_get_unique_id(buf), "fp8_comm_get_unique_id")
+        uid = torch.tensor(list(buf), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        uid = uid.cuda()
+    dist.broadcast(uid, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return bytes(uid.cpu().tolist())
+
+
 class Comm:
     """NCCL communicator owned by libfp8train.so, bootstrapped over a torch process group."""
 
     def __init__(self, group=None):
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        uid = torch.zeros(128, dtype=torch.uint8)
-        if self.rank == 0:
-            buf = (ctypes.c_uint8 * 128)()
-            L.check(L.lib.fp8_comm_get_unique_id(buf), "fp8_comm_get_unique_id")
-            uid = torch.tensor(list(buf), dtype=torch.uint8)
-        if dist.get_backend(group) == "nccl":
-            uid = uid.cuda()
-        dist.broadcast(uid, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
-        raw = (ctypes.c_uint8 * 128)(*uid.cpu().tolist())
+        raw = (ctypes.c_uint8 * 128)(*bootstrap_unique_id(group))
         self._h = ctypes.c_void_p()
         L.check(L.lib.fp8_comm_init(ctypes.byref(self._h), raw, self.world, self.rank), "fp8_comm_init")
 
