@@ -271,7 +271,7 @@ def run_ours(a):
         if fsdp:
             comm.allgather_fp8(ww, "e4m3", out=w_full, scale=w_scale, amax=w_amax)
             plan.forward(xx, None, saved, y=y, w_fp8=(w_full, w_scale))
-            plan.backward(gg, saved, dx=dx, dw=dw)
+            plan.backward(gg, saved, dx=dx, dw=dw, w_fp8=(w_full, w_scale))
             dist.reduce_scatter_tensor(dw_shard, dw)
         else:
             plan.forward(xx, ww, saved, y=y)
@@ -333,12 +333,15 @@ def run_ours(a):
     if cfg["recipe"] == "mxfp8":          # one fused dim0+dim1 read, 2 FP8 layouts + E8M0 scales
         cast_bytes = (M * K + N * K + M * N) * (2 + 2 + 2 / 32.0)
         cast_kinds = (2,)
-    elif not fsdp:                         # amax read 2 + cast read 2 + two FP8 layouts 1 + 1
+    elif cfg["recipe"] == "rowwise":       # amax read 2 + cast read 2 + row- and column-scaled layouts 1 + 1
         cast_bytes = (M * K + N * K + M * N) * 6
         cast_kinds = (0, 1)
-    else:                                  # X, dY as above; W shard: amax 2 + cast 2 + slot 1;
-        cast_bytes = (M * K + M * N) * 6 + (N // world) * K * 5 + N * K * 2   # + u8 transpose 1 + 1
-        cast_kinds = (0, 1, 3)
+    elif not fsdp:                         # tensorwise: amax 2 + cast 2 + one row-major layout 1 (the
+        cast_bytes = (M * K + N * K + M * N) * 5   # backward GEMMs read it MN-major)
+        cast_kinds = (0, 1)
+    else:                                  # X, dY: amax 2 + cast 2 + one layout 1; W shard: 2 + 2 + 1
+        cast_bytes = (M * K + M * N + (N // world) * K) * 5
+        cast_kinds = (0, 1)
     cast_ms = sum(sum(by.get(k, [])) for k in cast_kinds) / a.steps
     cast_gbps = cast_bytes / (cast_ms / 1e3) / 1e9 if cast_ms > 0 else None
     step_gemm_share = sum(gemm_ms) / a.steps / ms_step if ms_step > 0 else None

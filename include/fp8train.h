@@ -69,7 +69,7 @@
 extern "C" {
 #endif
 
-#define FP8TRAIN_ABI_VERSION 1
+#define FP8TRAIN_ABI_VERSION 2
 
 typedef enum {
   FP8_OK = 0,
@@ -172,18 +172,24 @@ fp8_status_t fp8_cast_scaled(fp8_hp_t x, fp8_mx_round_t mx_round, const float* a
 /* ---------------------------------------------------------------------------
  * fp8_gemm -- the scaled FP8 GEMM on tcgen05 tensor cores:
  *   D[m,n] = sum_k dec(A[m,k]) dec(B[n,k]) * (1/sa) * (1/sb)   fp32 accumulate
- * A [M,K] and B [N,K] are FP8 codes, both K-contiguous ("K-major"); ld in bytes
- * == elements.  Scale modes:
+ * Operand storage (`major_a`, `major_b`):
+ *   FP8_K_MAJOR : A stored [M,K] row-major (lda >= K); B stored [N,K] (ldb >= K)
+ *   FP8_MN_MAJOR: A stored [K,M] row-major (lda >= M); B stored [K,N] (ldb >= N)
+ *   (MN-major lets the backward GEMMs read the forward's row-major codes directly,
+ *    with no transposed copy; ld in bytes == elements.)
+ * Scale modes:
  *   gran TENSOR: sa, sb float[1] (multiplicative scales, device)
  *   gran ROW   : sa float[M], sb float[N]
  *   gran MX32  : sa, sb E8M0 blocked codes of A [M x K/32] and B [N x K/32];
- *                the per-32-block 2^(c-127) factors are applied inside the MMA.
+ *                the per-32-block 2^(c-127) factors are applied inside the MMA
+ *                (K-major operands only).
  * D is [M,N] row-major with leading dimension ldd elements, dtype out_dtype
  * (BF16 = RN of the fp32 result; F32 = the fp32 result).  Order of the fp32
  * accumulation and of the epilogue products is unspecified (R-c16).
  * ------------------------------------------------------------------------- */
-fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, const void* sa,
-                      const uint8_t* B, fp8_format_t fmt_b, const void* sb,
+typedef enum { FP8_K_MAJOR = 0, FP8_MN_MAJOR = 1 } fp8_major_t;
+fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, fp8_major_t major_a, const void* sa,
+                      const uint8_t* B, fp8_format_t fmt_b, fp8_major_t major_b, const void* sb,
                       fp8_gran_t gran, int64_t M, int64_t N, int64_t K,
                       int64_t lda, int64_t ldb, void* D, fp8_dtype_t out_dtype, int64_t ldd,
                       void* stream);
@@ -198,7 +204,9 @@ fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, const void* sa,
  *   (its rows/cols still give the shape).
  * saved: caller buffer of fp8_linear_saved_bytes() bytes; the forward writes
  *   the FP8 operands the backward needs (the X operand of dW and the W operand
- *   of dX with their scales, per the operand plan of DESIGN.md §2).
+ *   of dX with their scales, per the operand plan of DESIGN.md §2).  Tensorwise
+ *   saves the row-major codes the forward GEMM used (the backward GEMMs read
+ *   them MN-major); rowwise saves column-scaled copies, MXFP8 dim1 copies.
  * ws: fp8_linear_workspace_bytes() bytes of scratch.
  * ------------------------------------------------------------------------- */
 size_t fp8_linear_saved_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K);
@@ -213,9 +221,11 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
  *   operand, columns of the right"); mxfp8: dY blocks along N (dX) and along M
  *   (dW), W along N, X along M.
  * dy [M,N]; dx [M,K] and dw [N,K] out_dtype dense, either may be NULL.
- * `saved` must be the buffer the matching fp8_linear_fwd wrote. */
+ * `saved` must be the buffer the matching fp8_linear_fwd wrote.  If the forward
+ * ran with a pre-cast weight (w_fp8), pass the same codes again (FSDP2 re-gathers
+ * the weight for the backward); otherwise pass NULL. */
 fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K,
-                            const void* saved, void* dx, void* dw,
+                            const void* saved, const fp8_tensor_t* w_fp8, void* dx, void* dw,
                             void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------

@@ -259,19 +259,22 @@ fp8_status_t fp8_cast_scaled(fp8_hp_t x, fp8_mx_round_t mx_round, const float* a
 // ---------------------------------------------------------------------------
 // GEMM
 // ---------------------------------------------------------------------------
-fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, const void* sa, const uint8_t* B, fp8_format_t fmt_b,
-                      const void* sb, fp8_gran_t gran, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
-                      void* D, fp8_dtype_t out_dtype, int64_t ldd, void* stream) {
+fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, fp8_major_t major_a, const void* sa, const uint8_t* B,
+                      fp8_format_t fmt_b, fp8_major_t major_b, const void* sb, fp8_gran_t gran, int64_t M, int64_t N,
+                      int64_t K, int64_t lda, int64_t ldb, void* D, fp8_dtype_t out_dtype, int64_t ldd, void* stream) {
   FP8T_TRY(check_ptr(A, "A"));
   FP8T_TRY(check_ptr(B, "B"));
   FP8T_TRY(check_ptr(D, "D"));
   FP8T_TRY(check_fmt(fmt_a));
   FP8T_TRY(check_fmt(fmt_b));
+  if ((major_a != FP8_K_MAJOR && major_a != FP8_MN_MAJOR) || (major_b != FP8_K_MAJOR && major_b != FP8_MN_MAJOR))
+    return fail(FP8_EINVAL, "bad operand major");
   if (!sa || !sb) return fail(FP8_EINVAL, "scales: null pointer");
   if (M < 16 || N < 16 || K < 16) return fail(FP8_EINVAL, "M, N, K must be >= 16");
   if (M % 16 || N % 16 || K % 16) return fail(FP8_EALIGN, "M, N, K must be multiples of 16");
   if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return fail(FP8_EINVAL, "dims too large");
-  if (lda < K || ldb < K || ldd < N) return fail(FP8_EINVAL, "leading dimension too small");
+  if (lda < (major_a == FP8_K_MAJOR ? K : M) || ldb < (major_b == FP8_K_MAJOR ? K : N) || ldd < N)
+    return fail(FP8_EINVAL, "leading dimension too small");
   if (lda % 16 || ldb % 16) return fail(FP8_EALIGN, "lda/ldb must be multiples of 16 bytes");
   if (out_dtype != FP8_DT_BF16 && out_dtype != FP8_DT_F32) return fail(FP8_EINVAL, "bad out_dtype");
   if ((ldd * (int64_t)esize(out_dtype)) % 16) return fail(FP8_EALIGN, "ldd*elem_size must be a multiple of 16");
@@ -281,10 +284,13 @@ fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, const void* sa, cons
   else if (gran == FP8_GRAN_MX32) {
     mode = 2;
     if (M % 128 || N % 128 || K % 128) return fail(FP8_EALIGN, "MX32 GEMM needs M, N, K multiples of 128");
+    if (major_a != FP8_K_MAJOR || major_b != FP8_K_MAJOR)
+      return fail(FP8_EUNSUPPORTED, "MX32 GEMM needs K-major operands");
     FP8T_TRY(check_ptr(sa, "sfa"));
     FP8T_TRY(check_ptr(sb, "sfb"));
   } else return fail(FP8_EINVAL, "fp8_gemm: gran must be TENSOR, ROW or MX32");
-  GemmProblem p{A, B, (int)fmt_a, (int)fmt_b, sa, sb, mode, M, N, K, lda, ldb, D, out_dtype == FP8_DT_F32, ldd};
+  GemmProblem p{A, B, (int)fmt_a, (int)fmt_b, major_a == FP8_MN_MAJOR, major_b == FP8_MN_MAJOR,
+                sa, sb, mode, M, N, K, lda, ldb, D, out_dtype == FP8_DT_F32, ldd};
   FP8T_CUDA(launch_gemm(p, S(stream)), "gemm kernel");
   return FP8_OK;
 }
@@ -295,8 +301,8 @@ fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, const void* sa, cons
 namespace {
 
 struct Saved {          // written by fwd, read by bwd
-  uint8_t* xT;          // [K, M]  X operand of dW (K-major over M)
-  uint8_t* wT;          // [K, N]  W operand of dX (K-major over N)
+  uint8_t* xT;          // tensorwise: Xq [M,K] row-major (read MN-major by dW); else [K,M] (K-major over M)
+  uint8_t* wT;          // tensorwise: Wq [N,K] row-major (read MN-major by dX); else [K,N] (K-major over N)
   void* sx;             // tensorwise float[1] | rowwise float[K] | mx E8M0 [K x M/32]
   void* sw;             // tensorwise float[1] | rowwise float[K] | mx E8M0 [K x N/32]
 };
@@ -328,11 +334,14 @@ struct FwdWs {
 FwdWs carve_fwd(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K, void* base, size_t* bytes) {
   Carve c(base);
   FwdWs w{};
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {   // codes go straight to the saved buffer
+    w.amax = c.take<float>(8);
+    if (bytes) *bytes = c.off;
+    return w;
+  }
   w.xq = c.take<uint8_t>((size_t)M * K);
   w.wq = c.take<uint8_t>((size_t)N * K);
-  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
-    w.amax = c.take<float>(8);
-  } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+  if (cfg->recipe == FP8_RECIPE_ROWWISE) {
     w.amax = c.take<float>(4 * (M + K + N + K));
     w.sxr = c.take<float>(4 * M);
     w.swr = c.take<float>(4 * N);
@@ -353,8 +362,8 @@ BwdWs carve_bwd(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, void* base, s
   Carve c(base);
   BwdWs w{};
   w.g = c.take<uint8_t>((size_t)M * N);
-  w.gT = c.take<uint8_t>((size_t)M * N);
-  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+  w.gT = cfg->recipe == FP8_RECIPE_TENSORWISE ? nullptr : c.take<uint8_t>((size_t)M * N);
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {   // dW reads the row-major codes MN-major
     w.amax = c.take<float>(4);
     w.sg = c.take<float>(4);
     w.sgT = w.sg;
@@ -427,25 +436,25 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
   const int of32 = cfg->out_dtype == FP8_DT_F32;
 
   if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    // row-major codes only: the backward GEMMs read them MN-major (no transposed copies)
     uint32_t* ax = reinterpret_cast<uint32_t*>(fw.amax);
     uint32_t* aw = ax + 1;
     FP8T_CUDA(cudaMemsetAsync(ax, 0, 8, st), "memset");
     FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
-    FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 1, 1, fw.amax, fw.amax, fw.xq, sv.xT, (float*)sv.sx,
-                          (float*)sv.sx, st),
+    FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 1, 0, fw.amax, fw.amax, sv.xT, nullptr, (float*)sv.sx,
+                          nullptr, st),
               "cast x");
-    const uint8_t* wq = fw.wq;
+    const uint8_t* wq = sv.wT;
     if (w_fp8) {
       wq = w_fp8->q;
-      FP8T_CUDA(launch_transpose_u8(w_fp8->q, N, K, sv.wT, st), "transpose w");
       FP8T_CUDA(cudaMemcpyAsync(sv.sw, w_fp8->scale, 4, cudaMemcpyDeviceToDevice, st), "copy w scale");
     } else {
       FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 1, aw, nullptr, nullptr, st), "amax w");
-      FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 1, 1, fw.amax + 1, fw.amax + 1, fw.wq, sv.wT, (float*)sv.sw,
-                            (float*)sv.sw, st),
+      FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 1, 0, fw.amax + 1, fw.amax + 1, sv.wT, nullptr,
+                            (float*)sv.sw, nullptr, st),
                 "cast w");
     }
-    GemmProblem p{fw.xq, wq, ff, ff, sv.sx, sv.sw, 0, M, N, K, K, K, y, of32, N};
+    GemmProblem p{sv.xT, wq, ff, ff, 0, 0, sv.sx, sv.sw, 0, M, N, K, K, K, y, of32, N};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
   } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
     float* axr = fw.amax;
@@ -459,20 +468,20 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
               "cast x");
     FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 3, awr, awc, fw.wq, sv.wT, fw.swr, (float*)sv.sw, st),
               "cast w");
-    GemmProblem p{fw.xq, fw.wq, ff, ff, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N};
+    GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
   } else {
     const bool rc = cfg->mx_round == FP8_MX_RCEIL;
     FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, fw.xq, fw.sfx, sv.xT, (uint8_t*)sv.sx, st), "mx cast x");
     FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, fw.wq, fw.sfw, sv.wT, (uint8_t*)sv.sw, st), "mx cast w");
-    GemmProblem p{fw.xq, fw.wq, ff, ff, fw.sfx, fw.sfw, 2, M, N, K, K, K, y, of32, N};
+    GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sfx, fw.sfw, 2, M, N, K, K, K, y, of32, N};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
   }
   return FP8_OK;
 }
 
-fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K, const void* saved, void* dx,
-                            void* dw, void* ws, size_t ws_bytes, void* stream) {
+fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K, const void* saved,
+                            const fp8_tensor_t* w_fp8, void* dx, void* dw, void* ws, size_t ws_bytes, void* stream) {
   FP8T_TRY(check_hp(dy, "dy"));
   const int64_t M = dy.rows, N = dy.cols;
   FP8T_TRY(check_cfg(cfg, M, N, K));
@@ -481,6 +490,11 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K,
   if (dx) FP8T_TRY(check_ptr(dx, "dx"));
   if (dw) FP8T_TRY(check_ptr(dw, "dw"));
   if (ws_bytes < fp8_linear_workspace_bytes(cfg, M, N, K)) return fail(FP8_EWORKSPACE, "workspace too small");
+  if (w_fp8) {
+    if (cfg->recipe != FP8_RECIPE_TENSORWISE) return fail(FP8_EUNSUPPORTED, "w_fp8 needs the tensorwise recipe");
+    if (w_fp8->rows != N || w_fp8->cols != K) return fail(FP8_EINVAL, "w_fp8 shape");
+    FP8T_TRY(check_ptr(w_fp8->q, "w_fp8->q"));
+  }
   cudaStream_t st = S(stream);
   const bool gb = dy.dtype == FP8_DT_BF16;
   const int ff = cfg->fmt_fwd, fg = cfg->fmt_grad;
@@ -492,8 +506,8 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K,
     mode = 0;
     FP8T_CUDA(cudaMemsetAsync(bw.amax, 0, 4, st), "memset");
     FP8T_CUDA(launch_amax(dy.ptr, gb, M, N, dy.ld, 1, (uint32_t*)bw.amax, nullptr, nullptr, st), "amax dy");
-    FP8T_CUDA(launch_cast(dy.ptr, gb, fg, M, N, dy.ld, dx ? 1 : 0, dw ? 1 : 0, bw.amax, bw.amax, bw.g, bw.gT,
-                          (float*)bw.sg, (float*)bw.sg, st),
+    FP8T_CUDA(launch_cast(dy.ptr, gb, fg, M, N, dy.ld, 1, 0, bw.amax, bw.amax, bw.g, nullptr, (float*)bw.sg,
+                          nullptr, st),
               "cast dy");
   } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
     mode = 1;
@@ -511,12 +525,25 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K,
               "mx cast dy");
   }
   if (!dx && !dw) return FP8_OK;
+  if (mode == 0) {
+    // tensorwise: operands are the row-major codes; B of dX and both operands of dW are MN-major
+    const uint8_t* wq = w_fp8 ? w_fp8->q : sv.wT;
+    if (dx) {  // dX[M,K] = dY[M,N] . W[N,K]: A = Gq K-major over N, B = Wq stored [N,K] = MN-major
+      GemmProblem p{bw.g, wq, fg, ff, 0, 1, bw.sg, sv.sw, 0, M, K, N, N, K, dx, of32, K};
+      FP8T_CUDA(launch_gemm(p, st), "gemm dx");
+    }
+    if (dw) {  // dW[N,K] = dY^T . X: A = Gq stored [M,N] = MN-major, B = Xq stored [M,K] = MN-major
+      GemmProblem p{bw.g, sv.xT, fg, ff, 1, 1, bw.sg, sv.sx, 0, N, K, M, N, K, dw, of32, K};
+      FP8T_CUDA(launch_gemm(p, st), "gemm dw");
+    }
+    return FP8_OK;
+  }
   if (dx) {  // dX[M,K] = dY[M,N] . W  : A = dY (K-major over N), B = W^T [K,N]
-    GemmProblem p{bw.g, sv.wT, fg, ff, bw.sg, sv.sw, mode, M, K, N, N, N, dx, of32, K};
+    GemmProblem p{bw.g, sv.wT, fg, ff, 0, 0, bw.sg, sv.sw, mode, M, K, N, N, N, dx, of32, K};
     FP8T_CUDA(launch_gemm(p, st), "gemm dx");
   }
   if (dw) {  // dW[N,K] = dY^T[N,M] . X : A = dY^T [N,M], B = X^T [K,M]
-    GemmProblem p{bw.gT, sv.xT, fg, ff, bw.sgT, sv.sx, mode, N, K, M, M, M, dw, of32, K};
+    GemmProblem p{bw.gT, sv.xT, fg, ff, 0, 0, bw.sgT, sv.sx, mode, N, K, M, M, M, dw, of32, K};
     FP8T_CUDA(launch_gemm(p, st), "gemm dw");
   }
   return FP8_OK;

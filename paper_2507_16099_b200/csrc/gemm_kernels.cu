@@ -47,6 +47,7 @@ struct GemmArgs {
   const uint8_t* sfa; const uint8_t* sfb;
   int sf_tiles_k;     // K / 128: 512-byte scale tiles per 128-row block
   void* D; int64_t ldd; int out_f32; int row_scales;
+  int a_mn, b_mn;     // operand majors (MN-major: TMA boxes 128 MN x 128 K, K step 4 KB)
 };
 
 template <bool MX, int CG> struct Layout {
@@ -141,15 +142,25 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(empty_bar + 8 * stage, phase ^ 1);
         if (lane == 0) {
           const uint32_t fb = full_bar + 8 * stage;
+          const uint32_t sa_dst = base + L::off_a + stage * L::A_STAGE;
+          const uint32_t sb_dst = base + L::off_b + stage * L::B_STAGE;
+          // K-major boxes: (k, row); MN-major boxes: (mn, k), one per 128-wide MN atom
+          const int ac0 = args.a_mn ? m0 : kb * BK, ac1 = args.a_mn ? kb * BK : m0;
+          const int bc0 = args.b_mn ? n0 : kb * BK, bc1 = args.b_mn ? kb * BK : n0;
           if (CG == 2) {
             if (leader) mbar_arrive_expect_tx(fb, tx);
             else mbar_arrive_cluster(mapa_shared(fb, 0));
-            tma_load_2d_2sm(base + L::off_a + stage * L::A_STAGE, &tmA, kb * BK, m0, fb);
-            tma_load_2d_2sm(base + L::off_b + stage * L::B_STAGE, &tmB, kb * BK, n0, fb);
+            tma_load_2d_2sm(sa_dst, &tmA, ac0, ac1, fb);
+            tma_load_2d_2sm(sb_dst, &tmB, bc0, bc1, fb);
           } else {
             mbar_arrive_expect_tx(fb, tx);
-            tma_load_2d(base + L::off_a + stage * L::A_STAGE, &tmA, kb * BK, m0, fb, 0);
-            tma_load_2d(base + L::off_b + stage * L::B_STAGE, &tmB, kb * BK, n0, fb, 0);
+            tma_load_2d(sa_dst, &tmA, ac0, ac1, fb, 0);
+            if (args.b_mn) {
+              tma_load_2d(sb_dst, &tmB, n0, kb * BK, fb, 0);
+              tma_load_2d(sb_dst + 16384, &tmB, n0 + 128, kb * BK, fb, 0);
+            } else {
+              tma_load_2d(sb_dst, &tmB, bc0, bc1, fb, 0);
+            }
             if (MX) {
               const uint8_t* sa = args.sfa + ((int64_t)mb * args.sf_tiles_k + kb) * 512;
               const uint8_t* sb = args.sfb + ((int64_t)(2 * nb) * args.sf_tiles_k + kb) * 512;
@@ -184,19 +195,23 @@ __global__ void __launch_bounds__(256, 1)
             tmem_cp_32x128b_warpx4(tmem_base + L::sfb_col + 4,
                                    make_sf_desc(base + L::off_sfb + stage * SFB_STAGE + 512));
           }
-          const uint64_t adesc = make_sw128_kmajor_desc(base + L::off_a + stage * L::A_STAGE);
-          const uint64_t bdesc = make_sw128_kmajor_desc(base + L::off_b + stage * L::B_STAGE);
+          const uint32_t sa_src = base + L::off_a + stage * L::A_STAGE;
+          const uint32_t sb_src = base + L::off_b + stage * L::B_STAGE;
+          const uint64_t adesc = args.a_mn ? make_sw128_mnmajor_desc(sa_src) : make_sw128_kmajor_desc(sa_src);
+          const uint64_t bdesc = args.b_mn ? make_sw128_mnmajor_desc(sb_src) : make_sw128_kmajor_desc(sb_src);
+          // per K=32 step: K-major advances 32 B inside the 128-B swizzle row; MN-major advances
+          // 32 K-rows = 4 KB (descriptor start address is in 16-B units)
+          const uint64_t astep = args.a_mn ? 256 : 2, bstep = args.b_mn ? 256 : 2;
 #pragma unroll
           for (int k = 0; k < BK / 32; ++k) {
-            // advance 32 bytes along K inside the 128-byte swizzle atom (start address >> 4)
-            const uint64_t koff = (uint64_t)(k * 32 >> 4);
+            const uint64_t ad = adesc + astep * k, bd = bdesc + bstep * k;
             if (MX)
-              mma_mxf8f6f4(d_tmem, adesc + koff, bdesc + koff, idesc_with_sf_id(args.idesc, k, k),
-                           (kb | k) != 0, tmem_base + L::sfa_col, tmem_base + L::sfb_col);
+              mma_mxf8f6f4(d_tmem, ad, bd, idesc_with_sf_id(args.idesc, k, k), (kb | k) != 0,
+                           tmem_base + L::sfa_col, tmem_base + L::sfb_col);
             else if (CG == 2)
-              mma_f8f6f4_cg2(d_tmem, adesc + koff, bdesc + koff, args.idesc, (kb | k) != 0);
+              mma_f8f6f4_cg2(d_tmem, ad, bd, args.idesc, (kb | k) != 0);
             else
-              mma_f8f6f4(d_tmem, adesc + koff, bdesc + koff, args.idesc, (kb | k) != 0);
+              mma_f8f6f4(d_tmem, ad, bd, args.idesc, (kb | k) != 0);
           }
           if (CG == 2) {
             mma_commit_cg2_mc(empty_bar + 8 * stage, 0x3);
@@ -299,12 +314,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-static bool make_kmajor_map(CUtensorMap* m, const uint8_t* ptr, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+// 2-D u8 tensor map with SWIZZLE_128B.  K-major operand [rows, K]: dims {K, rows}, box {BK, box_rows}.
+// MN-major operand stored [K, MN]: dims {MN, K}, box {128, BK}.
+static bool make_operand_map(CUtensorMap* m, const uint8_t* ptr, bool mn_major, int64_t mn, int64_t K, int64_t ld,
+                             int box_rows) {
   auto enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t dims[2] = {(cuuint64_t)(mn_major ? mn : K), (cuuint64_t)(mn_major ? K : mn)};
   cuuint64_t strides[1] = {(cuuint64_t)ld};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)(mn_major ? 128 : BK), (cuuint32_t)(mn_major ? BK : box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(ptr), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -341,7 +359,8 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
   });
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap ta, tb;
-  if (!make_kmajor_map(&ta, p.A, p.M, p.K, p.lda, BM) || !make_kmajor_map(&tb, p.B, p.N, p.K, p.ldb, BN / CG))
+  if (!make_operand_map(&ta, p.A, p.a_mn, p.M, p.K, p.lda, BM) ||
+      !make_operand_map(&tb, p.B, p.b_mn, p.N, p.K, p.ldb, BN / CG))
     return cudaErrorInvalidValue;
   GemmArgs a{};
   a.M = (int)p.M; a.N = (int)p.N; a.K = (int)p.K;
@@ -349,7 +368,10 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
   a.tiles_n = (int)((p.N + BN - 1) / BN);
   a.num_tiles = a.tiles_m * a.tiles_n;
   a.num_kb = (int)((p.K + BK - 1) / BK);
-  a.idesc = MX ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM, BN) : make_idesc_f8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN);
+  a.idesc = MX ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM, BN)
+               : make_idesc_f8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u);
+  a.a_mn = p.a_mn;
+  a.b_mn = p.b_mn;
   if (MX) {
     a.sfa = static_cast<const uint8_t*>(p.sa);
     a.sfb = static_cast<const uint8_t*>(p.sb);

@@ -33,6 +33,7 @@ cudaError_t launch_transpose_u8(const uint8_t* in, int64_t R, int64_t C, uint8_t
 struct GemmProblem {
   const uint8_t* A; const uint8_t* B;
   int fmt_a, fmt_b;
+  int a_mn, b_mn;      // 1: operand stored MN-major ([K,M] / [K,N] row-major)
   const void* sa; const void* sb;
   int scale_mode;
   int64_t M, N, K, lda, ldb;

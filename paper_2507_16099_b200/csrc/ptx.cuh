@@ -229,6 +229,18 @@ __device__ __forceinline__ uint64_t make_sw128_kmajor_desc(uint32_t smem_addr) {
   d |= (uint64_t)2 << 61;                             // layout = SWIZZLE_128B [61,64)
   return d;
 }
+// MN-major operand tile staged by TMA with SWIZZLE_128B: 128 MN-contiguous bytes per K row,
+// 8-row (1024 B) swizzle atoms stacked along K (SBO = 1024 B); consecutive 128-wide MN atoms
+// are 128 K-rows x 128 B = 16 KB apart (LBO).
+__device__ __forceinline__ uint64_t make_sw128_mnmajor_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((16384 >> 4) & 0x3FFF) << 16;       // LBO = 16 KB between MN atoms
+  d |= (uint64_t)((1024 >> 4) & 0x3FFF) << 32;        // SBO = 1024 B between 8-row K groups
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
 // Scale-factor source for tcgen05.cp 32x128b: 32 rows x 16 B, no swizzle,
 // 8-row core matrices 128 B apart (SBO = 128 B).
 __device__ __forceinline__ uint64_t make_sf_desc(uint32_t smem_addr) {
@@ -240,12 +252,13 @@ __device__ __forceinline__ uint64_t make_sf_desc(uint32_t smem_addr) {
 }
 
 // kind::f8f6f4 instruction descriptor: D f32, A/B e4m3(0)/e5m2(1), both K-major.
-__host__ __device__ constexpr uint32_t make_idesc_f8f6f4(uint32_t a_fmt, uint32_t b_fmt, uint32_t M, uint32_t N) {
+__host__ __device__ constexpr uint32_t make_idesc_f8f6f4(uint32_t a_fmt, uint32_t b_fmt, uint32_t M, uint32_t N,
+                                                         uint32_t a_mn = 0, uint32_t b_mn = 0) {
   return (1u << 4)              // c_format = F32
          | (a_fmt << 7)         // a_format
          | (b_fmt << 10)        // b_format
-         | (0u << 15)           // a_major = K
-         | (0u << 16)           // b_major = K
+         | (a_mn << 15)         // a_major: 0 = K, 1 = MN
+         | (b_mn << 16)         // b_major
          | ((N >> 3) << 17)     // n_dim
          | ((M >> 4) << 24);    // m_dim
 }

@@ -89,17 +89,18 @@ def cast(x, fmt="e4m3", gran="tensor", want_q=True, want_qt=False, mx_round="flo
     return out
 
 
-def gemm(A, fmt_a, sa, B, fmt_b, sb, gran="tensor", out_dtype=torch.bfloat16, M=None, N=None, K=None,
+def gemm(A, fmt_a, sa, B, fmt_b, sb, gran="tensor", out_dtype=torch.bfloat16, a_mn=False, b_mn=False,
          stream=None):
-    """D = A B^T with scales (fp8_gemm).  A [M,K], B [N,K] uint8 codes."""
-    M = A.shape[0] if M is None else M
-    N = B.shape[0] if N is None else N
-    K = A.shape[1] if K is None else K
+    """D = A B^T with scales (fp8_gemm).  K-major: A [M,K], B [N,K]; MN-major (a_mn / b_mn):
+    A stored [K,M], B stored [K,N].  uint8 codes."""
+    M = A.shape[1] if a_mn else A.shape[0]
+    K = A.shape[0] if a_mn else A.shape[1]
+    N = B.shape[1] if b_mn else B.shape[0]
     D = torch.empty((M, N), dtype=out_dtype, device=A.device)
     od = L.DT_F32 if out_dtype == torch.float32 else L.DT_BF16
-    L.check(L.lib.fp8_gemm(_ptr(A), FORMATS[fmt_a], _ptr(sa), _ptr(B), FORMATS[fmt_b], _ptr(sb), GRANS[gran],
-                           M, N, K, A.stride(0), B.stride(0), _ptr(D), od, D.stride(0), _stream(stream)),
-            "fp8_gemm")
+    L.check(L.lib.fp8_gemm(_ptr(A), FORMATS[fmt_a], int(a_mn), _ptr(sa), _ptr(B), FORMATS[fmt_b], int(b_mn),
+                           _ptr(sb), GRANS[gran], M, N, K, A.stride(0), B.stride(0), _ptr(D), od, D.stride(0),
+                           _stream(stream)), "fp8_gemm")
     return D
 
 
@@ -119,27 +120,33 @@ class LinearPlan:
     def new_saved(self, device="cuda"):
         return torch.empty(self.saved_bytes, dtype=torch.uint8, device=device)
 
+    def _wq(self, w_fp8):
+        if w_fp8 is None:
+            return None
+        q, s = w_fp8
+        return L.Tensor8(q.data_ptr(), None, s.data_ptr(), None, None, None, self.cfg.fmt_fwd, L.GRAN_TENSOR,
+                         self.N, self.K)
+
     def forward(self, x, w, saved, y=None, w_fp8=None, stream=None):
+        """w_fp8: optional (codes [N,K] uint8, scale float[1]) pre-cast weight (FSDP FP8 gather)."""
         if y is None:
             y = torch.empty((self.M, self.N), dtype=self.out_dtype, device=x.device)
-        wq = None
-        if w_fp8 is not None:
-            q, s = w_fp8
-            wq = L.Tensor8(q.data_ptr(), None, s.data_ptr(), None, None, None, self.cfg.fmt_fwd,
-                           L.GRAN_TENSOR, self.N, self.K)
+        wq = self._wq(w_fp8)
         wh = hp(w) if w is not None else L.HP(None, L.DT_BF16, self.N, self.K, self.K)
         L.check(L.lib.fp8_linear_fwd(ctypes.byref(self.cfg), hp(x), wh, ctypes.byref(wq) if wq else None,
                                      _ptr(y), _ptr(saved), _ptr(self.ws), self.ws_bytes, _stream(stream)),
                 "fp8_linear_fwd")
         return y
 
-    def backward(self, dy, saved, dx=None, dw=None, want_dx=True, want_dw=True, stream=None):
+    def backward(self, dy, saved, dx=None, dw=None, want_dx=True, want_dw=True, w_fp8=None, stream=None):
         dev = dy.device
         if want_dx and dx is None:
             dx = torch.empty((self.M, self.K), dtype=self.out_dtype, device=dev)
         if want_dw and dw is None:
             dw = torch.empty((self.N, self.K), dtype=self.out_dtype, device=dev)
+        wq = self._wq(w_fp8)
         L.check(L.lib.fp8_linear_bwd(ctypes.byref(self.cfg), hp(dy), self.K, _ptr(saved),
+                                     ctypes.byref(wq) if wq else None,
                                      _ptr(dx) if want_dx else None, _ptr(dw) if want_dw else None,
                                      _ptr(self.ws), self.ws_bytes, _stream(stream)), "fp8_linear_bwd")
         return dx, dw

@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol(L):
 
 
 def test_abi_version(L):
-    assert L.lib.fp8_abi_version() == 1
+    assert L.lib.fp8_abi_version() == 2
 
 
 def test_sizes_host_only(L):
@@ -52,7 +52,9 @@ def test_sizes_host_only(L):
     saved = L.lib.fp8_linear_saved_bytes(ctypes.byref(cfg), M, N, K)
     assert saved >= K * M + K * N + 8
     ws = L.lib.fp8_linear_workspace_bytes(ctypes.byref(cfg), M, N, K)
-    assert ws >= 2 * M * N  # backward holds dY codes in both layouts
+    assert ws >= M * N  # backward holds the dY codes (read K-major by dX, MN-major by dW)
+    cfg.recipe = L.RECIPE_ROWWISE
+    assert L.lib.fp8_linear_workspace_bytes(ctypes.byref(cfg), M, N, K) >= 2 * M * N  # row- and column-scaled
     cfg.recipe = L.RECIPE_MXFP8
     assert L.lib.fp8_linear_saved_bytes(ctypes.byref(cfg), M, N, K) >= K * M + K * N + (K * M + K * N) // 32
 
@@ -74,7 +76,11 @@ def test_validation_returns_before_launch(L):
     # amax gran ROW_COL is not an amax unit
     assert L.lib.fp8_amax(L.HP(16, L.DT_BF16, 128, 96, 96), L.GRAN_ROW_COL, 16, None, 0, None) == L.FP8_EINVAL
     # GEMM K not multiple of 16
-    assert L.lib.fp8_gemm(16, 0, 32, 48, 0, 64, L.GRAN_TENSOR, 128, 128, 40, 48, 48, 80, L.DT_BF16, 128, None) == L.FP8_EALIGN
+    assert L.lib.fp8_gemm(16, 0, 0, 32, 48, 0, 0, 64, L.GRAN_TENSOR, 128, 128, 40, 48, 48, 80, L.DT_BF16, 128,
+                          None) == L.FP8_EALIGN
+    # MX GEMM with an MN-major operand is unsupported
+    assert L.lib.fp8_gemm(16, 0, 1, 32, 48, 0, 0, 64, L.GRAN_MX32, 128, 128, 128, 128, 128, 80, L.DT_BF16, 128,
+                          None) == L.FP8_EUNSUPPORTED
     # linear: workspace too small
     cfg = L.LinearCfg(L.RECIPE_TENSORWISE, L.E4M3, L.E5M2, L.MX_FLOOR, L.DT_BF16)
     st = L.lib.fp8_linear_fwd(ctypes.byref(cfg), L.HP(16, L.DT_BF16, 128, 128, 128), L.HP(32, L.DT_BF16, 128, 128, 128),

@@ -219,17 +219,20 @@ def cta_group(request, monkeypatch):
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 128), (272, 400, 272), (1024, 768, 512), (16, 16, 16), (768, 1280, 384)])
 @pytest.mark.parametrize("out", [torch.float32, torch.bfloat16])
-def test_gemm_integer_grid_exact(M, N, K, out, cta_group):
+@pytest.mark.parametrize("majors", ["KK", "KM", "MM", "MK"])
+def test_gemm_integer_grid_exact(M, N, K, out, majors, cta_group):
+    # majors: operand storage of A and B, K = K-major ([M,K] / [N,K]), M = MN-major ([K,M] / [K,N])
     a, b = _grid_operands(M, N, K)
     qa, sa, _ = fp8.cast_tensorwise(a, E4M3)
     qb, sb, _ = fp8.cast_tensorwise(b, E4M3)
     want = ogemm.gemm_ref(qa, E4M3, sa, qb, E4M3, sb)
     assert np.array_equal(want, a.astype(np.float64) @ b.astype(np.float64).T)
-    A = torch.from_numpy(qa).cuda()
-    B = torch.from_numpy(qb).cuda()
+    a_mn, b_mn = majors[0] == "M", majors[1] == "M"
+    A = torch.from_numpy(np.ascontiguousarray(qa.T if a_mn else qa)).cuda()
+    B = torch.from_numpy(np.ascontiguousarray(qb.T if b_mn else qb)).cuda()
     SA = torch.tensor([sa], device="cuda")
     SB = torch.tensor([sb], device="cuda")
-    D = ops.gemm(A, "e4m3", SA, B, "e4m3", SB, "tensor", out_dtype=out)
+    D = ops.gemm(A, "e4m3", SA, B, "e4m3", SB, "tensor", out_dtype=out, a_mn=a_mn, b_mn=b_mn)
     got = _np(D.float()).astype(np.float64)
     exp = want.astype(np.float32).astype(np.float64) if out == torch.float32 else \
         torch.from_numpy(want.astype(np.float32)).to(torch.bfloat16).float().numpy().astype(np.float64)
