@@ -15,7 +15,10 @@
 // CG = 2 (default for the plain FP8 kinds): a CTA pair (cluster of 2) computes a 256 x 256
 // tile with tcgen05.mma.cta_group::2 (M = 256): each CTA stages its own 128 rows of A and
 // half (128 rows) of B, so per-SM operand traffic is 32 KB per 128-deep K block instead of
-// 48 KB; the leader CTA issues the MMAs, both CTAs hold 128 accumulator lanes.
+// 48 KB; the leader CTA issues the MMAs, both CTAs hold 128 accumulator lanes.  A stage holds
+// KS = 2 K atoms (256-deep K, 64 KB per CTA, 3 stages): 8 MMAs per full/empty barrier round
+// trip, which halves the per-MMA synchronisation overhead of the single-atom ring (measured
+// +10-25% on the C2 shapes).
 // CG = 1: a single CTA computes 128 x 256 (used by the MX kind and for tiny problems).
 // Accumulators are double-buffered in TMEM (2 x 256 columns) for the plain FP8 kinds so the
 // epilogue of tile i overlaps the mainloop of tile i+1; the MX kind keeps one accumulator
@@ -48,13 +51,15 @@ struct GemmArgs {
   int sf_tiles_k;     // K / 128: 512-byte scale tiles per 128-row block
   void* D; int64_t ldd; int out_f32; int row_scales;
   int a_mn, b_mn;     // operand majors (MN-major: TMA boxes 128 MN x 128 K, K step 4 KB)
+  int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
 };
 
-template <bool MX, int CG> struct Layout {
-  static constexpr int STAGES = CG == 2 ? 6 : 4;
+template <bool MX, int CG, int ST, int KS> struct Layout {
+  static constexpr int STAGES = ST;
   static constexpr int ACC = MX ? 1 : 2;
-  static constexpr uint32_t A_STAGE = BM * BK;              // 16 KB
-  static constexpr uint32_t B_STAGE = (BN / CG) * BK;       // 32 KB (CG=1) / 16 KB (CG=2)
+  // a stage holds KS 128-byte K atoms (16 KB sub-tiles of 128 rows each)
+  static constexpr uint32_t A_STAGE = BM * BK * KS;         // 16 KB x KS
+  static constexpr uint32_t B_STAGE = (BN / CG) * BK * KS;  // 32 KB (CG=1) / 16 KB (CG=2), x KS
   static constexpr uint32_t off_a = 0;
   static constexpr uint32_t off_b = off_a + STAGES * A_STAGE;
   static constexpr uint32_t off_sfa = off_b + STAGES * B_STAGE;
@@ -77,11 +82,12 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nb = local / gsz;
 }
 
-template <bool MX, int CG>
+template <bool MX, int CG, int ST, int KS>
 __global__ void __launch_bounds__(256, 1)
     fp8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmArgs args) {
-  using L = Layout<MX, CG>;
+  static_assert(KS == 1 || (CG == 2 && !MX), "multi-atom stages: CTA-pair plain FP8 only");
+  using L = Layout<MX, CG, ST, KS>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -150,8 +156,12 @@ __global__ void __launch_bounds__(256, 1)
           if (CG == 2) {
             if (leader) mbar_arrive_expect_tx(fb, tx);
             else mbar_arrive_cluster(mapa_shared(fb, 0));
-            tma_load_2d_2sm(sa_dst, &tmA, ac0, ac1, fb);
-            tma_load_2d_2sm(sb_dst, &tmB, bc0, bc1, fb);
+#pragma unroll
+            for (int j = 0; j < KS; ++j) {   // K atom j of this stage: k0 = (kb*KS + j)*BK
+              const int k0 = (kb * KS + j) * BK;
+              tma_load_2d_2sm(sa_dst + j * 16384, &tmA, args.a_mn ? m0 : k0, args.a_mn ? k0 : m0, fb);
+              tma_load_2d_2sm(sb_dst + j * 16384, &tmB, args.b_mn ? n0 : k0, args.b_mn ? k0 : n0, fb);
+            }
           } else {
             mbar_arrive_expect_tx(fb, tx);
             tma_load_2d(sa_dst, &tmA, ac0, ac1, fb, 0);
@@ -201,10 +211,14 @@ __global__ void __launch_bounds__(256, 1)
           const uint64_t bdesc = args.b_mn ? make_sw128_mnmajor_desc(sb_src) : make_sw128_kmajor_desc(sb_src);
           // per K=32 step: K-major advances 32 B inside the 128-B swizzle row; MN-major advances
           // 32 K-rows = 4 KB (descriptor start address is in 16-B units)
-          const uint64_t astep = args.a_mn ? 256 : 2, bstep = args.b_mn ? 256 : 2;
+          // K atoms of one stage are 16 KB apart: K-major jumps 1024 (16-B units) every 4 steps;
+          // MN-major atoms are contiguous (4 steps x 4 KB = 16 KB)
+          auto koff = [](int mn, int k) -> uint64_t {
+            return mn ? (uint64_t)(256 * k) : (uint64_t)(1024 * (k >> 2) + 2 * (k & 3));
+          };
 #pragma unroll
-          for (int k = 0; k < BK / 32; ++k) {
-            const uint64_t ad = adesc + astep * k, bd = bdesc + bstep * k;
+          for (int k = 0; k < KS * BK / 32; ++k) {
+            const uint64_t ad = adesc + koff(args.a_mn, k), bd = bdesc + koff(args.b_mn, k);
             if (MX)
               mma_mxf8f6f4(d_tmem, ad, bd, idesc_with_sf_id(args.idesc, k, k), (kb | k) != 0,
                            tmem_base + L::sfa_col, tmem_base + L::sfb_col);
@@ -249,7 +263,7 @@ __global__ void __launch_bounds__(256, 1)
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_wait_ld();
         const int col0 = nb * BN + c * 32;
-        if (!rvalid || col0 >= args.N) continue;
+        if (!rvalid || col0 >= args.N || (args.debug & 1)) continue;
         float v[32];
         if (args.row_scales) {
 #pragma unroll
@@ -349,13 +363,14 @@ static int cta_group_for(bool mx) {
   return (e && e[0] == '1') ? 1 : 2;
 }
 
-template <bool MX, int CG>
+template <bool MX, int CG, int ST, int KS>
 static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
-  using L = Layout<MX, CG>;
+  using L = Layout<MX, CG, ST, KS>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
+    attr_err =
+        cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG, ST, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
   });
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap ta, tb;
@@ -367,7 +382,7 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
   a.tiles_m = (int)((p.M + BM * CG - 1) / (BM * CG));
   a.tiles_n = (int)((p.N + BN - 1) / BN);
   a.num_tiles = a.tiles_m * a.tiles_n;
-  a.num_kb = (int)((p.K + BK - 1) / BK);
+  a.num_kb = (int)((p.K + BK * KS - 1) / (BK * KS));
   a.idesc = MX ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM, BN)
                : make_idesc_f8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u);
   a.a_mn = p.a_mn;
@@ -382,11 +397,15 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
     a.row_scales = p.scale_mode == 1;
   }
   a.D = p.D; a.ldd = p.ldd; a.out_f32 = p.out_f32;
+  {
+    const char* d = getenv("FP8T_GEMM_DEBUG");
+    a.debug = d ? atoi(d) : 0;
+  }
   const int slots = num_sms() / CG;
   const int grid = CG * (a.num_tiles < slots ? a.num_tiles : slots);
   LaunchScope ls(MX ? K_GEMM_MX : K_GEMM, st);
   if (CG == 1) {
-    fp8_gemm_kernel<MX, CG><<<grid, 256, L::bytes, st>>>(ta, tb, a);
+    fp8_gemm_kernel<MX, CG, ST, KS><<<grid, 256, L::bytes, st>>>(ta, tb, a);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -400,15 +419,21 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG>, ta, tb, a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS>, ta, tb, a);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st) {
-  if (p.scale_mode == 2) return launch_t<true, 1>(p, st);
-  return cta_group_for(false) == 2 ? launch_t<false, 2>(p, st) : launch_t<false, 1>(p, st);
+  if (p.scale_mode == 2) return launch_t<true, 1, 4, 1>(p, st);
+  if (cta_group_for(false) == 1) return launch_t<false, 1, 4, 1>(p, st);
+  // default: 3 stages x 2 K atoms (64 KB per CTA per stage, 8 MMAs per barrier round trip);
+  // FP8T_GEMM_STAGES=6 selects 6 x 1 atom (4 MMAs per round trip) for comparison
+  const char* e = getenv("FP8T_GEMM_STAGES");
+  if (e && e[0] == '6') return launch_t<false, 2, 6, 1>(p, st);
+  if (e && e[0] == '4') return launch_t<false, 2, 4, 1>(p, st);
+  return launch_t<false, 2, 3, 2>(p, st);
 }
 
 }  // namespace fp8t

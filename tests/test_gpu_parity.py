@@ -210,10 +210,12 @@ def _grid_operands(M, N, K, seed=0):
     return a, b
 
 
-@pytest.fixture(params=["2", "1"], ids=["cta_pair", "single_cta"])
+@pytest.fixture(params=["2", "2s6", "1"], ids=["cta_pair", "cta_pair_1atom", "single_cta"])
 def cta_group(request, monkeypatch):
-    """Run a GEMM test with the CTA-pair (cta_group::2) kernel and the single-CTA kernel."""
-    monkeypatch.setenv("FP8T_GEMM_CTA_GROUP", request.param)
+    """Run a GEMM test with each kernel variant: CTA pair (cta_group::2) with 2-atom stages
+    (default), CTA pair with 1-atom stages, single CTA."""
+    monkeypatch.setenv("FP8T_GEMM_CTA_GROUP", request.param[0])
+    monkeypatch.setenv("FP8T_GEMM_STAGES", "6" if request.param == "2s6" else "3")
     return request.param
 
 

@@ -36,21 +36,26 @@ def main():
         D = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
         flops = 2.0 * M * N * K
         row = {"M": M, "N": N, "K": K}
-        for cg in ("1", "2"):
+        for cg, st, dbg in (("2", "6", "0"), ("2", "3", "0"), ("2", "4", "0"), ("2", "6", "1"), ("2", "3", "1")):
             os.environ["FP8T_GEMM_CTA_GROUP"] = cg
+            os.environ["FP8T_GEMM_STAGES"] = st
+            os.environ["FP8T_GEMM_DEBUG"] = dbg
             ms = timeit(lambda: ops.gemm(A, "e4m3", s, B, "e4m3", s, "tensor"))
-            row[f"ours_cg{cg}_tflops"] = flops / ms / 1e9
+            row[f"cg{cg}_st{st}_dbg{dbg}"] = round(flops / ms / 1e9)
+        os.environ["FP8T_GEMM_DEBUG"] = "0"
+        os.environ["FP8T_GEMM_STAGES"] = "6"
+        os.environ["FP8T_GEMM_CTA_GROUP"] = "2"
         try:
             a8 = A.view(torch.float8_e4m3fn)
             b8 = B.view(torch.float8_e4m3fn)
             ms = timeit(lambda: torch._scaled_mm(a8, b8.t(), scale_a=s, scale_b=s, out_dtype=torch.bfloat16))
-            row["cublaslt_fp8_tflops"] = flops / ms / 1e9
+            row["cublaslt_fp8_tflops"] = round(flops / ms / 1e9)
         except Exception as e:  # noqa: BLE001
             row["cublaslt_fp8_tflops"] = f"n/a: {e}"[:80]
         Ab = torch.randn((M, K), dtype=torch.bfloat16, device="cuda")
         Bb = torch.randn((N, K), dtype=torch.bfloat16, device="cuda")
         ms = timeit(lambda: torch.matmul(Ab, Bb.t()), iters=10)
-        row["cublas_bf16_tflops"] = flops / ms / 1e9
+        row["cublas_bf16_tflops"] = round(flops / ms / 1e9)
         out.append(row)
         print(json.dumps(row), flush=True)
         del A, B, D, Ab, Bb
