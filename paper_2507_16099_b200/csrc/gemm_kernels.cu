@@ -19,10 +19,12 @@
 // KS = 2 K atoms (256-deep K, 64 KB per CTA, 3 stages): 8 MMAs per full/empty barrier round
 // trip, which halves the per-MMA synchronisation overhead of the single-atom ring (measured
 // +10-25% on the C2 shapes).
-// CG = 1: a single CTA computes 128 x 256 (used by the MX kind and for tiny problems).
+// CG = 1: a single CTA computes 128 x 256 (kept as a reference variant; FP8T_GEMM_CTA_GROUP=1).
 // Accumulators are double-buffered in TMEM (2 x 256 columns) for the plain FP8 kinds so the
 // epilogue of tile i overlaps the mainloop of tile i+1; the MX kind keeps one accumulator
-// (256 columns) plus the scale-factor columns.
+// (256 columns) plus the scale-factor columns (E8M0 tiles loaded by TMA next to the operands,
+// tcgen05.cp'd into TMEM per stage; in CTA-pair mode each CTA holds SFA for its own rows and
+// SFB for all 256 N rows).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -37,9 +39,8 @@
 
 namespace fp8t {
 
-constexpr int BM = 128, BN = 256, BK = 128;   // per-CTA M rows, MMA N, K block (bytes)
-constexpr int SFA_STAGE = 512;                // 128 rows x 4 K-blocks of E8M0
-constexpr int SFB_STAGE = 1024;               // 256 rows x 4
+constexpr int BM = 128, BN = 256, BK = 128;   // per-CTA M rows, MMA N, K atom (bytes)
+constexpr int SF_CHUNK = 512;                 // E8M0 tile: 128 rows x 4 K-blocks of 32 (one K atom)
 constexpr int GROUP_M = 16;                   // tile raster: 16 M-tiles share the N sweep (L2 reuse)
 
 struct GemmArgs {
@@ -47,8 +48,7 @@ struct GemmArgs {
   int tiles_m, tiles_n, num_tiles, num_kb;
   uint32_t idesc;
   const float* sa; const float* sb;
-  const uint8_t* sfa; const uint8_t* sfb;
-  int sf_tiles_k;     // K / 128: 512-byte scale tiles per 128-row block
+  int sf_tiles_k;     // K / 128: 512-byte scale tiles per 128-row block (MX)
   void* D; int64_t ldd; int out_f32; int row_scales;
   int a_mn, b_mn;     // operand majors (MN-major: TMA boxes 128 MN x 128 K, K step 4 KB)
   int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
@@ -60,17 +60,22 @@ template <bool MX, int CG, int ST, int KS> struct Layout {
   // a stage holds KS 128-byte K atoms (16 KB sub-tiles of 128 rows each)
   static constexpr uint32_t A_STAGE = BM * BK * KS;         // 16 KB x KS
   static constexpr uint32_t B_STAGE = (BN / CG) * BK * KS;  // 32 KB (CG=1) / 16 KB (CG=2), x KS
+  // MX scale factors per stage: SFA = this CTA's 128 rows x KS atoms; SFB = all 256 N rows x KS
+  static constexpr uint32_t SFA_STAGE = MX ? KS * SF_CHUNK : 0;
+  static constexpr uint32_t SFB_STAGE = MX ? 2 * KS * SF_CHUNK : 0;
   static constexpr uint32_t off_a = 0;
   static constexpr uint32_t off_b = off_a + STAGES * A_STAGE;
   static constexpr uint32_t off_sfa = off_b + STAGES * B_STAGE;
-  static constexpr uint32_t off_sfb = off_sfa + (MX ? STAGES * SFA_STAGE : 0);
-  static constexpr uint32_t off_bar = off_sfb + (MX ? STAGES * SFB_STAGE : 0);
+  static constexpr uint32_t off_sfb = off_sfa + STAGES * SFA_STAGE;
+  static constexpr uint32_t off_bar = off_sfb + STAGES * SFB_STAGE;
   static constexpr uint32_t n_bar = 2 * STAGES + 2 * ACC;
   static constexpr uint32_t off_tmem = off_bar + 8 * n_bar;
   static constexpr uint32_t bytes = off_tmem + 16 + 1024;  // + alignment slack
   static constexpr uint32_t tmem_cols = 512;
-  static constexpr uint32_t sfa_col = 256, sfb_col = 260;  // MX only (after one accumulator)
-  static constexpr uint32_t tx_bytes = CG * (A_STAGE + B_STAGE);  // per stage, counted on the leader
+  // MX TMEM columns after the single accumulator: SFA atom t at sfa_col + 4t; SFB (row block h,
+  // atom t) at sfb_col + 8t + 4h
+  static constexpr uint32_t sfa_col = 256, sfb_col = 256 + 4 * KS;
+  static constexpr uint32_t tx_bytes = CG * (A_STAGE + B_STAGE + SFA_STAGE + SFB_STAGE);  // counted on the leader
 };
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
@@ -85,8 +90,9 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 template <bool MX, int CG, int ST, int KS>
 __global__ void __launch_bounds__(256, 1)
     fp8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                     const GemmArgs args) {
-  static_assert(KS == 1 || (CG == 2 && !MX), "multi-atom stages: CTA-pair plain FP8 only");
+  static_assert(KS == 1 || CG == 2, "multi-atom stages need the CTA-pair kernel");
   using L = Layout<MX, CG, ST, KS>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -109,6 +115,10 @@ __global__ void __launch_bounds__(256, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (MX) {
+      tma_prefetch_desc(&tmSFA);
+      tma_prefetch_desc(&tmSFB);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar + 8 * s, CG);
       mbar_init(empty_bar + 8 * s, 1);
@@ -142,42 +152,53 @@ __global__ void __launch_bounds__(256, 1)
       tile_coords(tile, args.tiles_m, args.tiles_n, mb, nb);
       const int m0 = mb * BM * CG + (int)crank * BM;
       const int n0 = nb * BN + (int)crank * (BN / CG);
-      const bool sfb_hi = MX && (2 * nb + 1) * 128 < args.N;
-      const uint32_t tx = L::tx_bytes + (MX ? SFA_STAGE + (sfb_hi ? SFB_STAGE : SFB_STAGE / 2) : 0);
+      const uint32_t tx = L::tx_bytes;
+      const int KT = args.sf_tiles_k;
       for (int kb = 0; kb < args.num_kb; ++kb) {
         mbar_wait(empty_bar + 8 * stage, phase ^ 1);
         if (lane == 0) {
           const uint32_t fb = full_bar + 8 * stage;
           const uint32_t sa_dst = base + L::off_a + stage * L::A_STAGE;
           const uint32_t sb_dst = base + L::off_b + stage * L::B_STAGE;
-          // K-major boxes: (k, row); MN-major boxes: (mn, k), one per 128-wide MN atom
-          const int ac0 = args.a_mn ? m0 : kb * BK, ac1 = args.a_mn ? kb * BK : m0;
-          const int bc0 = args.b_mn ? n0 : kb * BK, bc1 = args.b_mn ? kb * BK : n0;
           if (CG == 2) {
             if (leader) mbar_arrive_expect_tx(fb, tx);
             else mbar_arrive_cluster(mapa_shared(fb, 0));
-#pragma unroll
-            for (int j = 0; j < KS; ++j) {   // K atom j of this stage: k0 = (kb*KS + j)*BK
-              const int k0 = (kb * KS + j) * BK;
-              tma_load_2d_2sm(sa_dst + j * 16384, &tmA, args.a_mn ? m0 : k0, args.a_mn ? k0 : m0, fb);
-              tma_load_2d_2sm(sb_dst + j * 16384, &tmB, args.b_mn ? n0 : k0, args.b_mn ? k0 : n0, fb);
-            }
           } else {
             mbar_arrive_expect_tx(fb, tx);
-            tma_load_2d(sa_dst, &tmA, ac0, ac1, fb, 0);
-            if (args.b_mn) {
-              tma_load_2d(sb_dst, &tmB, n0, kb * BK, fb, 0);
-              tma_load_2d(sb_dst + 16384, &tmB, n0 + 128, kb * BK, fb, 0);
+          }
+          // K-major boxes: (k, row); MN-major boxes: (mn, k), one per 128-wide MN atom.
+          // K atom j of this stage starts at k0 = (kb*KS + j)*BK; atoms are 16 KB apart in smem.
+#pragma unroll
+          for (int j = 0; j < KS; ++j) {
+            const int k0 = (kb * KS + j) * BK;
+            const uint32_t da = sa_dst + j * 16384, db = sb_dst + j * 16384;
+            if (CG == 2) {
+              tma_load_2d_2sm(da, &tmA, args.a_mn ? m0 : k0, args.a_mn ? k0 : m0, fb);
+              tma_load_2d_2sm(db, &tmB, args.b_mn ? n0 : k0, args.b_mn ? k0 : n0, fb);
             } else {
-              tma_load_2d(sb_dst, &tmB, bc0, bc1, fb, 0);
+              tma_load_2d(da, &tmA, args.a_mn ? m0 : k0, args.a_mn ? k0 : m0, fb, 0);
+              if (args.b_mn) {
+                tma_load_2d(db, &tmB, n0, k0, fb, 0);
+                tma_load_2d(db + 16384, &tmB, n0 + 128, k0, fb, 0);
+              } else {
+                tma_load_2d(db, &tmB, k0, n0, fb, 0);
+              }
             }
-            if (MX) {
-              const uint8_t* sa = args.sfa + ((int64_t)mb * args.sf_tiles_k + kb) * 512;
-              const uint8_t* sb = args.sfb + ((int64_t)(2 * nb) * args.sf_tiles_k + kb) * 512;
-              bulk_load(base + L::off_sfa + stage * SFA_STAGE, sa, 512, fb);
-              bulk_load(base + L::off_sfb + stage * SFB_STAGE, sb, 512, fb);
-              if (sfb_hi)
-                bulk_load(base + L::off_sfb + stage * SFB_STAGE + 512, sb + (int64_t)args.sf_tiles_k * 512, 512, fb);
+          }
+          if (MX) {
+            // E8M0 tiles: SF tensor = [row_block * KT + k_atom][512 B]; boxes of KS consecutive atoms
+            const int kt0 = kb * KS;
+            const uint32_t dsa = base + L::off_sfa + stage * L::SFA_STAGE;
+            const uint32_t dsb = base + L::off_sfb + stage * L::SFB_STAGE;
+            const int rba = mb * CG + (int)crank;   // this CTA's 128-row block of A
+            if (CG == 2) {
+              tma_load_2d_2sm(dsa, &tmSFA, 0, rba * KT + kt0, fb);
+              tma_load_2d_2sm(dsb, &tmSFB, 0, (2 * nb) * KT + kt0, fb);
+              tma_load_2d_2sm(dsb + KS * SF_CHUNK, &tmSFB, 0, (2 * nb + 1) * KT + kt0, fb);
+            } else {
+              tma_load_2d(dsa, &tmSFA, 0, rba * KT + kt0, fb, 0);
+              tma_load_2d(dsb, &tmSFB, 0, (2 * nb) * KT + kt0, fb, 0);
+              tma_load_2d(dsb + KS * SF_CHUNK, &tmSFB, 0, (2 * nb + 1) * KT + kt0, fb, 0);
             }
           }
         }
@@ -199,33 +220,49 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(full_bar + 8 * stage, phase);
         tc_fence_after();
         if (lane == 0) {
-          if (MX) {
-            tmem_cp_32x128b_warpx4(tmem_base + L::sfa_col, make_sf_desc(base + L::off_sfa + stage * SFA_STAGE));
-            tmem_cp_32x128b_warpx4(tmem_base + L::sfb_col, make_sf_desc(base + L::off_sfb + stage * SFB_STAGE));
-            tmem_cp_32x128b_warpx4(tmem_base + L::sfb_col + 4,
-                                   make_sf_desc(base + L::off_sfb + stage * SFB_STAGE + 512));
+          if (MX) {   // this stage's scale factors -> TMEM (in order with the MMAs that follow)
+            const uint32_t ssa = base + L::off_sfa + stage * L::SFA_STAGE;
+            const uint32_t ssb = base + L::off_sfb + stage * L::SFB_STAGE;
+#pragma unroll
+            for (int t = 0; t < KS; ++t) {
+              const uint32_t ca = tmem_base + L::sfa_col + 4 * t;
+              const uint32_t cb0 = tmem_base + L::sfb_col + 8 * t, cb1 = cb0 + 4;
+              if (CG == 2) {
+                tmem_cp_32x128b_warpx4_cg2(ca, make_sf_desc(ssa + t * SF_CHUNK));
+                tmem_cp_32x128b_warpx4_cg2(cb0, make_sf_desc(ssb + t * SF_CHUNK));
+                tmem_cp_32x128b_warpx4_cg2(cb1, make_sf_desc(ssb + (KS + t) * SF_CHUNK));
+              } else {
+                tmem_cp_32x128b_warpx4(ca, make_sf_desc(ssa + t * SF_CHUNK));
+                tmem_cp_32x128b_warpx4(cb0, make_sf_desc(ssb + t * SF_CHUNK));
+                tmem_cp_32x128b_warpx4(cb1, make_sf_desc(ssb + (KS + t) * SF_CHUNK));
+              }
+            }
           }
           const uint32_t sa_src = base + L::off_a + stage * L::A_STAGE;
           const uint32_t sb_src = base + L::off_b + stage * L::B_STAGE;
           const uint64_t adesc = args.a_mn ? make_sw128_mnmajor_desc(sa_src) : make_sw128_kmajor_desc(sa_src);
           const uint64_t bdesc = args.b_mn ? make_sw128_mnmajor_desc(sb_src) : make_sw128_kmajor_desc(sb_src);
-          // per K=32 step: K-major advances 32 B inside the 128-B swizzle row; MN-major advances
-          // 32 K-rows = 4 KB (descriptor start address is in 16-B units)
-          // K atoms of one stage are 16 KB apart: K-major jumps 1024 (16-B units) every 4 steps;
-          // MN-major atoms are contiguous (4 steps x 4 KB = 16 KB)
+          // per K=32 step: K-major advances 32 B inside the 128-B swizzle row and jumps 16 KB
+          // (1024 in 16-B units) to the next K atom every 4 steps; MN-major advances 32 K-rows
+          // = 4 KB per step (atoms are contiguous)
           auto koff = [](int mn, int k) -> uint64_t {
             return mn ? (uint64_t)(256 * k) : (uint64_t)(1024 * (k >> 2) + 2 * (k & 3));
           };
 #pragma unroll
           for (int k = 0; k < KS * BK / 32; ++k) {
             const uint64_t ad = adesc + koff(args.a_mn, k), bd = bdesc + koff(args.b_mn, k);
-            if (MX)
-              mma_mxf8f6f4(d_tmem, ad, bd, idesc_with_sf_id(args.idesc, k, k), (kb | k) != 0,
-                           tmem_base + L::sfa_col, tmem_base + L::sfb_col);
-            else if (CG == 2)
-              mma_f8f6f4_cg2(d_tmem, ad, bd, args.idesc, (kb | k) != 0);
-            else
-              mma_f8f6f4(d_tmem, ad, bd, args.idesc, (kb | k) != 0);
+            const uint32_t acc_flag = (kb | k) != 0;
+            if (MX) {
+              const uint32_t t = (uint32_t)k >> 2;
+              const uint32_t id = idesc_with_sf_id(args.idesc, k & 3, k & 3);
+              const uint32_t sfa = tmem_base + L::sfa_col + 4 * t, sfb = tmem_base + L::sfb_col + 8 * t;
+              if (CG == 2) mma_mxf8f6f4_cg2(d_tmem, ad, bd, id, acc_flag, sfa, sfb);
+              else mma_mxf8f6f4(d_tmem, ad, bd, id, acc_flag, sfa, sfb);
+            } else if (CG == 2) {
+              mma_f8f6f4_cg2(d_tmem, ad, bd, args.idesc, acc_flag);
+            } else {
+              mma_f8f6f4(d_tmem, ad, bd, args.idesc, acc_flag);
+            }
           }
           if (CG == 2) {
             mma_commit_cg2_mc(empty_bar + 8 * stage, 0x3);
@@ -263,19 +300,20 @@ __global__ void __launch_bounds__(256, 1)
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_wait_ld();
         const int col0 = nb * BN + c * 32;
-        if (!rvalid || col0 >= args.N || (args.debug & 1)) continue;
+        if (col0 >= args.N || (args.debug & 1)) continue;   // warp-uniform
         float v[32];
         if (args.row_scales) {
+          // lane j computes 1/sb for column col0 + j once; the warp shares them by shuffles
+          const float rcol = __frcp_rn(args.sb[min(col0 + (int)lane, args.N - 1)]);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = min(col0 + j, args.N - 1);
-            v[j] = __fmul_rn(__fmul_rn(__uint_as_float(r[j]), rs), __frcp_rn(args.sb[col]));
-          }
+          for (int j = 0; j < 32; ++j)
+            v[j] = __fmul_rn(__fmul_rn(__uint_as_float(r[j]), rs), __shfl_sync(0xffffffffu, rcol, j));
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__uint_as_float(r[j]), rs);
         }
         const int nvalid = min(32, args.N - col0);  // 16 or 32 (N % 16 == 0)
+        if (!rvalid) continue;
         if (args.out_f32) {
           float* dst = reinterpret_cast<float*>(args.D) + (int64_t)row * args.ldd + col0;
 #pragma unroll
@@ -357,10 +395,23 @@ static int num_sms() {
 
 // CTA-pair mode for the plain FP8 kinds; FP8T_GEMM_CTA_GROUP=1 forces single-CTA tiles
 // (used by the tests to cover both code paths).
-static int cta_group_for(bool mx) {
-  if (mx) return 1;
+static int cta_group_for() {
   const char* e = getenv("FP8T_GEMM_CTA_GROUP");
   return (e && e[0] == '1') ? 1 : 2;
+}
+
+// E8M0 blocked scale buffer of an MX operand with `rows` rows viewed as a 2-D u32 tensor
+// [rows/128 * K/128 tiles][128 words]; a box of KS consecutive tiles = KS K atoms.
+static bool make_sf_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K, int ks) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {128, (cuuint64_t)((rows / 128) * (K / 128))};
+  cuuint64_t strides[1] = {512};
+  cuuint32_t box[2] = {128, (cuuint32_t)ks};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <bool MX, int CG, int ST, int KS>
@@ -373,23 +424,27 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
         cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG, ST, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tsa, tsb;
   if (!make_operand_map(&ta, p.A, p.a_mn, p.M, p.K, p.lda, BM) ||
       !make_operand_map(&tb, p.B, p.b_mn, p.N, p.K, p.ldb, BN / CG))
     return cudaErrorInvalidValue;
+  if (MX) {
+    if (!make_sf_map(&tsa, p.sa, p.M, p.K, KS) || !make_sf_map(&tsb, p.sb, p.N, p.K, KS)) return cudaErrorInvalidValue;
+  } else {
+    tsa = ta;   // unused by the plain FP8 kinds
+    tsb = tb;
+  }
   GemmArgs a{};
   a.M = (int)p.M; a.N = (int)p.N; a.K = (int)p.K;
   a.tiles_m = (int)((p.M + BM * CG - 1) / (BM * CG));
   a.tiles_n = (int)((p.N + BN - 1) / BN);
   a.num_tiles = a.tiles_m * a.tiles_n;
   a.num_kb = (int)((p.K + BK * KS - 1) / (BK * KS));
-  a.idesc = MX ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM, BN)
+  a.idesc = MX ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN)
                : make_idesc_f8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u);
   a.a_mn = p.a_mn;
   a.b_mn = p.b_mn;
   if (MX) {
-    a.sfa = static_cast<const uint8_t*>(p.sa);
-    a.sfb = static_cast<const uint8_t*>(p.sb);
     a.sf_tiles_k = (int)(p.K / 128);
   } else {
     a.sa = static_cast<const float*>(p.sa);
@@ -405,7 +460,7 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
   const int grid = CG * (a.num_tiles < slots ? a.num_tiles : slots);
   LaunchScope ls(MX ? K_GEMM_MX : K_GEMM, st);
   if (CG == 1) {
-    fp8_gemm_kernel<MX, CG, ST, KS><<<grid, 256, L::bytes, st>>>(ta, tb, a);
+    fp8_gemm_kernel<MX, CG, ST, KS><<<grid, 256, L::bytes, st>>>(ta, tb, tsa, tsb, a);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -419,15 +474,16 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS>, ta, tb, a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS>, ta, tb, tsa, tsb, a);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st) {
-  if (p.scale_mode == 2) return launch_t<true, 1, 4, 1>(p, st);
-  if (cta_group_for(false) == 1) return launch_t<false, 1, 4, 1>(p, st);
+  const int cg = cta_group_for();
+  if (p.scale_mode == 2) return cg == 1 ? launch_t<true, 1, 4, 1>(p, st) : launch_t<true, 2, 3, 2>(p, st);
+  if (cg == 1) return launch_t<false, 1, 4, 1>(p, st);
   // default: 3 stages x 2 K atoms (64 KB per CTA per stage, 8 MMAs per barrier round trip);
   // FP8T_GEMM_STAGES=6 selects 6 x 1 atom (4 MMAs per round trip) for comparison
   const char* e = getenv("FP8T_GEMM_STAGES");

@@ -206,6 +206,21 @@ __device__ __forceinline__ void mma_f8f6f4_cg2(uint32_t tmem_d, uint64_t adesc, 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Block-scaled MMA over a CTA pair (scale factors in each CTA's TMEM: SFA for its own M half,
+// SFB for all N).
+__device__ __forceinline__ void mma_mxf8f6f4_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate, uint32_t tmem_sfa, uint32_t tmem_sfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb)
+      : "memory");
+}
+// smem -> TMEM scale-factor copy on both CTAs of the pair (each from its own smem).
+__device__ __forceinline__ void tmem_cp_32x128b_warpx4_cg2(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 // Arrive on the mbarrier at the same offset in every CTA of `mask` once the pair's MMAs complete.
 __device__ __forceinline__ void mma_commit_cg2_mc(uint32_t bar, uint16_t mask) {
   asm volatile(

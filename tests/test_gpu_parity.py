@@ -282,8 +282,8 @@ def _block(codes_logical):
 
 
 @pytest.mark.parametrize("fa,fb", [(E4M3, E4M3), (E5M2, E4M3)])
-@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (256, 384, 512)])
-def test_gemm_mx_tolerance(fa, fb, M, N, K):
+@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (256, 384, 512), (384, 640, 384)])
+def test_gemm_mx_tolerance(fa, fb, M, N, K, cta_group):
     a = synth.tensor_c4("x", (M, K), seed=6)
     b = synth.tensor_c4("w", (N, K), seed=6)
     qa, sa = omx.quantize_dim0(a, fa)
@@ -296,7 +296,7 @@ def test_gemm_mx_tolerance(fa, fb, M, N, K):
     _tol_check(_np(D).astype(np.float64), ref, bd)
 
 
-def test_gemm_mx_integer_grid_exact():
+def test_gemm_mx_integer_grid_exact(cta_group):
     M, N, K = 256, 256, 256
     a, b = _grid_operands(M, N, K, seed=1)
     # unit-ish blocks: scale codes chosen so the grid is lossless (amax 14 -> FLOOR code 127+3-8)
