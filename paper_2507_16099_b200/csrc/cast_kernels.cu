@@ -363,65 +363,77 @@ __device__ __forceinline__ int64_t sf_offset(int64_t r, int64_t cblk, int64_t nc
 }
 
 template <typename T, int FMT, bool RCEIL, bool DIM0, bool DIM1>
-__global__ void __launch_bounds__(256) mx_cast_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
+__global__ void __launch_bounds__(256, 3) mx_cast_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
                                                       uint8_t* __restrict__ q0, uint8_t* __restrict__ sf0,
                                                       uint8_t* __restrict__ q1, uint8_t* __restrict__ sf1) {
+  // Thread t owns 8 consecutive rows (8*(t/16) .. +7) x 8 consecutive columns (8*(t%16) .. +7)
+  // of the 128 x 128 tile.  dim0 blocks (32 columns of one row) span 4 lanes; dim1 blocks
+  // (32 rows of one column) span the two half-warps of warps 2j and 2j+1.
   __shared__ __align__(16) uint32_t tile[128 * 32];
-  __shared__ uint32_t red[8][4][128];
-  __shared__ float mult1[4][128];
+  __shared__ __align__(16) uint32_t red[8][128];
+  __shared__ __align__(16) float mult1[4][128];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t r0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 128;
   const int cc = (t & 15) * 8;
-  float v[8][8];
+  const int rbase = 8 * (t >> 4);
+  Raw8<T> raw[8];
+  const T* xp = x + (r0 + rbase) * ld + c0 + cc;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) Ld8<T>::load(x + (r0 + (t >> 4) + 16 * i) * ld + c0 + cc, v[i]);
+  for (int i = 0; i < 8; ++i) raw[i].load(xp + i * ld);
 
-  if (DIM0) {
+  // one pass over the 8 rows: dim0 block codes + casts, and the dim1 column maxima
+  uint32_t cm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint8_t* q0p = DIM0 ? q0 + (r0 + rbase) * C + c0 + cc : nullptr;
+  // E8M0 blocked offset of (row r0+rbase+i, 32-block (c0+cc)/32): rows of a 128-row tile are
+  // 16 B apart within each group of 32 and 4 B apart across groups
+  const int64_t sf0_base = (((r0 >> 7) * (C >> 7) + (c0 >> 7)) * 512) + ((rbase >> 5) & 3) * 4 + (cc >> 5);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      uint32_t m = 0;
+  for (int i = 0; i < 8; ++i) {
+    float v[8];
+    raw[i].get(v);
+    uint32_t m = 0;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) m = max(m, abs_bits(v[i][e]));
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t a = abs_bits(v[e]);
+      m = max(m, a);
+      if (DIM1) cm[e] = max(cm[e], a);
+    }
+    if (DIM0) {
       m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
       m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
       const uint32_t code = e8m0_code<FMT, RCEIL>(m);
-      const int64_t r = r0 + (t >> 4) + 16 * i;
-      *reinterpret_cast<uint2*>(q0 + r * C + c0 + cc) = cast8<FMT>(v[i], e8m0_mult(code));
-      if ((t & 3) == 0) sf0[sf_offset(r, (c0 + cc) >> 5, C >> 7)] = (uint8_t)code;
+      *reinterpret_cast<uint2*>(q0p + i * C) = cast8<FMT>(v, e8m0_mult(code));
+      if ((t & 3) == 0) sf0[sf0_base + ((rbase + i) & 31) * 16] = (uint8_t)code;
     }
   }
   if (DIM1) {
-    // per-column maxima over the 2 rows-per-block this thread holds, for each 32-row block j
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int e = 0; e < 8; ++e) cm[e] = max(cm[e], __shfl_xor_sync(0xffffffffu, cm[e], 16));
+    if (lane < 16) {
+      *reinterpret_cast<uint4*>(&red[warp][cc]) = make_uint4(cm[0], cm[1], cm[2], cm[3]);
+      *reinterpret_cast<uint4*>(&red[warp][cc + 4]) = make_uint4(cm[4], cm[5], cm[6], cm[7]);
+    }
+    __syncthreads();
+    {
+      const int j = t >> 6, col = (t & 63) * 2;   // 32-row block j, columns col, col+1
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        uint32_t m = max(abs_bits(v[2 * j][e]), abs_bits(v[2 * j + 1][e]));
-        m = max(m, __shfl_xor_sync(0xffffffffu, m, 16));
-        if (lane < 16) red[warp][j][cc + e] = m;
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t m = max(red[2 * j][col + h], red[2 * j + 1][col + h]);
+        const uint32_t code = e8m0_code<FMT, RCEIL>(m);
+        mult1[j][col + h] = e8m0_mult(code);
+        sf1[sf_offset(c0 + col + h, (r0 >> 5) + j, R >> 7)] = (uint8_t)code;
       }
     }
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int idx = t + 256 * k;  // (j, col) pairs, 4 x 128
-      const int j = idx >> 7, col = idx & 127;
-      uint32_t m = red[0][j][col];
-#pragma unroll
-      for (int w = 1; w < 8; ++w) m = max(m, red[w][j][col]);
-      const uint32_t code = e8m0_code<FMT, RCEIL>(m);
-      mult1[j][col] = e8m0_mult(code);
-      sf1[sf_offset(c0 + col, (r0 >> 5) + j, R >> 7)] = (uint8_t)code;
-    }
-    __syncthreads();
+    const int j = t >> 6;                          // all 8 rows of this thread lie in block j
+    const float4 ma = *reinterpret_cast<const float4*>(&mult1[j][cc]);
+    const float4 mb = *reinterpret_cast<const float4*>(&mult1[j][cc + 4]);
+    const float mu[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int rr = (t >> 4) + 16 * i;
-      const int j = i >> 1;  // rows 16i..16i+15 (+t>>4) lie in 32-row block i/2
-      float s[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) s[e] = mult1[j][cc + e];
-      *reinterpret_cast<uint2*>(&tile[swz(rr, cc >> 2)]) = cast8v<FMT>(v[i], s);
+      float v[8];
+      raw[i].get(v);
+      *reinterpret_cast<uint2*>(&tile[swz(rbase + i, cc >> 2)]) = cast8v<FMT>(v, mu);
     }
     __syncthreads();
     store_transposed(tile, q1, R, r0, c0, 128, 128);
