@@ -186,6 +186,7 @@ def _peaks():
 
 
 def _traffic(workload_key):
+    """Per-launch DRAM bytes of the GEMM from the committed ncu --set full capture (or None)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         d = json.load(open(p))
@@ -327,7 +328,10 @@ def run_ours(a):
     gemm_avg = sum(gemm_ms) / len(gemm_ms)
     gemm_tflops = 2.0 * M * N * K / (gemm_avg / 1e3) / 1e12
     peaks = _peaks()
-    fp8_peak = 2.0 * peaks["bf16_sus"]      # dense FP8 = 2 x bf16 (guide's nominal ratio), sustained
+    # dense FP8 peak = 2 x measured bf16 cuBLAS (the guide's nominal FP8/BF16 ratio).  The timed region
+    # is well under a second, so the burst figure is the denominator; sustained is reported beside it.
+    fp8_peak = 2.0 * peaks["bf16"]
+    fp8_peak_sus = 2.0 * peaks["bf16_sus"]
     # algorithmic cast bytes per step: per hp element read by amax 2 B, by the cast 2 B,
     # plus 1 B per FP8 layout written (X, W, dY each written in 2 layouts)
     if cfg["recipe"] == "mxfp8":          # one fused dim0+dim1 read, 2 FP8 layouts + E8M0 scales
@@ -421,12 +425,14 @@ def run_ours(a):
             "data": "synthetic (seeded, device-generated, config value recipe)",
             "config": {"workload": cfg["workload"], "M_per_gpu": M, "N": N, "K": K, "recipe": cfg["recipe"],
                        "parallelism": f"fsdp{world} (fp8 all-gather + amax all-reduce)" if fsdp else "single GPU",
-                       "l2": "inputs larger than L2: X 128 MiB, dY 448 MiB, ~1.2 GB streamed per step; no flush"},
+                       "l2": f"inputs larger than L2 (126 MB): X {M * K * 2 / 2**20:.0f} MiB, "
+                             f"dY {M * N * 2 / 2**20:.0f} MiB, W {N * K * 2 / 2**20:.0f} MiB bf16; no flush"},
             "roofline": {"bound": "tensor", "kernel": "fp8_gemm_kernel (tcgen05 kind::%s)" %
                          ("mxf8f6f4.block_scale" if cfg["recipe"] == "mxfp8" else "f8f6f4"),
                          "achieved": gemm_tflops, "peak": fp8_peak, "unit": "TFLOP/s",
                          "frac": gemm_tflops / fp8_peak, "traffic": _traffic(a.config),
-                         "peak_source": f"{peaks['src']}: bf16_tflops_sustained x 2 (dense FP8/BF16 ratio)",
+                         "peak_source": f"{peaks['src']}: bf16_tflops (burst) x 2 (dense FP8/BF16 ratio)",
+                         "frac_of_sustained": gemm_tflops / fp8_peak_sus,
                          "algorithmic": f"2*M*N*K = {2.0 * M * N * K:.4g} flop per GEMM launch",
                          "avg_launch_ms": gemm_avg, "share_of_step": step_gemm_share},
             "cast": {"gbps": cast_gbps, "peak_gbps": peaks["hbm"], "frac": (cast_gbps / peaks["hbm"])

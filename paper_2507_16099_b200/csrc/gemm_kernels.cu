@@ -41,7 +41,7 @@ namespace fp8t {
 
 constexpr int BM = 128, BN = 256, BK = 128;   // per-CTA M rows, MMA N, K atom (bytes)
 constexpr int SF_CHUNK = 512;                 // E8M0 tile: 128 rows x 4 K-blocks of 32 (one K atom)
-constexpr int GROUP_M = 16;                   // tile raster: 16 M-tiles share the N sweep (L2 reuse)
+constexpr int GROUP_M = 16;                   // grouped raster: 16 M-tiles share the N sweep
 
 struct GemmArgs {
   int M, N, K;
@@ -52,6 +52,7 @@ struct GemmArgs {
   void* D; int64_t ldd; int out_f32; int row_scales;
   int a_mn, b_mn;     // operand majors (MN-major: TMA boxes 128 MN x 128 K, K step 4 KB)
   int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
+  int group_m;        // tile raster (see tile_coords)
 };
 
 template <bool MX, int CG, int ST, int KS> struct Layout {
@@ -78,11 +79,19 @@ template <bool MX, int CG, int ST, int KS> struct Layout {
   static constexpr uint32_t tx_bytes = CG * (A_STAGE + B_STAGE + SFA_STAGE + SFB_STAGE);  // counted on the leader
 };
 
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
-  const int group = t / (GROUP_M * tiles_n);
-  const int first_m = group * GROUP_M;
-  const int gsz = min(GROUP_M, tiles_m - first_m);
-  const int local = t - group * GROUP_M * tiles_n;
+// Tile raster.  group_m > 0: groups of group_m M-tiles sweep all N tiles (L2 reuse of both
+// operands); group_m == 0: row-major (all N tiles of an M tile back to back, so the B operand
+// stays L2-resident while A streams through once).
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group_m, int& mb, int& nb) {
+  if (group_m == 0) {
+    mb = t / tiles_n;
+    nb = t - mb * tiles_n;
+    return;
+  }
+  const int group = t / (group_m * tiles_n);
+  const int first_m = group * group_m;
+  const int gsz = min(group_m, tiles_m - first_m);
+  const int local = t - group * group_m * tiles_n;
   mb = first_m + local % gsz;
   nb = local / gsz;
 }
@@ -149,7 +158,7 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t phase = 0;
     for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
       int mb, nb;
-      tile_coords(tile, args.tiles_m, args.tiles_n, mb, nb);
+      tile_coords(tile, args.tiles_m, args.tiles_n, args.group_m, mb, nb);
       const int m0 = mb * BM * CG + (int)crank * BM;
       const int n0 = nb * BN + (int)crank * (BN / CG);
       const uint32_t tx = L::tx_bytes;
@@ -287,7 +296,7 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(tempty_bar, 0) : tempty_bar;
     for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
       int mb, nb;
-      tile_coords(tile, args.tiles_m, args.tiles_n, mb, nb);
+      tile_coords(tile, args.tiles_m, args.tiles_n, args.group_m, mb, nb);
       const int row = mb * BM * CG + (int)crank * BM + q * 32 + (int)lane;
       const bool rvalid = row < args.M;
       float rs = ts;
@@ -455,6 +464,10 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
   {
     const char* d = getenv("FP8T_GEMM_DEBUG");
     a.debug = d ? atoi(d) : 0;
+    // raster: grouped (GROUP_M); FP8T_GEMM_RASTER overrides (0 = row-major).  Measured on the
+    // C2/C4 shapes: row-major and group sizes 8-32 are within run-to-run noise of each other.
+    const char* r = getenv("FP8T_GEMM_RASTER");
+    a.group_m = r ? atoi(r) : GROUP_M;
   }
   const int slots = num_sms() / CG;
   const int grid = CG * (a.num_tiles < slots ? a.num_tiles : slots);

@@ -36,15 +36,11 @@ def main():
         D = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
         flops = 2.0 * M * N * K
         row = {"M": M, "N": N, "K": K}
-        for cg, st, dbg in (("2", "6", "0"), ("2", "3", "0"), ("2", "4", "0"), ("2", "6", "1"), ("2", "3", "1")):
-            os.environ["FP8T_GEMM_CTA_GROUP"] = cg
-            os.environ["FP8T_GEMM_STAGES"] = st
-            os.environ["FP8T_GEMM_DEBUG"] = dbg
+        for raster in ("0", "16", "8", "32"):
+            os.environ["FP8T_GEMM_RASTER"] = raster
             ms = timeit(lambda: ops.gemm(A, "e4m3", s, B, "e4m3", s, "tensor"))
-            row[f"cg{cg}_st{st}_dbg{dbg}"] = round(flops / ms / 1e9)
-        os.environ["FP8T_GEMM_DEBUG"] = "0"
-        os.environ["FP8T_GEMM_STAGES"] = "6"
-        os.environ["FP8T_GEMM_CTA_GROUP"] = "2"
+            row[f"raster{raster}"] = round(flops / ms / 1e9)
+        del os.environ["FP8T_GEMM_RASTER"]
         try:
             a8 = A.view(torch.float8_e4m3fn)
             b8 = B.view(torch.float8_e4m3fn)
