@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bf16", action="store_true")
+    ap.add_argument("--fsdp", action="store_true",
+                    help="use the FSDP path (fp8_fsdp_allgather + pre-cast weight) even at N=1")
     return ap.parse_args()
 
 
@@ -242,6 +244,10 @@ def run_ours(a):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    elif a.fsdp:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("gloo", rank=0, world_size=1)
 
     import paper_2507_16099_b200 as fp8t  # noqa: F401  (loads libfp8train.so; raises if missing)
     from paper_2507_16099_b200 import _lib as L, ops
@@ -249,7 +255,7 @@ def run_ours(a):
 
     cfg = CONFIGS[a.config]
     M, N, K = cfg["M"], cfg["N"], cfg["K"]
-    fsdp = world > 1
+    fsdp = world > 1 or a.fsdp
     if fsdp and cfg["recipe"] != "tensorwise":
         raise SystemExit("FP8 all-gather is tensorwise-only (PAPER.md:596)")
     x, w_shard, dy, w_full_hp = make_inputs(cfg, M, N, K, rank, world, dev)
@@ -273,13 +279,14 @@ def run_ours(a):
             comm.allgather_fp8(ww, "e4m3", out=w_full, scale=w_scale, amax=w_amax)
             plan.forward(xx, None, saved, y=y, w_fp8=(w_full, w_scale))
             plan.backward(gg, saved, dx=dx, dw=dw, w_fp8=(w_full, w_scale))
-            dist.reduce_scatter_tensor(dw_shard, dw)
+            if world > 1:
+                dist.reduce_scatter_tensor(dw_shard, dw)
         else:
             plan.forward(xx, ww, saved, y=y)
             plan.backward(gg, saved, dx=dx, dw=dw)
 
     def barrier():
-        if fsdp:
+        if world > 1:
             dist.barrier()
 
     for _ in range(max(a.warmup, 3)):
@@ -309,7 +316,7 @@ def run_ours(a):
     durs = (ctypes.c_float * cap)()
     nrec = L.lib.fp8_profile_collect(kinds, durs, cap)
     ms = ev0.elapsed_time(ev1)
-    if fsdp:
+    if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -380,7 +387,7 @@ def run_ours(a):
         e1.record(stream)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
-        if fsdp:
+        if world > 1:
             t = torch.tensor([ems], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
@@ -449,7 +456,7 @@ def run_ours(a):
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
-    if fsdp:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

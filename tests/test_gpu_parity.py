@@ -370,3 +370,40 @@ def test_errors_before_launch():
     with pytest.raises(fp8t._lib.Fp8Error) as e:
         ops.cast(x, "e4m3", "mx32", want_q=True)
     assert e.value.status == fp8t._lib.FP8_EALIGN
+
+
+# ----------------------------------------------------------------------------- FSDP (one rank)
+
+def test_fsdp_allgather_single_rank_equals_cast():
+    """fp8_fsdp_allgather through NCCL with one rank: amax -> all-reduce MAX -> cast into slot 0 ->
+    all-gather must equal the unsharded tensorwise cast (oracle), and drive the linear forward/backward
+    through the pre-cast weight path.  (Multi-rank data movement needs >= 2 GPUs.)"""
+    import os
+    import torch.distributed as dist
+    from paper_2507_16099_b200.fsdp import Comm
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = Comm()
+        Mx, Nw, Kw = 256, 384, 512
+        x, w, dy = synth.linear_inputs("c5", Mx, Nw, Kw, seed=0)
+        q, s, a = fp8.cast_tensorwise(w, E4M3)
+        wq, ws_, wa = comm.allgather_fp8(_dev(w, torch.bfloat16), "e4m3")
+        torch.cuda.synchronize()
+        assert _bits(_np(wa))[0] == _bits(a).reshape(-1)[0]
+        assert _bits(_np(ws_))[0] == _bits(s).reshape(-1)[0]
+        assert np.array_equal(_np(wq), q)
+        # linear with the gathered weight == linear with the hp weight (bit-identical outputs)
+        plan = ops.LinearPlan(Mx, Nw, Kw, recipe="tensorwise", out_dtype=torch.float32)
+        s1, s2 = plan.new_saved(), plan.new_saved()
+        X, W, G = _dev(x, torch.bfloat16), _dev(w, torch.bfloat16), _dev(dy, torch.bfloat16)
+        y1 = plan.forward(X, W, s1).clone()
+        dx1, dw1 = (t.clone() for t in plan.backward(G, s1))
+        y2 = plan.forward(X, None, s2, w_fp8=(wq, ws_)).clone()
+        dx2, dw2 = plan.backward(G, s2, w_fp8=(wq, ws_))
+        torch.cuda.synchronize()
+        assert torch.equal(y1, y2) and torch.equal(dx1, dx2) and torch.equal(dw1, dw2)
+        comm.close()
+    finally:
+        dist.destroy_process_group()
