@@ -301,8 +301,10 @@ fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, fp8_major_t major_a,
 namespace {
 
 struct Saved {          // written by fwd, read by bwd
-  uint8_t* xT;          // tensorwise: Xq [M,K] row-major (read MN-major by dW); else [K,M] (K-major over M)
-  uint8_t* wT;          // tensorwise: Wq [N,K] row-major (read MN-major by dX); else [K,N] (K-major over N)
+  uint8_t* xT;          // tensorwise: Xq [M,K]; rowwise: column-scaled X [M,K] (both row-major, read MN-major
+                        // by dW); mxfp8: dim1 copy [K,M] (K-major over M)
+  uint8_t* wT;          // tensorwise: Wq [N,K]; rowwise: column-scaled W [N,K] (read MN-major by dX);
+                        // mxfp8: dim1 copy [K,N]
   void* sx;             // tensorwise float[1] | rowwise float[K] | mx E8M0 [K x M/32]
   void* sw;             // tensorwise float[1] | rowwise float[K] | mx E8M0 [K x N/32]
 };
@@ -464,9 +466,11 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
     FP8T_CUDA(cudaMemsetAsync(fw.amax, 0, 4 * (M + K + N + K), st), "memset");
     FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 6, nullptr, (uint32_t*)axr, (uint32_t*)axc, st), "amax x");
     FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 6, nullptr, (uint32_t*)awr, (uint32_t*)awc, st), "amax w");
-    FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 2, 3, axr, axc, fw.xq, sv.xT, fw.sxr, (float*)sv.sx, st),
+    // row-scaled codes for the forward GEMM; column-scaled codes written row-major for the
+    // backward GEMMs (read MN-major, no transposed copy)
+    FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 2, 5, axr, axc, fw.xq, sv.xT, fw.sxr, (float*)sv.sx, st),
               "cast x");
-    FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 3, awr, awc, fw.wq, sv.wT, fw.swr, (float*)sv.sw, st),
+    FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 5, awr, awc, fw.wq, sv.wT, fw.swr, (float*)sv.sw, st),
               "cast w");
     GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
@@ -515,7 +519,7 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K,
     float* ac = ar + M;
     FP8T_CUDA(cudaMemsetAsync(bw.amax, 0, 4 * (M + N), st), "memset");
     FP8T_CUDA(launch_amax(dy.ptr, gb, M, N, dy.ld, 6, nullptr, (uint32_t*)ar, (uint32_t*)ac, st), "amax dy");
-    FP8T_CUDA(launch_cast(dy.ptr, gb, fg, M, N, dy.ld, dx ? 2 : 0, dw ? 3 : 0, ar, ac, bw.g, bw.gT, (float*)bw.sg,
+    FP8T_CUDA(launch_cast(dy.ptr, gb, fg, M, N, dy.ld, dx ? 2 : 0, dw ? 5 : 0, ar, ac, bw.g, bw.gT, (float*)bw.sg,
                           (float*)bw.sgT, st),
               "cast dy");
   } else {
@@ -525,27 +529,30 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K,
               "mx cast dy");
   }
   if (!dx && !dw) return FP8_OK;
+  // dX and dW run as one persistent launch (tiles of dX, then dW): no wave tail between them
+  GemmProblem ps[2];
+  int n = 0;
   if (mode == 0) {
     // tensorwise: operands are the row-major codes; B of dX and both operands of dW are MN-major
     const uint8_t* wq = w_fp8 ? w_fp8->q : sv.wT;
-    if (dx) {  // dX[M,K] = dY[M,N] . W[N,K]: A = Gq K-major over N, B = Wq stored [N,K] = MN-major
-      GemmProblem p{bw.g, wq, fg, ff, 0, 1, bw.sg, sv.sw, 0, M, K, N, N, K, dx, of32, K};
-      FP8T_CUDA(launch_gemm(p, st), "gemm dx");
-    }
-    if (dw) {  // dW[N,K] = dY^T . X: A = Gq stored [M,N] = MN-major, B = Xq stored [M,K] = MN-major
-      GemmProblem p{bw.g, sv.xT, fg, ff, 1, 1, bw.sg, sv.sx, 0, N, K, M, N, K, dw, of32, K};
-      FP8T_CUDA(launch_gemm(p, st), "gemm dw");
-    }
-    return FP8_OK;
+    // dX[M,K] = dY[M,N] . W[N,K]: A = Gq K-major over N, B = Wq stored [N,K] = MN-major
+    if (dx) ps[n++] = GemmProblem{bw.g, wq, fg, ff, 0, 1, bw.sg, sv.sw, 0, M, K, N, N, K, dx, of32, K};
+    // dW[N,K] = dY^T . X: A = Gq stored [M,N] = MN-major, B = Xq stored [M,K] = MN-major
+    if (dw) ps[n++] = GemmProblem{bw.g, sv.xT, fg, ff, 1, 1, bw.sg, sv.sx, 0, N, K, M, N, K, dw, of32, K};
+  } else if (mode == 1) {
+    // rowwise: column-scaled copies are row-major too -> read MN-major
+    // dX[M,K] = dY_r[M,N] . W_c[N,K]: A K-major over N, B stored [N,K] = MN-major
+    if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 1, bw.sg, sv.sw, mode, M, K, N, N, K, dx, of32, K};
+    // dW[N,K] = dY_c^T . X_c: A stored [M,N] = MN-major, B stored [M,K] = MN-major
+    if (dw) ps[n++] = GemmProblem{bw.gT, sv.xT, fg, ff, 1, 1, bw.sgT, sv.sx, mode, N, K, M, N, K, dw, of32, K};
+  } else {
+    // MXFP8: dim1 copies are transposed (blocks along the contraction dim), K-major
+    // dX[M,K] = dY[M,N] . W  : A = dY (K-major over N), B = W^T [K,N]
+    if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 0, bw.sg, sv.sw, mode, M, K, N, N, N, dx, of32, K};
+    // dW[N,K] = dY^T[N,M] . X : A = dY^T [N,M], B = X^T [K,M]
+    if (dw) ps[n++] = GemmProblem{bw.gT, sv.xT, fg, ff, 0, 0, bw.sgT, sv.sx, mode, N, K, M, M, M, dw, of32, K};
   }
-  if (dx) {  // dX[M,K] = dY[M,N] . W  : A = dY (K-major over N), B = W^T [K,N]
-    GemmProblem p{bw.g, sv.wT, fg, ff, 0, 0, bw.sg, sv.sw, mode, M, K, N, N, N, dx, of32, K};
-    FP8T_CUDA(launch_gemm(p, st), "gemm dx");
-  }
-  if (dw) {  // dW[N,K] = dY^T[N,M] . X : A = dY^T [N,M], B = X^T [K,M]
-    GemmProblem p{bw.gT, sv.xT, fg, ff, 0, 0, bw.sgT, sv.sx, mode, N, K, M, M, M, dw, of32, K};
-    FP8T_CUDA(launch_gemm(p, st), "gemm dw");
-  }
+  FP8T_CUDA(launch_gemms(ps, n, st), "gemm dx/dw");
   return FP8_OK;
 }
 

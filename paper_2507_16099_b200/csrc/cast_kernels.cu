@@ -259,11 +259,15 @@ __global__ void __launch_bounds__(256) amax_flat_kernel(const uint4* __restrict_
 // Modes: 0 none, 1 tensor (amax[1]), 2 per row (amax[R]), 3 per column (amax[C]).
 // Scale outputs are written by the tiles on the first tile row / column.
 // ---------------------------------------------------------------------------
-template <typename T, int FMT, int QM, int TM>
+template <typename T, int FMT, int QM, int TM_>
 __global__ void __launch_bounds__(256) cast_tile_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
                                                         const float* __restrict__ amax_q,
                                                         const float* __restrict__ amax_t, uint8_t* __restrict__ q,
                                                         uint8_t* __restrict__ qt, float* scale_q, float* scale_t) {
+  // TM_ >= 4: the second output is written row-major ([R,C], like q) with scale mode TM_ - 2,
+  // i.e. the column-scaled copy the backward GEMMs read MN-major (no transpose).
+  constexpr bool TRM = TM_ >= 4;
+  constexpr int TM = TRM ? TM_ - 2 : TM_;
   __shared__ __align__(16) uint32_t tile[128 * 32];
   __shared__ float sq[128];
   __shared__ float st[128];
@@ -326,10 +330,11 @@ __global__ void __launch_bounds__(256) cast_tile_kernel(const T* __restrict__ x,
       else if (TM == 1) bt = cast8<FMT>(v, st[0]);
       else if (TM == 2) bt = cast8<FMT>(v, st[rr]);
       else bt = cast8v<FMT>(v, &st[cc]);
-      *reinterpret_cast<uint2*>(&tile[swz(rr, cc >> 2)]) = bt;
+      if (TRM) *reinterpret_cast<uint2*>(qt + (r0 + rr) * C + c0 + cc) = bt;
+      else *reinterpret_cast<uint2*>(&tile[swz(rr, cc >> 2)]) = bt;
     }
   }
-  if (TM != 0) {
+  if (TM != 0 && !TRM) {
     __syncthreads();
     store_transposed(tile, qt, R, r0, c0, vrows, vcols);
   }
@@ -521,7 +526,7 @@ static cudaError_t cast_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
   FP8T_CAST(1, 0) FP8T_CAST(0, 1) FP8T_CAST(1, 1)
   FP8T_CAST(2, 0) FP8T_CAST(0, 2) FP8T_CAST(2, 2)
   FP8T_CAST(3, 0) FP8T_CAST(0, 3) FP8T_CAST(3, 3)
-  FP8T_CAST(2, 3)
+  FP8T_CAST(2, 3) FP8T_CAST(2, 5)
 #undef FP8T_CAST
   return cudaErrorInvalidValue;
 }

@@ -43,16 +43,24 @@ constexpr int BM = 128, BN = 256, BK = 128;   // per-CTA M rows, MMA N, K atom (
 constexpr int SF_CHUNK = 512;                 // E8M0 tile: 128 rows x 4 K-blocks of 32 (one K atom)
 constexpr int GROUP_M = 16;                   // grouped raster: 16 M-tiles share the N sweep
 
-struct GemmArgs {
+// One GEMM problem of a (possibly two-problem) launch.
+struct Prob {
   int M, N, K;
-  int tiles_m, tiles_n, num_tiles, num_kb;
+  int tiles_m, tiles_n, num_kb;
+  int sf_tiles_k;     // K / 128: 512-byte scale tiles per 128-row block (MX)
   uint32_t idesc;
   const float* sa; const float* sb;
-  int sf_tiles_k;     // K / 128: 512-byte scale tiles per 128-row block (MX)
-  void* D; int64_t ldd; int out_f32; int row_scales;
+  void* D; int64_t ldd;
+  int out_f32, row_scales;
   int a_mn, b_mn;     // operand majors (MN-major: TMA boxes 128 MN x 128 K, K step 4 KB)
-  int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
+};
+// A launch processes the tiles of p0 ([0, t1)) then p1 ([t1, num_tiles)) on one persistent grid:
+// the backward's dX and dW GEMMs share one launch, so neither has its own wave-quantisation tail.
+struct GemmArgs {
+  Prob p0, p1;
+  int t1, num_tiles;
   int group_m;        // tile raster (see tile_coords)
+  int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
 };
 
 template <bool MX, int CG, int ST, int KS> struct Layout {
@@ -98,9 +106,11 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 
 template <bool MX, int CG, int ST, int KS>
 __global__ void __launch_bounds__(256, 1)
-    fp8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
-                    const GemmArgs args) {
+    fp8_gemm_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tB0,
+                    const __grid_constant__ CUtensorMap tSA0, const __grid_constant__ CUtensorMap tSB0,
+                    const __grid_constant__ CUtensorMap tA1, const __grid_constant__ CUtensorMap tB1,
+                    const __grid_constant__ CUtensorMap tSA1, const __grid_constant__ CUtensorMap tSB1,
+                    const __grid_constant__ GemmArgs args) {
   static_assert(KS == 1 || CG == 2, "multi-atom stages need the CTA-pair kernel");
   using L = Layout<MX, CG, ST, KS>;
   constexpr int STAGES = L::STAGES;
@@ -121,12 +131,27 @@ __global__ void __launch_bounds__(256, 1)
   const int cta_slot = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // pair / CTA index
   const int cta_stride = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
+  // problem of a global tile index, its local tile coordinates and its tensor maps
+  auto locate = [&](int tile, int& pi, int& mb, int& nb) {
+    pi = tile >= args.t1 ? 1 : 0;
+    const Prob& P = pi ? args.p1 : args.p0;
+    tile_coords(pi ? tile - args.t1 : tile, P.tiles_m, P.tiles_n, args.group_m, mb, nb);
+  };
+
   if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tA0);
+    tma_prefetch_desc(&tB0);
+    if (args.t1 < args.num_tiles) {
+      tma_prefetch_desc(&tA1);
+      tma_prefetch_desc(&tB1);
+    }
     if (MX) {
-      tma_prefetch_desc(&tmSFA);
-      tma_prefetch_desc(&tmSFB);
+      tma_prefetch_desc(&tSA0);
+      tma_prefetch_desc(&tSB0);
+      if (args.t1 < args.num_tiles) {
+        tma_prefetch_desc(&tSA1);
+        tma_prefetch_desc(&tSB1);
+      }
     }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar + 8 * s, CG);
@@ -157,13 +182,20 @@ __global__ void __launch_bounds__(256, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
-      int mb, nb;
-      tile_coords(tile, args.tiles_m, args.tiles_n, args.group_m, mb, nb);
+      int pi, mb, nb;
+      locate(tile, pi, mb, nb);
+      const Prob& P = pi ? args.p1 : args.p0;
+      const CUtensorMap* tmA = pi ? &tA1 : &tA0;
+      const CUtensorMap* tmB = pi ? &tB1 : &tB0;
+      const CUtensorMap* tmSFA = pi ? &tSA1 : &tSA0;
+      const CUtensorMap* tmSFB = pi ? &tSB1 : &tSB0;
+      const int a_mn = P.a_mn, b_mn = P.b_mn;
       const int m0 = mb * BM * CG + (int)crank * BM;
       const int n0 = nb * BN + (int)crank * (BN / CG);
       const uint32_t tx = L::tx_bytes;
-      const int KT = args.sf_tiles_k;
-      for (int kb = 0; kb < args.num_kb; ++kb) {
+      const int KT = P.sf_tiles_k;
+      const int num_kb = P.num_kb;
+      for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(empty_bar + 8 * stage, phase ^ 1);
         if (lane == 0) {
           const uint32_t fb = full_bar + 8 * stage;
@@ -182,15 +214,15 @@ __global__ void __launch_bounds__(256, 1)
             const int k0 = (kb * KS + j) * BK;
             const uint32_t da = sa_dst + j * 16384, db = sb_dst + j * 16384;
             if (CG == 2) {
-              tma_load_2d_2sm(da, &tmA, args.a_mn ? m0 : k0, args.a_mn ? k0 : m0, fb);
-              tma_load_2d_2sm(db, &tmB, args.b_mn ? n0 : k0, args.b_mn ? k0 : n0, fb);
+              tma_load_2d_2sm(da, tmA, a_mn ? m0 : k0, a_mn ? k0 : m0, fb);
+              tma_load_2d_2sm(db, tmB, b_mn ? n0 : k0, b_mn ? k0 : n0, fb);
             } else {
-              tma_load_2d(da, &tmA, args.a_mn ? m0 : k0, args.a_mn ? k0 : m0, fb, 0);
-              if (args.b_mn) {
-                tma_load_2d(db, &tmB, n0, k0, fb, 0);
-                tma_load_2d(db + 16384, &tmB, n0 + 128, k0, fb, 0);
+              tma_load_2d(da, tmA, a_mn ? m0 : k0, a_mn ? k0 : m0, fb, 0);
+              if (b_mn) {
+                tma_load_2d(db, tmB, n0, k0, fb, 0);
+                tma_load_2d(db + 16384, tmB, n0 + 128, k0, fb, 0);
               } else {
-                tma_load_2d(db, &tmB, k0, n0, fb, 0);
+                tma_load_2d(db, tmB, k0, n0, fb, 0);
               }
             }
           }
@@ -201,13 +233,13 @@ __global__ void __launch_bounds__(256, 1)
             const uint32_t dsb = base + L::off_sfb + stage * L::SFB_STAGE;
             const int rba = mb * CG + (int)crank;   // this CTA's 128-row block of A
             if (CG == 2) {
-              tma_load_2d_2sm(dsa, &tmSFA, 0, rba * KT + kt0, fb);
-              tma_load_2d_2sm(dsb, &tmSFB, 0, (2 * nb) * KT + kt0, fb);
-              tma_load_2d_2sm(dsb + KS * SF_CHUNK, &tmSFB, 0, (2 * nb + 1) * KT + kt0, fb);
+              tma_load_2d_2sm(dsa, tmSFA, 0, rba * KT + kt0, fb);
+              tma_load_2d_2sm(dsb, tmSFB, 0, (2 * nb) * KT + kt0, fb);
+              tma_load_2d_2sm(dsb + KS * SF_CHUNK, tmSFB, 0, (2 * nb + 1) * KT + kt0, fb);
             } else {
-              tma_load_2d(dsa, &tmSFA, 0, rba * KT + kt0, fb, 0);
-              tma_load_2d(dsb, &tmSFB, 0, (2 * nb) * KT + kt0, fb, 0);
-              tma_load_2d(dsb + KS * SF_CHUNK, &tmSFB, 0, (2 * nb + 1) * KT + kt0, fb, 0);
+              tma_load_2d(dsa, tmSFA, 0, rba * KT + kt0, fb, 0);
+              tma_load_2d(dsb, tmSFB, 0, (2 * nb) * KT + kt0, fb, 0);
+              tma_load_2d(dsb + KS * SF_CHUNK, tmSFB, 0, (2 * nb + 1) * KT + kt0, fb, 0);
             }
           }
         }
@@ -222,10 +254,13 @@ __global__ void __launch_bounds__(256, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
+      const Prob& P = tile >= args.t1 ? args.p1 : args.p0;
+      const int a_mn = P.a_mn, b_mn = P.b_mn, num_kb = P.num_kb;
+      const uint32_t idesc = P.idesc;
       mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < args.num_kb; ++kb) {
+      for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(full_bar + 8 * stage, phase);
         tc_fence_after();
         if (lane == 0) {
@@ -249,8 +284,8 @@ __global__ void __launch_bounds__(256, 1)
           }
           const uint32_t sa_src = base + L::off_a + stage * L::A_STAGE;
           const uint32_t sb_src = base + L::off_b + stage * L::B_STAGE;
-          const uint64_t adesc = args.a_mn ? make_sw128_mnmajor_desc(sa_src) : make_sw128_kmajor_desc(sa_src);
-          const uint64_t bdesc = args.b_mn ? make_sw128_mnmajor_desc(sb_src) : make_sw128_kmajor_desc(sb_src);
+          const uint64_t adesc = a_mn ? make_sw128_mnmajor_desc(sa_src) : make_sw128_kmajor_desc(sa_src);
+          const uint64_t bdesc = b_mn ? make_sw128_mnmajor_desc(sb_src) : make_sw128_kmajor_desc(sb_src);
           // per K=32 step: K-major advances 32 B inside the 128-B swizzle row and jumps 16 KB
           // (1024 in 16-B units) to the next K atom every 4 steps; MN-major advances 32 K-rows
           // = 4 KB per step (atoms are contiguous)
@@ -259,26 +294,26 @@ __global__ void __launch_bounds__(256, 1)
           };
 #pragma unroll
           for (int k = 0; k < KS * BK / 32; ++k) {
-            const uint64_t ad = adesc + koff(args.a_mn, k), bd = bdesc + koff(args.b_mn, k);
+            const uint64_t ad = adesc + koff(a_mn, k), bd = bdesc + koff(b_mn, k);
             const uint32_t acc_flag = (kb | k) != 0;
             if (MX) {
               const uint32_t t = (uint32_t)k >> 2;
-              const uint32_t id = idesc_with_sf_id(args.idesc, k & 3, k & 3);
+              const uint32_t id = idesc_with_sf_id(idesc, k & 3, k & 3);
               const uint32_t sfa = tmem_base + L::sfa_col + 4 * t, sfb = tmem_base + L::sfb_col + 8 * t;
               if (CG == 2) mma_mxf8f6f4_cg2(d_tmem, ad, bd, id, acc_flag, sfa, sfb);
               else mma_mxf8f6f4(d_tmem, ad, bd, id, acc_flag, sfa, sfb);
             } else if (CG == 2) {
-              mma_f8f6f4_cg2(d_tmem, ad, bd, args.idesc, acc_flag);
+              mma_f8f6f4_cg2(d_tmem, ad, bd, idesc, acc_flag);
             } else {
-              mma_f8f6f4(d_tmem, ad, bd, args.idesc, acc_flag);
+              mma_f8f6f4(d_tmem, ad, bd, idesc, acc_flag);
             }
           }
           if (CG == 2) {
             mma_commit_cg2_mc(empty_bar + 8 * stage, 0x3);
-            if (kb == args.num_kb - 1) mma_commit_cg2_mc(tfull_bar + 8 * acc, 0x3);
+            if (kb == num_kb - 1) mma_commit_cg2_mc(tfull_bar + 8 * acc, 0x3);
           } else {
             mma_commit(empty_bar + 8 * stage);
-            if (kb == args.num_kb - 1) mma_commit(tfull_bar + 8 * acc);
+            if (kb == num_kb - 1) mma_commit(tfull_bar + 8 * acc);
           }
         }
         __syncwarp();
@@ -291,16 +326,18 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
-    float ts = 1.f;
-    if (!args.row_scales && args.sa) ts = __frcp_rn(args.sa[0]) * __frcp_rn(args.sb[0]);
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(tempty_bar, 0) : tempty_bar;
     for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
-      int mb, nb;
-      tile_coords(tile, args.tiles_m, args.tiles_n, args.group_m, mb, nb);
+      int pi, mb, nb;
+      locate(tile, pi, mb, nb);
+      const Prob& P = pi ? args.p1 : args.p0;
+      const int N = P.N, row_scales = P.row_scales, out_f32 = P.out_f32;
+      const float* sb = P.sb;
       const int row = mb * BM * CG + (int)crank * BM + q * 32 + (int)lane;
-      const bool rvalid = row < args.M;
-      float rs = ts;
-      if (args.row_scales && rvalid) rs = __frcp_rn(args.sa[row]);
+      const bool rvalid = row < P.M;
+      float rs = 1.f;
+      if (!row_scales && P.sa) rs = __frcp_rn(P.sa[0]) * __frcp_rn(P.sb[0]);
+      if (row_scales && rvalid) rs = __frcp_rn(P.sa[row]);
       mbar_wait(tfull_bar + 8 * acc, acc_phase);
       tc_fence_after();
 #pragma unroll 1
@@ -309,11 +346,11 @@ __global__ void __launch_bounds__(256, 1)
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_wait_ld();
         const int col0 = nb * BN + c * 32;
-        if (col0 >= args.N || (args.debug & 1)) continue;   // warp-uniform
+        if (col0 >= N || (args.debug & 1)) continue;   // warp-uniform
         float v[32];
-        if (args.row_scales) {
+        if (row_scales) {
           // lane j computes 1/sb for column col0 + j once; the warp shares them by shuffles
-          const float rcol = __frcp_rn(args.sb[min(col0 + (int)lane, args.N - 1)]);
+          const float rcol = __frcp_rn(sb[min(col0 + (int)lane, N - 1)]);
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             v[j] = __fmul_rn(__fmul_rn(__uint_as_float(r[j]), rs), __shfl_sync(0xffffffffu, rcol, j));
@@ -321,10 +358,10 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__uint_as_float(r[j]), rs);
         }
-        const int nvalid = min(32, args.N - col0);  // 16 or 32 (N % 16 == 0)
+        const int nvalid = min(32, N - col0);  // 16 or 32 (N % 16 == 0)
         if (!rvalid) continue;
-        if (args.out_f32) {
-          float* dst = reinterpret_cast<float*>(args.D) + (int64_t)row * args.ldd + col0;
+        if (out_f32) {
+          float* dst = reinterpret_cast<float*>(P.D) + (int64_t)row * P.ldd + col0;
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             if (4 * j < nvalid)
@@ -336,7 +373,7 @@ __global__ void __launch_bounds__(256, 1)
             __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
             pk[j] = *reinterpret_cast<uint32_t*>(&h);
           }
-          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.D) + (int64_t)row * args.ldd + col0;
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(P.D) + (int64_t)row * P.ldd + col0;
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             if (8 * j < nvalid)
@@ -424,7 +461,38 @@ static bool make_sf_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K
 }
 
 template <bool MX, int CG, int ST, int KS>
-static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
+static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
+  if (!make_operand_map(&maps[0], p.A, p.a_mn, p.M, p.K, p.lda, BM) ||
+      !make_operand_map(&maps[1], p.B, p.b_mn, p.N, p.K, p.ldb, BN / CG))
+    return false;
+  if (MX) {
+    if (!make_sf_map(&maps[2], p.sa, p.M, p.K, KS) || !make_sf_map(&maps[3], p.sb, p.N, p.K, KS)) return false;
+  } else {
+    maps[2] = maps[0];   // unused by the plain FP8 kinds
+    maps[3] = maps[1];
+  }
+  P = Prob{};
+  P.M = (int)p.M; P.N = (int)p.N; P.K = (int)p.K;
+  P.tiles_m = (int)((p.M + BM * CG - 1) / (BM * CG));
+  P.tiles_n = (int)((p.N + BN - 1) / BN);
+  P.num_kb = (int)((p.K + BK * KS - 1) / (BK * KS));
+  P.idesc = MX ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN)
+               : make_idesc_f8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u);
+  P.a_mn = p.a_mn;
+  P.b_mn = p.b_mn;
+  if (MX) {
+    P.sf_tiles_k = (int)(p.K / 128);
+  } else {
+    P.sa = static_cast<const float*>(p.sa);
+    P.sb = static_cast<const float*>(p.sb);
+    P.row_scales = p.scale_mode == 1;
+  }
+  P.D = p.D; P.ldd = p.ldd; P.out_f32 = p.out_f32;
+  return true;
+}
+
+template <bool MX, int CG, int ST, int KS>
+static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   using L = Layout<MX, CG, ST, KS>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -433,34 +501,18 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
         cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG, ST, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  CUtensorMap ta, tb, tsa, tsb;
-  if (!make_operand_map(&ta, p.A, p.a_mn, p.M, p.K, p.lda, BM) ||
-      !make_operand_map(&tb, p.B, p.b_mn, p.N, p.K, p.ldb, BN / CG))
-    return cudaErrorInvalidValue;
-  if (MX) {
-    if (!make_sf_map(&tsa, p.sa, p.M, p.K, KS) || !make_sf_map(&tsb, p.sb, p.N, p.K, KS)) return cudaErrorInvalidValue;
-  } else {
-    tsa = ta;   // unused by the plain FP8 kinds
-    tsb = tb;
-  }
+  CUtensorMap m0[4], m1[4];
   GemmArgs a{};
-  a.M = (int)p.M; a.N = (int)p.N; a.K = (int)p.K;
-  a.tiles_m = (int)((p.M + BM * CG - 1) / (BM * CG));
-  a.tiles_n = (int)((p.N + BN - 1) / BN);
-  a.num_tiles = a.tiles_m * a.tiles_n;
-  a.num_kb = (int)((p.K + BK * KS - 1) / (BK * KS));
-  a.idesc = MX ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN)
-               : make_idesc_f8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u);
-  a.a_mn = p.a_mn;
-  a.b_mn = p.b_mn;
-  if (MX) {
-    a.sf_tiles_k = (int)(p.K / 128);
+  if (!setup_prob<MX, CG, ST, KS>(ps[0], a.p0, m0)) return cudaErrorInvalidValue;
+  a.t1 = a.p0.tiles_m * a.p0.tiles_n;
+  if (n > 1) {
+    if (!setup_prob<MX, CG, ST, KS>(ps[1], a.p1, m1)) return cudaErrorInvalidValue;
+    a.num_tiles = a.t1 + a.p1.tiles_m * a.p1.tiles_n;
   } else {
-    a.sa = static_cast<const float*>(p.sa);
-    a.sb = static_cast<const float*>(p.sb);
-    a.row_scales = p.scale_mode == 1;
+    a.p1 = a.p0;
+    for (int i = 0; i < 4; ++i) m1[i] = m0[i];
+    a.num_tiles = a.t1;
   }
-  a.D = p.D; a.ldd = p.ldd; a.out_f32 = p.out_f32;
   {
     const char* d = getenv("FP8T_GEMM_DEBUG");
     a.debug = d ? atoi(d) : 0;
@@ -473,7 +525,8 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
   const int grid = CG * (a.num_tiles < slots ? a.num_tiles : slots);
   LaunchScope ls(MX ? K_GEMM_MX : K_GEMM, st);
   if (CG == 1) {
-    fp8_gemm_kernel<MX, CG, ST, KS><<<grid, 256, L::bytes, st>>>(ta, tb, tsa, tsb, a);
+    fp8_gemm_kernel<MX, CG, ST, KS><<<grid, 256, L::bytes, st>>>(m0[0], m0[1], m0[2], m0[3], m1[0], m1[1], m1[2],
+                                                                 m1[3], a);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -487,22 +540,28 @@ static cudaError_t launch_t(const GemmProblem& p, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS>, ta, tb, tsa, tsb, a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS>, m0[0], m0[1], m0[2], m0[3], m1[0], m1[1],
+                                       m1[2], m1[3], a);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st) {
+// One or two problems of the same kind (scale mode) on one persistent launch.
+cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st) {
+  if (n < 1 || n > 2) return cudaErrorInvalidValue;
+  if (n == 2 && ((ps[0].scale_mode == 2) != (ps[1].scale_mode == 2))) return cudaErrorInvalidValue;
   const int cg = cta_group_for();
-  if (p.scale_mode == 2) return cg == 1 ? launch_t<true, 1, 4, 1>(p, st) : launch_t<true, 2, 3, 2>(p, st);
-  if (cg == 1) return launch_t<false, 1, 4, 1>(p, st);
+  if (ps[0].scale_mode == 2) return cg == 1 ? launch_t<true, 1, 4, 1>(ps, n, st) : launch_t<true, 2, 3, 2>(ps, n, st);
+  if (cg == 1) return launch_t<false, 1, 4, 1>(ps, n, st);
   // default: 3 stages x 2 K atoms (64 KB per CTA per stage, 8 MMAs per barrier round trip);
   // FP8T_GEMM_STAGES=6 selects 6 x 1 atom (4 MMAs per round trip) for comparison
   const char* e = getenv("FP8T_GEMM_STAGES");
-  if (e && e[0] == '6') return launch_t<false, 2, 6, 1>(p, st);
-  if (e && e[0] == '4') return launch_t<false, 2, 4, 1>(p, st);
-  return launch_t<false, 2, 3, 2>(p, st);
+  if (e && e[0] == '6') return launch_t<false, 2, 6, 1>(ps, n, st);
+  if (e && e[0] == '4') return launch_t<false, 2, 4, 1>(ps, n, st);
+  return launch_t<false, 2, 3, 2>(ps, n, st);
 }
+
+cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st) { return launch_gemms(&p, 1, st); }
 
 }  // namespace fp8t

@@ -19,7 +19,8 @@ struct LaunchScope {
 // amax_tile: mode bit0 tensor -> at[1], bit1 rows -> ar[R], bit2 cols -> ac[C] (u32 |x| bits, pre-zeroed)
 cudaError_t launch_amax(const void* x, bool bf16, int64_t R, int64_t C, int64_t ld, int mode, uint32_t* at,
                         uint32_t* ar, uint32_t* ac, cudaStream_t st);
-// cast_tile: scale modes 0 none / 1 tensor / 2 row / 3 col for q (row-major) and qt (transposed)
+// cast_tile: scale modes 0 none / 1 tensor / 2 row / 3 col for q (row-major) and qt (transposed);
+// tm = 5: column-scaled second copy written row-major (MN-major operand of the rowwise backward)
 cudaError_t launch_cast(const void* x, bool bf16, int fmt, int64_t R, int64_t C, int64_t ld, int qm, int tm,
                         const float* aq, const float* at, uint8_t* q, uint8_t* qt, float* sq, float* st,
                         cudaStream_t s);
@@ -40,5 +41,7 @@ struct GemmProblem {
   void* D; int out_f32; int64_t ldd;
 };
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st);
+// Two problems of the same kind on one persistent launch (tiles of ps[0] then ps[1]).
+cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st);
 
 }  // namespace fp8t
