@@ -208,9 +208,15 @@ fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, fp8_major_t major_a,
  *   saves the row-major codes the forward GEMM used (the backward GEMMs read
  *   them MN-major); rowwise saves column-scaled copies, MXFP8 dim1 copies.
  * ws: fp8_linear_workspace_bytes() bytes of scratch.
+ * saved == NULL: forward-only FP8 (inference, the paper's float8 dynamic activation +
+ *   weight quantisation, PAPER.md:470-471 / 636, "same configurations as FP8
+ *   training" PAPER.md:364-366): only the forward operands are cast (rowwise: row
+ *   scales only; mxfp8: dim0 only) and `ws` must hold
+ *   fp8_linear_infer_workspace_bytes() bytes.
  * ------------------------------------------------------------------------- */
 size_t fp8_linear_saved_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K);
 size_t fp8_linear_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K);
+size_t fp8_linear_infer_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K);
 fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
                             const fp8_tensor_t* w_fp8, void* y, void* saved,
                             void* ws, size_t ws_bytes, void* stream);

@@ -57,6 +57,8 @@ SIGNATURES = {
                             _c.c_void_p, _c.c_int, _c.c_int64, _c.c_void_p]),
     "fp8_linear_saved_bytes": (_c.c_size_t, [_c.POINTER(LinearCfg), _c.c_int64, _c.c_int64, _c.c_int64]),
     "fp8_linear_workspace_bytes": (_c.c_size_t, [_c.POINTER(LinearCfg), _c.c_int64, _c.c_int64, _c.c_int64]),
+    "fp8_linear_infer_workspace_bytes": (_c.c_size_t, [_c.POINTER(LinearCfg), _c.c_int64, _c.c_int64,
+                                                       _c.c_int64]),
     "fp8_linear_fwd": (_c.c_int, [_c.POINTER(LinearCfg), HP, HP, _c.POINTER(Tensor8), _c.c_void_p, _c.c_void_p,
                                   _c.c_void_p, _c.c_size_t, _c.c_void_p]),
     "fp8_linear_bwd": (_c.c_int, [_c.POINTER(LinearCfg), HP, _c.c_int64, _c.c_void_p, _c.POINTER(Tensor8),

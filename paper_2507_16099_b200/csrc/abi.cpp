@@ -381,6 +381,33 @@ BwdWs carve_bwd(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, void* base, s
   return w;
 }
 
+// Forward-only (inference) workspace: the forward's codes and scales, nothing kept for a backward.
+struct InferWs {
+  uint8_t* xq; uint8_t* wq;
+  void* sx; void* sw;        // tensorwise float[1] | rowwise float[M], float[N] | mx E8M0 dim0
+  float* amax;               // tensorwise [2] | rowwise [M + N]
+};
+InferWs carve_infer(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K, void* base, size_t* bytes) {
+  Carve c(base);
+  InferWs w{};
+  w.xq = c.take<uint8_t>((size_t)M * K);
+  w.wq = c.take<uint8_t>((size_t)N * K);
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    w.sx = c.take<float>(4);
+    w.sw = c.take<float>(4);
+    w.amax = c.take<float>(8);
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+    w.sx = c.take<float>(4 * M);
+    w.sw = c.take<float>(4 * N);
+    w.amax = c.take<float>(4 * (M + N));
+  } else {
+    w.sx = c.take<uint8_t>((size_t)M * K / 32);
+    w.sw = c.take<uint8_t>((size_t)N * K / 32);
+  }
+  if (bytes) *bytes = c.off;
+  return w;
+}
+
 fp8_status_t check_cfg(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K) {
   if (!cfg) return fail(FP8_EINVAL, "cfg: null pointer");
   if (cfg->recipe < FP8_RECIPE_TENSORWISE || cfg->recipe > FP8_RECIPE_MXFP8) return fail(FP8_EINVAL, "bad recipe");
@@ -404,6 +431,13 @@ size_t fp8_linear_saved_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N,
   return b;
 }
 
+size_t fp8_linear_infer_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K) {
+  if (!cfg) return 0;
+  size_t b = 0;
+  carve_infer(cfg, M, N, K, nullptr, &b);
+  return b;
+}
+
 size_t fp8_linear_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K) {
   if (!cfg) return 0;
   size_t f = 0, b = 0;
@@ -420,9 +454,10 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
   if (w.cols != K) return fail(FP8_EINVAL, "w.cols != x.cols");
   FP8T_TRY(check_cfg(cfg, M, N, K));
   FP8T_TRY(check_ptr(y, "y"));
-  FP8T_TRY(check_ptr(saved, "saved"));
+  if (saved) FP8T_TRY(check_ptr(saved, "saved"));
   FP8T_TRY(check_ptr(ws, "ws"));
-  if (ws_bytes < fp8_linear_workspace_bytes(cfg, M, N, K)) return fail(FP8_EWORKSPACE, "workspace too small");
+  const size_t need = saved ? fp8_linear_workspace_bytes(cfg, M, N, K) : fp8_linear_infer_workspace_bytes(cfg, M, N, K);
+  if (ws_bytes < need) return fail(FP8_EWORKSPACE, "workspace too small (%zu < %zu)", ws_bytes, need);
   if (w_fp8) {
     if (cfg->recipe != FP8_RECIPE_TENSORWISE) return fail(FP8_EUNSUPPORTED, "w_fp8 needs the tensorwise recipe");
     if (w_fp8->rows != N || w_fp8->cols != K) return fail(FP8_EINVAL, "w_fp8 shape");
@@ -433,9 +468,56 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
   cudaStream_t st = S(stream);
   const bool xb = x.dtype == FP8_DT_BF16, wb = w.dtype == FP8_DT_BF16;
   const int ff = cfg->fmt_fwd;
+  const int of32 = cfg->out_dtype == FP8_DT_F32;
+
+  if (!saved) {
+    // forward-only FP8 (inference / float8 dynamic activation + weight, PAPER.md:470-471, 636:
+    // "same configurations as FP8 training"): only the forward operands are cast
+    InferWs iw = carve_infer(cfg, M, N, K, ws, nullptr);
+    if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+      uint32_t* ax = reinterpret_cast<uint32_t*>(iw.amax);
+      FP8T_CUDA(cudaMemsetAsync(ax, 0, 8, st), "memset");
+      FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
+      FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 1, 0, iw.amax, iw.amax, iw.xq, nullptr, (float*)iw.sx, nullptr,
+                            st),
+                "cast x");
+      const uint8_t* wq = iw.wq;
+      const void* swp = iw.sw;
+      if (w_fp8) {
+        wq = w_fp8->q;
+        swp = w_fp8->scale;
+      } else {
+        FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 1, ax + 1, nullptr, nullptr, st), "amax w");
+        FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 1, 0, iw.amax + 1, iw.amax + 1, iw.wq, nullptr,
+                              (float*)iw.sw, nullptr, st),
+                  "cast w");
+      }
+      GemmProblem p{iw.xq, wq, ff, ff, 0, 0, iw.sx, swp, 0, M, N, K, K, K, y, of32, N};
+      FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+    } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {   // PerRow: row amax only
+      float* axr = iw.amax;
+      float* awr = axr + M;
+      FP8T_CUDA(cudaMemsetAsync(iw.amax, 0, 4 * (M + N), st), "memset");
+      FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 2, nullptr, (uint32_t*)axr, nullptr, st), "amax x");
+      FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 2, nullptr, (uint32_t*)awr, nullptr, st), "amax w");
+      FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 2, 0, axr, axr, iw.xq, nullptr, (float*)iw.sx, nullptr, st),
+                "cast x");
+      FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 0, awr, awr, iw.wq, nullptr, (float*)iw.sw, nullptr, st),
+                "cast w");
+      GemmProblem p{iw.xq, iw.wq, ff, ff, 0, 0, iw.sx, iw.sw, 1, M, N, K, K, K, y, of32, N};
+      FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+    } else {   // MXFP8: dim0 only
+      const bool rc = cfg->mx_round == FP8_MX_RCEIL;
+      FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, iw.xq, (uint8_t*)iw.sx, nullptr, nullptr, st), "mx x");
+      FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, iw.wq, (uint8_t*)iw.sw, nullptr, nullptr, st), "mx w");
+      GemmProblem p{iw.xq, iw.wq, ff, ff, 0, 0, iw.sx, iw.sw, 2, M, N, K, K, K, y, of32, N};
+      FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+    }
+    return FP8_OK;
+  }
+
   Saved sv = carve_saved(cfg, M, N, K, saved, nullptr);
   FwdWs fw = carve_fwd(cfg, M, N, K, ws, nullptr);
-  const int of32 = cfg->out_dtype == FP8_DT_F32;
 
   if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
     // row-major codes only: the backward GEMMs read them MN-major (no transposed copies)

@@ -60,7 +60,13 @@ class Float8Linear(nn.Linear):
         x2d = x.reshape(-1, shp[-1])
         if x2d.dtype != torch.bfloat16 and x2d.dtype != torch.float32:
             x2d = x2d.to(torch.bfloat16)
-        y = _Float8LinearFn.apply(x2d, self.weight, self.recipe)
+        if not torch.is_grad_enabled() or not (x2d.requires_grad or self.weight.requires_grad):
+            # forward-only FP8 (inference): no backward operands are cast or kept
+            M, K = x2d.shape
+            plan = _PLANS.get(M, self.out_features, K, self.recipe, torch.bfloat16, x2d.device)
+            y = plan.forward(x2d.contiguous(), self.weight.detach().contiguous(), None)
+        else:
+            y = _Float8LinearFn.apply(x2d, self.weight, self.recipe)
         if self.bias is not None:
             y = y + self.bias.to(y.dtype)
         return y.reshape(*shp[:-1], self.out_features)

@@ -128,14 +128,19 @@ class LinearPlan:
                          self.N, self.K)
 
     def forward(self, x, w, saved, y=None, w_fp8=None, stream=None):
-        """w_fp8: optional (codes [N,K] uint8, scale float[1]) pre-cast weight (FSDP FP8 gather)."""
+        """w_fp8: optional (codes [N,K] uint8, scale float[1]) pre-cast weight (FSDP FP8 gather).
+        saved=None: forward-only (inference) -- nothing is kept for a backward."""
         if y is None:
             y = torch.empty((self.M, self.N), dtype=self.out_dtype, device=x.device)
         wq = self._wq(w_fp8)
         wh = hp(w) if w is not None else L.HP(None, L.DT_BF16, self.N, self.K, self.K)
+        ws, wsb = self.ws, self.ws_bytes
+        if saved is None:
+            wsb = L.lib.fp8_linear_infer_workspace_bytes(ctypes.byref(self.cfg), self.M, self.N, self.K)
+            if wsb > self.ws_bytes:
+                ws = torch.empty(wsb, dtype=torch.uint8, device=x.device)
         L.check(L.lib.fp8_linear_fwd(ctypes.byref(self.cfg), hp(x), wh, ctypes.byref(wq) if wq else None,
-                                     _ptr(y), _ptr(saved), _ptr(self.ws), self.ws_bytes, _stream(stream)),
-                "fp8_linear_fwd")
+                                     _ptr(y), _ptr(saved), _ptr(ws), wsb, _stream(stream)), "fp8_linear_fwd")
         return y
 
     def backward(self, dy, saved, dx=None, dw=None, want_dx=True, want_dw=True, w_fp8=None, stream=None):

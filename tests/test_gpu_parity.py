@@ -407,3 +407,18 @@ def test_fsdp_allgather_single_rank_equals_cast():
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("recipe,cfg,M,N,K", [("tensorwise", "c2", 272, 400, 528), ("rowwise", "c3", 384, 400, 272),
+                                               ("mxfp8", "c4", 256, 384, 512)])
+def test_linear_forward_only_inference(recipe, cfg, M, N, K):
+    """saved=NULL: forward-only FP8 (float8dq); same Y as the training forward, bit-identical."""
+    x, w, _ = synth.linear_inputs(cfg, M, N, K, seed=0)
+    y, yb, _ = olin.forward(x, w, recipe)
+    plan = ops.LinearPlan(M, N, K, recipe=recipe, out_dtype=torch.float32)
+    X, W = _dev(x, torch.bfloat16), _dev(w, torch.bfloat16)
+    y_inf = plan.forward(X, W, None).clone()
+    y_trn = plan.forward(X, W, plan.new_saved())
+    torch.cuda.synchronize()
+    assert torch.equal(y_inf, y_trn)
+    _tol_check(_np(y_inf).astype(np.float64), y, yb)
