@@ -38,6 +38,11 @@ CONFIGS = {
     "c3w1": dict(M=16384, N=14336, K=4096, recipe="rowwise", cfg="c3",
                  workload="c3 (w1 linear): Llama-3-8B MLP w1 fwd+bwd, rowwise scaling, bf16 in/out "
                           "(BASELINE.json configs[2])"),
+    "c3w1hp": dict(M=16384, N=14336, K=4096, recipe="rowwise_gw_hp", cfg="c3",
+                   workload="c3 (w1 linear), rowwise_gw_hp recipe (dW in bf16, PAPER.md:598)"),
+    "c5": dict(M=8192, N=53248, K=16384, recipe="tensorwise", cfg="c5",
+               workload="c5: Llama-3.1-405B w1 linear fwd+bwd, M=8192 tokens per GPU, K=16384, N=53248, "
+                        "tensorwise (BASELINE.json configs[4]; FSDP2 FP8 all-gather at N>1)"),
 }
 # oracle sample for the CPU baseline / reference arm: same K and value recipe, fewer rows
 CPU_SAMPLE = dict(M=128, N=2048)
@@ -283,7 +288,7 @@ def run_ours(a):
                 dist.reduce_scatter_tensor(dw_shard, dw)
         else:
             plan.forward(xx, ww, saved, y=y)
-            plan.backward(gg, saved, dx=dx, dw=dw)
+            plan.backward(gg, saved, dx=dx, dw=dw, x=xx)
 
     def barrier():
         if world > 1:
@@ -330,13 +335,14 @@ def run_ours(a):
     by = {}
     for i in range(max(nrec, 0)):
         by.setdefault(kinds[i], []).append(durs[i])
-    gemm_kind = 5 if cfg["recipe"] == "mxfp8" else 4
+    gemm_kind = 5 if cfg["recipe"] == "mxfp8" else 4   # (rowwise_gw_hp's BF16 dW GEMM is kind 6)
     gemm_ms = by.get(gemm_kind, [float("nan")])
     gemm_avg = sum(gemm_ms) / len(gemm_ms)
     # launches per step: forward (1 problem) + backward (dX and dW grouped in one launch);
     # algorithmic flops per launch differ, so achieved = GEMM flops per step / GEMM time per step
     gemm_launches_per_step = len(gemm_ms) / a.steps
-    gemm_tflops = flops_step / (sum(gemm_ms) / a.steps / 1e3) / 1e12
+    fp8_gemm_flops = (4.0 if cfg["recipe"] == "rowwise_gw_hp" else 6.0) * M * N * K   # gw_hp: dW is bf16
+    gemm_tflops = fp8_gemm_flops / (sum(gemm_ms) / a.steps / 1e3) / 1e12
     peaks = _peaks()
     # dense FP8 peak = 2 x measured bf16 cuBLAS (the guide's nominal FP8/BF16 ratio).  The timed region
     # is well under a second, so the burst figure is the denominator; sustained is reported beside it.
@@ -349,6 +355,9 @@ def run_ours(a):
         cast_kinds = (2,)
     elif cfg["recipe"] == "rowwise":       # amax read 2 + cast read 2 + row- and column-scaled layouts 1 + 1
         cast_bytes = (M * K + N * K + M * N) * 6
+        cast_kinds = (0, 1)
+    elif cfg["recipe"] == "rowwise_gw_hp":  # X, dY: row-scaled layout only (5 B); W: both layouts (6 B)
+        cast_bytes = (M * K + M * N) * 5 + N * K * 6
         cast_kinds = (0, 1)
     elif not fsdp:                         # tensorwise: amax 2 + cast 2 + one row-major layout 1 (the
         cast_bytes = (M * K + N * K + M * N) * 5   # backward GEMMs read it MN-major)
@@ -451,7 +460,7 @@ def run_ours(a):
                      if cast_gbps else None, "ms_per_step": cast_ms, "algorithmic_bytes_per_step": cast_bytes},
             "kernels_ms_per_step": {name: round(sum(by.get(k, [])) / a.steps, 4)
                                     for k, name in ((0, "amax"), (1, "cast"), (2, "mx_cast"), (3, "transpose_u8"),
-                                                    (4, "gemm_fp8"), (5, "gemm_mxfp8"))},
+                                                    (4, "gemm_fp8"), (5, "gemm_mxfp8"), (6, "gemm_bf16"))},
             "bf16": bf16,
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -69,7 +69,7 @@
 extern "C" {
 #endif
 
-#define FP8TRAIN_ABI_VERSION 2
+#define FP8TRAIN_ABI_VERSION 3
 
 typedef enum {
   FP8_OK = 0,
@@ -98,9 +98,10 @@ typedef enum {
 typedef enum { FP8_MX_FLOOR = 0, FP8_MX_RCEIL = 1 } fp8_mx_round_t;
 
 typedef enum {
-  FP8_RECIPE_TENSORWISE = 0,  /* PAPER.md:596 */
-  FP8_RECIPE_ROWWISE = 1,     /* PAPER.md:597 */
-  FP8_RECIPE_MXFP8 = 2        /* PAPER.md:735 (MX formats for training) */
+  FP8_RECIPE_TENSORWISE = 0,     /* PAPER.md:596 */
+  FP8_RECIPE_ROWWISE = 1,        /* PAPER.md:597 */
+  FP8_RECIPE_MXFP8 = 2,          /* PAPER.md:735 (MX formats for training) */
+  FP8_RECIPE_ROWWISE_GW_HP = 3   /* PAPER.md:598: rowwise, but dL/dW stays in bfloat16 */
 } fp8_recipe_t;
 
 /* High-precision input matrix: row-major, `ld` in elements (>= cols). */
@@ -227,10 +228,14 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
  *   operand, columns of the right"); mxfp8: dY blocks along N (dX) and along M
  *   (dW), W along N, X along M.
  * dy [M,N]; dx [M,K] and dw [N,K] out_dtype dense, either may be NULL.
+ * x: the forward's input [M,K]; its shape gives K.  Its data is read only by
+ *   FP8_RECIPE_ROWWISE_GW_HP, whose dW = dY^T X is a BF16 x BF16 tcgen05 GEMM
+ *   (kind::f16, fp32 accumulate) on the high-precision dY and X (both must be BF16);
+ *   for the other recipes x.ptr may be NULL.
  * `saved` must be the buffer the matching fp8_linear_fwd wrote.  If the forward
  * ran with a pre-cast weight (w_fp8), pass the same codes again (FSDP2 re-gathers
  * the weight for the backward); otherwise pass NULL. */
-fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K,
+fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x,
                             const void* saved, const fp8_tensor_t* w_fp8, void* dx, void* dw,
                             void* ws, size_t ws_bytes, void* stream);
 

@@ -28,6 +28,7 @@ from .codecs import E4M3, E5M2
 TENSORWISE = "tensorwise"
 ROWWISE = "rowwise"
 MXFP8 = "mxfp8"
+ROWWISE_GW_HP = "rowwise_gw_hp"
 
 
 def forward(x, w, recipe, fmt_fwd=E4M3, mx_mode=mx.FLOOR):
@@ -40,7 +41,7 @@ def forward(x, w, recipe, fmt_fwd=E4M3, mx_mode=mx.FLOOR):
         y = gemm.gemm_ref(xq, fmt_fwd, sx, wq, fmt_fwd, sw)
         bd = gemm.abs_bound(xq, fmt_fwd, sx, wq, fmt_fwd, sw)
         saved = dict(xq=xq, sx=sx, amax_x=ax, wq=wq, sw=sw, amax_w=aw)
-    elif recipe == ROWWISE:
+    elif recipe in (ROWWISE, ROWWISE_GW_HP):
         xq, sx, ax = fp8.cast_rowwise(x, fmt_fwd)
         wq, sw, aw = fp8.cast_rowwise(w, fmt_fwd)
         y = gemm.gemm_ref(xq, fmt_fwd, sx, wq, fmt_fwd, sw)
@@ -86,6 +87,18 @@ def backward(x, w, dy, recipe, fmt_fwd=E4M3, fmt_grad=E5M2, mx_mode=mx.FLOOR):
         dw = gemm.gemm_ref(g_c.T, fmt_grad, sg_c, x_c.T, fmt_fwd, sx_c)
         dwb = gemm.abs_bound(g_c.T, fmt_grad, sg_c, x_c.T, fmt_fwd, sx_c)
         casts = dict(g_r=g_r, sg_r=sg_r, w_c=w_c, sw_c=sw_c, g_c=g_c, sg_c=sg_c, x_c=x_c, sx_c=sx_c)
+    elif recipe == ROWWISE_GW_HP:
+        # Appendix A: "like rowwise but it keeps the dL/dW computation in bfloat16";
+        # grad_weight = gemm_ref(grad_out^T, x) with no FP8 casting.
+        g_r, sg_r, _ = fp8.cast_rowwise(dy, fmt_grad)
+        w_c, sw_c, _ = fp8.cast_colwise(w, fmt_fwd)
+        dx = gemm.gemm_ref(g_r, fmt_grad, sg_r, w_c.T, fmt_fwd, sw_c)
+        dxb = gemm.abs_bound(g_r, fmt_grad, sg_r, w_c.T, fmt_fwd, sw_c)
+        G = dy.astype(np.float64)
+        X = x.astype(np.float64)
+        dw = G.T @ X
+        dwb = np.abs(G).T @ np.abs(X)
+        casts = dict(g_r=g_r, sg_r=sg_r, w_c=w_c, sw_c=sw_c)
     elif recipe == MXFP8:
         g0, g0s = mx.quantize_dim0(dy, fmt_grad, mx_mode)   # dY along N  -> [M,N]
         w1, w1s = mx.quantize_dim1(w, fmt_fwd, mx_mode)     # W along N   -> [K,N]

@@ -17,7 +17,7 @@ E4M3, E5M2 = 0, 1
 GRAN_TENSOR, GRAN_ROW, GRAN_COL, GRAN_ROW_COL, GRAN_MX32 = range(5)
 MX_FLOOR, MX_RCEIL = 0, 1
 K_MAJOR, MN_MAJOR = 0, 1
-RECIPE_TENSORWISE, RECIPE_ROWWISE, RECIPE_MXFP8 = range(3)
+RECIPE_TENSORWISE, RECIPE_ROWWISE, RECIPE_MXFP8, RECIPE_ROWWISE_GW_HP = range(4)
 
 STATUS_NAMES = {0: "FP8_OK", 1: "FP8_EINVAL", 2: "FP8_EALIGN", 3: "FP8_EUNSUPPORTED",
                 4: "FP8_ECUDA", 5: "FP8_ENCCL", 6: "FP8_EWORKSPACE"}
@@ -61,7 +61,7 @@ SIGNATURES = {
                                                        _c.c_int64]),
     "fp8_linear_fwd": (_c.c_int, [_c.POINTER(LinearCfg), HP, HP, _c.POINTER(Tensor8), _c.c_void_p, _c.c_void_p,
                                   _c.c_void_p, _c.c_size_t, _c.c_void_p]),
-    "fp8_linear_bwd": (_c.c_int, [_c.POINTER(LinearCfg), HP, _c.c_int64, _c.c_void_p, _c.POINTER(Tensor8),
+    "fp8_linear_bwd": (_c.c_int, [_c.POINTER(LinearCfg), HP, HP, _c.c_void_p, _c.POINTER(Tensor8),
                                   _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
     "fp8_comm_get_unique_id": (_c.c_int, [_c.c_void_p]),
     "fp8_comm_init": (_c.c_int, [_c.POINTER(_c.c_void_p), _c.c_void_p, _c.c_int, _c.c_int]),

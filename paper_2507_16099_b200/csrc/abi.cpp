@@ -316,7 +316,7 @@ Saved carve_saved(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K, 
   if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
     s.sx = c.take<float>(4);
     s.sw = c.take<float>(4);
-  } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {
     s.sx = c.take<float>(4 * K);
     s.sw = c.take<float>(4 * K);
   } else {
@@ -343,7 +343,7 @@ FwdWs carve_fwd(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K, vo
   }
   w.xq = c.take<uint8_t>((size_t)M * K);
   w.wq = c.take<uint8_t>((size_t)N * K);
-  if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+  if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {
     w.amax = c.take<float>(4 * (M + K + N + K));
     w.sxr = c.take<float>(4 * M);
     w.swr = c.take<float>(4 * N);
@@ -369,7 +369,7 @@ BwdWs carve_bwd(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, void* base, s
     w.amax = c.take<float>(4);
     w.sg = c.take<float>(4);
     w.sgT = w.sg;
-  } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {
     w.amax = c.take<float>(4 * (M + N));
     w.sg = c.take<float>(4 * M);
     w.sgT = c.take<float>(4 * N);
@@ -396,7 +396,7 @@ InferWs carve_infer(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K
     w.sx = c.take<float>(4);
     w.sw = c.take<float>(4);
     w.amax = c.take<float>(8);
-  } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {
     w.sx = c.take<float>(4 * M);
     w.sw = c.take<float>(4 * N);
     w.amax = c.take<float>(4 * (M + N));
@@ -410,7 +410,8 @@ InferWs carve_infer(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K
 
 fp8_status_t check_cfg(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K) {
   if (!cfg) return fail(FP8_EINVAL, "cfg: null pointer");
-  if (cfg->recipe < FP8_RECIPE_TENSORWISE || cfg->recipe > FP8_RECIPE_MXFP8) return fail(FP8_EINVAL, "bad recipe");
+  if (cfg->recipe < FP8_RECIPE_TENSORWISE || cfg->recipe > FP8_RECIPE_ROWWISE_GW_HP)
+    return fail(FP8_EINVAL, "bad recipe");
   FP8T_TRY(check_fmt(cfg->fmt_fwd));
   FP8T_TRY(check_fmt(cfg->fmt_grad));
   if (cfg->out_dtype != FP8_DT_BF16 && cfg->out_dtype != FP8_DT_F32) return fail(FP8_EINVAL, "bad out_dtype");
@@ -494,7 +495,7 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
       }
       GemmProblem p{iw.xq, wq, ff, ff, 0, 0, iw.sx, swp, 0, M, N, K, K, K, y, of32, N};
       FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
-    } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {   // PerRow: row amax only
+    } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {   // PerRow
       float* axr = iw.amax;
       float* awr = axr + M;
       FP8T_CUDA(cudaMemsetAsync(iw.amax, 0, 4 * (M + N), st), "memset");
@@ -540,17 +541,20 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
     }
     GemmProblem p{sv.xT, wq, ff, ff, 0, 0, sv.sx, sv.sw, 0, M, N, K, K, K, y, of32, N};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
-  } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {
+    const bool gw_hp = cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;   // X's column-scaled copy unused
     float* axr = fw.amax;
     float* axc = axr + M;
     float* awr = axc + K;
     float* awc = awr + N;
     FP8T_CUDA(cudaMemsetAsync(fw.amax, 0, 4 * (M + K + N + K), st), "memset");
-    FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 6, nullptr, (uint32_t*)axr, (uint32_t*)axc, st), "amax x");
+    FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, gw_hp ? 2 : 6, nullptr, (uint32_t*)axr, (uint32_t*)axc, st),
+              "amax x");
     FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 6, nullptr, (uint32_t*)awr, (uint32_t*)awc, st), "amax w");
     // row-scaled codes for the forward GEMM; column-scaled codes written row-major for the
     // backward GEMMs (read MN-major, no transposed copy)
-    FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 2, 5, axr, axc, fw.xq, sv.xT, fw.sxr, (float*)sv.sx, st),
+    FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 2, gw_hp ? 0 : 5, axr, axc, fw.xq, gw_hp ? nullptr : sv.xT,
+                          fw.sxr, gw_hp ? nullptr : (float*)sv.sx, st),
               "cast x");
     FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 5, awr, awc, fw.wq, sv.wT, fw.swr, (float*)sv.sw, st),
               "cast w");
@@ -566,10 +570,15 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
   return FP8_OK;
 }
 
-fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K, const void* saved,
+fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x, const void* saved,
                             const fp8_tensor_t* w_fp8, void* dx, void* dw, void* ws, size_t ws_bytes, void* stream) {
   FP8T_TRY(check_hp(dy, "dy"));
-  const int64_t M = dy.rows, N = dy.cols;
+  const int64_t M = dy.rows, N = dy.cols, K = x.cols;
+  const bool gw_hp = cfg && cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;
+  FP8T_TRY(check_hp(x, "x", gw_hp && dw));
+  if (x.rows != M) return fail(FP8_EINVAL, "x.rows != dy.rows");
+  if (gw_hp && dw && (x.dtype != FP8_DT_BF16 || dy.dtype != FP8_DT_BF16))
+    return fail(FP8_EUNSUPPORTED, "rowwise_gw_hp: the BF16 dW GEMM needs bf16 dy and x");
   FP8T_TRY(check_cfg(cfg, M, N, K));
   FP8T_TRY(check_ptr(saved, "saved"));
   FP8T_TRY(check_ptr(ws, "ws"));
@@ -595,14 +604,18 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K,
     FP8T_CUDA(launch_cast(dy.ptr, gb, fg, M, N, dy.ld, 1, 0, bw.amax, bw.amax, bw.g, nullptr, (float*)bw.sg,
                           nullptr, st),
               "cast dy");
-  } else if (cfg->recipe == FP8_RECIPE_ROWWISE) {
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE || gw_hp) {
     mode = 1;
     float* ar = bw.amax;
     float* ac = ar + M;
+    const bool colcopy = dw && !gw_hp;   // gw_hp: dW is a BF16 GEMM on the hp dY
+    if (!dx && !colcopy) goto gemms;
     FP8T_CUDA(cudaMemsetAsync(bw.amax, 0, 4 * (M + N), st), "memset");
-    FP8T_CUDA(launch_amax(dy.ptr, gb, M, N, dy.ld, 6, nullptr, (uint32_t*)ar, (uint32_t*)ac, st), "amax dy");
-    FP8T_CUDA(launch_cast(dy.ptr, gb, fg, M, N, dy.ld, dx ? 2 : 0, dw ? 5 : 0, ar, ac, bw.g, bw.gT, (float*)bw.sg,
-                          (float*)bw.sgT, st),
+    FP8T_CUDA(launch_amax(dy.ptr, gb, M, N, dy.ld, colcopy ? (dx ? 6 : 4) : 2, nullptr, (uint32_t*)ar,
+                          (uint32_t*)ac, st),
+              "amax dy");
+    FP8T_CUDA(launch_cast(dy.ptr, gb, fg, M, N, dy.ld, dx ? 2 : 0, colcopy ? 5 : 0, ar, ac, bw.g, bw.gT,
+                          (float*)bw.sg, (float*)bw.sgT, st),
               "cast dy");
   } else {
     mode = 2;
@@ -610,7 +623,22 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, int64_t K,
                              (uint8_t*)bw.sg, dw ? bw.gT : nullptr, (uint8_t*)bw.sgT, st),
               "mx cast dy");
   }
+gemms:
   if (!dx && !dw) return FP8_OK;
+  if (gw_hp) {
+    // dX in FP8 (row-scaled dY x column-scaled W, read MN-major); dW = dY^T X in BF16 on the
+    // high-precision operands (both row-major [M, .] -> MN-major)
+    if (dx) {
+      GemmProblem p{bw.g, sv.wT, fg, ff, 0, 1, bw.sg, sv.sw, 1, M, K, N, N, K, dx, of32, K};
+      FP8T_CUDA(launch_gemm(p, st), "gemm dx");
+    }
+    if (dw) {
+      GemmProblem p{static_cast<const uint8_t*>(dy.ptr), static_cast<const uint8_t*>(x.ptr), 0, 0, 1, 1, nullptr,
+                    nullptr, 0, N, K, M, dy.ld, x.ld, dw, of32, K, 1};
+      FP8T_CUDA(launch_gemm(p, st), "gemm dw bf16");
+    }
+    return FP8_OK;
+  }
   // dX and dW run as one persistent launch (tiles of dX, then dW): no wave tail between them
   GemmProblem ps[2];
   int n = 0;

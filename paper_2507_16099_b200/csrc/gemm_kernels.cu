@@ -63,7 +63,7 @@ struct GemmArgs {
   int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
 };
 
-template <bool MX, int CG, int ST, int KS> struct Layout {
+template <bool MX, int CG, int ST, int KS, bool BF = false> struct Layout {
   static constexpr int STAGES = ST;
   static constexpr int ACC = MX ? 1 : 2;
   // a stage holds KS 128-byte K atoms (16 KB sub-tiles of 128 rows each)
@@ -104,7 +104,7 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nb = local / gsz;
 }
 
-template <bool MX, int CG, int ST, int KS>
+template <bool MX, int CG, int ST, int KS, bool BF>
 __global__ void __launch_bounds__(256, 1)
     fp8_gemm_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tB0,
                     const __grid_constant__ CUtensorMap tSA0, const __grid_constant__ CUtensorMap tSB0,
@@ -112,7 +112,8 @@ __global__ void __launch_bounds__(256, 1)
                     const __grid_constant__ CUtensorMap tSA1, const __grid_constant__ CUtensorMap tSB1,
                     const __grid_constant__ GemmArgs args) {
   static_assert(KS == 1 || CG == 2, "multi-atom stages need the CTA-pair kernel");
-  using L = Layout<MX, CG, ST, KS>;
+  static_assert(!BF || (CG == 2 && KS == 2 && !MX), "BF16 operands: CTA-pair, 2-atom stages");
+  using L = Layout<MX, CG, ST, KS, BF>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -211,11 +212,16 @@ __global__ void __launch_bounds__(256, 1)
           // K atom j of this stage starts at k0 = (kb*KS + j)*BK; atoms are 16 KB apart in smem.
 #pragma unroll
           for (int j = 0; j < KS; ++j) {
-            const int k0 = (kb * KS + j) * BK;
+            // FP8: atom j = K bytes [(kb*KS + j)*128, +128) (MN-major: 128 K rows of 128 MN bytes).
+            // BF16: K-major atom j = K elements [(kb*KS + j)*64, +64); MN-major: the stage covers
+            // 128 K rows and atom j is MN elements [mn0 + 64j, +64).
+            const int k0 = BF ? (kb * KS + j) * 64 : (kb * KS + j) * BK;
+            const int kmn = BF ? kb * 128 : k0;          // K row of an MN-major box
+            const int am = BF ? m0 + 64 * j : m0, bn = BF ? n0 + 64 * j : n0;
             const uint32_t da = sa_dst + j * 16384, db = sb_dst + j * 16384;
             if (CG == 2) {
-              tma_load_2d_2sm(da, tmA, a_mn ? m0 : k0, a_mn ? k0 : m0, fb);
-              tma_load_2d_2sm(db, tmB, b_mn ? n0 : k0, b_mn ? k0 : n0, fb);
+              tma_load_2d_2sm(da, tmA, a_mn ? am : k0, a_mn ? kmn : m0, fb);
+              tma_load_2d_2sm(db, tmB, b_mn ? bn : k0, b_mn ? kmn : n0, fb);
             } else {
               tma_load_2d(da, tmA, a_mn ? m0 : k0, a_mn ? k0 : m0, fb, 0);
               if (b_mn) {
@@ -289,8 +295,9 @@ __global__ void __launch_bounds__(256, 1)
           // per K=32 step: K-major advances 32 B inside the 128-B swizzle row and jumps 16 KB
           // (1024 in 16-B units) to the next K atom every 4 steps; MN-major advances 32 K-rows
           // = 4 KB per step (atoms are contiguous)
+          // (BF16 MN-major: 16 K rows = 2 KB per step inside one MN atom; atoms are LBO = 16 KB apart)
           auto koff = [](int mn, int k) -> uint64_t {
-            return mn ? (uint64_t)(256 * k) : (uint64_t)(1024 * (k >> 2) + 2 * (k & 3));
+            return mn ? (uint64_t)((BF ? 128 : 256) * k) : (uint64_t)(1024 * (k >> 2) + 2 * (k & 3));
           };
 #pragma unroll
           for (int k = 0; k < KS * BK / 32; ++k) {
@@ -302,6 +309,8 @@ __global__ void __launch_bounds__(256, 1)
               const uint32_t sfa = tmem_base + L::sfa_col + 4 * t, sfb = tmem_base + L::sfb_col + 8 * t;
               if (CG == 2) mma_mxf8f6f4_cg2(d_tmem, ad, bd, id, acc_flag, sfa, sfb);
               else mma_mxf8f6f4(d_tmem, ad, bd, id, acc_flag, sfa, sfb);
+            } else if (BF) {
+              mma_f16_cg2(d_tmem, ad, bd, idesc, acc_flag);
             } else if (CG == 2) {
               mma_f8f6f4_cg2(d_tmem, ad, bd, idesc, acc_flag);
             } else {
@@ -414,15 +423,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // 2-D u8 tensor map with SWIZZLE_128B.  K-major operand [rows, K]: dims {K, rows}, box {BK, box_rows}.
 // MN-major operand stored [K, MN]: dims {MN, K}, box {128, BK}.
+// (BF16 operands: elements of 2 bytes, boxes of 64 elements = 128 bytes along the contiguous dim;
+//  ld is in elements and converted to bytes here)
 static bool make_operand_map(CUtensorMap* m, const uint8_t* ptr, bool mn_major, int64_t mn, int64_t K, int64_t ld,
-                             int box_rows) {
+                             int box_rows, bool bf16 = false) {
   auto enc = get_encode();
   if (!enc) return false;
+  const int es = bf16 ? 2 : 1;
+  const cuuint32_t inner = 128 / es;
   cuuint64_t dims[2] = {(cuuint64_t)(mn_major ? mn : K), (cuuint64_t)(mn_major ? K : mn)};
-  cuuint64_t strides[1] = {(cuuint64_t)ld};
-  cuuint32_t box[2] = {(cuuint32_t)(mn_major ? 128 : BK), (cuuint32_t)(mn_major ? BK : box_rows)};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * es};
+  cuuint32_t box[2] = {inner, (cuuint32_t)(mn_major ? BK : box_rows)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(ptr), dims, strides, box, estr,
+  CUresult r = enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                   const_cast<uint8_t*>(ptr), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -460,10 +474,10 @@ static bool make_sf_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool MX, int CG, int ST, int KS>
+template <bool MX, int CG, int ST, int KS, bool BF>
 static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
-  if (!make_operand_map(&maps[0], p.A, p.a_mn, p.M, p.K, p.lda, BM) ||
-      !make_operand_map(&maps[1], p.B, p.b_mn, p.N, p.K, p.ldb, BN / CG))
+  if (!make_operand_map(&maps[0], p.A, p.a_mn, p.M, p.K, p.lda, BM, BF) ||
+      !make_operand_map(&maps[1], p.B, p.b_mn, p.N, p.K, p.ldb, BN / CG, BF))
     return false;
   if (MX) {
     if (!make_sf_map(&maps[2], p.sa, p.M, p.K, KS) || !make_sf_map(&maps[3], p.sb, p.N, p.K, KS)) return false;
@@ -475,9 +489,11 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   P.M = (int)p.M; P.N = (int)p.N; P.K = (int)p.K;
   P.tiles_m = (int)((p.M + BM * CG - 1) / (BM * CG));
   P.tiles_n = (int)((p.N + BN - 1) / BN);
-  P.num_kb = (int)((p.K + BK * KS - 1) / (BK * KS));
-  P.idesc = MX ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN)
-               : make_idesc_f8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u);
+  const int k_per_stage = BF ? KS * 64 : KS * BK;   // elements
+  P.num_kb = (int)((p.K + k_per_stage - 1) / k_per_stage);
+  P.idesc = MX   ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN)
+            : BF ? make_idesc_bf16(BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u)
+                 : make_idesc_f8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u);
   P.a_mn = p.a_mn;
   P.b_mn = p.b_mn;
   if (MX) {
@@ -491,22 +507,22 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   return true;
 }
 
-template <bool MX, int CG, int ST, int KS>
+template <bool MX, int CG, int ST, int KS, bool BF = false>
 static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
-  using L = Layout<MX, CG, ST, KS>;
+  using L = Layout<MX, CG, ST, KS, BF>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
     attr_err =
-        cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG, ST, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
+        cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG, ST, KS, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
   });
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m0[4], m1[4];
   GemmArgs a{};
-  if (!setup_prob<MX, CG, ST, KS>(ps[0], a.p0, m0)) return cudaErrorInvalidValue;
+  if (!setup_prob<MX, CG, ST, KS, BF>(ps[0], a.p0, m0)) return cudaErrorInvalidValue;
   a.t1 = a.p0.tiles_m * a.p0.tiles_n;
   if (n > 1) {
-    if (!setup_prob<MX, CG, ST, KS>(ps[1], a.p1, m1)) return cudaErrorInvalidValue;
+    if (!setup_prob<MX, CG, ST, KS, BF>(ps[1], a.p1, m1)) return cudaErrorInvalidValue;
     a.num_tiles = a.t1 + a.p1.tiles_m * a.p1.tiles_n;
   } else {
     a.p1 = a.p0;
@@ -523,9 +539,9 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   }
   const int slots = num_sms() / CG;
   const int grid = CG * (a.num_tiles < slots ? a.num_tiles : slots);
-  LaunchScope ls(MX ? K_GEMM_MX : K_GEMM, st);
+  LaunchScope ls(MX ? K_GEMM_MX : (BF ? K_GEMM_BF16 : K_GEMM), st);
   if (CG == 1) {
-    fp8_gemm_kernel<MX, CG, ST, KS><<<grid, 256, L::bytes, st>>>(m0[0], m0[1], m0[2], m0[3], m1[0], m1[1], m1[2],
+    fp8_gemm_kernel<MX, CG, ST, KS, BF><<<grid, 256, L::bytes, st>>>(m0[0], m0[1], m0[2], m0[3], m1[0], m1[1], m1[2],
                                                                  m1[3], a);
   } else {
     cudaLaunchConfig_t cfg{};
@@ -540,7 +556,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS>, m0[0], m0[1], m0[2], m0[3], m1[0], m1[1],
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS, BF>, m0[0], m0[1], m0[2], m0[3], m1[0], m1[1],
                                        m1[2], m1[3], a);
     if (e != cudaSuccess) return e;
   }
@@ -551,6 +567,11 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
 cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st) {
   if (n < 1 || n > 2) return cudaErrorInvalidValue;
   if (n == 2 && ((ps[0].scale_mode == 2) != (ps[1].scale_mode == 2))) return cudaErrorInvalidValue;
+  if (ps[0].bf16_in) {
+    for (int i = 1; i < n; ++i)
+      if (!ps[i].bf16_in) return cudaErrorInvalidValue;
+    return launch_t<false, 2, 3, 2, true>(ps, n, st);
+  }
   const int cg = cta_group_for();
   if (ps[0].scale_mode == 2) return cg == 1 ? launch_t<true, 1, 4, 1>(ps, n, st) : launch_t<true, 2, 3, 2>(ps, n, st);
   if (cg == 1) return launch_t<false, 1, 4, 1>(ps, n, st);

@@ -8,7 +8,7 @@ namespace fp8t {
 void count_launch();
 
 // Launch accounting + optional per-launch CUDA-event timing (fp8_profile_enable).
-enum { K_AMAX = 0, K_CAST = 1, K_MX = 2, K_TRANSPOSE = 3, K_GEMM = 4, K_GEMM_MX = 5 };
+enum { K_AMAX = 0, K_CAST = 1, K_MX = 2, K_TRANSPOSE = 3, K_GEMM = 4, K_GEMM_MX = 5, K_GEMM_BF16 = 6 };
 struct LaunchScope {
   int slot;
   cudaStream_t st;
@@ -39,6 +39,7 @@ struct GemmProblem {
   int scale_mode;
   int64_t M, N, K, lda, ldb;
   void* D; int out_f32; int64_t ldd;
+  int bf16_in = 0;     // 1: A and B are BF16 (kind::f16, no scales; rowwise_gw_hp dW)
 };
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st);
 // Two problems of the same kind on one persistent launch (tiles of ps[0] then ps[1]).

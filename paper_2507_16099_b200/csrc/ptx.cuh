@@ -221,6 +221,16 @@ __device__ __forceinline__ void mma_mxf8f6f4_cg2(uint32_t tmem_d, uint64_t adesc
 __device__ __forceinline__ void tmem_cp_32x128b_warpx4_cg2(uint32_t taddr, uint64_t sdesc) {
   asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
 }
+// BF16 x BF16 -> FP32 over a CTA pair (kind::f16, K = 16 per instruction).
+__device__ __forceinline__ void mma_f16_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // Arrive on the mbarrier at the same offset in every CTA of `mask` once the pair's MMAs complete.
 __device__ __forceinline__ void mma_commit_cg2_mc(uint32_t bar, uint16_t mask) {
   asm volatile(
@@ -276,6 +286,10 @@ __host__ __device__ constexpr uint32_t make_idesc_f8f6f4(uint32_t a_fmt, uint32_
          | (b_mn << 16)         // b_major
          | ((N >> 3) << 17)     // n_dim
          | ((M >> 4) << 24);    // m_dim
+}
+// kind::f16 instruction descriptor with BF16 A/B (format 1), F32 accumulate.
+__host__ __device__ constexpr uint32_t make_idesc_bf16(uint32_t M, uint32_t N, uint32_t a_mn, uint32_t b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 // kind::mxf8f6f4.block_scale descriptor: scale_format = UE8M0, sf ids set per MMA.
 __host__ __device__ constexpr uint32_t make_idesc_mxf8f6f4(uint32_t a_fmt, uint32_t b_fmt, uint32_t M, uint32_t N) {

@@ -35,14 +35,17 @@ class _Float8LinearFn(torch.autograd.Function):
         N = w.shape[0]
         plan = _PLANS.get(M, N, K, recipe, torch.bfloat16, x2d.device)
         saved = plan.new_saved(x2d.device)
-        y = plan.forward(x2d.contiguous(), w.contiguous(), saved)
+        x2d = x2d.contiguous()
+        y = plan.forward(x2d, w.contiguous(), saved)
         ctx.plan, ctx.buf, ctx.wdtype = plan, saved, w.dtype
+        # rowwise_gw_hp keeps dL/dW in bf16: its dW GEMM reads the hp input
+        ctx.x = x2d if recipe == "rowwise_gw_hp" else None
         return y
 
     @staticmethod
     def backward(ctx, dy):
         dx, dw = ctx.plan.backward(dy.contiguous(), ctx.buf, want_dx=ctx.needs_input_grad[0],
-                                   want_dw=ctx.needs_input_grad[1])
+                                   want_dw=ctx.needs_input_grad[1], x=ctx.x)
         if dw is not None and dw.dtype != ctx.wdtype:
             dw = dw.to(ctx.wdtype)
         return dx, dw, None

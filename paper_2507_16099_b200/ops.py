@@ -14,7 +14,8 @@ from . import _lib as L
 FORMATS = {"e4m3": L.E4M3, "e5m2": L.E5M2}
 GRANS = {"tensor": L.GRAN_TENSOR, "row": L.GRAN_ROW, "col": L.GRAN_COL, "row_col": L.GRAN_ROW_COL,
          "mx32": L.GRAN_MX32}
-RECIPES = {"tensorwise": L.RECIPE_TENSORWISE, "rowwise": L.RECIPE_ROWWISE, "mxfp8": L.RECIPE_MXFP8}
+RECIPES = {"tensorwise": L.RECIPE_TENSORWISE, "rowwise": L.RECIPE_ROWWISE, "mxfp8": L.RECIPE_MXFP8,
+           "rowwise_gw_hp": L.RECIPE_ROWWISE_GW_HP}
 MX_ROUND = {"floor": L.MX_FLOOR, "rceil": L.MX_RCEIL}
 
 
@@ -143,14 +144,16 @@ class LinearPlan:
                                      _ptr(y), _ptr(saved), _ptr(ws), wsb, _stream(stream)), "fp8_linear_fwd")
         return y
 
-    def backward(self, dy, saved, dx=None, dw=None, want_dx=True, want_dw=True, w_fp8=None, stream=None):
+    def backward(self, dy, saved, dx=None, dw=None, want_dx=True, want_dw=True, w_fp8=None, x=None, stream=None):
+        """x: the forward input (read by rowwise_gw_hp's BF16 dW GEMM only)."""
         dev = dy.device
         if want_dx and dx is None:
             dx = torch.empty((self.M, self.K), dtype=self.out_dtype, device=dev)
         if want_dw and dw is None:
             dw = torch.empty((self.N, self.K), dtype=self.out_dtype, device=dev)
         wq = self._wq(w_fp8)
-        L.check(L.lib.fp8_linear_bwd(ctypes.byref(self.cfg), hp(dy), self.K, _ptr(saved),
+        xh = hp(x) if x is not None else L.HP(None, L.DT_BF16, self.M, self.K, self.K)
+        L.check(L.lib.fp8_linear_bwd(ctypes.byref(self.cfg), hp(dy), xh, _ptr(saved),
                                      ctypes.byref(wq) if wq else None,
                                      _ptr(dx) if want_dx else None, _ptr(dw) if want_dw else None,
                                      _ptr(self.ws), self.ws_bytes, _stream(stream)), "fp8_linear_bwd")

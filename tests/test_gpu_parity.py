@@ -316,6 +316,8 @@ def test_gemm_mx_integer_grid_exact(cta_group):
     ("tensorwise", "c2", 400, 272, 528),
     ("rowwise", "c3", 384, 400, 272),
     ("mxfp8", "c4", 256, 384, 512),
+    ("rowwise_gw_hp", "c3", 384, 400, 272),
+    ("rowwise_gw_hp", "c2", 1024, 768, 512),
 ])
 def test_linear_fwd_bwd(recipe, cfg, M, N, K):
     x, w, dy = synth.linear_inputs(cfg, M, N, K, seed=0)
@@ -324,8 +326,9 @@ def test_linear_fwd_bwd(recipe, cfg, M, N, K):
     dx, dxb, dw, dwb, _ = olin.backward(x, w, dy, recipe)
     plan = ops.LinearPlan(M, N, K, recipe=recipe, out_dtype=torch.float32)
     saved = plan.new_saved()
-    Y = plan.forward(_dev(x, dt), _dev(w, dt), saved)
-    DX, DW = plan.backward(_dev(dy, dt), saved)
+    X = _dev(x, dt)
+    Y = plan.forward(X, _dev(w, dt), saved)
+    DX, DW = plan.backward(_dev(dy, dt), saved, x=X)
     torch.cuda.synchronize()
     _tol_check(_np(Y).astype(np.float64), y, yb)
     _tol_check(_np(DX).astype(np.float64), dx, dxb)

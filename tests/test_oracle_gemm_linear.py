@@ -162,3 +162,14 @@ def test_fsdp_gather_equals_unsharded_cast(P):
     q, s, a = fsdp.allgather_ref(shards, E4M3)
     q1, s1, a1 = fp8.cast_tensorwise(w, E4M3)
     assert np.array_equal(q, q1) and s == s1 and a == a1
+
+
+def test_rowwise_gw_hp_weight_grad_is_high_precision():
+    # S:300-301 "RowwiseGwHp grad_weight = gemm_ref(grad_out^T, x) bit-exactly" (no FP8 casting);
+    # its grad_input equals the rowwise recipe's (same casts, "like rowwise").
+    x, w, dy = synth.linear_inputs("c3", 48, 40, 64, seed=2)
+    dx_r, _, _, _, _ = linear.backward(x, w, dy, linear.ROWWISE)
+    dx_h, _, dw_h, _, _ = linear.backward(x, w, dy, linear.ROWWISE_GW_HP)
+    assert np.array_equal(dx_h, dx_r)
+    want = _frac_gemm(dy.T, x.T, np.ones(40, np.float32), np.ones(64, np.float32))
+    np.testing.assert_allclose(dw_h, want, rtol=1e-12)
