@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bf16", action="store_true")
     ap.add_argument("--fsdp", action="store_true",
@@ -370,32 +370,83 @@ def run_ours(a):
     step_gemm_share = sum(gemm_ms) / a.steps / ms_step if ms_step > 0 else None
 
     # ---------------- end-to-end through the public API with host buffers ----------------
+    # Every step copies its inputs (X, W, dY) from pinned host memory and its outputs (Y, dX, dW)
+    # back, inside the timed region.  Copies run on their own streams, double-buffered against the
+    # compute stream (inputs of step i+1 and outputs of step i-1 move while step i computes), i.e.
+    # the steady state of a training loop that streams its batches.
     e2e = None
     if a.e2e_steps > 0:
         xh = x.cpu().pin_memory()
         wh = w_shard.cpu().pin_memory()
         gh = dy.cpu().pin_memory()
+        dw_out = dw if not fsdp else dw_shard
         yh = torch.empty_like(y, device="cpu").pin_memory()
         dxh = torch.empty_like(dx, device="cpu").pin_memory()
-        dwh = torch.empty_like(dw if not fsdp else dw_shard, device="cpu").pin_memory()
-        xd, wd, gd = torch.empty_like(x), torch.empty_like(w_shard), torch.empty_like(dy)
+        dwh = torch.empty_like(dw_out, device="cpu").pin_memory()
+        ins = [(torch.empty_like(x), torch.empty_like(w_shard), torch.empty_like(dy)) for _ in range(2)]
+        outs = [(torch.empty_like(y), torch.empty_like(dx), torch.empty_like(dw_out)) for _ in range(2)]
+        s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_used = [torch.cuda.Event() for _ in range(2)]     # compute done with the set's inputs
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        ev_read = [torch.cuda.Event() for _ in range(2)]     # D2H done with the set's outputs
 
-        def e2e_step():
-            xd.copy_(xh, non_blocking=True)
-            wd.copy_(wh, non_blocking=True)
-            gd.copy_(gh, non_blocking=True)
-            step(xd, wd, gd)
-            yh.copy_(y, non_blocking=True)
-            dxh.copy_(dx, non_blocking=True)
-            dwh.copy_(dw if not fsdp else dw_shard, non_blocking=True)
+        def copy_in(i):
+            b = i % 2
+            with torch.cuda.stream(s_h2d):
+                if i >= 2:
+                    s_h2d.wait_event(ev_used[b])
+                for d_, h_ in zip(ins[b], (xh, wh, gh)):
+                    d_.copy_(h_, non_blocking=True)
+                ev_in[b].record(s_h2d)
 
-        e2e_step()
+        def compute(i):
+            b = i % 2
+            stream.wait_event(ev_in[b])
+            if i >= 2:
+                stream.wait_event(ev_read[b])
+            xd, wd, gd = ins[b]
+            yo, dxo, dwo = outs[b]
+            if fsdp:
+                comm.allgather_fp8(wd, "e4m3", out=w_full, scale=w_scale, amax=w_amax)
+                plan.forward(xd, None, saved, y=yo, w_fp8=(w_full, w_scale))
+                plan.backward(gd, saved, dx=dxo, dw=dw, w_fp8=(w_full, w_scale))
+                if world > 1:
+                    dist.reduce_scatter_tensor(dwo, dw)
+                else:
+                    dwo.copy_(dw)
+            else:
+                plan.forward(xd, wd, saved, y=yo)
+                plan.backward(gd, saved, dx=dxo, dw=dwo, x=xd)
+            ev_used[b].record(stream)
+            ev_out[b].record(stream)
+
+        def copy_out(i):
+            b = i % 2
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev_out[b])
+                for h_, d_ in zip((yh, dxh, dwh), outs[b]):
+                    h_.copy_(d_, non_blocking=True)
+                ev_read[b].record(s_d2h)
+
+        def run(n):
+            copy_in(0)
+            for i in range(n):
+                if i + 1 < n:
+                    copy_in(i + 1)
+                compute(i)
+                copy_out(i)
+            ev_last = torch.cuda.Event()
+            ev_last.record(s_d2h)
+            stream.wait_event(ev_last)
+
+        run(2)
         torch.cuda.synchronize()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(a.e2e_steps):
-            e2e_step()
+        s_h2d.wait_event(e0)
+        run(a.e2e_steps)
         e1.record(stream)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
@@ -404,10 +455,11 @@ def run_ours(a):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         h2d = (x.numel() + w_shard.numel() + dy.numel()) * 2
-        d2h = (y.numel() + dx.numel() + dwh.numel()) * 2
+        d2h = (y.numel() + dx.numel() + dw_out.numel()) * 2
         e2e = {"value": flops_step * a.e2e_steps * world / (ems / 1e3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ems / a.e2e_steps,
-               "path": "pinned host -> device copies + fp8_linear_fwd/bwd (C-ABI) + device -> host copies"}
+               "path": "pinned host -> device copies of X, W, dY + fp8_linear_fwd/bwd (C-ABI) + device -> host "
+                       "copies of Y, dX, dW, every step; copies on separate streams, double-buffered"}
 
     # ---------------- cuBLAS BF16 linear of the same shape (context) ----------------
     bf16 = None
