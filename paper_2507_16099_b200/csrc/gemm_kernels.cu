@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
   tc_fence_before();
-  if (CG == 2) cluster_sync(); else __syncthreads();
+  if (CG == 2) cluster_sync();   // barrier inits and the pair's TMEM allocation visible cluster-wide
+  __syncthreads();               // (also the CTA-level barrier racecheck models for the smem slot)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
