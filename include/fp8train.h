@@ -222,6 +222,17 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
                             const fp8_tensor_t* w_fp8, void* y, void* saved,
                             void* ws, size_t ws_bytes, void* stream);
 
+/* Forward with amax hand-over ("amax out of the critical path"; the
+ * dynamic-quantisation overhead of PAPER.md:284-287):
+ *   x_amax (nullable, device float[1], tensorwise only): amax(|X|) already known -- e.g. written
+ *     by the epilogue of the GEMM that produced X -- so the X amax pass is skipped;
+ *   y_amax (nullable, device float[1], any recipe): the GEMM epilogue writes amax(|Y|) of the
+ *     stored (out_dtype-rounded) outputs, ready to be the next layer's x_amax.
+ * fp8_linear_fwd(...) == fp8_linear_fwd_ex(..., x_amax = NULL, ..., y_amax = NULL, ...). */
+fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const float* x_amax, fp8_hp_t w,
+                               const fp8_tensor_t* w_fp8, void* y, float* y_amax, void* saved,
+                               void* ws, size_t ws_bytes, void* stream);
+
 /* Float8Linear backward: dX = dY W and dW = dY^T X (S:289-299 notation):
  *   tensorwise: dY one scale, reuse X/W scales; rowwise: dY per row for dX and
  *   per column for dW, W per column, X per column ("rows of the left
@@ -238,6 +249,11 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
 fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x,
                             const void* saved, const fp8_tensor_t* w_fp8, void* dx, void* dw,
                             void* ws, size_t ws_bytes, void* stream);
+/* Backward with amax hand-over: dy_amax (tensorwise only) skips the dY amax pass; dx_amax gets
+ * amax(|dX|) from the dX GEMM epilogue (the previous layer's dy_amax).  May share a buffer. */
+fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
+                               const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax,
+                               void* dw, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * FSDP2-style FP8 weight all-gather (PAPER.md:596 enable_fp8_all_gather;

@@ -449,6 +449,12 @@ size_t fp8_linear_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_
 
 fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w, const fp8_tensor_t* w_fp8,
                             void* y, void* saved, void* ws, size_t ws_bytes, void* stream) {
+  return fp8_linear_fwd_ex(cfg, x, nullptr, w, w_fp8, y, nullptr, saved, ws, ws_bytes, stream);
+}
+
+fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const float* x_amax, fp8_hp_t w,
+                               const fp8_tensor_t* w_fp8, void* y, float* y_amax, void* saved, void* ws,
+                               size_t ws_bytes, void* stream) {
   FP8T_TRY(check_hp(x, "x"));
   FP8T_TRY(check_hp(w, "w", w_fp8 == nullptr));
   const int64_t M = x.rows, K = x.cols, N = w.rows;
@@ -466,10 +472,14 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
     FP8T_TRY(check_ptr(w_fp8->q, "w_fp8->q"));
     if (!w_fp8->scale) return fail(FP8_EINVAL, "w_fp8->scale: null pointer");
   }
+  if (x_amax && cfg->recipe != FP8_RECIPE_TENSORWISE)
+    return fail(FP8_EUNSUPPORTED, "x_amax (precomputed tensor amax) needs the tensorwise recipe");
   cudaStream_t st = S(stream);
   const bool xb = x.dtype == FP8_DT_BF16, wb = w.dtype == FP8_DT_BF16;
   const int ff = cfg->fmt_fwd;
   const int of32 = cfg->out_dtype == FP8_DT_F32;
+  uint32_t* yam = reinterpret_cast<uint32_t*>(y_amax);
+  if (yam) FP8T_CUDA(cudaMemsetAsync(yam, 0, 4, st), "memset y_amax");
 
   if (!saved) {
     // forward-only FP8 (inference / float8 dynamic activation + weight, PAPER.md:470-471, 636:
@@ -478,9 +488,9 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
     if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
       uint32_t* ax = reinterpret_cast<uint32_t*>(iw.amax);
       FP8T_CUDA(cudaMemsetAsync(ax, 0, 8, st), "memset");
-      FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
-      FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 1, 0, iw.amax, iw.amax, iw.xq, nullptr, (float*)iw.sx, nullptr,
-                            st),
+      if (!x_amax) FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
+      const float* axp = x_amax ? x_amax : iw.amax;
+      FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 1, 0, axp, axp, iw.xq, nullptr, (float*)iw.sx, nullptr, st),
                 "cast x");
       const uint8_t* wq = iw.wq;
       const void* swp = iw.sw;
@@ -493,7 +503,7 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
                               (float*)iw.sw, nullptr, st),
                   "cast w");
       }
-      GemmProblem p{iw.xq, wq, ff, ff, 0, 0, iw.sx, swp, 0, M, N, K, K, K, y, of32, N};
+      GemmProblem p{iw.xq, wq, ff, ff, 0, 0, iw.sx, swp, 0, M, N, K, K, K, y, of32, N, 0, yam};
       FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
     } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {   // PerRow
       float* axr = iw.amax;
@@ -505,13 +515,13 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
                 "cast x");
       FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 0, awr, awr, iw.wq, nullptr, (float*)iw.sw, nullptr, st),
                 "cast w");
-      GemmProblem p{iw.xq, iw.wq, ff, ff, 0, 0, iw.sx, iw.sw, 1, M, N, K, K, K, y, of32, N};
+      GemmProblem p{iw.xq, iw.wq, ff, ff, 0, 0, iw.sx, iw.sw, 1, M, N, K, K, K, y, of32, N, 0, yam};
       FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
     } else {   // MXFP8: dim0 only
       const bool rc = cfg->mx_round == FP8_MX_RCEIL;
       FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, iw.xq, (uint8_t*)iw.sx, nullptr, nullptr, st), "mx x");
       FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, iw.wq, (uint8_t*)iw.sw, nullptr, nullptr, st), "mx w");
-      GemmProblem p{iw.xq, iw.wq, ff, ff, 0, 0, iw.sx, iw.sw, 2, M, N, K, K, K, y, of32, N};
+      GemmProblem p{iw.xq, iw.wq, ff, ff, 0, 0, iw.sx, iw.sw, 2, M, N, K, K, K, y, of32, N, 0, yam};
       FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
     }
     return FP8_OK;
@@ -525,9 +535,10 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
     uint32_t* ax = reinterpret_cast<uint32_t*>(fw.amax);
     uint32_t* aw = ax + 1;
     FP8T_CUDA(cudaMemsetAsync(ax, 0, 8, st), "memset");
-    FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
-    FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 1, 0, fw.amax, fw.amax, sv.xT, nullptr, (float*)sv.sx,
-                          nullptr, st),
+    // x_amax: amax(X) precomputed by X's producer (e.g. the previous layer's epilogue) -> no amax pass
+    if (!x_amax) FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
+    const float* axp = x_amax ? x_amax : fw.amax;
+    FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 1, 0, axp, axp, sv.xT, nullptr, (float*)sv.sx, nullptr, st),
               "cast x");
     const uint8_t* wq = sv.wT;
     if (w_fp8) {
@@ -539,7 +550,7 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
                             (float*)sv.sw, nullptr, st),
                 "cast w");
     }
-    GemmProblem p{sv.xT, wq, ff, ff, 0, 0, sv.sx, sv.sw, 0, M, N, K, K, K, y, of32, N};
+    GemmProblem p{sv.xT, wq, ff, ff, 0, 0, sv.sx, sv.sw, 0, M, N, K, K, K, y, of32, N, 0, yam};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
   } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {
     const bool gw_hp = cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;   // X's column-scaled copy unused
@@ -558,13 +569,13 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
               "cast x");
     FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 5, awr, awc, fw.wq, sv.wT, fw.swr, (float*)sv.sw, st),
               "cast w");
-    GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N};
+    GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N, 0, yam};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
   } else {
     const bool rc = cfg->mx_round == FP8_MX_RCEIL;
     FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, fw.xq, fw.sfx, sv.xT, (uint8_t*)sv.sx, st), "mx cast x");
     FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, fw.wq, fw.sfw, sv.wT, (uint8_t*)sv.sw, st), "mx cast w");
-    GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sfx, fw.sfw, 2, M, N, K, K, K, y, of32, N};
+    GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sfx, fw.sfw, 2, M, N, K, K, K, y, of32, N, 0, yam};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
   }
   return FP8_OK;
@@ -572,6 +583,12 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
 
 fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x, const void* saved,
                             const fp8_tensor_t* w_fp8, void* dx, void* dw, void* ws, size_t ws_bytes, void* stream) {
+  return fp8_linear_bwd_ex(cfg, dy, nullptr, x, saved, w_fp8, dx, nullptr, dw, ws, ws_bytes, stream);
+}
+
+fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
+                               const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax, void* dw,
+                               void* ws, size_t ws_bytes, void* stream) {
   FP8T_TRY(check_hp(dy, "dy"));
   const int64_t M = dy.rows, N = dy.cols, K = x.cols;
   const bool gw_hp = cfg && cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;
@@ -590,19 +607,24 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x
     if (w_fp8->rows != N || w_fp8->cols != K) return fail(FP8_EINVAL, "w_fp8 shape");
     FP8T_TRY(check_ptr(w_fp8->q, "w_fp8->q"));
   }
+  if (dy_amax && cfg->recipe != FP8_RECIPE_TENSORWISE)
+    return fail(FP8_EUNSUPPORTED, "dy_amax (precomputed tensor amax) needs the tensorwise recipe");
   cudaStream_t st = S(stream);
   const bool gb = dy.dtype == FP8_DT_BF16;
   const int ff = cfg->fmt_fwd, fg = cfg->fmt_grad;
+  uint32_t* dxam = dx ? reinterpret_cast<uint32_t*>(dx_amax) : nullptr;
   Saved sv = carve_saved(cfg, M, N, K, const_cast<void*>(saved), nullptr);
   BwdWs bw = carve_bwd(cfg, M, N, ws, nullptr);
   const int of32 = cfg->out_dtype == FP8_DT_F32;
   int mode;
   if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
     mode = 0;
-    FP8T_CUDA(cudaMemsetAsync(bw.amax, 0, 4, st), "memset");
-    FP8T_CUDA(launch_amax(dy.ptr, gb, M, N, dy.ld, 1, (uint32_t*)bw.amax, nullptr, nullptr, st), "amax dy");
-    FP8T_CUDA(launch_cast(dy.ptr, gb, fg, M, N, dy.ld, 1, 0, bw.amax, bw.amax, bw.g, nullptr, (float*)bw.sg,
-                          nullptr, st),
+    if (!dy_amax) {
+      FP8T_CUDA(cudaMemsetAsync(bw.amax, 0, 4, st), "memset");
+      FP8T_CUDA(launch_amax(dy.ptr, gb, M, N, dy.ld, 1, (uint32_t*)bw.amax, nullptr, nullptr, st), "amax dy");
+    }
+    const float* agp = dy_amax ? dy_amax : bw.amax;
+    FP8T_CUDA(launch_cast(dy.ptr, gb, fg, M, N, dy.ld, 1, 0, agp, agp, bw.g, nullptr, (float*)bw.sg, nullptr, st),
               "cast dy");
   } else if (cfg->recipe == FP8_RECIPE_ROWWISE || gw_hp) {
     mode = 1;
@@ -625,11 +647,13 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x
   }
 gemms:
   if (!dx && !dw) return FP8_OK;
+  // zeroed after the dY cast has read dy_amax, so the two may share a buffer
+  if (dxam) FP8T_CUDA(cudaMemsetAsync(dxam, 0, 4, st), "memset dx_amax");
   if (gw_hp) {
     // dX in FP8 (row-scaled dY x column-scaled W, read MN-major); dW = dY^T X in BF16 on the
     // high-precision operands (both row-major [M, .] -> MN-major)
     if (dx) {
-      GemmProblem p{bw.g, sv.wT, fg, ff, 0, 1, bw.sg, sv.sw, 1, M, K, N, N, K, dx, of32, K};
+      GemmProblem p{bw.g, sv.wT, fg, ff, 0, 1, bw.sg, sv.sw, 1, M, K, N, N, K, dx, of32, K, 0, dxam};
       FP8T_CUDA(launch_gemm(p, st), "gemm dx");
     }
     if (dw) {
@@ -646,19 +670,19 @@ gemms:
     // tensorwise: operands are the row-major codes; B of dX and both operands of dW are MN-major
     const uint8_t* wq = w_fp8 ? w_fp8->q : sv.wT;
     // dX[M,K] = dY[M,N] . W[N,K]: A = Gq K-major over N, B = Wq stored [N,K] = MN-major
-    if (dx) ps[n++] = GemmProblem{bw.g, wq, fg, ff, 0, 1, bw.sg, sv.sw, 0, M, K, N, N, K, dx, of32, K};
+    if (dx) ps[n++] = GemmProblem{bw.g, wq, fg, ff, 0, 1, bw.sg, sv.sw, 0, M, K, N, N, K, dx, of32, K, 0, dxam};
     // dW[N,K] = dY^T . X: A = Gq stored [M,N] = MN-major, B = Xq stored [M,K] = MN-major
     if (dw) ps[n++] = GemmProblem{bw.g, sv.xT, fg, ff, 1, 1, bw.sg, sv.sx, 0, N, K, M, N, K, dw, of32, K};
   } else if (mode == 1) {
     // rowwise: column-scaled copies are row-major too -> read MN-major
     // dX[M,K] = dY_r[M,N] . W_c[N,K]: A K-major over N, B stored [N,K] = MN-major
-    if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 1, bw.sg, sv.sw, mode, M, K, N, N, K, dx, of32, K};
+    if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 1, bw.sg, sv.sw, mode, M, K, N, N, K, dx, of32, K, 0, dxam};
     // dW[N,K] = dY_c^T . X_c: A stored [M,N] = MN-major, B stored [M,K] = MN-major
     if (dw) ps[n++] = GemmProblem{bw.gT, sv.xT, fg, ff, 1, 1, bw.sgT, sv.sx, mode, N, K, M, N, K, dw, of32, K};
   } else {
     // MXFP8: dim1 copies are transposed (blocks along the contraction dim), K-major
     // dX[M,K] = dY[M,N] . W  : A = dY (K-major over N), B = W^T [K,N]
-    if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 0, bw.sg, sv.sw, mode, M, K, N, N, N, dx, of32, K};
+    if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 0, bw.sg, sv.sw, mode, M, K, N, N, N, dx, of32, K, 0, dxam};
     // dW[N,K] = dY^T[N,M] . X : A = dY^T [N,M], B = X^T [K,M]
     if (dw) ps[n++] = GemmProblem{bw.gT, sv.xT, fg, ff, 0, 0, bw.sgT, sv.sx, mode, N, K, M, M, M, dw, of32, K};
   }

@@ -53,6 +53,7 @@ struct Prob {
   void* D; int64_t ldd;
   int out_f32, row_scales;
   int a_mn, b_mn;     // operand majors (MN-major: TMA boxes 128 MN x 128 K, K step 4 KB)
+  uint32_t* out_amax; // optional: atomicMax of |D| bit patterns (amax of the stored output values)
 };
 // A launch processes the tiles of p0 ([0, t1)) then p1 ([t1, num_tiles)) on one persistent grid:
 // the backward's dX and dW GEMMs share one launch, so neither has its own wave-quantisation tail.
@@ -348,6 +349,7 @@ __global__ void __launch_bounds__(256, 1)
       float rs = 1.f;
       if (!row_scales && P.sa) rs = __frcp_rn(P.sa[0]) * __frcp_rn(P.sb[0]);
       if (row_scales && rvalid) rs = __frcp_rn(P.sa[row]);
+      uint32_t dmax = 0;   // |D| max over this thread's stored values (fp32 bit patterns)
       mbar_wait(tfull_bar + 8 * acc, acc_phase);
       tc_fence_after();
 #pragma unroll 1
@@ -372,6 +374,11 @@ __global__ void __launch_bounds__(256, 1)
         if (!rvalid) continue;
         if (out_f32) {
           float* dst = reinterpret_cast<float*>(P.D) + (int64_t)row * P.ldd + col0;
+          if (P.out_amax) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < nvalid) dmax = max(dmax, __float_as_uint(v[j]) & 0x7FFFFFFFu);
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             if (4 * j < nvalid)
@@ -384,11 +391,22 @@ __global__ void __launch_bounds__(256, 1)
             pk[j] = *reinterpret_cast<uint32_t*>(&h);
           }
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(P.D) + (int64_t)row * P.ldd + col0;
+          if (P.out_amax) {   // amax of the bf16-rounded outputs (what a consumer reads)
+            uint32_t m2 = 0;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (2 * j < nvalid) m2 = __vmaxu2(m2, pk[j] & 0x7FFF7FFFu);
+            dmax = max(dmax, max(m2 & 0xFFFFu, m2 >> 16) << 16);
+          }
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             if (8 * j < nvalid)
               reinterpret_cast<uint4*>(dst)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         }
+      }
+      if (P.out_amax) {   // (P is uniform across the CTA; every lane reaches this point)
+        dmax = __reduce_max_sync(0xffffffffu, dmax);
+        if (lane == 0 && dmax) atomicMax(P.out_amax, dmax);
       }
       tc_fence_before();
       if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * acc);
@@ -505,6 +523,7 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
     P.row_scales = p.scale_mode == 1;
   }
   P.D = p.D; P.ldd = p.ldd; P.out_f32 = p.out_f32;
+  P.out_amax = p.out_amax;
   return true;
 }
 

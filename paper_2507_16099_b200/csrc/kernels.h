@@ -40,6 +40,7 @@ struct GemmProblem {
   int64_t M, N, K, lda, ldb;
   void* D; int out_f32; int64_t ldd;
   int bf16_in = 0;     // 1: A and B are BF16 (kind::f16, no scales; rowwise_gw_hp dW)
+  uint32_t* out_amax = nullptr;  // optional epilogue amax of |D| (pre-zeroed u32 accumulator)
 };
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st);
 // Two problems of the same kind on one persistent launch (tiles of ps[0] then ps[1]).

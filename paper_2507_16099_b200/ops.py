@@ -128,9 +128,11 @@ class LinearPlan:
         return L.Tensor8(q.data_ptr(), None, s.data_ptr(), None, None, None, self.cfg.fmt_fwd, L.GRAN_TENSOR,
                          self.N, self.K)
 
-    def forward(self, x, w, saved, y=None, w_fp8=None, stream=None):
+    def forward(self, x, w, saved, y=None, w_fp8=None, x_amax=None, y_amax=None, stream=None):
         """w_fp8: optional (codes [N,K] uint8, scale float[1]) pre-cast weight (FSDP FP8 gather).
-        saved=None: forward-only (inference) -- nothing is kept for a backward."""
+        saved=None: forward-only (inference) -- nothing is kept for a backward.
+        x_amax: optional precomputed amax(|X|) (float[1]); y_amax: optional float[1] that receives
+        amax(|Y|) from the GEMM epilogue."""
         if y is None:
             y = torch.empty((self.M, self.N), dtype=self.out_dtype, device=x.device)
         wq = self._wq(w_fp8)
@@ -140,12 +142,15 @@ class LinearPlan:
             wsb = L.lib.fp8_linear_infer_workspace_bytes(ctypes.byref(self.cfg), self.M, self.N, self.K)
             if wsb > self.ws_bytes:
                 ws = torch.empty(wsb, dtype=torch.uint8, device=x.device)
-        L.check(L.lib.fp8_linear_fwd(ctypes.byref(self.cfg), hp(x), wh, ctypes.byref(wq) if wq else None,
-                                     _ptr(y), _ptr(saved), _ptr(ws), wsb, _stream(stream)), "fp8_linear_fwd")
+        L.check(L.lib.fp8_linear_fwd_ex(ctypes.byref(self.cfg), hp(x), _ptr(x_amax), wh,
+                                        ctypes.byref(wq) if wq else None, _ptr(y), _ptr(y_amax), _ptr(saved),
+                                        _ptr(ws), wsb, _stream(stream)), "fp8_linear_fwd_ex")
         return y
 
-    def backward(self, dy, saved, dx=None, dw=None, want_dx=True, want_dw=True, w_fp8=None, x=None, stream=None):
-        """x: the forward input (read by rowwise_gw_hp's BF16 dW GEMM only)."""
+    def backward(self, dy, saved, dx=None, dw=None, want_dx=True, want_dw=True, w_fp8=None, x=None,
+                 dy_amax=None, dx_amax=None, stream=None):
+        """x: the forward input (read by rowwise_gw_hp's BF16 dW GEMM only); dy_amax / dx_amax: amax
+        hand-over as in forward()."""
         dev = dy.device
         if want_dx and dx is None:
             dx = torch.empty((self.M, self.K), dtype=self.out_dtype, device=dev)
@@ -153,10 +158,10 @@ class LinearPlan:
             dw = torch.empty((self.N, self.K), dtype=self.out_dtype, device=dev)
         wq = self._wq(w_fp8)
         xh = hp(x) if x is not None else L.HP(None, L.DT_BF16, self.M, self.K, self.K)
-        L.check(L.lib.fp8_linear_bwd(ctypes.byref(self.cfg), hp(dy), xh, _ptr(saved),
-                                     ctypes.byref(wq) if wq else None,
-                                     _ptr(dx) if want_dx else None, _ptr(dw) if want_dw else None,
-                                     _ptr(self.ws), self.ws_bytes, _stream(stream)), "fp8_linear_bwd")
+        L.check(L.lib.fp8_linear_bwd_ex(ctypes.byref(self.cfg), hp(dy), _ptr(dy_amax), xh, _ptr(saved),
+                                        ctypes.byref(wq) if wq else None, _ptr(dx) if want_dx else None,
+                                        _ptr(dx_amax), _ptr(dw) if want_dw else None, _ptr(self.ws), self.ws_bytes,
+                                        _stream(stream)), "fp8_linear_bwd_ex")
         return dx, dw
 
 

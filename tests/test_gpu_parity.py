@@ -425,3 +425,32 @@ def test_linear_forward_only_inference(recipe, cfg, M, N, K):
     torch.cuda.synchronize()
     assert torch.equal(y_inf, y_trn)
     _tol_check(_np(y_inf).astype(np.float64), y, yb)
+
+
+def test_amax_handover_chain():
+    """f2: the fwd GEMM epilogue's amax(|Y|) feeds the next layer's cast (its amax pass skipped):
+    identical results to recomputing it; and the bwd epilogue's amax(|dX|) likewise."""
+    M, N, K = 512, 384, 256
+    x, w1, dy = synth.linear_inputs("c2", M, N, K, seed=5)
+    w2 = synth.tensor_c2("w", (K, N), seed=6)
+    X, W1, W2 = _dev(x, torch.bfloat16), _dev(w1, torch.bfloat16), _dev(w2, torch.bfloat16)
+    p1 = ops.LinearPlan(M, N, K, recipe="tensorwise")
+    p2 = ops.LinearPlan(M, K, N, recipe="tensorwise")
+    y_amax = torch.empty(1, device="cuda")
+    Y1 = p1.forward(X, W1, p1.new_saved(), y_amax=y_amax)
+    torch.cuda.synchronize()
+    assert y_amax.item() == Y1.float().abs().max().item()
+    s_a, s_b = p2.new_saved(), p2.new_saved()
+    Y2a = p2.forward(Y1, W2, s_a).clone()
+    Y2b = p2.forward(Y1, W2, s_b, x_amax=y_amax)
+    torch.cuda.synchronize()
+    assert torch.equal(Y2a, Y2b)
+    # backward: dX amax from the epilogue
+    G = _dev(synth.tensor_c2("dy", (M, K), seed=7), torch.bfloat16)
+    dx_amax = torch.empty(1, device="cuda")
+    g_amax = G.float().abs().max().reshape(1).contiguous()
+    DXa, DWa = (t.clone() for t in p2.backward(G, s_a))
+    DXb, DWb = p2.backward(G, s_b, dy_amax=g_amax, dx_amax=dx_amax)
+    torch.cuda.synchronize()
+    assert torch.equal(DXa, DXb) and torch.equal(DWa, DWb)
+    assert dx_amax.item() == DXb.float().abs().max().item()
