@@ -77,7 +77,8 @@ template <bool MX, int CG, int ST, int KS, bool BF = false> struct Layout {
   static constexpr uint32_t off_b = off_a + STAGES * A_STAGE;
   static constexpr uint32_t off_sfa = off_b + STAGES * B_STAGE;
   static constexpr uint32_t off_sfb = off_sfa + STAGES * SFA_STAGE;
-  static constexpr uint32_t off_bar = off_sfb + STAGES * SFB_STAGE;
+  static constexpr uint32_t off_epi = off_sfb + STAGES * SFB_STAGE;   // 4 warps x 2 KB bf16 staging
+  static constexpr uint32_t off_bar = off_epi + 4 * 2048;
   static constexpr uint32_t n_bar = 2 * STAGES + 2 * ACC;
   static constexpr uint32_t off_tmem = off_bar + 8 * n_bar;
   static constexpr uint32_t bytes = off_tmem + 16 + 1024;  // + alignment slack
@@ -338,6 +339,7 @@ __global__ void __launch_bounds__(256, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(tempty_bar, 0) : tempty_bar;
+    uint8_t* epi = gbase + L::off_epi + q * 2048;   // this warp's bf16 staging slot
     for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
       int pi, mb, nb;
       locate(tile, pi, mb, nb);
@@ -371,8 +373,8 @@ __global__ void __launch_bounds__(256, 1)
           for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__uint_as_float(r[j]), rs);
         }
         const int nvalid = min(32, N - col0);  // 16 or 32 (N % 16 == 0)
-        if (!rvalid) continue;
         if (out_f32) {
+          if (!rvalid) continue;
           float* dst = reinterpret_cast<float*>(P.D) + (int64_t)row * P.ldd + col0;
           if (P.out_amax) {
 #pragma unroll
@@ -390,18 +392,31 @@ __global__ void __launch_bounds__(256, 1)
             __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
             pk[j] = *reinterpret_cast<uint32_t*>(&h);
           }
-          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(P.D) + (int64_t)row * P.ldd + col0;
-          if (P.out_amax) {   // amax of the bf16-rounded outputs (what a consumer reads)
+          if (P.out_amax && rvalid) {   // amax of the bf16-rounded outputs (what a consumer reads)
             uint32_t m2 = 0;
 #pragma unroll
             for (int j = 0; j < 16; ++j)
               if (2 * j < nvalid) m2 = __vmaxu2(m2, pk[j] & 0x7FFF7FFFu);
             dmax = max(dmax, max(m2 & 0xFFFFu, m2 >> 16) << 16);
           }
+          // Stage this warp's 32 rows x 64 B through smem so each global store instruction writes
+          // whole 64-B row segments (8 rows per instruction) instead of 32 scattered 16-B pieces.
+          // 16-B unit j of row l sits at l*64 + ((j ^ ((l >> 1) & 3)) * 16): conflict-free both ways.
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (8 * j < nvalid)
-              reinterpret_cast<uint4*>(dst)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            *reinterpret_cast<uint4*>(epi + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16)) =
+                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = 8 * i + ((int)lane >> 2), j = lane & 3;
+            const uint4 val = *reinterpret_cast<const uint4*>(epi + rr * 64 + ((j ^ ((rr >> 1) & 3)) * 16));
+            const int grow = row - (int)lane + rr;
+            if (grow < P.M && 8 * j < nvalid)
+              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.D) + (int64_t)grow * P.ldd + col0 + 8 * j) =
+                  val;
+          }
+          __syncwarp();
         }
       }
       if (P.out_amax) {   // (P is uniform across the CTA; every lane reaches this point)
