@@ -67,6 +67,8 @@ struct GemmArgs {
 template <bool MX, int CG, int ST, int KS, bool BF = false> struct Layout {
   static constexpr int STAGES = ST;
   static constexpr int ACC = MX ? 1 : 2;
+  static constexpr int EPI_WARPS = ACC == 1 ? 8 : 4;        // see the epilogue
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   // a stage holds KS 128-byte K atoms (16 KB sub-tiles of 128 rows each)
   static constexpr uint32_t A_STAGE = BM * BK * KS;         // 16 KB x KS
   static constexpr uint32_t B_STAGE = (BN / CG) * BK * KS;  // 32 KB (CG=1) / 16 KB (CG=2), x KS
@@ -77,15 +79,18 @@ template <bool MX, int CG, int ST, int KS, bool BF = false> struct Layout {
   static constexpr uint32_t off_b = off_a + STAGES * A_STAGE;
   static constexpr uint32_t off_sfa = off_b + STAGES * B_STAGE;
   static constexpr uint32_t off_sfb = off_sfa + STAGES * SFA_STAGE;
-  static constexpr uint32_t off_epi = off_sfb + STAGES * SFB_STAGE;   // 4 warps x 2 KB bf16 staging
-  static constexpr uint32_t off_bar = off_epi + 4 * 2048;
+  static constexpr uint32_t off_epi = off_sfb + STAGES * SFB_STAGE;   // 2 KB bf16 staging per epilogue warp
+  static constexpr uint32_t off_bar = off_epi + EPI_WARPS * 2048;
   static constexpr uint32_t n_bar = 2 * STAGES + 2 * ACC;
   static constexpr uint32_t off_tmem = off_bar + 8 * n_bar;
   static constexpr uint32_t bytes = off_tmem + 16 + 1024;  // + alignment slack
   static constexpr uint32_t tmem_cols = 512;
-  // MX TMEM columns after the single accumulator: SFA atom t at sfa_col + 4t; SFB (row block h,
-  // atom t) at sfb_col + 8t + 4h
+  // MX TMEM columns after the single accumulator, one set per pipeline stage (so the tcgen05.cp of
+  // stage s+1 never overwrites columns the MMAs of stage s still read): stage s, SFA atom t at
+  // sfa_col + s*SF_COLS + 4t; SFB (row block h, atom t) at sfb_col + s*SF_COLS + 8t + 4h
+  static constexpr uint32_t SF_COLS = 12 * KS;
   static constexpr uint32_t sfa_col = 256, sfb_col = 256 + 4 * KS;
+  static_assert(!MX || 256 + STAGES * SF_COLS <= 512, "TMEM columns");
   static constexpr uint32_t tx_bytes = CG * (A_STAGE + B_STAGE + SFA_STAGE + SFB_STAGE);  // counted on the leader
 };
 
@@ -107,7 +112,7 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 }
 
 template <bool MX, int CG, int ST, int KS, bool BF>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
     fp8_gemm_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tB0,
                     const __grid_constant__ CUtensorMap tSA0, const __grid_constant__ CUtensorMap tSB0,
                     const __grid_constant__ CUtensorMap tA1, const __grid_constant__ CUtensorMap tB1,
@@ -162,7 +167,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < L::ACC; ++a) {
       mbar_init(tfull_bar + 8 * a, 1);
-      mbar_init(tempty_bar + 8 * a, CG * 128);
+      mbar_init(tempty_bar + 8 * a, CG * 32 * L::EPI_WARPS);
     }
     fence_mbar_init();
   }
@@ -196,7 +201,8 @@ __global__ void __launch_bounds__(256, 1)
       const int a_mn = P.a_mn, b_mn = P.b_mn;
       const int m0 = mb * BM * CG + (int)crank * BM;
       const int n0 = nb * BN + (int)crank * (BN / CG);
-      const uint32_t tx = L::tx_bytes;
+      // debug bit 2: skip the MX scale-factor loads (timing experiments only; results invalid)
+      const uint32_t tx = L::tx_bytes - ((MX && (args.debug & 4)) ? CG * (L::SFA_STAGE + L::SFB_STAGE) : 0);
       const int KT = P.sf_tiles_k;
       const int num_kb = P.num_kb;
       for (int kb = 0; kb < num_kb; ++kb) {
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(256, 1)
               }
             }
           }
-          if (MX) {
+          if (MX && !(args.debug & 4)) {
             // E8M0 tiles: SF tensor = [row_block * KT + k_atom][512 B]; boxes of KS consecutive atoms
             const int kt0 = kb * KS;
             const uint32_t dsa = base + L::off_sfa + stage * L::SFA_STAGE;
@@ -273,13 +279,13 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(full_bar + 8 * stage, phase);
         tc_fence_after();
         if (lane == 0) {
-          if (MX) {   // this stage's scale factors -> TMEM (in order with the MMAs that follow)
+          if (MX && !(args.debug & 2)) {   // this stage's scale factors -> TMEM (in order with the MMAs that follow)
             const uint32_t ssa = base + L::off_sfa + stage * L::SFA_STAGE;
             const uint32_t ssb = base + L::off_sfb + stage * L::SFB_STAGE;
 #pragma unroll
             for (int t = 0; t < KS; ++t) {
-              const uint32_t ca = tmem_base + L::sfa_col + 4 * t;
-              const uint32_t cb0 = tmem_base + L::sfb_col + 8 * t, cb1 = cb0 + 4;
+              const uint32_t ca = tmem_base + L::sfa_col + stage * L::SF_COLS + 4 * t;
+              const uint32_t cb0 = tmem_base + L::sfb_col + stage * L::SF_COLS + 8 * t, cb1 = cb0 + 4;
               if (CG == 2) {
                 tmem_cp_32x128b_warpx4_cg2(ca, make_sf_desc(ssa + t * SF_CHUNK));
                 tmem_cp_32x128b_warpx4_cg2(cb0, make_sf_desc(ssb + t * SF_CHUNK));
@@ -309,7 +315,8 @@ __global__ void __launch_bounds__(256, 1)
             if (MX) {
               const uint32_t t = (uint32_t)k >> 2;
               const uint32_t id = idesc_with_sf_id(idesc, k & 3, k & 3);
-              const uint32_t sfa = tmem_base + L::sfa_col + 4 * t, sfb = tmem_base + L::sfb_col + 8 * t;
+              const uint32_t sfa = tmem_base + L::sfa_col + stage * L::SF_COLS + 4 * t;
+              const uint32_t sfb = tmem_base + L::sfb_col + stage * L::SF_COLS + 8 * t;
               if (CG == 2) mma_mxf8f6f4_cg2(d_tmem, ad, bd, id, acc_flag, sfa, sfb);
               else mma_mxf8f6f4(d_tmem, ad, bd, id, acc_flag, sfa, sfb);
             } else if (BF) {
@@ -335,11 +342,18 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs, own 128 accumulator lanes) ----------------
+    // EPIW = 4: one warp per TMEM lane quadrant, 8 chunks of 32 columns, TMEM released after the
+    //           tile (the other accumulator buffer keeps the MMAs busy meanwhile).
+    // EPIW = 8 (single-accumulator MX kernel): two warps per quadrant, 128 columns each, loaded into
+    //           registers and TMEM released BEFORE scaling/storing, so the next tile's MMAs start
+    //           after the TMEM drain instead of after the whole epilogue.
+    constexpr int EPIW = L::EPI_WARPS;
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int half = EPIW == 8 ? ((warp - 4) >> 2) : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(tempty_bar, 0) : tempty_bar;
-    uint8_t* epi = gbase + L::off_epi + q * 2048;   // this warp's bf16 staging slot
+    uint8_t* epi = gbase + L::off_epi + (warp - 4) * 2048;   // this warp's bf16 staging slot
     for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
       int pi, mb, nb;
       locate(tile, pi, mb, nb);
@@ -352,15 +366,10 @@ __global__ void __launch_bounds__(256, 1)
       if (!row_scales && P.sa) rs = __frcp_rn(P.sa[0]) * __frcp_rn(P.sb[0]);
       if (row_scales && rvalid) rs = __frcp_rn(P.sa[row]);
       uint32_t dmax = 0;   // |D| max over this thread's stored values (fp32 bit patterns)
-      mbar_wait(tfull_bar + 8 * acc, acc_phase);
-      tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
-        tmem_wait_ld();
-        const int col0 = nb * BN + c * 32;
-        if (col0 >= N || (args.debug & 1)) continue;   // warp-uniform
+
+      // scale + convert + store 32 columns [col0, col0 + 32) of this thread's row
+      auto process = [&](const uint32_t (&r)[32], int col0) {
+        if (col0 >= N || (args.debug & 1)) return;   // warp-uniform
         float v[32];
         if (row_scales) {
           // lane j computes 1/sb for column col0 + j once; the warp shares them by shuffles
@@ -374,7 +383,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         const int nvalid = min(32, N - col0);  // 16 or 32 (N % 16 == 0)
         if (out_f32) {
-          if (!rvalid) continue;
+          if (!rvalid) return;
           float* dst = reinterpret_cast<float*>(P.D) + (int64_t)row * P.ldd + col0;
           if (P.out_amax) {
 #pragma unroll
@@ -385,47 +394,70 @@ __global__ void __launch_bounds__(256, 1)
           for (int j = 0; j < 8; ++j)
             if (4 * j < nvalid)
               reinterpret_cast<float4*>(dst)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-        } else {
-          uint32_t pk[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-            pk[j] = *reinterpret_cast<uint32_t*>(&h);
-          }
-          if (P.out_amax && rvalid) {   // amax of the bf16-rounded outputs (what a consumer reads)
-            uint32_t m2 = 0;
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (2 * j < nvalid) m2 = __vmaxu2(m2, pk[j] & 0x7FFF7FFFu);
-            dmax = max(dmax, max(m2 & 0xFFFFu, m2 >> 16) << 16);
-          }
-          // Stage this warp's 32 rows x 64 B through smem so each global store instruction writes
-          // whole 64-B row segments (8 rows per instruction) instead of 32 scattered 16-B pieces.
-          // 16-B unit j of row l sits at l*64 + ((j ^ ((l >> 1) & 3)) * 16): conflict-free both ways.
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<uint4*>(epi + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16)) =
-                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-          __syncwarp();
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int rr = 8 * i + ((int)lane >> 2), j = lane & 3;
-            const uint4 val = *reinterpret_cast<const uint4*>(epi + rr * 64 + ((j ^ ((rr >> 1) & 3)) * 16));
-            const int grow = row - (int)lane + rr;
-            if (grow < P.M && 8 * j < nvalid)
-              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.D) + (int64_t)grow * P.ldd + col0 + 8 * j) =
-                  val;
-          }
-          __syncwarp();
+          return;
         }
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+          pk[j] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        if (P.out_amax && rvalid) {   // amax of the bf16-rounded outputs (what a consumer reads)
+          uint32_t m2 = 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (2 * j < nvalid) m2 = __vmaxu2(m2, pk[j] & 0x7FFF7FFFu);
+          dmax = max(dmax, max(m2 & 0xFFFFu, m2 >> 16) << 16);
+        }
+        // Stage this warp's 32 rows x 64 B through smem so each global store instruction writes
+        // whole 64-B row segments (8 rows per instruction) instead of 32 scattered 16-B pieces.
+        // 16-B unit j of row l sits at l*64 + ((j ^ ((l >> 1) & 3)) * 16): conflict-free both ways.
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<uint4*>(epi + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16)) =
+              make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rr = 8 * i + ((int)lane >> 2), j = lane & 3;
+          const uint4 val = *reinterpret_cast<const uint4*>(epi + rr * 64 + ((j ^ ((rr >> 1) & 3)) * 16));
+          const int grow = row - (int)lane + rr;
+          if (grow < P.M && 8 * j < nvalid)
+            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.D) + (int64_t)grow * P.ldd + col0 + 8 * j) =
+                val;
+        }
+        __syncwarp();
+      };
+
+      mbar_wait(tfull_bar + 8 * acc, acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (EPIW == 8) {
+        uint32_t r[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tbase + half * 128 + c * 32, r[c]);
+        tmem_wait_ld();
+        tc_fence_before();   // TMEM drained: release it to the MMA warp before the stores
+        if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * acc);
+        else mbar_arrive(tempty_bar + 8 * acc);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) process(r[c], nb * BN + half * 128 + c * 32);
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tbase + c * 32, r);
+          tmem_wait_ld();
+          process(r, nb * BN + c * 32);
+        }
+        tc_fence_before();
+        if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * acc);
+        else mbar_arrive(tempty_bar + 8 * acc);
       }
       if (P.out_amax) {   // (P is uniform across the CTA; every lane reaches this point)
         dmax = __reduce_max_sync(0xffffffffu, dmax);
         if (lane == 0 && dmax) atomicMax(P.out_amax, dmax);
       }
-      tc_fence_before();
-      if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * acc);
-      else mbar_arrive(tempty_bar + 8 * acc);
       if (++acc == L::ACC) { acc = 0; acc_phase ^= 1; }
     }
   }
@@ -576,12 +608,12 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   const int grid = CG * (a.num_tiles < slots ? a.num_tiles : slots);
   LaunchScope ls(MX ? K_GEMM_MX : (BF ? K_GEMM_BF16 : K_GEMM), st);
   if (CG == 1) {
-    fp8_gemm_kernel<MX, CG, ST, KS, BF><<<grid, 256, L::bytes, st>>>(m0[0], m0[1], m0[2], m0[3], m1[0], m1[1], m1[2],
+    fp8_gemm_kernel<MX, CG, ST, KS, BF><<<grid, L::THREADS, L::bytes, st>>>(m0[0], m0[1], m0[2], m0[3], m1[0], m1[1], m1[2],
                                                                  m1[3], a);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(L::THREADS);
     cfg.dynamicSmemBytes = L::bytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];

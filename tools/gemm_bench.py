@@ -41,6 +41,14 @@ def main():
             ms = timeit(lambda: ops.gemm(A, "e4m3", s, B, "e4m3", s, "tensor"))
             row["ours" if dbg == "0" else "ours_nostore"] = round(flops / ms / 1e9)
         os.environ["FP8T_GEMM_DEBUG"] = "0"
+        if M % 128 == 0 and N % 128 == 0 and K % 128 == 0:   # MXFP8 block-scaled kind, codes 127 (=1.0)
+            sfa = torch.full((M * K // 32,), 127, dtype=torch.uint8, device="cuda")
+            sfb = torch.full((N * K // 32,), 127, dtype=torch.uint8, device="cuda")
+            for dbg in ("0", "1", "2", "6"):   # 2: no tcgen05.cp of scales; 4: no scale TMA loads
+                os.environ["FP8T_GEMM_DEBUG"] = dbg
+                ms = timeit(lambda: ops.gemm(A, "e4m3", sfa, B, "e4m3", sfb, "mx32"))
+                row["ours_mx" + ("" if dbg == "0" else "_dbg" + dbg)] = round(flops / ms / 1e9)
+            os.environ["FP8T_GEMM_DEBUG"] = "0"
         try:
             a8 = A.view(torch.float8_e4m3fn)
             b8 = B.view(torch.float8_e4m3fn)
