@@ -44,8 +44,11 @@ CONFIGS = {
                workload="c5: Llama-3.1-405B w1 linear fwd+bwd, M=8192 tokens per GPU, K=16384, N=53248, "
                         "tensorwise (BASELINE.json configs[4]; FSDP2 FP8 all-gather at N>1)"),
 }
-# oracle sample for the CPU baseline / reference arm: same K and value recipe, fewer rows
+# oracle sample for the reference arm (per step, so the whole --steps/--warmup run stays within a
+# few minutes) and for the cpu_baseline (one step of ~10-30 s of CPU work): same K and value
+# recipe, fewer rows
 CPU_SAMPLE = dict(M=128, N=2048)
+CPU_BASELINE_M = 512
 
 
 def parse():
@@ -74,11 +77,11 @@ def _threads_used():
         return os.cpu_count() or 1
 
 
-def oracle_step_fn(cfg):
+def oracle_step_fn(cfg, Ms=CPU_SAMPLE["M"]):
     """One oracle fwd+bwd on the bounded sample (CPU).  Returns (fn, flops, sample_desc)."""
     import synth
     from oracle import linear as olin
-    Ms, Ns, K = CPU_SAMPLE["M"], CPU_SAMPLE["N"], cfg["K"]
+    Ns, K = CPU_SAMPLE["N"], cfg["K"]
     f = synth.RECIPES[cfg["cfg"]]
     x, w, dy = f("x", (Ms, K), 0, cfg["cfg"]), f("w", (Ns, K), 0, cfg["cfg"]), f("dy", (Ms, Ns), 0, cfg["cfg"])
     recipe = cfg["recipe"]
@@ -94,8 +97,8 @@ def oracle_step_fn(cfg):
 
 
 def cpu_baseline(cfg):
-    step, flops, desc = oracle_step_fn(cfg)
-    step()  # untimed warm run
+    oracle_step_fn(cfg)[0]()  # untimed warm run on the small sample (thread pools, page faults)
+    step, flops, desc = oracle_step_fn(cfg, CPU_BASELINE_M)
     t0 = time.perf_counter()
     step()
     dt = time.perf_counter() - t0

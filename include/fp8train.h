@@ -69,7 +69,7 @@
 extern "C" {
 #endif
 
-#define FP8TRAIN_ABI_VERSION 3
+#define FP8TRAIN_ABI_VERSION 4
 
 typedef enum {
   FP8_OK = 0,
@@ -91,8 +91,11 @@ typedef enum {
   FP8_GRAN_COL = 2,      /* one scale per column, reduced over the rows */
   FP8_GRAN_ROW_COL = 3,  /* rowwise recipe dual cast from one input: q with per-row
                             scales, q_t with per-column scales */
-  FP8_GRAN_MX32 = 4      /* MXFP8: q = blocks of 32 along columns ("dim0"),
+  FP8_GRAN_MX32 = 4,     /* MXFP8: q = blocks of 32 along columns ("dim0"),
                             q_t = blocks of 32 along rows ("dim1"), E8M0 scales */
+  FP8_GRAN_MX32_RM = 5   /* as MX32, but q_t (dim1) is written in the input's layout
+                            [rows, cols] instead of transposed: same codes, no transpose;
+                            fp8_gemm reads it as an MN-major operand */
 } fp8_gran_t;
 
 typedef enum { FP8_MX_FLOOR = 0, FP8_MX_RCEIL = 1 } fp8_mx_round_t;
@@ -114,13 +117,14 @@ typedef struct {
 /* A quantised tensor produced by fp8_cast_scaled (caller-owned buffers).
  *   q      : codes [rows, cols] row-major, or NULL
  *   q_t    : codes of the transposed copy [cols, rows] row-major, or NULL
+ *            (MX32_RM: the dim1 codes [rows, cols] row-major, not transposed)
  *   scale  : scales that go with q:
  *              TENSOR float[1], ROW float[rows], COL float[cols],
  *              ROW_COL float[rows] (row scales), MX32 E8M0 blocked [rows x cols/32]
  *   scale_t: scales that go with q_t:
  *              TENSOR/ROW/COL: may alias `scale` or be NULL (same values),
  *              ROW_COL float[cols] (column scales),
- *              MX32 E8M0 blocked [cols x rows/32]
+ *              MX32 / MX32_RM E8M0 blocked [cols x rows/32]
  *   amax   : float[ ] amax behind `scale` (same shape), or NULL
  *   amax_t : float[ ] amax behind `scale_t` (ROW_COL: [cols]), or NULL
  * For MX32 amax/amax_t are unused (the block amax is fused into the cast). */
@@ -157,6 +161,16 @@ fp8_status_t fp8_amax(fp8_hp_t x, fp8_gran_t gran, float* amax_out,
                       void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * fp8_amax_multi -- tensorwise amax of n tensors in ONE launch (SURVEY §8f.2:
+ * the weights' amax after the optimizer step, computed together instead of one
+ * pass per weight).  xs: HOST array of n descriptors (read during the call);
+ * amax_out: device float[n], amax_out[t] = max |xs[t]| (exact, as fp8_amax).
+ * 1 <= n <= 48 (FP8_AMAX_MULTI_MAX) per call; no workspace.
+ * ------------------------------------------------------------------------- */
+#define FP8_AMAX_MULTI_MAX 48
+fp8_status_t fp8_amax_multi(const fp8_hp_t* xs, int n, float* amax_out, void* stream);
+
+/* ---------------------------------------------------------------------------
  * fp8_cast_scaled -- scale from amax, then saturating RNE cast (PAPER.md:281-287,
  * Appendix A).  Writes out->q and/or out->q_t (at least one non-NULL), the
  * scales and (optionally) the amax, per out->gran (see fp8_tensor_t).
@@ -183,7 +197,7 @@ fp8_status_t fp8_cast_scaled(fp8_hp_t x, fp8_mx_round_t mx_round, const float* a
  *   gran ROW   : sa float[M], sb float[N]
  *   gran MX32  : sa, sb E8M0 blocked codes of A [M x K/32] and B [N x K/32];
  *                the per-32-block 2^(c-127) factors are applied inside the MMA
- *                (K-major operands only).
+ *                (either operand major; the codes' logical layout is unchanged).
  * D is [M,N] row-major with leading dimension ldd elements, dtype out_dtype
  * (BF16 = RN of the fp32 result; F32 = the fp32 result).  Order of the fp32
  * accumulation and of the epilogue products is unspecified (R-c16).
@@ -277,6 +291,18 @@ size_t fp8_fsdp_workspace_bytes(fp8_hp_t w_shard);
 fp8_status_t fp8_fsdp_allgather(fp8_comm_t comm, fp8_hp_t w_shard, fp8_format_t fmt,
                                 uint8_t* w_full, float* scale_out, float* amax_out,
                                 void* ws, size_t ws_bytes, void* stream);
+/* Precomputed global amax for all of a model's FP8-gathered weights at once (the
+ * torchtitan-style precompute after the optimizer step): one
+ * fp8_amax_multi launch over this rank's n shards + ONE ncclAllReduce(MAX) of the n
+ * amaxes.  amax_out: device float[n] (the global amaxes), 1 <= n <= 48. */
+fp8_status_t fp8_fsdp_precompute_amax(fp8_comm_t comm, const fp8_hp_t* w_shards, int n,
+                                      float* amax_out, void* stream);
+/* As fp8_fsdp_allgather, but with amax_in = the global amax from
+ * fp8_fsdp_precompute_amax (device float[1]): no amax pass and no all-reduce, only
+ * cast-into-slot + all-gather.  amax_in NULL = fp8_fsdp_allgather. */
+fp8_status_t fp8_fsdp_allgather_ex(fp8_comm_t comm, fp8_hp_t w_shard, fp8_format_t fmt,
+                                   const float* amax_in, uint8_t* w_full, float* scale_out,
+                                   float* amax_out, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Helpers

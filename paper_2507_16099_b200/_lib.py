@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libfp8train.so")
 FP8_OK, FP8_EINVAL, FP8_EALIGN, FP8_EUNSUPPORTED, FP8_ECUDA, FP8_ENCCL, FP8_EWORKSPACE = range(7)
 DT_F32, DT_BF16 = 0, 1
 E4M3, E5M2 = 0, 1
-GRAN_TENSOR, GRAN_ROW, GRAN_COL, GRAN_ROW_COL, GRAN_MX32 = range(5)
+GRAN_TENSOR, GRAN_ROW, GRAN_COL, GRAN_ROW_COL, GRAN_MX32, GRAN_MX32_RM = range(6)
 MX_FLOOR, MX_RCEIL = 0, 1
 K_MAJOR, MN_MAJOR = 0, 1
 RECIPE_TENSORWISE, RECIPE_ROWWISE, RECIPE_MXFP8, RECIPE_ROWWISE_GW_HP = range(4)
@@ -49,6 +49,7 @@ SIGNATURES = {
     "fp8_profile_collect": (_c.c_int, [_c.POINTER(_c.c_int), _c.POINTER(_c.c_float), _c.c_int]),
     "fp8_amax_workspace_bytes": (_c.c_size_t, [HP, _c.c_int]),
     "fp8_amax": (_c.c_int, [HP, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
+    "fp8_amax_multi": (_c.c_int, [_c.POINTER(HP), _c.c_int, _c.c_void_p, _c.c_void_p]),
     "fp8_cast_workspace_bytes": (_c.c_size_t, [HP, _c.c_int]),
     "fp8_cast_scaled": (_c.c_int, [HP, _c.c_int, _c.c_void_p, _c.POINTER(Tensor8), _c.c_void_p, _c.c_size_t,
                                    _c.c_void_p]),
@@ -73,7 +74,11 @@ SIGNATURES = {
     "fp8_fsdp_workspace_bytes": (_c.c_size_t, [HP]),
     "fp8_fsdp_allgather": (_c.c_int, [_c.c_void_p, HP, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_void_p,
                                       _c.c_void_p, _c.c_size_t, _c.c_void_p]),
+    "fp8_fsdp_precompute_amax": (_c.c_int, [_c.c_void_p, _c.POINTER(HP), _c.c_int, _c.c_void_p, _c.c_void_p]),
+    "fp8_fsdp_allgather_ex": (_c.c_int, [_c.c_void_p, HP, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_void_p,
+                                         _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
 }
+AMAX_MULTI_MAX = 48
 
 
 class Fp8Error(RuntimeError):

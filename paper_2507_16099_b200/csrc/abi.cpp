@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -81,6 +82,12 @@ static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 static inline size_t al(size_t b) { return (b + 255) & ~size_t(255); }
 static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 static inline size_t esize(fp8_dtype_t d) { return d == FP8_DT_F32 ? 4 : 2; }
+// MXFP8 linear: dim1 codes written transposed and read K-major (FP8T_MX_TRANSPOSED=1, the A/B
+// variant) instead of row-major and read MN-major (default).  Forward and backward must agree.
+static inline bool mx_transposed() {
+  const char* e = getenv("FP8T_MX_TRANSPOSED");
+  return e && e[0] == '1';
+}
 
 static fp8_status_t check_hp(const fp8_hp_t& x, const char* name, bool need_ptr = true) {
   if (x.dtype != FP8_DT_F32 && x.dtype != FP8_DT_BF16) return fail(FP8_EINVAL, "%s: bad dtype", name);
@@ -167,6 +174,29 @@ fp8_status_t fp8_amax(fp8_hp_t x, fp8_gran_t gran, float* amax_out, void*, size_
   return FP8_OK;
 }
 
+fp8_status_t fp8_amax_multi(const fp8_hp_t* xs, int n, float* amax_out, void* stream) {
+  if (!xs || !amax_out) return fail(FP8_EINVAL, "xs/amax_out: null pointer");
+  if (n < 1 || n > FP8_AMAX_MULTI_MAX) return fail(FP8_EINVAL, "n must be in [1, %d]", FP8_AMAX_MULTI_MAX);
+  static_assert(FP8_AMAX_MULTI_MAX == AMAX_MULTI_MAX, "multi-tensor amax capacity");
+  AmaxMultiArgs a{};
+  a.n = n;
+  a.out = reinterpret_cast<uint32_t*>(amax_out);
+  a.chunk_start[0] = 0;
+  for (int t = 0; t < n; ++t) {
+    FP8T_TRY(check_hp(xs[t], "xs[t]"));
+    const int64_t es = (int64_t)esize(xs[t].dtype);
+    a.ptr[t] = static_cast<const uint8_t*>(xs[t].ptr);
+    a.ld_bytes[t] = xs[t].ld * es;
+    a.vecs[t] = xs[t].cols * es / 16;
+    a.cpr[t] = (a.vecs[t] + 255) / 256;
+    a.bf16[t] = xs[t].dtype == FP8_DT_BF16;
+    a.chunk_start[t + 1] = a.chunk_start[t] + xs[t].rows * a.cpr[t];
+  }
+  FP8T_CUDA(cudaMemsetAsync(amax_out, 0, 4 * (size_t)n, S(stream)), "memset amax");
+  FP8T_CUDA(launch_amax_multi(a, S(stream)), "amax_multi kernel");
+  return FP8_OK;
+}
+
 // ---------------------------------------------------------------------------
 // cast
 // ---------------------------------------------------------------------------
@@ -194,13 +224,14 @@ fp8_status_t fp8_cast_scaled(fp8_hp_t x, fp8_mx_round_t mx_round, const float* a
   cudaStream_t st = S(stream);
   const int fmt = out->fmt;
 
-  if (out->gran == FP8_GRAN_MX32) {
+  if (out->gran == FP8_GRAN_MX32 || out->gran == FP8_GRAN_MX32_RM) {
     if (x.rows % 128 || x.cols % 128) return fail(FP8_EALIGN, "MX32 needs rows and cols multiples of 128");
     if (mx_round != FP8_MX_FLOOR && mx_round != FP8_MX_RCEIL) return fail(FP8_EINVAL, "bad mx_round");
     if (out->q && !out->scale) return fail(FP8_EINVAL, "MX32: q needs scale");
     if (out->q_t && !out->scale_t) return fail(FP8_EINVAL, "MX32: q_t needs scale_t");
     FP8T_CUDA(launch_mx_cast(x.ptr, bf16, fmt, mx_round == FP8_MX_RCEIL, x.rows, x.cols, x.ld, out->q,
-                             static_cast<uint8_t*>(out->scale), out->q_t, static_cast<uint8_t*>(out->scale_t), st),
+                             static_cast<uint8_t*>(out->scale), out->q_t, static_cast<uint8_t*>(out->scale_t), st,
+                             out->gran == FP8_GRAN_MX32),
               "mx cast kernel");
     return FP8_OK;
   }
@@ -284,8 +315,6 @@ fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, fp8_major_t major_a,
   else if (gran == FP8_GRAN_MX32) {
     mode = 2;
     if (M % 128 || N % 128 || K % 128) return fail(FP8_EALIGN, "MX32 GEMM needs M, N, K multiples of 128");
-    if (major_a != FP8_K_MAJOR || major_b != FP8_K_MAJOR)
-      return fail(FP8_EUNSUPPORTED, "MX32 GEMM needs K-major operands");
     FP8T_TRY(check_ptr(sa, "sfa"));
     FP8T_TRY(check_ptr(sb, "sfb"));
   } else return fail(FP8_EINVAL, "fp8_gemm: gran must be TENSOR, ROW or MX32");
@@ -572,9 +601,11 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
     GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N, 0, yam};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
   } else {
-    const bool rc = cfg->mx_round == FP8_MX_RCEIL;
-    FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, fw.xq, fw.sfx, sv.xT, (uint8_t*)sv.sx, st), "mx cast x");
-    FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, fw.wq, fw.sfw, sv.wT, (uint8_t*)sv.sw, st), "mx cast w");
+    const bool rc = cfg->mx_round == FP8_MX_RCEIL, tr = mx_transposed();
+    FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, fw.xq, fw.sfx, sv.xT, (uint8_t*)sv.sx, st, tr),
+              "mx cast x");
+    FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, fw.wq, fw.sfw, sv.wT, (uint8_t*)sv.sw, st, tr),
+              "mx cast w");
     GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sfx, fw.sfw, 2, M, N, K, K, K, y, of32, N, 0, yam};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
   }
@@ -642,7 +673,7 @@ fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const f
   } else {
     mode = 2;
     FP8T_CUDA(launch_mx_cast(dy.ptr, gb, fg, cfg->mx_round == FP8_MX_RCEIL, M, N, dy.ld, dx ? bw.g : nullptr,
-                             (uint8_t*)bw.sg, dw ? bw.gT : nullptr, (uint8_t*)bw.sgT, st),
+                             (uint8_t*)bw.sg, dw ? bw.gT : nullptr, (uint8_t*)bw.sgT, st, mx_transposed()),
               "mx cast dy");
   }
 gemms:
@@ -679,8 +710,15 @@ gemms:
     if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 1, bw.sg, sv.sw, mode, M, K, N, N, K, dx, of32, K, 0, dxam};
     // dW[N,K] = dY_c^T . X_c: A stored [M,N] = MN-major, B stored [M,K] = MN-major
     if (dw) ps[n++] = GemmProblem{bw.gT, sv.xT, fg, ff, 1, 1, bw.sgT, sv.sx, mode, N, K, M, N, K, dw, of32, K};
+  } else if (!mx_transposed()) {
+    // MXFP8: dim1 copies (blocks along the contraction dim) kept in the input's row-major layout
+    // and read MN-major, like the tensorwise / rowwise backward
+    // dX[M,K] = dY[M,N] . W : A = dY dim0 (K-major over N), B = W dim1 stored [N,K] = MN-major
+    if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 1, bw.sg, sv.sw, mode, M, K, N, N, K, dx, of32, K, 0, dxam};
+    // dW[N,K] = dY^T . X : A = dY dim1 stored [M,N] = MN-major, B = X dim1 stored [M,K] = MN-major
+    if (dw) ps[n++] = GemmProblem{bw.gT, sv.xT, fg, ff, 1, 1, bw.sgT, sv.sx, mode, N, K, M, N, K, dw, of32, K};
   } else {
-    // MXFP8: dim1 copies are transposed (blocks along the contraction dim), K-major
+    // MXFP8 with transposed dim1 copies (FP8T_MX_TRANSPOSED=1), all operands K-major
     // dX[M,K] = dY[M,N] . W  : A = dY (K-major over N), B = W^T [K,N]
     if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 0, bw.sg, sv.sw, mode, M, K, N, N, N, dx, of32, K, 0, dxam};
     // dW[N,K] = dY^T[N,M] . X : A = dY^T [N,M], B = X^T [K,M]

@@ -261,6 +261,58 @@ __global__ void __launch_bounds__(256) amax_flat_kernel(const uint4* __restrict_
   }
 }
 
+// Tensorwise amax of up to AMAX_MULTI_MAX tensors in one launch (the weights after an optimizer
+// step: one pass instead of one launch per weight).  Work unit = a warp chunk of 32*8 16-byte
+// vectors inside one row; the chunks of all tensors are numbered consecutively and every warp
+// takes one contiguous range of them, so a warp crosses at most a few tensor boundaries and
+// issues one atomicMax per (warp, tensor) it touched.
+__global__ void __launch_bounds__(256) amax_multi_kernel(const __grid_constant__ AmaxMultiArgs a) {
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t total = a.chunk_start[a.n];
+  const int64_t c_begin = total * gwarp / nwarps, c_end = total * (gwarp + 1) / nwarps;
+  int t = 0;
+  while (t + 1 < a.n && a.chunk_start[t + 1] <= c_begin) ++t;
+  uint32_t m = 0;
+  auto flush = [&](int tt) {
+    const uint32_t r = __reduce_max_sync(0xffffffffu, m);
+    if (lane == 0 && r) atomicMax(a.out + tt, r);
+    m = 0;
+  };
+  for (int64_t c = c_begin; c < c_end; ++c) {
+    if (c >= a.chunk_start[t + 1]) {   // warp-uniform
+      flush(t);
+      do { ++t; } while (c >= a.chunk_start[t + 1]);
+    }
+    const int64_t local = c - a.chunk_start[t];
+    const int64_t row = local / a.cpr[t], seg = local - row * a.cpr[t];
+    const uint4* p = reinterpret_cast<const uint4*>(a.ptr[t] + row * a.ld_bytes[t]) + seg * (32 * U);
+    const int64_t rem = a.vecs[t] - seg * (32 * U);
+    const int valid = rem < 32 * U ? (int)rem : 32 * U;
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = (lane + 32 * u < valid) ? __ldg(p + lane + 32 * u) : make_uint4(0, 0, 0, 0);
+    if (a.bf16[t]) {
+      uint32_t h = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        h = __vmaxu2(h, v[u].x & 0x7FFF7FFFu); h = __vmaxu2(h, v[u].y & 0x7FFF7FFFu);
+        h = __vmaxu2(h, v[u].z & 0x7FFF7FFFu); h = __vmaxu2(h, v[u].w & 0x7FFF7FFFu);
+      }
+      m = max(m, max(h & 0xFFFFu, h >> 16) << 16);   // bf16 |x| bits -> fp32 bit pattern
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        m = max(m, v[u].x & 0x7FFFFFFFu); m = max(m, v[u].y & 0x7FFFFFFFu);
+        m = max(m, v[u].z & 0x7FFFFFFFu); m = max(m, v[u].w & 0x7FFFFFFFu);
+      }
+    }
+  }
+  if (c_begin < c_end) flush(t);
+}
+
 // ---------------------------------------------------------------------------
 // cast_tile: q (row-major) with scale mode QM, q_t (transposed) with scale mode TM.
 // Modes: 0 none, 1 tensor (amax[1]), 2 per row (amax[R]), 3 per column (amax[C]).
@@ -374,7 +426,7 @@ __device__ __forceinline__ int64_t sf_offset(int64_t r, int64_t cblk, int64_t nc
   return ((r >> 7) * ncol_tiles + (cblk >> 2)) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (cblk & 3);
 }
 
-template <typename T, int FMT, bool RCEIL, bool DIM0, bool DIM1>
+template <typename T, int FMT, bool RCEIL, bool DIM0, bool DIM1, bool TR1>
 __global__ void __launch_bounds__(256, 3) mx_cast_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
                                                       uint8_t* __restrict__ q0, uint8_t* __restrict__ sf0,
                                                       uint8_t* __restrict__ q1, uint8_t* __restrict__ sf1) {
@@ -441,14 +493,24 @@ __global__ void __launch_bounds__(256, 3) mx_cast_kernel(const T* __restrict__ x
     const float4 ma = *reinterpret_cast<const float4*>(&mult1[j][cc]);
     const float4 mb = *reinterpret_cast<const float4*>(&mult1[j][cc + 4]);
     const float mu[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+    if (TR1) {   // q1 = the dim1 codes transposed, [C, R] (K-major for the backward GEMMs)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float v[8];
-      raw[i].get(v);
-      *reinterpret_cast<uint2*>(&tile[swz(rbase + i, cc >> 2)]) = cast8v<FMT>(v, mu);
+      for (int i = 0; i < 8; ++i) {
+        float v[8];
+        raw[i].get(v);
+        *reinterpret_cast<uint2*>(&tile[swz(rbase + i, cc >> 2)]) = cast8v<FMT>(v, mu);
+      }
+      __syncthreads();
+      store_transposed(tile, q1, R, r0, c0, 128, 128);
+    } else {     // q1 = the dim1 codes in the input's layout, [R, C] (read MN-major by the GEMMs)
+      uint8_t* q1p = q1 + (r0 + rbase) * C + c0 + cc;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float v[8];
+        raw[i].get(v);
+        *reinterpret_cast<uint2*>(q1p + i * C) = cast8v<FMT>(v, mu);
+      }
     }
-    __syncthreads();
-    store_transposed(tile, q1, R, r0, c0, 128, 128);
   }
 }
 
@@ -522,6 +584,16 @@ static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
   return cudaGetLastError();
 }
 
+cudaError_t launch_amax_multi(const AmaxMultiArgs& a, cudaStream_t st) {
+  const int64_t total = a.chunk_start[a.n];
+  if (total == 0) return cudaSuccess;
+  const int64_t cap = (int64_t)sm_count() * 8 * 8;   // warps: 8 CTAs of 8 warps per SM
+  const int64_t warps = total < cap ? total : cap;
+  LaunchScope ls(K_AMAX, st);
+  amax_multi_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_amax(const void* x, bool bf16, int64_t R, int64_t C, int64_t ld, int mode, uint32_t* at,
                         uint32_t* ar, uint32_t* ac, cudaStream_t st) {
   return bf16 ? amax_launch_t<__nv_bfloat16>(x, R, C, ld, mode, at, ar, ac, st)
@@ -560,23 +632,29 @@ cudaError_t launch_cast(const void* x, bool bf16, int fmt, int64_t R, int64_t C,
 
 template <typename T, int FMT, bool RC>
 static cudaError_t mx_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, uint8_t* q0, uint8_t* sf0,
-                               uint8_t* q1, uint8_t* sf1, cudaStream_t s) {
+                               uint8_t* q1, uint8_t* sf1, bool tr1, cudaStream_t s) {
   const T* p = static_cast<const T*>(x);
   dim3 g = tile_grid(R, C);
   LaunchScope ls(K_MX, s);
-  if (q0 && q1) mx_cast_kernel<T, FMT, RC, true, true><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
-  else if (q0) mx_cast_kernel<T, FMT, RC, true, false><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
-  else mx_cast_kernel<T, FMT, RC, false, true><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
+  if (q0 && q1) {
+    if (tr1) mx_cast_kernel<T, FMT, RC, true, true, true><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
+    else mx_cast_kernel<T, FMT, RC, true, true, false><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
+  } else if (q0) {
+    mx_cast_kernel<T, FMT, RC, true, false, true><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
+  } else {
+    if (tr1) mx_cast_kernel<T, FMT, RC, false, true, true><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
+    else mx_cast_kernel<T, FMT, RC, false, true, false><<<g, 256, 0, s>>>(p, R, C, ld, q0, sf0, q1, sf1);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_mx_cast(const void* x, bool bf16, int fmt, bool rceil, int64_t R, int64_t C, int64_t ld,
-                           uint8_t* q0, uint8_t* sf0, uint8_t* q1, uint8_t* sf1, cudaStream_t s) {
+                           uint8_t* q0, uint8_t* sf0, uint8_t* q1, uint8_t* sf1, cudaStream_t s, bool tr1) {
 #define FP8T_MX(T)                                                                                  \
-  if (fmt == 0) return rceil ? mx_launch_t<T, 0, true>(x, R, C, ld, q0, sf0, q1, sf1, s)            \
-                             : mx_launch_t<T, 0, false>(x, R, C, ld, q0, sf0, q1, sf1, s);          \
-  return rceil ? mx_launch_t<T, 1, true>(x, R, C, ld, q0, sf0, q1, sf1, s)                          \
-               : mx_launch_t<T, 1, false>(x, R, C, ld, q0, sf0, q1, sf1, s);
+  if (fmt == 0) return rceil ? mx_launch_t<T, 0, true>(x, R, C, ld, q0, sf0, q1, sf1, tr1, s)       \
+                             : mx_launch_t<T, 0, false>(x, R, C, ld, q0, sf0, q1, sf1, tr1, s);     \
+  return rceil ? mx_launch_t<T, 1, true>(x, R, C, ld, q0, sf0, q1, sf1, tr1, s)                     \
+               : mx_launch_t<T, 1, false>(x, R, C, ld, q0, sf0, q1, sf1, tr1, s);
   if (bf16) { FP8T_MX(__nv_bfloat16) }
   FP8T_MX(float)
 #undef FP8T_MX

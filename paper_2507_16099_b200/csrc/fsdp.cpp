@@ -66,10 +66,24 @@ fp8_status_t fp8_comm_destroy(fp8_comm_t comm) {
 
 size_t fp8_fsdp_workspace_bytes(fp8_hp_t) { return 0; }
 
-fp8_status_t fp8_fsdp_allgather(fp8_comm_t comm, fp8_hp_t w, fp8_format_t fmt, uint8_t* w_full, float* scale_out,
-                                float* amax_out, void*, size_t, void* stream) {
+fp8_status_t fp8_fsdp_precompute_amax(fp8_comm_t comm, const fp8_hp_t* w, int n, float* amax_out, void* stream) {
   if (!comm) return fail(FP8_EINVAL, "comm: null");
-  if (!w.ptr || !w_full || !scale_out || !amax_out) return fail(FP8_EINVAL, "null pointer");
+  fp8_status_t s = fp8_amax_multi(w, n, amax_out, stream);
+  if (s != FP8_OK) return s;
+  return nccl_check(ncclAllReduce(amax_out, amax_out, (size_t)n, ncclUint32, ncclMax, comm->nccl,
+                                  static_cast<cudaStream_t>(stream)),
+                    "ncclAllReduce");
+}
+
+fp8_status_t fp8_fsdp_allgather(fp8_comm_t comm, fp8_hp_t w, fp8_format_t fmt, uint8_t* w_full, float* scale_out,
+                                float* amax_out, void* ws, size_t ws_bytes, void* stream) {
+  return fp8_fsdp_allgather_ex(comm, w, fmt, nullptr, w_full, scale_out, amax_out, ws, ws_bytes, stream);
+}
+
+fp8_status_t fp8_fsdp_allgather_ex(fp8_comm_t comm, fp8_hp_t w, fp8_format_t fmt, const float* amax_in,
+                                   uint8_t* w_full, float* scale_out, float* amax_out, void*, size_t, void* stream) {
+  if (!comm) return fail(FP8_EINVAL, "comm: null");
+  if (!w.ptr || !w_full || !scale_out || (!amax_out && !amax_in)) return fail(FP8_EINVAL, "null pointer");
   if (fmt != FP8_E4M3 && fmt != FP8_E5M2) return fail(FP8_EINVAL, "bad fp8 format");
   if (w.dtype != FP8_DT_F32 && w.dtype != FP8_DT_BF16) return fail(FP8_EINVAL, "bad dtype");
   if (w.rows < 16 || w.cols < 16 || w.rows % 16 || w.cols % 16) return fail(FP8_EALIGN, "shard rows/cols: multiples of 16");
@@ -80,14 +94,18 @@ fp8_status_t fp8_fsdp_allgather(fp8_comm_t comm, fp8_hp_t w, fp8_format_t fmt, u
   const bool bf16 = w.dtype == FP8_DT_BF16;
   const size_t chunk = (size_t)w.rows * (size_t)w.cols;
   uint8_t* slot = w_full + (size_t)comm->rank * chunk;
-  uint32_t* acc = reinterpret_cast<uint32_t*>(amax_out);
   fp8_status_t s;
-  if ((s = cuda_check(cudaMemsetAsync(acc, 0, 4, st), "memset")) != FP8_OK) return s;
-  if ((s = cuda_check(launch_amax(w.ptr, bf16, w.rows, w.cols, w.ld, 1, acc, nullptr, nullptr, st), "amax")) != FP8_OK)
-    return s;
-  if ((s = nccl_check(ncclAllReduce(acc, acc, 1, ncclUint32, ncclMax, comm->nccl, st), "ncclAllReduce")) != FP8_OK)
-    return s;
-  if ((s = cuda_check(launch_cast(w.ptr, bf16, fmt, w.rows, w.cols, w.ld, 1, 0, amax_out, amax_out, slot, nullptr,
+  if (!amax_in) {
+    uint32_t* acc = reinterpret_cast<uint32_t*>(amax_out);
+    if ((s = cuda_check(cudaMemsetAsync(acc, 0, 4, st), "memset")) != FP8_OK) return s;
+    if ((s = cuda_check(launch_amax(w.ptr, bf16, w.rows, w.cols, w.ld, 1, acc, nullptr, nullptr, st), "amax")) !=
+        FP8_OK)
+      return s;
+    if ((s = nccl_check(ncclAllReduce(acc, acc, 1, ncclUint32, ncclMax, comm->nccl, st), "ncclAllReduce")) != FP8_OK)
+      return s;
+    amax_in = amax_out;
+  }
+  if ((s = cuda_check(launch_cast(w.ptr, bf16, fmt, w.rows, w.cols, w.ld, 1, 0, amax_in, amax_in, slot, nullptr,
                                   scale_out, nullptr, st),
                       "cast")) != FP8_OK)
     return s;

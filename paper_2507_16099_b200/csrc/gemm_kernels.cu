@@ -557,7 +557,7 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   P.tiles_n = (int)((p.N + BN - 1) / BN);
   const int k_per_stage = BF ? KS * 64 : KS * BK;   // elements
   P.num_kb = (int)((p.K + k_per_stage - 1) / k_per_stage);
-  P.idesc = MX   ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN)
+  P.idesc = MX   ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u)
             : BF ? make_idesc_bf16(BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u)
                  : make_idesc_f8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u);
   P.a_mn = p.a_mn;

@@ -24,9 +24,25 @@ cudaError_t launch_amax(const void* x, bool bf16, int64_t R, int64_t C, int64_t 
 cudaError_t launch_cast(const void* x, bool bf16, int fmt, int64_t R, int64_t C, int64_t ld, int qm, int tm,
                         const float* aq, const float* at, uint8_t* q, uint8_t* qt, float* sq, float* st,
                         cudaStream_t s);
-// MXFP8 dim0 (q0, sf0) and/or dim1 (q1, sf1) casts, blocked E8M0 layout
+// Tensorwise amax of n <= AMAX_MULTI_MAX tensors in one launch; out[t] (u32 bit patterns of
+// non-negative floats) must be zeroed by the caller.  chunk_start[t] = first warp chunk of
+// tensor t (chunks of 256 16-byte vectors within one row), chunk_start[n] = total.
+constexpr int AMAX_MULTI_MAX = 48;
+struct AmaxMultiArgs {
+  int n;
+  const uint8_t* ptr[AMAX_MULTI_MAX];
+  int64_t ld_bytes[AMAX_MULTI_MAX];
+  int64_t vecs[AMAX_MULTI_MAX];   // 16-byte vectors per row
+  int64_t cpr[AMAX_MULTI_MAX];    // chunks per row
+  int64_t chunk_start[AMAX_MULTI_MAX + 1];
+  uint8_t bf16[AMAX_MULTI_MAX];
+  uint32_t* out;
+};
+cudaError_t launch_amax_multi(const AmaxMultiArgs& a, cudaStream_t st);
+// MXFP8 dim0 (q0, sf0) and/or dim1 (q1, sf1) casts, blocked E8M0 layout; tr1: dim1 codes written
+// transposed [C,R] (else in the input's layout [R,C])
 cudaError_t launch_mx_cast(const void* x, bool bf16, int fmt, bool rceil, int64_t R, int64_t C, int64_t ld,
-                           uint8_t* q0, uint8_t* sf0, uint8_t* q1, uint8_t* sf1, cudaStream_t s);
+                           uint8_t* q0, uint8_t* sf0, uint8_t* q1, uint8_t* sf1, cudaStream_t s, bool tr1 = true);
 cudaError_t launch_transpose_u8(const uint8_t* in, int64_t R, int64_t C, uint8_t* out, cudaStream_t s);
 
 // tcgen05 GEMM: D[M,N] = A[M,K] B[N,K]^T with scales.

@@ -292,8 +292,10 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(uint32_t M, uint32_t N, u
   return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 // kind::mxf8f6f4.block_scale descriptor: scale_format = UE8M0, sf ids set per MMA.
-__host__ __device__ constexpr uint32_t make_idesc_mxf8f6f4(uint32_t a_fmt, uint32_t b_fmt, uint32_t M, uint32_t N) {
-  return (a_fmt << 7) | (b_fmt << 10) | ((N >> 3) << 17) | (1u << 23) | ((M >> 4) << 24);
+__host__ __device__ constexpr uint32_t make_idesc_mxf8f6f4(uint32_t a_fmt, uint32_t b_fmt, uint32_t M, uint32_t N,
+                                                           uint32_t a_mn = 0, uint32_t b_mn = 0) {
+  return (a_fmt << 7) | (b_fmt << 10) | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) | (1u << 23) |
+         ((M >> 4) << 24);
 }
 __device__ __forceinline__ uint32_t idesc_with_sf_id(uint32_t idesc, uint32_t a_sf_id, uint32_t b_sf_id) {
   return idesc | (b_sf_id << 4) | (a_sf_id << 29);

@@ -47,14 +47,33 @@ class Comm:
         self._h = ctypes.c_void_p()
         L.check(L.lib.fp8_comm_init(ctypes.byref(self._h), raw, self.world, self.rank), "fp8_comm_init")
 
-    def allgather_fp8(self, w_shard, fmt="e4m3", out=None, scale=None, amax=None, stream=None):
-        """Returns (w_full uint8 [P*rows, cols], scale float[1], global amax float[1])."""
+    def precompute_amax(self, w_shards, out=None, stream=None):
+        """Global (all-reduced MAX) amax of each of this rank's weight shards: one fused amax launch
+        and one NCCL all-reduce per 48 weights (fp8_fsdp_precompute_amax).  float32 [len]."""
+        n = len(w_shards)
+        if out is None:
+            out = torch.empty(n, dtype=torch.float32, device=w_shards[0].device)
+        for i in range(0, n, L.AMAX_MULTI_MAX):
+            part = w_shards[i:i + L.AMAX_MULTI_MAX]
+            arr = (L.HP * len(part))(*[hp(w) for w in part])
+            L.check(L.lib.fp8_fsdp_precompute_amax(self._h, arr, len(part), ctypes.c_void_p(out.data_ptr() + 4 * i),
+                                                   _stream(stream)), "fp8_fsdp_precompute_amax")
+        return out
+
+    def allgather_fp8(self, w_shard, fmt="e4m3", out=None, scale=None, amax=None, amax_in=None, stream=None):
+        """Returns (w_full uint8 [P*rows, cols], scale float[1], global amax float[1]).
+        amax_in: the precomputed global amax (a float[1] view, e.g. precompute_amax(...)[i:i+1]):
+        skips the amax pass and the all-reduce."""
         rows, cols = w_shard.shape
         dev = w_shard.device
         if out is None:
             out = torch.empty((self.world * rows, cols), dtype=torch.uint8, device=dev)
         if scale is None:
             scale = torch.empty(1, dtype=torch.float32, device=dev)
+        if amax_in is not None:
+            L.check(L.lib.fp8_fsdp_allgather_ex(self._h, hp(w_shard), FORMATS[fmt], _ptr(amax_in), _ptr(out),
+                                                _ptr(scale), None, None, 0, _stream(stream)), "fp8_fsdp_allgather_ex")
+            return out, scale, amax_in
         if amax is None:
             amax = torch.empty(1, dtype=torch.float32, device=dev)
         L.check(L.lib.fp8_fsdp_allgather(self._h, hp(w_shard), FORMATS[fmt], _ptr(out), _ptr(scale), _ptr(amax),

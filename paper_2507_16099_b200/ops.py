@@ -13,7 +13,7 @@ from . import _lib as L
 
 FORMATS = {"e4m3": L.E4M3, "e5m2": L.E5M2}
 GRANS = {"tensor": L.GRAN_TENSOR, "row": L.GRAN_ROW, "col": L.GRAN_COL, "row_col": L.GRAN_ROW_COL,
-         "mx32": L.GRAN_MX32}
+         "mx32": L.GRAN_MX32, "mx32_rm": L.GRAN_MX32_RM}
 RECIPES = {"tensorwise": L.RECIPE_TENSORWISE, "rowwise": L.RECIPE_ROWWISE, "mxfp8": L.RECIPE_MXFP8,
            "rowwise_gw_hp": L.RECIPE_ROWWISE_GW_HP}
 MX_ROUND = {"floor": L.MX_FLOOR, "rceil": L.MX_RCEIL}
@@ -55,18 +55,33 @@ def amax(x, gran="tensor", stream=None):
     return out
 
 
+def amax_multi(xs, out=None, stream=None):
+    """fp8_amax_multi: tensorwise amax of every tensor in `xs` in one launch (per 48 tensors).
+    Returns float32 [len(xs)]."""
+    n = len(xs)
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device=xs[0].device)
+    for i in range(0, n, L.AMAX_MULTI_MAX):
+        part = xs[i:i + L.AMAX_MULTI_MAX]
+        arr = (L.HP * len(part))(*[hp(x) for x in part])
+        L.check(L.lib.fp8_amax_multi(arr, len(part), ctypes.c_void_p(out.data_ptr() + 4 * i), _stream(stream)),
+                "fp8_amax_multi")
+    return out
+
+
 def cast(x, fmt="e4m3", gran="tensor", want_q=True, want_qt=False, mx_round="floor", amax_in=None,
          stream=None):
-    """fp8_cast_scaled.  Returns a dict with q [R,C] / q_t [C,R] (uint8), scale(s), amax."""
+    """fp8_cast_scaled.  Returns a dict with q [R,C] / q_t [C,R] (uint8), scale(s), amax.
+    gran "mx32_rm": q_t holds the dim1 codes in the input's layout [R,C] (not transposed)."""
     R, C = x.shape
     dev = x.device
     out = {"q": None, "q_t": None, "scale": None, "scale_t": None, "amax": None, "amax_t": None}
     if want_q:
         out["q"] = torch.empty((R, C), dtype=torch.uint8, device=dev)
     if want_qt:
-        out["q_t"] = torch.empty((C, R), dtype=torch.uint8, device=dev)
+        out["q_t"] = torch.empty((R, C) if gran == "mx32_rm" else (C, R), dtype=torch.uint8, device=dev)
     f32 = dict(dtype=torch.float32, device=dev)
-    if gran == "mx32":
+    if gran in ("mx32", "mx32_rm"):
         if want_q:
             out["scale"] = torch.empty(sf_bytes(R, C), dtype=torch.uint8, device=dev)
         if want_qt:

@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol(L):
 
 
 def test_abi_version(L):
-    assert L.lib.fp8_abi_version() == 3
+    assert L.lib.fp8_abi_version() == 4
 
 
 def test_sizes_host_only(L):
@@ -78,9 +78,9 @@ def test_validation_returns_before_launch(L):
     # GEMM K not multiple of 16
     assert L.lib.fp8_gemm(16, 0, 0, 32, 48, 0, 0, 64, L.GRAN_TENSOR, 128, 128, 40, 48, 48, 80, L.DT_BF16, 128,
                           None) == L.FP8_EALIGN
-    # MX GEMM with an MN-major operand is unsupported
-    assert L.lib.fp8_gemm(16, 0, 1, 32, 48, 0, 0, 64, L.GRAN_MX32, 128, 128, 128, 128, 128, 80, L.DT_BF16, 128,
-                          None) == L.FP8_EUNSUPPORTED
+    # MX GEMM needs M, N, K multiples of 128 (either operand major)
+    assert L.lib.fp8_gemm(16, 0, 1, 32, 48, 0, 0, 64, L.GRAN_MX32, 128, 128, 144, 128, 144, 80, L.DT_BF16, 128,
+                          None) == L.FP8_EALIGN
     # linear: workspace too small
     cfg = L.LinearCfg(L.RECIPE_TENSORWISE, L.E4M3, L.E5M2, L.MX_FLOOR, L.DT_BF16)
     st = L.lib.fp8_linear_fwd(ctypes.byref(cfg), L.HP(16, L.DT_BF16, 128, 128, 128), L.HP(32, L.DT_BF16, 128, 128, 128),

@@ -176,16 +176,19 @@ def test_amax_entry(gran):
 @pytest.mark.parametrize("mode", [omx.FLOOR, omx.RCEIL])
 @pytest.mark.parametrize("fmt", [E4M3, E5M2])
 @pytest.mark.parametrize("shape", [(128, 128), (256, 384)])
-def test_mx_cast(mode, fmt, shape):
+@pytest.mark.parametrize("gran,want_q", [("mx32", True), ("mx32_rm", True), ("mx32_rm", False)])
+def test_mx_cast(mode, fmt, shape, gran, want_q):
+    # mx32_rm: the dim1 codes stay in the input's [R, C] layout (no transpose), same bytes
     x = synth.tensor_c4("x", shape, seed=0)
     q0, s0 = omx.quantize_dim0(x, fmt, mode)
     q1, s1 = omx.quantize_dim1(x, fmt, mode)
-    out = ops.cast(_dev(x, torch.bfloat16), FMTNAME[fmt], "mx32", want_q=True, want_qt=True, mx_round=mode)
+    out = ops.cast(_dev(x, torch.bfloat16), FMTNAME[fmt], gran, want_q=want_q, want_qt=True, mx_round=mode)
     R, C = shape
-    assert np.array_equal(_unblock(out["scale"], R, C), s0)
+    if want_q:
+        assert np.array_equal(_unblock(out["scale"], R, C), s0)
+        assert np.array_equal(_np(out["q"]), q0)
     assert np.array_equal(_unblock(out["scale_t"], C, R), s1)
-    assert np.array_equal(_np(out["q"]), q0)
-    assert np.array_equal(_np(out["q_t"]), q1)
+    assert np.array_equal(_np(out["q_t"]), q1.T if gran == "mx32_rm" else q1)
 
 
 def test_mx_cast_fp32_subnormal_block():
@@ -283,16 +286,21 @@ def _block(codes_logical):
 
 @pytest.mark.parametrize("fa,fb", [(E4M3, E4M3), (E5M2, E4M3)])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 128), (256, 384, 512), (384, 640, 384)])
-def test_gemm_mx_tolerance(fa, fb, M, N, K, cta_group):
+@pytest.mark.parametrize("majors", ["KK", "KM", "MM", "MK"])
+def test_gemm_mx_tolerance(fa, fb, M, N, K, majors, cta_group):
+    # MN-major operands keep the same logical [rows, K/32] scale factors (blocked layout)
     a = synth.tensor_c4("x", (M, K), seed=6)
     b = synth.tensor_c4("w", (N, K), seed=6)
     qa, sa = omx.quantize_dim0(a, fa)
     qb, sb = omx.quantize_dim0(b, fb)
     ref = ogemm.mx_gemm_ref(qa, sa, fa, qb, sb, fb)
     bd = ogemm.mx_abs_bound(qa, sa, fa, qb, sb, fb)
-    D = ops.gemm(torch.from_numpy(qa).cuda(), FMTNAME[fa], torch.from_numpy(_block(sa)).cuda(),
-                 torch.from_numpy(qb).cuda(), FMTNAME[fb], torch.from_numpy(_block(sb)).cuda(), "mx32",
-                 out_dtype=torch.float32)
+    a_mn, b_mn = majors[0] == "M", majors[1] == "M"
+    A = torch.from_numpy(np.ascontiguousarray(qa.T if a_mn else qa)).cuda()
+    B = torch.from_numpy(np.ascontiguousarray(qb.T if b_mn else qb)).cuda()
+    D = ops.gemm(A, FMTNAME[fa], torch.from_numpy(_block(sa)).cuda(),
+                 B, FMTNAME[fb], torch.from_numpy(_block(sb)).cuda(), "mx32",
+                 out_dtype=torch.float32, a_mn=a_mn, b_mn=b_mn)
     _tol_check(_np(D).astype(np.float64), ref, bd)
 
 
@@ -329,6 +337,26 @@ def test_linear_fwd_bwd(recipe, cfg, M, N, K):
     X = _dev(x, dt)
     Y = plan.forward(X, _dev(w, dt), saved)
     DX, DW = plan.backward(_dev(dy, dt), saved, x=X)
+    torch.cuda.synchronize()
+    _tol_check(_np(Y).astype(np.float64), y, yb)
+    _tol_check(_np(DX).astype(np.float64), dx, dxb)
+    _tol_check(_np(DW).astype(np.float64), dw, dwb)
+
+
+@pytest.mark.parametrize("transposed", ["0", "1"], ids=["dim1_rowmajor_mn", "dim1_transposed_k"])
+@pytest.mark.parametrize("mx_round", ["floor", "rceil"])
+def test_linear_mx_dim1_layouts(transposed, mx_round, monkeypatch):
+    """MXFP8 backward operands: dim1 codes kept row-major and read MN-major (default) or written
+    transposed and read K-major (FP8T_MX_TRANSPOSED=1): same results within the bound."""
+    monkeypatch.setenv("FP8T_MX_TRANSPOSED", transposed)
+    M, N, K = 384, 640, 256
+    x, w, dy = synth.linear_inputs("c4", M, N, K, seed=2)
+    y, yb, _ = olin.forward(x, w, "mxfp8", mx_mode=mx_round)
+    dx, dxb, dw, dwb, _ = olin.backward(x, w, dy, "mxfp8", mx_mode=mx_round)
+    plan = ops.LinearPlan(M, N, K, recipe="mxfp8", out_dtype=torch.float32, mx_round=mx_round)
+    saved = plan.new_saved()
+    Y = plan.forward(_dev(x, torch.bfloat16), _dev(w, torch.bfloat16), saved)
+    DX, DW = plan.backward(_dev(dy, torch.bfloat16), saved)
     torch.cuda.synchronize()
     _tol_check(_np(Y).astype(np.float64), y, yb)
     _tol_check(_np(DX).astype(np.float64), dx, dxb)
@@ -407,9 +435,46 @@ def test_fsdp_allgather_single_rank_equals_cast():
         dx2, dw2 = plan.backward(G, s2, w_fp8=(wq, ws_))
         torch.cuda.synchronize()
         assert torch.equal(y1, y2) and torch.equal(dx1, dx2) and torch.equal(dw1, dw2)
+        # precomputed global amax for several weights at once (one launch + one all-reduce), then
+        # the gather with amax_in: same bytes and scale as the self-contained gather
+        ws_list = [synth.tensor_c2("w", shp, seed=7 + i) for i, shp in enumerate([(384, 512), (128, 256), (272, 96)])]
+        dev_list = [_dev(v, torch.bfloat16) for v in ws_list]
+        am = comm.precompute_amax(dev_list)
+        torch.cuda.synchronize()
+        assert np.array_equal(_bits(_np(am)), _bits(np.array([fp8.amax(v) for v in ws_list], np.float32)))
+        for i, v in enumerate(ws_list):
+            q, s, _ = fp8.cast_tensorwise(v, E4M3)
+            wq3, ws3, _ = comm.allgather_fp8(dev_list[i], "e4m3", amax_in=am[i:i + 1])
+            torch.cuda.synchronize()
+            assert _bits(_np(ws3))[0] == _bits(s).reshape(-1)[0]
+            assert np.array_equal(_np(wq3), q)
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_amax_multi():
+    """fp8_amax_multi: many tensors (bf16 and fp32, strided rows, ragged sizes, one all-zero) in one
+    launch == the oracle's per-tensor amax, bit-exact."""
+    shapes = [(16, 16), (48, 4096), (1024, 1040), (16, 16), (4096, 2048), (272, 400), (128, 96)] * 7
+    xs, want = [], []
+    for i, shp in enumerate(shapes[:48]):
+        v = synth.tensor_c3("w", shp, seed=20 + i)
+        if i == 3:
+            v = np.zeros(shp, np.float32)
+        dt = torch.float32 if i % 3 == 1 else torch.bfloat16
+        d = _dev(v, dt)
+        want.append(fp8.amax(_np(d.float()).astype(np.float32)))
+        if i % 5 == 2:   # strided rows: a column slice of a wider buffer
+            wide = torch.zeros((shp[0], shp[1] + 32), dtype=dt, device="cuda")
+            wide[:, 16:16 + shp[1]] = d
+            d = wide[:, 16:16 + shp[1]]
+        xs.append(d)
+    got = ops.amax_multi(xs)
+    assert np.array_equal(_bits(_np(got)), _bits(np.array(want, np.float32)))
+    # > 48 tensors: split over several launches by the binding
+    got2 = ops.amax_multi(xs + xs[:5])
+    assert np.array_equal(_bits(_np(got2)), _bits(np.array(want + want[:5], np.float32)))
 
 
 @pytest.mark.parametrize("recipe,cfg,M,N,K", [("tensorwise", "c2", 272, 400, 528), ("rowwise", "c3", 384, 400, 272),

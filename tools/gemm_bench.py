@@ -44,11 +44,25 @@ def main():
         if M % 128 == 0 and N % 128 == 0 and K % 128 == 0:   # MXFP8 block-scaled kind, codes 127 (=1.0)
             sfa = torch.full((M * K // 32,), 127, dtype=torch.uint8, device="cuda")
             sfb = torch.full((N * K // 32,), 127, dtype=torch.uint8, device="cuda")
-            for dbg in ("0", "1", "2", "6"):   # 2: no tcgen05.cp of scales; 4: no scale TMA loads
+            for dbg in os.environ.get("GEMM_BENCH_MX_DBG", "0,2").split(","):
+                # 1: no epilogue stores; 2: no tcgen05.cp of scales; 4: no scale TMA loads
                 os.environ["FP8T_GEMM_DEBUG"] = dbg
                 ms = timeit(lambda: ops.gemm(A, "e4m3", sfa, B, "e4m3", sfb, "mx32"))
                 row["ours_mx" + ("" if dbg == "0" else "_dbg" + dbg)] = round(flops / ms / 1e9)
             os.environ["FP8T_GEMM_DEBUG"] = "0"
+            # MN-major operands (the MXFP8 backward's layout): A stored [K,M], B stored [K,N]
+            At, Bt = A.t().contiguous(), B.t().contiguous()
+            ms = timeit(lambda: ops.gemm(At, "e4m3", sfa, Bt, "e4m3", sfb, "mx32", a_mn=True, b_mn=True))
+            row["ours_mx_mnmn"] = round(flops / ms / 1e9)
+            del At, Bt
+            try:   # cuBLASLt MXFP8 (block-scaled) through torch._scaled_mm with e8m0 scales
+                e8 = torch.float8_e8m0fnu
+                ms = timeit(lambda: torch._scaled_mm(A.view(torch.float8_e4m3fn), B.view(torch.float8_e4m3fn).t(),
+                                                     scale_a=sfa.view(e8), scale_b=sfb.view(e8),
+                                                     out_dtype=torch.bfloat16))
+                row["cublaslt_mxfp8_tflops"] = round(flops / ms / 1e9)
+            except Exception as e:  # noqa: BLE001
+                row["cublaslt_mxfp8_tflops"] = f"n/a: {e}"[:120]
         try:
             a8 = A.view(torch.float8_e4m3fn)
             b8 = B.view(torch.float8_e4m3fn)

@@ -1,17 +1,26 @@
 # Round profile captures (run under gpurun from the repo root):
 #   bash tools/profile_round.sh <tag>
-# 1. launch list of one bench step per config (cold-cache, serialised: compare shares)
-# 2. ncu --set full of the top kernel (GEMM) and the cast kernels of the c2 step
+# 1. bench lines per config (the numbers; never taken under a profiler)
+# 2. launch list of one bench step per config (cold-cache, serialised: compare shares)
+# 3. ncu --set full of the two GEMM launches of one step (fwd; grouped dX+dW) for c2 and c4,
+#    and of the cast kernels of the c2 step
 TAG=${1:-r01}
 mkdir -p gpurun_out
+for CFG in c2 c4 c3w1 c3w1hp; do
+  timeout 600 python bench.py --config $CFG > gpurun_out/${TAG}_bench_${CFG}.json 2> gpurun_out/${TAG}_bench_${CFG}.err
+done
 for CFG in c2 c4 c3w1; do
   B="python bench.py --config $CFG --steps 2 --warmup 3 --e2e-steps 0 --no-bf16 --no-cpu-baseline"
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"amax|cast|gemm|transpose" -c 60 --csv --log-file gpurun_out/${TAG}_launches_${CFG}.csv $B > gpurun_out/${TAG}_launches_${CFG}.log 2>&1
+    -k regex:"amax|cast|gemm|transpose" -c 80 --csv --log-file gpurun_out/${TAG}_launches_${CFG}.csv $B > gpurun_out/${TAG}_launches_${CFG}.log 2>&1
+done
+for CFG in c2 c4; do
+  B="python bench.py --config $CFG --steps 1 --warmup 3 --e2e-steps 0 --no-bf16 --no-cpu-baseline"
+  # warm-up steps launch 2 GEMMs each: skip them, capture the fwd and the grouped bwd launch of step 4
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:fp8_gemm -s 6 -c 2 \
+    -o gpurun_out/${TAG}_gemm_${CFG} $B > gpurun_out/${TAG}_gemm_${CFG}.log 2>&1
 done
 B="python bench.py --config c2 --steps 1 --warmup 3 --e2e-steps 0 --no-bf16 --no-cpu-baseline"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fp8_gemm -s 3 -c 3 \
-  -o gpurun_out/${TAG}_gemm_c2 $B > gpurun_out/${TAG}_gemm_c2.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"amax|cast" -s 6 -c 6 \
   -o gpurun_out/${TAG}_casts_c2 $B > gpurun_out/${TAG}_casts_c2.log 2>&1
-ls -la gpurun_out | tail -20
+ls -la gpurun_out | tail -30
