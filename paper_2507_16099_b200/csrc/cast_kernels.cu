@@ -514,6 +514,155 @@ __global__ void __launch_bounds__(256, 3) mx_cast_kernel(const T* __restrict__ x
   }
 }
 
+// ---------------------------------------------------------------------------
+// MXFP8 cast, TMA-pipelined persistent variant (bf16 input; rows, cols multiples of 128).
+// Same arithmetic and outputs as mx_cast_kernel.  CTA b walks tiles b, b+G, b+2G, ...;
+// thread 0 streams the 128 x 128 bf16 tiles (32 KB) into an ST-deep shared-memory ring with
+// cp.async.bulk.tensor, so the HBM reads of the next ST tiles stay in flight while the 8 warps
+// reduce and cast the current one.  |x| maxima run on packed bf16 pairs (__vmaxu2 on the raw
+// bits), the power-of-two scaling on fp32 pairs (__fmul2_rn, IEEE RN, no FTZ), and each
+// tile's two 512-byte E8M0 scale tiles leave as 16-byte stores.
+// ---------------------------------------------------------------------------
+template <int ST, bool TR1> struct MxSmem {
+  static constexpr int STAGE = 128 * 256;             // one bf16 tile, row-major, 256 B per row
+  static constexpr int RED = ST * STAGE;              // u32 [8][64]: per-warp packed column maxima
+  static constexpr int MULT = RED + 8 * 64 * 4;       // f32 [4][128]: dim1 multipliers
+  static constexpr int SF0 = MULT + 4 * 128 * 4;      // u8 [512]: dim0 E8M0 tile (blocked layout)
+  static constexpr int SF1 = SF0 + 512;               // u8 [512]: dim1 E8M0 tile
+  static constexpr int TILE = SF1 + 512;              // u32 [128*32]: transposed staging (TR1)
+  static constexpr int BAR = TILE + (TR1 ? 128 * 32 * 4 : 0);
+  static constexpr int BYTES = BAR + ST * 8;
+};
+
+// 8 bf16 (4 packed words) -> 8 FP8 codes of x * mult (pairs of fp32 multipliers m[0..3]).
+template <int FMT>
+__device__ __forceinline__ uint2 cast8_bf16x2(const uint32_t (&w)[4], const float2 (&m)[4]) {
+  uint32_t b[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 p = __fmul2_rn(make_float2(__uint_as_float(w[j] << 16), __uint_as_float(w[j] & 0xFFFF0000u)), m[j]);
+    b[j] = FMT == 0 ? cvt_e4m3x2(p.y, p.x) : cvt_e5m2x2(p.y, p.x);
+  }
+  return make_uint2(b[0] | (b[1] << 16), b[2] | (b[3] << 16));
+}
+
+template <int FMT, bool RCEIL, bool DIM0, bool DIM1, bool TR1, int ST>
+__global__ void __launch_bounds__(256) mx_cast_tma_kernel(const __grid_constant__ CUtensorMap tmap, int64_t R,
+                                                          int64_t C, uint8_t* __restrict__ q0,
+                                                          uint8_t* __restrict__ sf0, uint8_t* __restrict__ q1,
+                                                          uint8_t* __restrict__ sf1) {
+  using L = MxSmem<ST, TR1>;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint32_t(*red)[64] = reinterpret_cast<uint32_t(*)[64]>(sm + L::RED);
+  float(*mult1)[128] = reinterpret_cast<float(*)[128]>(sm + L::MULT);
+  uint8_t* s_sf0 = sm + L::SF0;
+  uint8_t* s_sf1 = sm + L::SF1;
+  uint32_t* tile = reinterpret_cast<uint32_t*>(sm + L::TILE);
+  const uint32_t bar0 = smem_u32(sm + L::BAR), stage0 = smem_u32(sm);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int tiles_x = (int)(C >> 7);
+  const int num_tiles = tiles_x * (int)(R >> 7);
+  const int G = (int)gridDim.x;
+  auto issue = [&](int k) {   // thread 0: TMA of this CTA's k-th tile into stage k % ST
+    const int id = (int)blockIdx.x + k * G;
+    if (id < num_tiles) {
+      const uint32_t bar = bar0 + 8 * (k % ST);
+      mbar_arrive_expect_tx(bar, L::STAGE);
+      tma_load_2d(stage0 + (k % ST) * L::STAGE, &tmap, (id % tiles_x) * 128, (id / tiles_x) * 128, bar,
+                  l2_policy_evict_first());
+    }
+  };
+  if (t == 0) {
+    tma_prefetch_desc(&tmap);
+    for (int i = 0; i < ST; ++i) mbar_init(bar0 + 8 * i, 1);
+    fence_mbar_init();
+    for (int k = 0; k < ST; ++k) issue(k);
+  }
+  __syncthreads();
+  const int cc = (t & 15) * 8, rbase = 8 * (t >> 4);
+  for (int k = 0;; ++k) {
+    const int id = (int)blockIdx.x + k * G;
+    if (id >= num_tiles) break;
+    const int64_t r0 = (int64_t)(id / tiles_x) * 128, c0 = (int64_t)(id % tiles_x) * 128;
+    mbar_wait(bar0 + 8 * (k % ST), (uint32_t)(k / ST) & 1u);
+    uint4 raw[8];
+    const uint8_t* sp = sm + (k % ST) * L::STAGE + rbase * 256 + cc * 2;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) raw[i] = *reinterpret_cast<const uint4*>(sp + i * 256);
+    __syncthreads();                       // (1) stage consumed by every thread
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(k + ST);
+    }
+
+    // one pass over the 8 rows: dim0 block codes + casts, packed dim1 column maxima
+    uint32_t cmw[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
+      uint32_t a[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a[j] = w[j] & 0x7FFF7FFFu;
+        if (DIM1) cmw[j] = __vmaxu2(cmw[j], a[j]);
+      }
+      if (DIM0) {
+        const uint32_t m2 = __vmaxu2(__vmaxu2(a[0], a[1]), __vmaxu2(a[2], a[3]));
+        uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+        const uint32_t code = e8m0_code<FMT, RCEIL>(m << 16);
+        const float mu = e8m0_mult(code);
+        const float2 mm[4] = {make_float2(mu, mu), make_float2(mu, mu), make_float2(mu, mu), make_float2(mu, mu)};
+        *reinterpret_cast<uint2*>(q0 + (r0 + rbase + i) * C + c0 + cc) = cast8_bf16x2<FMT>(w, mm);
+        const int rr = rbase + i;
+        if ((t & 3) == 0) s_sf0[(rr & 31) * 16 + (rr >> 5) * 4 + (cc >> 5)] = (uint8_t)code;
+      }
+    }
+    const int64_t base0 = ((r0 >> 7) * (C >> 7) + (c0 >> 7)) * 512;
+    if (DIM1) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cmw[j] = __vmaxu2(cmw[j], __shfl_xor_sync(0xffffffffu, cmw[j], 16));
+      if (lane < 16) *reinterpret_cast<uint4*>(&red[warp][cc >> 1]) = make_uint4(cmw[0], cmw[1], cmw[2], cmw[3]);
+      __syncthreads();                     // (2)
+      {
+        const int j = t >> 6, wp = t & 63;   // 32-row block j, columns 2wp, 2wp+1
+        const uint32_t m2 = __vmaxu2(red[2 * j][wp], red[2 * j + 1][wp]);
+        const uint32_t clo = e8m0_code<FMT, RCEIL>(m2 << 16), chi = e8m0_code<FMT, RCEIL>(m2 & 0xFFFF0000u);
+        *reinterpret_cast<float2*>(&mult1[j][2 * wp]) = make_float2(e8m0_mult(clo), e8m0_mult(chi));
+        const int c = 2 * wp;
+        s_sf1[(c & 31) * 16 + (c >> 5) * 4 + j] = (uint8_t)clo;
+        s_sf1[((c + 1) & 31) * 16 + ((c + 1) >> 5) * 4 + j] = (uint8_t)chi;
+      }
+      __syncthreads();                     // (3)
+      if (DIM0 && t < 32)
+        *reinterpret_cast<uint4*>(sf0 + base0 + t * 16) = *reinterpret_cast<const uint4*>(s_sf0 + t * 16);
+      if (t >= 32 && t < 64)
+        *reinterpret_cast<uint4*>(sf1 + ((c0 >> 7) * (R >> 7) + (r0 >> 7)) * 512 + (t - 32) * 16) =
+            *reinterpret_cast<const uint4*>(s_sf1 + (t - 32) * 16);
+      const int j = t >> 6;                // all 8 rows of this thread lie in 32-row block j
+      const float4 ma = *reinterpret_cast<const float4*>(&mult1[j][cc]);
+      const float4 mb = *reinterpret_cast<const float4*>(&mult1[j][cc + 4]);
+      const float2 mu[4] = {make_float2(ma.x, ma.y), make_float2(ma.z, ma.w), make_float2(mb.x, mb.y),
+                            make_float2(mb.z, mb.w)};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
+        const uint2 b = cast8_bf16x2<FMT>(w, mu);
+        if (TR1) *reinterpret_cast<uint2*>(&tile[swz(rbase + i, cc >> 2)]) = b;
+        else *reinterpret_cast<uint2*>(q1 + (r0 + rbase + i) * C + c0 + cc) = b;
+      }
+      if (TR1) {
+        __syncthreads();                   // (4)
+        store_transposed(tile, q1, R, r0, c0, 128, 128);
+      }
+    } else {
+      __syncthreads();
+      if (t < 32) *reinterpret_cast<uint4*>(sf0 + base0 + t * 16) = *reinterpret_cast<const uint4*>(s_sf0 + t * 16);
+    }
+  }
+}
+
 // FP8 byte transpose [R, C] -> [C, R] (R, C multiples of 16).
 __global__ void __launch_bounds__(256) transpose_u8_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C,
                                                            uint8_t* __restrict__ out) {
@@ -648,8 +797,63 @@ static cudaError_t mx_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, 
   return cudaGetLastError();
 }
 
+template <int FMT, bool RC, bool D0, bool D1, bool TR, int ST>
+static cudaError_t mx_tma_go(const CUtensorMap& m, int64_t R, int64_t C, uint8_t* q0, uint8_t* sf0, uint8_t* q1,
+                             uint8_t* sf1, cudaStream_t s) {
+  auto kern = mx_cast_tma_kernel<FMT, RC, D0, D1, TR, ST>;
+  constexpr int smem = MxSmem<ST, TR>::BYTES;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t tiles = (R >> 7) * (C >> 7);
+  int64_t cap = (int64_t)sm_count() * (TR ? 1 : 2);
+  const char* g = getenv("FP8T_CAST_GRID");   // tests: cap the persistent grid (many tiles per CTA)
+  if (g && atoi(g) > 0 && atoi(g) < cap) cap = atoi(g);
+  LaunchScope ls(K_MX, s);
+  kern<<<(unsigned)(tiles < cap ? tiles : cap), 256, smem, s>>>(m, R, C, q0, sf0, q1, sf1);
+  return cudaGetLastError();
+}
+
+template <int FMT, bool RC>
+static cudaError_t mx_tma_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, uint8_t* q0, uint8_t* sf0,
+                                   uint8_t* q1, uint8_t* sf1, bool tr1, cudaStream_t s) {
+  auto enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)R};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {128, 128};
+  cuuint32_t estr[2] = {1, 1};
+  if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  if (q0 && q1) {
+    if (tr1) return mx_tma_go<FMT, RC, true, true, true, 4>(m, R, C, q0, sf0, q1, sf1, s);
+    return mx_tma_go<FMT, RC, true, true, false, 3>(m, R, C, q0, sf0, q1, sf1, s);
+  }
+  if (q0) return mx_tma_go<FMT, RC, true, false, false, 3>(m, R, C, q0, sf0, q1, sf1, s);
+  if (tr1) return mx_tma_go<FMT, RC, false, true, true, 4>(m, R, C, q0, sf0, q1, sf1, s);
+  return mx_tma_go<FMT, RC, false, true, false, 3>(m, R, C, q0, sf0, q1, sf1, s);
+}
+
+// FP8T_MX_CAST=0 selects the register-only mx_cast_kernel (A/B comparisons; fp32 inputs always use it).
+static bool mx_use_tma() {
+  const char* e = getenv("FP8T_MX_CAST");
+  return !(e && e[0] == '0');
+}
+
 cudaError_t launch_mx_cast(const void* x, bool bf16, int fmt, bool rceil, int64_t R, int64_t C, int64_t ld,
                            uint8_t* q0, uint8_t* sf0, uint8_t* q1, uint8_t* sf1, cudaStream_t s, bool tr1) {
+  if (bf16 && mx_use_tma()) {
+    if (fmt == 0) return rceil ? mx_tma_launch_t<0, true>(x, R, C, ld, q0, sf0, q1, sf1, tr1, s)
+                               : mx_tma_launch_t<0, false>(x, R, C, ld, q0, sf0, q1, sf1, tr1, s);
+    return rceil ? mx_tma_launch_t<1, true>(x, R, C, ld, q0, sf0, q1, sf1, tr1, s)
+                 : mx_tma_launch_t<1, false>(x, R, C, ld, q0, sf0, q1, sf1, tr1, s);
+  }
 #define FP8T_MX(T)                                                                                  \
   if (fmt == 0) return rceil ? mx_launch_t<T, 0, true>(x, R, C, ld, q0, sf0, q1, sf1, tr1, s)       \
                              : mx_launch_t<T, 0, false>(x, R, C, ld, q0, sf0, q1, sf1, tr1, s);     \

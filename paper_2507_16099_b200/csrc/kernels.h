@@ -1,11 +1,16 @@
 // Internal launcher declarations (not part of the C-ABI).
 #pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
 namespace fp8t {
 
 void count_launch();
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (nullptr if unavailable).
+PFN_cuTensorMapEncodeTiled_v12000 get_encode();
 
 // Launch accounting + optional per-launch CUDA-event timing (fp8_profile_enable).
 enum { K_AMAX = 0, K_CAST = 1, K_MX = 2, K_TRANSPOSE = 3, K_GEMM = 4, K_GEMM_MX = 5, K_GEMM_BF16 = 6 };

@@ -519,3 +519,40 @@ def test_amax_handover_chain():
     torch.cuda.synchronize()
     assert torch.equal(DXa, DXb) and torch.equal(DWa, DWb)
     assert dx_amax.item() == DXb.float().abs().max().item()
+
+
+@pytest.mark.parametrize("grid", ["1", "3"])
+@pytest.mark.parametrize("gran", ["mx32", "mx32_rm"])
+@pytest.mark.parametrize("fmt,mode", [(E4M3, omx.FLOOR), (E5M2, omx.RCEIL)])
+def test_mx_cast_persistent_ring(grid, gran, fmt, mode, monkeypatch):
+    # the TMA-pipelined MX cast walks many tiles per CTA when the grid is capped: every
+    # shared-memory ring slot is refilled several times (mbarrier parity wrap-around)
+    monkeypatch.setenv("FP8T_CAST_GRID", grid)
+    R, C = 512, 1280   # 40 tiles
+    x = synth.tensor_c4("x", (R, C), seed=5)
+    q0, s0 = omx.quantize_dim0(x, fmt, mode)
+    q1, s1 = omx.quantize_dim1(x, fmt, mode)
+    out = ops.cast(_dev(x, torch.bfloat16), FMTNAME[fmt], gran, want_q=True, want_qt=True, mx_round=mode)
+    assert np.array_equal(_unblock(out["scale"], R, C), s0)
+    assert np.array_equal(_np(out["q"]), q0)
+    assert np.array_equal(_unblock(out["scale_t"], C, R), s1)
+    assert np.array_equal(_np(out["q_t"]), q1.T if gran == "mx32_rm" else q1)
+    # dim1 only
+    out = ops.cast(_dev(x, torch.bfloat16), FMTNAME[fmt], gran, want_q=False, want_qt=True, mx_round=mode)
+    assert np.array_equal(_unblock(out["scale_t"], C, R), s1)
+    assert np.array_equal(_np(out["q_t"]), q1.T if gran == "mx32_rm" else q1)
+
+
+@pytest.mark.parametrize("impl", ["0", "1"])
+def test_mx_cast_impls_agree_c4_sized(impl, monkeypatch):
+    # both MX cast kernels (register-only: FP8T_MX_CAST=0; TMA ring: default) on a C4-like
+    # tensor with many tiles per CTA, sampled rows against the oracle
+    monkeypatch.setenv("FP8T_MX_CAST", impl)
+    R, C = 2048, 8192
+    x = synth.tensor_c4("x", (R, C), seed=7)
+    out = ops.cast(_dev(x, torch.bfloat16), "e4m3", "mx32_rm", want_q=True, want_qt=True)
+    rows = slice(96, 160)   # straddles a 128-row tile and two 32-row blocks
+    q0, s0 = omx.quantize_dim0(x[rows], E4M3)
+    assert np.array_equal(_np(out["q"])[rows], q0)
+    q1, s1 = omx.quantize_dim1(x[:, 4000:4256], E4M3)
+    assert np.array_equal(_np(out["q_t"])[:, 4000:4256], q1.T)
