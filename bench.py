@@ -23,6 +23,10 @@ import sys
 import threading
 import time
 
+# NCCL writes its debug/version banner to stdout by default; the contract wants exactly one JSON
+# line on stdout, so route NCCL's log to stderr unless the caller chose a file.
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -264,8 +268,9 @@ def run_ours(a):
     cfg = CONFIGS[a.config]
     M, N, K = cfg["M"], cfg["N"], cfg["K"]
     fsdp = world > 1 or a.fsdp
-    if fsdp and cfg["recipe"] != "tensorwise":
-        raise SystemExit("FP8 all-gather is tensorwise-only (PAPER.md:596)")
+    if fsdp and cfg["recipe"] not in ("tensorwise", "mxfp8"):
+        raise SystemExit("low-precision weight all-gather: tensorwise (PAPER.md:596) or mxfp8 (SURVEY §8f.3)")
+    mx_fsdp = fsdp and cfg["recipe"] == "mxfp8"
     x, w_shard, dy, w_full_hp = make_inputs(cfg, M, N, K, rank, world, dev)
     if not fsdp:
         w_shard = w_full_hp
@@ -281,12 +286,24 @@ def run_ours(a):
         w_scale = torch.empty(1, dtype=torch.float32, device=dev)
         w_amax = torch.empty(1, dtype=torch.float32, device=dev)
         dw_shard = torch.empty((N // world, K), dtype=torch.bfloat16, device=dev)
+        if mx_fsdp:   # MXFP8 gather (fp8_fsdp_allgather_mx): dim0 + dim1 codes and E8M0 scales
+            mx_out = {"q": w_full, "scale": torch.empty(N * K // 32, dtype=torch.uint8, device=dev),
+                      "q_t": torch.empty((N, K), dtype=torch.uint8, device=dev),
+                      "scale_t": torch.empty(N * K // 32, dtype=torch.uint8, device=dev)}
+            mx_ws = torch.empty(N * K // 32, dtype=torch.uint8, device=dev)
+
+    def gather(ww):
+        """FSDP weight gather of this step: the pre-cast weight the linear consumes."""
+        if mx_fsdp:
+            return comm.allgather_mx(ww, "e4m3", out=mx_out, ws=mx_ws)
+        comm.allgather_fp8(ww, "e4m3", out=w_full, scale=w_scale, amax=w_amax)
+        return (w_full, w_scale)
 
     def step(xx=x, ww=w_shard, gg=dy):
         if fsdp:
-            comm.allgather_fp8(ww, "e4m3", out=w_full, scale=w_scale, amax=w_amax)
-            plan.forward(xx, None, saved, y=y, w_fp8=(w_full, w_scale))
-            plan.backward(gg, saved, dx=dx, dw=dw, w_fp8=(w_full, w_scale))
+            wf = gather(ww)
+            plan.forward(xx, None, saved, y=y, w_fp8=wf)
+            plan.backward(gg, saved, dx=dx, dw=dw, w_fp8=wf)
             if world > 1:
                 dist.reduce_scatter_tensor(dw_shard, dw)
         else:
@@ -354,7 +371,7 @@ def run_ours(a):
     # algorithmic cast bytes per step: per hp element read by amax 2 B, by the cast 2 B,
     # plus 1 B per FP8 layout written (X, W, dY each written in 2 layouts)
     if cfg["recipe"] == "mxfp8":          # one fused dim0+dim1 read, 2 FP8 layouts + E8M0 scales
-        cast_bytes = (M * K + N * K + M * N) * (2 + 2 + 2 / 32.0)
+        cast_bytes = (M * K + (N // world) * K + M * N) * (2 + 2 + 2 / 32.0)
         cast_kinds = (2,)
     elif cfg["recipe"] == "rowwise":       # amax read 2 + cast read 2 + row- and column-scaled layouts 1 + 1
         cast_bytes = (M * K + N * K + M * N) * 6
@@ -411,9 +428,9 @@ def run_ours(a):
             xd, wd, gd = ins[b]
             yo, dxo, dwo = outs[b]
             if fsdp:
-                comm.allgather_fp8(wd, "e4m3", out=w_full, scale=w_scale, amax=w_amax)
-                plan.forward(xd, None, saved, y=yo, w_fp8=(w_full, w_scale))
-                plan.backward(gd, saved, dx=dxo, dw=dw, w_fp8=(w_full, w_scale))
+                wf = gather(wd)
+                plan.forward(xd, None, saved, y=yo, w_fp8=wf)
+                plan.backward(gd, saved, dx=dxo, dw=dw, w_fp8=wf)
                 if world > 1:
                     dist.reduce_scatter_tensor(dwo, dw)
                 else:
@@ -498,7 +515,8 @@ def run_ours(a):
             "vs_baseline": None, "dtype": "fp8 (e4m3 x e5m2 codes, fp32 accumulate, bf16 out)",
             "data": "synthetic (seeded, device-generated, config value recipe)",
             "config": {"workload": cfg["workload"], "M_per_gpu": M, "N": N, "K": K, "recipe": cfg["recipe"],
-                       "parallelism": f"fsdp{world} (fp8 all-gather + amax all-reduce)" if fsdp else "single GPU",
+                       "parallelism": (f"fsdp{world} (mxfp8 all-gather, shard-local E8M0 scales)" if mx_fsdp else
+                                       f"fsdp{world} (fp8 all-gather + amax all-reduce)") if fsdp else "single GPU",
                        "l2": f"inputs larger than L2 (126 MB): X {M * K * 2 / 2**20:.0f} MiB, "
                              f"dY {M * N * 2 / 2**20:.0f} MiB, W {N * K * 2 / 2**20:.0f} MiB bf16; no flush"},
             "roofline": {"bound": "tensor", "kernel": "fp8_gemm_kernel (tcgen05 kind::%s)" %

@@ -214,9 +214,11 @@ fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, fp8_major_t major_a,
  *   tensorwise: X, W one scale each;  rowwise: X per row, W per row (over K);
  *   mxfp8: X, W blocks of 32 along K.
  * x [M,K], w [N,K] high precision; y [M,N] out_dtype, dense (ld = N).
- * w_fp8 (nullable): pre-cast tensorwise weight (e.g. from fp8_fsdp_allgather):
- *   w_fp8->q [N,K] codes + w_fp8->scale float[1]; then `w` may have ptr NULL
- *   (its rows/cols still give the shape).
+ * w_fp8 (nullable): pre-cast weight; then `w` may have ptr NULL (its rows/cols still give
+ *   the shape).  tensorwise (e.g. from fp8_fsdp_allgather): w_fp8->q [N,K] codes +
+ *   w_fp8->scale float[1].  mxfp8 (e.g. from fp8_fsdp_allgather_mx): gran FP8_GRAN_MX32_RM,
+ *   q + scale (dim0) for the forward, q_t + scale_t (dim1) for the backward's dX (the
+ *   forward then saves nothing for W).  Other recipes: FP8_EUNSUPPORTED.
  * saved: caller buffer of fp8_linear_saved_bytes() bytes; the forward writes
  *   the FP8 operands the backward needs (the X operand of dW and the W operand
  *   of dX with their scales, per the operand plan of DESIGN.md §2).  Tensorwise
@@ -303,6 +305,33 @@ fp8_status_t fp8_fsdp_precompute_amax(fp8_comm_t comm, const fp8_hp_t* w_shards,
 fp8_status_t fp8_fsdp_allgather_ex(fp8_comm_t comm, fp8_hp_t w_shard, fp8_format_t fmt,
                                    const float* amax_in, uint8_t* w_full, float* scale_out,
                                    float* amax_out, void* ws, size_t ws_bytes, void* stream);
+
+/* MXFP8 FSDP weight all-gather (MX formats for training, PAPER.md:735;
+ * FSDP gathers in low precision).  E8M0 block scales are shard-local -- a
+ * 32-block never crosses a shard boundary when rows_local % 128 == 0 -- so there is no amax
+ * exchange: rank r casts its shard [rows_local, cols] straight into slot r of
+ *   out->q       [nranks*rows_local, cols] u8  dim0 codes (blocks of 32 along cols = K: the
+ *                                               forward GEMM's W operand)
+ *   out->scale   E8M0 blocked [N, K/32]         (N = nranks*rows_local, K = cols)
+ *   out->q_t     [N, K] u8                      dim1 codes (blocks of 32 along rows = N: the dX
+ *                                               GEMM's W operand), row-major MX32_RM layout
+ *   out->scale_t E8M0 blocked [K, N/32]
+ * then one NCCL group all-gathers the four buffers, and the dim1 scales (gathered rank-major
+ * into `ws`) are re-tiled into the blocked layout of the full matrix.  The result is
+ * bit-identical on every rank and equal to fp8_cast_scaled(W, MX32_RM) of the unsharded W.
+ * out->gran must be FP8_GRAN_MX32_RM; out->q_t / out->scale_t may both be NULL (forward-only
+ * gather: dim0 only, no workspace).  rows_local, cols: multiples of 128.  `out` may be passed
+ * as w_fp8 to fp8_linear_fwd / fp8_linear_bwd with the mxfp8 recipe.
+ * ws: fp8_fsdp_mx_workspace_bytes(w_shard, nranks) bytes (device). */
+size_t fp8_fsdp_mx_workspace_bytes(fp8_hp_t w_shard, int nranks);
+fp8_status_t fp8_fsdp_allgather_mx(fp8_comm_t comm, fp8_hp_t w_shard, fp8_mx_round_t mx_round,
+                                   fp8_tensor_t* out, void* ws, size_t ws_bytes, void* stream);
+/* The re-tiling step of fp8_fsdp_allgather_mx, exported for composition: rank_major holds
+ * nranks consecutive E8M0 blocked buffers, buffer p = the dim1 scales of shard p
+ * ([cols, rows_local/32] blocked); out gets the blocked [cols, nranks*rows_local/32] buffer.
+ * rows_local, cols multiples of 128; pointers 16-byte aligned; async on `stream`. */
+fp8_status_t fp8_mx_scales_unshard(const uint8_t* rank_major, int nranks, int64_t rows_local,
+                                   int64_t cols, uint8_t* out, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Helpers

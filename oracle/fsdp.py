@@ -27,3 +27,20 @@ def allgather_ref(shards, fmt):
     s = fp8.scale_from_amax(a, fmt)
     q = np.concatenate([fp8.cast_scaled(w, s, fmt) for w in shards], axis=0)
     return q, s, np.float32(a)
+
+
+def allgather_mx_ref(shards, fmt, mode="floor"):
+    """MXFP8 FSDP gather (MX formats for training).
+
+    No amax exchange: every 32-block lies inside one shard (rows_local % 32 == 0), so each
+    rank quantizes its own shard (oracle.mx.quantize_dim0 / quantize_dim1) and the gather is
+    a concatenation:
+      dim0 (blocks along K):  codes and scales stacked along rows      -> [N, K], [N, K/32]
+      dim1 (blocks along N):  transposed codes / scales along columns  -> [K, N], [K, N/32]
+    Returns (q0, s0, q1, s1) in the orientation of oracle.mx.
+    """
+    from . import mx
+    d0 = [mx.quantize_dim0(w, fmt, mode) for w in shards]
+    d1 = [mx.quantize_dim1(w, fmt, mode) for w in shards]
+    return (np.concatenate([q for q, _ in d0], axis=0), np.concatenate([s for _, s in d0], axis=0),
+            np.concatenate([q for q, _ in d1], axis=1), np.concatenate([s for _, s in d1], axis=1))

@@ -77,6 +77,10 @@ SIGNATURES = {
     "fp8_fsdp_precompute_amax": (_c.c_int, [_c.c_void_p, _c.POINTER(HP), _c.c_int, _c.c_void_p, _c.c_void_p]),
     "fp8_fsdp_allgather_ex": (_c.c_int, [_c.c_void_p, HP, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_void_p,
                                          _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
+    "fp8_fsdp_mx_workspace_bytes": (_c.c_size_t, [HP, _c.c_int]),
+    "fp8_fsdp_allgather_mx": (_c.c_int, [_c.c_void_p, HP, _c.c_int, _c.POINTER(Tensor8), _c.c_void_p, _c.c_size_t,
+                                         _c.c_void_p]),
+    "fp8_mx_scales_unshard": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),
 }
 AMAX_MULTI_MAX = 48
 

@@ -452,6 +452,29 @@ fp8_status_t check_cfg(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_
   return FP8_OK;
 }
 
+// Pre-cast weight (FSDP gathers): tensorwise codes + float scale, or MXFP8 dim0 (forward) and
+// dim1 (backward dX) codes with E8M0 scales in the layout the backward GEMMs read.
+fp8_status_t check_w_fp8(const fp8_linear_cfg_t* cfg, const fp8_tensor_t* w_fp8, int64_t N, int64_t K, bool bwd_dx) {
+  if (w_fp8->rows != N || w_fp8->cols != K) return fail(FP8_EINVAL, "w_fp8 shape");
+  if (w_fp8->fmt != cfg->fmt_fwd) return fail(FP8_EINVAL, "w_fp8 format != cfg->fmt_fwd");
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    FP8T_TRY(check_ptr(w_fp8->q, "w_fp8->q"));
+    if (!w_fp8->scale) return fail(FP8_EINVAL, "w_fp8->scale: null pointer");
+    return FP8_OK;
+  }
+  if (cfg->recipe != FP8_RECIPE_MXFP8) return fail(FP8_EUNSUPPORTED, "w_fp8 needs the tensorwise or mxfp8 recipe");
+  if (w_fp8->gran != (mx_transposed() ? FP8_GRAN_MX32 : FP8_GRAN_MX32_RM))
+    return fail(FP8_EINVAL, "w_fp8->gran must be FP8_GRAN_MX32_RM (FP8_GRAN_MX32 with FP8T_MX_TRANSPOSED=1)");
+  if (!bwd_dx) {
+    FP8T_TRY(check_ptr(w_fp8->q, "w_fp8->q"));
+    if (!w_fp8->scale) return fail(FP8_EINVAL, "w_fp8->scale: null pointer");
+  } else {
+    FP8T_TRY(check_ptr(w_fp8->q_t, "w_fp8->q_t"));
+    if (!w_fp8->scale_t) return fail(FP8_EINVAL, "w_fp8->scale_t: null pointer");
+  }
+  return FP8_OK;
+}
+
 }  // namespace
 
 size_t fp8_linear_saved_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K) {
@@ -494,13 +517,7 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
   FP8T_TRY(check_ptr(ws, "ws"));
   const size_t need = saved ? fp8_linear_workspace_bytes(cfg, M, N, K) : fp8_linear_infer_workspace_bytes(cfg, M, N, K);
   if (ws_bytes < need) return fail(FP8_EWORKSPACE, "workspace too small (%zu < %zu)", ws_bytes, need);
-  if (w_fp8) {
-    if (cfg->recipe != FP8_RECIPE_TENSORWISE) return fail(FP8_EUNSUPPORTED, "w_fp8 needs the tensorwise recipe");
-    if (w_fp8->rows != N || w_fp8->cols != K) return fail(FP8_EINVAL, "w_fp8 shape");
-    if (w_fp8->fmt != cfg->fmt_fwd) return fail(FP8_EINVAL, "w_fp8 format != cfg->fmt_fwd");
-    FP8T_TRY(check_ptr(w_fp8->q, "w_fp8->q"));
-    if (!w_fp8->scale) return fail(FP8_EINVAL, "w_fp8->scale: null pointer");
-  }
+  if (w_fp8) FP8T_TRY(check_w_fp8(cfg, w_fp8, N, K, false));
   if (x_amax && cfg->recipe != FP8_RECIPE_TENSORWISE)
     return fail(FP8_EUNSUPPORTED, "x_amax (precomputed tensor amax) needs the tensorwise recipe");
   cudaStream_t st = S(stream);
@@ -549,8 +566,11 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
     } else {   // MXFP8: dim0 only
       const bool rc = cfg->mx_round == FP8_MX_RCEIL;
       FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, iw.xq, (uint8_t*)iw.sx, nullptr, nullptr, st), "mx x");
-      FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, iw.wq, (uint8_t*)iw.sw, nullptr, nullptr, st), "mx w");
-      GemmProblem p{iw.xq, iw.wq, ff, ff, 0, 0, iw.sx, iw.sw, 2, M, N, K, K, K, y, of32, N, 0, yam};
+      if (!w_fp8)
+        FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, iw.wq, (uint8_t*)iw.sw, nullptr, nullptr, st), "mx w");
+      const uint8_t* wq = w_fp8 ? w_fp8->q : iw.wq;
+      const void* swp = w_fp8 ? w_fp8->scale : iw.sw;
+      GemmProblem p{iw.xq, wq, ff, ff, 0, 0, iw.sx, swp, 2, M, N, K, K, K, y, of32, N, 0, yam};
       FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
     }
     return FP8_OK;
@@ -604,9 +624,14 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
     const bool rc = cfg->mx_round == FP8_MX_RCEIL, tr = mx_transposed();
     FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, fw.xq, fw.sfx, sv.xT, (uint8_t*)sv.sx, st, tr),
               "mx cast x");
-    FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, fw.wq, fw.sfw, sv.wT, (uint8_t*)sv.sw, st, tr),
-              "mx cast w");
-    GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sfx, fw.sfw, 2, M, N, K, K, K, y, of32, N, 0, yam};
+    // pre-gathered weight (fp8_fsdp_allgather_mx): its dim0 copy feeds this GEMM and its dim1 copy
+    // the backward, so nothing of W is cast or saved here
+    if (!w_fp8)
+      FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, fw.wq, fw.sfw, sv.wT, (uint8_t*)sv.sw, st, tr),
+                "mx cast w");
+    const uint8_t* wq = w_fp8 ? w_fp8->q : fw.wq;
+    const void* swp = w_fp8 ? w_fp8->scale : fw.sfw;
+    GemmProblem p{fw.xq, wq, ff, ff, 0, 0, fw.sfx, swp, 2, M, N, K, K, K, y, of32, N, 0, yam};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
   }
   return FP8_OK;
@@ -633,11 +658,7 @@ fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const f
   if (dx) FP8T_TRY(check_ptr(dx, "dx"));
   if (dw) FP8T_TRY(check_ptr(dw, "dw"));
   if (ws_bytes < fp8_linear_workspace_bytes(cfg, M, N, K)) return fail(FP8_EWORKSPACE, "workspace too small");
-  if (w_fp8) {
-    if (cfg->recipe != FP8_RECIPE_TENSORWISE) return fail(FP8_EUNSUPPORTED, "w_fp8 needs the tensorwise recipe");
-    if (w_fp8->rows != N || w_fp8->cols != K) return fail(FP8_EINVAL, "w_fp8 shape");
-    FP8T_TRY(check_ptr(w_fp8->q, "w_fp8->q"));
-  }
+  if (w_fp8) FP8T_TRY(check_w_fp8(cfg, w_fp8, N, K, dx != nullptr));
   if (dy_amax && cfg->recipe != FP8_RECIPE_TENSORWISE)
     return fail(FP8_EUNSUPPORTED, "dy_amax (precomputed tensor amax) needs the tensorwise recipe");
   cudaStream_t st = S(stream);
@@ -711,16 +732,20 @@ gemms:
     // dW[N,K] = dY_c^T . X_c: A stored [M,N] = MN-major, B stored [M,K] = MN-major
     if (dw) ps[n++] = GemmProblem{bw.gT, sv.xT, fg, ff, 1, 1, bw.sgT, sv.sx, mode, N, K, M, N, K, dw, of32, K};
   } else if (!mx_transposed()) {
+    const uint8_t* w1 = w_fp8 ? w_fp8->q_t : sv.wT;
+    const void* s1 = w_fp8 ? w_fp8->scale_t : sv.sw;
     // MXFP8: dim1 copies (blocks along the contraction dim) kept in the input's row-major layout
     // and read MN-major, like the tensorwise / rowwise backward
     // dX[M,K] = dY[M,N] . W : A = dY dim0 (K-major over N), B = W dim1 stored [N,K] = MN-major
-    if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 1, bw.sg, sv.sw, mode, M, K, N, N, K, dx, of32, K, 0, dxam};
+    if (dx) ps[n++] = GemmProblem{bw.g, w1, fg, ff, 0, 1, bw.sg, s1, mode, M, K, N, N, K, dx, of32, K, 0, dxam};
     // dW[N,K] = dY^T . X : A = dY dim1 stored [M,N] = MN-major, B = X dim1 stored [M,K] = MN-major
     if (dw) ps[n++] = GemmProblem{bw.gT, sv.xT, fg, ff, 1, 1, bw.sgT, sv.sx, mode, N, K, M, N, K, dw, of32, K};
   } else {
+    const uint8_t* w1 = w_fp8 ? w_fp8->q_t : sv.wT;
+    const void* s1 = w_fp8 ? w_fp8->scale_t : sv.sw;
     // MXFP8 with transposed dim1 copies (FP8T_MX_TRANSPOSED=1), all operands K-major
     // dX[M,K] = dY[M,N] . W  : A = dY (K-major over N), B = W^T [K,N]
-    if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 0, bw.sg, sv.sw, mode, M, K, N, N, N, dx, of32, K, 0, dxam};
+    if (dx) ps[n++] = GemmProblem{bw.g, w1, fg, ff, 0, 0, bw.sg, s1, mode, M, K, N, N, N, dx, of32, K, 0, dxam};
     // dW[N,K] = dY^T[N,M] . X : A = dY^T [N,M], B = X^T [K,M]
     if (dw) ps[n++] = GemmProblem{bw.gT, sv.xT, fg, ff, 0, 0, bw.sgT, sv.sx, mode, N, K, M, M, M, dw, of32, K};
   }

@@ -663,6 +663,20 @@ __global__ void __launch_bounds__(256) mx_cast_tma_kernel(const __grid_constant_
   }
 }
 
+// MXFP8 FSDP gather helper: re-tile gathered dim1 E8M0 scales from rank-major order
+// [P][Kt][Tl] 512-byte tiles (rank p's shard-local blocked [K, Nl/32] matrix) into the blocked
+// layout of the full [K, P*Nl/32] matrix, [Kt][P*Tl] tiles.  One thread per 16-byte unit.
+__global__ void __launch_bounds__(256) sf_unshard_kernel(const uint4* __restrict__ in, int P, int64_t Kt, int64_t Tl,
+                                                         uint4* __restrict__ out) {
+  const int64_t n = (int64_t)P * Kt * Tl * 32;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tile = i >> 5, u = i & 31;
+    const int64_t kt = tile / (P * Tl), jc = tile - kt * (P * Tl);
+    const int64_t p = jc / Tl, jl = jc - p * Tl;
+    out[i] = __ldg(in + ((p * Kt + kt) * Tl + jl) * 32 + u);
+  }
+}
+
 // FP8 byte transpose [R, C] -> [C, R] (R, C multiples of 16).
 __global__ void __launch_bounds__(256) transpose_u8_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C,
                                                            uint8_t* __restrict__ out) {
@@ -862,6 +876,16 @@ cudaError_t launch_mx_cast(const void* x, bool bf16, int fmt, bool rceil, int64_
   if (bf16) { FP8T_MX(__nv_bfloat16) }
   FP8T_MX(float)
 #undef FP8T_MX
+}
+
+cudaError_t launch_sf_unshard(const uint8_t* in, int P, int64_t Kt, int64_t Tl, uint8_t* out, cudaStream_t s) {
+  const int64_t n = (int64_t)P * Kt * Tl * 32;
+  if (n == 0) return cudaSuccess;
+  const int64_t cap = (int64_t)sm_count() * 8, want = (n + 255) / 256;
+  LaunchScope ls(K_TRANSPOSE, s);
+  sf_unshard_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(reinterpret_cast<const uint4*>(in), P, Kt, Tl,
+                                                                        reinterpret_cast<uint4*>(out));
+  return cudaGetLastError();
 }
 
 cudaError_t launch_transpose_u8(const uint8_t* in, int64_t R, int64_t C, uint8_t* out, cudaStream_t s) {

@@ -112,4 +112,71 @@ fp8_status_t fp8_fsdp_allgather_ex(fp8_comm_t comm, fp8_hp_t w, fp8_format_t fmt
   return nccl_check(ncclAllGather(slot, w_full, chunk, ncclUint8, comm->nccl, st), "ncclAllGather");
 }
 
+// ---------------------------------------------------------------------------
+// MXFP8 FSDP gather.  A 32-block never crosses a shard boundary when
+// rows_local % 128 == 0, so every E8M0 code is shard-local: no amax exchange.  Rank r casts its
+// shard straight into its slots (dim0 codes + blocked scales are contiguous per shard; dim1 codes
+// too, in the row-major MX32_RM layout), the dim1 scales into slot r of a rank-major staging
+// buffer; one NCCL group all-gathers the four buffers; the dim1 scales are then re-tiled into
+// the full blocked layout.
+// ---------------------------------------------------------------------------
+size_t fp8_fsdp_mx_workspace_bytes(fp8_hp_t w, int nranks) {
+  return nranks > 0 && w.rows > 0 && w.cols > 0 ? (size_t)nranks * (size_t)w.rows * (size_t)w.cols / 32 : 0;
+}
+
+fp8_status_t fp8_mx_scales_unshard(const uint8_t* rank_major, int nranks, int64_t rows_local, int64_t cols,
+                                   uint8_t* out, void* stream) {
+  if (!rank_major || !out) return fail(FP8_EINVAL, "null pointer");
+  if (nranks < 1 || rows_local < 128 || cols < 128 || rows_local % 128 || cols % 128)
+    return fail(FP8_EALIGN, "rows_local and cols must be positive multiples of 128");
+  if ((reinterpret_cast<uintptr_t>(rank_major) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(FP8_EALIGN, "pointers must be 16-byte aligned");
+  return cuda_check(launch_sf_unshard(rank_major, nranks, cols / 128, rows_local / 128, out,
+                                      static_cast<cudaStream_t>(stream)),
+                    "sf_unshard");
+}
+
+fp8_status_t fp8_fsdp_allgather_mx(fp8_comm_t comm, fp8_hp_t w, fp8_mx_round_t mx_round, fp8_tensor_t* out, void* ws,
+                                   size_t ws_bytes, void* stream) {
+  if (!comm) return fail(FP8_EINVAL, "comm: null");
+  if (!w.ptr || !out || !out->q || !out->scale) return fail(FP8_EINVAL, "null pointer (w, out, out->q, out->scale)");
+  if (out->fmt != FP8_E4M3 && out->fmt != FP8_E5M2) return fail(FP8_EINVAL, "bad fp8 format");
+  if (out->gran != FP8_GRAN_MX32_RM) return fail(FP8_EUNSUPPORTED, "out->gran must be FP8_GRAN_MX32_RM");
+  if (mx_round != FP8_MX_FLOOR && mx_round != FP8_MX_RCEIL) return fail(FP8_EINVAL, "bad mx_round");
+  if (w.dtype != FP8_DT_F32 && w.dtype != FP8_DT_BF16) return fail(FP8_EINVAL, "bad dtype");
+  if ((out->q_t == nullptr) != (out->scale_t == nullptr)) return fail(FP8_EINVAL, "q_t and scale_t: both or neither");
+  if (w.rows < 128 || w.cols < 128 || w.rows % 128 || w.cols % 128)
+    return fail(FP8_EALIGN, "MX shard rows/cols: multiples of 128");
+  if (out->rows != (int64_t)comm->nranks * w.rows || out->cols != w.cols) return fail(FP8_EINVAL, "out shape");
+  if (w.ld < w.cols || (w.ld * (w.dtype == FP8_DT_F32 ? 4 : 2)) % 16) return fail(FP8_EALIGN, "bad ld");
+  uintptr_t al = reinterpret_cast<uintptr_t>(w.ptr) | reinterpret_cast<uintptr_t>(out->q) |
+                 reinterpret_cast<uintptr_t>(out->scale) | reinterpret_cast<uintptr_t>(out->q_t) |
+                 reinterpret_cast<uintptr_t>(out->scale_t) | reinterpret_cast<uintptr_t>(ws);
+  if (al & 15) return fail(FP8_EALIGN, "pointers must be 16-byte aligned");
+  const bool dim1 = out->q_t != nullptr;
+  if (dim1 && (!ws || ws_bytes < fp8_fsdp_mx_workspace_bytes(w, comm->nranks)))
+    return fail(FP8_EWORKSPACE, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t chunk = (size_t)w.rows * (size_t)w.cols, r = (size_t)comm->rank;
+  uint8_t* q0 = out->q + r * chunk;
+  uint8_t* s0 = static_cast<uint8_t*>(out->scale) + r * chunk / 32;
+  uint8_t* q1 = dim1 ? out->q_t + r * chunk : nullptr;
+  uint8_t* s1 = dim1 ? static_cast<uint8_t*>(ws) + r * chunk / 32 : nullptr;
+  fp8_status_t s;
+  if ((s = cuda_check(launch_mx_cast(w.ptr, w.dtype == FP8_DT_BF16, out->fmt, mx_round == FP8_MX_RCEIL, w.rows,
+                                     w.cols, w.ld, q0, s0, q1, s1, st, false),
+                      "mx cast")) != FP8_OK)
+    return s;
+  if ((s = nccl_check(ncclGroupStart(), "ncclGroupStart")) != FP8_OK) return s;
+  ncclResult_t e = ncclAllGather(q0, out->q, chunk, ncclUint8, comm->nccl, st);
+  if (e == ncclSuccess) e = ncclAllGather(s0, out->scale, chunk / 32, ncclUint8, comm->nccl, st);
+  if (e == ncclSuccess && dim1) e = ncclAllGather(q1, out->q_t, chunk, ncclUint8, comm->nccl, st);
+  if (e == ncclSuccess && dim1) e = ncclAllGather(s1, ws, chunk / 32, ncclUint8, comm->nccl, st);
+  ncclResult_t e2 = ncclGroupEnd();
+  if ((s = nccl_check(e != ncclSuccess ? e : e2, "ncclAllGather (mx group)")) != FP8_OK) return s;
+  if (!dim1) return FP8_OK;
+  return fp8_mx_scales_unshard(static_cast<const uint8_t*>(ws), comm->nranks, w.rows, w.cols,
+                               static_cast<uint8_t*>(out->scale_t), stream);
+}
+
 }  // extern "C"

@@ -48,6 +48,8 @@ cudaError_t launch_amax_multi(const AmaxMultiArgs& a, cudaStream_t st);
 // transposed [C,R] (else in the input's layout [R,C])
 cudaError_t launch_mx_cast(const void* x, bool bf16, int fmt, bool rceil, int64_t R, int64_t C, int64_t ld,
                            uint8_t* q0, uint8_t* sf0, uint8_t* q1, uint8_t* sf1, cudaStream_t s, bool tr1 = true);
+// Rank-major gathered dim1 E8M0 tiles [P][Kt][Tl][512 B] -> blocked full layout [Kt][P*Tl][512 B].
+cudaError_t launch_sf_unshard(const uint8_t* in, int P, int64_t Kt, int64_t Tl, uint8_t* out, cudaStream_t s);
 cudaError_t launch_transpose_u8(const uint8_t* in, int64_t R, int64_t C, uint8_t* out, cudaStream_t s);
 
 // tcgen05 GEMM: D[M,N] = A[M,K] B[N,K]^T with scales.

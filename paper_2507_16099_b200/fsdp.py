@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib as L
-from .ops import FORMATS, _ptr, _stream, hp
+from .ops import FORMATS, MX_ROUND, _ptr, _stream, hp
 
 
 def shard_rows(N, world, rank):
@@ -79,6 +79,29 @@ class Comm:
         L.check(L.lib.fp8_fsdp_allgather(self._h, hp(w_shard), FORMATS[fmt], _ptr(out), _ptr(scale), _ptr(amax),
                                          None, 0, _stream(stream)), "fp8_fsdp_allgather")
         return out, scale, amax
+
+    def allgather_mx(self, w_shard, fmt="e4m3", mx_round="floor", dim1=True, out=None, ws=None, stream=None):
+        """MXFP8 FSDP gather (fp8_fsdp_allgather_mx): shard-local E8M0 scales, no amax exchange.
+        Returns {"q", "scale"} (dim0: [P*rows, cols] codes + blocked E8M0) and, with dim1,
+        {"q_t", "scale_t"} (dim1 codes row-major [P*rows, cols] + blocked E8M0 of the [cols, P*rows/32]
+        scale matrix) -- the w_fp8 of an mxfp8 LinearPlan."""
+        rows, cols = w_shard.shape
+        dev = w_shard.device
+        N = self.world * rows
+        if out is None:
+            out = {"q": torch.empty((N, cols), dtype=torch.uint8, device=dev),
+                   "scale": torch.empty(N * cols // 32, dtype=torch.uint8, device=dev)}
+            if dim1:
+                out["q_t"] = torch.empty((N, cols), dtype=torch.uint8, device=dev)
+                out["scale_t"] = torch.empty(N * cols // 32, dtype=torch.uint8, device=dev)
+        wsb = L.lib.fp8_fsdp_mx_workspace_bytes(hp(w_shard), self.world) if out.get("q_t") is not None else 0
+        if wsb and (ws is None or ws.numel() < wsb):
+            ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        t = L.Tensor8(*[(out[k].data_ptr() if out.get(k) is not None else None) for k in ("q", "q_t", "scale", "scale_t")],
+                      None, None, FORMATS[fmt], L.GRAN_MX32_RM, N, cols)
+        L.check(L.lib.fp8_fsdp_allgather_mx(self._h, hp(w_shard), MX_ROUND[mx_round], ctypes.byref(t),
+                                            _ptr(ws) if wsb else None, wsb, _stream(stream)), "fp8_fsdp_allgather_mx")
+        return out
 
     def close(self):
         if self._h:

@@ -120,6 +120,16 @@ def gemm(A, fmt_a, sa, B, fmt_b, sb, gran="tensor", out_dtype=torch.bfloat16, a_
     return D
 
 
+def mx_scales_unshard(rank_major, nranks, rows_local, cols, out=None, stream=None):
+    """fp8_mx_scales_unshard: nranks shard-local blocked dim1 E8M0 buffers ([cols, rows_local/32]
+    each, concatenated) -> the blocked buffer of the full [cols, nranks*rows_local/32] matrix."""
+    if out is None:
+        out = torch.empty_like(rank_major)
+    L.check(L.lib.fp8_mx_scales_unshard(_ptr(rank_major), nranks, rows_local, cols, _ptr(out), _stream(stream)),
+            "fp8_mx_scales_unshard")
+    return out
+
+
 class LinearPlan:
     """Sizes and buffers for one Float8Linear shape (caller-owned, as the ABI requires)."""
 
@@ -139,12 +149,17 @@ class LinearPlan:
     def _wq(self, w_fp8):
         if w_fp8 is None:
             return None
+        if isinstance(w_fp8, dict):   # MXFP8 gather (Comm.allgather_mx): q/scale dim0, q_t/scale_t dim1
+            return L.Tensor8(*[(w_fp8[k].data_ptr() if w_fp8.get(k) is not None else None)
+                               for k in ("q", "q_t", "scale", "scale_t")], None, None, self.cfg.fmt_fwd,
+                             L.GRAN_MX32_RM, self.N, self.K)
         q, s = w_fp8
         return L.Tensor8(q.data_ptr(), None, s.data_ptr(), None, None, None, self.cfg.fmt_fwd, L.GRAN_TENSOR,
                          self.N, self.K)
 
     def forward(self, x, w, saved, y=None, w_fp8=None, x_amax=None, y_amax=None, stream=None):
-        """w_fp8: optional (codes [N,K] uint8, scale float[1]) pre-cast weight (FSDP FP8 gather).
+        """w_fp8: optional pre-cast weight: tensorwise (codes [N,K] uint8, scale float[1]) from
+        Comm.allgather_fp8, or the mxfp8 dict of Comm.allgather_mx.
         saved=None: forward-only (inference) -- nothing is kept for a backward.
         x_amax: optional precomputed amax(|X|) (float[1]); y_amax: optional float[1] that receives
         amax(|Y|) from the GEMM epilogue."""

@@ -10,7 +10,7 @@ import pytest
 import torch
 
 import synth
-from oracle import codecs, fp8, gemm as ogemm, linear as olin, mx as omx
+from oracle import codecs, fp8, fsdp as ofsdp, gemm as ogemm, linear as olin, mx as omx
 from oracle.codecs import E4M3, E5M2
 
 pytestmark = pytest.mark.gpu
@@ -556,3 +556,71 @@ def test_mx_cast_impls_agree_c4_sized(impl, monkeypatch):
     assert np.array_equal(_np(out["q"])[rows], q0)
     q1, s1 = omx.quantize_dim1(x[:, 4000:4256], E4M3)
     assert np.array_equal(_np(out["q_t"])[:, 4000:4256], q1.T)
+
+
+# ----------------------------------------------------------------------------- MXFP8 FSDP gather
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_mx_fsdp_gather_composition_simulated_ranks(P):
+    """The per-rank steps of fp8_fsdp_allgather_mx for P ranks, run on one GPU: each shard is
+    MX-cast into its slots (what rank r does before the NCCL group), the byte concatenation
+    stands in for the all-gather, and fp8_mx_scales_unshard re-tiles the dim1 scales.  Must
+    equal the unsharded cast and the oracle."""
+    N, K = 128 * P * 2, 384
+    w = synth.tensor_c4("w", (N, K), seed=3)
+    Nl = N // P
+    slots = [ops.cast(_dev(w[r * Nl:(r + 1) * Nl], torch.bfloat16), "e4m3", "mx32_rm", want_q=True, want_qt=True)
+             for r in range(P)]
+    q0 = torch.cat([s["q"] for s in slots])
+    s0 = torch.cat([s["scale"] for s in slots])
+    q1 = torch.cat([s["q_t"] for s in slots])
+    s1 = ops.mx_scales_unshard(torch.cat([s["scale_t"] for s in slots]), P, Nl, K)
+    full = ops.cast(_dev(w, torch.bfloat16), "e4m3", "mx32_rm", want_q=True, want_qt=True)
+    torch.cuda.synchronize()
+    for a, b in ((q0, full["q"]), (s0, full["scale"]), (q1, full["q_t"]), (s1, full["scale_t"])):
+        assert torch.equal(a, b)
+    oq0, os0, oq1, os1 = ofsdp.allgather_mx_ref(np.split(w, P, axis=0), E4M3)
+    assert np.array_equal(_np(q0), oq0) and np.array_equal(_unblock(s0, N, K), os0)
+    assert np.array_equal(_np(q1), oq1.T) and np.array_equal(_unblock(s1, K, N), os1)
+
+
+def test_mx_fsdp_allgather_single_rank():
+    """fp8_fsdp_allgather_mx through NCCL with one rank == the unsharded MX32_RM cast (oracle), and
+    the gathered weight drives the mxfp8 linear bit-identically to the hp weight."""
+    import os
+    import torch.distributed as dist
+    from paper_2507_16099_b200.fsdp import Comm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = "29541"
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = Comm()
+        Mx, Nw, Kw = 256, 384, 512
+        x, w, dy = synth.linear_inputs("c4", Mx, Nw, Kw, seed=0)
+        for fmt, mode in ((E4M3, "floor"), (E5M2, "rceil")):
+            g = comm.allgather_mx(_dev(w, torch.bfloat16), FMTNAME[fmt], mode)
+            torch.cuda.synchronize()
+            m = omx.FLOOR if mode == "floor" else omx.RCEIL
+            q0, s0 = omx.quantize_dim0(w, fmt, m)
+            q1, s1 = omx.quantize_dim1(w, fmt, m)
+            assert np.array_equal(_np(g["q"]), q0) and np.array_equal(_unblock(g["scale"], Nw, Kw), s0)
+            assert np.array_equal(_np(g["q_t"]), q1.T) and np.array_equal(_unblock(g["scale_t"], Kw, Nw), s1)
+        # forward-only gather (dim0 only, no workspace)
+        g0 = comm.allgather_mx(_dev(w, torch.bfloat16), "e4m3", dim1=False)
+        torch.cuda.synchronize()
+        assert np.array_equal(_np(g0["q"]), omx.quantize_dim0(w, E4M3)[0])
+        # linear with the gathered weight == linear with the hp weight (bit-identical)
+        g = comm.allgather_mx(_dev(w, torch.bfloat16), "e4m3")
+        plan = ops.LinearPlan(Mx, Nw, Kw, recipe="mxfp8", out_dtype=torch.float32)
+        sa, sb = plan.new_saved(), plan.new_saved()
+        X, W, G = _dev(x, torch.bfloat16), _dev(w, torch.bfloat16), _dev(dy, torch.bfloat16)
+        y1 = plan.forward(X, W, sa).clone()
+        dx1, dw1 = (t.clone() for t in plan.backward(G, sa))
+        y2 = plan.forward(X, None, sb, w_fp8=g).clone()
+        dx2, dw2 = plan.backward(G, sb, w_fp8=g)
+        y3 = plan.forward(X, None, None, w_fp8=g0).clone()   # forward-only with the dim0-only gather
+        torch.cuda.synchronize()
+        assert torch.equal(y1, y2) and torch.equal(dx1, dx2) and torch.equal(dw1, dw2) and torch.equal(y1, y3)
+        comm.close()
+    finally:
+        dist.destroy_process_group()

@@ -66,7 +66,21 @@ def _worker(rank, world, port, q):
         qo, so, ao = ofsdp.allgather_ref([synth.weight_shard_c5((N, K), 0, r, world) for r in range(world)], "e4m3")
         assert np.array_equal(qo, q1)
 
-        # 4. max-over-ranks timing reduction (bench.py)
+        # 4. MXFP8 gather: shard-local E8M0 quantization, no amax exchange; the
+        #    gloo-gathered dim0 rows / dim1 columns equal the unsharded quantization
+        from oracle import mx as omx
+        Nm, Km = 64 * world, 64
+        wm = synth.tensor_c4("w", (Nm, Km), 4)
+        mine = wm[rank * 64:(rank + 1) * 64]
+        parts = []
+        for arr in (omx.quantize_dim0(mine, "e4m3")[0], omx.quantize_dim1(mine, "e4m3")[1]):
+            g = [torch.empty_like(torch.from_numpy(arr)) for _ in range(world)]
+            dist.all_gather(g, torch.from_numpy(arr))
+            parts.append(g)
+        assert np.array_equal(torch.cat(parts[0], 0).numpy(), omx.quantize_dim0(wm, "e4m3")[0])
+        assert np.array_equal(torch.cat(parts[1], 1).numpy(), omx.quantize_dim1(wm, "e4m3")[1])
+
+        # 5. max-over-ranks timing reduction (bench.py)
         ms = torch.tensor([1.0 + rank])
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         assert ms.item() == float(world)

@@ -164,6 +164,29 @@ def test_fsdp_gather_equals_unsharded_cast(P):
     assert np.array_equal(q, q1) and s == s1 and a == a1
 
 
+@pytest.mark.parametrize("P", [1, 2, 4])
+@pytest.mark.parametrize("fmt,mode", [(E4M3, mx.FLOOR), (E5M2, mx.RCEIL)])
+def test_fsdp_mx_gather_equals_unsharded_quantize(P, fmt, mode):
+    # MX scales are shard-local, so per-shard quantization + concatenation equals
+    # the unsharded dim0 / dim1 quantization (no amax exchange), when shards hold whole 32-blocks
+    w = synth.tensor_c4("w", (256, 128), seed=1)
+    q0, s0, q1, s1 = fsdp.allgather_mx_ref(np.split(w, P, axis=0), fmt, mode)
+    f0, g0 = mx.quantize_dim0(w, fmt, mode)
+    f1, g1 = mx.quantize_dim1(w, fmt, mode)
+    assert np.array_equal(q0, f0) and np.array_equal(s0, g0)
+    assert np.array_equal(q1, f1) and np.array_equal(s1, g1)
+
+
+def test_fsdp_mx_gather_needs_block_aligned_shards():
+    # the alignment rule is load-bearing: 16-row shards split dim1 blocks, and a block whose
+    # amax sits in one half gets a different (smaller) code in the other half
+    w = synth.tensor_c2("w", (64, 32), seed=2)
+    w[3, 5] = 7.0
+    full = mx.quantize_dim1(w, E4M3)[1][5, 0]          # block rows 0..31 of column 5
+    half = mx.scale_code(np.array([[np.max(np.abs(w[16:32, 5]))]], np.float32), E4M3)[0, 0]
+    assert full == mx.scale_code(np.array([[np.float32(7.0)]]), E4M3)[0, 0] and half < full
+
+
 def test_rowwise_gw_hp_weight_grad_is_high_precision():
     # S:300-301 "RowwiseGwHp grad_weight = gemm_ref(grad_out^T, x) bit-exactly" (no FP8 casting);
     # its grad_input equals the rowwise recipe's (same casts, "like rowwise").
