@@ -65,6 +65,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bf16", action="store_true")
+    ap.add_argument("--gather", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="tensorwise FSDP weight gather: p2p = fused cast-and-push over NVLink peer memory "
+                         "(fp8_fsdp_allgather_p2p), nccl = cast + ncclAllGather; auto = p2p, falling back to "
+                         "nccl if the peer windows cannot be created (auto uses nccl at N=1: no peers)")
     ap.add_argument("--fsdp", action="store_true",
                     help="use the FSDP path (fp8_fsdp_allgather + pre-cast weight) even at N=1")
     return ap.parse_args()
@@ -286,6 +290,18 @@ def run_ours(a):
         w_scale = torch.empty(1, dtype=torch.float32, device=dev)
         w_amax = torch.empty(1, dtype=torch.float32, device=dev)
         dw_shard = torch.empty((N // world, K), dtype=torch.bfloat16, device=dev)
+        p2p = None
+        gather_impl = "nccl (fp8_fsdp_allgather_mx)" if mx_fsdp else "nccl (fp8_fsdp_allgather)"
+        if not mx_fsdp and (a.gather == "p2p" or (a.gather == "auto" and world > 1)):
+            from paper_2507_16099_b200.fsdp import P2PWindow
+            try:
+                p2p = P2PWindow(comm, N * K)
+                w_full = p2p.buffer(N, K, dev)
+                gather_impl = "p2p (fp8_fsdp_allgather_p2p: cast pushes codes to every rank over NVLink)"
+            except Exception as e:  # noqa: BLE001  (IPC / peer access unavailable)
+                if a.gather == "p2p":
+                    raise
+                gather_impl = f"nccl (p2p window failed: {str(e)[:120]})"
         if mx_fsdp:   # MXFP8 gather (fp8_fsdp_allgather_mx): dim0 + dim1 codes and E8M0 scales
             mx_out = {"q": w_full, "scale": torch.empty(N * K // 32, dtype=torch.uint8, device=dev),
                       "q_t": torch.empty((N, K), dtype=torch.uint8, device=dev),
@@ -296,7 +312,10 @@ def run_ours(a):
         """FSDP weight gather of this step: the pre-cast weight the linear consumes."""
         if mx_fsdp:
             return comm.allgather_mx(ww, "e4m3", out=mx_out, ws=mx_ws)
-        comm.allgather_fp8(ww, "e4m3", out=w_full, scale=w_scale, amax=w_amax)
+        if p2p is not None:
+            p2p.allgather_fp8(ww, "e4m3", scale=w_scale, amax=w_amax)
+        else:
+            comm.allgather_fp8(ww, "e4m3", out=w_full, scale=w_scale, amax=w_amax)
         return (w_full, w_scale)
 
     def step(xx=x, ww=w_shard, gg=dy):
@@ -346,6 +365,29 @@ def run_ours(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / a.steps
+
+    gather_info = None
+    if fsdp:
+        # the weight gather alone (same calls as inside the step), device-timed, max over ranks
+        for _ in range(3):
+            gather(w_shard)
+        torch.cuda.synchronize()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(a.steps):
+            gather(w_shard)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = g0.elapsed_time(g1) / a.steps
+        if world > 1:
+            t = torch.tensor([gms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            gms = float(t.item())
+        recv = N * K * (world - 1) // world * (2 + 2 / 32 if mx_fsdp else 1)   # bytes each rank receives
+        gather_info = {"impl": gather_impl, "ms": gms, "recv_bytes_per_rank": recv,
+                       "busbw_GBps": recv / (gms / 1e3) / 1e9 if world > 1 else None,
+                       "nvlink_peak_GBps": 900.0}
 
     flops_step = 6.0 * M * N * K            # three GEMMs of 2*M*N*K each (per rank)
     total_flops = flops_step * a.steps * world
@@ -533,14 +575,18 @@ def run_ours(a):
                      if cast_gbps else None, "ms_per_step": cast_ms, "algorithmic_bytes_per_step": cast_bytes},
             "kernels_ms_per_step": {name: round(sum(by.get(k, [])) / a.steps, 4)
                                     for k, name in ((0, "amax"), (1, "cast"), (2, "mx_cast"), (3, "transpose_u8"),
-                                                    (4, "gemm_fp8"), (5, "gemm_mxfp8"), (6, "gemm_bf16"))},
+                                                    (4, "gemm_fp8"), (5, "gemm_mxfp8"), (6, "gemm_bf16"),
+                                                    (7, "p2p_sync"))},
             "bf16": bf16,
+            "gather": gather_info,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    if fsdp and p2p is not None:
+        p2p.close()
     if comm is not None:
         comm.close()
     if dist.is_initialized():

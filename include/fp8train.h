@@ -334,6 +334,43 @@ fp8_status_t fp8_mx_scales_unshard(const uint8_t* rank_major, int nranks, int64_
                                    int64_t cols, uint8_t* out, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Fused FP8 FSDP all-gather over NVLink peer memory (the B200-native form of the
+ * tensorwise enable_fp8_all_gather of PAPER.md:596, reading R-c18).  The cast kernel
+ * stores each rank's FP8 codes straight into slot `rank` of EVERY rank's gather buffer
+ * (CUDA-IPC peer pointers over NVLink / NVSwitch): the all-gather's data movement is
+ * the cast's own output stream, with no NCCL kernel and no local round trip of the
+ * codes.  The global amax is exchanged through per-rank signal slots in the same
+ * windows (release/acquire at system scope), which also serves as the barrier that
+ * keeps a fast rank from overwriting a buffer a slow rank is still reading.
+ * Result: bit-identical to fp8_fsdp_allgather (and to the unsharded tensorwise cast).
+ * ------------------------------------------------------------------------- */
+typedef struct fp8_p2p_s* fp8_p2p_t;
+/* Host, collective over the communicator's ranks: allocate this rank's window (a
+ * gather buffer of `bytes` + a signal block, zeroed), exchange CUDA IPC handles over
+ * NCCL, open every peer's window (needs peer access: NVLink / NVSwitch).  One window
+ * per concurrently live gathered weight; bytes >= nranks * rows_local * cols. */
+fp8_status_t fp8_p2p_create(fp8_comm_t comm, size_t bytes, fp8_p2p_t* win);
+/* Test / single-GPU form: nranks windows on the current device, wins[r] acting as rank
+ * r, all mapped to each other (plain device pointers).  The ranks' calls must then be
+ * issued on different streams (each call waits for every rank's signals). */
+fp8_status_t fp8_p2p_create_local(int nranks, size_t bytes, fp8_p2p_t* wins);
+/* Device pointer of this rank's gather buffer: the codes [nranks*rows_local, cols] u8
+ * after fp8_fsdp_allgather_p2p (valid in stream order after the call). */
+void* fp8_p2p_buffer(fp8_p2p_t win);
+fp8_status_t fp8_p2p_destroy(fp8_p2p_t win);
+/* Per rank, on `stream` (every rank calls it for the same weight in the same order):
+ *   amax(W_r) (skipped if amax_in, a device float[1] global amax, e.g. from
+ *   fp8_fsdp_precompute_amax) -> signal it into every peer's slot r -> wait for all
+ *   P slots, s = RN32(fmax / max(max_p amax_p, eps)) -> scale_out (device float[1]),
+ *   amax_out (device float[1], the global amax; also the accumulator when amax_in is
+ *   NULL) -> cast W_r pushing codes to every peer -> wait until every rank's pushes
+ *   into this buffer are visible.  Spins carry a 10 s watchdog (kernel trap ->
+ *   FP8_ECUDA at the next sync) instead of hanging.  w_shard rows/cols multiples of 16. */
+fp8_status_t fp8_fsdp_allgather_p2p(fp8_p2p_t win, fp8_hp_t w_shard, fp8_format_t fmt,
+                                    const float* amax_in, float* scale_out, float* amax_out,
+                                    void* stream);
+
+/* ---------------------------------------------------------------------------
  * Helpers
  * ------------------------------------------------------------------------- */
 int fp8_abi_version(void);
@@ -348,7 +385,8 @@ uint64_t fp8_launch_count(void);
  * fp8_profile_collect() waits for the recorded events, writes up to max_n records
  * (kind, duration in ms) in launch order and clears the list; returns the number of
  * records written (or -1 on a CUDA error).  Kinds: 0 amax, 1 cast, 2 mx_cast,
- * 3 transpose_u8, 4 gemm (FP8), 5 gemm (MXFP8). */
+ * 3 transpose_u8 (and the MX scale re-tiling), 4 gemm (FP8), 5 gemm (MXFP8), 6 gemm (BF16,
+ * rowwise_gw_hp dW), 7 P2P gather signal / wait kernels. */
 void fp8_profile_enable(int on);
 int fp8_profile_collect(int* kinds, float* ms, int max_n);
 

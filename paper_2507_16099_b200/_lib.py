@@ -80,6 +80,12 @@ SIGNATURES = {
     "fp8_fsdp_mx_workspace_bytes": (_c.c_size_t, [HP, _c.c_int]),
     "fp8_fsdp_allgather_mx": (_c.c_int, [_c.c_void_p, HP, _c.c_int, _c.POINTER(Tensor8), _c.c_void_p, _c.c_size_t,
                                          _c.c_void_p]),
+    "fp8_p2p_create": (_c.c_int, [_c.c_void_p, _c.c_size_t, _c.POINTER(_c.c_void_p)]),
+    "fp8_p2p_create_local": (_c.c_int, [_c.c_int, _c.c_size_t, _c.POINTER(_c.c_void_p)]),
+    "fp8_p2p_buffer": (_c.c_void_p, [_c.c_void_p]),
+    "fp8_p2p_destroy": (_c.c_int, [_c.c_void_p]),
+    "fp8_fsdp_allgather_p2p": (_c.c_int, [_c.c_void_p, HP, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_void_p,
+                                          _c.c_void_p]),
     "fp8_mx_scales_unshard": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),
 }
 AMAX_MULTI_MAX = 48

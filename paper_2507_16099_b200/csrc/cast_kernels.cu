@@ -13,19 +13,10 @@
 
 #include "kernels.h"
 #include "ptx.cuh"
+#include "scale.cuh"
 
 namespace fp8t {
 
-// eps = fp32(1e-12) (DESIGN.md R-c5), written as its bit pattern.
-__device__ __forceinline__ float kEps() { return __int_as_float(0x2B8CBCCC); }
-template <int FMT> __device__ __forceinline__ float kFmax() { return FMT == 0 ? 448.0f : 57344.0f; }
-template <int FMT> __device__ __forceinline__ int kEmax() { return FMT == 0 ? 8 : 15; }
-
-// s = RN32(fmax / max(amax, eps)), IEEE division (R-c3, R-c6).
-template <int FMT>
-__device__ __forceinline__ float scale_of(float amax) {
-  return __fdiv_rn(kFmax<FMT>(), fmaxf(amax, kEps()));
-}
 
 // ---------------------------------------------------------------------------
 // 8-element loads as fp32 (exact widening) and |x| bit patterns
@@ -677,6 +668,56 @@ __global__ void __launch_bounds__(256) sf_unshard_kernel(const uint4* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// cast_push: the tensorwise cast of an FSDP weight shard fused with the all-gather's data
+// movement (PAPER.md:596 enable_fp8_all_gather): each 8-byte group of codes is written straight
+// into slot `rank` of every rank's gather buffer over NVLink (peer pointers), so the FP8 bytes
+// never round-trip through local HBM and no collective kernel runs.  The last CTA to finish
+// (ticket on the local counter) fences at system scope and publishes the epoch to every peer.
+// ---------------------------------------------------------------------------
+template <typename T, int FMT>
+__global__ void __launch_bounds__(256) cast_push_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
+                                                        const float* __restrict__ scale,
+                                                        const __grid_constant__ P2PPeers pe, int64_t slot_off,
+                                                        P2PSig* mine, uint32_t epoch) {
+  const int t = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 128;
+  const int vrows = imin128(R - r0), vcols = imin128(C - c0);
+  const int cc = (t & 15) * 8;
+  const bool cvalid = cc < vcols;
+  Raw8<T> raw[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int rr = (t >> 4) + 16 * i;
+    if (cvalid && rr < vrows) raw[i].load(x + (r0 + rr) * ld + c0 + cc);
+  }
+  const float s = __ldg(scale);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int rr = (t >> 4) + 16 * i;
+    if (!cvalid || rr >= vrows) continue;
+    float v[8];
+    raw[i].get(v);
+    const uint2 b = cast8<FMT>(v, s);
+    const int64_t off = slot_off + (r0 + rr) * C + c0 + cc;
+    for (int j = 0; j < pe.P; ++j) {
+      int p = pe.rank + j;
+      if (p >= pe.P) p -= pe.P;
+      *reinterpret_cast<uint2*>(pe.buf[p] + off) = b;
+    }
+  }
+  __syncthreads();
+  if (t == 0) {
+    __threadfence_system();
+    const unsigned total = gridDim.x * gridDim.y;
+    if (atomicAdd(&mine->ctas, 1u) == total - 1) {   // every CTA's pushes happen-before this point
+      mine->ctas = 0;
+      __threadfence_system();
+      for (int p = 0; p < pe.P; ++p) st_release_sys_u64(&pe.sig[p]->done[pe.rank], epoch);
+    }
+  }
+}
+
 // FP8 byte transpose [R, C] -> [C, R] (R, C multiples of 16).
 __global__ void __launch_bounds__(256) transpose_u8_kernel(const uint8_t* __restrict__ in, int64_t R, int64_t C,
                                                            uint8_t* __restrict__ out) {
@@ -885,6 +926,20 @@ cudaError_t launch_sf_unshard(const uint8_t* in, int P, int64_t Kt, int64_t Tl, 
   LaunchScope ls(K_TRANSPOSE, s);
   sf_unshard_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(reinterpret_cast<const uint4*>(in), P, Kt, Tl,
                                                                         reinterpret_cast<uint4*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cast_push(const void* x, bool bf16, int fmt, int64_t R, int64_t C, int64_t ld, const float* scale,
+                             const P2PPeers& pe, int64_t slot_off, P2PSig* mine, uint32_t epoch, cudaStream_t s) {
+  const dim3 g = tile_grid(R, C);
+  LaunchScope ls(K_CAST, s);
+  if (bf16) {
+    if (fmt == 0) cast_push_kernel<__nv_bfloat16, 0><<<g, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), R, C, ld, scale, pe, slot_off, mine, epoch);
+    else cast_push_kernel<__nv_bfloat16, 1><<<g, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), R, C, ld, scale, pe, slot_off, mine, epoch);
+  } else {
+    if (fmt == 0) cast_push_kernel<float, 0><<<g, 256, 0, s>>>(static_cast<const float*>(x), R, C, ld, scale, pe, slot_off, mine, epoch);
+    else cast_push_kernel<float, 1><<<g, 256, 0, s>>>(static_cast<const float*>(x), R, C, ld, scale, pe, slot_off, mine, epoch);
+  }
   return cudaGetLastError();
 }
 

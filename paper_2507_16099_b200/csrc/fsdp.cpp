@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "fp8train.h"
+#include "comm.h"
 #include "kernels.h"
 
 namespace fp8t {
@@ -23,10 +24,6 @@ fp8_status_t cuda_check(cudaError_t e, const char* what);
 }  // namespace fp8t
 using namespace fp8t;
 
-struct fp8_comm_s {
-  ncclComm_t nccl;
-  int nranks, rank;
-};
 
 static fp8_status_t nccl_check(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return FP8_OK;

@@ -13,7 +13,8 @@ void count_launch();
 PFN_cuTensorMapEncodeTiled_v12000 get_encode();
 
 // Launch accounting + optional per-launch CUDA-event timing (fp8_profile_enable).
-enum { K_AMAX = 0, K_CAST = 1, K_MX = 2, K_TRANSPOSE = 3, K_GEMM = 4, K_GEMM_MX = 5, K_GEMM_BF16 = 6 };
+enum { K_AMAX = 0, K_CAST = 1, K_MX = 2, K_TRANSPOSE = 3, K_GEMM = 4, K_GEMM_MX = 5, K_GEMM_BF16 = 6,
+       K_SYNC = 7 };   // K_SYNC: the P2P gather's signal / wait kernels
 struct LaunchScope {
   int slot;
   cudaStream_t st;
@@ -50,6 +51,32 @@ cudaError_t launch_mx_cast(const void* x, bool bf16, int fmt, bool rceil, int64_
                            uint8_t* q0, uint8_t* sf0, uint8_t* q1, uint8_t* sf1, cudaStream_t s, bool tr1 = true);
 // Rank-major gathered dim1 E8M0 tiles [P][Kt][Tl][512 B] -> blocked full layout [Kt][P*Tl][512 B].
 cudaError_t launch_sf_unshard(const uint8_t* in, int P, int64_t Kt, int64_t Tl, uint8_t* out, cudaStream_t s);
+// ---- fused FP8 FSDP gather over NVLink peer memory (p2p.cu, cast_push in cast_kernels.cu) ----
+constexpr int P2P_MAXP = 64;
+struct P2PSig {                        // tail of every rank's window, written by peers
+  unsigned long long amax[P2P_MAXP];   // slot p: (epoch << 32) | amax bits of rank p's shard
+  unsigned long long done[P2P_MAXP];   // slot p: last epoch whose pushes from rank p are visible
+  unsigned int ctas;                   // local: finished CTAs of the running cast_push (last-CTA ticket)
+};
+struct P2PPeers {
+  uint8_t* buf[P2P_MAXP];              // every rank's gather buffer (peer pointers, UVA)
+  P2PSig* sig[P2P_MAXP];
+  int P, rank;
+};
+// Tensorwise cast of the shard x [R, C] with the device scale *scale, every 8-byte code group
+// stored to all P gather buffers at byte offset slot_off (rank-rotated order); the last CTA then
+// publishes `epoch` in done[rank] of every peer (release, system scope).
+cudaError_t launch_cast_push(const void* x, bool bf16, int fmt, int64_t R, int64_t C, int64_t ld, const float* scale,
+                             const P2PPeers& pe, int64_t slot_off, P2PSig* mine, uint32_t epoch, cudaStream_t s);
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 cudaError_t launch_transpose_u8(const uint8_t* in, int64_t R, int64_t C, uint8_t* out, cudaStream_t s);
 
 // tcgen05 GEMM: D[M,N] = A[M,K] B[N,K]^T with scales.

@@ -1,0 +1,263 @@
+// Fused FP8 FSDP weight all-gather over NVLink / NVSwitch peer memory (SURVEY §8a row a7,
+// PAPER.md:596 enable_fp8_all_gather; reading R-c18: one global scale from the MAX of the shard
+// amaxes).  Instead of cast -> ncclAllGather, each rank's cast kernel stores its FP8 codes
+// directly into slot `rank` of every rank's gather buffer (peer pointers opened with CUDA IPC),
+// so the collective's data movement IS the cast's output stream.
+//
+// Per call (rank r, epoch e = this window's call counter, identical on all ranks):
+//   1. amax(W_r) -> local u32 accumulator                       (existing amax kernel)
+//   2. p2p_signal_amax: amax slot r of every peer := (e << 32) | amax   (release, .sys)
+//   3. p2p_wait_scale : spin until all P slots carry epoch e; s = fmax / max(max_p amax_p, eps)
+//   4. cast_push      : q = satRNE(RN32(W_r * s)) stored to every peer's buffer at slot r;
+//                       the last CTA publishes done slot r := e on every peer  (release, .sys)
+//   5. p2p_wait_done  : spin until all P done slots >= e  -> the gathered codes are complete
+// Step 3 doubles as the cross-rank WAR barrier: rank p pushes epoch-e codes into my buffer only
+// after my epoch-e amax signal, which my stream issues after all my earlier work (the GEMMs that
+// read epoch e-1's codes).  Every spin has a 10 s watchdog (globaltimer) that traps instead of
+// hanging the GPU.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "comm.h"
+#include "fp8train.h"
+#include "kernels.h"
+#include "scale.cuh"
+
+namespace fp8t {
+fp8_status_t fail(fp8_status_t st, const char* fmt, ...);
+fp8_status_t cuda_check(cudaError_t e, const char* what);
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr uint64_t kWatchdogNs = 10ull * 1000 * 1000 * 1000;
+
+__global__ void p2p_signal_amax_kernel(const __grid_constant__ P2PPeers pe, const uint32_t* amax_bits, uint32_t epoch) {
+  const unsigned long long v = ((unsigned long long)epoch << 32) | (unsigned long long)*amax_bits;
+  for (int p = threadIdx.x; p < pe.P; p += blockDim.x) st_release_sys_u64(&pe.sig[p]->amax[pe.rank], v);
+}
+
+template <int FMT>
+__global__ void p2p_wait_scale_kernel(P2PSig* mine, int P, uint32_t epoch, float* scale_out, float* amax_out) {
+  const int lane = threadIdx.x;
+  uint32_t m = 0;
+  const uint64_t t0 = globaltimer_ns();
+  for (int p = lane; p < P; p += 32) {
+    unsigned long long v;
+    while (((v = ld_acquire_sys_u64(&mine->amax[p])) >> 32) != epoch) {
+      if (globaltimer_ns() - t0 > kWatchdogNs) {
+        printf("fp8train p2p: rank amax slot %d never reached epoch %u (watchdog)\n", p, epoch);
+        asm volatile("trap;");
+      }
+      __nanosleep(100);
+    }
+    m = max(m, (uint32_t)(v & 0xFFFFFFFFull));
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  if (lane == 0) {
+    const float a = __uint_as_float(m);
+    scale_out[0] = scale_of<FMT>(a);
+    if (amax_out) amax_out[0] = a;
+  }
+}
+
+__global__ void p2p_wait_done_kernel(P2PSig* mine, int P, uint32_t epoch) {
+  const uint64_t t0 = globaltimer_ns();
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    while (ld_acquire_sys_u64(&mine->done[p]) < epoch) {
+      if (globaltimer_ns() - t0 > kWatchdogNs) {
+        printf("fp8train p2p: rank %d pushes of epoch %u never completed (watchdog)\n", p, epoch);
+        asm volatile("trap;");
+      }
+      __nanosleep(100);
+    }
+  }
+}
+
+}  // namespace fp8t
+using namespace fp8t;
+
+struct fp8_p2p_s {
+  int P, rank;
+  size_t bytes;            // gather buffer bytes (the window's data part)
+  uint8_t* base;           // this rank's window (cudaMalloc), data then P2PSig
+  P2PSig* sig;             // this rank's signal block
+  P2PPeers peers;
+  std::vector<uint8_t*> opened;   // IPC-opened peer bases (to close)
+  uint32_t epoch;
+};
+
+static size_t sig_offset(size_t bytes) { return (bytes + 255) & ~size_t(255); }
+static size_t window_bytes(size_t bytes) { return sig_offset(bytes) + ((sizeof(P2PSig) + 255) & ~size_t(255)); }
+
+static fp8_status_t alloc_window(size_t bytes, uint8_t** base) {
+  fp8_status_t s = cuda_check(cudaMalloc(base, window_bytes(bytes)), "cudaMalloc (p2p window)");
+  if (s != FP8_OK) return s;
+  return cuda_check(cudaMemset(*base, 0, window_bytes(bytes)), "cudaMemset (p2p window)");
+}
+
+extern "C" {
+
+fp8_status_t fp8_p2p_create(fp8_comm_t comm, size_t bytes, fp8_p2p_t* out) {
+  if (!comm || !out) return fail(FP8_EINVAL, "comm/out: null pointer");
+  if (bytes == 0) return fail(FP8_EINVAL, "bytes must be > 0");
+  if (comm->nranks > P2P_MAXP) return fail(FP8_EUNSUPPORTED, "p2p window: at most %d ranks", P2P_MAXP);
+  const int P = comm->nranks, r = comm->rank;
+  uint8_t* base = nullptr;
+  fp8_status_t s = alloc_window(bytes, &base);
+  if (s != FP8_OK) return s;
+  auto* w = new fp8_p2p_s{};
+  w->P = P;
+  w->rank = r;
+  w->bytes = bytes;
+  w->base = base;
+  w->sig = reinterpret_cast<P2PSig*>(base + sig_offset(bytes));
+  w->epoch = 0;
+  w->peers.P = P;
+  w->peers.rank = r;
+  // exchange IPC handles over NCCL (device buffer of P handles, in-place all-gather)
+  cudaIpcMemHandle_t h;
+  std::vector<cudaIpcMemHandle_t> all(P);
+  void* d = nullptr;
+  cudaStream_t st = nullptr;
+  auto bail = [&](fp8_status_t e) {
+    if (d) cudaFree(d);
+    if (st) cudaStreamDestroy(st);
+    for (uint8_t* p : w->opened) cudaIpcCloseMemHandle(p);
+    cudaFree(base);
+    delete w;
+    return e;
+  };
+  if ((s = cuda_check(cudaIpcGetMemHandle(&h, base), "cudaIpcGetMemHandle")) != FP8_OK) return bail(s);
+  if ((s = cuda_check(cudaMalloc(&d, sizeof(h) * P), "cudaMalloc")) != FP8_OK) return bail(s);
+  if ((s = cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate")) != FP8_OK)
+    return bail(s);
+  if ((s = cuda_check(cudaMemcpy(static_cast<uint8_t*>(d) + sizeof(h) * r, &h, sizeof(h), cudaMemcpyHostToDevice),
+                      "cudaMemcpy")) != FP8_OK)
+    return bail(s);
+  ncclResult_t nr = ncclAllGather(static_cast<uint8_t*>(d) + sizeof(h) * r, d, sizeof(h), ncclUint8, comm->nccl, st);
+  if (nr != ncclSuccess) return bail(fail(FP8_ENCCL, "ncclAllGather (ipc handles): %s", ncclGetErrorString(nr)));
+  if ((s = cuda_check(cudaStreamSynchronize(st), "sync")) != FP8_OK) return bail(s);
+  if ((s = cuda_check(cudaMemcpy(all.data(), d, sizeof(h) * P, cudaMemcpyDeviceToHost), "cudaMemcpy")) != FP8_OK)
+    return bail(s);
+  for (int p = 0; p < P; ++p) {
+    uint8_t* pb = base;
+    if (p != r) {
+      void* ptr = nullptr;
+      if ((s = cuda_check(cudaIpcOpenMemHandle(&ptr, all[p], cudaIpcMemLazyEnablePeerAccess),
+                          "cudaIpcOpenMemHandle (peer window; needs P2P / NVLink)")) != FP8_OK)
+        return bail(s);
+      pb = static_cast<uint8_t*>(ptr);
+      w->opened.push_back(pb);
+    }
+    w->peers.buf[p] = pb;
+    w->peers.sig[p] = reinterpret_cast<P2PSig*>(pb + sig_offset(bytes));
+  }
+  // every window is zeroed and mapped before anyone signals into it
+  int* one = static_cast<int*>(d);
+  nr = ncclAllReduce(one, one, 1, ncclInt32, ncclSum, comm->nccl, st);
+  if (nr != ncclSuccess) return bail(fail(FP8_ENCCL, "ncclAllReduce (barrier): %s", ncclGetErrorString(nr)));
+  if ((s = cuda_check(cudaStreamSynchronize(st), "sync")) != FP8_OK) return bail(s);
+  cudaFree(d);
+  cudaStreamDestroy(st);
+  *out = w;
+  return FP8_OK;
+}
+
+fp8_status_t fp8_p2p_create_local(int nranks, size_t bytes, fp8_p2p_t* out) {
+  if (!out) return fail(FP8_EINVAL, "out: null pointer");
+  if (nranks < 1 || nranks > P2P_MAXP || bytes == 0) return fail(FP8_EINVAL, "bad nranks / bytes");
+  std::vector<uint8_t*> bases(nranks, nullptr);
+  for (int p = 0; p < nranks; ++p) {
+    fp8_status_t s = alloc_window(bytes, &bases[p]);
+    if (s != FP8_OK) {
+      for (uint8_t* b : bases)
+        if (b) cudaFree(b);
+      return s;
+    }
+  }
+  for (int r = 0; r < nranks; ++r) {
+    auto* w = new fp8_p2p_s{};
+    w->P = nranks;
+    w->rank = r;
+    w->bytes = bytes;
+    w->base = bases[r];
+    w->sig = reinterpret_cast<P2PSig*>(bases[r] + sig_offset(bytes));
+    w->epoch = 0;
+    w->peers.P = nranks;
+    w->peers.rank = r;
+    for (int p = 0; p < nranks; ++p) {
+      w->peers.buf[p] = bases[p];
+      w->peers.sig[p] = reinterpret_cast<P2PSig*>(bases[p] + sig_offset(bytes));
+    }
+    out[r] = w;
+  }
+  return FP8_OK;
+}
+
+void* fp8_p2p_buffer(fp8_p2p_t win) { return win ? win->base : nullptr; }
+
+fp8_status_t fp8_p2p_destroy(fp8_p2p_t win) {
+  if (!win) return FP8_OK;
+  fp8_status_t s = FP8_OK;
+  for (uint8_t* p : win->opened)
+    if (cudaIpcCloseMemHandle(p) != cudaSuccess) s = fail(FP8_ECUDA, "cudaIpcCloseMemHandle");
+  if (cudaFree(win->base) != cudaSuccess) s = fail(FP8_ECUDA, "cudaFree (p2p window)");
+  delete win;
+  return s;
+}
+
+fp8_status_t fp8_fsdp_allgather_p2p(fp8_p2p_t win, fp8_hp_t w, fp8_format_t fmt, const float* amax_in,
+                                    float* scale_out, float* amax_out, void* stream) {
+  if (!win) return fail(FP8_EINVAL, "win: null");
+  if (!w.ptr || !scale_out || (!amax_out && !amax_in)) return fail(FP8_EINVAL, "null pointer");
+  if (fmt != FP8_E4M3 && fmt != FP8_E5M2) return fail(FP8_EINVAL, "bad fp8 format");
+  if (w.dtype != FP8_DT_F32 && w.dtype != FP8_DT_BF16) return fail(FP8_EINVAL, "bad dtype");
+  if (w.rows < 16 || w.cols < 16 || w.rows % 16 || w.cols % 16)
+    return fail(FP8_EALIGN, "shard rows/cols: multiples of 16");
+  if (reinterpret_cast<uintptr_t>(w.ptr) & 15) return fail(FP8_EALIGN, "w_shard must be 16-byte aligned");
+  if (w.ld < w.cols || (w.ld * (w.dtype == FP8_DT_F32 ? 4 : 2)) % 16) return fail(FP8_EALIGN, "bad ld");
+  const size_t chunk = (size_t)w.rows * (size_t)w.cols;
+  if (chunk * (size_t)win->P > win->bytes) return fail(FP8_EINVAL, "window too small for nranks * shard bytes");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool bf16 = w.dtype == FP8_DT_BF16;
+  const uint32_t epoch = ++win->epoch;
+  fp8_status_t s;
+  const uint32_t* abits = reinterpret_cast<const uint32_t*>(amax_in);
+  if (!amax_in) {
+    uint32_t* acc = reinterpret_cast<uint32_t*>(amax_out);
+    if ((s = cuda_check(cudaMemsetAsync(acc, 0, 4, st), "memset")) != FP8_OK) return s;
+    if ((s = cuda_check(launch_amax(w.ptr, bf16, w.rows, w.cols, w.ld, 1, acc, nullptr, nullptr, st), "amax")) !=
+        FP8_OK)
+      return s;
+    abits = acc;
+  }
+  {
+    LaunchScope ls(K_SYNC, st);
+    p2p_signal_amax_kernel<<<1, 64, 0, st>>>(win->peers, abits, epoch);
+  }
+  if ((s = cuda_check(cudaGetLastError(), "p2p_signal_amax")) != FP8_OK) return s;
+  {
+    LaunchScope ls(K_SYNC, st);
+    if (fmt == FP8_E4M3) p2p_wait_scale_kernel<0><<<1, 32, 0, st>>>(win->sig, win->P, epoch, scale_out, amax_out);
+    else p2p_wait_scale_kernel<1><<<1, 32, 0, st>>>(win->sig, win->P, epoch, scale_out, amax_out);
+  }
+  if ((s = cuda_check(cudaGetLastError(), "p2p_wait_scale")) != FP8_OK) return s;
+  if ((s = cuda_check(launch_cast_push(w.ptr, bf16, fmt, w.rows, w.cols, w.ld, scale_out, win->peers,
+                                       (int64_t)(chunk * (size_t)win->rank), win->sig, epoch, st),
+                      "cast_push")) != FP8_OK)
+    return s;
+  {
+    LaunchScope ls(K_SYNC, st);
+    p2p_wait_done_kernel<<<1, 64, 0, st>>>(win->sig, win->P, epoch);
+  }
+  return cuda_check(cudaGetLastError(), "p2p_wait_done");
+}
+
+}  // extern "C"

@@ -107,3 +107,63 @@ class Comm:
         if self._h:
             L.check(L.lib.fp8_comm_destroy(self._h), "fp8_comm_destroy")
             self._h = ctypes.c_void_p()
+
+
+class _DevBuf:
+    """__cuda_array_interface__ view of library-owned device memory (the P2P gather buffer)."""
+
+    def __init__(self, ptr, shape, device):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+        self.device = device
+
+
+class P2PWindow:
+    """Fused FP8 FSDP gather over NVLink peer memory (fp8_fsdp_allgather_p2p): the cast kernel pushes
+    each rank's codes straight into every rank's gather buffer.  `bytes` >= world * shard bytes."""
+
+    def __init__(self, comm=None, nbytes=0, _handle=None, world=None, rank=None):
+        if _handle is not None:
+            self._h, self.world, self.rank = _handle, world, rank
+        else:
+            self._h = ctypes.c_void_p()
+            L.check(L.lib.fp8_p2p_create(comm._h, nbytes, ctypes.byref(self._h)), "fp8_p2p_create")
+            self.world, self.rank = comm.world, comm.rank
+        self.nbytes = nbytes
+
+    @classmethod
+    def local_group(cls, nranks, nbytes):
+        """nranks windows on this GPU mapped to each other (single-GPU simulation of the ranks; issue
+        each rank's gather on its own stream)."""
+        arr = (ctypes.c_void_p * nranks)()
+        L.check(L.lib.fp8_p2p_create_local(nranks, nbytes, arr), "fp8_p2p_create_local")
+        out = []
+        for r in range(nranks):
+            w = cls(_handle=ctypes.c_void_p(arr[r]), world=nranks, rank=r)
+            w.nbytes = nbytes
+            out.append(w)
+        return out
+
+    def buffer(self, rows, cols, device="cuda"):
+        """uint8 [rows, cols] torch view of this rank's gather buffer (library-owned memory)."""
+        if rows * cols > self.nbytes:
+            raise ValueError("view larger than the window")
+        ptr = L.lib.fp8_p2p_buffer(self._h)
+        return torch.as_tensor(_DevBuf(ptr, (rows, cols), device), device=device)
+
+    def allgather_fp8(self, w_shard, fmt="e4m3", scale=None, amax=None, amax_in=None, stream=None):
+        """Returns (codes [world*rows, cols] uint8 view of the window, scale float[1], global amax float[1])."""
+        rows, cols = w_shard.shape
+        dev = w_shard.device
+        if scale is None:
+            scale = torch.empty(1, dtype=torch.float32, device=dev)
+        if amax is None:
+            amax = torch.empty(1, dtype=torch.float32, device=dev)
+        L.check(L.lib.fp8_fsdp_allgather_p2p(self._h, hp(w_shard), FORMATS[fmt], _ptr(amax_in), _ptr(scale),
+                                             _ptr(amax), _stream(stream)), "fp8_fsdp_allgather_p2p")
+        return self.buffer(self.world * rows, cols, dev), scale, amax
+
+    def close(self):
+        if self._h:
+            L.check(L.lib.fp8_p2p_destroy(self._h), "fp8_p2p_destroy")
+            self._h = ctypes.c_void_p()

@@ -624,3 +624,98 @@ def test_mx_fsdp_allgather_single_rank():
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- fused P2P FP8 gather
+
+def _p2p_run(wins, shards, amax_in=None):
+    """Issue every simulated rank's fp8_fsdp_allgather_p2p on its own stream (each call waits for
+    the other ranks' signals), then wait for all of them."""
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in wins]
+    outs = []
+    for r, (w, sh) in enumerate(zip(wins, shards)):
+        with torch.cuda.stream(streams[r]):
+            outs.append(w.allgather_fp8(sh, "e4m3", amax_in=None if amax_in is None else amax_in[r]))
+    torch.cuda.synchronize()
+    return outs
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_p2p_gather_simulated_ranks(P):
+    """fp8_fsdp_allgather_p2p with P ranks simulated on one GPU (windows mapped to each other): every
+    rank's buffer == the unsharded tensorwise cast (oracle) and the global scale/amax agree, over
+    several epochs with a different weight each time (the signal slots are reused)."""
+    from paper_2507_16099_b200.fsdp import P2PWindow
+    N, K = 128 * P, 272
+    wins = P2PWindow.local_group(P, N * K)
+    try:
+        for it in range(3):
+            w = synth.weight_shard_c5((N, K), it, 0, 1)
+            if it == 1:
+                w[N - 3, 5] = 0.75    # global amax on the last rank's shard
+            q, s, a = ofsdp.allgather_ref(np.split(w, P, axis=0), E4M3)
+            shards = [_dev(v, torch.bfloat16) for v in np.split(w, P, axis=0)]
+            outs = _p2p_run(wins, shards)
+            for codes, sc, am in outs:
+                assert np.array_equal(_np(codes), q)
+                assert _bits(_np(sc))[0] == _bits(s).reshape(-1)[0]
+                assert _bits(_np(am))[0] == _bits(a).reshape(-1)[0]
+    finally:
+        for w_ in wins:
+            w_.close()
+
+
+def test_p2p_gather_precomputed_amax_and_linear():
+    """amax_in variant (no amax pass) and the gathered buffer as the tensorwise linear's w_fp8:
+    bit-identical to the hp-weight linear."""
+    from paper_2507_16099_b200.fsdp import P2PWindow
+    P, Mx, Nw, Kw = 2, 256, 384, 512
+    x, w, dy = synth.linear_inputs("c5", Mx, Nw, Kw, seed=1)
+    wins = P2PWindow.local_group(P, Nw * Kw)
+    try:
+        shards = [_dev(v, torch.bfloat16) for v in np.split(w, P, axis=0)]
+        gam = torch.tensor([fp8.amax(w)], dtype=torch.float32, device="cuda")
+        outs = _p2p_run(wins, shards, amax_in=[gam, gam])
+        q, s, _ = fp8.cast_tensorwise(w, E4M3)
+        plan = ops.LinearPlan(Mx, Nw, Kw, recipe="tensorwise", out_dtype=torch.float32)
+        X, W, G = _dev(x, torch.bfloat16), _dev(w, torch.bfloat16), _dev(dy, torch.bfloat16)
+        s1 = plan.new_saved()
+        y1 = plan.forward(X, W, s1).clone()
+        dx1, dw1 = (t.clone() for t in plan.backward(G, s1))
+        for codes, sc, _ in outs:
+            assert np.array_equal(_np(codes), q) and _bits(_np(sc))[0] == _bits(s).reshape(-1)[0]
+            s2 = plan.new_saved()
+            y2 = plan.forward(X, None, s2, w_fp8=(codes, sc)).clone()
+            dx2, dw2 = plan.backward(G, s2, w_fp8=(codes, sc))
+            torch.cuda.synchronize()
+            assert torch.equal(y1, y2) and torch.equal(dx1, dx2) and torch.equal(dw1, dw2)
+    finally:
+        for w_ in wins:
+            w_.close()
+
+
+def test_p2p_window_ipc_single_rank():
+    """fp8_p2p_create over a real (1-rank) NCCL communicator: IPC handle exchange + barrier, then
+    the fused gather == the NCCL gather == the oracle."""
+    import os
+    import torch.distributed as dist
+    from paper_2507_16099_b200.fsdp import Comm, P2PWindow
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = "29543"
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = Comm()
+        N, K = 384, 512
+        w = synth.weight_shard_c5((N, K), 3, 0, 1)
+        win = P2PWindow(comm, N * K)
+        for _ in range(2):
+            codes, sc, am = win.allgather_fp8(_dev(w, torch.bfloat16), "e4m3")
+            wq, ws_, wa = comm.allgather_fp8(_dev(w, torch.bfloat16), "e4m3")
+            torch.cuda.synchronize()
+            assert torch.equal(codes, wq) and torch.equal(sc, ws_) and torch.equal(am, wa)
+        assert np.array_equal(_np(codes), fp8.cast_tensorwise(w, E4M3)[0])
+        win.close()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
