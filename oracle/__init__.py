@@ -29,6 +29,6 @@ one deliberately unpinned quantity is the GPU GEMM's fp32 accumulation
 order, which is graded by tolerance.
 """
 
-from . import codecs, fp8, mx, gemm, linear, fsdp  # noqa: F401
+from . import codecs, fp8, mx, gemm, linear, fsdp, grouped  # noqa: F401
 
-__all__ = ["codecs", "fp8", "mx", "gemm", "linear", "fsdp"]
+__all__ = ["codecs", "fp8", "mx", "gemm", "linear", "fsdp", "grouped"]
