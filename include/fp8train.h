@@ -272,6 +272,32 @@ fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const f
                                void* dw, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * MoE scaled grouped GEMM ("scaled_grouped_mm: differentiable scaled
+ * grouped GEMM for MoE FP8 training"; reading R-c22): the Float8Linear recipe applied
+ * per expert to expert-sorted tokens, each pass ONE persistent tcgen05 launch.
+ *   x [T,K] tokens sorted by expert; w [E*N, K] the E expert weights stacked (expert g
+ *   = rows g*N..(g+1)*N-1, nn.Linear layout); dy [T,N]; y [T,N], dx [T,K], dw [E*N,K].
+ *   offs: DEVICE int32[E+1], offs[0] = 0 <= offs[1] <= ... <= offs[E] = T, every entry
+ *   a multiple of 128 (MoE token groups padded to 128 rows); expert g owns token rows
+ *   [offs[g], offs[g+1]); empty experts allowed (dW_g = 0).  The offsets are validated
+ *   on the device: a violation traps the kernel (reported as FP8_ECUDA at the next
+ *   sync) -- the call never reads them on the host, so it never synchronises.
+ *   Recipes: tensorwise (one scale per X, W, dY) or rowwise (per token row, per expert
+ *   weight row / column, per (expert, column) over the expert's tokens for dW).
+ *   T, N multiples of 128; K multiple of 16; 1 <= E <= 256.
+ *   saved: fp8_grouped_saved_bytes(); ws: fp8_grouped_workspace_bytes() bytes.
+ *   x in fp8_grouped_linear_bwd gives K only (ptr may be NULL).
+ * ------------------------------------------------------------------------- */
+size_t fp8_grouped_saved_bytes(const fp8_linear_cfg_t* cfg, int64_t T, int64_t E, int64_t N, int64_t K);
+size_t fp8_grouped_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t T, int64_t E, int64_t N, int64_t K);
+fp8_status_t fp8_grouped_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w, int64_t E,
+                                    const int32_t* offs, void* y, void* saved, void* ws,
+                                    size_t ws_bytes, void* stream);
+fp8_status_t fp8_grouped_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x, int64_t E,
+                                    const int32_t* offs, const void* saved, void* dx, void* dw,
+                                    void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
  * FSDP2-style FP8 weight all-gather (PAPER.md:596 enable_fp8_all_gather;
  * reading R-c18): per rank, amax of the local shard -> NCCL all-reduce MAX ->
  * s = RN32(fmax / max(amax, eps)) -> cast the shard into slot `rank` of

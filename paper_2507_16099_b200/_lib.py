@@ -68,6 +68,14 @@ SIGNATURES = {
                                      _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
     "fp8_linear_bwd_ex": (_c.c_int, [_c.POINTER(LinearCfg), HP, _c.c_void_p, HP, _c.c_void_p, _c.POINTER(Tensor8),
                                      _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
+    "fp8_grouped_saved_bytes": (_c.c_size_t, [_c.POINTER(LinearCfg), _c.c_int64, _c.c_int64, _c.c_int64,
+                                               _c.c_int64]),
+    "fp8_grouped_workspace_bytes": (_c.c_size_t, [_c.POINTER(LinearCfg), _c.c_int64, _c.c_int64, _c.c_int64,
+                                                   _c.c_int64]),
+    "fp8_grouped_linear_fwd": (_c.c_int, [_c.POINTER(LinearCfg), HP, HP, _c.c_int64, _c.c_void_p, _c.c_void_p,
+                                          _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
+    "fp8_grouped_linear_bwd": (_c.c_int, [_c.POINTER(LinearCfg), HP, HP, _c.c_int64, _c.c_void_p, _c.c_void_p,
+                                          _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
     "fp8_comm_get_unique_id": (_c.c_int, [_c.c_void_p]),
     "fp8_comm_init": (_c.c_int, [_c.POINTER(_c.c_void_p), _c.c_void_p, _c.c_int, _c.c_int]),
     "fp8_comm_destroy": (_c.c_int, [_c.c_void_p]),

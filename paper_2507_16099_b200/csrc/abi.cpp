@@ -753,4 +753,204 @@ gemms:
   return FP8_OK;
 }
 
+// ---------------------------------------------------------------------------
+// MoE scaled grouped GEMM (PAPER.md:739 scaled_grouped_mm; reading R-c22): the Float8Linear
+// recipe per expert on expert-sorted tokens.  One M-grouped launch for Y; one launch carrying
+// the M-grouped dX and the K-grouped dW problems.  Scaling units never cross an expert: rowwise
+// column scales are kept per (expert, column) (segmented amax / cast kernels).
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+namespace {
+
+struct GSaved {
+  uint8_t* xT; uint8_t* wT;   // tensorwise: Xq [T,K], Wq [E*N,K]; rowwise: per-expert column-scaled copies
+  float* sx; float* sw;       // tensorwise [1], [1]; rowwise [E*K], [E*K]
+};
+GSaved carve_gsaved(const fp8_linear_cfg_t* cfg, int64_t T, int64_t E, int64_t N, int64_t K, void* base,
+                    size_t* bytes) {
+  Carve c(base);
+  GSaved g;
+  g.xT = c.take<uint8_t>((size_t)T * K);
+  g.wT = c.take<uint8_t>((size_t)E * N * K);
+  const bool tw = cfg->recipe == FP8_RECIPE_TENSORWISE;
+  g.sx = c.take<float>(tw ? 4 : 4 * E * K);
+  g.sw = c.take<float>(tw ? 4 : 4 * E * K);
+  if (bytes) *bytes = c.off;
+  return g;
+}
+struct GFwdWs {
+  uint8_t* xq; uint8_t* wq;          // rowwise row-scaled codes
+  float* amax;                       // tensorwise [2]; rowwise [T + E*K + E*N + E*K]
+  float* sxr; float* swr;            // rowwise row scales [T], [E*N]
+};
+GFwdWs carve_gfwd(const fp8_linear_cfg_t* cfg, int64_t T, int64_t E, int64_t N, int64_t K, void* base, size_t* bytes) {
+  Carve c(base);
+  GFwdWs w{};
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    w.amax = c.take<float>(8);
+  } else {
+    w.xq = c.take<uint8_t>((size_t)T * K);
+    w.wq = c.take<uint8_t>((size_t)E * N * K);
+    w.amax = c.take<float>(4 * (T + E * K + E * N + E * K));
+    w.sxr = c.take<float>(4 * T);
+    w.swr = c.take<float>(4 * E * N);
+  }
+  if (bytes) *bytes = c.off;
+  return w;
+}
+struct GBwdWs {
+  uint8_t* g; uint8_t* gT;           // dY row-scaled [T,N]; rowwise: per-expert column-scaled [T,N]
+  float* amax;                       // tensorwise [1]; rowwise [T + E*N]
+  float* sg; float* sgT;             // tensorwise [1]; rowwise [T], [E*N]
+};
+GBwdWs carve_gbwd(const fp8_linear_cfg_t* cfg, int64_t T, int64_t E, int64_t N, void* base, size_t* bytes) {
+  Carve c(base);
+  GBwdWs w{};
+  const bool tw = cfg->recipe == FP8_RECIPE_TENSORWISE;
+  w.g = c.take<uint8_t>((size_t)T * N);
+  w.gT = tw ? nullptr : c.take<uint8_t>((size_t)T * N);
+  w.amax = c.take<float>(tw ? 4 : 4 * (T + E * N));
+  w.sg = c.take<float>(tw ? 4 : 4 * T);
+  w.sgT = tw ? w.sg : c.take<float>(4 * E * N);
+  if (bytes) *bytes = c.off;
+  return w;
+}
+
+fp8_status_t check_grouped(const fp8_linear_cfg_t* cfg, int64_t T, int64_t E, int64_t N, int64_t K, const int* offs) {
+  if (!cfg) return fail(FP8_EINVAL, "cfg: null pointer");
+  if (cfg->recipe != FP8_RECIPE_TENSORWISE && cfg->recipe != FP8_RECIPE_ROWWISE)
+    return fail(FP8_EUNSUPPORTED, "grouped GEMM: tensorwise or rowwise recipe");
+  FP8T_TRY(check_fmt(cfg->fmt_fwd));
+  FP8T_TRY(check_fmt(cfg->fmt_grad));
+  if (cfg->out_dtype != FP8_DT_BF16 && cfg->out_dtype != FP8_DT_F32) return fail(FP8_EINVAL, "bad out_dtype");
+  if (E < 1 || E > GEMM_MAX_GROUPS) return fail(FP8_EINVAL, "E must be in [1, %d]", GEMM_MAX_GROUPS);
+  if (!offs) return fail(FP8_EINVAL, "offs: null pointer");
+  if (T < 128 || T % 128) return fail(FP8_EALIGN, "T (tokens) must be a positive multiple of 128");
+  if (N < 128 || N % 128) return fail(FP8_EALIGN, "N (expert rows) must be a positive multiple of 128");
+  if (K < 16 || K % 16) return fail(FP8_EALIGN, "K must be a positive multiple of 16");
+  if (T > (1 << 30) || E * N > (1 << 30)) return fail(FP8_EINVAL, "dims too large");
+  return FP8_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t fp8_grouped_saved_bytes(const fp8_linear_cfg_t* cfg, int64_t T, int64_t E, int64_t N, int64_t K) {
+  if (!cfg) return 0;
+  size_t b = 0;
+  carve_gsaved(cfg, T, E, N, K, nullptr, &b);
+  return b;
+}
+
+size_t fp8_grouped_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t T, int64_t E, int64_t N, int64_t K) {
+  if (!cfg) return 0;
+  size_t f = 0, b = 0;
+  carve_gfwd(cfg, T, E, N, K, nullptr, &f);
+  carve_gbwd(cfg, T, E, N, nullptr, &b);
+  return f > b ? f : b;
+}
+
+fp8_status_t fp8_grouped_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w, int64_t E, const int32_t* offs,
+                                    void* y, void* saved, void* ws, size_t ws_bytes, void* stream) {
+  FP8T_TRY(check_hp(x, "x"));
+  FP8T_TRY(check_hp(w, "w"));
+  const int64_t T = x.rows, K = x.cols;
+  if (E < 1 || w.rows % E) return fail(FP8_EINVAL, "w.rows must be E * N");
+  const int64_t N = w.rows / E;
+  if (w.cols != K) return fail(FP8_EINVAL, "w.cols != x.cols");
+  FP8T_TRY(check_grouped(cfg, T, E, N, K, offs));
+  FP8T_TRY(check_ptr(y, "y"));
+  FP8T_TRY(check_ptr(saved, "saved"));
+  FP8T_TRY(check_ptr(ws, "ws"));
+  if (ws_bytes < fp8_grouped_workspace_bytes(cfg, T, E, N, K)) return fail(FP8_EWORKSPACE, "workspace too small");
+  cudaStream_t st = S(stream);
+  const bool xb = x.dtype == FP8_DT_BF16, wb = w.dtype == FP8_DT_BF16;
+  const int ff = cfg->fmt_fwd, of32 = cfg->out_dtype == FP8_DT_F32;
+  GSaved sv = carve_gsaved(cfg, T, E, N, K, saved, nullptr);
+  GFwdWs fw = carve_gfwd(cfg, T, E, N, K, ws, nullptr);
+  Seg tok{offs, (int)E, 0}, exp_rows{nullptr, 0, (int)N};
+  GemmProblem p{};
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    uint32_t* a = reinterpret_cast<uint32_t*>(fw.amax);
+    FP8T_CUDA(cudaMemsetAsync(a, 0, 8, st), "memset");
+    FP8T_CUDA(launch_amax(x.ptr, xb, T, K, x.ld, 1, a, nullptr, nullptr, st), "amax x");
+    FP8T_CUDA(launch_amax(w.ptr, wb, E * N, K, w.ld, 1, a + 1, nullptr, nullptr, st), "amax w");
+    FP8T_CUDA(launch_cast(x.ptr, xb, ff, T, K, x.ld, 1, 0, fw.amax, fw.amax, sv.xT, nullptr, sv.sx, nullptr, st), "cast x");
+    FP8T_CUDA(launch_cast(w.ptr, wb, ff, E * N, K, w.ld, 1, 0, fw.amax + 1, fw.amax + 1, sv.wT, nullptr, sv.sw, nullptr,
+                          st), "cast w");
+    p = GemmProblem{sv.xT, sv.wT, ff, ff, 0, 0, sv.sx, sv.sw, 0, T, N, K, K, K, y, of32, N};
+  } else {
+    float* axr = fw.amax;
+    float* axc = axr + T;          // [E, K] per (expert, column) over the expert's tokens
+    float* awr = axc + E * K;      // [E*N]
+    float* awc = awr + E * N;      // [E, K] per (expert, column) over the expert's N rows
+    FP8T_CUDA(cudaMemsetAsync(fw.amax, 0, 4 * (T + E * K + E * N + E * K), st), "memset");
+    FP8T_CUDA(launch_amax(x.ptr, xb, T, K, x.ld, 6, nullptr, (uint32_t*)axr, (uint32_t*)axc, st, tok), "amax x");
+    FP8T_CUDA(launch_amax(w.ptr, wb, E * N, K, w.ld, 6, nullptr, (uint32_t*)awr, (uint32_t*)awc, st, exp_rows),
+              "amax w");
+    FP8T_CUDA(launch_cast(x.ptr, xb, ff, T, K, x.ld, 2, 5, axr, axc, fw.xq, sv.xT, fw.sxr, sv.sx, st, tok), "cast x");
+    FP8T_CUDA(launch_cast(w.ptr, wb, ff, E * N, K, w.ld, 2, 5, awr, awc, fw.wq, sv.wT, fw.swr, sv.sw, st, exp_rows),
+              "cast w");
+    p = GemmProblem{fw.xq, fw.wq, ff, ff, 0, 0, fw.sxr, fw.swr, 1, T, N, K, K, K, y, of32, N};
+  }
+  p.grouped = 1;
+  p.G = (int)E;
+  p.offs = offs;
+  FP8T_CUDA(launch_gemm(p, st), "grouped gemm fwd");
+  return FP8_OK;
+}
+
+fp8_status_t fp8_grouped_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x, int64_t E, const int32_t* offs,
+                                    const void* saved, void* dx, void* dw, void* ws, size_t ws_bytes, void* stream) {
+  FP8T_TRY(check_hp(dy, "dy"));
+  FP8T_TRY(check_hp(x, "x", false));
+  const int64_t T = dy.rows, N = dy.cols, K = x.cols;
+  if (x.rows != T) return fail(FP8_EINVAL, "x.rows != dy.rows");
+  FP8T_TRY(check_grouped(cfg, T, E, N, K, offs));
+  FP8T_TRY(check_ptr(saved, "saved"));
+  FP8T_TRY(check_ptr(ws, "ws"));
+  if (dx) FP8T_TRY(check_ptr(dx, "dx"));
+  if (dw) FP8T_TRY(check_ptr(dw, "dw"));
+  if (ws_bytes < fp8_grouped_workspace_bytes(cfg, T, E, N, K)) return fail(FP8_EWORKSPACE, "workspace too small");
+  if (!dx && !dw) return FP8_OK;
+  cudaStream_t st = S(stream);
+  const bool gb = dy.dtype == FP8_DT_BF16;
+  const int ff = cfg->fmt_fwd, fg = cfg->fmt_grad, of32 = cfg->out_dtype == FP8_DT_F32;
+  GSaved sv = carve_gsaved(cfg, T, E, N, K, const_cast<void*>(saved), nullptr);
+  GBwdWs bw = carve_gbwd(cfg, T, E, N, ws, nullptr);
+  Seg tok{offs, (int)E, 0};
+  GemmProblem ps[2];
+  int n = 0;
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    FP8T_CUDA(cudaMemsetAsync(bw.amax, 0, 4, st), "memset");
+    FP8T_CUDA(launch_amax(dy.ptr, gb, T, N, dy.ld, 1, (uint32_t*)bw.amax, nullptr, nullptr, st), "amax dy");
+    FP8T_CUDA(launch_cast(dy.ptr, gb, fg, T, N, dy.ld, 1, 0, bw.amax, bw.amax, bw.g, nullptr, bw.sg, nullptr, st),
+              "cast dy");
+    // dX_g = dY_g W_g: A = Gq K-major over N; B = Wq [E*N, K] read MN-major (expert g = contraction rows g*N..)
+    if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 1, bw.sg, sv.sw, 0, T, K, N, N, K, dx, of32, K};
+    // dW_g = dY_g^T X_g: both MN-major, contraction over the expert's tokens
+    if (dw) ps[n++] = GemmProblem{bw.g, sv.xT, fg, ff, 1, 1, bw.sg, sv.sx, 0, N, K, T, N, K, dw, of32, K};
+  } else {
+    float* ar = bw.amax;
+    float* ac = ar + T;   // [E, N]
+    FP8T_CUDA(cudaMemsetAsync(bw.amax, 0, 4 * (T + E * N), st), "memset");
+    FP8T_CUDA(launch_amax(dy.ptr, gb, T, N, dy.ld, dw ? (dx ? 6 : 4) : 2, nullptr, (uint32_t*)ar, (uint32_t*)ac, st, tok),
+              "amax dy");
+    FP8T_CUDA(launch_cast(dy.ptr, gb, fg, T, N, dy.ld, dx ? 2 : 0, dw ? 5 : 0, ar, ac, bw.g, bw.gT, bw.sg, bw.sgT, st,
+                          tok),
+              "cast dy");
+    if (dx) ps[n++] = GemmProblem{bw.g, sv.wT, fg, ff, 0, 1, bw.sg, sv.sw, 1, T, K, N, N, K, dx, of32, K};
+    if (dw) ps[n++] = GemmProblem{bw.gT, sv.xT, fg, ff, 1, 1, bw.sgT, sv.sx, 1, N, K, T, N, K, dw, of32, K};
+  }
+  for (int i = 0; i < n; ++i) {
+    ps[i].grouped = ps[i].a_mn && ps[i].b_mn ? 2 : 1;
+    ps[i].G = (int)E;
+    ps[i].offs = offs;
+  }
+  FP8T_CUDA(launch_gemms(ps, n, st), "grouped gemm dx/dw");
+  return FP8_OK;
+}
+
 }  // extern "C"

@@ -69,6 +69,27 @@ template <> struct Raw8<__nv_bfloat16> {
 };
 
 __device__ __forceinline__ int imin128(int64_t v) { return v < 128 ? (int)v : 128; }
+
+// Segment of row r0 (grouped recipe): returns its index and first row.  offs: the g with
+// offs[g] <= r0 < offs[g+1] (empty groups skipped); seg_rows: fixed-size segments.
+__device__ __forceinline__ int seg_of(const Seg& sg, int64_t r0, int64_t& start) {
+  if (sg.offs) {
+    int lo = 0, hi = sg.G;   // invariant: offs[lo] <= r0 < offs[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(sg.offs + mid) <= r0) lo = mid; else hi = mid;
+    }
+    start = __ldg(sg.offs + lo);
+    return lo;
+  }
+  if (sg.seg_rows > 0) {
+    const int g = (int)(r0 / sg.seg_rows);
+    start = (int64_t)g * sg.seg_rows;
+    return g;
+  }
+  start = 0;
+  return 0;
+}
 __device__ __forceinline__ uint32_t abs_bits(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
 
 template <int FMT>
@@ -136,7 +157,7 @@ __device__ __forceinline__ void store_transposed(const uint32_t* tile, uint8_t* 
 template <typename T, int MODE>  // MODE bit0: tensor, bit1: row, bit2: col
 __global__ void __launch_bounds__(256) amax_tile_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
                                                         uint32_t* amax_tensor, uint32_t* amax_row,
-                                                        uint32_t* amax_col) {
+                                                        uint32_t* amax_col, const Seg seg) {
   // Persistent over 128 x 128 tiles in increasing linear order (the cast kernel walks them in
   // decreasing order, so its first reads hit the tiles this kernel touched last, still in L2).
   __shared__ uint32_t colred[8][128];
@@ -190,7 +211,9 @@ __global__ void __launch_bounds__(256) amax_tile_kernel(const T* __restrict__ x,
         uint32_t m = colred[0][t];
 #pragma unroll
         for (int w = 1; w < 8; ++w) m = max(m, colred[w][t]);
-        atomicMax(amax_col + c0 + t, m);
+        int64_t sstart;
+        const int g = seg_of(seg, r0, sstart);
+        atomicMax(amax_col + (int64_t)g * C + c0 + t, m);
       }
       __syncthreads();
     }
@@ -313,7 +336,8 @@ template <typename T, int FMT, int QM, int TM_>
 __global__ void __launch_bounds__(256) cast_tile_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
                                                         const float* __restrict__ amax_q,
                                                         const float* __restrict__ amax_t, uint8_t* __restrict__ q,
-                                                        uint8_t* __restrict__ qt, float* scale_q, float* scale_t) {
+                                                        uint8_t* __restrict__ qt, float* scale_q, float* scale_t,
+                                                        const Seg seg) {
   // TM_ >= 4: the second output is written row-major ([R,C], like q) with scale mode TM_ - 2,
   // i.e. the column-scaled copy the backward GEMMs read MN-major (no transpose).
   constexpr bool TRM = TM_ >= 4;
@@ -342,11 +366,13 @@ __global__ void __launch_bounds__(256) cast_tile_kernel(const T* __restrict__ x,
         sv[t] = s;
         if (out && bx == 0) out[r0 + t] = s;
       }
-    } else if (mode == 3) {
+    } else if (mode == 3) {   // per column (per segment of rows in the grouped recipe)
       if (t < vcols) {
-        const float s = scale_of<FMT>(amax[c0 + t]);
+        int64_t sstart;
+        const int64_t cbase = (int64_t)seg_of(seg, r0, sstart) * C;
+        const float s = scale_of<FMT>(amax[cbase + c0 + t]);
         sv[t] = s;
-        if (out && by == 0) out[c0 + t] = s;
+        if (out && r0 == sstart) out[cbase + c0 + t] = s;
       }
     }
   };
@@ -754,7 +780,7 @@ static inline dim3 tile_grid(int64_t R, int64_t C) { return dim3((unsigned)((C +
 
 template <typename T>
 static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, int mode, uint32_t* at,
-                                 uint32_t* ar, uint32_t* ac, cudaStream_t st) {
+                                 uint32_t* ar, uint32_t* ac, cudaStream_t st, const Seg& seg) {
   const T* p = static_cast<const T*>(x);
   if (mode == 1 && ld == C) {
     const int64_t n16 = R * C * (int64_t)sizeof(T) / 16;
@@ -779,10 +805,10 @@ static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
   dim3 g((unsigned)(tiles < cap ? tiles : cap));
   LaunchScope ls(K_AMAX, st);
   switch (mode) {
-    case 1: amax_tile_kernel<T, 1><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac); break;
-    case 2: amax_tile_kernel<T, 2><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac); break;
-    case 4: amax_tile_kernel<T, 4><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac); break;
-    case 6: amax_tile_kernel<T, 6><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac); break;
+    case 1: amax_tile_kernel<T, 1><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac, seg); break;
+    case 2: amax_tile_kernel<T, 2><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac, seg); break;
+    case 4: amax_tile_kernel<T, 4><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac, seg); break;
+    case 6: amax_tile_kernel<T, 6><<<g, 256, 0, st>>>(p, R, C, ld, at, ar, ac, seg); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -799,39 +825,39 @@ cudaError_t launch_amax_multi(const AmaxMultiArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_amax(const void* x, bool bf16, int64_t R, int64_t C, int64_t ld, int mode, uint32_t* at,
-                        uint32_t* ar, uint32_t* ac, cudaStream_t st) {
-  return bf16 ? amax_launch_t<__nv_bfloat16>(x, R, C, ld, mode, at, ar, ac, st)
-              : amax_launch_t<float>(x, R, C, ld, mode, at, ar, ac, st);
+                        uint32_t* ar, uint32_t* ac, cudaStream_t st, const Seg& seg) {
+  return bf16 ? amax_launch_t<__nv_bfloat16>(x, R, C, ld, mode, at, ar, ac, st, seg)
+              : amax_launch_t<float>(x, R, C, ld, mode, at, ar, ac, st, seg);
 }
 
 template <typename T, int FMT>
 static cudaError_t cast_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, int qm, int tm,
                                  const float* aq, const float* at, uint8_t* q, uint8_t* qt, float* sq, float* st,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, const Seg& seg) {
   const T* p = static_cast<const T*>(x);
   dim3 g = tile_grid(R, C);
 #define FP8T_CAST(QM, TM)                                                                       \
   if (qm == QM && tm == TM) {                                                                   \
     LaunchScope ls(K_CAST, s);                                                                  \
-    cast_tile_kernel<T, FMT, QM, TM><<<g, 256, 0, s>>>(p, R, C, ld, aq, at, q, qt, sq, st);     \
+    cast_tile_kernel<T, FMT, QM, TM><<<g, 256, 0, s>>>(p, R, C, ld, aq, at, q, qt, sq, st, seg);\
     return cudaGetLastError();                                                                  \
   }
   FP8T_CAST(1, 0) FP8T_CAST(0, 1) FP8T_CAST(1, 1)
   FP8T_CAST(2, 0) FP8T_CAST(0, 2) FP8T_CAST(2, 2)
   FP8T_CAST(3, 0) FP8T_CAST(0, 3) FP8T_CAST(3, 3)
-  FP8T_CAST(2, 3) FP8T_CAST(2, 5)
+  FP8T_CAST(2, 3) FP8T_CAST(2, 5) FP8T_CAST(0, 5)
 #undef FP8T_CAST
   return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_cast(const void* x, bool bf16, int fmt, int64_t R, int64_t C, int64_t ld, int qm, int tm,
                         const float* aq, const float* at, uint8_t* q, uint8_t* qt, float* sq, float* st,
-                        cudaStream_t s) {
+                        cudaStream_t s, const Seg& seg) {
   if (bf16)
-    return fmt == 0 ? cast_launch_t<__nv_bfloat16, 0>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s)
-                    : cast_launch_t<__nv_bfloat16, 1>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s);
-  return fmt == 0 ? cast_launch_t<float, 0>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s)
-                  : cast_launch_t<float, 1>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s);
+    return fmt == 0 ? cast_launch_t<__nv_bfloat16, 0>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s, seg)
+                    : cast_launch_t<__nv_bfloat16, 1>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s, seg);
+  return fmt == 0 ? cast_launch_t<float, 0>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s, seg)
+                  : cast_launch_t<float, 1>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s, seg);
 }
 
 template <typename T, int FMT, bool RC>

@@ -42,6 +42,7 @@ namespace fp8t {
 constexpr int BM = 128, BN = 256, BK = 128;   // per-CTA M rows, MMA N, K atom (bytes)
 constexpr int SF_CHUNK = 512;                 // E8M0 tile: 128 rows x 4 K-blocks of 32 (one K atom)
 constexpr int GROUP_M = 16;                   // grouped raster: 16 M-tiles share the N sweep
+constexpr int GMAX = GEMM_MAX_GROUPS;         // MoE grouped GEMM: groups per problem
 
 // One GEMM problem of a (possibly two-problem) launch.
 struct Prob {
@@ -54,6 +55,13 @@ struct Prob {
   int out_f32, row_scales;
   int a_mn, b_mn;     // operand majors (MN-major: TMA boxes 128 MN x 128 K, K step 4 KB)
   uint32_t* out_amax; // optional: atomicMax of |D| bit patterns (amax of the stored output values)
+  // MoE grouped problems (scaled_grouped_mm): offs = device [G+1] row offsets
+  //   grouped 1 (M-grouped, fwd / dX): group g owns rows [offs[g], offs[g+1]) of A, D and sa; B is
+  //             expert g's block (K-major: rows g*N.., MN-major: K rows g*K..); sb index g*N + col
+  //   grouped 2 (K-grouped, dW): group g contracts over rows [offs[g], offs[g+1]) of both MN-major
+  //             operands; D rows g*M.., sa index g*M + row, sb index g*N + col; empty group -> 0
+  int grouped, G;
+  const int* offs;
 };
 // A launch processes the tiles of p0 ([0, t1)) then p1 ([t1, num_tiles)) on one persistent grid:
 // the backward's dX and dW GEMMs share one launch, so neither has its own wave-quantisation tail.
@@ -64,7 +72,7 @@ struct GemmArgs {
   int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
 };
 
-template <bool MX, int CG, int ST, int KS, bool BF = false> struct Layout {
+template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false> struct Layout {
   static constexpr int STAGES = ST;
   static constexpr int ACC = MX ? 1 : 2;
   static constexpr int EPI_WARPS = ACC == 1 ? 8 : 4;        // see the epilogue
@@ -83,7 +91,10 @@ template <bool MX, int CG, int ST, int KS, bool BF = false> struct Layout {
   static constexpr uint32_t off_bar = off_epi + EPI_WARPS * 2048;
   static constexpr uint32_t n_bar = 2 * STAGES + 2 * ACC;
   static constexpr uint32_t off_tmem = off_bar + 8 * n_bar;
-  static constexpr uint32_t bytes = off_tmem + 16 + 1024;  // + alignment slack
+  // grouped: per problem the group offsets and the prefix of M tiles (ints, 2 x 2 x (GMAX + 1))
+  static constexpr uint32_t off_grp = off_tmem + 16;
+  static constexpr uint32_t grp_bytes = GRP ? 16 * (GMAX + 1) : 0;
+  static constexpr uint32_t bytes = off_grp + grp_bytes + 1024;  // + alignment slack
   static constexpr uint32_t tmem_cols = 512;
   // MX TMEM columns after the single accumulator, one set per pipeline stage (so the tcgen05.cp of
   // stage s+1 never overwrites columns the MMAs of stage s still read): stage s, SFA atom t at
@@ -92,6 +103,15 @@ template <bool MX, int CG, int ST, int KS, bool BF = false> struct Layout {
   static constexpr uint32_t sfa_col = 256, sfb_col = 256 + 4 * KS;
   static_assert(!MX || 256 + STAGES * SF_COLS <= 512, "TMEM columns");
   static constexpr uint32_t tx_bytes = CG * (A_STAGE + B_STAGE + SFA_STAGE + SFB_STAGE);  // counted on the leader
+};
+
+// Where one output tile of a (possibly grouped) problem lives.
+struct TileInfo {
+  int pi, mb, nb;
+  int m_valid;                     // rows of this problem / group
+  int a_row0, a_k0, b_row0, b_k0;  // operand coordinate offsets (grouped problems)
+  int num_kb, katoms;              // K stages of the tile, valid 128-deep K atoms
+  int64_t d_row0, sa_off, sb_off;  // output row / scale index offsets
 };
 
 // Tile raster.  group_m > 0: groups of group_m M-tiles sweep all N tiles (L2 reuse of both
@@ -111,8 +131,8 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nb = local / gsz;
 }
 
-template <bool MX, int CG, int ST, int KS, bool BF>
-__global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
+template <bool MX, int CG, int ST, int KS, bool BF, bool GRP>
+__global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
     fp8_gemm_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tB0,
                     const __grid_constant__ CUtensorMap tSA0, const __grid_constant__ CUtensorMap tSB0,
                     const __grid_constant__ CUtensorMap tA1, const __grid_constant__ CUtensorMap tB1,
@@ -120,7 +140,8 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
                     const __grid_constant__ GemmArgs args) {
   static_assert(KS == 1 || CG == 2, "multi-atom stages need the CTA-pair kernel");
   static_assert(!BF || (CG == 2 && KS == 2 && !MX), "BF16 operands: CTA-pair, 2-atom stages");
-  using L = Layout<MX, CG, ST, KS, BF>;
+  static_assert(!GRP || (!MX && !BF), "grouped problems: plain FP8 kinds");
+  using L = Layout<MX, CG, ST, KS, BF, GRP>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -139,11 +160,88 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
   const int cta_slot = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // pair / CTA index
   const int cta_stride = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
-  // problem of a global tile index, its local tile coordinates and its tensor maps
-  auto locate = [&](int tile, int& pi, int& mb, int& nb) {
-    pi = tile >= args.t1 ? 1 : 0;
-    const Prob& P = pi ? args.p1 : args.p0;
-    tile_coords(pi ? tile - args.t1 : tile, P.tiles_m, P.tiles_n, args.group_m, mb, nb);
+  // grouped problems: smem copies of the offsets and the prefix sums of M tiles per group
+  int* goffs = reinterpret_cast<int*>(gbase + L::off_grp);   // [2][GMAX + 1]
+  int* gpre = goffs + 2 * (GMAX + 1);                         // [2][GMAX + 1]
+  if (GRP && warp == 3 && lane < 2) {
+    const Prob& P = lane ? args.p1 : args.p0;
+    int* o = goffs + lane * (GMAX + 1);
+    int* pre = gpre + lane * (GMAX + 1);
+    if (P.grouped) {
+      // group offsets must start at 0, never decrease, be multiples of 128 and end at the
+      // grouped extent (rows for grouped 1, the contraction length for grouped 2)
+      const int extent = P.grouped == 1 ? P.M : P.K;
+      int prev = 0, acc = 0;
+      bool ok = __ldg(P.offs) == 0;
+      pre[0] = 0;
+      for (int g = 0; g <= P.G; ++g) {
+        const int v = __ldg(P.offs + g);
+        ok = ok && v >= prev && (v & 127) == 0 && v <= extent;
+        o[g] = v;
+        if (g > 0) {
+          acc += (v - prev + BM * CG - 1) / (BM * CG);
+          pre[g] = acc;
+        }
+        prev = v;
+      }
+      if (!ok || prev != extent) {
+        if (blockIdx.x == 0) printf("fp8_gemm: bad group offsets (need 0 = offs[0] <= ... <= offs[G] = %d, multiples of 128)\n", extent);
+        asm volatile("trap;");
+      }
+    }
+  }
+  // problem of a global tile index, its coordinates and offsets
+  auto count = [&](const Prob& P, int pi) -> int {
+    if (!GRP || P.grouped == 0) return P.tiles_m * P.tiles_n;
+    if (P.grouped == 1) return gpre[pi * (GMAX + 1) + P.G] * P.tiles_n;
+    return P.G * P.tiles_m * P.tiles_n;
+  };
+  int t1 = args.t1, num_tiles = args.num_tiles;   // (grouped: known after the setup barrier)
+  auto locate = [&](int tile) -> TileInfo {
+    TileInfo ti{};
+    ti.pi = tile >= t1 ? 1 : 0;
+    const Prob& P = ti.pi ? args.p1 : args.p0;
+    const int local = ti.pi ? tile - t1 : tile;
+    ti.m_valid = P.M;
+    ti.num_kb = P.num_kb;
+    ti.katoms = 1 << 30;
+    if (!GRP || P.grouped == 0) {
+      tile_coords(local, P.tiles_m, P.tiles_n, args.group_m, ti.mb, ti.nb);
+      return ti;
+    }
+    const int* o = goffs + ti.pi * (GMAX + 1);
+    int g;
+    if (P.grouped == 1) {
+      const int* pre = gpre + ti.pi * (GMAX + 1);
+      int mi;
+      tile_coords(local, pre[P.G], P.tiles_n, args.group_m, mi, ti.nb);
+      int lo = 0, hi = P.G;   // pre[lo] <= mi < pre[hi]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (pre[mid] <= mi) lo = mid; else hi = mid;
+      }
+      g = lo;
+      ti.mb = mi - pre[g];
+      ti.katoms = (P.K + BK - 1) / BK;   // MN-major B: expert g's contraction rows end at (g+1)*K
+      ti.m_valid = o[g + 1] - o[g];
+      ti.a_row0 = o[g];
+      ti.d_row0 = o[g];
+      ti.sa_off = o[g];
+      if (P.b_mn) ti.b_k0 = g * P.K; else ti.b_row0 = g * P.N;
+      ti.sb_off = (int64_t)g * P.N;
+    } else {
+      const int per = P.tiles_m * P.tiles_n;
+      g = local / per;
+      tile_coords(local - g * per, P.tiles_m, P.tiles_n, args.group_m, ti.mb, ti.nb);
+      ti.a_k0 = o[g];
+      ti.b_k0 = o[g];
+      ti.katoms = (o[g + 1] - o[g]) / BK;
+      ti.num_kb = (ti.katoms + KS - 1) / KS;
+      ti.d_row0 = (int64_t)g * P.M;
+      ti.sa_off = (int64_t)g * P.M;
+      ti.sb_off = (int64_t)g * P.N;
+    }
+    return ti;
   };
 
   if (threadIdx.x == 0) {
@@ -185,14 +283,18 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
   __syncthreads();               // (also the CTA-level barrier racecheck models for the smem slot)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (GRP) {
+    t1 = count(args.p0, 0);
+    num_tiles = t1 + (args.num_tiles > args.t1 ? count(args.p1, 1) : 0);
+  }
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
-      int pi, mb, nb;
-      locate(tile, pi, mb, nb);
+    for (int tile = cta_slot; tile < num_tiles; tile += cta_stride) {
+      const TileInfo ti = locate(tile);
+      const int pi = ti.pi, mb = ti.mb, nb = ti.nb;
       const Prob& P = pi ? args.p1 : args.p0;
       const CUtensorMap* tmA = pi ? &tA1 : &tA0;
       const CUtensorMap* tmB = pi ? &tB1 : &tB0;
@@ -204,7 +306,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
       // debug bit 2: skip the MX scale-factor loads (timing experiments only; results invalid)
       const uint32_t tx = L::tx_bytes - ((MX && (args.debug & 4)) ? CG * (L::SFA_STAGE + L::SFB_STAGE) : 0);
       const int KT = P.sf_tiles_k;
-      const int num_kb = P.num_kb;
+      const int num_kb = ti.num_kb;
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(empty_bar + 8 * stage, phase ^ 1);
         if (lane == 0) {
@@ -229,8 +331,15 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
             const int am = BF ? m0 + 64 * j : m0, bn = BF ? n0 + 64 * j : n0;
             const uint32_t da = sa_dst + j * 16384, db = sb_dst + j * 16384;
             if (CG == 2) {
-              tma_load_2d_2sm(da, tmA, a_mn ? am : k0, a_mn ? kmn : m0, fb);
-              tma_load_2d_2sm(db, tmB, b_mn ? bn : k0, b_mn ? kmn : n0, fb);
+              if (GRP) {   // grouped problems: per-group row / K offsets into the shared maps
+                tma_load_2d_2sm(da, tmA, a_mn ? am + ti.a_row0 : k0 + ti.a_k0,
+                                a_mn ? kmn + ti.a_k0 : m0 + ti.a_row0, fb);
+                tma_load_2d_2sm(db, tmB, b_mn ? bn + ti.b_row0 : k0 + ti.b_k0,
+                                b_mn ? kmn + ti.b_k0 : n0 + ti.b_row0, fb);
+              } else {
+                tma_load_2d_2sm(da, tmA, a_mn ? am : k0, a_mn ? kmn : m0, fb);
+                tma_load_2d_2sm(db, tmB, b_mn ? bn : k0, b_mn ? kmn : n0, fb);
+              }
             } else {
               tma_load_2d(da, tmA, a_mn ? m0 : k0, a_mn ? k0 : m0, fb, 0);
               if (b_mn) {
@@ -268,9 +377,10 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
-      const Prob& P = tile >= args.t1 ? args.p1 : args.p0;
-      const int a_mn = P.a_mn, b_mn = P.b_mn, num_kb = P.num_kb;
+    for (int tile = cta_slot; tile < num_tiles; tile += cta_stride) {
+      const TileInfo ti = locate(tile);
+      const Prob& P = ti.pi ? args.p1 : args.p0;
+      const int a_mn = P.a_mn, b_mn = P.b_mn, num_kb = ti.num_kb;
       const uint32_t idesc = P.idesc;
       mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
       tc_fence_after();
@@ -310,6 +420,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
           };
 #pragma unroll
           for (int k = 0; k < KS * BK / 32; ++k) {
+            if (GRP && kb * KS + (k >> 2) >= ti.katoms) break;   // K-grouped: the group's last atom ends here
             const uint64_t ad = adesc + koff(a_mn, k), bd = bdesc + koff(b_mn, k);
             const uint32_t acc_flag = (kb | k) != 0;
             if (MX) {
@@ -338,6 +449,13 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (GRP && num_kb == 0) {   // empty K group: no MMAs; publish the (unused) accumulator at once
+        if (lane == 0) {
+          if (CG == 2) mma_commit_cg2_mc(tfull_bar + 8 * acc, 0x3);
+          else mma_commit(tfull_bar + 8 * acc);
+        }
+        __syncwarp();
+      }
       if (++acc == L::ACC) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4) {
@@ -354,24 +472,29 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(tempty_bar, 0) : tempty_bar;
     uint8_t* epi = gbase + L::off_epi + (warp - 4) * 2048;   // this warp's bf16 staging slot
-    for (int tile = cta_slot; tile < args.num_tiles; tile += cta_stride) {
-      int pi, mb, nb;
-      locate(tile, pi, mb, nb);
-      const Prob& P = pi ? args.p1 : args.p0;
+    for (int tile = cta_slot; tile < num_tiles; tile += cta_stride) {
+      const TileInfo ti = locate(tile);
+      const int mb = ti.mb, nb = ti.nb;
+      const Prob& P = ti.pi ? args.p1 : args.p0;
       const int N = P.N, row_scales = P.row_scales, out_f32 = P.out_f32;
-      const float* sb = P.sb;
-      const int row = mb * BM * CG + (int)crank * BM + q * 32 + (int)lane;
-      const bool rvalid = row < P.M;
+      const float* sb = P.sb + ti.sb_off;
+      const int row = mb * BM * CG + (int)crank * BM + q * 32 + (int)lane;   // row within the problem / group
+      const bool rvalid = row < ti.m_valid;
+      const bool kzero = GRP && ti.katoms == 0;   // empty K group: D = 0
       float rs = 1.f;
       if (!row_scales && P.sa) rs = __frcp_rn(P.sa[0]) * __frcp_rn(P.sb[0]);
-      if (row_scales && rvalid) rs = __frcp_rn(P.sa[row]);
+      if (row_scales && rvalid) rs = __frcp_rn(P.sa[ti.sa_off + row]);
+      uint8_t* Dbase = static_cast<uint8_t*>(P.D) + ti.d_row0 * P.ldd * (out_f32 ? 4 : 2);
       uint32_t dmax = 0;   // |D| max over this thread's stored values (fp32 bit patterns)
 
       // scale + convert + store 32 columns [col0, col0 + 32) of this thread's row
       auto process = [&](const uint32_t (&r)[32], int col0) {
         if (col0 >= N || (args.debug & 1)) return;   // warp-uniform
         float v[32];
-        if (row_scales) {
+        if (kzero) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        } else if (row_scales) {
           // lane j computes 1/sb for column col0 + j once; the warp shares them by shuffles
           const float rcol = __frcp_rn(sb[min(col0 + (int)lane, N - 1)]);
 #pragma unroll
@@ -384,7 +507,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
         const int nvalid = min(32, N - col0);  // 16 or 32 (N % 16 == 0)
         if (out_f32) {
           if (!rvalid) return;
-          float* dst = reinterpret_cast<float*>(P.D) + (int64_t)row * P.ldd + col0;
+          float* dst = reinterpret_cast<float*>(Dbase) + (int64_t)row * P.ldd + col0;
           if (P.out_amax) {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
@@ -422,8 +545,8 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF>::THREADS, 1)
           const int rr = 8 * i + ((int)lane >> 2), j = lane & 3;
           const uint4 val = *reinterpret_cast<const uint4*>(epi + rr * 64 + ((j ^ ((rr >> 1) & 3)) * 16));
           const int grow = row - (int)lane + rr;
-          if (grow < P.M && 8 * j < nvalid)
-            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.D) + (int64_t)grow * P.ldd + col0 + 8 * j) =
+          if (grow < ti.m_valid && 8 * j < nvalid)
+            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(Dbase) + (int64_t)grow * P.ldd + col0 + 8 * j) =
                 val;
         }
         __syncwarp();
@@ -542,8 +665,11 @@ static bool make_sf_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K
 
 template <bool MX, int CG, int ST, int KS, bool BF>
 static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
+  // grouped 1: B holds G experts (K-major: G*N rows; MN-major: G*K contraction rows)
+  const int64_t bN = p.grouped == 1 && !p.b_mn ? p.G * p.N : p.N;
+  const int64_t bK = p.grouped == 1 && p.b_mn ? p.G * p.K : p.K;
   if (!make_operand_map(&maps[0], p.A, p.a_mn, p.M, p.K, p.lda, BM, BF) ||
-      !make_operand_map(&maps[1], p.B, p.b_mn, p.N, p.K, p.ldb, BN / CG, BF))
+      !make_operand_map(&maps[1], p.B, p.b_mn, bN, bK, p.ldb, BN / CG, BF))
     return false;
   if (MX) {
     if (!make_sf_map(&maps[2], p.sa, p.M, p.K, KS) || !make_sf_map(&maps[3], p.sb, p.N, p.K, KS)) return false;
@@ -571,17 +697,20 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   }
   P.D = p.D; P.ldd = p.ldd; P.out_f32 = p.out_f32;
   P.out_amax = p.out_amax;
+  P.grouped = p.grouped;
+  P.G = p.G;
+  P.offs = p.offs;
   return true;
 }
 
-template <bool MX, int CG, int ST, int KS, bool BF = false>
+template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false>
 static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
-  using L = Layout<MX, CG, ST, KS, BF>;
+  using L = Layout<MX, CG, ST, KS, BF, GRP>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err =
-        cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG, ST, KS, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
+    attr_err = cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
   });
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m0[4], m1[4];
@@ -605,11 +734,12 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     a.group_m = r ? atoi(r) : GROUP_M;
   }
   const int slots = num_sms() / CG;
-  const int grid = CG * (a.num_tiles < slots ? a.num_tiles : slots);
+  // grouped: the tile count depends on the device-side offsets -> a full persistent grid
+  const int grid = GRP ? CG * slots : CG * (a.num_tiles < slots ? a.num_tiles : slots);
   LaunchScope ls(MX ? K_GEMM_MX : (BF ? K_GEMM_BF16 : K_GEMM), st);
   if (CG == 1) {
-    fp8_gemm_kernel<MX, CG, ST, KS, BF><<<grid, L::THREADS, L::bytes, st>>>(m0[0], m0[1], m0[2], m0[3], m1[0], m1[1], m1[2],
-                                                                 m1[3], a);
+    fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP><<<grid, L::THREADS, L::bytes, st>>>(m0[0], m0[1], m0[2], m0[3], m1[0], m1[1],
+                                                                      m1[2], m1[3], a);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -623,8 +753,8 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS, BF>, m0[0], m0[1], m0[2], m0[3], m1[0], m1[1],
-                                       m1[2], m1[3], a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP>, m0[0], m0[1], m0[2], m0[3], m1[0],
+                                       m1[1], m1[2], m1[3], a);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
@@ -633,6 +763,15 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
 // One or two problems of the same kind (scale mode) on one persistent launch.
 cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st) {
   if (n < 1 || n > 2) return cudaErrorInvalidValue;
+  bool grp = false;
+  for (int i = 0; i < n; ++i) {
+    if (ps[i].grouped) {
+      if (ps[i].scale_mode == 2 || ps[i].bf16_in || !ps[i].offs || ps[i].G < 1 || ps[i].G > GMAX)
+        return cudaErrorInvalidValue;
+      grp = true;
+    }
+  }
+  if (grp) return launch_t<false, 2, 3, 2, false, true>(ps, n, st);
   if (n == 2 && ((ps[0].scale_mode == 2) != (ps[1].scale_mode == 2))) return cudaErrorInvalidValue;
   if (ps[0].bf16_in) {
     for (int i = 1; i < n; ++i)

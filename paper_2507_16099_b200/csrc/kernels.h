@@ -22,14 +22,22 @@ struct LaunchScope {
   ~LaunchScope();
 };
 
+// Row segments for the grouped (MoE) recipe: column amaxes / column scales are kept per segment,
+// out index = segment(row) * C + col.  offs (device, G+1 non-decreasing row offsets, multiples of
+// 128) or a fixed seg_rows (multiple of 128); neither = one segment (the plain column scales).
+struct Seg {
+  const int* offs = nullptr;
+  int G = 0;
+  int seg_rows = 0;
+};
 // amax_tile: mode bit0 tensor -> at[1], bit1 rows -> ar[R], bit2 cols -> ac[C] (u32 |x| bits, pre-zeroed)
 cudaError_t launch_amax(const void* x, bool bf16, int64_t R, int64_t C, int64_t ld, int mode, uint32_t* at,
-                        uint32_t* ar, uint32_t* ac, cudaStream_t st);
+                        uint32_t* ar, uint32_t* ac, cudaStream_t st, const Seg& seg = Seg{});
 // cast_tile: scale modes 0 none / 1 tensor / 2 row / 3 col for q (row-major) and qt (transposed);
 // tm = 5: column-scaled second copy written row-major (MN-major operand of the rowwise backward)
 cudaError_t launch_cast(const void* x, bool bf16, int fmt, int64_t R, int64_t C, int64_t ld, int qm, int tm,
                         const float* aq, const float* at, uint8_t* q, uint8_t* qt, float* sq, float* st,
-                        cudaStream_t s);
+                        cudaStream_t s, const Seg& seg = Seg{});
 // Tensorwise amax of n <= AMAX_MULTI_MAX tensors in one launch; out[t] (u32 bit patterns of
 // non-negative floats) must be zeroed by the caller.  chunk_start[t] = first warp chunk of
 // tensor t (chunks of 256 16-byte vectors within one row), chunk_start[n] = total.
@@ -91,7 +99,13 @@ struct GemmProblem {
   void* D; int out_f32; int64_t ldd;
   int bf16_in = 0;     // 1: A and B are BF16 (kind::f16, no scales; rowwise_gw_hp dW)
   uint32_t* out_amax = nullptr;  // optional epilogue amax of |D| (pre-zeroed u32 accumulator)
+  // MoE grouped problem (see Prob in gemm_kernels.cu): 1 = M-grouped (fwd, dX), 2 = K-grouped (dW);
+  // offs = device int[G+1] group offsets (multiples of 128), G <= GEMM_MAX_GROUPS.
+  int grouped = 0;
+  int G = 0;
+  const int* offs = nullptr;
 };
+constexpr int GEMM_MAX_GROUPS = 256;
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st);
 // Two problems of the same kind on one persistent launch (tiles of ps[0] then ps[1]).
 cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st);

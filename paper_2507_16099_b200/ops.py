@@ -195,5 +195,46 @@ class LinearPlan:
         return dx, dw
 
 
+class GroupedPlan:
+    """MoE scaled grouped GEMM (fp8_grouped_linear_fwd / _bwd): E experts with
+    weights stacked [E*N, K], tokens [T, K] sorted by expert, device int32 offsets [E+1]."""
+
+    def __init__(self, T, E, N, K, recipe="rowwise", fmt_fwd="e4m3", fmt_grad="e5m2", out_dtype=torch.bfloat16,
+                 device="cuda"):
+        self.T, self.E, self.N, self.K = T, E, N, K
+        self.out_dtype = out_dtype
+        self.cfg = L.LinearCfg(RECIPES[recipe], FORMATS[fmt_fwd], FORMATS[fmt_grad], L.MX_FLOOR,
+                               L.DT_F32 if out_dtype == torch.float32 else L.DT_BF16)
+        self.saved_bytes = L.lib.fp8_grouped_saved_bytes(ctypes.byref(self.cfg), T, E, N, K)
+        self.ws_bytes = L.lib.fp8_grouped_workspace_bytes(ctypes.byref(self.cfg), T, E, N, K)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
+
+    def new_saved(self, device="cuda"):
+        return torch.empty(self.saved_bytes, dtype=torch.uint8, device=device)
+
+    def forward(self, x, w, offs, saved, y=None, stream=None):
+        if y is None:
+            y = torch.empty((self.T, self.N), dtype=self.out_dtype, device=x.device)
+        if offs.dtype != torch.int32 or not offs.is_cuda:
+            raise TypeError("offs must be a CUDA int32 tensor [E+1]")
+        L.check(L.lib.fp8_grouped_linear_fwd(ctypes.byref(self.cfg), hp(x), hp(w), self.E, _ptr(offs), _ptr(y),
+                                             _ptr(saved), _ptr(self.ws), self.ws_bytes, _stream(stream)),
+                "fp8_grouped_linear_fwd")
+        return y
+
+    def backward(self, dy, offs, saved, dx=None, dw=None, want_dx=True, want_dw=True, stream=None):
+        dev = dy.device
+        if want_dx and dx is None:
+            dx = torch.empty((self.T, self.K), dtype=self.out_dtype, device=dev)
+        if want_dw and dw is None:
+            dw = torch.empty((self.E * self.N, self.K), dtype=self.out_dtype, device=dev)
+        xh = L.HP(None, L.DT_BF16, self.T, self.K, self.K)
+        L.check(L.lib.fp8_grouped_linear_bwd(ctypes.byref(self.cfg), hp(dy), xh, self.E, _ptr(offs),
+                                             _ptr(saved), _ptr(dx) if want_dx else None,
+                                             _ptr(dw) if want_dw else None, _ptr(self.ws), self.ws_bytes,
+                                             _stream(stream)), "fp8_grouped_linear_bwd")
+        return dx, dw
+
+
 def launch_count():
     return int(L.lib.fp8_launch_count())

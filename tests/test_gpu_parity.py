@@ -719,3 +719,87 @@ def test_p2p_window_ipc_single_rank():
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- MoE grouped GEMM
+
+def _offs_dev(sizes):
+    return torch.tensor(np.concatenate([[0], np.cumsum(sizes)]), dtype=torch.int32, device="cuda")
+
+
+@pytest.mark.parametrize("recipe", ["tensorwise", "rowwise"])
+@pytest.mark.parametrize("sizes", [[128, 0, 512, 384], [1024], [0, 256, 128, 128, 0, 512]])
+def test_grouped_linear_tolerance(recipe, sizes):
+    """fp8_grouped_linear_fwd/bwd vs the grouped oracle: per expert Y, dX, dW within the north-star
+    tolerance; experts of 128 rows (half a CTA-pair tile), empty experts, tiles straddling experts."""
+    from oracle import grouped as ogrp
+    E, N, K = len(sizes), 256, 384
+    T = int(sum(sizes))
+    x = synth.tensor_c3("x", (T, K), seed=1)
+    w = synth.tensor_c3("w", (E * N, K), seed=2)
+    dy = synth.tensor_c3("dy", (T, N), seed=3)
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    y, yb = ogrp.forward(x, w, offs, recipe)
+    dx, dxb, dw, dwb = ogrp.backward(x, w, dy, offs, recipe)
+    plan = ops.GroupedPlan(T, E, N, K, recipe=recipe, out_dtype=torch.float32)
+    saved = plan.new_saved()
+    od = _offs_dev(sizes)
+    Y = plan.forward(_dev(x, torch.bfloat16), _dev(w, torch.bfloat16), od, saved)
+    DX, DW = plan.backward(_dev(dy, torch.bfloat16), od, saved)
+    torch.cuda.synchronize()
+    for name, got, ref, bd in (("y", Y, y, yb), ("dx", DX, dx, dxb), ("dw", DW, dw, dwb)):
+        g = _np(got).astype(np.float64)
+        err = np.abs(g - ref)
+        assert np.all(err <= 1e-2 * bd + 1e-30), f"{recipe} {name}: max err/bound {np.max(err / (bd + 1e-30)):.3e}"
+    # empty experts: exactly zero dW rows
+    for g_, n_ in enumerate(sizes):
+        if n_ == 0:
+            assert not torch.any(DW[g_ * N:(g_ + 1) * N])
+
+
+@pytest.mark.parametrize("recipe", ["tensorwise", "rowwise"])
+def test_grouped_linear_exact_on_lossless_grid(recipe):
+    """Lossless integer-like grid (every scaling unit holds an entry of magnitude fmax, so all
+    scales are 1 and every cast is exact; fp32 sums exact): bit-exact vs the oracle."""
+    from oracle import grouped as ogrp
+    import importlib.util, os
+    spec = importlib.util.spec_from_file_location("tog", os.path.join(os.path.dirname(__file__), "test_oracle_grouped.py"))
+    tog = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(tog)
+    rng = np.random.default_rng(5)
+    sizes = [256, 128, 0, 384]
+    E, N, K = len(sizes), 128, 256
+    T = sum(sizes)
+    x = tog._lossless(sizes, K, E4M3, rng)
+    w = np.concatenate([tog._lossless([N], K, E4M3, rng) for _ in range(E)])
+    dy = tog._lossless(sizes, N, E4M3, rng)
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    y, _ = ogrp.forward(x, w, offs, recipe)
+    dx, _, dw, _ = ogrp.backward(x, w, dy, offs, recipe, fmt_grad=E4M3)
+    plan = ops.GroupedPlan(T, E, N, K, recipe=recipe, fmt_grad="e4m3", out_dtype=torch.float32)
+    saved = plan.new_saved()
+    od = _offs_dev(sizes)
+    Y = plan.forward(_dev(x, torch.bfloat16), _dev(w, torch.bfloat16), od, saved)
+    DX, DW = plan.backward(_dev(dy, torch.bfloat16), od, saved)
+    torch.cuda.synchronize()
+    assert np.array_equal(_np(Y).astype(np.float64), y)
+    assert np.array_equal(_np(DX).astype(np.float64), dx)
+    assert np.array_equal(_np(DW).astype(np.float64), dw)
+
+
+def test_grouped_single_expert_equals_linear():
+    """E = 1 through the grouped kernels == the plain Float8Linear path (bit-identical, rowwise)."""
+    T, N, K = 512, 256, 384
+    x, w, dy = synth.linear_inputs("c3", T, N, K, seed=4)
+    X, W, G = _dev(x, torch.bfloat16), _dev(w, torch.bfloat16), _dev(dy, torch.bfloat16)
+    gp = ops.GroupedPlan(T, 1, N, K, recipe="rowwise", out_dtype=torch.float32)
+    gs = gp.new_saved()
+    od = _offs_dev([T])
+    y1 = gp.forward(X, W, od, gs).clone()
+    dx1, dw1 = gp.backward(G, od, gs)
+    lp = ops.LinearPlan(T, N, K, recipe="rowwise", out_dtype=torch.float32)
+    ls = lp.new_saved()
+    y2 = lp.forward(X, W, ls)
+    dx2, dw2 = lp.backward(G, ls)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2) and torch.equal(dx1, dx2) and torch.equal(dw1, dw2)
