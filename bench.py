@@ -47,6 +47,11 @@ CONFIGS = {
     "c5": dict(M=8192, N=53248, K=16384, recipe="tensorwise", cfg="c5",
                workload="c5: Llama-3.1-405B w1 linear fwd+bwd, M=8192 tokens per GPU, K=16384, N=53248, "
                         "tensorwise (BASELINE.json configs[4]; FSDP2 FP8 all-gather at N>1)"),
+    "moe": dict(T=32768, E=8, N=14336, K=4096, recipe="rowwise", cfg="c3", kind="moe",
+                workload="moe: Mixtral-8x7B-style expert w1 scaled grouped GEMM fwd+bwd (PAPER.md:739 "
+                         "scaled_grouped_mm), E=8 experts, K=4096, N=14336, 16384 tokens x top-2 = 32768 routed "
+                         "rows, seeded imbalanced routing (expert groups padded to 128 rows), rowwise e4m3/e5m2, "
+                         "bf16 in/out"),
 }
 # oracle sample for the reference arm (per step, so the whole --steps/--warmup run stays within a
 # few minutes) and for the cpu_baseline (one step of ~10-30 s of CPU work): same K and value
@@ -89,6 +94,20 @@ def oracle_step_fn(cfg, Ms=CPU_SAMPLE["M"]):
     """One oracle fwd+bwd on the bounded sample (CPU).  Returns (fn, flops, sample_desc)."""
     import synth
     from oracle import linear as olin
+    if cfg.get("kind") == "moe":
+        from oracle import grouped as ogrp
+        Ts, Es, Ns, K = max(Ms, 128), 2, CPU_SAMPLE["N"] // 2, cfg["K"]
+        f = synth.RECIPES[cfg["cfg"]]
+        x, w, dy = f("x", (Ts, K), 0, cfg["cfg"]), f("w", (Es * Ns, K), 0, cfg["cfg"]), f("dy", (Ts, Ns), 0, cfg["cfg"])
+        offs = [0, Ts // 2 // 64 * 64, Ts]
+
+        def mstep():
+            ogrp.forward(x, w, offs, cfg["recipe"])
+            ogrp.backward(x, w, dy, offs, cfg["recipe"])
+
+        desc = (f"oracle/grouped forward+backward ({cfg['recipe']}) on a T={Ts}, E={Es}, N={Ns}, K={K} sample of "
+                f"the moe workload (same K and value recipe); numpy fp64 GEMMs + fp32/numpy encodes")
+        return mstep, 6.0 * Ts * Ns * K, desc
     Ns, K = CPU_SAMPLE["N"], cfg["K"]
     f = synth.RECIPES[cfg["cfg"]]
     x, w, dy = f("x", (Ms, K), 0, cfg["cfg"]), f("w", (Ns, K), 0, cfg["cfg"]), f("dy", (Ms, Ns), 0, cfg["cfg"])
@@ -593,10 +612,182 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+def moe_offsets(T, E, seed=0):
+    """Seeded imbalanced routing: expert loads ~ exp(N(0, 0.5^2)) normalised, rounded to multiples of
+    128 rows with the total kept at T (MoE frameworks pad each expert's token group)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    p = np.exp(rng.normal(0.0, 0.5, E))
+    p /= p.sum()
+    units = T // 128
+    c = np.floor(p * units).astype(np.int64)
+    for i in np.argsort(-(p * units - c))[:units - int(c.sum())]:
+        c[i] += 1
+    return np.concatenate([[0], np.cumsum(c * 128)]).astype(np.int32)
+
+
+def run_moe(a):
+    """MoE scaled grouped GEMM fwd+bwd (fp8_grouped_linear_fwd/bwd) on one GPU (replicas at N>1:
+    the grouped GEMM has no exchange step of its own; expert parallelism's all-to-all is out of scope)."""
+    import ctypes
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2507_16099_b200 as fp8t  # noqa: F401  (loads libfp8train.so; raises if missing)
+    from paper_2507_16099_b200 import _lib as L, ops
+    cfg = CONFIGS[a.config]
+    T, E, N, K = cfg["T"], cfg["E"], cfg["N"], cfg["K"]
+    offs_h = moe_offsets(T, E)
+    offs = torch.from_numpy(offs_h).to(dev)
+    x, _, dy, _ = make_inputs(cfg, T, N, K, rank, 1, dev)
+    gw = torch.Generator(device=dev)
+    gw.manual_seed(77)   # E stacked expert weights, c3 value recipe: N(0, 0.02^2) x 2^U(-4,4) per row
+    w = (torch.randn((E * N, K), generator=gw, device=dev) * 0.02 *
+         torch.exp2((2 * torch.rand((E * N, 1), generator=gw, device=dev) - 1) * 4)).to(torch.bfloat16)
+    plan = ops.GroupedPlan(T, E, N, K, recipe=cfg["recipe"], out_dtype=torch.bfloat16, device=dev)
+    saved = plan.new_saved(dev)
+    y = torch.empty((T, N), dtype=torch.bfloat16, device=dev)
+    dx = torch.empty((T, K), dtype=torch.bfloat16, device=dev)
+    dw = torch.empty((E * N, K), dtype=torch.bfloat16, device=dev)
+
+    def step(xx=x, ww=w, gg=dy, yy=y, dxx=dx, dww=dw):
+        plan.forward(xx, ww, offs, saved, y=yy)
+        plan.backward(gg, offs, saved, dx=dxx, dw=dww)
+
+    for _ in range(max(a.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    L.lib.fp8_profile_collect(None, None, 0)
+    L.lib.fp8_profile_enable(1)
+    n0 = ops.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(a.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = ops.launch_count() - n0
+    L.lib.fp8_profile_enable(0)
+    cap = launches + 16
+    kinds, durs = (ctypes.c_int * cap)(), (ctypes.c_float * cap)()
+    nrec = L.lib.fp8_profile_collect(kinds, durs, cap)
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / a.steps
+    flops_step = 6.0 * T * N * K
+    value = flops_step * a.steps * world / (ms / 1e3) / 1e12
+    by = {}
+    for i in range(max(nrec, 0)):
+        by.setdefault(kinds[i], []).append(durs[i])
+    gemm_ms = by.get(4, [float("nan")])
+    gemm_tflops = flops_step / (sum(gemm_ms) / a.steps / 1e3) / 1e12
+    peaks = _peaks()
+    fp8_peak = 2.0 * peaks["bf16"]
+    cast_bytes = (T * K + E * N * K + T * N) * 6
+    cast_ms = sum(sum(by.get(k, [])) for k in (0, 1)) / a.steps
+    # end to end through the public API: pinned host inputs (X, W, dY, offsets) in, Y, dX, dW out, every step
+    e2e = None
+    if a.e2e_steps > 0:
+        hx, hw, hg = x.cpu().pin_memory(), w.cpu().pin_memory(), dy.cpu().pin_memory()
+        ho = torch.from_numpy(offs_h).pin_memory()
+        hy, hdx, hdw = (torch.empty_like(t_, device="cpu").pin_memory() for t_ in (y, dx, dw))
+        dxi, dwi, dgi, doi = torch.empty_like(x), torch.empty_like(w), torch.empty_like(dy), torch.empty_like(offs)
+
+        def e2e_step():
+            for d_, h_ in ((dxi, hx), (dwi, hw), (dgi, hg), (doi, ho)):
+                d_.copy_(h_, non_blocking=True)
+            plan.forward(dxi, dwi, doi, saved, y=y)
+            plan.backward(dgi, doi, saved, dx=dx, dw=dw)
+            for h_, d_ in ((hy, y), (hdx, dx), (hdw, dw)):
+                h_.copy_(d_, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        e2e = {"value": flops_step * a.e2e_steps * world / (ems / 1e3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": (x.numel() + w.numel() + dy.numel()) * 2 + offs.numel() * 4,
+               "d2h_bytes_per_step": (y.numel() + dx.numel() + dw.numel()) * 2, "ms_per_step": ems / a.e2e_steps,
+               "path": "pinned host -> device X, W, dY, offsets + fp8_grouped_linear_fwd/bwd (C-ABI) + device -> "
+                       "host Y, dX, dW, every step, on the compute stream"}
+    bf16 = None
+    if not a.no_bf16:
+        def bstep():
+            for g in range(E):
+                r0, r1 = int(offs_h[g]), int(offs_h[g + 1])
+                if r1 == r0:
+                    continue
+                wg = w[g * N:(g + 1) * N]
+                torch.matmul(x[r0:r1], wg.t(), out=y[r0:r1])
+                torch.matmul(dy[r0:r1], wg, out=dx[r0:r1])
+                torch.matmul(dy[r0:r1].t(), x[r0:r1], out=dw[g * N:(g + 1) * N])
+        for _ in range(3):
+            bstep()
+        torch.cuda.synchronize()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(a.steps):
+            bstep()
+        b1.record(stream)
+        torch.cuda.synchronize()
+        bms = b0.elapsed_time(b1) / a.steps
+        bf16 = {"ms_per_step": bms, "tflops": flops_step / (bms / 1e3) / 1e12, "speedup_fp8_vs_bf16": bms / ms_step,
+                "impl": "torch.matmul (cuBLAS) bf16, 3 GEMMs per expert"}
+    cpu = cpu_baseline(cfg) if (rank == 0 and world == 1 and not a.no_cpu_baseline) else None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
+            "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp8 (e4m3 x e5m2 codes, fp32 accumulate, bf16 out)",
+            "data": "synthetic (seeded, device-generated, config value recipe; seeded routing)",
+            "config": {"workload": cfg["workload"], "T": T, "E": E, "N": N, "K": K, "recipe": cfg["recipe"],
+                       "group_rows": [int(offs_h[i + 1] - offs_h[i]) for i in range(E)],
+                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                       "l2": "inputs larger than L2 (126 MB); no flush"},
+            "roofline": {"bound": "tensor", "kernel": "fp8_gemm_kernel (tcgen05 kind::f8f6f4, grouped)",
+                         "achieved": gemm_tflops, "peak": fp8_peak, "unit": "TFLOP/s", "frac": gemm_tflops / fp8_peak,
+                         "traffic": None,
+                         "peak_source": f"{peaks['src']}: bf16_tflops (burst) x 2 (dense FP8/BF16 ratio)",
+                         "algorithmic": "2*T*N*K flop per grouped GEMM (sum over experts of 2*M_g*N*K); fwd launch "
+                                        "1 grouped problem, bwd launch 2 (dX M-grouped, dW K-grouped)",
+                         "launches_per_step": len(gemm_ms) / a.steps, "share_of_step": sum(gemm_ms) / a.steps / ms_step},
+            "cast": {"gbps": cast_bytes / (cast_ms / 1e3) / 1e9 if cast_ms > 0 else None, "peak_gbps": peaks["hbm"],
+                     "frac": cast_bytes / (cast_ms / 1e3) / 1e9 / peaks["hbm"] if cast_ms > 0 else None,
+                     "ms_per_step": cast_ms, "algorithmic_bytes_per_step": cast_bytes},
+            "kernels_ms_per_step": {name: round(sum(by.get(k, [])) / a.steps, 4)
+                                    for k, name in ((0, "amax"), (1, "cast"), (4, "gemm_fp8_grouped"))},
+            "bf16": bf16, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif CONFIGS[a.config].get("kind") == "moe":
+        run_moe(a)
     else:
         run_ours(a)
 

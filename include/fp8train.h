@@ -377,8 +377,9 @@ typedef struct fp8_p2p_s* fp8_p2p_t;
  * per concurrently live gathered weight; bytes >= nranks * rows_local * cols. */
 fp8_status_t fp8_p2p_create(fp8_comm_t comm, size_t bytes, fp8_p2p_t* win);
 /* Test / single-GPU form: nranks windows on the current device, wins[r] acting as rank
- * r, all mapped to each other (plain device pointers).  The ranks' calls must then be
- * issued on different streams (each call waits for every rank's signals). */
+ * r, all mapped to each other (plain device pointers).  Drive it with
+ * fp8_fsdp_allgather_p2p_local (one stream); per-rank calls on separate streams would
+ * rely on those streams running concurrently, which CUDA does not guarantee. */
 fp8_status_t fp8_p2p_create_local(int nranks, size_t bytes, fp8_p2p_t* wins);
 /* Device pointer of this rank's gather buffer: the codes [nranks*rows_local, cols] u8
  * after fp8_fsdp_allgather_p2p (valid in stream order after the call). */
@@ -395,6 +396,14 @@ fp8_status_t fp8_p2p_destroy(fp8_p2p_t win);
 fp8_status_t fp8_fsdp_allgather_p2p(fp8_p2p_t win, fp8_hp_t w_shard, fp8_format_t fmt,
                                     const float* amax_in, float* scale_out, float* amax_out,
                                     void* stream);
+/* Single-process form for a fp8_p2p_create_local group: rank r's call with shard w[r] for every
+ * r, issued phase by phase on ONE stream (all signals, then all scale waits, then all casts,
+ * then all completion waits), so the ranks' spins never wait on work queued behind them.
+ * amax_in / amax_out may be NULL arrays (amax_out[r] is needed when amax_in is NULL). */
+fp8_status_t fp8_fsdp_allgather_p2p_local(fp8_p2p_t* wins, int nranks, const fp8_hp_t* w_shards,
+                                          fp8_format_t fmt, const float* const* amax_in,
+                                          float* const* scale_out, float* const* amax_out,
+                                          void* stream);
 
 /* ---------------------------------------------------------------------------
  * Helpers

@@ -94,6 +94,8 @@ SIGNATURES = {
     "fp8_p2p_destroy": (_c.c_int, [_c.c_void_p]),
     "fp8_fsdp_allgather_p2p": (_c.c_int, [_c.c_void_p, HP, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_void_p,
                                           _c.c_void_p]),
+    "fp8_fsdp_allgather_p2p_local": (_c.c_int, [_c.POINTER(_c.c_void_p), _c.c_int, _c.POINTER(HP), _c.c_int,
+                                                _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_void_p]),
     "fp8_mx_scales_unshard": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),
 }
 AMAX_MULTI_MAX = 48

@@ -231,6 +231,135 @@ __global__ void __launch_bounds__(256) amax_tile_kernel(const T* __restrict__ x,
   }
 }
 
+// ---------------------------------------------------------------------------
+// amax_tile, TMA-pipelined persistent variant (bf16; rows, cols multiples of 128).  Same outputs
+// as amax_tile_kernel.  CTA b owns the contiguous row-major tile range [b*per, (b+1)*per), so its
+// tiles run along one or two 128-row strips: per-row maxima stay in registers across the strip
+// and are flushed (half-warp reduce + one atomicMax per row) only when the strip changes, while
+// thread 0 streams 32 KB tiles into an ST-deep smem ring with cp.async.bulk.tensor.
+// ---------------------------------------------------------------------------
+template <int MODE, int ST>
+__global__ void __launch_bounds__(256) amax_tile_tma_kernel(const __grid_constant__ CUtensorMap tmap, int64_t R,
+                                                            int64_t C, uint32_t* amax_tensor, uint32_t* amax_row,
+                                                            uint32_t* amax_col, const Seg seg) {
+  constexpr int STAGE = 128 * 256;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint32_t(*colred)[128] = reinterpret_cast<uint32_t(*)[128]>(sm + ST * STAGE);
+  uint32_t* wred = reinterpret_cast<uint32_t*>(sm + ST * STAGE + 8 * 128 * 4);
+  const uint32_t bar0 = smem_u32(sm + ST * STAGE + 8 * 128 * 4 + 64), stage0 = smem_u32(sm);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int tiles_x = (int)(C >> 7);
+  const int num_tiles = tiles_x * (int)(R >> 7);
+  const int per = (num_tiles + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int first = (int)blockIdx.x * per;
+  const int last = min(first + per, num_tiles);
+  auto issue = [&](int k) {
+    const int id = first + k;
+    if (id < last) {
+      const uint32_t bar = bar0 + 8 * (k % ST);
+      mbar_arrive_expect_tx(bar, STAGE);
+      tma_load_2d(stage0 + (k % ST) * STAGE, &tmap, (id % tiles_x) * 128, (id / tiles_x) * 128, bar,
+                  l2_policy_evict_first());
+    }
+  };
+  if (t == 0) {
+    tma_prefetch_desc(&tmap);
+    for (int i = 0; i < ST; ++i) mbar_init(bar0 + 8 * i, 1);
+    fence_mbar_init();
+    for (int k = 0; k < ST; ++k) issue(k);
+  }
+  __syncthreads();
+  const int cc = (t & 15) * 8;
+  uint32_t tmax = 0;
+  uint32_t rm[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // this thread's partial row maxima of the current strip
+  int strip = first < last ? first / tiles_x : -1;
+  auto flush_rows = [&](int st_) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t m = rm[i];
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, 4));
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, 8));
+      if ((t & 15) == 0) atomicMax(amax_row + (int64_t)st_ * 128 + (t >> 4) + 16 * i, m);
+      rm[i] = 0;
+    }
+  };
+  for (int k = 0; first + k < last; ++k) {
+    const int id = first + k;
+    const int rt = id / tiles_x;
+    const int64_t r0 = (int64_t)rt * 128, c0 = (int64_t)(id - rt * tiles_x) * 128;
+    if ((MODE & 2) && rt != strip) {
+      flush_rows(strip);
+      strip = rt;
+    }
+    mbar_wait(bar0 + 8 * (k % ST), (uint32_t)(k / ST) & 1u);
+    uint4 raw[8];
+    const uint8_t* sp = sm + (k % ST) * STAGE + (t >> 4) * 256 + cc * 2;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) raw[i] = *reinterpret_cast<const uint4*>(sp + i * 16 * 256);
+    __syncthreads();   // (1) stage consumed
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(k + ST);
+    }
+    uint32_t cmw[4] = {0, 0, 0, 0};   // packed column maxima (bf16 |x| bit pairs)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t a0 = raw[i].x & 0x7FFF7FFFu, a1 = raw[i].y & 0x7FFF7FFFu;
+      const uint32_t a2 = raw[i].z & 0x7FFF7FFFu, a3 = raw[i].w & 0x7FFF7FFFu;
+      if (MODE & 4) {
+        cmw[0] = __vmaxu2(cmw[0], a0); cmw[1] = __vmaxu2(cmw[1], a1);
+        cmw[2] = __vmaxu2(cmw[2], a2); cmw[3] = __vmaxu2(cmw[3], a3);
+      }
+      if (MODE & 3) {
+        const uint32_t m2 = __vmaxu2(__vmaxu2(a0, a1), __vmaxu2(a2, a3));
+        const uint32_t m = max(m2 & 0xFFFFu, m2 >> 16) << 16;
+        if (MODE & 2) rm[i] = max(rm[i], m);
+        else tmax = max(tmax, m);
+      }
+    }
+    if (MODE & 4) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cmw[j] = __vmaxu2(cmw[j], __shfl_xor_sync(0xffffffffu, cmw[j], 16));
+      if (lane < 16) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          colred[warp][cc + 2 * j] = cmw[j] << 16;
+          colred[warp][cc + 2 * j + 1] = cmw[j] & 0xFFFF0000u;
+        }
+      }
+      __syncthreads();   // (2)
+      if (t < 128) {
+        uint32_t m = colred[0][t];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) m = max(m, colred[w][t]);
+        int64_t sstart;
+        const int g = seg_of(seg, r0, sstart);
+        atomicMax(amax_col + (int64_t)g * C + c0 + t, m);
+      }
+    }
+  }
+  if (MODE & 2) {
+    if (strip >= 0) flush_rows(strip);
+    if (MODE & 1) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) tmax = max(tmax, rm[i]);
+    }
+  }
+  if (MODE & 1) {
+    tmax = __reduce_max_sync(0xffffffffu, tmax);
+    if (lane == 0) wred[warp] = tmax;
+    __syncthreads();
+    if (t == 0) {
+      uint32_t m = wred[0];
+#pragma unroll
+      for (int i = 1; i < 8; ++i) m = max(m, wred[i]);
+      if (m) atomicMax(amax_tensor, m);
+    }
+  }
+}
+
 // Tensorwise amax of a contiguous tensor: persistent grid-stride stream of 16-byte vectors,
 // 8 independent loads in flight per thread, |x| max on raw bit patterns (bf16: two 16-bit
 // lanes per word via __vmaxu2), one atomicMax per CTA.
@@ -778,6 +907,32 @@ static int sm_count() {
 }
 static inline dim3 tile_grid(int64_t R, int64_t C) { return dim3((unsigned)((C + 127) / 128), (unsigned)((R + 127) / 128)); }
 
+// FP8T_AMAX_TILE=0 selects the register-only amax_tile_kernel (A/B comparisons).
+static bool amax_tile_use_tma() {
+  const char* e = getenv("FP8T_AMAX_TILE");
+  return !(e && e[0] == '0');
+}
+
+template <int MODE>
+static cudaError_t amax_tma_go(const CUtensorMap& m, int64_t R, int64_t C, int64_t tiles, uint32_t* at, uint32_t* ar,
+                               uint32_t* ac, cudaStream_t st, const Seg& seg) {
+  constexpr int ST = 3;
+  constexpr int smem = ST * 128 * 256 + 8 * 128 * 4 + 64 + ST * 8;
+  auto kern = amax_tile_tma_kernel<MODE, ST>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int64_t cap = (int64_t)sm_count() * 2;
+  const char* g = getenv("FP8T_CAST_GRID");   // tests: cap the persistent grid (many tiles per CTA)
+  if (g && atoi(g) > 0 && atoi(g) < cap) cap = atoi(g);
+  LaunchScope ls(K_AMAX, st);
+  kern<<<(unsigned)(tiles < cap ? tiles : cap), 256, smem, st>>>(m, R, C, at, ar, ac, seg);
+  return cudaGetLastError();
+}
+
 template <typename T>
 static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, int mode, uint32_t* at,
                                  uint32_t* ar, uint32_t* ac, cudaStream_t st, const Seg& seg) {
@@ -801,6 +956,24 @@ static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
     return cudaGetLastError();
   }
   const int64_t tiles = ((R + 127) / 128) * ((C + 127) / 128);
+  if (sizeof(T) == 2 && R % 128 == 0 && C % 128 == 0 && mode != 1 && amax_tile_use_tma()) {
+    auto enc = get_encode();
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)R};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {128, 128};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc && enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+      switch (mode) {
+        case 2: return amax_tma_go<2>(m, R, C, tiles, at, ar, ac, st, seg);
+        case 4: return amax_tma_go<4>(m, R, C, tiles, at, ar, ac, st, seg);
+        case 6: return amax_tma_go<6>(m, R, C, tiles, at, ar, ac, st, seg);
+        default: break;
+      }
+    }
+  }
   const int64_t cap = (int64_t)sm_count() * 8;   // persistent: up to 8 resident CTAs per SM
   dim3 g((unsigned)(tiles < cap ? tiles : cap));
   LaunchScope ls(K_AMAX, st);

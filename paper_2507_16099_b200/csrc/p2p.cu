@@ -83,6 +83,12 @@ __global__ void p2p_wait_done_kernel(P2PSig* mine, int P, uint32_t epoch) {
 }  // namespace fp8t
 using namespace fp8t;
 
+#define FP8T_P2P_TRY(expr)               \
+  do {                                   \
+    fp8_status_t s_ = (expr);            \
+    if (s_ != FP8_OK) return s_;         \
+  } while (0)
+
 struct fp8_p2p_s {
   int P, rank;
   size_t bytes;            // gather buffer bytes (the window's data part)
@@ -213,8 +219,12 @@ fp8_status_t fp8_p2p_destroy(fp8_p2p_t win) {
   return s;
 }
 
-fp8_status_t fp8_fsdp_allgather_p2p(fp8_p2p_t win, fp8_hp_t w, fp8_format_t fmt, const float* amax_in,
-                                    float* scale_out, float* amax_out, void* stream) {
+}  // extern "C"
+
+namespace {
+
+fp8_status_t p2p_check(fp8_p2p_t win, const fp8_hp_t& w, fp8_format_t fmt, const float* amax_in, float* scale_out,
+                       float* amax_out) {
   if (!win) return fail(FP8_EINVAL, "win: null");
   if (!w.ptr || !scale_out || (!amax_out && !amax_in)) return fail(FP8_EINVAL, "null pointer");
   if (fmt != FP8_E4M3 && fmt != FP8_E5M2) return fail(FP8_EINVAL, "bad fp8 format");
@@ -223,41 +233,74 @@ fp8_status_t fp8_fsdp_allgather_p2p(fp8_p2p_t win, fp8_hp_t w, fp8_format_t fmt,
     return fail(FP8_EALIGN, "shard rows/cols: multiples of 16");
   if (reinterpret_cast<uintptr_t>(w.ptr) & 15) return fail(FP8_EALIGN, "w_shard must be 16-byte aligned");
   if (w.ld < w.cols || (w.ld * (w.dtype == FP8_DT_F32 ? 4 : 2)) % 16) return fail(FP8_EALIGN, "bad ld");
-  const size_t chunk = (size_t)w.rows * (size_t)w.cols;
-  if (chunk * (size_t)win->P > win->bytes) return fail(FP8_EINVAL, "window too small for nranks * shard bytes");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool bf16 = w.dtype == FP8_DT_BF16;
+  if ((size_t)w.rows * (size_t)w.cols * (size_t)win->P > win->bytes)
+    return fail(FP8_EINVAL, "window too small for nranks * shard bytes");
+  return FP8_OK;
+}
+
+// The four phases of one rank's call (see the file header); phase 1 advances the epoch.
+fp8_status_t phase_signal(fp8_p2p_t win, const fp8_hp_t& w, const float* amax_in, float* amax_out, cudaStream_t st) {
   const uint32_t epoch = ++win->epoch;
   fp8_status_t s;
   const uint32_t* abits = reinterpret_cast<const uint32_t*>(amax_in);
   if (!amax_in) {
     uint32_t* acc = reinterpret_cast<uint32_t*>(amax_out);
     if ((s = cuda_check(cudaMemsetAsync(acc, 0, 4, st), "memset")) != FP8_OK) return s;
-    if ((s = cuda_check(launch_amax(w.ptr, bf16, w.rows, w.cols, w.ld, 1, acc, nullptr, nullptr, st), "amax")) !=
-        FP8_OK)
+    if ((s = cuda_check(launch_amax(w.ptr, w.dtype == FP8_DT_BF16, w.rows, w.cols, w.ld, 1, acc, nullptr, nullptr, st),
+                        "amax")) != FP8_OK)
       return s;
     abits = acc;
   }
-  {
-    LaunchScope ls(K_SYNC, st);
-    p2p_signal_amax_kernel<<<1, 64, 0, st>>>(win->peers, abits, epoch);
-  }
-  if ((s = cuda_check(cudaGetLastError(), "p2p_signal_amax")) != FP8_OK) return s;
-  {
-    LaunchScope ls(K_SYNC, st);
-    if (fmt == FP8_E4M3) p2p_wait_scale_kernel<0><<<1, 32, 0, st>>>(win->sig, win->P, epoch, scale_out, amax_out);
-    else p2p_wait_scale_kernel<1><<<1, 32, 0, st>>>(win->sig, win->P, epoch, scale_out, amax_out);
-  }
-  if ((s = cuda_check(cudaGetLastError(), "p2p_wait_scale")) != FP8_OK) return s;
-  if ((s = cuda_check(launch_cast_push(w.ptr, bf16, fmt, w.rows, w.cols, w.ld, scale_out, win->peers,
-                                       (int64_t)(chunk * (size_t)win->rank), win->sig, epoch, st),
-                      "cast_push")) != FP8_OK)
-    return s;
-  {
-    LaunchScope ls(K_SYNC, st);
-    p2p_wait_done_kernel<<<1, 64, 0, st>>>(win->sig, win->P, epoch);
-  }
+  LaunchScope ls(K_SYNC, st);
+  p2p_signal_amax_kernel<<<1, 64, 0, st>>>(win->peers, abits, epoch);
+  return cuda_check(cudaGetLastError(), "p2p_signal_amax");
+}
+fp8_status_t phase_wait_scale(fp8_p2p_t win, fp8_format_t fmt, float* scale_out, float* amax_out, cudaStream_t st) {
+  LaunchScope ls(K_SYNC, st);
+  if (fmt == FP8_E4M3) p2p_wait_scale_kernel<0><<<1, 32, 0, st>>>(win->sig, win->P, win->epoch, scale_out, amax_out);
+  else p2p_wait_scale_kernel<1><<<1, 32, 0, st>>>(win->sig, win->P, win->epoch, scale_out, amax_out);
+  return cuda_check(cudaGetLastError(), "p2p_wait_scale");
+}
+fp8_status_t phase_cast_push(fp8_p2p_t win, const fp8_hp_t& w, fp8_format_t fmt, const float* scale, cudaStream_t st) {
+  const size_t chunk = (size_t)w.rows * (size_t)w.cols;
+  return cuda_check(launch_cast_push(w.ptr, w.dtype == FP8_DT_BF16, fmt, w.rows, w.cols, w.ld, scale, win->peers,
+                                     (int64_t)(chunk * (size_t)win->rank), win->sig, win->epoch, st),
+                    "cast_push");
+}
+fp8_status_t phase_wait_done(fp8_p2p_t win, cudaStream_t st) {
+  LaunchScope ls(K_SYNC, st);
+  p2p_wait_done_kernel<<<1, 64, 0, st>>>(win->sig, win->P, win->epoch);
   return cuda_check(cudaGetLastError(), "p2p_wait_done");
+}
+
+}  // namespace
+
+extern "C" {
+
+fp8_status_t fp8_fsdp_allgather_p2p(fp8_p2p_t win, fp8_hp_t w, fp8_format_t fmt, const float* amax_in,
+                                    float* scale_out, float* amax_out, void* stream) {
+  FP8T_P2P_TRY(p2p_check(win, w, fmt, amax_in, scale_out, amax_out));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  FP8T_P2P_TRY(phase_signal(win, w, amax_in, amax_out, st));
+  FP8T_P2P_TRY(phase_wait_scale(win, fmt, scale_out, amax_out, st));
+  FP8T_P2P_TRY(phase_cast_push(win, w, fmt, scale_out, st));
+  return phase_wait_done(win, st);
+}
+
+fp8_status_t fp8_fsdp_allgather_p2p_local(fp8_p2p_t* wins, int n, const fp8_hp_t* w, fp8_format_t fmt,
+                                          const float* const* amax_in, float* const* scale_out,
+                                          float* const* amax_out, void* stream) {
+  if (!wins || !w || !scale_out || n < 1) return fail(FP8_EINVAL, "null pointer / n < 1");
+  for (int r = 0; r < n; ++r) {
+    if (!wins[r] || wins[r]->P != n || wins[r]->rank != r) return fail(FP8_EINVAL, "wins must be one local group, in rank order");
+    FP8T_P2P_TRY(p2p_check(wins[r], w[r], fmt, amax_in ? amax_in[r] : nullptr, scale_out[r], amax_out ? amax_out[r] : nullptr));
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int r = 0; r < n; ++r) FP8T_P2P_TRY(phase_signal(wins[r], w[r], amax_in ? amax_in[r] : nullptr, amax_out ? amax_out[r] : nullptr, st));
+  for (int r = 0; r < n; ++r) FP8T_P2P_TRY(phase_wait_scale(wins[r], fmt, scale_out[r], amax_out ? amax_out[r] : nullptr, st));
+  for (int r = 0; r < n; ++r) FP8T_P2P_TRY(phase_cast_push(wins[r], w[r], fmt, scale_out[r], st));
+  for (int r = 0; r < n; ++r) FP8T_P2P_TRY(phase_wait_done(wins[r], st));
+  return FP8_OK;
 }
 
 }  // extern "C"

@@ -144,6 +144,24 @@ class P2PWindow:
             out.append(w)
         return out
 
+    @staticmethod
+    def allgather_local(wins, shards, fmt="e4m3", amax_in=None, stream=None):
+        """fp8_fsdp_allgather_p2p_local: every simulated rank's gather of a local_group, phase by phase on
+        one stream.  Returns [(codes view, scale, amax)] per rank."""
+        n = len(wins)
+        dev = shards[0].device
+        scales = [torch.empty(1, dtype=torch.float32, device=dev) for _ in range(n)]
+        amaxes = [torch.empty(1, dtype=torch.float32, device=dev) for _ in range(n)]
+        vp = ctypes.c_void_p * n
+        hs = (L.HP * n)(*[hp(s_) for s_ in shards])
+        ain = vp(*[a.data_ptr() for a in amax_in]) if amax_in is not None else None
+        L.check(L.lib.fp8_fsdp_allgather_p2p_local(
+            (ctypes.c_void_p * n)(*[w._h.value for w in wins]), n, hs, FORMATS[fmt], ain,
+            vp(*[s_.data_ptr() for s_ in scales]), vp(*[a.data_ptr() for a in amaxes]), _stream(stream)),
+            "fp8_fsdp_allgather_p2p_local")
+        rows, cols = shards[0].shape
+        return [(w.buffer(n * rows, cols, dev), scales[r], amaxes[r]) for r, w in enumerate(wins)]
+
     def buffer(self, rows, cols, device="cuda"):
         """uint8 [rows, cols] torch view of this rank's gather buffer (library-owned memory)."""
         if rows * cols > self.nbytes:

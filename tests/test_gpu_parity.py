@@ -629,14 +629,10 @@ def test_mx_fsdp_allgather_single_rank():
 # ----------------------------------------------------------------------------- fused P2P FP8 gather
 
 def _p2p_run(wins, shards, amax_in=None):
-    """Issue every simulated rank's fp8_fsdp_allgather_p2p on its own stream (each call waits for
-    the other ranks' signals), then wait for all of them."""
-    torch.cuda.synchronize()
-    streams = [torch.cuda.Stream() for _ in wins]
-    outs = []
-    for r, (w, sh) in enumerate(zip(wins, shards)):
-        with torch.cuda.stream(streams[r]):
-            outs.append(w.allgather_fp8(sh, "e4m3", amax_in=None if amax_in is None else amax_in[r]))
+    """Every simulated rank's fp8_fsdp_allgather_p2p, phase by phase on one stream
+    (fp8_fsdp_allgather_p2p_local), then wait."""
+    from paper_2507_16099_b200.fsdp import P2PWindow
+    outs = P2PWindow.allgather_local(wins, shards, "e4m3", amax_in=amax_in)
     torch.cuda.synchronize()
     return outs
 
@@ -803,3 +799,22 @@ def test_grouped_single_expert_equals_linear():
     dx2, dw2 = lp.backward(G, ls)
     torch.cuda.synchronize()
     assert torch.equal(y1, y2) and torch.equal(dx1, dx2) and torch.equal(dw1, dw2)
+
+
+@pytest.mark.parametrize("grid", ["0", "1", "5"])
+@pytest.mark.parametrize("impl", ["1", "0"])
+def test_amax_tile_strips(grid, impl, monkeypatch):
+    """Row / column / dual amax on 128-multiple shapes (the TMA strip kernel, FP8T_AMAX_TILE=1, and the
+    register kernel), with capped persistent grids so CTAs cross row strips: bit-exact vs the oracle."""
+    if grid != "0":
+        monkeypatch.setenv("FP8T_CAST_GRID", grid)
+    monkeypatch.setenv("FP8T_AMAX_TILE", impl)
+    x = synth.tensor_c3("x", (384, 1280), seed=9)
+    X = _dev(x, torch.bfloat16)
+    assert np.array_equal(_bits(_np(ops.amax(X, "row"))), _bits(fp8.amax(x, 1)))
+    assert np.array_equal(_bits(_np(ops.amax(X, "col"))), _bits(fp8.amax(x, 0)))
+    out = ops.cast(X, "e4m3", "row_col", want_q=True, want_qt=True)
+    q, s, _ = fp8.cast_rowwise(x, E4M3)
+    qc, sc, _ = fp8.cast_colwise(x, E4M3)
+    assert np.array_equal(_np(out["q"]), q) and np.array_equal(_bits(_np(out["scale"])), _bits(s))
+    assert np.array_equal(_np(out["q_t"]), qc.T) and np.array_equal(_bits(_np(out["scale_t"])), _bits(sc))
