@@ -47,6 +47,11 @@ CONFIGS = {
     "c5": dict(M=8192, N=53248, K=16384, recipe="tensorwise", cfg="c5",
                workload="c5: Llama-3.1-405B w1 linear fwd+bwd, M=8192 tokens per GPU, K=16384, N=53248, "
                         "tensorwise (BASELINE.json configs[4]; FSDP2 FP8 all-gather at N>1)"),
+    "c3": dict(M=16384, K=4096, N=14336, recipe="rowwise", cfg="c3", kind="layer",
+               linears=[("wq", 4096, 4096), ("wk", 1024, 4096), ("wv", 1024, 4096), ("wo", 4096, 4096),
+                        ("w1", 14336, 4096), ("w3", 14336, 4096), ("w2", 4096, 14336)],
+               workload="c3: one Llama-3-8B layer's seven linears (attention wq/wk/wv/wo + MLP w1/w3/w2) fwd+bwd, "
+                        "M=16384 tokens, rowwise scaling, bf16 in/out (BASELINE.json configs[2])"),
     "moe": dict(T=32768, E=8, N=14336, K=4096, recipe="rowwise", cfg="c3", kind="moe",
                 workload="moe: Mixtral-8x7B-style expert w1 scaled grouped GEMM fwd+bwd (PAPER.md:739 "
                          "scaled_grouped_mm), E=8 experts, K=4096, N=14336, 16384 tokens x top-2 = 32768 routed "
@@ -179,6 +184,17 @@ class ClockSampler:
             self.max = None
         self._stop = threading.Event()
 
+    def _violation(self):
+        """Cumulative power / thermal policy violation times (ns) -- they advance whenever the driver
+        held clocks down for that reason, even between two samples."""
+        out = {}
+        for key, pol in (("sw_power_cap", "NVML_PERF_POLICY_POWER"), ("sw_thermal_slowdown", "NVML_PERF_POLICY_THERMAL")):
+            try:
+                out[key] = self.nv.nvmlDeviceGetViolationStatus(self.h, getattr(self.nv, pol)).violationTime
+            except Exception:
+                pass
+        return out
+
     def _run(self):
         while not self._stop.is_set():
             try:
@@ -189,10 +205,11 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.01)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.ok:
+            self.v0 = self._violation()
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
@@ -201,12 +218,18 @@ class ClockSampler:
         if self.ok:
             self._stop.set()
             self.t.join()
+            v1 = self._violation()
+            self.violation_ns = {k: v1[k] - self.v0[k] for k in v1 if k in self.v0}
+            for k, dv in self.violation_ns.items():
+                if dv > 0:
+                    self.reasons.add(k)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": sorted(self.reasons), "samples": 0}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "violation_ns": getattr(self, "violation_ns", None)}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -626,6 +649,155 @@ def moe_offsets(T, E, seed=0):
     return np.concatenate([[0], np.cumsum(c * 128)]).astype(np.int32)
 
 
+def run_layer(a):
+    """All linears of one transformer layer (BASELINE.json configs[2]), each a Float8Linear fwd+bwd
+    through the C-ABI, back to back on one stream (replicas at N>1)."""
+    import ctypes
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2507_16099_b200 as fp8t  # noqa: F401  (loads libfp8train.so; raises if missing)
+    from paper_2507_16099_b200 import _lib as L, ops
+    cfg = CONFIGS[a.config]
+    M = cfg["M"]
+    units = []
+    for i, (name, N, K) in enumerate(cfg["linears"]):
+        x, _, dy, w = make_inputs(dict(cfg, N=N, K=K), M, N, K, 10 * i + rank, 1, dev)
+        plan = ops.LinearPlan(M, N, K, recipe=cfg["recipe"], out_dtype=torch.bfloat16, device=dev)
+        units.append(dict(name=name, N=N, K=K, x=x, w=w, dy=dy, plan=plan, saved=plan.new_saved(dev),
+                          y=torch.empty((M, N), dtype=torch.bfloat16, device=dev),
+                          dx=torch.empty((M, K), dtype=torch.bfloat16, device=dev),
+                          dw=torch.empty((N, K), dtype=torch.bfloat16, device=dev)))
+
+    def step():
+        for u in units:
+            u["plan"].forward(u["x"], u["w"], u["saved"], y=u["y"])
+            u["plan"].backward(u["dy"], u["saved"], dx=u["dx"], dw=u["dw"], x=u["x"])
+
+    for _ in range(max(a.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    L.lib.fp8_profile_collect(None, None, 0)
+    L.lib.fp8_profile_enable(1)
+    n0 = ops.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(a.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = ops.launch_count() - n0
+    L.lib.fp8_profile_enable(0)
+    cap = launches + 16
+    kinds, durs = (ctypes.c_int * cap)(), (ctypes.c_float * cap)()
+    nrec = L.lib.fp8_profile_collect(kinds, durs, cap)
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / a.steps
+    flops_step = sum(6.0 * M * u["N"] * u["K"] for u in units)
+    value = flops_step * a.steps * world / (ms / 1e3) / 1e12
+    by = {}
+    for i in range(max(nrec, 0)):
+        by.setdefault(kinds[i], []).append(durs[i])
+    gemm_ms = by.get(4, [float("nan")])
+    gemm_tflops = flops_step / (sum(gemm_ms) / a.steps / 1e3) / 1e12
+    peaks = _peaks()
+    fp8_peak = 2.0 * peaks["bf16"]
+    cast_bytes = sum((M * u["K"] + u["N"] * u["K"] + M * u["N"]) * 6 for u in units)   # rowwise: 6 B / element
+    cast_ms = sum(sum(by.get(k, [])) for k in (0, 1)) / a.steps
+    e2e = None
+    if a.e2e_steps > 0:
+        host = [dict(x=u["x"].cpu().pin_memory(), w=u["w"].cpu().pin_memory(), dy=u["dy"].cpu().pin_memory(),
+                     y=torch.empty_like(u["y"], device="cpu").pin_memory(),
+                     dx=torch.empty_like(u["dx"], device="cpu").pin_memory(),
+                     dw=torch.empty_like(u["dw"], device="cpu").pin_memory()) for u in units]
+        dbuf = [dict(x=torch.empty_like(u["x"]), w=torch.empty_like(u["w"]), dy=torch.empty_like(u["dy"])) for u in units]
+
+        def e2e_step():
+            for u, h, d in zip(units, host, dbuf):
+                for k in ("x", "w", "dy"):
+                    d[k].copy_(h[k], non_blocking=True)
+                u["plan"].forward(d["x"], d["w"], u["saved"], y=u["y"])
+                u["plan"].backward(d["dy"], u["saved"], dx=u["dx"], dw=u["dw"], x=d["x"])
+                for k in ("y", "dx", "dw"):
+                    h[k].copy_(u[k], non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        e2e = {"value": flops_step * a.e2e_steps * world / (ems / 1e3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": sum((u["x"].numel() + u["w"].numel() + u["dy"].numel()) * 2 for u in units),
+               "d2h_bytes_per_step": sum((u["y"].numel() + u["dx"].numel() + u["dw"].numel()) * 2 for u in units),
+               "ms_per_step": ems / a.e2e_steps,
+               "path": "per linear: pinned host -> device X, W, dY + fp8_linear_fwd/bwd (C-ABI) + device -> host "
+                       "Y, dX, dW, every step, on the compute stream"}
+    bf16 = None
+    if not a.no_bf16:
+        def bstep():
+            for u in units:
+                torch.matmul(u["x"], u["w"].t(), out=u["y"])
+                torch.matmul(u["dy"], u["w"], out=u["dx"])
+                torch.matmul(u["dy"].t(), u["x"], out=u["dw"])
+        for _ in range(3):
+            bstep()
+        torch.cuda.synchronize()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(a.steps):
+            bstep()
+        b1.record(stream)
+        torch.cuda.synchronize()
+        bms = b0.elapsed_time(b1) / a.steps
+        bf16 = {"ms_per_step": bms, "tflops": flops_step / (bms / 1e3) / 1e12, "speedup_fp8_vs_bf16": bms / ms_step,
+                "impl": "torch.matmul (cuBLAS) bf16, same 3 GEMMs per linear"}
+    cpu = cpu_baseline(dict(cfg, N=14336)) if (rank == 0 and world == 1 and not a.no_cpu_baseline) else None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
+            "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp8 (e4m3 x e5m2 codes, fp32 accumulate, bf16 out)",
+            "data": "synthetic (seeded, device-generated, config value recipe)",
+            "config": {"workload": cfg["workload"], "M_per_gpu": M, "linears": cfg["linears"], "recipe": cfg["recipe"],
+                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                       "l2": "inputs larger than L2 (126 MB) for the MLP linears; no flush"},
+            "roofline": {"bound": "tensor", "kernel": "fp8_gemm_kernel (tcgen05 kind::f8f6f4)",
+                         "achieved": gemm_tflops, "peak": fp8_peak, "unit": "TFLOP/s", "frac": gemm_tflops / fp8_peak,
+                         "traffic": None,
+                         "peak_source": f"{peaks['src']}: bf16_tflops (burst) x 2 (dense FP8/BF16 ratio)",
+                         "algorithmic": "2*M*N*K flop per GEMM problem, summed over the 7 linears x 3 GEMMs",
+                         "launches_per_step": len(gemm_ms) / a.steps, "share_of_step": sum(gemm_ms) / a.steps / ms_step},
+            "cast": {"gbps": cast_bytes / (cast_ms / 1e3) / 1e9 if cast_ms > 0 else None, "peak_gbps": peaks["hbm"],
+                     "frac": cast_bytes / (cast_ms / 1e3) / 1e9 / peaks["hbm"] if cast_ms > 0 else None,
+                     "ms_per_step": cast_ms, "algorithmic_bytes_per_step": cast_bytes},
+            "kernels_ms_per_step": {name: round(sum(by.get(k, [])) / a.steps, 4)
+                                    for k, name in ((0, "amax"), (1, "cast"), (4, "gemm_fp8"))},
+            "bf16": bf16, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
 def run_moe(a):
     """MoE scaled grouped GEMM fwd+bwd (fp8_grouped_linear_fwd/bwd) on one GPU (replicas at N>1:
     the grouped GEMM has no exchange step of its own; expert parallelism's all-to-all is out of scope)."""
@@ -788,6 +960,8 @@ def main():
         run_reference(a)
     elif CONFIGS[a.config].get("kind") == "moe":
         run_moe(a)
+    elif CONFIGS[a.config].get("kind") == "layer":
+        run_layer(a)
     else:
         run_ours(a)
 
