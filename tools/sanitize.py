@@ -11,12 +11,35 @@ x, w, dy = synth.linear_inputs("c2", M, N, K, seed=0)
 X, W, G = (torch.from_numpy(a).to(torch.bfloat16).cuda() for a in (x, w, dy))
 for gran in ("tensor", "row", "col", "row_col"):
     ops.cast(X, "e4m3", gran, want_q=True, want_qt=True)
-ops.cast(X, "e4m3", "mx32", want_q=True, want_qt=True)
+ops.cast(X, "e4m3", "mx32", want_q=True, want_qt=True)      # TMA-ring MX cast (transposed dim1)
+ops.cast(X, "e5m2", "mx32_rm", want_q=True, want_qt=True)   # TMA-ring MX cast (row-major dim1)
+ops.amax(X, "row"), ops.amax(X, "col")                      # TMA-ring strip amax
 for recipe in ("tensorwise", "rowwise", "rowwise_gw_hp", "mxfp8"):
     plan = ops.LinearPlan(M, N, K, recipe=recipe)
     saved = plan.new_saved()
     plan.forward(X, W, saved)
     plan.backward(G, saved, x=X)
     plan.forward(X, W, None)
+# MoE grouped GEMM (M-grouped fwd / dX, K-grouped dW, an empty expert)
+sizes = [128, 0, 256, 128]
+E, T = len(sizes), sum(sizes)
+offs = torch.tensor(np.concatenate([[0], np.cumsum(sizes)]), dtype=torch.int32, device="cuda")
+for recipe in ("tensorwise", "rowwise"):
+    gp = ops.GroupedPlan(T, E, 256, K, recipe=recipe)
+    gs = gp.new_saved()
+    Xg = torch.randn((T, K), device="cuda").to(torch.bfloat16)
+    Wg = (torch.randn((E * 256, K), device="cuda") * 0.02).to(torch.bfloat16)
+    Gg = (torch.randn((T, 256), device="cuda") * 1e-3).to(torch.bfloat16)
+    gp.forward(Xg, Wg, offs, gs)
+    gp.backward(Gg, offs, gs)
+# fused P2P FSDP gather over 2 simulated ranks, and the MX scale re-tiling
+from paper_2507_16099_b200.fsdp import P2PWindow
+wins = P2PWindow.local_group(2, N * K)
+P2PWindow.allgather_local(wins, [W[:N // 2].contiguous(), W[N // 2:].contiguous()])
+torch.cuda.synchronize()
+for w_ in wins:
+    w_.close()
+slots = [ops.cast(W[r * 128:(r + 1) * 128].contiguous(), "e4m3", "mx32_rm", want_q=True, want_qt=True) for r in range(3)]
+ops.mx_scales_unshard(torch.cat([s["scale_t"] for s in slots]), 3, 128, K)
 torch.cuda.synchronize()
 print("ok")
