@@ -339,11 +339,23 @@ def run_ours(a):
             try:
                 p2p = P2PWindow(comm, N * K)
                 w_full = p2p.buffer(N, K, dev)
+                # pre-flight: the fused gather must reproduce the NCCL gather byte for byte on every rank
+                ref_q, ref_s, _ = comm.allgather_fp8(w_shard, "e4m3")
+                got_q, got_s, _ = p2p.allgather_fp8(w_shard, "e4m3")
+                ok = torch.tensor([int(torch.equal(ref_q, got_q) and torch.equal(ref_s, got_s))], device=dev)
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+                del ref_q
+                if not ok.item():
+                    raise RuntimeError("p2p pre-flight: gathered bytes differ from the NCCL gather")
                 gather_impl = "p2p (fp8_fsdp_allgather_p2p: cast pushes codes to every rank over NVLink)"
-            except Exception as e:  # noqa: BLE001  (IPC / peer access unavailable)
+            except Exception as e:  # noqa: BLE001  (IPC / peer access unavailable, pre-flight mismatch)
                 if a.gather == "p2p":
                     raise
-                gather_impl = f"nccl (p2p window failed: {str(e)[:120]})"
+                if p2p is not None:
+                    p2p.close()
+                    p2p = None
+                w_full = torch.empty((N, K), dtype=torch.uint8, device=dev)
+                gather_impl = f"nccl (p2p unavailable: {str(e)[:120]})"
         if mx_fsdp:   # MXFP8 gather (fp8_fsdp_allgather_mx): dim0 + dim1 codes and E8M0 scales
             mx_out = {"q": w_full, "scale": torch.empty(N * K // 32, dtype=torch.uint8, device=dev),
                       "q_t": torch.empty((N, K), dtype=torch.uint8, device=dev),
