@@ -11,7 +11,7 @@ amax -> scale -> saturating RNE cast -> tcgen05 scaled GEMM, for Y, dX and dW.
 import torch
 from torch import nn
 
-from .ops import LinearPlan
+from .ops import GroupedPlan, LinearPlan
 
 
 class _Plans:
@@ -99,3 +99,53 @@ def convert(model, recipe="tensorwise", module_filter_fn=None):
         else:
             convert(child, recipe, module_filter_fn)
     return model
+
+
+# ----------------------------------------------------------------------------- MoE
+
+class _GroupedPlans:
+    def __init__(self):
+        self._p = {}
+
+    def get(self, T, E, N, K, recipe, device):
+        key = (T, E, N, K, recipe, str(device))
+        if key not in self._p:
+            self._p[key] = GroupedPlan(T, E, N, K, recipe=recipe, out_dtype=torch.bfloat16, device=device)
+        return self._p[key]
+
+
+_GPLANS = _GroupedPlans()
+
+
+class _ScaledGroupedMMFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, offs, recipe):
+        T, K = x.shape
+        E, N, _ = w.shape
+        plan = _GPLANS.get(T, E, N, K, recipe, x.device)
+        saved = plan.new_saved(x.device)
+        y = plan.forward(x.contiguous(), w.reshape(E * N, K).contiguous(), offs, saved)
+        ctx.plan, ctx.buf, ctx.offs, ctx.wshape, ctx.wdtype = plan, saved, offs, w.shape, w.dtype
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        dx, dw = ctx.plan.backward(dy.contiguous(), ctx.offs, ctx.buf, want_dx=ctx.needs_input_grad[0],
+                                   want_dw=ctx.needs_input_grad[1])
+        if dw is not None:
+            dw = dw.view(ctx.wshape)
+            if dw.dtype != ctx.wdtype:
+                dw = dw.to(ctx.wdtype)
+        return dx, dw, None, None
+
+
+def scaled_grouped_mm(x, w, offs, recipe="rowwise"):
+    """Differentiable FP8 scaled grouped GEMM for MoE training (reading R-c22):
+    out[offs[g]:offs[g+1]] = x[offs[g]:offs[g+1]] @ w[g].T for every expert g, each GEMM (and its
+    backward dX, dW) in FP8 with the recipe's dynamic scaling, in one grouped launch per pass.
+      x [T, K] bf16 tokens sorted by expert; w [E, N, K] bf16 expert weights (nn.Linear layout);
+      offs int32 [E+1] on the device (offs[0] = 0, offs[E] = T, multiples of 128, non-decreasing).
+    Returns out [T, N] bf16."""
+    if x.dtype != torch.bfloat16:
+        x = x.to(torch.bfloat16)
+    return _ScaledGroupedMMFn.apply(x, w, offs, recipe)
