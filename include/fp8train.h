@@ -404,6 +404,23 @@ fp8_status_t fp8_fsdp_allgather_p2p_local(fp8_p2p_t* wins, int nranks, const fp8
                                           fp8_format_t fmt, const float* const* amax_in,
                                           float* const* scale_out, float* const* amax_out,
                                           void* stream);
+/* Async-TP FP8 linear forward ("float8 training with async
+ * tensor parallelism"): sequence-parallel activations X_r [M_local, K] (rank r's tokens) are
+ * all-gathered in FP8 and multiplied by this rank's column shard of the weight W_r [N_local, K],
+ *   y [nranks*M_local, N_local] = X_full W_r^T,
+ * with the gather and the GEMM overlapped inside ONE GEMM launch: each rank's cast kernel pushes
+ * its codes (tensorwise, one global scale from the same amax signal slots as the FSDP gather)
+ * into slot r of every window and publishes done[r]; the GEMM's TMA producer waits for done[c]
+ * before loading the rows of chunk c, computing its own chunk first.  The window (from
+ * fp8_p2p_create) must hold nranks*M_local*K bytes; M_local % 256 == 0; cfg->recipe
+ * tensorwise; y and ws 256-byte aligned; ws: fp8_tp_workspace_bytes(N_local, K) bytes. */
+size_t fp8_tp_workspace_bytes(int64_t n_local, int64_t K);
+fp8_status_t fp8_tp_allgather_linear_fwd(fp8_p2p_t win, const fp8_linear_cfg_t* cfg, fp8_hp_t x_shard,
+                                         fp8_hp_t w, void* y, void* ws, size_t ws_bytes, void* stream);
+/* Single-process form for a fp8_p2p_create_local group (phase by phase on one stream). */
+fp8_status_t fp8_tp_allgather_linear_fwd_local(fp8_p2p_t* wins, int nranks, const fp8_linear_cfg_t* cfg,
+                                               const fp8_hp_t* x_shards, const fp8_hp_t* w, void* const* y,
+                                               void* const* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Helpers

@@ -96,6 +96,12 @@ SIGNATURES = {
                                           _c.c_void_p]),
     "fp8_fsdp_allgather_p2p_local": (_c.c_int, [_c.POINTER(_c.c_void_p), _c.c_int, _c.POINTER(HP), _c.c_int,
                                                 _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_void_p]),
+    "fp8_tp_workspace_bytes": (_c.c_size_t, [_c.c_int64, _c.c_int64]),
+    "fp8_tp_allgather_linear_fwd": (_c.c_int, [_c.c_void_p, _c.POINTER(LinearCfg), HP, HP, _c.c_void_p, _c.c_void_p,
+                                               _c.c_size_t, _c.c_void_p]),
+    "fp8_tp_allgather_linear_fwd_local": (_c.c_int, [_c.POINTER(_c.c_void_p), _c.c_int, _c.POINTER(LinearCfg),
+                                                     _c.POINTER(HP), _c.POINTER(HP), _c.c_void_p, _c.c_void_p,
+                                                     _c.c_size_t, _c.c_void_p]),
     "fp8_mx_scales_unshard": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),
 }
 AMAX_MULTI_MAX = 48

@@ -62,6 +62,12 @@ struct Prob {
   //             operands; D rows g*M.., sa index g*M + row, sb index g*N + col; empty group -> 0
   int grouped, G;
   const int* offs;
+  // async-TP (fp8_tp_allgather_linear_fwd): rows of A arrive by chunks of chunk_rows pushed by the
+  // other ranks; the producer waits for chunk_done[c] >= chunk_epoch before loading chunk c, and
+  // M tiles are rotated by mrot so this rank's own chunk is computed first
+  const unsigned long long* chunk_done;
+  int chunk_rows, mrot;
+  unsigned chunk_epoch;
 };
 // A launch processes the tiles of p0 ([0, t1)) then p1 ([t1, num_tiles)) on one persistent grid:
 // the backward's dX and dW GEMMs share one launch, so neither has its own wave-quantisation tail.
@@ -207,6 +213,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
     ti.katoms = 1 << 30;
     if (!GRP || P.grouped == 0) {
       tile_coords(local, P.tiles_m, P.tiles_n, args.group_m, ti.mb, ti.nb);
+      if (P.mrot) ti.mb = (ti.mb + P.mrot) % P.tiles_m;
       return ti;
     }
     const int* o = goffs + ti.pi * (GMAX + 1);
@@ -307,6 +314,21 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
       const uint32_t tx = L::tx_bytes - ((MX && (args.debug & 4)) ? CG * (L::SFA_STAGE + L::SFB_STAGE) : 0);
       const int KT = P.sf_tiles_k;
       const int num_kb = ti.num_kb;
+      if (P.chunk_done) {   // async-TP: wait until the rank that owns these A rows has pushed them
+        if (lane == 0) {
+          const unsigned long long* f = P.chunk_done + (m0 + ti.a_row0) / P.chunk_rows;
+          uint32_t n = 0;
+          while (ld_acquire_sys_u64(f) < P.chunk_epoch) {
+            __nanosleep(64);
+            if (++n > (1u << 27)) {
+              printf("fp8_gemm: A chunk %d never arrived (watchdog)\n", (m0 + ti.a_row0) / P.chunk_rows);
+              asm volatile("trap;");
+            }
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");   // generic-proxy acquire -> TMA reads
+        }
+        __syncwarp();
+      }
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(empty_bar + 8 * stage, phase ^ 1);
         if (lane == 0) {
@@ -700,6 +722,10 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   P.grouped = p.grouped;
   P.G = p.G;
   P.offs = p.offs;
+  P.chunk_done = p.chunk_done;
+  P.chunk_rows = p.chunk_rows;
+  P.mrot = p.mrot;
+  P.chunk_epoch = p.chunk_epoch;
   return true;
 }
 

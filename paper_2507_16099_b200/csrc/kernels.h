@@ -104,6 +104,11 @@ struct GemmProblem {
   int grouped = 0;
   int G = 0;
   const int* offs = nullptr;
+  // async-TP: per-chunk arrival flags of A's rows (see Prob in gemm_kernels.cu)
+  const unsigned long long* chunk_done = nullptr;
+  int chunk_rows = 0;
+  int mrot = 0;
+  unsigned chunk_epoch = 0;
 };
 constexpr int GEMM_MAX_GROUPS = 256;
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st);

@@ -303,4 +303,97 @@ fp8_status_t fp8_fsdp_allgather_p2p_local(fp8_p2p_t* wins, int n, const fp8_hp_t
   return FP8_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Async-TP FP8 linear forward ("float8 training with async tensor
+// parallelism"): sequence-parallel X shards [M_local, K] are all-gathered in FP8 and multiplied by
+// this rank's column shard of W [N_local, K] in ONE GEMM launch that overlaps the gather: every rank's
+// cast_push stores its codes into slot r of all windows and publishes done[r]; the GEMM's TMA producer
+// waits for done[c] before loading chunk c's rows, starting with its own chunk (tile rotation).
+//   y [P*M_local, N_local] = X_full W_local^T, tensorwise (global X scale from the signal slots).
+// ---------------------------------------------------------------------------
+size_t fp8_tp_workspace_bytes(int64_t n_local, int64_t K) { return 1024 + (((size_t)n_local * K + 255) & ~size_t(255)); }
+
+}  // extern "C"
+
+namespace {
+struct TpWs {
+  float* amax_x; float* scale_x; float* amax_w; float* scale_w; uint8_t* wq;
+};
+TpWs carve_tp(void* ws) {
+  uint8_t* b = static_cast<uint8_t*>(ws);
+  return TpWs{reinterpret_cast<float*>(b), reinterpret_cast<float*>(b + 256), reinterpret_cast<float*>(b + 512),
+              reinterpret_cast<float*>(b + 768), b + 1024};
+}
+fp8_status_t tp_check(fp8_p2p_t win, const fp8_linear_cfg_t* cfg, const fp8_hp_t& x, const fp8_hp_t& w, void* y,
+                      void* ws, size_t ws_bytes) {
+  if (!cfg || cfg->recipe != FP8_RECIPE_TENSORWISE) return fail(FP8_EUNSUPPORTED, "async-TP: tensorwise recipe");
+  if (cfg->out_dtype != FP8_DT_BF16 && cfg->out_dtype != FP8_DT_F32) return fail(FP8_EINVAL, "bad out_dtype");
+  if (!y || !ws || !w.ptr) return fail(FP8_EINVAL, "null pointer");
+  if (x.rows % 256) return fail(FP8_EALIGN, "async-TP: M_local must be a multiple of 256");
+  if (w.cols != x.cols || w.rows < 16 || w.rows % 16 || w.dtype != x.dtype) return fail(FP8_EINVAL, "w shape / dtype");
+  if (w.ld < w.cols || (w.ld * (w.dtype == FP8_DT_F32 ? 4 : 2)) % 16 || (reinterpret_cast<uintptr_t>(w.ptr) & 15))
+    return fail(FP8_EALIGN, "w: ld / alignment");
+  if ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(ws)) & 255)
+    return fail(FP8_EALIGN, "y / ws must be 256-byte aligned");
+  if (ws_bytes < fp8_tp_workspace_bytes(w.rows, w.cols)) return fail(FP8_EWORKSPACE, "workspace too small");
+  return p2p_check(win, x, (fp8_format_t)cfg->fmt_fwd, nullptr, reinterpret_cast<float*>(ws), reinterpret_cast<float*>(ws));
+}
+// W cast (local) + the chunk-waiting GEMM of one rank
+fp8_status_t tp_gemm(fp8_p2p_t win, const fp8_linear_cfg_t* cfg, const fp8_hp_t& x, const fp8_hp_t& w, void* y,
+                     const TpWs& t, cudaStream_t st) {
+  const bool wb = w.dtype == FP8_DT_BF16;
+  const int ff = cfg->fmt_fwd;
+  fp8_status_t s;
+  if ((s = cuda_check(cudaMemsetAsync(t.amax_w, 0, 4, st), "memset")) != FP8_OK) return s;
+  if ((s = cuda_check(launch_amax(w.ptr, wb, w.rows, w.cols, w.ld, 1, reinterpret_cast<uint32_t*>(t.amax_w), nullptr,
+                                  nullptr, st), "amax w")) != FP8_OK)
+    return s;
+  if ((s = cuda_check(launch_cast(w.ptr, wb, ff, w.rows, w.cols, w.ld, 1, 0, t.amax_w, t.amax_w, t.wq, nullptr,
+                                  t.scale_w, nullptr, st), "cast w")) != FP8_OK)
+    return s;
+  const int64_t M = (int64_t)win->P * x.rows, N = w.rows, K = x.cols;
+  GemmProblem p{win->base, t.wq, ff, ff, 0, 0, t.scale_x, t.scale_w, 0, M, N, K, K, K, y,
+                cfg->out_dtype == FP8_DT_F32, N};
+  p.chunk_done = win->sig->done;
+  p.chunk_rows = (int)x.rows;
+  p.chunk_epoch = win->epoch;
+  p.mrot = win->rank * (int)(x.rows / 256);
+  return cuda_check(launch_gemm(p, st), "tp gemm");
+}
+}  // namespace
+
+extern "C" {
+
+fp8_status_t fp8_tp_allgather_linear_fwd(fp8_p2p_t win, const fp8_linear_cfg_t* cfg, fp8_hp_t x_shard, fp8_hp_t w,
+                                         void* y, void* ws, size_t ws_bytes, void* stream) {
+  FP8T_P2P_TRY(tp_check(win, cfg, x_shard, w, y, ws, ws_bytes));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const TpWs t = carve_tp(ws);
+  const fp8_format_t f = (fp8_format_t)cfg->fmt_fwd;
+  FP8T_P2P_TRY(phase_signal(win, x_shard, nullptr, t.amax_x, st));
+  FP8T_P2P_TRY(phase_wait_scale(win, f, t.scale_x, t.amax_x, st));
+  FP8T_P2P_TRY(phase_cast_push(win, x_shard, f, t.scale_x, st));
+  return tp_gemm(win, cfg, x_shard, w, y, t, st);
+}
+
+fp8_status_t fp8_tp_allgather_linear_fwd_local(fp8_p2p_t* wins, int n, const fp8_linear_cfg_t* cfg,
+                                               const fp8_hp_t* x_shards, const fp8_hp_t* w, void* const* y,
+                                               void* const* ws, size_t ws_bytes, void* stream) {
+  if (!wins || !x_shards || !w || !y || !ws || n < 1) return fail(FP8_EINVAL, "null pointer / n < 1");
+  for (int r = 0; r < n; ++r) {
+    if (!wins[r] || wins[r]->P != n || wins[r]->rank != r) return fail(FP8_EINVAL, "wins must be one local group, in rank order");
+    FP8T_P2P_TRY(tp_check(wins[r], cfg, x_shards[r], w[r], y[r], ws[r], ws_bytes));
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const fp8_format_t f = (fp8_format_t)cfg->fmt_fwd;
+  for (int r = 0; r < n; ++r) FP8T_P2P_TRY(phase_signal(wins[r], x_shards[r], nullptr, carve_tp(ws[r]).amax_x, st));
+  for (int r = 0; r < n; ++r) {
+    const TpWs t = carve_tp(ws[r]);
+    FP8T_P2P_TRY(phase_wait_scale(wins[r], f, t.scale_x, t.amax_x, st));
+  }
+  for (int r = 0; r < n; ++r) FP8T_P2P_TRY(phase_cast_push(wins[r], x_shards[r], f, carve_tp(ws[r]).scale_x, st));
+  for (int r = 0; r < n; ++r) FP8T_P2P_TRY(tp_gemm(wins[r], cfg, x_shards[r], w[r], y[r], carve_tp(ws[r]), st));
+  return FP8_OK;
+}
+
 }  // extern "C"

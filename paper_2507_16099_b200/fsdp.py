@@ -109,6 +109,11 @@ class Comm:
             self._h = ctypes.c_void_p()
 
 
+def _tp_cfg(fmt, out_dtype):
+    return L.LinearCfg(L.RECIPE_TENSORWISE, FORMATS[fmt], L.E5M2, L.MX_FLOOR,
+                       L.DT_F32 if out_dtype == torch.float32 else L.DT_BF16)
+
+
 class _DevBuf:
     """__cuda_array_interface__ view of library-owned device memory (the P2P gather buffer)."""
 
@@ -161,6 +166,38 @@ class P2PWindow:
             "fp8_fsdp_allgather_p2p_local")
         rows, cols = shards[0].shape
         return [(w.buffer(n * rows, cols, dev), scales[r], amaxes[r]) for r, w in enumerate(wins)]
+
+    def tp_linear_fwd(self, x_shard, w, out_dtype=torch.bfloat16, fmt="e4m3", y=None, ws=None, stream=None):
+        """Async-TP FP8 forward (fp8_tp_allgather_linear_fwd): y [world*M_local, N_local] = X_full W^T with
+        the FP8 all-gather of X overlapped inside the GEMM launch."""
+        cfg = _tp_cfg(fmt, out_dtype)
+        M, K = x_shard.shape
+        if y is None:
+            y = torch.empty((self.world * M, w.shape[0]), dtype=out_dtype, device=x_shard.device)
+        wsb = L.lib.fp8_tp_workspace_bytes(w.shape[0], K)
+        if ws is None:
+            ws = torch.empty(wsb, dtype=torch.uint8, device=x_shard.device)
+        L.check(L.lib.fp8_tp_allgather_linear_fwd(self._h, ctypes.byref(cfg), hp(x_shard), hp(w), _ptr(y), _ptr(ws), wsb,
+                                                  _stream(stream)), "fp8_tp_allgather_linear_fwd")
+        return y
+
+    @staticmethod
+    def tp_linear_fwd_local(wins, x_shards, ws_, out_dtype=torch.bfloat16, fmt="e4m3", stream=None):
+        """Every simulated rank's async-TP forward of a local_group, phase by phase on one stream."""
+        n = len(wins)
+        cfg = _tp_cfg(fmt, out_dtype)
+        dev = x_shards[0].device
+        M, K = x_shards[0].shape
+        ys = [torch.empty((n * M, w.shape[0]), dtype=out_dtype, device=dev) for w in ws_]
+        wsb = max(L.lib.fp8_tp_workspace_bytes(w.shape[0], K) for w in ws_)
+        scratch = [torch.empty(wsb, dtype=torch.uint8, device=dev) for _ in range(n)]
+        vp = ctypes.c_void_p * n
+        L.check(L.lib.fp8_tp_allgather_linear_fwd_local(
+            (ctypes.c_void_p * n)(*[w._h.value for w in wins]), n, ctypes.byref(cfg),
+            (L.HP * n)(*[hp(x) for x in x_shards]), (L.HP * n)(*[hp(w) for w in ws_]),
+            vp(*[y.data_ptr() for y in ys]), vp(*[t.data_ptr() for t in scratch]), wsb, _stream(stream)),
+            "fp8_tp_allgather_linear_fwd_local")
+        return ys
 
     def buffer(self, rows, cols, device="cuda"):
         """uint8 [rows, cols] torch view of this rank's gather buffer (library-owned memory)."""

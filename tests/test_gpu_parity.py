@@ -848,3 +848,35 @@ def test_scaled_grouped_mm_autograd():
         ref = x.detach()[a:b].float() @ w.detach()[g].float().t()
         rel = (y[a:b].float() - ref).norm() / ref.norm()
         assert rel < 0.08, float(rel)
+
+
+# ----------------------------------------------------------------------------- async-TP
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_tp_allgather_linear_simulated_ranks(P):
+    """fp8_tp_allgather_linear_fwd for P simulated ranks on one GPU: every rank's y = X_full W_r^T equals
+    the plain tensorwise forward of (X_full, W_r) bit for bit (same codes, same global X scale, same
+    tcgen05 tiles, only their order rotated) and is within tolerance of the oracle; repeated epochs."""
+    from paper_2507_16099_b200.fsdp import P2PWindow
+    Ml, K, Nl = 256, 384, 272
+    M = P * Ml
+    wins = P2PWindow.local_group(P, M * K)
+    try:
+        for it in range(2):
+            x = synth.tensor_c2("x", (M, K), seed=20 + it)
+            ws_np = [synth.tensor_c2("w", (Nl, K), seed=30 + r + it) for r in range(P)]
+            X = _dev(x, torch.bfloat16)
+            shards = [X[r * Ml:(r + 1) * Ml].contiguous() for r in range(P)]
+            Ws = [_dev(w_, torch.bfloat16) for w_ in ws_np]
+            ys = P2PWindow.tp_linear_fwd_local(wins, shards, Ws, out_dtype=torch.float32)
+            torch.cuda.synchronize()
+            plan = ops.LinearPlan(M, Nl, K, recipe="tensorwise", out_dtype=torch.float32)
+            for r in range(P):
+                y_ref = plan.forward(X, Ws[r], None)
+                torch.cuda.synchronize()
+                assert torch.equal(ys[r], y_ref), f"rank {r}"
+                yo, bd, _ = olin.forward(x, ws_np[r], "tensorwise")
+                assert np.all(np.abs(_np(ys[r]).astype(np.float64) - yo) <= 1e-2 * bd + 1e-30)
+    finally:
+        for w_ in wins:
+            w_.close()
