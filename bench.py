@@ -24,8 +24,20 @@ import threading
 import time
 
 # NCCL writes its debug/version banner to stdout by default; the contract wants exactly one JSON
-# line on stdout, so route NCCL's log to stderr unless the caller chose a file.
+# line on stdout, so route NCCL's log to stderr unless the caller chose a file (and main() points
+# fd 1 at stderr for the whole run, writing only the JSON line to the original stdout).
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+_JSON_FD = None
+
+
+def emit(line):
+    """Write the one JSON result line to the original stdout."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -158,7 +170,7 @@ def run_reference(a):
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": _threads_used(), "kind": "oracle",
                              "sample": desc},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -372,13 +384,43 @@ def run_ours(a):
             comm.allgather_fp8(ww, "e4m3", out=w_full, scale=w_scale, amax=w_amax)
         return (w_full, w_scale)
 
+    # dW reduce-scatter at N > 1: fused into the dW GEMM's epilogue over a P2P window
+    # (fp8_linear_bwd_rs) unless --gather nccl, with a pre-flight against torch's NCCL reduce-scatter
+    rs_win = None
+    rs_impl = "torch NCCL reduce_scatter_tensor (bf16)" if world > 1 else None
+    if world > 1 and a.gather != "nccl":
+        from paper_2507_16099_b200.fsdp import P2PWindow
+        try:
+            rs_win = P2PWindow(comm, N * K * 2)
+            wf0 = gather(w_shard)
+            plan.forward(x, None, saved, y=y, w_fp8=wf0)
+            plan.backward(dy, saved, dx=dx, dw=dw, w_fp8=wf0)
+            ref = torch.empty_like(dw_shard)
+            dist.reduce_scatter_tensor(ref, dw)
+            ops.linear_backward_rs(plan, dy, saved, rs_win, dw_shard, dx=dx, w_fp8=wf0)
+            err = (dw_shard.float() - ref.float()).norm() / ref.float().norm().clamp_min(1e-30)
+            ok = torch.tensor([int(bool(err < 1e-2))], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            del ref
+            if not ok.item():
+                raise RuntimeError(f"fused reduce-scatter pre-flight: rel err {float(err):.3g} vs NCCL")
+            rs_impl = "fused (fp8_linear_bwd_rs: dW GEMM epilogue stores tiles into the owner's staging over NVLink)"
+        except Exception as e:  # noqa: BLE001
+            if rs_win is not None:
+                rs_win.close()
+                rs_win = None
+            rs_impl = f"torch NCCL reduce_scatter_tensor (fused RS unavailable: {str(e)[:120]})"
+
     def step(xx=x, ww=w_shard, gg=dy):
         if fsdp:
             wf = gather(ww)
             plan.forward(xx, None, saved, y=y, w_fp8=wf)
-            plan.backward(gg, saved, dx=dx, dw=dw, w_fp8=wf)
-            if world > 1:
-                dist.reduce_scatter_tensor(dw_shard, dw)
+            if rs_win is not None:
+                ops.linear_backward_rs(plan, gg, saved, rs_win, dw_shard, dx=dx, w_fp8=wf)
+            else:
+                plan.backward(gg, saved, dx=dx, dw=dw, w_fp8=wf)
+                if world > 1:
+                    dist.reduce_scatter_tensor(dw_shard, dw)
         else:
             plan.forward(xx, ww, saved, y=y)
             plan.backward(gg, saved, dx=dx, dw=dw, x=xx)
@@ -439,7 +481,7 @@ def run_ours(a):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             gms = float(t.item())
         recv = N * K * (world - 1) // world * (2 + 2 / 32 if mx_fsdp else 1)   # bytes each rank receives
-        gather_info = {"impl": gather_impl, "ms": gms, "recv_bytes_per_rank": recv,
+        gather_info = {"impl": gather_impl, "reduce_scatter": rs_impl, "ms": gms, "recv_bytes_per_rank": recv,
                        "busbw_GBps": recv / (gms / 1e3) / 1e9 if world > 1 else None,
                        "nvlink_peak_GBps": 900.0}
 
@@ -526,10 +568,13 @@ def run_ours(a):
             if fsdp:
                 wf = gather(wd)
                 plan.forward(xd, None, saved, y=yo, w_fp8=wf)
-                plan.backward(gd, saved, dx=dxo, dw=dw, w_fp8=wf)
-                if world > 1:
+                if rs_win is not None:
+                    ops.linear_backward_rs(plan, gd, saved, rs_win, dwo, dx=dxo, w_fp8=wf)
+                elif world > 1:
+                    plan.backward(gd, saved, dx=dxo, dw=dw, w_fp8=wf)
                     dist.reduce_scatter_tensor(dwo, dw)
                 else:
+                    plan.backward(gd, saved, dx=dxo, dw=dw, w_fp8=wf)
                     dwo.copy_(dw)
             else:
                 plan.forward(xd, wd, saved, y=yo)
@@ -638,9 +683,11 @@ def run_ours(a):
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if fsdp and p2p is not None:
         p2p.close()
+    if fsdp and rs_win is not None:
+        rs_win.close()
     if comm is not None:
         comm.close()
     if dist.is_initialized():
@@ -805,7 +852,7 @@ def run_layer(a):
                                     for k, name in ((0, "amax"), (1, "cast"), (4, "gemm_fp8"))},
             "bf16": bf16, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist.is_initialized():
         dist.destroy_process_group()
 
@@ -961,13 +1008,17 @@ def run_moe(a):
                                     for k, name in ((0, "amax"), (1, "cast"), (4, "gemm_fp8_grouped"))},
             "bf16": bf16, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist.is_initialized():
         dist.destroy_process_group()
 
 
 def main():
+    global _JSON_FD
     a = parse()
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)    # keep the real stdout for the JSON line; everything else -> stderr
+    os.dup2(2, 1)
     if a.impl == "reference":
         run_reference(a)
     elif CONFIGS[a.config].get("kind") == "moe":

@@ -417,6 +417,18 @@ fp8_status_t fp8_fsdp_allgather_p2p_local(fp8_p2p_t* wins, int nranks, const fp8
 size_t fp8_tp_workspace_bytes(int64_t n_local, int64_t K);
 fp8_status_t fp8_tp_allgather_linear_fwd(fp8_p2p_t win, const fp8_linear_cfg_t* cfg, fp8_hp_t x_shard,
                                          fp8_hp_t w, void* y, void* ws, size_t ws_bytes, void* stream);
+/* FSDP backward with the dW reduce-scatter fused into the dW GEMM (the "GEMM -> reduce-scatter"
+ * pattern; FSDP2 reduce-scatters weight gradients to their dim-0 shards): as fp8_linear_bwd, but
+ * every dW tile is stored by the GEMM epilogue straight into the staging buffer of the rank that
+ * owns its rows (rs_win: a window of >= nranks * (N/nranks) * K * 2 bytes from fp8_p2p_create, one
+ * per concurrently reduced gradient), and this rank then sums its nranks slots in rank order
+ * (fp32, one bf16 rounding) into dw_shard [N/nranks, K] bf16.  dx is computed locally as usual.
+ * Every rank calls it in the same order; N % (256 * nranks) == 0; cfg->out_dtype BF16.  A
+ * cross-rank barrier on rs_win at entry keeps a fast rank from overwriting a slot a slow rank is
+ * still summing.  Result == the bf16 sum of the ranks' fp8_linear_bwd dW rows (bit-exact). */
+fp8_status_t fp8_linear_bwd_rs(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x, const void* saved,
+                               const fp8_tensor_t* w_fp8, void* dx, fp8_p2p_t rs_win, int nranks,
+                               void* dw_shard, void* ws, size_t ws_bytes, void* stream);
 /* Single-process form for a fp8_p2p_create_local group (phase by phase on one stream). */
 fp8_status_t fp8_tp_allgather_linear_fwd_local(fp8_p2p_t* wins, int nranks, const fp8_linear_cfg_t* cfg,
                                                const fp8_hp_t* x_shards, const fp8_hp_t* w, void* const* y,

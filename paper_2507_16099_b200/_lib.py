@@ -102,6 +102,8 @@ SIGNATURES = {
     "fp8_tp_allgather_linear_fwd_local": (_c.c_int, [_c.POINTER(_c.c_void_p), _c.c_int, _c.POINTER(LinearCfg),
                                                      _c.POINTER(HP), _c.POINTER(HP), _c.c_void_p, _c.c_void_p,
                                                      _c.c_size_t, _c.c_void_p]),
+    "fp8_linear_bwd_rs": (_c.c_int, [_c.POINTER(LinearCfg), HP, HP, _c.c_void_p, _c.POINTER(Tensor8), _c.c_void_p,
+                                     _c.c_void_p, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
     "fp8_mx_scales_unshard": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),
 }
 AMAX_MULTI_MAX = 48

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "kernels.h"
+#include "p2p_internal.h"
 
 namespace fp8t {
 
@@ -642,9 +643,28 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x
   return fp8_linear_bwd_ex(cfg, dy, nullptr, x, saved, w_fp8, dx, nullptr, dw, ws, ws_bytes, stream);
 }
 
+static fp8_status_t linear_bwd_impl(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
+                                    const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax, void* dw,
+                                    void* ws, size_t ws_bytes, void* stream, fp8_p2p_t rs_win, int rs_nranks);
+
 fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
                                const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax, void* dw,
                                void* ws, size_t ws_bytes, void* stream) {
+  return linear_bwd_impl(cfg, dy, dy_amax, x, saved, w_fp8, dx, dx_amax, dw, ws, ws_bytes, stream, nullptr, 1);
+}
+
+fp8_status_t fp8_linear_bwd_rs(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x, const void* saved,
+                               const fp8_tensor_t* w_fp8, void* dx, fp8_p2p_t rs_win, int nranks, void* dw_shard,
+                               void* ws, size_t ws_bytes, void* stream) {
+  if (!rs_win || !dw_shard) return fail(FP8_EINVAL, "rs_win / dw_shard: null");
+  if (nranks < 1) return fail(FP8_EINVAL, "nranks < 1");
+  if (!cfg || cfg->out_dtype != FP8_DT_BF16) return fail(FP8_EUNSUPPORTED, "fused reduce-scatter: bf16 dW only");
+  return linear_bwd_impl(cfg, dy, nullptr, x, saved, w_fp8, dx, nullptr, dw_shard, ws, ws_bytes, stream, rs_win, nranks);
+}
+
+static fp8_status_t linear_bwd_impl(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
+                                    const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax, void* dw,
+                                    void* ws, size_t ws_bytes, void* stream, fp8_p2p_t rs_win, int rs_nranks) {
   FP8T_TRY(check_hp(dy, "dy"));
   const int64_t M = dy.rows, N = dy.cols, K = x.cols;
   const bool gw_hp = cfg && cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;
@@ -661,6 +681,9 @@ fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const f
   if (w_fp8) FP8T_TRY(check_w_fp8(cfg, w_fp8, N, K, dx != nullptr));
   if (dy_amax && cfg->recipe != FP8_RECIPE_TENSORWISE)
     return fail(FP8_EUNSUPPORTED, "dy_amax (precomputed tensor amax) needs the tensorwise recipe");
+  if (rs_win && (N % ((int64_t)rs_nranks * 256)))
+    return fail(FP8_EALIGN, "fused reduce-scatter: N must be a multiple of 256 * nranks");
+  const int64_t rs_rows = N / rs_nranks;   // dW rows per rank (FSDP2 dim-0 shard)
   cudaStream_t st = S(stream);
   const bool gb = dy.dtype == FP8_DT_BF16;
   const int ff = cfg->fmt_fwd, fg = cfg->fmt_grad;
@@ -711,7 +734,9 @@ gemms:
     if (dw) {
       GemmProblem p{static_cast<const uint8_t*>(dy.ptr), static_cast<const uint8_t*>(x.ptr), 0, 0, 1, 1, nullptr,
                     nullptr, 0, N, K, M, dy.ld, x.ld, dw, of32, K, 1};
+      if (rs_win) FP8T_TRY(p2p_rs_begin(rs_win, rs_rows, K, st, p));
       FP8T_CUDA(launch_gemm(p, st), "gemm dw bf16");
+      if (rs_win) FP8T_TRY(p2p_rs_end(rs_win, rs_rows, K, dw, K, st));
     }
     return FP8_OK;
   }
@@ -749,7 +774,9 @@ gemms:
     // dW[N,K] = dY^T[N,M] . X : A = dY^T [N,M], B = X^T [K,M]
     if (dw) ps[n++] = GemmProblem{bw.gT, sv.xT, fg, ff, 0, 0, bw.sgT, sv.sx, mode, N, K, M, M, M, dw, of32, K};
   }
+  if (rs_win && dw) FP8T_TRY(p2p_rs_begin(rs_win, rs_rows, K, st, ps[n - 1]));   // dW is the last problem
   FP8T_CUDA(launch_gemms(ps, n, st), "gemm dx/dw");
+  if (rs_win && dw) FP8T_TRY(p2p_rs_end(rs_win, rs_rows, K, dw, K, st));
   return FP8_OK;
 }
 

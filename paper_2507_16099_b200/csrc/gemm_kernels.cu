@@ -68,6 +68,16 @@ struct Prob {
   const unsigned long long* chunk_done;
   int chunk_rows, mrot;
   unsigned chunk_epoch;
+  // fused reduce-scatter (fp8_linear_bwd_rs / fp8_tp_linear_bwd): D's row chunk c (rs_chunk_rows rows)
+  // belongs to rank c.  The epilogue stores a tile of chunk c straight into rank c's staging buffer at
+  // source slot rs_rank ([P][rs_chunk_rows][N] bf16); each epilogue warp then counts itself on the local
+  // chunk counter, and the last of the chunk's rs_expect warps fences at system scope and publishes
+  // done[rs_rank] = rs_epoch in rank c's signal block.  Rank c sums its P slots afterwards.
+  uint8_t* const* rs_bufs;
+  P2PSig* const* rs_sigs;
+  unsigned* rs_cnt;
+  int rs_rank, rs_chunk_rows, rs_expect;
+  unsigned rs_epoch;
 };
 // A launch processes the tiles of p0 ([0, t1)) then p1 ([t1, num_tiles)) on one persistent grid:
 // the backward's dX and dW GEMMs share one launch, so neither has its own wave-quantisation tail.
@@ -507,6 +517,9 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
       if (!row_scales && P.sa) rs = __frcp_rn(P.sa[0]) * __frcp_rn(P.sb[0]);
       if (row_scales && rvalid) rs = __frcp_rn(P.sa[ti.sa_off + row]);
       uint8_t* Dbase = static_cast<uint8_t*>(P.D) + ti.d_row0 * P.ldd * (out_f32 ? 4 : 2);
+      const int rs_chunk = P.rs_bufs ? (mb * BM * CG) / P.rs_chunk_rows : 0;
+      if (P.rs_bufs)   // the tile's rows go to rank rs_chunk's staging slot rs_rank
+        Dbase = P.rs_bufs[rs_chunk] + (int64_t)(P.rs_rank - rs_chunk) * P.rs_chunk_rows * P.ldd * (out_f32 ? 4 : 2);
       uint32_t dmax = 0;   // |D| max over this thread's stored values (fp32 bit patterns)
 
       // scale + convert + store 32 columns [col0, col0 + 32) of this thread's row
@@ -602,6 +615,17 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
       if (P.out_amax) {   // (P is uniform across the CTA; every lane reaches this point)
         dmax = __reduce_max_sync(0xffffffffu, dmax);
         if (lane == 0 && dmax) atomicMax(P.out_amax, dmax);
+      }
+      if (P.rs_bufs) {    // fused reduce-scatter: this warp's rows of the tile are stored
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_system();
+          if (atomicAdd(P.rs_cnt + rs_chunk, 1u) == (unsigned)P.rs_expect - 1) {   // chunk complete
+            P.rs_cnt[rs_chunk] = 0;
+            __threadfence_system();
+            st_release_sys_u64(&P.rs_sigs[rs_chunk]->done[P.rs_rank], P.rs_epoch);
+          }
+        }
       }
       if (++acc == L::ACC) { acc = 0; acc_phase ^= 1; }
     }
@@ -726,6 +750,14 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   P.chunk_rows = p.chunk_rows;
   P.mrot = p.mrot;
   P.chunk_epoch = p.chunk_epoch;
+  P.rs_bufs = p.rs_bufs;
+  P.rs_sigs = p.rs_sigs;
+  P.rs_cnt = p.rs_cnt;
+  P.rs_rank = p.rs_rank;
+  P.rs_chunk_rows = p.rs_chunk_rows;
+  // every epilogue warp of both CTAs of a pair arrives once per tile of the chunk
+  P.rs_expect = p.rs_bufs ? (p.rs_chunk_rows / (BM * CG)) * P.tiles_n * Layout<MX, CG, ST, KS, BF>::EPI_WARPS * CG : 0;
+  P.rs_epoch = p.rs_epoch;
   return true;
 }
 

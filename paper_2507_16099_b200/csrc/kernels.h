@@ -65,6 +65,8 @@ struct P2PSig {                        // tail of every rank's window, written b
   unsigned long long amax[P2P_MAXP];   // slot p: (epoch << 32) | amax bits of rank p's shard
   unsigned long long done[P2P_MAXP];   // slot p: last epoch whose pushes from rank p are visible
   unsigned int ctas;                   // local: finished CTAs of the running cast_push (last-CTA ticket)
+  unsigned int rs_cnt[P2P_MAXP];       // local: finished epilogue warps per D row chunk (fused reduce-scatter)
+  float scratch[4];                    // local: [0] = 0 (barrier payload), [1..2] barrier scale / amax sink
 };
 struct P2PPeers {
   uint8_t* buf[P2P_MAXP];              // every rank's gather buffer (peer pointers, UVA)
@@ -87,6 +89,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
 
 cudaError_t launch_transpose_u8(const uint8_t* in, int64_t R, int64_t C, uint8_t* out, cudaStream_t s);
 
+struct P2PSig;
 // tcgen05 GEMM: D[M,N] = A[M,K] B[N,K]^T with scales.
 //   scale_mode 0: tensor (sa[1], sb[1] float), 1: row (sa[M], sb[N] float), 2: MX (E8M0 blocked)
 struct GemmProblem {
@@ -109,6 +112,12 @@ struct GemmProblem {
   int chunk_rows = 0;
   int mrot = 0;
   unsigned chunk_epoch = 0;
+  // fused reduce-scatter of D over row chunks (see Prob in gemm_kernels.cu)
+  uint8_t* const* rs_bufs = nullptr;   // device table [P]: every rank's staging buffer
+  P2PSig* const* rs_sigs = nullptr;    // device table [P]: every rank's signal block
+  unsigned* rs_cnt = nullptr;          // local per-chunk counters (this rank's signal block)
+  int rs_rank = 0, rs_chunk_rows = 0, rs_expect = 0;
+  unsigned rs_epoch = 0;
 };
 constexpr int GEMM_MAX_GROUPS = 256;
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st);

@@ -15,6 +15,7 @@
 // after my epoch-e amax signal, which my stream issues after all my earlier work (the GEMMs that
 // read epoch e-1's codes).  Every spin has a 10 s watchdog (globaltimer) that traps instead of
 // hanging the GPU.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -25,6 +26,7 @@
 #include "comm.h"
 #include "fp8train.h"
 #include "kernels.h"
+#include "p2p_internal.h"
 #include "scale.cuh"
 
 namespace fp8t {
@@ -80,6 +82,35 @@ __global__ void p2p_wait_done_kernel(P2PSig* mine, int P, uint32_t epoch) {
   }
 }
 
+// Fused reduce-scatter, owner side (after p2p_wait_done_kernel saw every rank's done[p] >= epoch):
+// out = sum_p staging[p] in rank order, fp32, one bf16 rounding.
+__global__ void __launch_bounds__(256) p2p_rs_reduce_kernel(const uint4* __restrict__ staging, int P,
+                                                            int64_t rows, int64_t cols,
+                                                            __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  // (the arrival of every rank's tiles was awaited by p2p_wait_done_kernel just before, in stream order)
+  const int64_t vec_per_row = cols / 8, n = rows * vec_per_row, slot = rows * vec_per_row;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int p = 0; p < P; ++p) {
+      const uint4 v = __ldcg(staging + p * slot + i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[2 * j] += __uint_as_float(w[j] << 16);
+        acc[2 * j + 1] += __uint_as_float(w[j] & 0xFFFF0000u);
+      }
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
+      o[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    const int64_t r = i / vec_per_row, c = i - r * vec_per_row;
+    *reinterpret_cast<uint4*>(out + r * ldo + c * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 }  // namespace fp8t
 using namespace fp8t;
 
@@ -97,7 +128,18 @@ struct fp8_p2p_s {
   P2PPeers peers;
   std::vector<uint8_t*> opened;   // IPC-opened peer bases (to close)
   uint32_t epoch;
+  uint8_t** d_bufs = nullptr;      // device copies of peers.buf / peers.sig (read by the GEMM epilogue)
+  P2PSig** d_sigs = nullptr;
 };
+
+static fp8_status_t upload_tables(fp8_p2p_s* w) {
+  const size_t b = sizeof(void*) * (size_t)w->P;
+  fp8_status_t s = cuda_check(cudaMalloc(&w->d_bufs, b), "cudaMalloc (peer table)");
+  if (s == FP8_OK) s = cuda_check(cudaMalloc(&w->d_sigs, b), "cudaMalloc (peer table)");
+  if (s == FP8_OK) s = cuda_check(cudaMemcpy(w->d_bufs, w->peers.buf, b, cudaMemcpyHostToDevice), "cudaMemcpy");
+  if (s == FP8_OK) s = cuda_check(cudaMemcpy(w->d_sigs, w->peers.sig, b, cudaMemcpyHostToDevice), "cudaMemcpy");
+  return s;
+}
 
 static size_t sig_offset(size_t bytes) { return (bytes + 255) & ~size_t(255); }
 static size_t window_bytes(size_t bytes) { return sig_offset(bytes) + ((sizeof(P2PSig) + 255) & ~size_t(255)); }
@@ -171,7 +213,10 @@ fp8_status_t fp8_p2p_create(fp8_comm_t comm, size_t bytes, fp8_p2p_t* out) {
   if (nr != ncclSuccess) return bail(fail(FP8_ENCCL, "ncclAllReduce (barrier): %s", ncclGetErrorString(nr)));
   if ((s = cuda_check(cudaStreamSynchronize(st), "sync")) != FP8_OK) return bail(s);
   cudaFree(d);
+  d = nullptr;
   cudaStreamDestroy(st);
+  st = nullptr;
+  if ((s = upload_tables(w)) != FP8_OK) return bail(s);
   *out = w;
   return FP8_OK;
 }
@@ -202,6 +247,8 @@ fp8_status_t fp8_p2p_create_local(int nranks, size_t bytes, fp8_p2p_t* out) {
       w->peers.buf[p] = bases[p];
       w->peers.sig[p] = reinterpret_cast<P2PSig*>(bases[p] + sig_offset(bytes));
     }
+    fp8_status_t s = upload_tables(w);
+    if (s != FP8_OK) return s;
     out[r] = w;
   }
   return FP8_OK;
@@ -215,6 +262,8 @@ fp8_status_t fp8_p2p_destroy(fp8_p2p_t win) {
   for (uint8_t* p : win->opened)
     if (cudaIpcCloseMemHandle(p) != cudaSuccess) s = fail(FP8_ECUDA, "cudaIpcCloseMemHandle");
   if (cudaFree(win->base) != cudaSuccess) s = fail(FP8_ECUDA, "cudaFree (p2p window)");
+  if (win->d_bufs) cudaFree(win->d_bufs);
+  if (win->d_sigs) cudaFree(win->d_sigs);
   delete win;
   return s;
 }
@@ -397,3 +446,42 @@ fp8_status_t fp8_tp_allgather_linear_fwd_local(fp8_p2p_t* wins, int n, const fp8
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Fused GEMM -> reduce-scatter (used by fp8_linear_bwd_rs, abi.cpp)
+// ---------------------------------------------------------------------------
+namespace fp8t {
+
+fp8_status_t p2p_rs_begin(fp8_p2p_t win, int64_t chunk_rows, int64_t cols, cudaStream_t st, GemmProblem& p) {
+  if (!win) return fail(FP8_EINVAL, "rs window: null");
+  if (chunk_rows <= 0 || chunk_rows % 256 || cols % 16) return fail(FP8_EALIGN, "reduce-scatter: chunk rows % 256, cols % 16");
+  if ((size_t)win->P * (size_t)chunk_rows * (size_t)cols * 2 > win->bytes)
+    return fail(FP8_EINVAL, "rs window too small (needs nranks * chunk_rows * cols * 2 bytes)");
+  // barrier: every rank reached this call after its previous reduce (stream order), so no staging
+  // slot of the previous epoch is still being read when this epoch's tiles land
+  fp8_hp_t dummy{win->base, FP8_DT_BF16, 16, 16, 16};
+  FP8T_P2P_TRY(phase_signal(win, dummy, win->sig->scratch, nullptr, st));
+  FP8T_P2P_TRY(phase_wait_scale(win, FP8_E4M3, win->sig->scratch + 1, win->sig->scratch + 2, st));
+  p.rs_bufs = win->d_bufs;
+  p.rs_sigs = win->d_sigs;
+  p.rs_cnt = win->sig->rs_cnt;
+  p.rs_rank = win->rank;
+  p.rs_chunk_rows = (int)chunk_rows;
+  p.rs_epoch = win->epoch;
+  p.ldd = cols;
+  return FP8_OK;
+}
+
+fp8_status_t p2p_rs_end(fp8_p2p_t win, int64_t chunk_rows, int64_t cols, void* out, int64_t ldo, cudaStream_t st) {
+  FP8T_P2P_TRY(phase_wait_done(win, st));   // one spinning warp; the reduce below never spins
+  const int64_t n = chunk_rows * cols / 8;
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  LaunchScope ls(K_SYNC, st);
+  p2p_rs_reduce_kernel<<<(unsigned)g, 256, 0, st>>>(reinterpret_cast<const uint4*>(win->base), win->P, chunk_rows, cols,
+                                                    static_cast<__nv_bfloat16*>(out), ldo);
+  return cuda_check(cudaGetLastError(), "rs reduce");
+}
+
+}  // namespace fp8t
+

@@ -120,6 +120,20 @@ def gemm(A, fmt_a, sa, B, fmt_b, sb, gran="tensor", out_dtype=torch.bfloat16, a_
     return D
 
 
+def linear_backward_rs(plan, dy, saved, rs_win, dw_shard, dx=None, want_dx=True, w_fp8=None, x=None, stream=None):
+    """fp8_linear_bwd_rs: the backward with dW reduce-scattered to its row shards by the dW GEMM's
+    epilogue over the P2P window `rs_win` (fsdp.P2PWindow); dw_shard [N/nranks, K] bf16 receives this
+    rank's summed shard.  Returns dx."""
+    if want_dx and dx is None:
+        dx = torch.empty((plan.M, plan.K), dtype=plan.out_dtype, device=dy.device)
+    wq = plan._wq(w_fp8)
+    xh = hp(x) if x is not None else L.HP(None, L.DT_BF16, plan.M, plan.K, plan.K)
+    L.check(L.lib.fp8_linear_bwd_rs(ctypes.byref(plan.cfg), hp(dy), xh, _ptr(saved), ctypes.byref(wq) if wq else None,
+                                    _ptr(dx) if want_dx else None, rs_win._h, rs_win.world, _ptr(dw_shard),
+                                    _ptr(plan.ws), plan.ws_bytes, _stream(stream)), "fp8_linear_bwd_rs")
+    return dx
+
+
 def mx_scales_unshard(rank_major, nranks, rows_local, cols, out=None, stream=None):
     """fp8_mx_scales_unshard: nranks shard-local blocked dim1 E8M0 buffers ([cols, rows_local/32]
     each, concatenated) -> the blocked buffer of the full [cols, nranks*rows_local/32] matrix."""

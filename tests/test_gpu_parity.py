@@ -880,3 +880,16 @@ def test_tp_allgather_linear_simulated_ranks(P):
     finally:
         for w_ in wins:
             w_.close()
+
+
+def test_p2p_per_rank_calls_on_streams():
+    """The per-rank P2P entry points (FSDP gather, dW GEMM with fused reduce-scatter, async-TP forward),
+    P in {1, 2, 3} simulated ranks each on its own stream, in a child process with
+    CUDA_DEVICE_MAX_CONNECTIONS=32 (one hardware queue per stream); bit-exact references."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    child = os.path.join(os.path.dirname(__file__), "gpu_p2p_streams_child.py")
+    r = subprocess.run([sys.executable, child], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-3000:]
