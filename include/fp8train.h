@@ -429,6 +429,19 @@ fp8_status_t fp8_tp_allgather_linear_fwd(fp8_p2p_t win, const fp8_linear_cfg_t* 
 fp8_status_t fp8_linear_bwd_rs(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x, const void* saved,
                                const fp8_tensor_t* w_fp8, void* dx, fp8_p2p_t rs_win, int nranks,
                                void* dw_shard, void* ws, size_t ws_bytes, void* stream);
+/* Async-TP FP8 linear backward (pairs with fp8_tp_allgather_linear_fwd; "GEMM -> reduce-scatter"):
+ *   dy [M, N_local] (this rank's output columns, all M tokens), tensorwise local scale;
+ *   dw [N_local, K] bf16 = dY^T X_full using the FP8 X codes the forward gathered into `win`
+ *     (call before the next forward on `win`) and its global X scale (fwd_ws = the forward's ws);
+ *   dx_shard [M/nranks, K] bf16 = sum over ranks of (dY_r W_r)[this rank's token rows]: the dX
+ *     GEMM's epilogue stores each tile into the staging slot of the rank owning its rows (rs_win,
+ *     >= M * K * 2 bytes), which sums its nranks slots in rank order (fp32, one bf16 rounding).
+ * dX and dW share one persistent launch.  M % (256 * nranks) == 0; ws:
+ * fp8_tp_bwd_workspace_bytes(M, N_local) bytes (256-byte aligned). */
+size_t fp8_tp_bwd_workspace_bytes(int64_t M, int64_t n_local);
+fp8_status_t fp8_tp_linear_bwd(fp8_p2p_t win, const void* fwd_ws, fp8_p2p_t rs_win, const fp8_linear_cfg_t* cfg,
+                               fp8_hp_t dy, int64_t K, void* dx_shard, void* dw, void* ws, size_t ws_bytes,
+                               void* stream);
 /* Single-process form for a fp8_p2p_create_local group (phase by phase on one stream). */
 fp8_status_t fp8_tp_allgather_linear_fwd_local(fp8_p2p_t* wins, int nranks, const fp8_linear_cfg_t* cfg,
                                                const fp8_hp_t* x_shards, const fp8_hp_t* w, void* const* y,

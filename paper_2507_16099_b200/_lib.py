@@ -104,6 +104,9 @@ SIGNATURES = {
                                                      _c.c_size_t, _c.c_void_p]),
     "fp8_linear_bwd_rs": (_c.c_int, [_c.POINTER(LinearCfg), HP, HP, _c.c_void_p, _c.POINTER(Tensor8), _c.c_void_p,
                                      _c.c_void_p, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
+    "fp8_tp_bwd_workspace_bytes": (_c.c_size_t, [_c.c_int64, _c.c_int64]),
+    "fp8_tp_linear_bwd": (_c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_void_p, _c.POINTER(LinearCfg), HP, _c.c_int64,
+                                     _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
     "fp8_mx_scales_unshard": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),
 }
 AMAX_MULTI_MAX = 48

@@ -485,3 +485,55 @@ fp8_status_t p2p_rs_end(fp8_p2p_t win, int64_t chunk_rows, int64_t cols, void* o
 
 }  // namespace fp8t
 
+
+// ---------------------------------------------------------------------------
+// Async-TP FP8 linear backward (pairs with fp8_tp_allgather_linear_fwd): the row-parallel dX
+// partials are reduce-scattered to the token shards inside the GEMM (fused RS epilogue), dW_r is
+// local.  Per rank r:  dY_r [M, N_local] tensorwise cast (local scale) ->
+//   dX partial = dYq W_r (contraction over N_local) -> rows of token chunk c stored into rank c's
+//                staging (rs_win), summed there in rank order  -> dx_shard [M_local, K]
+//   dW_r       = dYq^T X_full (the FP8 codes gathered by the forward, still in win)
+// both problems in one persistent launch.
+// ---------------------------------------------------------------------------
+extern "C" {
+
+size_t fp8_tp_bwd_workspace_bytes(int64_t M, int64_t n_local) { return 1024 + (((size_t)M * n_local + 255) & ~size_t(255)); }
+
+fp8_status_t fp8_tp_linear_bwd(fp8_p2p_t win, const void* fwd_ws, fp8_p2p_t rs_win, const fp8_linear_cfg_t* cfg,
+                               fp8_hp_t dy, int64_t K, void* dx_shard, void* dw, void* ws, size_t ws_bytes,
+                               void* stream) {
+  if (!win || !rs_win || !fwd_ws || !cfg || !ws || !dx_shard || !dw) return fail(FP8_EINVAL, "null pointer");
+  if (cfg->recipe != FP8_RECIPE_TENSORWISE || cfg->out_dtype != FP8_DT_BF16)
+    return fail(FP8_EUNSUPPORTED, "async-TP backward: tensorwise recipe, bf16 outputs");
+  if (win->P != rs_win->P || win->rank != rs_win->rank) return fail(FP8_EINVAL, "win / rs_win: different groups");
+  const int64_t M = dy.rows, Nl = dy.cols, Ml = M / win->P;
+  if (M % ((int64_t)win->P * 256) || Nl % 16 || K % 16 || dy.ld < Nl) return fail(FP8_EALIGN, "shapes: M % (256 P), N, K % 16");
+  if ((size_t)M * K > win->bytes) return fail(FP8_EINVAL, "win does not hold the forward's gathered X");
+  if (ws_bytes < fp8_tp_bwd_workspace_bytes(M, Nl)) return fail(FP8_EWORKSPACE, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const TpWs t = carve_tp(const_cast<void*>(fwd_ws));
+  uint8_t* b = static_cast<uint8_t*>(ws);
+  float* amax_g = reinterpret_cast<float*>(b);
+  float* scale_g = reinterpret_cast<float*>(b + 256);
+  uint8_t* gq = b + 1024;
+  const bool gb = dy.dtype == FP8_DT_BF16;
+  const int ff = cfg->fmt_fwd, fg = cfg->fmt_grad;
+  fp8_status_t s;
+  if ((s = cuda_check(cudaMemsetAsync(amax_g, 0, 4, st), "memset")) != FP8_OK) return s;
+  if ((s = cuda_check(launch_amax(dy.ptr, gb, M, Nl, dy.ld, 1, reinterpret_cast<uint32_t*>(amax_g), nullptr, nullptr, st),
+                      "amax dy")) != FP8_OK)
+    return s;
+  if ((s = cuda_check(launch_cast(dy.ptr, gb, fg, M, Nl, dy.ld, 1, 0, amax_g, amax_g, gq, nullptr, scale_g, nullptr, st),
+                      "cast dy")) != FP8_OK)
+    return s;
+  GemmProblem ps[2];
+  // dW_r [Nl, K] = dY^T X_full: both MN-major (contraction over the M tokens)
+  ps[0] = GemmProblem{gq, win->base, fg, ff, 1, 1, scale_g, t.scale_x, 0, Nl, K, M, Nl, K, dw, 0, K};
+  // dX partial [M, K] = dY W_r: A K-major over Nl, B = W_r codes [Nl, K] read MN-major; reduce-scattered
+  ps[1] = GemmProblem{gq, t.wq, fg, ff, 0, 1, scale_g, t.scale_w, 0, M, K, Nl, Nl, K, dx_shard, 0, K};
+  FP8T_P2P_TRY(p2p_rs_begin(rs_win, Ml, K, st, ps[1]));
+  if ((s = cuda_check(launch_gemms(ps, 2, st), "tp bwd gemms")) != FP8_OK) return s;
+  return p2p_rs_end(rs_win, Ml, K, dx_shard, K, st);
+}
+
+}  // extern "C"

@@ -109,8 +109,8 @@ class Comm:
             self._h = ctypes.c_void_p()
 
 
-def _tp_cfg(fmt, out_dtype):
-    return L.LinearCfg(L.RECIPE_TENSORWISE, FORMATS[fmt], L.E5M2, L.MX_FLOOR,
+def _tp_cfg(fmt, out_dtype, fmt_grad="e5m2"):
+    return L.LinearCfg(L.RECIPE_TENSORWISE, FORMATS[fmt], FORMATS[fmt_grad], L.MX_FLOOR,
                        L.DT_F32 if out_dtype == torch.float32 else L.DT_BF16)
 
 
@@ -179,7 +179,24 @@ class P2PWindow:
             ws = torch.empty(wsb, dtype=torch.uint8, device=x_shard.device)
         L.check(L.lib.fp8_tp_allgather_linear_fwd(self._h, ctypes.byref(cfg), hp(x_shard), hp(w), _ptr(y), _ptr(ws), wsb,
                                                   _stream(stream)), "fp8_tp_allgather_linear_fwd")
+        self.last_tp_ws = ws   # the backward reads the forward's scales and W codes from it
         return y
+
+    def tp_linear_bwd(self, dy, fwd_ws, rs_win, K, dx_shard=None, dw=None, fmt_grad="e5m2", stream=None):
+        """Async-TP FP8 backward (fp8_tp_linear_bwd): returns (dx_shard [M/world, K], dw [N_local, K]) bf16;
+        fwd_ws = the ws tensor the matching tp_linear_fwd used; rs_win = a P2PWindow of >= M*K*2 bytes."""
+        M, Nl = dy.shape
+        dev = dy.device
+        if dx_shard is None:
+            dx_shard = torch.empty((M // self.world, K), dtype=torch.bfloat16, device=dev)
+        if dw is None:
+            dw = torch.empty((Nl, K), dtype=torch.bfloat16, device=dev)
+        cfg = _tp_cfg("e4m3", torch.bfloat16, fmt_grad)
+        wsb = L.lib.fp8_tp_bwd_workspace_bytes(M, Nl)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        L.check(L.lib.fp8_tp_linear_bwd(self._h, _ptr(fwd_ws), rs_win._h, ctypes.byref(cfg), hp(dy), K, _ptr(dx_shard),
+                                        _ptr(dw), _ptr(ws), wsb, _stream(stream)), "fp8_tp_linear_bwd")
+        return dx_shard, dw
 
     @staticmethod
     def tp_linear_fwd_local(wins, x_shards, ws_, out_dtype=torch.bfloat16, fmt="e4m3", stream=None):

@@ -32,6 +32,7 @@ def run(P):
     gwin = P2PWindow.local_group(P, N * K)
     rwin = P2PWindow.local_group(P, N * K * 2)
     twin = P2PWindow.local_group(P, P * Ml * K)
+    trwin = P2PWindow.local_group(P, P * Ml * K * 2)
     plans = [ops.LinearPlan(Ml, N, K, recipe="tensorwise") for _ in range(P)]
     saved = [p.new_saved() for p in plans]
     q_ref, s_ref, _ = fp8.cast_tensorwise(w_np, "e4m3")
@@ -75,7 +76,29 @@ def run(P):
         pl = ops.LinearPlan(P * Ml, 272, K, recipe="tensorwise", out_dtype=torch.float32)
         for r in range(P):
             assert torch.equal(ys[r], pl.forward(Xf, Wl[r], None)), f"tp rank {r}"
-    for w_ in gwin + rwin + twin:
+        # async-TP backward (fused dX reduce-scatter), per-rank calls on their own streams
+        dYs = [dev(synth.tensor_c2("dy", (P * Ml, 272), seed=90 + r + it)) for r in range(P)]
+        bw = [None] * P
+        torch.cuda.synchronize()
+        for r in range(P):
+            with torch.cuda.stream(streams[r]):
+                bw[r] = twin[r].tp_linear_bwd(dYs[r], twin[r].last_tp_ws, trwin[r], K)
+        torch.cuda.synchronize()
+        plb = ops.LinearPlan(P * Ml, 272, K, recipe="tensorwise")
+        parts = []
+        for r in range(P):
+            sv = plb.new_saved()
+            plb.forward(Xf, Wl[r], sv)
+            dxr, dwr = plb.backward(dYs[r], sv)
+            assert torch.equal(bw[r][1], dwr), f"tp dw rank {r}"
+            parts.append(dxr.float())
+        acc = parts[0].clone()
+        for f in parts[1:]:
+            acc += f
+        ref = acc.to(torch.bfloat16)
+        for r in range(P):
+            assert torch.equal(bw[r][0], ref[r * Ml:(r + 1) * Ml]), f"tp dx shard {r}"
+    for w_ in gwin + rwin + twin + trwin:
         w_.close()
 
 
