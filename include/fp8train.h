@@ -69,7 +69,7 @@
 extern "C" {
 #endif
 
-#define FP8TRAIN_ABI_VERSION 4
+#define FP8TRAIN_ABI_VERSION 5
 
 typedef enum {
   FP8_OK = 0,

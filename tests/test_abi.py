@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol(L):
 
 
 def test_abi_version(L):
-    assert L.lib.fp8_abi_version() == 4
+    assert L.lib.fp8_abi_version() == 5
 
 
 def test_sizes_host_only(L):
@@ -104,3 +104,42 @@ def test_product_path_has_no_oracle_dependency():
                 s = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in s.replace("no oracle", ""), f
                 assert "import numpy" not in s, f
+
+
+def test_argument_errors_return_before_any_launch(L):
+    """Documented error behaviour of the newer entry points: argument / shape checks return a status
+    (and a message) before anything touches the device, so they run here without a GPU.  Fake but
+    16-byte-aligned addresses stand in for device pointers (never dereferenced on these paths)."""
+    A = 0x100000
+    hp = lambda r, c: L.HP(A, L.DT_BF16, r, c, c)  # noqa: E731
+    cfg = L.LinearCfg(L.RECIPE_MXFP8, L.E4M3, L.E5M2, L.MX_FLOOR, L.DT_BF16)
+    ws = ctypes.c_void_p(A)
+    # grouped GEMM: MXFP8 is not a grouped recipe; T and N alignment
+    st = L.lib.fp8_grouped_linear_fwd(ctypes.byref(cfg), hp(256, 256), hp(512, 256), 2, ws, ws, ws, ws, 1 << 40, None)
+    assert st == L.FP8_EUNSUPPORTED and b"grouped" in L.lib.fp8_last_error()
+    cfg.recipe = L.RECIPE_ROWWISE
+    st = L.lib.fp8_grouped_linear_fwd(ctypes.byref(cfg), hp(272, 256), hp(512, 256), 2, ws, ws, ws, ws, 1 << 40, None)
+    assert st == L.FP8_EALIGN
+    st = L.lib.fp8_grouped_linear_fwd(ctypes.byref(cfg), hp(256, 256), hp(288, 256), 2, ws, ws, ws, ws, 1 << 40, None)
+    assert st == L.FP8_EALIGN   # N = 144 per expert
+    st = L.lib.fp8_grouped_linear_fwd(ctypes.byref(cfg), hp(256, 256), hp(512, 256), 300, ws, ws, ws, ws, 1 << 40, None)
+    assert st == L.FP8_EINVAL   # E > 256 (and w.rows % E != 0)
+    # fused reduce-scatter / async-TP: null windows
+    cfg.recipe = L.RECIPE_TENSORWISE
+    st = L.lib.fp8_linear_bwd_rs(ctypes.byref(cfg), hp(256, 256), hp(256, 256), ws, None, ws, None, 2, ws, ws, 1 << 40,
+                                 None)
+    assert st == L.FP8_EINVAL
+    st = L.lib.fp8_tp_linear_bwd(None, ws, None, ctypes.byref(cfg), hp(512, 256), 256, ws, ws, ws, 1 << 40, None)
+    assert st == L.FP8_EINVAL
+    # P2P windows: bad rank counts
+    arr = (ctypes.c_void_p * 1)()
+    assert L.lib.fp8_p2p_create_local(0, 1024, arr) == L.FP8_EINVAL
+    assert L.lib.fp8_p2p_create_local(65, 1024, arr) == L.FP8_EINVAL
+    assert L.lib.fp8_fsdp_allgather_p2p(None, hp(256, 256), L.E4M3, None, ws, ws, None) == L.FP8_EINVAL
+    # MX scale re-tiling: alignment
+    assert L.lib.fp8_mx_scales_unshard(ws, 2, 96, 256, ws, None) == L.FP8_EALIGN
+    assert L.lib.fp8_mx_scales_unshard(ctypes.c_void_p(A + 8), 2, 128, 256, ws, None) == L.FP8_EALIGN
+    # MX FSDP gather: only the row-major dim1 layout
+    t8 = L.Tensor8(A, A, A, A, None, None, L.E4M3, L.GRAN_MX32, 256, 256)
+    assert L.lib.fp8_fsdp_allgather_mx(ctypes.c_void_p(A), hp(128, 256), L.MX_FLOOR, ctypes.byref(t8), ws, 1 << 20,
+                                       None) == L.FP8_EUNSUPPORTED
