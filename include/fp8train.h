@@ -376,6 +376,13 @@ typedef struct fp8_p2p_s* fp8_p2p_t;
  * NCCL, open every peer's window (needs peer access: NVLink / NVSwitch).  One window
  * per concurrently live gathered weight; bytes >= nranks * rows_local * cols. */
 fp8_status_t fp8_p2p_create(fp8_comm_t comm, size_t bytes, fp8_p2p_t* win);
+/* The two halves of fp8_p2p_create for callers that exchange the handles themselves (e.g. over
+ * a torch gloo group): fp8_p2p_alloc allocates and zeroes this rank's window and returns its
+ * 64-byte CUDA IPC handle; after every rank's handle is known (handles = nranks x 64 bytes in rank
+ * order), fp8_p2p_open maps the peers.  The caller must then barrier (no rank may signal into a
+ * peer before that peer's fp8_p2p_alloc has returned). */
+fp8_status_t fp8_p2p_alloc(size_t bytes, int nranks, int rank, fp8_p2p_t* win, uint8_t handle[64]);
+fp8_status_t fp8_p2p_open(fp8_p2p_t win, const uint8_t* handles);
 /* Test / single-GPU form: nranks windows on the current device, wins[r] acting as rank
  * r, all mapped to each other (plain device pointers).  Drive it with
  * fp8_fsdp_allgather_p2p_local (one stream); per-rank calls on separate streams would

@@ -89,6 +89,8 @@ SIGNATURES = {
     "fp8_fsdp_allgather_mx": (_c.c_int, [_c.c_void_p, HP, _c.c_int, _c.POINTER(Tensor8), _c.c_void_p, _c.c_size_t,
                                          _c.c_void_p]),
     "fp8_p2p_create": (_c.c_int, [_c.c_void_p, _c.c_size_t, _c.POINTER(_c.c_void_p)]),
+    "fp8_p2p_alloc": (_c.c_int, [_c.c_size_t, _c.c_int, _c.c_int, _c.POINTER(_c.c_void_p), _c.c_void_p]),
+    "fp8_p2p_open": (_c.c_int, [_c.c_void_p, _c.c_void_p]),
     "fp8_p2p_create_local": (_c.c_int, [_c.c_int, _c.c_size_t, _c.POINTER(_c.c_void_p)]),
     "fp8_p2p_buffer": (_c.c_void_p, [_c.c_void_p]),
     "fp8_p2p_destroy": (_c.c_int, [_c.c_void_p]),

@@ -55,6 +55,7 @@ struct Prob {
   int out_f32, row_scales;
   int a_mn, b_mn;     // operand majors (MN-major: TMA boxes 128 MN x 128 K, K step 4 KB)
   uint32_t* out_amax; // optional: atomicMax of |D| bit patterns (amax of the stored output values)
+  int raster;         // tile raster of this problem (see tile_coords / choose_raster)
   // MoE grouped problems (scaled_grouped_mm): offs = device [G+1] row offsets
   //   grouped 1 (M-grouped, fwd / dX): group g owns rows [offs[g], offs[g+1]) of A, D and sa; B is
   //             expert g's block (K-major: rows g*N.., MN-major: K rows g*K..); sb index g*N + col
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
     ti.num_kb = P.num_kb;
     ti.katoms = 1 << 30;
     if (!GRP || P.grouped == 0) {
-      tile_coords(local, P.tiles_m, P.tiles_n, args.group_m, ti.mb, ti.nb);
+      tile_coords(local, P.tiles_m, P.tiles_n, P.raster, ti.mb, ti.nb);
       if (P.mrot) ti.mb = (ti.mb + P.mrot) % P.tiles_m;
       return ti;
     }
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
     if (P.grouped == 1) {
       const int* pre = gpre + ti.pi * (GMAX + 1);
       int mi;
-      tile_coords(local, pre[P.G], P.tiles_n, args.group_m, mi, ti.nb);
+      tile_coords(local, pre[P.G], P.tiles_n, P.raster, mi, ti.nb);
       int lo = 0, hi = P.G;   // pre[lo] <= mi < pre[hi]
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
     } else {
       const int per = P.tiles_m * P.tiles_n;
       g = local / per;
-      tile_coords(local - g * per, P.tiles_m, P.tiles_n, args.group_m, ti.mb, ti.nb);
+      tile_coords(local - g * per, P.tiles_m, P.tiles_n, P.raster, ti.mb, ti.nb);
       ti.a_k0 = o[g];
       ti.b_k0 = o[g];
       ti.katoms = (o[g + 1] - o[g]) / BK;
@@ -761,6 +762,24 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   return true;
 }
 
+// Tile raster of one problem.  The GEMMs here stream long K panels, so a wave of concurrent tiles
+// only shares the K slices it reads at the same time, unless one whole operand stays L2-resident:
+//   B (all N tiles x K) <= ~80 MB  -> row-major: every wave sweeps all N tiles of a few M tiles, B is
+//                                     read from DRAM once and A streams through once (C2's GEMMs);
+//   otherwise                      -> groups of GROUP_M M tiles sweep the N tiles (C4's GEMMs: measured
+//                                     10.6-10.8 ms/step vs 12.1 row-major; the DRAM traffic also sets the
+//                                     power-capped clock).
+// FP8T_GEMM_L2_MB overrides the residency budget.
+static int choose_raster(const GemmProblem& p, bool bf16) {
+  static const double budget = [] {
+    const char* e = getenv("FP8T_GEMM_L2_MB");
+    return (e ? atof(e) : 80.0) * 1e6;
+  }();
+  const double b_bytes = (double)((p.N + BN - 1) / BN * BN) * (double)p.K * (bf16 ? 2.0 : 1.0) *
+                         (p.grouped == 1 ? (double)p.G : 1.0);
+  return b_bytes <= budget ? 0 : GROUP_M;
+}
+
 template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false>
 static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   using L = Layout<MX, CG, ST, KS, BF, GRP>;
@@ -786,10 +805,11 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   {
     const char* d = getenv("FP8T_GEMM_DEBUG");
     a.debug = d ? atoi(d) : 0;
-    // raster: grouped (GROUP_M); FP8T_GEMM_RASTER overrides (0 = row-major).  Measured on the
-    // C2/C4 shapes: row-major and group sizes 8-32 are within run-to-run noise of each other.
+    // raster per problem (choose_raster); FP8T_GEMM_RASTER overrides for every problem
     const char* r = getenv("FP8T_GEMM_RASTER");
     a.group_m = r ? atoi(r) : GROUP_M;
+    a.p0.raster = r ? a.group_m : choose_raster(ps[0], BF);
+    a.p1.raster = r ? a.group_m : (n > 1 ? choose_raster(ps[1], BF) : a.p0.raster);
   }
   const int slots = num_sms() / CG;
   // grouped: the tile count depends on the device-side offsets -> a full persistent grid

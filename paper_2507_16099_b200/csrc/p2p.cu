@@ -152,71 +152,99 @@ static fp8_status_t alloc_window(size_t bytes, uint8_t** base) {
 
 extern "C" {
 
-fp8_status_t fp8_p2p_create(fp8_comm_t comm, size_t bytes, fp8_p2p_t* out) {
-  if (!comm || !out) return fail(FP8_EINVAL, "comm/out: null pointer");
+fp8_status_t fp8_p2p_alloc(size_t bytes, int nranks, int rank, fp8_p2p_t* out, uint8_t handle[64]) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t size");
+  if (!out || !handle) return fail(FP8_EINVAL, "out/handle: null pointer");
   if (bytes == 0) return fail(FP8_EINVAL, "bytes must be > 0");
-  if (comm->nranks > P2P_MAXP) return fail(FP8_EUNSUPPORTED, "p2p window: at most %d ranks", P2P_MAXP);
-  const int P = comm->nranks, r = comm->rank;
+  if (nranks < 1 || nranks > P2P_MAXP || rank < 0 || rank >= nranks)
+    return fail(FP8_EINVAL, "bad nranks / rank (at most %d ranks)", P2P_MAXP);
   uint8_t* base = nullptr;
   fp8_status_t s = alloc_window(bytes, &base);
   if (s != FP8_OK) return s;
+  cudaIpcMemHandle_t h;
+  if ((s = cuda_check(cudaIpcGetMemHandle(&h, base), "cudaIpcGetMemHandle")) != FP8_OK) {
+    cudaFree(base);
+    return s;
+  }
+  if ((s = cuda_check(cudaDeviceSynchronize(), "sync (window zeroed)")) != FP8_OK) {
+    cudaFree(base);
+    return s;
+  }
   auto* w = new fp8_p2p_s{};
-  w->P = P;
-  w->rank = r;
+  w->P = nranks;
+  w->rank = rank;
   w->bytes = bytes;
   w->base = base;
   w->sig = reinterpret_cast<P2PSig*>(base + sig_offset(bytes));
   w->epoch = 0;
-  w->peers.P = P;
-  w->peers.rank = r;
-  // exchange IPC handles over NCCL (device buffer of P handles, in-place all-gather)
-  cudaIpcMemHandle_t h;
-  std::vector<cudaIpcMemHandle_t> all(P);
+  w->peers.P = nranks;
+  w->peers.rank = rank;
+  std::memcpy(handle, &h, 64);
+  *out = w;
+  return FP8_OK;
+}
+
+fp8_status_t fp8_p2p_open(fp8_p2p_t w, const uint8_t* handles) {
+  if (!w || !handles) return fail(FP8_EINVAL, "win/handles: null pointer");
+  if (!w->opened.empty() || w->d_bufs) return fail(FP8_EINVAL, "window already opened");
+  fp8_status_t s;
+  for (int p = 0; p < w->P; ++p) {
+    uint8_t* pb = w->base;
+    if (p != w->rank) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + 64 * (size_t)p, 64);
+      void* ptr = nullptr;
+      if ((s = cuda_check(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess),
+                          "cudaIpcOpenMemHandle (peer window; needs P2P / NVLink)")) != FP8_OK) {
+        for (uint8_t* q : w->opened) cudaIpcCloseMemHandle(q);
+        w->opened.clear();
+        return s;
+      }
+      pb = static_cast<uint8_t*>(ptr);
+      w->opened.push_back(pb);
+    }
+    w->peers.buf[p] = pb;
+    w->peers.sig[p] = reinterpret_cast<P2PSig*>(pb + sig_offset(w->bytes));
+  }
+  return upload_tables(w);
+}
+
+fp8_status_t fp8_p2p_create(fp8_comm_t comm, size_t bytes, fp8_p2p_t* out) {
+  if (!comm || !out) return fail(FP8_EINVAL, "comm/out: null pointer");
+  if (comm->nranks > P2P_MAXP) return fail(FP8_EUNSUPPORTED, "p2p window: at most %d ranks", P2P_MAXP);
+  const int P = comm->nranks, r = comm->rank;
+  fp8_p2p_t w = nullptr;
+  std::vector<uint8_t> all(64 * (size_t)P);
+  fp8_status_t s = fp8_p2p_alloc(bytes, P, r, &w, all.data() + 64 * (size_t)r);
+  if (s != FP8_OK) return s;
+  // exchange the IPC handles over NCCL (device buffer of P handles, in-place all-gather)
   void* d = nullptr;
   cudaStream_t st = nullptr;
   auto bail = [&](fp8_status_t e) {
     if (d) cudaFree(d);
     if (st) cudaStreamDestroy(st);
-    for (uint8_t* p : w->opened) cudaIpcCloseMemHandle(p);
-    cudaFree(base);
-    delete w;
+    fp8_p2p_destroy(w);
     return e;
   };
-  if ((s = cuda_check(cudaIpcGetMemHandle(&h, base), "cudaIpcGetMemHandle")) != FP8_OK) return bail(s);
-  if ((s = cuda_check(cudaMalloc(&d, sizeof(h) * P), "cudaMalloc")) != FP8_OK) return bail(s);
+  if ((s = cuda_check(cudaMalloc(&d, 64 * (size_t)P), "cudaMalloc")) != FP8_OK) return bail(s);
   if ((s = cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate")) != FP8_OK)
     return bail(s);
-  if ((s = cuda_check(cudaMemcpy(static_cast<uint8_t*>(d) + sizeof(h) * r, &h, sizeof(h), cudaMemcpyHostToDevice),
-                      "cudaMemcpy")) != FP8_OK)
+  if ((s = cuda_check(cudaMemcpy(static_cast<uint8_t*>(d) + 64 * (size_t)r, all.data() + 64 * (size_t)r, 64,
+                                 cudaMemcpyHostToDevice), "cudaMemcpy")) != FP8_OK)
     return bail(s);
-  ncclResult_t nr = ncclAllGather(static_cast<uint8_t*>(d) + sizeof(h) * r, d, sizeof(h), ncclUint8, comm->nccl, st);
+  ncclResult_t nr = ncclAllGather(static_cast<uint8_t*>(d) + 64 * (size_t)r, d, 64, ncclUint8, comm->nccl, st);
   if (nr != ncclSuccess) return bail(fail(FP8_ENCCL, "ncclAllGather (ipc handles): %s", ncclGetErrorString(nr)));
   if ((s = cuda_check(cudaStreamSynchronize(st), "sync")) != FP8_OK) return bail(s);
-  if ((s = cuda_check(cudaMemcpy(all.data(), d, sizeof(h) * P, cudaMemcpyDeviceToHost), "cudaMemcpy")) != FP8_OK)
+  if ((s = cuda_check(cudaMemcpy(all.data(), d, 64 * (size_t)P, cudaMemcpyDeviceToHost), "cudaMemcpy")) != FP8_OK)
     return bail(s);
-  for (int p = 0; p < P; ++p) {
-    uint8_t* pb = base;
-    if (p != r) {
-      void* ptr = nullptr;
-      if ((s = cuda_check(cudaIpcOpenMemHandle(&ptr, all[p], cudaIpcMemLazyEnablePeerAccess),
-                          "cudaIpcOpenMemHandle (peer window; needs P2P / NVLink)")) != FP8_OK)
-        return bail(s);
-      pb = static_cast<uint8_t*>(ptr);
-      w->opened.push_back(pb);
-    }
-    w->peers.buf[p] = pb;
-    w->peers.sig[p] = reinterpret_cast<P2PSig*>(pb + sig_offset(bytes));
-  }
+  if ((s = fp8_p2p_open(w, all.data())) != FP8_OK) return bail(s);
   // every window is zeroed and mapped before anyone signals into it
   int* one = static_cast<int*>(d);
   nr = ncclAllReduce(one, one, 1, ncclInt32, ncclSum, comm->nccl, st);
   if (nr != ncclSuccess) return bail(fail(FP8_ENCCL, "ncclAllReduce (barrier): %s", ncclGetErrorString(nr)));
   if ((s = cuda_check(cudaStreamSynchronize(st), "sync")) != FP8_OK) return bail(s);
   cudaFree(d);
-  d = nullptr;
   cudaStreamDestroy(st);
-  st = nullptr;
-  if ((s = upload_tables(w)) != FP8_OK) return bail(s);
   *out = w;
   return FP8_OK;
 }

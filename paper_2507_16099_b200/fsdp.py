@@ -137,6 +137,23 @@ class P2PWindow:
         self.nbytes = nbytes
 
     @classmethod
+    def over_group(cls, nbytes, group=None):
+        """Collective over a torch process group (any backend, e.g. gloo): fp8_p2p_alloc, all-gather the
+        64-byte CUDA IPC handles through torch.distributed, fp8_p2p_open, barrier.  No NCCL involved."""
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        h = ctypes.c_void_p()
+        mine = (ctypes.c_uint8 * 64)()
+        L.check(L.lib.fp8_p2p_alloc(nbytes, world, rank, ctypes.byref(h), mine), "fp8_p2p_alloc")
+        allh = [None] * world
+        dist.all_gather_object(allh, bytes(mine), group=group)
+        buf = (ctypes.c_uint8 * (64 * world))(*b"".join(allh))
+        L.check(L.lib.fp8_p2p_open(h, buf), "fp8_p2p_open")
+        dist.barrier(group=group)
+        w = cls(_handle=h, world=world, rank=rank)
+        w.nbytes = nbytes
+        return w
+
+    @classmethod
     def local_group(cls, nranks, nbytes):
         """nranks windows on this GPU mapped to each other (single-GPU simulation of the ranks; issue
         each rank's gather on its own stream)."""

@@ -893,3 +893,25 @@ def test_p2p_per_rank_calls_on_streams():
     child = os.path.join(os.path.dirname(__file__), "gpu_p2p_streams_child.py")
     r = subprocess.run([sys.executable, child], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-3000:]
+
+
+def test_p2p_two_processes_ipc():
+    """Two OS processes on one GPU, P2P windows mapped with real CUDA IPC handles (exchanged over gloo):
+    FSDP gather, fused dW reduce-scatter and async-TP fwd/bwd across the process boundary (the contexts
+    time-slice the GPU, so cross-rank waits also exercise preemption of spinning kernels)."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    child = os.path.join(os.path.dirname(__file__), "gpu_ipc_2proc_child.py")
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, child], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=600) for p in procs]
+    for r, (p, (o, e)) in enumerate(zip(procs, outs)):
+        assert p.returncode == 0 and f"rank {r} ok" in o, o[-1500:] + e[-3000:]
