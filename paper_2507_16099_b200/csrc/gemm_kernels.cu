@@ -87,6 +87,8 @@ struct GemmArgs {
   int t1, num_tiles;
   int group_m;        // tile raster (see tile_coords)
   int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
+  int sf_split;       // MX: scale-factor copies issued by their own warp (see the SF copier)
+  int sf_batch;       // MX: stages per batch of scale-factor copies
 };
 
 template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false> struct Layout {
@@ -106,7 +108,7 @@ template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false> st
   static constexpr uint32_t off_sfb = off_sfa + STAGES * SFA_STAGE;
   static constexpr uint32_t off_epi = off_sfb + STAGES * SFB_STAGE;   // 2 KB bf16 staging per epilogue warp
   static constexpr uint32_t off_bar = off_epi + EPI_WARPS * 2048;
-  static constexpr uint32_t n_bar = 2 * STAGES + 2 * ACC;
+  static constexpr uint32_t n_bar = 2 * STAGES + 2 * ACC + (MX ? 2 * STAGES : 0);   // MX: + sf_bar, sf_full
   static constexpr uint32_t off_tmem = off_bar + 8 * n_bar;
   // grouped: per problem the group offsets and the prefix of M tiles (ints, 2 x 2 x (GMAX + 1))
   static constexpr uint32_t off_grp = off_tmem + 16;
@@ -119,7 +121,8 @@ template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false> st
   static constexpr uint32_t SF_COLS = 12 * KS;
   static constexpr uint32_t sfa_col = 256, sfb_col = 256 + 4 * KS;
   static_assert(!MX || 256 + STAGES * SF_COLS <= 512, "TMEM columns");
-  static constexpr uint32_t tx_bytes = CG * (A_STAGE + B_STAGE + SFA_STAGE + SFB_STAGE);  // counted on the leader
+  static constexpr uint32_t tx_bytes = CG * (A_STAGE + B_STAGE);   // operands, counted on the leader
+  static constexpr uint32_t sf_tx_bytes = CG * (SFA_STAGE + SFB_STAGE);   // MX scale tiles (sf_full)
 };
 
 // Where one output tile of a (possibly grouped) problem lives.
@@ -168,6 +171,8 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
   const uint32_t empty_bar = full_bar + 8 * STAGES;            // [STAGES]
   const uint32_t tfull_bar = empty_bar + 8 * STAGES;           // [ACC]
   const uint32_t tempty_bar = tfull_bar + 8 * L::ACC;          // [ACC]    (leader counts both CTAs)
+  const uint32_t sf_bar = tempty_bar + 8 * L::ACC;             // [STAGES] MX: stage's scales are in TMEM
+  const uint32_t sf_full = sf_bar + 8 * STAGES;                // [STAGES] MX: stage's scale tiles in smem
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L::off_tmem);
 
   const int warp = threadIdx.x >> 5;
@@ -283,8 +288,13 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
     }
     for (int a = 0; a < L::ACC; ++a) {
       mbar_init(tfull_bar + 8 * a, 1);
-      mbar_init(tempty_bar + 8 * a, CG * 32 * L::EPI_WARPS);
+      mbar_init(tempty_bar + 8 * a, CG * L::EPI_WARPS);   // one arrival per epilogue warp
     }
+    if (MX)
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(sf_bar + 8 * s, 1);
+        mbar_init(sf_full + 8 * s, CG);
+      }
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -306,6 +316,35 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
     num_tiles = t1 + (args.num_tiles > args.t1 ? count(args.p1, 1) : 0);
   }
 
+  // MX: copy a stage's E8M0 tiles smem -> TMEM (tcgen05.cp; 3 copies of 512 B per K atom, each
+  // replicated into the 4 TMEM lane quadrants).  Every stage has its own TMEM columns.
+  auto copy_sf = [&](int st, uint32_t tmem_base) {
+    const uint32_t ssa = base + L::off_sfa + st * L::SFA_STAGE;
+    const uint32_t ssb = base + L::off_sfb + st * L::SFB_STAGE;
+#pragma unroll
+    for (int t = 0; t < KS; ++t) {
+      const uint32_t ca = tmem_base + L::sfa_col + st * L::SF_COLS + 4 * t;
+      const uint32_t cb0 = tmem_base + L::sfb_col + st * L::SF_COLS + 8 * t, cb1 = cb0 + 4;
+      if (CG == 2) {
+        tmem_cp_32x128b_warpx4_cg2(ca, make_sf_desc(ssa + t * SF_CHUNK));
+        tmem_cp_32x128b_warpx4_cg2(cb0, make_sf_desc(ssb + t * SF_CHUNK));
+        tmem_cp_32x128b_warpx4_cg2(cb1, make_sf_desc(ssb + (KS + t) * SF_CHUNK));
+      } else {
+        tmem_cp_32x128b_warpx4(ca, make_sf_desc(ssa + t * SF_CHUNK));
+        tmem_cp_32x128b_warpx4(cb0, make_sf_desc(ssb + t * SF_CHUNK));
+        tmem_cp_32x128b_warpx4(cb1, make_sf_desc(ssb + (KS + t) * SF_CHUNK));
+      }
+    }
+  };
+  // sf_split: a separate SF-copier warp issues the copies and commits them to sf_bar[stage]; the MMA
+  // warp waits on that barrier.  Measured: when one thread interleaves tcgen05.cp with its MMAs,
+  // every cp -> MMA transition costs ~800-1000 cycles (the cost scales with the number of
+  // transitions, not of copies), i.e. ~40 % of an 8-MMA stage; tcgen05 ops of different threads
+  // are not ordered with each other, so the copier's copies overlap the MMAs in flight.
+  // WAR on the stage's TMEM columns: full_bar[stage] of this round implies the producer refilled the
+  // slot after empty_bar[stage], i.e. after the MMAs that read the previous round's scales completed.
+  const bool sf_split = MX && args.sf_split && !(args.debug & 2);
+
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     int stage = 0;
@@ -321,8 +360,9 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
       const int a_mn = P.a_mn, b_mn = P.b_mn;
       const int m0 = mb * BM * CG + (int)crank * BM;
       const int n0 = nb * BN + (int)crank * (BN / CG);
-      // debug bit 2: skip the MX scale-factor loads (timing experiments only; results invalid)
-      const uint32_t tx = L::tx_bytes - ((MX && (args.debug & 4)) ? CG * (L::SFA_STAGE + L::SFB_STAGE) : 0);
+      // debug bit 4: skip the MX scale-factor loads (timing experiments only; results invalid)
+      const uint32_t tx = L::tx_bytes;
+      const uint32_t sf_tx = (args.debug & 4) ? 0u : L::sf_tx_bytes;
       const int KT = P.sf_tiles_k;
       const int num_kb = ti.num_kb;
       if (P.chunk_done) {   // async-TP: wait until the rank that owns these A rows has pushed them
@@ -343,6 +383,33 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(empty_bar + 8 * stage, phase ^ 1);
         if (lane == 0) {
+          // MX: E8M0 tiles first, on their own barrier: they land long before the operands, so the SF
+          // copier has them in TMEM by the time the MMA warp sees full_bar
+          const uint32_t sfb = sf_full + 8 * stage;
+          if (MX) {
+            if (CG == 2) {
+              if (leader) mbar_arrive_expect_tx(sfb, sf_tx);
+              else mbar_arrive_cluster(mapa_shared(sfb, 0));
+            } else {
+              mbar_arrive_expect_tx(sfb, sf_tx);
+            }
+          }
+          if (MX && !(args.debug & 4)) {
+            // E8M0 tiles: SF tensor = [row_block * KT + k_atom][512 B]; boxes of KS consecutive atoms
+            const int kt0 = kb * KS;
+            const uint32_t dsa = base + L::off_sfa + stage * L::SFA_STAGE;
+            const uint32_t dsb = base + L::off_sfb + stage * L::SFB_STAGE;
+            const int rba = mb * CG + (int)crank;   // this CTA's 128-row block of A
+            if (CG == 2) {
+              tma_load_2d_2sm(dsa, tmSFA, 0, rba * KT + kt0, sfb);
+              tma_load_2d_2sm(dsb, tmSFB, 0, (2 * nb) * KT + kt0, sfb);
+              tma_load_2d_2sm(dsb + KS * SF_CHUNK, tmSFB, 0, (2 * nb + 1) * KT + kt0, sfb);
+            } else {
+              tma_load_2d(dsa, tmSFA, 0, rba * KT + kt0, sfb, 0);
+              tma_load_2d(dsb, tmSFB, 0, (2 * nb) * KT + kt0, sfb, 0);
+              tma_load_2d(dsb + KS * SF_CHUNK, tmSFB, 0, (2 * nb + 1) * KT + kt0, sfb, 0);
+            }
+          }
           const uint32_t fb = full_bar + 8 * stage;
           const uint32_t sa_dst = base + L::off_a + stage * L::A_STAGE;
           const uint32_t sb_dst = base + L::off_b + stage * L::B_STAGE;
@@ -383,22 +450,6 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
               }
             }
           }
-          if (MX && !(args.debug & 4)) {
-            // E8M0 tiles: SF tensor = [row_block * KT + k_atom][512 B]; boxes of KS consecutive atoms
-            const int kt0 = kb * KS;
-            const uint32_t dsa = base + L::off_sfa + stage * L::SFA_STAGE;
-            const uint32_t dsb = base + L::off_sfb + stage * L::SFB_STAGE;
-            const int rba = mb * CG + (int)crank;   // this CTA's 128-row block of A
-            if (CG == 2) {
-              tma_load_2d_2sm(dsa, tmSFA, 0, rba * KT + kt0, fb);
-              tma_load_2d_2sm(dsb, tmSFB, 0, (2 * nb) * KT + kt0, fb);
-              tma_load_2d_2sm(dsb + KS * SF_CHUNK, tmSFB, 0, (2 * nb + 1) * KT + kt0, fb);
-            } else {
-              tma_load_2d(dsa, tmSFA, 0, rba * KT + kt0, fb, 0);
-              tma_load_2d(dsb, tmSFB, 0, (2 * nb) * KT + kt0, fb, 0);
-              tma_load_2d(dsb + KS * SF_CHUNK, tmSFB, 0, (2 * nb + 1) * KT + kt0, fb, 0);
-            }
-          }
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -420,25 +471,15 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(full_bar + 8 * stage, phase);
+        if (sf_split) mbar_wait(sf_bar + 8 * stage, phase);
+        else if (MX) mbar_wait(sf_full + 8 * stage, phase);
         tc_fence_after();
         if (lane == 0) {
-          if (MX && !(args.debug & 2)) {   // this stage's scale factors -> TMEM (in order with the MMAs that follow)
-            const uint32_t ssa = base + L::off_sfa + stage * L::SFA_STAGE;
-            const uint32_t ssb = base + L::off_sfb + stage * L::SFB_STAGE;
-#pragma unroll
-            for (int t = 0; t < KS; ++t) {
-              const uint32_t ca = tmem_base + L::sfa_col + stage * L::SF_COLS + 4 * t;
-              const uint32_t cb0 = tmem_base + L::sfb_col + stage * L::SF_COLS + 8 * t, cb1 = cb0 + 4;
-              if (CG == 2) {
-                tmem_cp_32x128b_warpx4_cg2(ca, make_sf_desc(ssa + t * SF_CHUNK));
-                tmem_cp_32x128b_warpx4_cg2(cb0, make_sf_desc(ssb + t * SF_CHUNK));
-                tmem_cp_32x128b_warpx4_cg2(cb1, make_sf_desc(ssb + (KS + t) * SF_CHUNK));
-              } else {
-                tmem_cp_32x128b_warpx4(ca, make_sf_desc(ssa + t * SF_CHUNK));
-                tmem_cp_32x128b_warpx4(cb0, make_sf_desc(ssb + t * SF_CHUNK));
-                tmem_cp_32x128b_warpx4(cb1, make_sf_desc(ssb + (KS + t) * SF_CHUNK));
-              }
-            }
+          // debug bits 16/32/64 (timing experiments only; results invalid): duplicate every stage's
+          // copies / copy on every 2nd / every 4th stage only
+          if (MX && !sf_split && !(args.debug & 2) && !((args.debug & 32) && (kb & 1)) && !((args.debug & 64) && (kb & 3))) {
+            copy_sf(stage, tmem_base);
+            if (args.debug & 16) copy_sf(stage, tmem_base);
           }
           const uint32_t sa_src = base + L::off_a + stage * L::A_STAGE;
           const uint32_t sb_src = base + L::off_b + stage * L::B_STAGE;
@@ -491,6 +532,36 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
       }
       if (++acc == L::ACC) { acc = 0; acc_phase ^= 1; }
     }
+  } else if (MX && warp == 3 && leader && sf_split) {
+    // ---------------- SF copier (leader CTA, MX) ----------------
+    // sf_batch > 1: the copies of sf_batch consecutive stages are issued back to back (fewer
+    // copy <-> MMA transitions in the tensor pipe), at the cost of the MMAs of the first stage of a
+    // batch waiting until the batch's last stage has landed.
+    const int batch = args.sf_batch < 1 ? 1 : (args.sf_batch > STAGES - 1 ? STAGES - 1 : args.sf_batch);
+    int stage = 0, npend = 0, pend0 = 0;
+    uint32_t phase = 0;
+    auto flush = [&]() {
+      if (lane == 0) {
+        for (int i = 0, st = pend0; i < npend; ++i, st = st + 1 == STAGES ? 0 : st + 1) copy_sf(st, tmem_base);
+        for (int i = 0, st = pend0; i < npend; ++i, st = st + 1 == STAGES ? 0 : st + 1) {
+          if (CG == 2) mma_commit_cg2_mc(sf_bar + 8 * st, 0x1);
+          else mma_commit(sf_bar + 8 * st);
+        }
+      }
+      __syncwarp();
+      npend = 0;
+    };
+    for (int tile = cta_slot; tile < num_tiles; tile += cta_stride) {
+      const int num_kb = locate(tile).num_kb;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(sf_full + 8 * stage, phase);
+        tc_fence_after();
+        if (npend == 0) pend0 = stage;
+        if (++npend == batch) flush();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    if (npend) flush();
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs, own 128 accumulator lanes) ----------------
     // EPIW = 4: one warp per TMEM lane quadrant, 8 chunks of 32 columns, TMEM released after the
@@ -597,8 +668,11 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
         for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tbase + half * 128 + c * 32, r[c]);
         tmem_wait_ld();
         tc_fence_before();   // TMEM drained: release it to the MMA warp before the stores
-        if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * acc);
-        else mbar_arrive(tempty_bar + 8 * acc);
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * acc);
+          else mbar_arrive(tempty_bar + 8 * acc);
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c) process(r[c], nb * BN + half * 128 + c * 32);
       } else {
@@ -610,8 +684,11 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
           process(r, nb * BN + c * 32);
         }
         tc_fence_before();
-        if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * acc);
-        else mbar_arrive(tempty_bar + 8 * acc);
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * acc);
+          else mbar_arrive(tempty_bar + 8 * acc);
+        }
       }
       if (P.out_amax) {   // (P is uniform across the CTA; every lane reaches this point)
         dmax = __reduce_max_sync(0xffffffffu, dmax);
@@ -805,6 +882,10 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   {
     const char* d = getenv("FP8T_GEMM_DEBUG");
     a.debug = d ? atoi(d) : 0;
+    const char* sf = getenv("FP8T_MX_SF_SPLIT");
+    a.sf_split = sf ? atoi(sf) : 1;
+    const char* sfb = getenv("FP8T_MX_SF_BATCH");
+    a.sf_batch = sfb ? atoi(sfb) : 1;
     // raster per problem (choose_raster); FP8T_GEMM_RASTER overrides for every problem
     const char* r = getenv("FP8T_GEMM_RASTER");
     a.group_m = r ? atoi(r) : GROUP_M;
