@@ -88,7 +88,6 @@ struct GemmArgs {
   int group_m;        // tile raster (see tile_coords)
   int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
   int sf_split;       // MX: scale-factor copies issued by their own warp (see the SF copier)
-  int sf_batch;       // MX: stages per batch of scale-factor copies
 };
 
 template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false> struct Layout {
@@ -534,34 +533,24 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
     }
   } else if (MX && warp == 3 && leader && sf_split) {
     // ---------------- SF copier (leader CTA, MX) ----------------
-    // sf_batch > 1: the copies of sf_batch consecutive stages are issued back to back (fewer
-    // copy <-> MMA transitions in the tensor pipe), at the cost of the MMAs of the first stage of a
-    // batch waiting until the batch's last stage has landed.
-    const int batch = args.sf_batch < 1 ? 1 : (args.sf_batch > STAGES - 1 ? STAGES - 1 : args.sf_batch);
-    int stage = 0, npend = 0, pend0 = 0;
+    // (batching the copies of two stages behind one wait was measured slower: the MMAs of the
+    // batch's first stage then wait for its second stage to land)
+    int stage = 0;
     uint32_t phase = 0;
-    auto flush = [&]() {
-      if (lane == 0) {
-        for (int i = 0, st = pend0; i < npend; ++i, st = st + 1 == STAGES ? 0 : st + 1) copy_sf(st, tmem_base);
-        for (int i = 0, st = pend0; i < npend; ++i, st = st + 1 == STAGES ? 0 : st + 1) {
-          if (CG == 2) mma_commit_cg2_mc(sf_bar + 8 * st, 0x1);
-          else mma_commit(sf_bar + 8 * st);
-        }
-      }
-      __syncwarp();
-      npend = 0;
-    };
     for (int tile = cta_slot; tile < num_tiles; tile += cta_stride) {
       const int num_kb = locate(tile).num_kb;
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(sf_full + 8 * stage, phase);
         tc_fence_after();
-        if (npend == 0) pend0 = stage;
-        if (++npend == batch) flush();
+        if (lane == 0) {
+          copy_sf(stage, tmem_base);
+          if (CG == 2) mma_commit_cg2_mc(sf_bar + 8 * stage, 0x1);
+          else mma_commit(sf_bar + 8 * stage);
+        }
+        __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-    if (npend) flush();
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs, own 128 accumulator lanes) ----------------
     // EPIW = 4: one warp per TMEM lane quadrant, 8 chunks of 32 columns, TMEM released after the
@@ -884,8 +873,6 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     a.debug = d ? atoi(d) : 0;
     const char* sf = getenv("FP8T_MX_SF_SPLIT");
     a.sf_split = sf ? atoi(sf) : 1;
-    const char* sfb = getenv("FP8T_MX_SF_BATCH");
-    a.sf_batch = sfb ? atoi(sfb) : 1;
     // raster per problem (choose_raster); FP8T_GEMM_RASTER overrides for every problem
     const char* r = getenv("FP8T_GEMM_RASTER");
     a.group_m = r ? atoi(r) : GROUP_M;
