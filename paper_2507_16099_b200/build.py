@@ -64,7 +64,8 @@ def build(verbose=False, force=False):
         objs.append(obj)
         if not force and not _stale(obj, [src] + headers):
             continue
-        cmd = [nvcc] + ARCH + NVFLAGS + ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
+        extra = os.environ.get("FP8T_NVCC_EXTRA", "").split()   # experiments, e.g. -DFP8T_EPI_WARPS_ACC2=4
+        cmd = [nvcc] + ARCH + NVFLAGS + extra + ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
                                          "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd))

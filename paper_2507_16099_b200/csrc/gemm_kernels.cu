@@ -90,10 +90,10 @@ struct GemmArgs {
   int sf_split;       // MX: scale-factor copies issued by their own warp (see the SF copier)
 };
 
-template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false> struct Layout {
+template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bool E8 = false> struct Layout {
   static constexpr int STAGES = ST;
   static constexpr int ACC = MX ? 1 : 2;
-  static constexpr int EPI_WARPS = ACC == 1 ? 8 : 4;        // see the epilogue
+  static constexpr int EPI_WARPS = E8 || ACC == 1 ? 8 : 4;   // see the epilogue
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   // a stage holds KS 128-byte K atoms (16 KB sub-tiles of 128 rows each)
   static constexpr uint32_t A_STAGE = BM * BK * KS;         // 16 KB x KS
@@ -150,8 +150,8 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nb = local / gsz;
 }
 
-template <bool MX, int CG, int ST, int KS, bool BF, bool GRP>
-__global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
+template <bool MX, int CG, int ST, int KS, bool BF, bool GRP, bool E8>
+__global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 1)
     fp8_gemm_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tB0,
                     const __grid_constant__ CUtensorMap tSA0, const __grid_constant__ CUtensorMap tSB0,
                     const __grid_constant__ CUtensorMap tA1, const __grid_constant__ CUtensorMap tB1,
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
   static_assert(KS == 1 || CG == 2, "multi-atom stages need the CTA-pair kernel");
   static_assert(!BF || (CG == 2 && KS == 2 && !MX), "BF16 operands: CTA-pair, 2-atom stages");
   static_assert(!GRP || (!MX && !BF), "grouped problems: plain FP8 kinds");
-  using L = Layout<MX, CG, ST, KS, BF, GRP>;
+  using L = Layout<MX, CG, ST, KS, BF, GRP, E8>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -555,9 +555,11 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP>::THREADS, 1)
     // ---------------- epilogue (both CTAs, own 128 accumulator lanes) ----------------
     // EPIW = 4: one warp per TMEM lane quadrant, 8 chunks of 32 columns, TMEM released after the
     //           tile (the other accumulator buffer keeps the MMAs busy meanwhile).
-    // EPIW = 8 (single-accumulator MX kernel): two warps per quadrant, 128 columns each, loaded into
-    //           registers and TMEM released BEFORE scaling/storing, so the next tile's MMAs start
-    //           after the TMEM drain instead of after the whole epilogue.
+    // EPIW = 8 (single-accumulator MX kernel; short-K launches): two warps per quadrant, 128 columns
+    //           each, loaded into registers and TMEM released BEFORE scaling/storing, so the next
+    //           tile's MMAs start after the TMEM drain instead of after the whole epilogue, and twice
+    //           the warps share the stores.  Measured (tools/mx_probe.py, flop/clk/SM): K = 1024
+    //           (Llama-3-8B wk/wv dX) 7.5k -> 8.6k with 8 warps; K >= 4096 shapes 1-2 % better with 4.
     constexpr int EPIW = L::EPI_WARPS;
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int half = EPIW == 8 ? ((warp - 4) >> 2) : 0;
@@ -776,7 +778,7 @@ static bool make_sf_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool MX, int CG, int ST, int KS, bool BF>
+template <bool MX, int CG, int ST, int KS, bool BF, bool GRP, bool E8>
 static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   // grouped 1: B holds G experts (K-major: G*N rows; MN-major: G*K contraction rows)
   const int64_t bN = p.grouped == 1 && !p.b_mn ? p.G * p.N : p.N;
@@ -823,7 +825,7 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   P.rs_rank = p.rs_rank;
   P.rs_chunk_rows = p.rs_chunk_rows;
   // every epilogue warp of both CTAs of a pair arrives once per tile of the chunk
-  P.rs_expect = p.rs_bufs ? (p.rs_chunk_rows / (BM * CG)) * P.tiles_n * Layout<MX, CG, ST, KS, BF>::EPI_WARPS * CG : 0;
+  P.rs_expect = p.rs_bufs ? (p.rs_chunk_rows / (BM * CG)) * P.tiles_n * Layout<MX, CG, ST, KS, BF, GRP, E8>::EPI_WARPS * CG : 0;
   P.rs_epoch = p.rs_epoch;
   return true;
 }
@@ -846,22 +848,22 @@ static int choose_raster(const GemmProblem& p, bool bf16) {
   return b_bytes <= budget ? 0 : GROUP_M;
 }
 
-template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false>
+template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bool E8 = false>
 static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
-  using L = Layout<MX, CG, ST, KS, BF, GRP>;
+  using L = Layout<MX, CG, ST, KS, BF, GRP, E8>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP>,
+    attr_err = cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
   });
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m0[4], m1[4];
   GemmArgs a{};
-  if (!setup_prob<MX, CG, ST, KS, BF>(ps[0], a.p0, m0)) return cudaErrorInvalidValue;
+  if (!setup_prob<MX, CG, ST, KS, BF, GRP, E8>(ps[0], a.p0, m0)) return cudaErrorInvalidValue;
   a.t1 = a.p0.tiles_m * a.p0.tiles_n;
   if (n > 1) {
-    if (!setup_prob<MX, CG, ST, KS, BF>(ps[1], a.p1, m1)) return cudaErrorInvalidValue;
+    if (!setup_prob<MX, CG, ST, KS, BF, GRP, E8>(ps[1], a.p1, m1)) return cudaErrorInvalidValue;
     a.num_tiles = a.t1 + a.p1.tiles_m * a.p1.tiles_n;
   } else {
     a.p1 = a.p0;
@@ -884,7 +886,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   const int grid = GRP ? CG * slots : CG * (a.num_tiles < slots ? a.num_tiles : slots);
   LaunchScope ls(MX ? K_GEMM_MX : (BF ? K_GEMM_BF16 : K_GEMM), st);
   if (CG == 1) {
-    fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP><<<grid, L::THREADS, L::bytes, st>>>(m0[0], m0[1], m0[2], m0[3], m1[0], m1[1],
+    fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8><<<grid, L::THREADS, L::bytes, st>>>(m0[0], m0[1], m0[2], m0[3], m1[0], m1[1],
                                                                       m1[2], m1[3], a);
   } else {
     cudaLaunchConfig_t cfg{};
@@ -899,7 +901,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP>, m0[0], m0[1], m0[2], m0[3], m1[0],
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8>, m0[0], m0[1], m0[2], m0[3], m1[0],
                                        m1[1], m1[2], m1[3], a);
     if (e != cudaSuccess) return e;
   }
@@ -932,7 +934,12 @@ cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st) {
   const char* e = getenv("FP8T_GEMM_STAGES");
   if (e && e[0] == '6') return launch_t<false, 2, 6, 1>(ps, n, st);
   if (e && e[0] == '4') return launch_t<false, 2, 4, 1>(ps, n, st);
-  return launch_t<false, 2, 3, 2>(ps, n, st);
+  // short-K launches (tiles of <= 2048-deep K) are epilogue-bound: 8 epilogue warps
+  bool short_k = false;
+  for (int i = 0; i < n; ++i) short_k = short_k || ps[i].K <= 2048;
+  const char* ew = getenv("FP8T_GEMM_EPI");
+  if (ew) short_k = ew[0] == '8';
+  return short_k ? launch_t<false, 2, 3, 2, false, false, true>(ps, n, st) : launch_t<false, 2, 3, 2>(ps, n, st);
 }
 
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st) { return launch_gemms(&p, 1, st); }

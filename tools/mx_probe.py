@@ -12,7 +12,7 @@ import time
 import pynvml
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("FP8T_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2507_16099_b200 import ops  # noqa: E402
 
 pynvml.nvmlInit()
