@@ -39,6 +39,11 @@ P2PWindow.allgather_local(wins, [W[:N // 2].contiguous(), W[N // 2:].contiguous(
 torch.cuda.synchronize()
 for w_ in wins:
     w_.close()
+# long-K plain GEMM (4 epilogue warps; the short-K launches above use 8)
+A8 = torch.randint(0, 0x70, (256, 2304), dtype=torch.uint8, device="cuda")
+B8 = torch.randint(0, 0x70, (256, 2304), dtype=torch.uint8, device="cuda")
+one = torch.ones(1, device="cuda")
+ops.gemm(A8, "e4m3", one, B8, "e4m3", one, "tensor")
 slots = [ops.cast(W[r * 128:(r + 1) * 128].contiguous(), "e4m3", "mx32_rm", want_q=True, want_qt=True) for r in range(3)]
 ops.mx_scales_unshard(torch.cat([s["scale_t"] for s in slots]), 3, 128, K)
 torch.cuda.synchronize()
