@@ -32,6 +32,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <mutex>
 
 #include "kernels.h"
@@ -43,6 +44,13 @@ constexpr int BM = 128, BN = 256, BK = 128;   // per-CTA M rows, MMA N, K atom (
 constexpr int SF_CHUNK = 512;                 // E8M0 tile: 128 rows x 4 K-blocks of 32 (one K atom)
 constexpr int GROUP_M = 16;                   // grouped raster: 16 M-tiles share the N sweep
 constexpr int GMAX = GEMM_MAX_GROUPS;         // MoE grouped GEMM: groups per problem
+constexpr int SD = 8;                         // depth of a CTA pair's tile-index ring (see the scheduler)
+constexpr int SCHED_SLOTS = 4096;             // launches in flight that may share the counter array
+
+// Dynamic tile scheduler state: [slot][0] = next dynamic tile, [slot][1] = pairs done fetching.  Every
+// launch takes its own slot (host-side round robin); the last pair to finish fetching resets both, so a
+// slot is zero again when it is reused.  Module-global device memory: no allocation in any call.
+__device__ unsigned g_sched[SCHED_SLOTS][2];
 
 // One GEMM problem of a (possibly two-problem) launch.
 struct Prob {
@@ -88,6 +96,7 @@ struct GemmArgs {
   int group_m;        // tile raster (see tile_coords)
   int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
   int sf_split;       // MX: scale-factor copies issued by their own warp (see the SF copier)
+  unsigned* sched;    // dynamic tile scheduler slot (g_sched[i]); null: static round robin
 };
 
 template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bool E8 = false> struct Layout {
@@ -107,10 +116,11 @@ template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bo
   static constexpr uint32_t off_sfb = off_sfa + STAGES * SFA_STAGE;
   static constexpr uint32_t off_epi = off_sfb + STAGES * SFB_STAGE;   // 2 KB bf16 staging per epilogue warp
   static constexpr uint32_t off_bar = off_epi + EPI_WARPS * 2048;
-  static constexpr uint32_t n_bar = 2 * STAGES + 2 * ACC + (MX ? 2 * STAGES : 0);   // MX: + sf_bar, sf_full
+  static constexpr uint32_t n_bar = 2 * STAGES + 2 * ACC + (MX ? 2 * STAGES : 0) + 2 * SD;   // MX: + sf_bar, sf_full; + sched_full, sched_empty
   static constexpr uint32_t off_tmem = off_bar + 8 * n_bar;
   // grouped: per problem the group offsets and the prefix of M tiles (ints, 2 x 2 x (GMAX + 1))
-  static constexpr uint32_t off_grp = off_tmem + 16;
+  static constexpr uint32_t off_ring = off_tmem + 16;      // [SD] tile indices published by the pair's scheduler
+  static constexpr uint32_t off_grp = off_ring + 4 * SD;
   static constexpr uint32_t grp_bytes = GRP ? 16 * (GMAX + 1) : 0;
   static constexpr uint32_t bytes = off_grp + grp_bytes + 1024;  // + alignment slack
   static constexpr uint32_t tmem_cols = 512;
@@ -172,12 +182,16 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
   const uint32_t tempty_bar = tfull_bar + 8 * L::ACC;          // [ACC]    (leader counts both CTAs)
   const uint32_t sf_bar = tempty_bar + 8 * L::ACC;             // [STAGES] MX: stage's scales are in TMEM
   const uint32_t sf_full = sf_bar + 8 * STAGES;                // [STAGES] MX: stage's scale tiles in smem
+  const uint32_t sched_full = sf_full + (MX ? 8 * STAGES : 0);  // [SD] ring slot holds the next tile index
+  const uint32_t sched_empty = sched_full + 8 * SD;            // [SD] (leader) every consumer has read it
+  const uint32_t ring = base + L::off_ring;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L::off_tmem);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;
   const bool leader = crank == 0;
+  const bool sf_split = MX && args.sf_split && !(args.debug & 2);   // (see the SF copier)
   const int cta_slot = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // pair / CTA index
   const int cta_stride = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
@@ -294,6 +308,13 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
         mbar_init(sf_bar + 8 * s, 1);
         mbar_init(sf_full + 8 * s, CG);
       }
+    // consumers of the tile sequence: MMA warp (+ SF copier) and epilogue warps of the leader, plus the
+    // peer's producer and epilogue warps; the leader's producer is the scheduler itself
+    const uint32_t consumers = 1 + (sf_split ? 1 : 0) + L::EPI_WARPS + (CG == 2 ? 1 + L::EPI_WARPS : 0);
+    for (int i = 0; i < SD; ++i) {
+      mbar_init(sched_full + 8 * i, 1);
+      mbar_init(sched_empty + 8 * i, consumers);
+    }
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -342,13 +363,81 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
   // are not ordered with each other, so the copier's copies overlap the MMAs in flight.
   // WAR on the stage's TMEM columns: full_bar[stage] of this round implies the producer refilled the
   // slot after empty_bar[stage], i.e. after the MMAs that read the previous round's scales completed.
-  const bool sf_split = MX && args.sf_split && !(args.debug & 2);
+  // Tile sequence of this CTA (pair).  Persistent CTAs take tiles from a scheduler: the leader's
+  // producer publishes each tile index into slot k % SD of both CTAs' rings (sched_full) before loading
+  // it; every other role reads the same sequence from its own CTA's ring and releases the slot on the
+  // leader (sched_empty).  Index >= num_tiles ends the sequence.  The first tile of a pair is its slot
+  // index; later ones come from a global atomic counter (args.sched) in tile order -- the host puts the
+  // problem with the longer K first, so long tiles are handed out first and short ones fill the gaps
+  // (dynamic, LPT-like) -- or, with args.sched == null, round robin (tile += pairs).
+  auto seq_get = [&](int& k) -> int {
+    const int slot = k & (SD - 1);
+    const uint32_t ph = (uint32_t)(k / SD) & 1u;
+    ++k;
+    mbar_wait_acq_cluster(sched_full + 8 * slot, ph);
+    const int t = ld_volatile_shared_s32(ring + 4 * slot);
+    __syncwarp();
+    if (lane == 0) {
+      if (CG == 2 && !leader) mbar_arrive_cluster(mapa_shared(sched_empty + 8 * slot, 0));
+      else mbar_arrive(sched_empty + 8 * slot);
+    }
+    return t;
+  };
+  auto seq_put = [&](int& k, int t) {   // leader producer
+    const int slot = k & (SD - 1);
+    const uint32_t ph = (uint32_t)(k / SD) & 1u;
+    ++k;
+    mbar_wait(sched_empty + 8 * slot, ph ^ 1u);
+    if (lane == 0) {
+      asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(ring + 4 * slot), "r"(t) : "memory");
+      if (CG == 2) {
+        st_shared_cluster_u32(mapa_shared(ring + 4 * slot, 1), (uint32_t)t);
+        mbar_arrive_release_cluster(mapa_shared(sched_full + 8 * slot, 1));
+      }
+      mbar_arrive(sched_full + 8 * slot);
+    }
+    __syncwarp();
+  };
+  // leader producer: the tile after t.  sched_fetch issues lane 0's atomic when tile t's loads start;
+  // sched_next consumes its result after them (the atomic's latency hides behind the loads).
+  auto sched_fetch = [&]() -> unsigned { return (lane == 0 && args.sched) ? atomicAdd(args.sched, 1u) : 0u; };
+  auto sched_next = [&](int t, unsigned fetched) -> int {
+    int nt = 0;
+    if (lane == 0) {
+      if (args.sched) {
+        nt = cta_stride + (int)fetched;
+        if (nt >= num_tiles && atomicAdd(args.sched + 1, 1u) == (unsigned)cta_stride - 1) {
+          atomicExch(args.sched, 0u);   // every pair has done its last fetch: reset the slot
+          atomicExch(args.sched + 1, 0u);
+        }
+      } else {
+        nt = t + cta_stride;
+      }
+    }
+    return __shfl_sync(0xffffffffu, nt, 0);
+  };
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = cta_slot; tile < num_tiles; tile += cta_stride) {
+    int sk = 0;
+    int tile = cta_slot;
+    if (leader && args.sched && tile >= num_tiles && lane == 0 &&   // (grouped grids: a pair with no tile)
+        atomicAdd(args.sched + 1, 1u) == (unsigned)cta_stride - 1) {
+      atomicExch(args.sched, 0u);
+      atomicExch(args.sched + 1, 0u);
+    }
+    for (;;) {
+      unsigned fetched = 0;
+      if (leader) {
+        seq_put(sk, tile);
+        if (tile >= num_tiles) break;
+        fetched = sched_fetch();
+      } else {
+        tile = seq_get(sk);
+        if (tile >= num_tiles) break;
+      }
       const TileInfo ti = locate(tile);
       const int pi = ti.pi, mb = ti.mb, nb = ti.nb;
       const Prob& P = pi ? args.p1 : args.p0;
@@ -453,6 +542,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (leader) tile = sched_next(tile, fetched);
     }
   } else if (warp == 1 && leader) {
     // ---------------- MMA issuer (leader CTA) ----------------
@@ -460,7 +550,9 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = cta_slot; tile < num_tiles; tile += cta_stride) {
+    for (int sk = 0;;) {
+      const int tile = seq_get(sk);
+      if (tile >= num_tiles) break;
       const TileInfo ti = locate(tile);
       const Prob& P = ti.pi ? args.p1 : args.p0;
       const int a_mn = P.a_mn, b_mn = P.b_mn, num_kb = ti.num_kb;
@@ -537,7 +629,9 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
     // batch's first stage then wait for its second stage to land)
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = cta_slot; tile < num_tiles; tile += cta_stride) {
+    for (int sk = 0;;) {
+      const int tile = seq_get(sk);
+      if (tile >= num_tiles) break;
       const int num_kb = locate(tile).num_kb;
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(sf_full + 8 * stage, phase);
@@ -567,7 +661,9 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(tempty_bar, 0) : tempty_bar;
     uint8_t* epi = gbase + L::off_epi + (warp - 4) * 2048;   // this warp's bf16 staging slot
-    for (int tile = cta_slot; tile < num_tiles; tile += cta_stride) {
+    for (int sk = 0;;) {
+      const int tile = seq_get(sk);
+      if (tile >= num_tiles) break;
       const TileInfo ti = locate(tile);
       const int mb = ti.mb, nb = ti.nb;
       const Prob& P = ti.pi ? args.p1 : args.p0;
@@ -848,6 +944,22 @@ static int choose_raster(const GemmProblem& p, bool bf16) {
   return b_bytes <= budget ? 0 : GROUP_M;
 }
 
+// This launch's slot of g_sched on the current device (round robin over SCHED_SLOTS).
+static unsigned* sched_slot() {
+  static std::atomic<unsigned*> base[64];
+  static std::atomic<unsigned> next_slot{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  unsigned* b = base[dev].load();
+  if (!b) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_sched) != cudaSuccess) return nullptr;
+    b = static_cast<unsigned*>(p);
+    base[dev].store(b);
+  }
+  return b + 2 * (next_slot.fetch_add(1) % SCHED_SLOTS);
+}
+
 template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bool E8 = false>
 static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   using L = Layout<MX, CG, ST, KS, BF, GRP, E8>;
@@ -860,6 +972,14 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m0[4], m1[4];
   GemmArgs a{};
+  // longer-K problem first: the dynamic scheduler then hands out the long tiles before the short ones
+  GemmProblem q[2];
+  q[0] = ps[0];
+  if (n > 1) {
+    q[1] = ps[1];
+    if (!GRP && ps[1].K > ps[0].K) { q[0] = ps[1]; q[1] = ps[0]; }
+  }
+  ps = q;
   if (!setup_prob<MX, CG, ST, KS, BF, GRP, E8>(ps[0], a.p0, m0)) return cudaErrorInvalidValue;
   a.t1 = a.p0.tiles_m * a.p0.tiles_n;
   if (n > 1) {
@@ -873,6 +993,12 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   {
     const char* d = getenv("FP8T_GEMM_DEBUG");
     a.debug = d ? atoi(d) : 0;
+    // FP8T_GEMM_SCHED=static: round-robin tiles (A/B); default: dynamic scheduler
+    const char* sc = getenv("FP8T_GEMM_SCHED");
+    if (!(sc && sc[0] == 's')) {
+      a.sched = sched_slot();
+      if (!a.sched) return cudaErrorInvalidValue;
+    }
     const char* sf = getenv("FP8T_MX_SF_SPLIT");
     a.sf_split = sf ? atoi(sf) : 1;
     // raster per problem (choose_raster); FP8T_GEMM_RASTER overrides for every problem

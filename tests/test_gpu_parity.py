@@ -213,17 +213,22 @@ def _grid_operands(M, N, K, seed=0):
     return a, b
 
 
-@pytest.fixture(params=["2", "2e4", "2s6", "1"], ids=["cta_pair", "cta_pair_epi4", "cta_pair_1atom", "single_cta"])
+@pytest.fixture(params=["2", "2e4", "2rr", "2s6", "1"],
+                ids=["cta_pair", "cta_pair_epi4", "cta_pair_roundrobin", "cta_pair_1atom", "single_cta"])
 def cta_group(request, monkeypatch):
     """Run a GEMM test with each kernel variant: CTA pair (cta_group::2) with 2-atom stages
-    (default: 8 epilogue warps at these short K), the same with 4 epilogue warps (the long-K
-    default), CTA pair with 1-atom stages, single CTA."""
+    (default: 8 epilogue warps at these short K, dynamic tile scheduler), the same with 4 epilogue
+    warps (the long-K default), with static round-robin tiles, CTA pair with 1-atom stages, single CTA."""
     monkeypatch.setenv("FP8T_GEMM_CTA_GROUP", request.param[0])
     monkeypatch.setenv("FP8T_GEMM_STAGES", "6" if request.param == "2s6" else "3")
     if request.param == "2e4":
         monkeypatch.setenv("FP8T_GEMM_EPI", "4")
     else:
         monkeypatch.delenv("FP8T_GEMM_EPI", raising=False)
+    if request.param == "2rr":   # static round-robin tiles instead of the dynamic scheduler
+        monkeypatch.setenv("FP8T_GEMM_SCHED", "static")
+    else:
+        monkeypatch.delenv("FP8T_GEMM_SCHED", raising=False)
     return request.param
 
 
