@@ -116,8 +116,16 @@ template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bo
   static constexpr uint32_t off_sfb = off_sfa + STAGES * SFA_STAGE;
   static constexpr uint32_t off_epi = off_sfb + STAGES * SFB_STAGE;   // 2 KB bf16 staging per epilogue warp
   static constexpr uint32_t off_bar = off_epi + EPI_WARPS * 2048;
-  static constexpr uint32_t n_bar = 2 * STAGES + 2 * ACC + (MX ? 2 * STAGES : 0) + 2 * SD;   // MX: + sf_bar, sf_full; + sched_full, sched_empty
-  static constexpr uint32_t off_tmem = off_bar + 8 * n_bar;
+  // mbarriers (8 B each), in this order from off_bar; the kernel takes every address from these offsets
+  static constexpr uint32_t off_full = off_bar;                                 // [STAGES]
+  static constexpr uint32_t off_empty = off_full + 8 * STAGES;                  // [STAGES]
+  static constexpr uint32_t off_tfull = off_empty + 8 * STAGES;                 // [ACC]
+  static constexpr uint32_t off_tempty = off_tfull + 8 * ACC;                   // [ACC]
+  static constexpr uint32_t off_sf_bar = off_tempty + 8 * ACC;                  // [STAGES] (MX only)
+  static constexpr uint32_t off_sf_full = off_sf_bar + (MX ? 8 * STAGES : 0);   // [STAGES] (MX only)
+  static constexpr uint32_t off_sched_full = off_sf_full + (MX ? 8 * STAGES : 0);   // [SD]
+  static constexpr uint32_t off_sched_empty = off_sched_full + 8 * SD;         // [SD]
+  static constexpr uint32_t off_tmem = off_sched_empty + 8 * SD;
   // grouped: per problem the group offsets and the prefix of M tiles (ints, 2 x 2 x (GMAX + 1))
   static constexpr uint32_t off_ring = off_tmem + 16;      // [SD] tile indices published by the pair's scheduler
   static constexpr uint32_t off_grp = off_ring + 4 * SD;
@@ -176,14 +184,14 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const uint32_t full_bar = base + L::off_bar;                 // [STAGES]  (leader counts both CTAs)
-  const uint32_t empty_bar = full_bar + 8 * STAGES;            // [STAGES]
-  const uint32_t tfull_bar = empty_bar + 8 * STAGES;           // [ACC]
-  const uint32_t tempty_bar = tfull_bar + 8 * L::ACC;          // [ACC]    (leader counts both CTAs)
-  const uint32_t sf_bar = tempty_bar + 8 * L::ACC;             // [STAGES] MX: stage's scales are in TMEM
-  const uint32_t sf_full = sf_bar + 8 * STAGES;                // [STAGES] MX: stage's scale tiles in smem
-  const uint32_t sched_full = sf_full + (MX ? 8 * STAGES : 0);  // [SD] ring slot holds the next tile index
-  const uint32_t sched_empty = sched_full + 8 * SD;            // [SD] (leader) every consumer has read it
+  const uint32_t full_bar = base + L::off_full;                // [STAGES]  (leader counts both CTAs)
+  const uint32_t empty_bar = base + L::off_empty;              // [STAGES]
+  const uint32_t tfull_bar = base + L::off_tfull;              // [ACC]
+  const uint32_t tempty_bar = base + L::off_tempty;            // [ACC]    (leader counts both CTAs)
+  const uint32_t sf_bar = base + L::off_sf_bar;                // [STAGES] MX: stage's scales are in TMEM
+  const uint32_t sf_full = base + L::off_sf_full;              // [STAGES] MX: stage's scale tiles in smem
+  const uint32_t sched_full = base + L::off_sched_full;        // [SD] ring slot holds the next tile index
+  const uint32_t sched_empty = base + L::off_sched_empty;      // [SD] (leader) every consumer has read it
   const uint32_t ring = base + L::off_ring;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L::off_tmem);
 
@@ -375,10 +383,11 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
     const uint32_t ph = (uint32_t)(k / SD) & 1u;
     ++k;
     mbar_wait_acq_cluster(sched_full + 8 * slot, ph);
-    const int t = ld_volatile_shared_s32(ring + 4 * slot);
-    __syncwarp();
+    int t = 0;
+    if (lane == 0) t = ld_volatile_shared_s32(ring + 4 * slot);
+    t = __shfl_sync(0xffffffffu, t, 0);   // the read has completed before the slot is released
     if (lane == 0) {
-      if (CG == 2 && !leader) mbar_arrive_cluster(mapa_shared(sched_empty + 8 * slot, 0));
+      if (CG == 2 && !leader) mbar_arrive_release_cluster(mapa_shared(sched_empty + 8 * slot, 0));
       else mbar_arrive(sched_empty + 8 * slot);
     }
     return t;

@@ -36,16 +36,18 @@ def probe(fn, flops, seconds=1.5):
                             pynvml.nvmlDeviceGetPowerUsage(H) / 1000.0))
             time.sleep(0.005)
 
-    th = threading.Thread(target=sample)
+    th = threading.Thread(target=sample, daemon=True)
     th.start()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(n):
-        fn()
-    b.record()
-    torch.cuda.synchronize()
-    stop.set()
-    th.join()
+    try:
+        a.record()
+        for _ in range(n):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+    finally:
+        stop.set()
+        th.join()
     ms = a.elapsed_time(b) / n
     clk = sorted(s[0] for s in samples) or [0]
     pw = sorted(s[1] for s in samples) or [0]
