@@ -925,3 +925,37 @@ def test_p2p_two_processes_ipc():
     outs = [p.communicate(timeout=600) for p in procs]
     for r, (p, (o, e)) in enumerate(zip(procs, outs)):
         assert p.returncode == 0 and f"rank {r} ok" in o, o[-1500:] + e[-3000:]
+
+
+@pytest.mark.parametrize("epi", ["8", "4"])
+def test_gemm_scheduler_long_launch_sequence(epi, monkeypatch):
+    """> 4096 back-to-back GEMM launches without a host sync (the dynamic tile scheduler's counter slots
+    wrap around; slots are reset by each launch's last pair), mixing tensorwise, MXFP8 and two-problem
+    launches: every launch's output stays bit-identical to the first one's (each tile is computed by
+    one CTA pair in a fixed K order, so the bits do not depend on the schedule)."""
+    monkeypatch.setenv("FP8T_GEMM_EPI", epi)
+    monkeypatch.delenv("FP8T_GEMM_SCHED", raising=False)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    M, N, K = 768, 1024, 512
+    A = torch.randint(0, 0x70, (M, K), dtype=torch.uint8, device="cuda", generator=g)
+    B = torch.randint(0, 0x70, (N, K), dtype=torch.uint8, device="cuda", generator=g)
+    sfa = torch.randint(118, 128, (M * K // 32,), dtype=torch.uint8, device="cuda", generator=g)
+    sfb = torch.randint(118, 128, (N * K // 32,), dtype=torch.uint8, device="cuda", generator=g)
+    s = torch.full((1,), 0.5, device="cuda")
+    ref_t = ops.gemm(A, "e4m3", s, B, "e4m3", s, "tensor").clone()
+    ref_m = ops.gemm(A, "e4m3", sfa, B, "e4m3", sfb, "mx32").clone()
+    outs_t, outs_m = [], []
+    for i in range(4400):
+        if i % 2 == 0:
+            D = ops.gemm(A, "e4m3", s, B, "e4m3", s, "tensor")
+            if i % 1100 == 0:
+                outs_t.append(D)
+        else:
+            D = ops.gemm(A, "e4m3", sfa, B, "e4m3", sfb, "mx32")
+            if i % 1100 == 1:
+                outs_m.append(D)
+    torch.cuda.synchronize()
+    for D in outs_t:
+        assert torch.equal(D.view(torch.int16), ref_t.view(torch.int16))
+    for D in outs_m:
+        assert torch.equal(D.view(torch.int16), ref_m.view(torch.int16))
