@@ -458,7 +458,8 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
       const int m0 = mb * BM * CG + (int)crank * BM;
       const int n0 = nb * BN + (int)crank * (BN / CG);
       // debug bit 4: skip the MX scale-factor loads (timing experiments only; results invalid)
-      const uint32_t tx = L::tx_bytes;
+      // debug bit 256 (timing experiment, results invalid): no operand loads, the stage completes on arrivals
+      const uint32_t tx = (args.debug & 256) ? 0u : L::tx_bytes;
       const uint32_t sf_tx = (args.debug & 4) ? 0u : L::sf_tx_bytes;
       const int KT = P.sf_tiles_k;
       const int num_kb = ti.num_kb;
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
           // K-major boxes: (k, row); MN-major boxes: (mn, k), one per 128-wide MN atom.
           // K atom j of this stage starts at k0 = (kb*KS + j)*BK; atoms are 16 KB apart in smem.
 #pragma unroll
-          for (int j = 0; j < KS; ++j) {
+          for (int j = 0; j < ((args.debug & 256) ? 0 : KS); ++j) {
             // FP8: atom j = K bytes [(kb*KS + j)*128, +128) (MN-major: 128 K rows of 128 MN bytes).
             // BF16: K-major atom j = K elements [(kb*KS + j)*64, +64); MN-major: the stage covers
             // 128 K rows and atom j is MN elements [mn0 + 64j, +64).
@@ -559,17 +560,29 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int sk = 0;;) {
-      const int tile = seq_get(sk);
-      if (tile >= num_tiles) break;
-      const TileInfo ti = locate(tile);
+    // The next tile's index and coordinates are fetched two stages before the current tile's last
+    // MMAs are issued, so that bookkeeping overlaps MMAs already queued in the tensor pipe.
+    int sk = 0;
+    int tile = seq_get(sk);
+    TileInfo ti{};
+    if (tile < num_tiles) ti = locate(tile);
+    while (tile < num_tiles) {
       const Prob& P = ti.pi ? args.p1 : args.p0;
       const int a_mn = P.a_mn, b_mn = P.b_mn, num_kb = ti.num_kb;
       const uint32_t idesc = P.idesc;
+      int next = 0;
+      bool have_next = false;
+      TileInfo nti{};
+      auto fetch_next = [&]() {
+        next = seq_get(sk);
+        if (next < num_tiles) nti = locate(next);
+        have_next = true;
+      };
       mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = 0; kb < num_kb; ++kb) {
+        if (!have_next && kb + 2 >= num_kb) fetch_next();
         mbar_wait(full_bar + 8 * stage, phase);
         if (sf_split) mbar_wait(sf_bar + 8 * stage, phase);
         else if (MX) mbar_wait(sf_full + 8 * stage, phase);
@@ -630,7 +643,10 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
         }
         __syncwarp();
       }
+      if (!have_next) fetch_next();
       if (++acc == L::ACC) { acc = 0; acc_phase ^= 1; }
+      tile = next;
+      ti = nti;
     }
   } else if (MX && warp == 3 && leader && sf_split) {
     // ---------------- SF copier (leader CTA, MX) ----------------
@@ -662,7 +678,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
     //           each, loaded into registers and TMEM released BEFORE scaling/storing, so the next
     //           tile's MMAs start after the TMEM drain instead of after the whole epilogue, and twice
     //           the warps share the stores.  Measured (tools/mx_probe.py, flop/clk/SM): K = 1024
-    //           (Llama-3-8B wk/wv dX) 7.5k -> 8.6k with 8 warps; K >= 4096 shapes 1-2 % better with 4.
+    //           (Llama-3-8B wk/wv dX) 7.5k -> 8.6k with 8 warps; K >= 2048 shapes 1-7 % better with 4.
     constexpr int EPIW = L::EPI_WARPS;
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int half = EPIW == 8 ? ((warp - 4) >> 2) : 0;
@@ -758,7 +774,14 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
       mbar_wait(tfull_bar + 8 * acc, acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if (EPIW == 8) {
+      if (args.debug & 8) {   // timing experiment (results invalid): release the accumulator untouched
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * acc);
+          else mbar_arrive(tempty_bar + 8 * acc);
+        }
+      } else if (EPIW == 8) {
         uint32_t r[4][32];
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tbase + half * 128 + c * 32, r[c]);
@@ -1069,9 +1092,10 @@ cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st) {
   const char* e = getenv("FP8T_GEMM_STAGES");
   if (e && e[0] == '6') return launch_t<false, 2, 6, 1>(ps, n, st);
   if (e && e[0] == '4') return launch_t<false, 2, 4, 1>(ps, n, st);
-  // short-K launches (tiles of <= 2048-deep K) are epilogue-bound: 8 epilogue warps
+  // short-K launches (tiles of <= 1024-deep K) are epilogue-bound: 8 epilogue warps (measured: K = 1024
+  // 7.5k -> 8.6k flop/clk/SM; K = 2048 10.6k with 4 warps vs 9.9k with 8)
   bool short_k = false;
-  for (int i = 0; i < n; ++i) short_k = short_k || ps[i].K <= 2048;
+  for (int i = 0; i < n; ++i) short_k = short_k || ps[i].K <= 1024;
   const char* ew = getenv("FP8T_GEMM_EPI");
   if (ew) short_k = ew[0] == '8';
   return short_k ? launch_t<false, 2, 3, 2, false, false, true>(ps, n, st) : launch_t<false, 2, 3, 2>(ps, n, st);

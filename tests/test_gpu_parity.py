@@ -217,7 +217,7 @@ def _grid_operands(M, N, K, seed=0):
                 ids=["cta_pair", "cta_pair_epi4", "cta_pair_roundrobin", "cta_pair_1atom", "single_cta"])
 def cta_group(request, monkeypatch):
     """Run a GEMM test with each kernel variant: CTA pair (cta_group::2) with 2-atom stages
-    (default: 8 epilogue warps at these short K, dynamic tile scheduler), the same with 4 epilogue
+    (default: 8 epilogue warps at K <= 1024, dynamic tile scheduler), the same with 4 epilogue
     warps (the long-K default), with static round-robin tiles, CTA pair with 1-atom stages, single CTA."""
     monkeypatch.setenv("FP8T_GEMM_CTA_GROUP", request.param[0])
     monkeypatch.setenv("FP8T_GEMM_STAGES", "6" if request.param == "2s6" else "3")
