@@ -99,14 +99,19 @@ struct GemmArgs {
   unsigned* sched;    // dynamic tile scheduler slot (g_sched[i]); null: static round robin
 };
 
-template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bool E8 = false> struct Layout {
+template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bool E8 = false, int BNT = 256> struct Layout {
   static constexpr int STAGES = ST;
-  static constexpr int ACC = MX ? 1 : 2;
+  // MMA N of a tile.  256 everywhere except the MXFP8 N = 192 variant (K-major operands, CTA pair): two
+  // 192-column accumulators + the scale-factor columns fit the 512 TMEM columns, 2 x 256 do not
+  static constexpr int BN = BNT;
+  static_assert(BN == 256 || (BN == 192 && MX && CG == 2), "N = 192 tiles: MX CTA-pair kernel only");
+  static constexpr int ACC = MX && BN == 256 ? 1 : 2;
   static constexpr int EPI_WARPS = E8 || ACC == 1 ? 8 : 4;   // see the epilogue
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   // a stage holds KS 128-byte K atoms (16 KB sub-tiles of 128 rows each)
   static constexpr uint32_t A_STAGE = BM * BK * KS;         // 16 KB x KS
-  static constexpr uint32_t B_STAGE = (BN / CG) * BK * KS;  // 32 KB (CG=1) / 16 KB (CG=2), x KS
+  static constexpr uint32_t B_STAGE = (256 / CG) * BK * KS;  // 32 KB (CG=1) / 16 KB (CG=2) atom slots, x KS
+  static constexpr uint32_t B_TX = (BN / CG) * BK * KS;     // bytes actually loaded (N = 192: 12 KB per atom)
   // MX scale factors per stage: SFA = this CTA's 128 rows x KS atoms; SFB = all 256 N rows x KS
   static constexpr uint32_t SFA_STAGE = MX ? KS * SF_CHUNK : 0;
   static constexpr uint32_t SFB_STAGE = MX ? 2 * KS * SF_CHUNK : 0;
@@ -136,9 +141,9 @@ template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bo
   // stage s+1 never overwrites columns the MMAs of stage s still read): stage s, SFA atom t at
   // sfa_col + s*SF_COLS + 4t; SFB (row block h, atom t) at sfb_col + s*SF_COLS + 8t + 4h
   static constexpr uint32_t SF_COLS = 12 * KS;
-  static constexpr uint32_t sfa_col = 256, sfb_col = 256 + 4 * KS;
-  static_assert(!MX || 256 + STAGES * SF_COLS <= 512, "TMEM columns");
-  static constexpr uint32_t tx_bytes = CG * (A_STAGE + B_STAGE);   // operands, counted on the leader
+  static constexpr uint32_t sfa_col = ACC * BN, sfb_col = ACC * BN + 4 * KS;
+  static_assert(!MX || sfa_col + STAGES * SF_COLS <= 512, "TMEM columns");
+  static constexpr uint32_t tx_bytes = CG * (A_STAGE + B_TX);   // operands, counted on the leader
   static constexpr uint32_t sf_tx_bytes = CG * (SFA_STAGE + SFB_STAGE);   // MX scale tiles (sf_full)
 };
 
@@ -168,8 +173,8 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nb = local / gsz;
 }
 
-template <bool MX, int CG, int ST, int KS, bool BF, bool GRP, bool E8>
-__global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 1)
+template <bool MX, int CG, int ST, int KS, bool BF, bool GRP, bool E8, int BNT>
+__global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THREADS, 1)
     fp8_gemm_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tB0,
                     const __grid_constant__ CUtensorMap tSA0, const __grid_constant__ CUtensorMap tSB0,
                     const __grid_constant__ CUtensorMap tA1, const __grid_constant__ CUtensorMap tB1,
@@ -178,7 +183,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
   static_assert(KS == 1 || CG == 2, "multi-atom stages need the CTA-pair kernel");
   static_assert(!BF || (CG == 2 && KS == 2 && !MX), "BF16 operands: CTA-pair, 2-atom stages");
   static_assert(!GRP || (!MX && !BF), "grouped problems: plain FP8 kinds");
-  using L = Layout<MX, CG, ST, KS, BF, GRP, E8>;
+  using L = Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -456,7 +461,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
       const CUtensorMap* tmSFB = pi ? &tSB1 : &tSB0;
       const int a_mn = P.a_mn, b_mn = P.b_mn;
       const int m0 = mb * BM * CG + (int)crank * BM;
-      const int n0 = nb * BN + (int)crank * (BN / CG);
+      const int n0 = nb * L::BN + (int)crank * (L::BN / CG);
       // debug bit 4: skip the MX scale-factor loads (timing experiments only; results invalid)
       // debug bit 256 (timing experiment, results invalid): no operand loads, the stage completes on arrivals
       const uint32_t tx = (args.debug & 256) ? 0u : L::tx_bytes;
@@ -500,8 +505,11 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
             const int rba = mb * CG + (int)crank;   // this CTA's 128-row block of A
             if (CG == 2) {
               tma_load_2d_2sm(dsa, tmSFA, 0, rba * KT + kt0, sfb);
-              tma_load_2d_2sm(dsb, tmSFB, 0, (2 * nb) * KT + kt0, sfb);
-              tma_load_2d_2sm(dsb + KS * SF_CHUNK, tmSFB, 0, (2 * nb + 1) * KT + kt0, sfb);
+              // the tile's N rows span 128-row scale blocks c0, c0 + 1 (N = 192: odd tiles start half-way
+              // into block c0; the MMA then reads SFB two TMEM columns further)
+              const int c0 = L::BN == 256 ? 2 * nb : (3 * nb) >> 1;
+              tma_load_2d_2sm(dsb, tmSFB, 0, c0 * KT + kt0, sfb);
+              tma_load_2d_2sm(dsb + KS * SF_CHUNK, tmSFB, 0, (c0 + 1) * KT + kt0, sfb);
             } else {
               tma_load_2d(dsa, tmSFA, 0, rba * KT + kt0, sfb, 0);
               tma_load_2d(dsb, tmSFB, 0, (2 * nb) * KT + kt0, sfb, 0);
@@ -580,7 +588,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
       };
       mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
+      const uint32_t d_tmem = tmem_base + acc * L::BN;
       for (int kb = 0; kb < num_kb; ++kb) {
         if (!have_next && kb + 2 >= num_kb) fetch_next();
         mbar_wait(full_bar + 8 * stage, phase);
@@ -614,7 +622,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
               const uint32_t t = (uint32_t)k >> 2;
               const uint32_t id = idesc_with_sf_id(idesc, k & 3, k & 3);
               const uint32_t sfa = tmem_base + L::sfa_col + stage * L::SF_COLS + 4 * t;
-              const uint32_t sfb = tmem_base + L::sfb_col + stage * L::SF_COLS + 8 * t;
+              const uint32_t sfb = tmem_base + L::sfb_col + stage * L::SF_COLS + 8 * t + (L::BN == 192 ? 2 * (ti.nb & 1) : 0);
               if (CG == 2) mma_mxf8f6f4_cg2(d_tmem, ad, bd, id, acc_flag, sfa, sfb);
               else mma_mxf8f6f4(d_tmem, ad, bd, id, acc_flag, sfa, sfb);
             } else if (BF) {
@@ -773,7 +781,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
 
       mbar_wait(tfull_bar + 8 * acc, acc_phase);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * L::BN;
       if (args.debug & 8) {   // timing experiment (results invalid): release the accumulator untouched
         tc_fence_before();
         __syncwarp();
@@ -782,9 +790,10 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
           else mbar_arrive(tempty_bar + 8 * acc);
         }
       } else if (EPIW == 8) {
-        uint32_t r[4][32];
+        constexpr int HC = L::BN / 64;   // 32-column chunks per half
+        uint32_t r[HC][32];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tbase + half * 128 + c * 32, r[c]);
+        for (int c = 0; c < HC; ++c) tmem_ld_32x32b_x32(tbase + half * (L::BN / 2) + c * 32, r[c]);
         tmem_wait_ld();
         tc_fence_before();   // TMEM drained: release it to the MMA warp before the stores
         __syncwarp();
@@ -793,14 +802,14 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8>::THREADS, 
           else mbar_arrive(tempty_bar + 8 * acc);
         }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) process(r[c], nb * BN + half * 128 + c * 32);
+        for (int c = 0; c < HC; ++c) process(r[c], nb * L::BN + half * (L::BN / 2) + c * 32);
       } else {
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < L::BN / 32; ++c) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(tbase + c * 32, r);
           tmem_wait_ld();
-          process(r, nb * BN + c * 32);
+          process(r, nb * L::BN + c * 32);
         }
         tc_fence_before();
         __syncwarp();
@@ -906,13 +915,13 @@ static bool make_sf_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool MX, int CG, int ST, int KS, bool BF, bool GRP, bool E8>
+template <bool MX, int CG, int ST, int KS, bool BF, bool GRP, bool E8, int BNT>
 static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   // grouped 1: B holds G experts (K-major: G*N rows; MN-major: G*K contraction rows)
   const int64_t bN = p.grouped == 1 && !p.b_mn ? p.G * p.N : p.N;
   const int64_t bK = p.grouped == 1 && p.b_mn ? p.G * p.K : p.K;
   if (!make_operand_map(&maps[0], p.A, p.a_mn, p.M, p.K, p.lda, BM, BF) ||
-      !make_operand_map(&maps[1], p.B, p.b_mn, bN, bK, p.ldb, BN / CG, BF))
+      !make_operand_map(&maps[1], p.B, p.b_mn, bN, bK, p.ldb, BNT / CG, BF))
     return false;
   if (MX) {
     if (!make_sf_map(&maps[2], p.sa, p.M, p.K, KS) || !make_sf_map(&maps[3], p.sb, p.N, p.K, KS)) return false;
@@ -923,10 +932,10 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   P = Prob{};
   P.M = (int)p.M; P.N = (int)p.N; P.K = (int)p.K;
   P.tiles_m = (int)((p.M + BM * CG - 1) / (BM * CG));
-  P.tiles_n = (int)((p.N + BN - 1) / BN);
+  P.tiles_n = (int)((p.N + BNT - 1) / BNT);
   const int k_per_stage = BF ? KS * 64 : KS * BK;   // elements
   P.num_kb = (int)((p.K + k_per_stage - 1) / k_per_stage);
-  P.idesc = MX   ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u)
+  P.idesc = MX   ? make_idesc_mxf8f6f4(p.fmt_a, p.fmt_b, BM * CG, BNT, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u)
             : BF ? make_idesc_bf16(BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u)
                  : make_idesc_f8f6f4(p.fmt_a, p.fmt_b, BM * CG, BN, p.a_mn ? 1u : 0u, p.b_mn ? 1u : 0u);
   P.a_mn = p.a_mn;
@@ -953,7 +962,7 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   P.rs_rank = p.rs_rank;
   P.rs_chunk_rows = p.rs_chunk_rows;
   // every epilogue warp of both CTAs of a pair arrives once per tile of the chunk
-  P.rs_expect = p.rs_bufs ? (p.rs_chunk_rows / (BM * CG)) * P.tiles_n * Layout<MX, CG, ST, KS, BF, GRP, E8>::EPI_WARPS * CG : 0;
+  P.rs_expect = p.rs_bufs ? (p.rs_chunk_rows / (BM * CG)) * P.tiles_n * Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::EPI_WARPS * CG : 0;
   P.rs_epoch = p.rs_epoch;
   return true;
 }
@@ -992,13 +1001,13 @@ static unsigned* sched_slot() {
   return b + 2 * (next_slot.fetch_add(1) % SCHED_SLOTS);
 }
 
-template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bool E8 = false>
+template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bool E8 = false, int BNT = 256>
 static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
-  using L = Layout<MX, CG, ST, KS, BF, GRP, E8>;
+  using L = Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8>,
+    attr_err = cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8, BNT>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
   });
   if (attr_err != cudaSuccess) return attr_err;
@@ -1012,10 +1021,10 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     if (!GRP && ps[1].K > ps[0].K) { q[0] = ps[1]; q[1] = ps[0]; }
   }
   ps = q;
-  if (!setup_prob<MX, CG, ST, KS, BF, GRP, E8>(ps[0], a.p0, m0)) return cudaErrorInvalidValue;
+  if (!setup_prob<MX, CG, ST, KS, BF, GRP, E8, BNT>(ps[0], a.p0, m0)) return cudaErrorInvalidValue;
   a.t1 = a.p0.tiles_m * a.p0.tiles_n;
   if (n > 1) {
-    if (!setup_prob<MX, CG, ST, KS, BF, GRP, E8>(ps[1], a.p1, m1)) return cudaErrorInvalidValue;
+    if (!setup_prob<MX, CG, ST, KS, BF, GRP, E8, BNT>(ps[1], a.p1, m1)) return cudaErrorInvalidValue;
     a.num_tiles = a.t1 + a.p1.tiles_m * a.p1.tiles_n;
   } else {
     a.p1 = a.p0;
@@ -1044,7 +1053,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   const int grid = GRP ? CG * slots : CG * (a.num_tiles < slots ? a.num_tiles : slots);
   LaunchScope ls(MX ? K_GEMM_MX : (BF ? K_GEMM_BF16 : K_GEMM), st);
   if (CG == 1) {
-    fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8><<<grid, L::THREADS, L::bytes, st>>>(m0[0], m0[1], m0[2], m0[3], m1[0], m1[1],
+    fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8, BNT><<<grid, L::THREADS, L::bytes, st>>>(m0[0], m0[1], m0[2], m0[3], m1[0], m1[1],
                                                                       m1[2], m1[3], a);
   } else {
     cudaLaunchConfig_t cfg{};
@@ -1059,7 +1068,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8>, m0[0], m0[1], m0[2], m0[3], m1[0],
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8, BNT>, m0[0], m0[1], m0[2], m0[3], m1[0],
                                        m1[1], m1[2], m1[3], a);
     if (e != cudaSuccess) return e;
   }
@@ -1085,7 +1094,17 @@ cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st) {
     return launch_t<false, 2, 3, 2, true>(ps, n, st);
   }
   const int cg = cta_group_for();
-  if (ps[0].scale_mode == 2) return cg == 1 ? launch_t<true, 1, 4, 1>(ps, n, st) : launch_t<true, 2, 3, 2>(ps, n, st);
+  if (ps[0].scale_mode == 2) {
+    if (cg == 1) return launch_t<true, 1, 4, 1>(ps, n, st);
+    // FP8T_MX_N192=1 (K-major operands only): N = 192 tiles with double-buffered accumulators.  Measured
+    // 18 % fewer flop/clk/SM than N = 256 with one accumulator (c4 shape 10.5k vs 12.8k): the extra
+    // operand traffic per flop costs more than the accumulator hand-over saves.  Kept as an option.
+    bool kmaj = true;
+    for (int i = 0; i < n; ++i) kmaj = kmaj && !ps[i].a_mn && !ps[i].b_mn;
+    const char* e = getenv("FP8T_MX_N192");
+    if (kmaj && e && e[0] == '1') return launch_t<true, 2, 3, 2, false, false, false, 192>(ps, n, st);
+    return launch_t<true, 2, 3, 2>(ps, n, st);
+  }
   if (cg == 1) return launch_t<false, 1, 4, 1>(ps, n, st);
   // default: 3 stages x 2 K atoms (64 KB per CTA per stage, 8 MMAs per barrier round trip);
   // FP8T_GEMM_STAGES=6 selects 6 x 1 atom (4 MMAs per round trip) for comparison

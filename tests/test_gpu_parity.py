@@ -297,8 +297,10 @@ def _block(codes_logical):
 @pytest.mark.parametrize("fa,fb", [(E4M3, E4M3), (E5M2, E4M3)])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 128), (256, 384, 512), (384, 640, 384)])
 @pytest.mark.parametrize("majors", ["KK", "KM", "MM", "MK"])
-def test_gemm_mx_tolerance(fa, fb, M, N, K, majors, cta_group):
+def test_gemm_mx_tolerance(fa, fb, M, N, K, majors, cta_group, monkeypatch):
     # MN-major operands keep the same logical [rows, K/32] scale factors (blocked layout)
+    if cta_group == "2rr" and majors == "KK":   # also cover the optional N = 192 MX tiles
+        monkeypatch.setenv("FP8T_MX_N192", "1")
     a = synth.tensor_c4("x", (M, K), seed=6)
     b = synth.tensor_c4("w", (N, K), seed=6)
     qa, sa = omx.quantize_dim0(a, fa)
