@@ -436,6 +436,7 @@ def run_ours(a):
     # ---------------- timed region (device events, max over ranks) ----------------
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_steps = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]   # per-step boundaries
     L.lib.fp8_profile_collect(None, None, 0)
     L.lib.fp8_profile_enable(1)
     n0 = ops.launch_count()
@@ -443,8 +444,9 @@ def run_ours(a):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ev0.record(stream)
-        for _ in range(a.steps):
+        for i_ in range(a.steps):
             step()
+            ev_steps[i_].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -461,6 +463,7 @@ def run_ours(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / a.steps
+    step_pct = step_percentiles(ev0, ev_steps)
 
     gather_info = None
     if fsdp:
@@ -652,7 +655,7 @@ def run_ours(a):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
-            "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "step_ms_p10_p50_p90": step_pct, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp8 (e4m3 x e5m2 codes, fp32 accumulate, bf16 out)",
             "data": "synthetic (seeded, device-generated, config value recipe)",
             "config": {"workload": cfg["workload"], "M_per_gpu": M, "N": N, "K": K, "recipe": cfg["recipe"],
@@ -692,6 +695,19 @@ def run_ours(a):
         comm.close()
     if dist.is_initialized():
         dist.destroy_process_group()
+
+
+def step_percentiles(ev0, ev_steps):
+    """p10 / median / p90 of the per-step device times (this rank; events on the step stream)."""
+    prev, t = ev0, []
+    for e in ev_steps:
+        t.append(prev.elapsed_time(e))
+        prev = e
+    if not t:
+        return None
+    t.sort()
+    pick = lambda q: t[min(len(t) - 1, int(round(q * (len(t) - 1))))]  # noqa: E731
+    return [round(pick(0.1), 4), round(pick(0.5), 4), round(pick(0.9), 4)]
 
 
 def moe_offsets(T, E, seed=0):
@@ -744,6 +760,7 @@ def run_layer(a):
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_steps = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]   # per-step boundaries
     L.lib.fp8_profile_collect(None, None, 0)
     L.lib.fp8_profile_enable(1)
     n0 = ops.launch_count()
@@ -752,8 +769,9 @@ def run_layer(a):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ev0.record(stream)
-        for _ in range(a.steps):
+        for i_ in range(a.steps):
             step()
+            ev_steps[i_].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = ops.launch_count() - n0
@@ -767,6 +785,7 @@ def run_layer(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / a.steps
+    step_pct = step_percentiles(ev0, ev_steps)
     flops_step = sum(6.0 * M * u["N"] * u["K"] for u in units)
     value = flops_step * a.steps * world / (ms / 1e3) / 1e12
     by = {}
@@ -833,7 +852,7 @@ def run_layer(a):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
-            "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "step_ms_p10_p50_p90": step_pct, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp8 (e4m3 x e5m2 codes, fp32 accumulate, bf16 out)",
             "data": "synthetic (seeded, device-generated, config value recipe)",
             "config": {"workload": cfg["workload"], "M_per_gpu": M, "linears": cfg["linears"], "recipe": cfg["recipe"],
@@ -896,6 +915,7 @@ def run_moe(a):
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_steps = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]   # per-step boundaries
     L.lib.fp8_profile_collect(None, None, 0)
     L.lib.fp8_profile_enable(1)
     n0 = ops.launch_count()
@@ -904,8 +924,9 @@ def run_moe(a):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ev0.record(stream)
-        for _ in range(a.steps):
+        for i_ in range(a.steps):
             step()
+            ev_steps[i_].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = ops.launch_count() - n0
@@ -919,6 +940,7 @@ def run_moe(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / a.steps
+    step_pct = step_percentiles(ev0, ev_steps)
     flops_step = 6.0 * T * N * K
     value = flops_step * a.steps * world / (ms / 1e3) / 1e12
     by = {}
@@ -987,7 +1009,7 @@ def run_moe(a):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
-            "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "step_ms_p10_p50_p90": step_pct, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp8 (e4m3 x e5m2 codes, fp32 accumulate, bf16 out)",
             "data": "synthetic (seeded, device-generated, config value recipe; seeded routing)",
             "config": {"workload": cfg["workload"], "T": T, "E": E, "N": N, "K": K, "recipe": cfg["recipe"],
