@@ -49,8 +49,10 @@ constexpr int SCHED_SLOTS = 4096;             // launches in flight that may sha
 
 // Dynamic tile scheduler state: [slot][0] = next dynamic tile, [slot][1] = pairs done fetching.  Every
 // launch takes its own slot (host-side round robin); the last pair to finish fetching resets both, so a
-// slot is zero again when it is reused.  Module-global device memory: no allocation in any call.
-__device__ unsigned g_sched[SCHED_SLOTS][2];
+// slot is zero again when it is reused.  Slots [0, SCHED_SLOTS) serve eager launches, [SCHED_SLOTS,
+// 2 SCHED_SLOTS) launches captured into CUDA graphs (a graph keeps its slot for every replay, so eager
+// launches never share it).  Module-global device memory: no allocation in any call.
+__device__ unsigned g_sched[2 * SCHED_SLOTS][2];
 
 // One GEMM problem of a (possibly two-problem) launch.
 struct Prob {
@@ -985,10 +987,11 @@ static int choose_raster(const GemmProblem& p, bool bf16) {
   return b_bytes <= budget ? 0 : GROUP_M;
 }
 
-// This launch's slot of g_sched on the current device (round robin over SCHED_SLOTS).
-static unsigned* sched_slot() {
+// This launch's slot of g_sched on the current device (round robin over SCHED_SLOTS; launches under
+// stream capture use the graph region).
+static unsigned* sched_slot(cudaStream_t st) {
   static std::atomic<unsigned*> base[64];
-  static std::atomic<unsigned> next_slot{0};
+  static std::atomic<unsigned> next_slot{0}, next_graph_slot{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
   unsigned* b = base[dev].load();
@@ -998,6 +1001,9 @@ static unsigned* sched_slot() {
     b = static_cast<unsigned*>(p);
     base[dev].store(b);
   }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return nullptr;
+  if (cs == cudaStreamCaptureStatusActive) return b + 2 * (SCHED_SLOTS + next_graph_slot.fetch_add(1) % SCHED_SLOTS);
   return b + 2 * (next_slot.fetch_add(1) % SCHED_SLOTS);
 }
 
@@ -1037,7 +1043,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     // FP8T_GEMM_SCHED=static: round-robin tiles (A/B); default: dynamic scheduler
     const char* sc = getenv("FP8T_GEMM_SCHED");
     if (!(sc && sc[0] == 's')) {
-      a.sched = sched_slot();
+      a.sched = sched_slot(st);
       if (!a.sched) return cudaErrorInvalidValue;
     }
     const char* sf = getenv("FP8T_MX_SF_SPLIT");
