@@ -969,23 +969,14 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   return true;
 }
 
-// Tile raster of one problem.  The GEMMs here stream long K panels, so a wave of concurrent tiles
-// only shares the K slices it reads at the same time, unless one whole operand stays L2-resident:
-//   B (all N tiles x K) <= ~80 MB  -> row-major: every wave sweeps all N tiles of a few M tiles, B is
-//                                     read from DRAM once and A streams through once (C2's GEMMs);
-//   otherwise                      -> groups of GROUP_M M tiles sweep the N tiles (C4's GEMMs: measured
-//                                     10.6-10.8 ms/step vs 12.1 row-major; the DRAM traffic also sets the
-//                                     power-capped clock).
-// FP8T_GEMM_L2_MB overrides the residency budget.
-static int choose_raster(const GemmProblem& p, bool bf16) {
-  static const double budget = [] {
-    const char* e = getenv("FP8T_GEMM_L2_MB");
-    return (e ? atof(e) : 80.0) * 1e6;
-  }();
-  const double b_bytes = (double)((p.N + BN - 1) / BN * BN) * (double)p.K * (bf16 ? 2.0 : 1.0) *
-                         (p.grouped == 1 ? (double)p.G : 1.0);
-  return b_bytes <= budget ? 0 : GROUP_M;
-}
+// Tile raster of one problem: groups of GROUP_M M tiles sweep the N tiles, so the ~74 concurrent tiles
+// of a wave cover 16 M x ~4.6 N tiles and share their K slices of A and B while they are read (the L2
+// de-duplicates concurrent reads; the operand traffic per flop is what bounds the GEMM at full clock,
+// DESIGN.md §5).  Measured (bench, 1.97 GHz): c2 step GEMMs 1.963 ms row-major -> 1.925 ms (16); 8: 1.939,
+// 32: 2.02, 64: 2.16; c4 8.42-8.47 ms (8, 16) vs 9.09 (32), 9.78 (64); c3 layer step -1 to -3 %.
+// (Round r01c chose row-major when all of B fit ~80 MB of L2; with the dynamic scheduler the grouped
+// raster is as good or better for every shape measured.)  FP8T_GEMM_RASTER overrides (0 = row-major).
+static int choose_raster(const GemmProblem&, bool) { return GROUP_M; }
 
 // This launch's slot of g_sched on the current device (round robin over SCHED_SLOTS; launches under
 // stream capture use the graph region).
