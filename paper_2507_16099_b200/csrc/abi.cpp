@@ -609,16 +609,37 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
     float* awr = axc + K;
     float* awc = awr + N;
     FP8T_CUDA(cudaMemsetAsync(fw.amax, 0, 4 * (M + K + N + K), st), "memset");
-    FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, gw_hp ? 2 : 6, nullptr, (uint32_t*)axr, (uint32_t*)axc, st),
-              "amax x");
-    FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 6, nullptr, (uint32_t*)awr, (uint32_t*)awc, st), "amax w");
+    // X and W in one amax launch and one cast launch where the shapes allow (the small weights of
+    // e.g. the wk/wv projections then cost no launch ramp and tail of their own); rowwise_gw_hp
+    // needs different scale modes for X and W, so it keeps separate launches
+    bool dual = false;
+    if (!gw_hp && xb && wb) {
+      const cudaError_t e = launch_amax_dual(x.ptr, M, K, x.ld, w.ptr, N, K, w.ld, 6, (uint32_t*)axr, (uint32_t*)axc,
+                                             (uint32_t*)awr, (uint32_t*)awc, st);
+      if (e != cudaErrorNotSupported) FP8T_CUDA(e, "amax x, w");
+      dual = e == cudaSuccess;
+    }
+    if (!dual) {
+      FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, gw_hp ? 2 : 6, nullptr, (uint32_t*)axr, (uint32_t*)axc, st),
+                "amax x");
+      FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 6, nullptr, (uint32_t*)awr, (uint32_t*)awc, st), "amax w");
+    }
     // row-scaled codes for the forward GEMM; column-scaled codes written row-major for the
     // backward GEMMs (read MN-major, no transposed copy)
-    FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 2, gw_hp ? 0 : 5, axr, axc, fw.xq, gw_hp ? nullptr : sv.xT,
-                          fw.sxr, gw_hp ? nullptr : (float*)sv.sx, st),
-              "cast x");
-    FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 5, awr, awc, fw.wq, sv.wT, fw.swr, (float*)sv.sw, st),
-              "cast w");
+    if (!gw_hp && xb == wb) {
+      CastDual cd{};
+      cd.x[0] = x.ptr; cd.R[0] = M; cd.C[0] = K; cd.ld[0] = x.ld; cd.amax_q[0] = axr; cd.amax_t[0] = axc;
+      cd.q[0] = fw.xq; cd.qt[0] = sv.xT; cd.scale_q[0] = fw.sxr; cd.scale_t[0] = (float*)sv.sx;
+      cd.x[1] = w.ptr; cd.R[1] = N; cd.C[1] = K; cd.ld[1] = w.ld; cd.amax_q[1] = awr; cd.amax_t[1] = awc;
+      cd.q[1] = fw.wq; cd.qt[1] = sv.wT; cd.scale_q[1] = fw.swr; cd.scale_t[1] = (float*)sv.sw;
+      FP8T_CUDA(launch_cast_dual(cd, xb, ff, 2, 5, st), "cast x, w");
+    } else {
+      FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 2, gw_hp ? 0 : 5, axr, axc, fw.xq, gw_hp ? nullptr : sv.xT,
+                            fw.sxr, gw_hp ? nullptr : (float*)sv.sx, st),
+                "cast x");
+      FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 5, awr, awc, fw.wq, sv.wT, fw.swr, (float*)sv.sw, st),
+                "cast w");
+    }
     GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N, 0, yam};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
   } else {

@@ -238,10 +238,21 @@ __global__ void __launch_bounds__(256) amax_tile_kernel(const T* __restrict__ x,
 // and are flushed (half-warp reduce + one atomicMax per row) only when the strip changes, while
 // thread 0 streams 32 KB tiles into an ST-deep smem ring with cp.async.bulk.tensor.
 // ---------------------------------------------------------------------------
+// Optional second tensor of an amax_tile_tma launch (the forward's W next to X): its tiles follow the
+// first tensor's in the tile order, with their own row / column outputs (row / column modes only).
+struct AmaxSecond {
+  int tiles0, tiles1;  // tiles of the first / second tensor (tiles1 = 0: one tensor)
+  int tiles_x1, strips0;
+  uint32_t* amax_row1;
+  uint32_t* amax_col1;
+};
+
 template <int MODE, int ST>
 __global__ void __launch_bounds__(256) amax_tile_tma_kernel(const __grid_constant__ CUtensorMap tmap, int64_t R,
                                                             int64_t C, uint32_t* amax_tensor, uint32_t* amax_row,
-                                                            uint32_t* amax_col, const Seg seg) {
+                                                            uint32_t* amax_col, const Seg seg,
+                                                            const __grid_constant__ CUtensorMap tmap1,
+                                                            const AmaxSecond d) {
   constexpr int STAGE = 128 * 256;
   extern __shared__ __align__(1024) uint8_t sm[];
   uint32_t(*colred)[128] = reinterpret_cast<uint32_t(*)[128]>(sm + ST * STAGE);
@@ -249,21 +260,31 @@ __global__ void __launch_bounds__(256) amax_tile_tma_kernel(const __grid_constan
   const uint32_t bar0 = smem_u32(sm + ST * STAGE + 8 * 128 * 4 + 64), stage0 = smem_u32(sm);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int tiles_x = (int)(C >> 7);
-  const int num_tiles = tiles_x * (int)(R >> 7);
+  const int num_tiles = d.tiles0 + d.tiles1;
   const int per = (num_tiles + (int)gridDim.x - 1) / (int)gridDim.x;
   const int first = (int)blockIdx.x * per;
   const int last = min(first + per, num_tiles);
+  // tile id -> (tensor k, strip key, column tile): strips of the second tensor are numbered after the first's
+  auto where = [&](int id, int& k, int& rt, int& ct) {
+    k = id >= d.tiles0 ? 1 : 0;
+    const int local = k ? id - d.tiles0 : id;
+    const int tx = k ? d.tiles_x1 : tiles_x;
+    rt = local / tx;
+    ct = local - rt * tx;
+  };
   auto issue = [&](int k) {
     const int id = first + k;
     if (id < last) {
+      int kk, rt, ct;
+      where(id, kk, rt, ct);
       const uint32_t bar = bar0 + 8 * (k % ST);
       mbar_arrive_expect_tx(bar, STAGE);
-      tma_load_2d(stage0 + (k % ST) * STAGE, &tmap, (id % tiles_x) * 128, (id / tiles_x) * 128, bar,
-                  l2_policy_evict_first());
+      tma_load_2d(stage0 + (k % ST) * STAGE, kk ? &tmap1 : &tmap, ct * 128, rt * 128, bar, l2_policy_evict_first());
     }
   };
   if (t == 0) {
     tma_prefetch_desc(&tmap);
+    if (d.tiles1) tma_prefetch_desc(&tmap1);
     for (int i = 0; i < ST; ++i) mbar_init(bar0 + 8 * i, 1);
     fence_mbar_init();
     for (int k = 0; k < ST; ++k) issue(k);
@@ -272,8 +293,15 @@ __global__ void __launch_bounds__(256) amax_tile_tma_kernel(const __grid_constan
   const int cc = (t & 15) * 8;
   uint32_t tmax = 0;
   uint32_t rm[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // this thread's partial row maxima of the current strip
-  int strip = first < last ? first / tiles_x : -1;
+  // strip key: row strip of the first tensor, or strips0 + row strip of the second
+  auto strip_of = [&](int id) {
+    int kk, rt, ct;
+    where(id, kk, rt, ct);
+    return kk ? d.strips0 + rt : rt;
+  };
+  int strip = first < last ? strip_of(first) : -1;
   auto flush_rows = [&](int st_) {
+    uint32_t* rowp = st_ >= d.strips0 ? d.amax_row1 + (int64_t)(st_ - d.strips0) * 128 : amax_row + (int64_t)st_ * 128;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       uint32_t m = rm[i];
@@ -281,17 +309,19 @@ __global__ void __launch_bounds__(256) amax_tile_tma_kernel(const __grid_constan
       m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
       m = max(m, __shfl_xor_sync(0xffffffffu, m, 4));
       m = max(m, __shfl_xor_sync(0xffffffffu, m, 8));
-      if ((t & 15) == 0) atomicMax(amax_row + (int64_t)st_ * 128 + (t >> 4) + 16 * i, m);
+      if ((t & 15) == 0) atomicMax(rowp + (t >> 4) + 16 * i, m);
       rm[i] = 0;
     }
   };
   for (int k = 0; first + k < last; ++k) {
     const int id = first + k;
-    const int rt = id / tiles_x;
-    const int64_t r0 = (int64_t)rt * 128, c0 = (int64_t)(id - rt * tiles_x) * 128;
-    if ((MODE & 2) && rt != strip) {
+    int kk, rt, ct;
+    where(id, kk, rt, ct);
+    const int64_t r0 = (int64_t)rt * 128, c0 = (int64_t)ct * 128;
+    const int skey = kk ? d.strips0 + rt : rt;
+    if ((MODE & 2) && skey != strip) {
       flush_rows(strip);
-      strip = rt;
+      strip = skey;
     }
     mbar_wait(bar0 + 8 * (k % ST), (uint32_t)(k / ST) & 1u);
     uint4 raw[8];
@@ -334,9 +364,13 @@ __global__ void __launch_bounds__(256) amax_tile_tma_kernel(const __grid_constan
         uint32_t m = colred[0][t];
 #pragma unroll
         for (int w = 1; w < 8; ++w) m = max(m, colred[w][t]);
-        int64_t sstart;
-        const int g = seg_of(seg, r0, sstart);
-        atomicMax(amax_col + (int64_t)g * C + c0 + t, m);
+        if (kk) {
+          atomicMax(d.amax_col1 + c0 + t, m);
+        } else {
+          int64_t sstart;
+          const int g = seg_of(seg, r0, sstart);
+          atomicMax(amax_col + (int64_t)g * C + c0 + t, m);
+        }
       }
     }
   }
@@ -462,11 +496,10 @@ __global__ void __launch_bounds__(256) amax_multi_kernel(const __grid_constant__
 // Scale outputs are written by the tiles on the first tile row / column.
 // ---------------------------------------------------------------------------
 template <typename T, int FMT, int QM, int TM_>
-__global__ void __launch_bounds__(256) cast_tile_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
-                                                        const float* __restrict__ amax_q,
-                                                        const float* __restrict__ amax_t, uint8_t* __restrict__ q,
-                                                        uint8_t* __restrict__ qt, float* scale_q, float* scale_t,
-                                                        const Seg seg) {
+__device__ __forceinline__ void cast_tile_body(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
+                                               const float* __restrict__ amax_q, const float* __restrict__ amax_t,
+                                               uint8_t* __restrict__ q, uint8_t* __restrict__ qt, float* scale_q,
+                                               float* scale_t, const Seg& seg, int bx, int by) {
   // TM_ >= 4: the second output is written row-major ([R,C], like q) with scale mode TM_ - 2,
   // i.e. the column-scaled copy the backward GEMMs read MN-major (no transpose).
   constexpr bool TRM = TM_ >= 4;
@@ -475,9 +508,6 @@ __global__ void __launch_bounds__(256) cast_tile_kernel(const T* __restrict__ x,
   __shared__ float sq[128];
   __shared__ float st[128];
   const int t = threadIdx.x;
-  // tiles in decreasing linear order: the first tiles read are the ones amax_tile read last
-  const int rtile = (int)(gridDim.x * gridDim.y - 1 - (blockIdx.y * gridDim.x + blockIdx.x));
-  const int bx = rtile % (int)gridDim.x, by = rtile / (int)gridDim.x;
   const int64_t r0 = (int64_t)by * 128, c0 = (int64_t)bx * 128;
   const int vrows = imin128(R - r0), vcols = imin128(C - c0);
 
@@ -543,6 +573,32 @@ __global__ void __launch_bounds__(256) cast_tile_kernel(const T* __restrict__ x,
     __syncthreads();
     store_transposed(tile, qt, R, r0, c0, vrows, vcols);
   }
+}
+
+template <typename T, int FMT, int QM, int TM_>
+__global__ void __launch_bounds__(256) cast_tile_kernel(const T* __restrict__ x, int64_t R, int64_t C, int64_t ld,
+                                                        const float* __restrict__ amax_q,
+                                                        const float* __restrict__ amax_t, uint8_t* __restrict__ q,
+                                                        uint8_t* __restrict__ qt, float* scale_q, float* scale_t,
+                                                        const Seg seg) {
+  // tiles in decreasing linear order: the first tiles read are the ones amax_tile read last
+  const int rtile = (int)(gridDim.x * gridDim.y - 1 - (blockIdx.y * gridDim.x + blockIdx.x));
+  cast_tile_body<T, FMT, QM, TM_>(x, R, C, ld, amax_q, amax_t, q, qt, scale_q, scale_t, seg,
+                                  rtile % (int)gridDim.x, rtile / (int)gridDim.x);
+}
+
+// Two tensors (the forward's X and W) cast by one launch: a 1-D grid over the tiles of both, walked in
+// decreasing order over [X tiles, W tiles] (the reverse of the dual amax launch), so the small weight
+// costs no launch ramp and tail of its own.
+template <typename T, int FMT, int QM, int TM_>
+__global__ void __launch_bounds__(256) cast_tile_dual_kernel(const CastDual a) {
+  const int total = a.tiles[0] + a.tiles[1];
+  int id = total - 1 - (int)blockIdx.x;
+  const int k = id >= a.tiles[0] ? 1 : 0;
+  if (k) id -= a.tiles[0];
+  const int tx = (int)((a.C[k] + 127) / 128);
+  cast_tile_body<T, FMT, QM, TM_>(static_cast<const T*>(a.x[k]), a.R[k], a.C[k], a.ld[k], a.amax_q[k], a.amax_t[k],
+                                  a.q[k], a.qt[k], a.scale_q[k], a.scale_t[k], Seg{}, id % tx, id / tx);
 }
 
 // ---------------------------------------------------------------------------
@@ -915,7 +971,8 @@ static bool amax_tile_use_tma() {
 
 template <int MODE>
 static cudaError_t amax_tma_go(const CUtensorMap& m, int64_t R, int64_t C, int64_t tiles, uint32_t* at, uint32_t* ar,
-                               uint32_t* ac, cudaStream_t st, const Seg& seg) {
+                               uint32_t* ac, cudaStream_t st, const Seg& seg, const CUtensorMap* m1 = nullptr,
+                               AmaxSecond d = AmaxSecond{}) {
   constexpr int ST = 3;
   constexpr int smem = ST * 128 * 256 + 8 * 128 * 4 + 64 + ST * 8;
   auto kern = amax_tile_tma_kernel<MODE, ST>;
@@ -928,8 +985,14 @@ static cudaError_t amax_tma_go(const CUtensorMap& m, int64_t R, int64_t C, int64
   int64_t cap = (int64_t)sm_count() * 2;
   const char* g = getenv("FP8T_CAST_GRID");   // tests: cap the persistent grid (many tiles per CTA)
   if (g && atoi(g) > 0 && atoi(g) < cap) cap = atoi(g);
+  if (!m1) {
+    d = AmaxSecond{};
+    d.tiles0 = (int)tiles;
+    d.strips0 = (int)(R >> 7);
+  }
+  const int64_t all = (int64_t)d.tiles0 + d.tiles1;
   LaunchScope ls(K_AMAX, st);
-  kern<<<(unsigned)(tiles < cap ? tiles : cap), 256, smem, st>>>(m, R, C, at, ar, ac, seg);
+  kern<<<(unsigned)(all < cap ? all : cap), 256, smem, st>>>(m, R, C, at, ar, ac, seg, m1 ? *m1 : m, d);
   return cudaGetLastError();
 }
 
@@ -987,6 +1050,43 @@ static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
   return cudaGetLastError();
 }
 
+// Row / column amax of two bf16 tensors (the forward's X and W) in one TMA-ring launch: the second
+// tensor's tiles follow the first's in the persistent tile order.  cudaErrorNotSupported when a shape
+// does not fit the TMA path (the caller then launches the tensors separately).
+cudaError_t launch_amax_dual(const void* x0, int64_t R0, int64_t C0, int64_t ld0, const void* x1, int64_t R1, int64_t C1,
+                             int64_t ld1, int mode, uint32_t* ar0, uint32_t* ac0, uint32_t* ar1, uint32_t* ac1,
+                             cudaStream_t st) {
+  auto enc = get_encode();
+  if (!enc || !amax_tile_use_tma() || (mode != 2 && mode != 4 && mode != 6)) return cudaErrorNotSupported;
+  const void* xs[2] = {x0, x1};
+  const int64_t Rs[2] = {R0, R1}, Cs[2] = {C0, C1}, lds[2] = {ld0, ld1};
+  CUtensorMap m[2];
+  for (int k = 0; k < 2; ++k) {
+    if (Rs[k] % 128 || Cs[k] % 128 || Rs[k] <= 0 || Cs[k] <= 0) return cudaErrorNotSupported;
+    cuuint64_t dims[2] = {(cuuint64_t)Cs[k], (cuuint64_t)Rs[k]};
+    cuuint64_t strides[1] = {(cuuint64_t)lds[k] * 2};
+    cuuint32_t box[2] = {128, 128};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc(&m[k], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(xs[k]), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorNotSupported;
+  }
+  AmaxSecond d{};
+  d.tiles0 = (int)((R0 / 128) * (C0 / 128));
+  d.tiles1 = (int)((R1 / 128) * (C1 / 128));
+  d.tiles_x1 = (int)(C1 / 128);
+  d.strips0 = (int)(R0 / 128);
+  d.amax_row1 = ar1;
+  d.amax_col1 = ac1;
+  const int64_t tiles = d.tiles0;
+  switch (mode) {
+    case 2: return amax_tma_go<2>(m[0], R0, C0, tiles, nullptr, ar0, ac0, st, Seg{}, &m[1], d);
+    case 4: return amax_tma_go<4>(m[0], R0, C0, tiles, nullptr, ar0, ac0, st, Seg{}, &m[1], d);
+    default: return amax_tma_go<6>(m[0], R0, C0, tiles, nullptr, ar0, ac0, st, Seg{}, &m[1], d);
+  }
+}
+
 cudaError_t launch_amax_multi(const AmaxMultiArgs& a, cudaStream_t st) {
   const int64_t total = a.chunk_start[a.n];
   if (total == 0) return cudaSuccess;
@@ -1021,6 +1121,27 @@ static cudaError_t cast_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
   FP8T_CAST(2, 3) FP8T_CAST(2, 5) FP8T_CAST(0, 5)
 #undef FP8T_CAST
   return cudaErrorInvalidValue;
+}
+
+template <typename T, int FMT>
+static cudaError_t cast_dual_launch_t(const CastDual& a, int qm, int tm, cudaStream_t s) {
+  const unsigned g = (unsigned)(a.tiles[0] + a.tiles[1]);
+#define FP8T_CAST2(QM, TM)                                                          \
+  if (qm == QM && tm == TM) {                                                       \
+    LaunchScope ls(K_CAST, s);                                                      \
+    cast_tile_dual_kernel<T, FMT, QM, TM><<<g, 256, 0, s>>>(a);                      \
+    return cudaGetLastError();                                                      \
+  }
+  FP8T_CAST2(1, 0) FP8T_CAST2(2, 5) FP8T_CAST2(2, 0)
+#undef FP8T_CAST2
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_cast_dual(CastDual a, bool bf16, int fmt, int qm, int tm, cudaStream_t s) {
+  for (int k = 0; k < 2; ++k) a.tiles[k] = (int)(((a.R[k] + 127) / 128) * ((a.C[k] + 127) / 128));
+  if (bf16)
+    return fmt == 0 ? cast_dual_launch_t<__nv_bfloat16, 0>(a, qm, tm, s) : cast_dual_launch_t<__nv_bfloat16, 1>(a, qm, tm, s);
+  return fmt == 0 ? cast_dual_launch_t<float, 0>(a, qm, tm, s) : cast_dual_launch_t<float, 1>(a, qm, tm, s);
 }
 
 cudaError_t launch_cast(const void* x, bool bf16, int fmt, int64_t R, int64_t C, int64_t ld, int qm, int tm,

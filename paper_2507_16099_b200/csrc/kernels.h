@@ -38,6 +38,24 @@ cudaError_t launch_amax(const void* x, bool bf16, int64_t R, int64_t C, int64_t 
 cudaError_t launch_cast(const void* x, bool bf16, int fmt, int64_t R, int64_t C, int64_t ld, int qm, int tm,
                         const float* aq, const float* at, uint8_t* q, uint8_t* qt, float* sq, float* st,
                         cudaStream_t s, const Seg& seg = Seg{});
+// Row (mode 2) / column (4) / row+column (6) amax of two bf16 tensors in one launch (outputs pre-zeroed);
+// cudaErrorNotSupported if a shape is not a multiple of 128 (launch them separately then).
+cudaError_t launch_amax_dual(const void* x0, int64_t R0, int64_t C0, int64_t ld0, const void* x1, int64_t R1, int64_t C1,
+                             int64_t ld1, int mode, uint32_t* ar0, uint32_t* ac0, uint32_t* ar1, uint32_t* ac1,
+                             cudaStream_t st);
+// Two tensors (same format and scale modes) cast by one launch; tiles[] is filled by the launcher.
+struct CastDual {
+  const void* x[2];
+  int64_t R[2], C[2], ld[2];
+  const float* amax_q[2];
+  const float* amax_t[2];
+  uint8_t* q[2];
+  uint8_t* qt[2];
+  float* scale_q[2];
+  float* scale_t[2];
+  int tiles[2];
+};
+cudaError_t launch_cast_dual(CastDual a, bool bf16, int fmt, int qm, int tm, cudaStream_t s);
 // Tensorwise amax of n <= AMAX_MULTI_MAX tensors in one launch; out[t] (u32 bit patterns of
 // non-negative floats) must be zeroed by the caller.  chunk_start[t] = first warp chunk of
 // tensor t (chunks of 256 16-byte vectors within one row), chunk_start[n] = total.

@@ -335,6 +335,7 @@ def test_gemm_mx_integer_grid_exact(cta_group):
     ("tensorwise", "c1", 256, 256, 256),
     ("tensorwise", "c2", 400, 272, 528),
     ("rowwise", "c3", 384, 400, 272),
+    ("rowwise", "c3", 768, 384, 640),        # X and W amax / cast in one launch each
     ("mxfp8", "c4", 256, 384, 512),
     ("rowwise_gw_hp", "c3", 384, 400, 272),
     ("rowwise_gw_hp", "c2", 1024, 768, 512),
@@ -1007,3 +1008,26 @@ def test_linear_cuda_graph_replay(recipe):
         torch.cuda.synchronize()
         for got, want in zip((Y, DX, DW), ref):
             assert torch.equal(got.view(torch.int16), want.view(torch.int16))
+
+
+@pytest.mark.parametrize("grid", ["3", "7", "0"])
+def test_linear_rowwise_dual_launch_straddle(grid, monkeypatch):
+    """Rowwise forward with X and W amax'd by one persistent TMA launch (capped grids make CTA tile
+    ranges straddle the X -> W boundary, so a row strip of W follows one of X in the same CTA) and cast
+    by one launch: the forward codes, scales and outputs match the oracle; the saved column-scaled
+    copies drive a backward in tolerance."""
+    if grid != "0":
+        monkeypatch.setenv("FP8T_CAST_GRID", grid)
+    M, N, K = 640, 384, 512
+    x, w, dy = synth.linear_inputs("c3", M, N, K, seed=5)
+    y, yb, _ = olin.forward(x, w, "rowwise")
+    dx, dxb, dw, dwb, _ = olin.backward(x, w, dy, "rowwise")
+    plan = ops.LinearPlan(M, N, K, recipe="rowwise", out_dtype=torch.float32)
+    saved = plan.new_saved()
+    X = _dev(x, torch.bfloat16)
+    Y = plan.forward(X, _dev(w, torch.bfloat16), saved)
+    DX, DW = plan.backward(_dev(dy, torch.bfloat16), saved, x=X)
+    torch.cuda.synchronize()
+    _tol_check(_np(Y).astype(np.float64), y, yb)
+    _tol_check(_np(DX).astype(np.float64), dx, dxb)
+    _tol_check(_np(DW).astype(np.float64), dw, dwb)
