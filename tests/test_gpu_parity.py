@@ -336,6 +336,7 @@ def test_gemm_mx_integer_grid_exact(cta_group):
     ("tensorwise", "c2", 400, 272, 528),
     ("rowwise", "c3", 384, 400, 272),
     ("rowwise", "c3", 768, 384, 640),        # X and W amax / cast in one launch each
+    ("rowwise", "c1", 256, 384, 256),        # fp32 inputs: separate amax launches, one cast launch
     ("mxfp8", "c4", 256, 384, 512),
     ("rowwise_gw_hp", "c3", 384, 400, 272),
     ("rowwise_gw_hp", "c2", 1024, 768, 512),
