@@ -83,6 +83,12 @@ def main():
                     fn = lambda: ops.gemm(A, "e4m3", s, B, "e4m3", s, "tensor")  # noqa: E731
                 elif v == "mx":
                     fn = lambda: ops.gemm(A, "e4m3", sfa, B, "e4m3", sfb, "mx32")  # noqa: E731
+                elif v in ("mx_mn", "fp8_mn"):   # both operands MN-major (the backward's layout)
+                    At, Bt = A.t().contiguous(), B.t().contiguous()
+                    if v == "mx_mn":
+                        fn = lambda: ops.gemm(At, "e4m3", sfa, Bt, "e4m3", sfb, "mx32", a_mn=True, b_mn=True)  # noqa: E731
+                    else:
+                        fn = lambda: ops.gemm(At, "e4m3", s, Bt, "e4m3", s, "tensor", a_mn=True, b_mn=True)  # noqa: E731
                 elif v == "cublas_fp8":
                     a8, b8 = A.view(torch.float8_e4m3fn), B.view(torch.float8_e4m3fn)
                     fn = lambda: torch._scaled_mm(a8, b8.t(), scale_a=s, scale_b=s, out_dtype=torch.bfloat16)  # noqa: E731
