@@ -33,8 +33,14 @@
  *  - Inputs must be finite (PAPER.md:281 recipes assume it; R-c9).  NaN
  *    propagates through amax; it is not detected.
  *  - Thread safety: re-entrant; no mutable global state beyond cached device
- *    attributes, the lazily resolved cuTensorMapEncodeTiled entry point and
- *    the thread-local error string.
+ *    attributes, the lazily resolved cuTensorMapEncodeTiled entry point, the
+ *    thread-local error string, and the GEMM tile scheduler's counters: a
+ *    module-global device array of 2 x 4096 slots (no allocation in any call);
+ *    each GEMM launch takes the next slot (atomic round robin; launches under
+ *    CUDA-graph capture use a separate region, so a graph keeps its slot on
+ *    every replay) and the launch resets it when its last CTA pair has fetched
+ *    its last tile.  More than 4096 GEMM launches executing concurrently would
+ *    share slots; stream-ordered launches never do.
  *
  * Number formats (R-c1, R-c2, R-c10, R-c11)
  *  - FP8_E4M3: "FN" variant, no inf, NaN 0x7F/0xFF, max 448.
