@@ -1032,3 +1032,23 @@ def test_linear_rowwise_dual_launch_straddle(grid, monkeypatch):
     _tol_check(_np(Y).astype(np.float64), y, yb)
     _tol_check(_np(DX).astype(np.float64), dx, dxb)
     _tol_check(_np(DW).astype(np.float64), dw, dwb)
+
+
+@pytest.mark.parametrize("dual", ["1", "0"], ids=["xw_one_cast_launch", "separate_casts"])
+def test_linear_tensorwise_cast_launches(dual, monkeypatch):
+    """Tensorwise forward with X and W cast by one launch (default) or separately: identical bytes,
+    scales and outputs (bit-identical GEMM results), both in tolerance of the oracle."""
+    monkeypatch.setenv("FP8T_TW_DUAL", dual)
+    M, N, K = 640, 384, 512
+    x, w, dy = synth.linear_inputs("c2", M, N, K, seed=6)
+    y, yb, _ = olin.forward(x, w, "tensorwise")
+    dx, dxb, dw, dwb, _ = olin.backward(x, w, dy, "tensorwise")
+    plan = ops.LinearPlan(M, N, K, recipe="tensorwise", out_dtype=torch.float32)
+    saved = plan.new_saved()
+    X = _dev(x, torch.bfloat16)
+    Y = plan.forward(X, _dev(w, torch.bfloat16), saved)
+    DX, DW = plan.backward(_dev(dy, torch.bfloat16), saved)
+    torch.cuda.synchronize()
+    _tol_check(_np(Y).astype(np.float64), y, yb)
+    _tol_check(_np(DX).astype(np.float64), dx, dxb)
+    _tol_check(_np(DW).astype(np.float64), dw, dwb)
