@@ -585,16 +585,23 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
     uint32_t* ax = reinterpret_cast<uint32_t*>(fw.amax);
     uint32_t* aw = ax + 1;
     FP8T_CUDA(cudaMemsetAsync(ax, 0, 8, st), "memset");
-    // x_amax: amax(X) precomputed by X's producer (e.g. the previous layer's epilogue) -> no amax pass
-    if (!x_amax) FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
     const float* axp = x_amax ? x_amax : fw.amax;
     const uint8_t* wq = sv.wT;
-    // amax W, then X and W cast by one launch (measured on c2: casts 0.165 -> 0.158 ms per step);
-    // FP8T_TW_DUAL=0 casts them separately (X right after its amax, re-reading X's tail from L2)
+    // amax X and W by one launch, then X and W cast by one launch (measured on c2: casts 0.165 ->
+    // 0.158 ms per step); FP8T_TW_DUAL=0 keeps four launches (X's cast right after its amax).
+    // x_amax: amax(X) precomputed by X's producer (e.g. the previous layer's epilogue) -> no amax pass
     const char* twd = getenv("FP8T_TW_DUAL");
     const bool tw_dual = !(twd && twd[0] == '0');
     if (tw_dual && !w_fp8 && xb == wb) {
-      FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 1, aw, nullptr, nullptr, st), "amax w");
+      cudaError_t e = cudaErrorNotSupported;
+      if (!x_amax && x.ld == K && w.ld == K)
+        e = launch_amax_flat_dual(x.ptr, M * K, ax, w.ptr, N * K, aw, xb, st);
+      if (e != cudaErrorNotSupported) {
+        FP8T_CUDA(e, "amax x, w");
+      } else {
+        if (!x_amax) FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
+        FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 1, aw, nullptr, nullptr, st), "amax w");
+      }
       CastDual cd{};
       cd.x[0] = x.ptr; cd.R[0] = M; cd.C[0] = K; cd.ld[0] = x.ld; cd.amax_q[0] = axp; cd.amax_t[0] = axp;
       cd.q[0] = sv.xT; cd.scale_q[0] = (float*)sv.sx;
@@ -602,17 +609,18 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
       cd.amax_t[1] = fw.amax + 1; cd.q[1] = sv.wT; cd.scale_q[1] = (float*)sv.sw;
       FP8T_CUDA(launch_cast_dual(cd, xb, ff, 1, 0, st), "cast x, w");
     } else {
-    FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 1, 0, axp, axp, sv.xT, nullptr, (float*)sv.sx, nullptr, st),
-              "cast x");
-    if (w_fp8) {
-      wq = w_fp8->q;
-      FP8T_CUDA(cudaMemcpyAsync(sv.sw, w_fp8->scale, 4, cudaMemcpyDeviceToDevice, st), "copy w scale");
-    } else {
-      FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 1, aw, nullptr, nullptr, st), "amax w");
-      FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 1, 0, fw.amax + 1, fw.amax + 1, sv.wT, nullptr,
-                            (float*)sv.sw, nullptr, st),
-                "cast w");
-    }
+      if (!x_amax) FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
+      FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 1, 0, axp, axp, sv.xT, nullptr, (float*)sv.sx, nullptr, st),
+                "cast x");
+      if (w_fp8) {
+        wq = w_fp8->q;
+        FP8T_CUDA(cudaMemcpyAsync(sv.sw, w_fp8->scale, 4, cudaMemcpyDeviceToDevice, st), "copy w scale");
+      } else {
+        FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 1, aw, nullptr, nullptr, st), "amax w");
+        FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 1, 0, fw.amax + 1, fw.amax + 1, sv.wT, nullptr,
+                              (float*)sv.sw, nullptr, st),
+                  "cast w");
+      }
     }
     GemmProblem p{sv.xT, wq, ff, ff, 0, 0, sv.sx, sv.sw, 0, M, N, K, K, K, y, of32, N, 0, yam};
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");

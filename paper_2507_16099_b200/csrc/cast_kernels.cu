@@ -398,17 +398,26 @@ __global__ void __launch_bounds__(256) amax_tile_tma_kernel(const __grid_constan
 // 8 independent loads in flight per thread, |x| max on raw bit patterns (bf16: two 16-bit
 // lanes per word via __vmaxu2), one atomicMax per CTA.
 template <typename T, int U>
-__global__ void __launch_bounds__(256) amax_flat_kernel(const uint4* __restrict__ x, int64_t n16, uint32_t* out) {
+__global__ void __launch_bounds__(256) amax_flat_kernel(const uint4* __restrict__ x0, int64_t n0, uint32_t* out0,
+                                                        const uint4* __restrict__ x1, int64_t n1, uint32_t* out1,
+                                                        int g0) {
   // Each warp streams contiguous 512*U-byte chunks (U coalesced 512-B loads in flight per thread),
   // chunks strided over the grid; |x| max on raw bit patterns (bf16: two 16-bit lanes per word
-  // via __vmaxu2), one atomicMax per CTA.
+  // via __vmaxu2), one atomicMax per CTA.  Two tensors (X and W of the forward): CTAs [0, g0) stream
+  // the first, [g0, grid) the second.
   __shared__ uint32_t wred[8];
+  const bool second = (int)blockIdx.x >= g0;
+  const uint4* __restrict__ x = second ? x1 : x0;
+  const int64_t n16 = second ? n1 : n0;
+  uint32_t* out = second ? out1 : out0;
+  const int64_t bid = second ? (int64_t)blockIdx.x - g0 : (int64_t)blockIdx.x;
+  const int64_t nblk = second ? (int64_t)gridDim.x - g0 : (int64_t)g0;
   constexpr bool BF = sizeof(T) == 2;
   const uint32_t mask = BF ? 0x7FFF7FFFu : 0x7FFFFFFFu;
   uint32_t m = 0;
   const int lane = threadIdx.x & 31;
-  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t gwarp = (bid * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (nblk * blockDim.x) >> 5;
   auto fold = [&](const uint4& v) {
     if (BF) {
       m = __vmaxu2(m, v.x & mask); m = __vmaxu2(m, v.y & mask);
@@ -1012,10 +1021,11 @@ static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
     const unsigned g = (unsigned)(want < cap ? want : cap);
     const uint4* xv = reinterpret_cast<const uint4*>(x);
     LaunchScope ls(K_AMAX, st);
-    if (u == 4) amax_flat_kernel<T, 4><<<g, 256, 0, st>>>(xv, n16, at);
-    else if (u == 12) amax_flat_kernel<T, 12><<<g, 256, 0, st>>>(xv, n16, at);
-    else if (u == 16) amax_flat_kernel<T, 16><<<g, 256, 0, st>>>(xv, n16, at);
-    else amax_flat_kernel<T, 8><<<g, 256, 0, st>>>(xv, n16, at);
+    const int gi = (int)g;
+    if (u == 4) amax_flat_kernel<T, 4><<<g, 256, 0, st>>>(xv, n16, at, xv, 0, at, gi);
+    else if (u == 12) amax_flat_kernel<T, 12><<<g, 256, 0, st>>>(xv, n16, at, xv, 0, at, gi);
+    else if (u == 16) amax_flat_kernel<T, 16><<<g, 256, 0, st>>>(xv, n16, at, xv, 0, at, gi);
+    else amax_flat_kernel<T, 8><<<g, 256, 0, st>>>(xv, n16, at, xv, 0, at, gi);
     return cudaGetLastError();
   }
   const int64_t tiles = ((R + 127) / 128) * ((C + 127) / 128);
@@ -1094,6 +1104,27 @@ cudaError_t launch_amax_multi(const AmaxMultiArgs& a, cudaStream_t st) {
   const int64_t warps = total < cap ? total : cap;
   LaunchScope ls(K_AMAX, st);
   amax_multi_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Tensorwise amax of two contiguous tensors of one dtype in one launch (the forward's X and W): the
+// persistent grid is split between them in proportion to their sizes.
+cudaError_t launch_amax_flat_dual(const void* x0, int64_t n0_elems, uint32_t* out0, const void* x1, int64_t n1_elems,
+                                  uint32_t* out1, bool bf16, cudaStream_t st) {
+  const int es = bf16 ? 2 : 4;
+  if ((n0_elems * es) % 16 || (n1_elems * es) % 16 || n0_elems <= 0 || n1_elems <= 0) return cudaErrorNotSupported;
+  const int64_t a16 = n0_elems * es / 16, b16 = n1_elems * es / 16;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  const int64_t want = (a16 + b16 + 255) / 256;
+  const int g = (int)(want < cap ? want : cap);
+  if (g < 2) return cudaErrorNotSupported;
+  int g0 = (int)((double)g * (double)a16 / (double)(a16 + b16) + 0.5);
+  g0 = g0 < 1 ? 1 : (g0 > g - 1 ? g - 1 : g0);
+  const uint4* v0 = reinterpret_cast<const uint4*>(x0);
+  const uint4* v1 = reinterpret_cast<const uint4*>(x1);
+  LaunchScope ls(K_AMAX, st);
+  if (bf16) amax_flat_kernel<__nv_bfloat16, 8><<<g, 256, 0, st>>>(v0, a16, out0, v1, b16, out1, g0);
+  else amax_flat_kernel<float, 8><<<g, 256, 0, st>>>(v0, a16, out0, v1, b16, out1, g0);
   return cudaGetLastError();
 }
 

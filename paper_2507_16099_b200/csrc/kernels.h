@@ -43,6 +43,9 @@ cudaError_t launch_cast(const void* x, bool bf16, int fmt, int64_t R, int64_t C,
 cudaError_t launch_amax_dual(const void* x0, int64_t R0, int64_t C0, int64_t ld0, const void* x1, int64_t R1, int64_t C1,
                              int64_t ld1, int mode, uint32_t* ar0, uint32_t* ac0, uint32_t* ar1, uint32_t* ac1,
                              cudaStream_t st);
+// Tensorwise amax of two contiguous tensors (same dtype) in one launch; outputs pre-zeroed.
+cudaError_t launch_amax_flat_dual(const void* x0, int64_t n0_elems, uint32_t* out0, const void* x1, int64_t n1_elems,
+                                  uint32_t* out1, bool bf16, cudaStream_t st);
 // Two tensors (same format and scale modes) cast by one launch; tiles[] is filled by the launcher.
 struct CastDual {
   const void* x[2];
