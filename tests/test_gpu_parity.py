@@ -1052,3 +1052,29 @@ def test_linear_tensorwise_cast_launches(dual, monkeypatch):
     _tol_check(_np(Y).astype(np.float64), y, yb)
     _tol_check(_np(DX).astype(np.float64), dx, dxb)
     _tol_check(_np(DW).astype(np.float64), dw, dwb)
+
+
+@pytest.mark.parametrize("recipe", ["tensorwise", "rowwise"])
+def test_linear_strided_inputs(recipe):
+    """X and W as row-strided views (ld > K, e.g. slices of a wider activation / fused weight): the flat
+    amax cannot stream them, so the per-tensor strided amax runs, and the shared cast launch reads
+    them with their ld: same outputs as contiguous copies, bit for bit."""
+    M, N, K = 512, 384, 256
+    x, w, dy = synth.linear_inputs("c3" if recipe == "rowwise" else "c2", M, N, K, seed=9)
+    bf = torch.bfloat16
+    Xw = torch.zeros((M, K + 64), dtype=bf, device="cuda")
+    Ww = torch.zeros((N, K + 128), dtype=bf, device="cuda")
+    Xw[:, 32:32 + K] = _dev(x, bf)
+    Ww[:, 64:64 + K] = _dev(w, bf)
+    Xs, Ws = Xw[:, 32:32 + K], Ww[:, 64:64 + K]
+    G = _dev(dy, bf)
+    outs = []
+    for X, W in ((Xs, Ws), (Xs.contiguous(), Ws.contiguous())):
+        plan = ops.LinearPlan(M, N, K, recipe=recipe, out_dtype=torch.float32)
+        saved = plan.new_saved()
+        Y = plan.forward(X, W, saved).clone()
+        DX, DW = plan.backward(G, saved, x=X)
+        outs.append((Y, DX.clone(), DW.clone()))
+    torch.cuda.synchronize()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
