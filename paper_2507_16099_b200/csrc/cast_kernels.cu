@@ -985,12 +985,9 @@ static cudaError_t amax_tma_go(const CUtensorMap& m, int64_t R, int64_t C, int64
   constexpr int ST = 3;
   constexpr int smem = ST * 128 * 256 + 8 * 128 * 4 + 64 + ST * 8;
   auto kern = amax_tile_tma_kernel<MODE, ST>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // once per instantiation (thread-safe static initialisation)
+  static const cudaError_t attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (attr_err != cudaSuccess) return attr_err;
   int64_t cap = (int64_t)sm_count() * 2;
   const char* g = getenv("FP8T_CAST_GRID");   // tests: cap the persistent grid (many tiles per CTA)
   if (g && atoi(g) > 0 && atoi(g) < cap) cap = atoi(g);
@@ -1208,12 +1205,9 @@ static cudaError_t mx_tma_go(const CUtensorMap& m, int64_t R, int64_t C, uint8_t
                              uint8_t* sf1, cudaStream_t s) {
   auto kern = mx_cast_tma_kernel<FMT, RC, D0, D1, TR, ST>;
   constexpr int smem = MxSmem<ST, TR>::BYTES;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // once per instantiation (thread-safe static initialisation)
+  static const cudaError_t attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (attr_err != cudaSuccess) return attr_err;
   const int64_t tiles = (R >> 7) * (C >> 7);
   int64_t cap = (int64_t)sm_count() * (TR ? 1 : 2);
   const char* g = getenv("FP8T_CAST_GRID");   // tests: cap the persistent grid (many tiles per CTA)
