@@ -196,3 +196,118 @@ def test_rowwise_gw_hp_weight_grad_is_high_precision():
     assert np.array_equal(dx_h, dx_r)
     want = _frac_gemm(dy.T, x.T, np.ones(40, np.float32), np.ones(64, np.float32))
     np.testing.assert_allclose(dw_h, want, rtol=1e-12)
+
+
+# ---------------------------------------------------------------- tolerance-scale pins
+# abs_bound / mx_abs_bound set the scale of every random-data GEMM verdict
+# (|err| <= 1e-2 * sum_k |a||b|, BASELINE.json north_star), so they are pinned
+# against things other than themselves: an exact-rational brute force over the
+# ml_dtypes decoders (not oracle.codecs), the invariants bound >= |y| with
+# equality for non-negative operands, the exact 1/(s_a s_b) scaling, and the
+# high-precision product sum_k |x||w| of the unquantised inputs.
+
+def _ml_decode(codes, fmt):
+    import ml_dtypes
+    dt = ml_dtypes.float8_e4m3fn if fmt == E4M3 else ml_dtypes.float8_e5m2
+    return np.asarray(codes, np.uint8).view(dt).astype(np.float64)
+
+
+def _frac_abs(A, B, sa, sb):
+    M, K = A.shape
+    N = B.shape[0]
+    out = np.zeros((M, N))
+    for m in range(M):
+        for n in range(N):
+            acc = Fraction(0)
+            for k in range(K):
+                acc += abs(Fraction(float(A[m, k]))) * abs(Fraction(float(B[n, k])))
+            out[m, n] = float(acc / (Fraction(float(sa[m])) * Fraction(float(sb[n]))))
+    return out
+
+
+def _finite_codes(rng, shape, fmt):
+    c = rng.integers(0, 256, shape).astype(np.uint8)
+    c[(c & 0x7F) >= (0x7F if fmt == E4M3 else 0x7C)] = 0x91   # finite, negative
+    return c
+
+
+@pytest.mark.parametrize("fa,fb", [(E4M3, E4M3), (E5M2, E4M3), (E4M3, E5M2)])
+def test_abs_bound_vs_fraction(fa, fb):
+    rng = np.random.default_rng(11)
+    M, N, K = 4, 6, 11
+    a, b = _finite_codes(rng, (M, K), fa), _finite_codes(rng, (N, K), fb)
+    sa = rng.uniform(0.01, 3000, M).astype(np.float32)
+    sb = rng.uniform(0.01, 3000, N).astype(np.float32)
+    want = _frac_abs(_ml_decode(a, fa), _ml_decode(b, fb), sa, sb)
+    np.testing.assert_allclose(gemm.abs_bound(a, fa, sa, b, fb, sb), want, rtol=1e-13, atol=1e-300)
+    want_t = _frac_abs(_ml_decode(a, fa), _ml_decode(b, fb), np.full(M, sa[1]), np.full(N, sb[2]))
+    np.testing.assert_allclose(gemm.abs_bound(a, fa, sa[1], b, fb, sb[2]), want_t, rtol=1e-13, atol=1e-300)
+
+
+def test_mx_abs_bound_vs_fraction():
+    rng = np.random.default_rng(12)
+    M, N, K = 3, 5, 64
+    a, b = _finite_codes(rng, (M, K), E4M3), _finite_codes(rng, (N, K), E5M2)
+    asc = rng.integers(90, 160, (M, K // 32)).astype(np.uint8)
+    bsc = rng.integers(90, 160, (N, K // 32)).astype(np.uint8)
+    A, B = _ml_decode(a, E4M3), _ml_decode(b, E5M2)
+    got = gemm.mx_abs_bound(a, asc, E4M3, b, bsc, E5M2)
+    for m in range(M):
+        for n in range(N):
+            acc = Fraction(0)
+            for k in range(K):
+                acc += (abs(Fraction(float(A[m, k]))) * Fraction(2) ** (int(asc[m, k // 32]) - 127)
+                        * abs(Fraction(float(B[n, k]))) * Fraction(2) ** (int(bsc[n, k // 32]) - 127))
+            assert abs(got[m, n] - float(acc)) <= 1e-13 * float(acc) + 1e-300
+
+
+def test_abs_bound_invariants():
+    rng = np.random.default_rng(13)
+    M, N, K = 24, 20, 96
+    a, b = _finite_codes(rng, (M, K), E5M2), _finite_codes(rng, (N, K), E4M3)
+    sa = rng.uniform(1, 1e4, M).astype(np.float32)
+    sb = rng.uniform(1, 1e4, N).astype(np.float32)
+    bd = gemm.abs_bound(a, E5M2, sa, b, E4M3, sb)
+    y = gemm.gemm_ref(a, E5M2, sa, b, E4M3, sb)
+    assert np.all(bd >= np.abs(y) * (1 - 1e-15))
+    assert np.any(bd > 2 * np.abs(y))                       # mixed signs: the bound is not |y|
+    # non-negative operands: bound == y exactly (same products, no cancellation)
+    ap, bp = a & 0x7F, b & 0x7F
+    np.testing.assert_array_equal(gemm.abs_bound(ap, E5M2, sa, bp, E4M3, sb),
+                                  gemm.gemm_ref(ap, E5M2, sa, bp, E4M3, sb))
+    # sign flips of operands do not move the bound
+    np.testing.assert_array_equal(gemm.abs_bound(a ^ 0x80, E5M2, sa, b, E4M3, sb), bd)
+    # exact 1/(s_a s_b) scaling: doubling a scale halves the bound (powers of two are exact)
+    np.testing.assert_array_equal(gemm.abs_bound(a, E5M2, sa * 2, b, E4M3, sb), bd / 2)
+    np.testing.assert_array_equal(gemm.abs_bound(a, E5M2, sa, b, E4M3, sb * 4), bd / 4)
+    # mx: code +1 on one operand's block doubles that block's share only
+    asc = rng.integers(110, 140, (M, K // 32)).astype(np.uint8)
+    bsc = rng.integers(110, 140, (N, K // 32)).astype(np.uint8)
+    mb = gemm.mx_abs_bound(a, asc, E5M2, b, bsc, E4M3)
+    assert np.all(mb >= np.abs(gemm.mx_gemm_ref(a, asc, E5M2, b, bsc, E4M3)) * (1 - 1e-15))
+    np.testing.assert_array_equal(gemm.mx_abs_bound(a, asc + 1, E5M2, b, bsc, E4M3), 2 * mb)
+
+
+@pytest.mark.parametrize("recipe", [linear.TENSORWISE, linear.ROWWISE, linear.MXFP8])
+def test_linear_bounds_track_unquantised_product(recipe):
+    """The bound of each linear GEMM is sum_k |dec(a)/s_a||dec(b)/s_b|, i.e. the absolute
+    product of the DEQUANTISED operands, which are the hp inputs up to one FP8 rounding each
+    (relative error <= 2^-4 e4m3, 2^-3 e5m2, for normal values).  So it must sit within
+    [(1-2^-4)(1-2^-3), (1+2^-4)(1+2^-3)] of sum_k |x||w| of the hp inputs.  A dropped or
+    inverted 1/(s_a s_b) factor moves it by s_a s_b (>= 1e2 here)."""
+    # unit-variance data keeps every element away from FP8 underflow (exact relative bounds)
+    rng = np.random.default_rng(14)
+    M, N, K = 64, 96, 128
+    x = (rng.standard_normal((M, K)) * 3).astype(np.float32)
+    w = (rng.standard_normal((N, K)) * 0.02).astype(np.float32)
+    dy = (rng.standard_normal((M, N)) * 1e-3).astype(np.float32)
+    x[np.abs(x) < 0.1] = 0.1
+    w[np.abs(w) < 2e-3] = 2e-3
+    dy[np.abs(dy) < 1e-4] = 1e-4
+    _, yb, _ = linear.forward(x, w, recipe)
+    _, dxb, _, dwb, _ = linear.backward(x, w, dy, recipe)
+    X, W, G = (np.abs(t.astype(np.float64)) for t in (x, w, dy))
+    lo, hi = (1 - 2.0 ** -4) * (1 - 2.0 ** -3), (1 + 2.0 ** -4) * (1 + 2.0 ** -3)
+    for got, ref in ((yb, X @ W.T), (dxb, G @ W), (dwb, G.T @ X)):
+        r = got / ref
+        assert lo <= r.min() and r.max() <= hi, (recipe, r.min(), r.max())
