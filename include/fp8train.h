@@ -32,15 +32,20 @@
  *    Violations -> FP8_EALIGN.
  *  - Inputs must be finite (PAPER.md:281 recipes assume it; R-c9).  NaN
  *    propagates through amax; it is not detected.
- *  - Thread safety: re-entrant; no mutable global state beyond cached device
- *    attributes, the lazily resolved cuTensorMapEncodeTiled entry point, the
- *    thread-local error string, and the GEMM tile scheduler's counters: a
- *    module-global device array of 2 x 4096 slots (no allocation in any call);
- *    each GEMM launch takes the next slot (atomic round robin; launches under
- *    CUDA-graph capture use a separate region, so a graph keeps its slot on
- *    every replay) and the launch resets it when its last CTA pair has fetched
- *    its last tile.  More than 4096 GEMM launches executing concurrently would
- *    share slots; stream-ordered launches never do.
+ *  - Thread safety: re-entrant; no mutable global state beyond per-device
+ *    cached attributes (SM count, shared-memory limits), the lazily resolved
+ *    cuTensorMapEncodeTiled entry point, the thread-local error string, the
+ *    kernel-variant knobs (fp8_set_knob), and the GEMM tile scheduler's
+ *    counters: a module-global device array of 2 x 4096 slots per device (no
+ *    allocation in any call).  Each eager GEMM launch takes the next slot of
+ *    the first region (atomic round robin) and resets it when its last CTA
+ *    pair has fetched its last tile; more than 4096 GEMM launches executing
+ *    concurrently would share slots (stream-ordered launches never do).  A GEMM
+ *    captured into a CUDA graph takes a slot of the second region for good
+ *    (kept on every replay, never handed out again); after 4096 captured GEMMs
+ *    on a device, further captures use the static tile schedule.  Replays of
+ *    one captured graph (or of two execs instantiated from it) must therefore
+ *    not execute concurrently.
  *
  * Number formats (R-c1, R-c2, R-c10, R-c11)
  *  - FP8_E4M3: "FN" variant, no inf, NaN 0x7F/0xFF, max 448.
@@ -75,7 +80,7 @@
 extern "C" {
 #endif
 
-#define FP8TRAIN_ABI_VERSION 5
+#define FP8TRAIN_ABI_VERSION 6
 
 typedef enum {
   FP8_OK = 0,
@@ -249,7 +254,8 @@ fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,
  *   x_amax (nullable, device float[1], tensorwise only): amax(|X|) already known -- e.g. written
  *     by the epilogue of the GEMM that produced X -- so the X amax pass is skipped;
  *   y_amax (nullable, device float[1], any recipe): the GEMM epilogue writes amax(|Y|) of the
- *     stored (out_dtype-rounded) outputs, ready to be the next layer's x_amax.
+ *     stored (out_dtype-rounded) outputs, ready to be the next layer's x_amax.  It is zeroed on
+ *     `stream` only after every cast has read x_amax, so x_amax and y_amax may share a buffer.
  * fp8_linear_fwd(...) == fp8_linear_fwd_ex(..., x_amax = NULL, ..., y_amax = NULL, ...). */
 fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const float* x_amax, fp8_hp_t w,
                                const fp8_tensor_t* w_fp8, void* y, float* y_amax, void* saved,
@@ -469,6 +475,19 @@ const char* fp8_last_error(void);
 /* Number of kernels this library has launched in the calling process (all
  * threads); for launch accounting in benchmarks. */
 uint64_t fp8_launch_count(void);
+
+/* Kernel-variant knobs (host-side, process-wide, thread-safe).  The library never reads the
+ * process environment; every variant other than the product default is selected explicitly:
+ *   amax_tile_tma (1) | cast_grid (0 = uncapped) | amax_blocks_per_sm (8) | amax_loads (8) |
+ *   mx_cast_tma (1) | gemm_cta_group (2) | gemm_debug (0) | gemm_sched (1 = dynamic) |
+ *   mx_sf_split (1) | gemm_raster (-1 = per problem) | mx_n192 (0) | gemm_stages (3) |
+ *   gemm_epi (0 = by K) | mx_transposed (0; forward and backward of one linear must agree) |
+ *   tw_dual (1)   -- defaults in parentheses.
+ * A knob changes launches enqueued after the call.  Unknown name or out-of-range value:
+ * FP8_EINVAL, nothing changed.  fp8_reset_knobs restores every default. */
+fp8_status_t fp8_set_knob(const char* name, int value);
+fp8_status_t fp8_get_knob(const char* name, int* value);
+void fp8_reset_knobs(void);
 
 /* Per-launch device timing for benchmarks.  While enabled, every kernel this library
  * launches is bracketed by two CUDA events recorded on its own stream.

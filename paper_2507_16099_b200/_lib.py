@@ -46,6 +46,9 @@ SIGNATURES = {
     "fp8_last_error": (_c.c_char_p, []),
     "fp8_launch_count": (_c.c_uint64, []),
     "fp8_profile_enable": (None, [_c.c_int]),
+    "fp8_set_knob": (_c.c_int, [_c.c_char_p, _c.c_int]),
+    "fp8_get_knob": (_c.c_int, [_c.c_char_p, _c.POINTER(_c.c_int)]),
+    "fp8_reset_knobs": (None, []),
     "fp8_profile_collect": (_c.c_int, [_c.POINTER(_c.c_int), _c.POINTER(_c.c_float), _c.c_int]),
     "fp8_amax_workspace_bytes": (_c.c_size_t, [HP, _c.c_int]),
     "fp8_amax": (_c.c_int, [HP, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),

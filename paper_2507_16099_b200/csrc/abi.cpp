@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -21,6 +22,43 @@ namespace fp8t {
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// ---- kernel-variant knobs (defaults = the product path) ----
+struct KnobDef { const char* name; int def, lo, hi; };
+static const KnobDef kKnobs[KNOB_COUNT] = {
+    {"amax_tile_tma", 1, 0, 1},     {"cast_grid", 0, 0, 1 << 20},  {"amax_blocks_per_sm", 8, 1, 9},
+    {"amax_loads", 8, 4, 16},       {"mx_cast_tma", 1, 0, 1},      {"gemm_cta_group", 2, 1, 2},
+    {"gemm_debug", 0, 0, 1 << 16},  {"gemm_sched", 1, 0, 1},       {"mx_sf_split", 1, 0, 8},
+    {"gemm_raster", -1, -1, 64},    {"mx_n192", 0, 0, 1},          {"gemm_stages", 3, 3, 6},
+    {"gemm_epi", 0, 0, 8},          {"mx_transposed", 0, 0, 1},    {"tw_dual", 1, 0, 1},
+};
+static std::atomic<int> g_knobs[KNOB_COUNT] = {
+    {1}, {0}, {8}, {8}, {1}, {2}, {0}, {1}, {1}, {-1}, {0}, {3}, {0}, {0}, {1},
+};
+int knob(Knob k) { return g_knobs[k].load(std::memory_order_relaxed); }
+static int knob_index(const char* name) {
+  if (!name) return -1;
+  for (int i = 0; i < KNOB_COUNT; ++i)
+    if (std::strcmp(name, kKnobs[i].name) == 0) return i;
+  return -1;
+}
+
+// ---- per-device host caches ----
+cudaError_t current_device(int* dev) {
+  cudaError_t e = cudaGetDevice(dev);
+  if (e == cudaSuccess && *dev < 0) return cudaErrorInvalidDevice;
+  return e;
+}
+int device_sm_count() {
+  static std::atomic<int> cache[MAX_DEVICES];
+  int dev = 0;
+  if (current_device(&dev) != cudaSuccess) return 148;
+  int n = dev < MAX_DEVICES ? cache[dev].load(std::memory_order_relaxed) : 0;
+  if (n > 0) return n;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  if (dev < MAX_DEVICES) cache[dev].store(n, std::memory_order_relaxed);
+  return n;
+}
 
 // ---- optional per-launch event timing (fp8_profile_enable / fp8_profile_collect) ----
 struct ProfRec { int kind; cudaEvent_t a, b; };
@@ -83,12 +121,9 @@ static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 static inline size_t al(size_t b) { return (b + 255) & ~size_t(255); }
 static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 static inline size_t esize(fp8_dtype_t d) { return d == FP8_DT_F32 ? 4 : 2; }
-// MXFP8 linear: dim1 codes written transposed and read K-major (FP8T_MX_TRANSPOSED=1, the A/B
+// MXFP8 linear: dim1 codes written transposed and read K-major (knob mx_transposed = 1, the A/B
 // variant) instead of row-major and read MN-major (default).  Forward and backward must agree.
-static inline bool mx_transposed() {
-  const char* e = getenv("FP8T_MX_TRANSPOSED");
-  return e && e[0] == '1';
-}
+static inline bool mx_transposed() { return knob(KNOB_MX_TRANSPOSED) == 1; }
 
 static fp8_status_t check_hp(const fp8_hp_t& x, const char* name, bool need_ptr = true) {
   if (x.dtype != FP8_DT_F32 && x.dtype != FP8_DT_BF16) return fail(FP8_EINVAL, "%s: bad dtype", name);
@@ -129,6 +164,25 @@ using namespace fp8t;
 extern "C" {
 
 int fp8_abi_version(void) { return FP8TRAIN_ABI_VERSION; }
+
+fp8_status_t fp8_set_knob(const char* name, int value) {
+  const int i = knob_index(name);
+  if (i < 0) return fail(FP8_EINVAL, "unknown knob '%s'", name ? name : "(null)");
+  if (value < kKnobs[i].lo || value > kKnobs[i].hi)
+    return fail(FP8_EINVAL, "knob %s: value %d outside [%d, %d]", name, value, kKnobs[i].lo, kKnobs[i].hi);
+  g_knobs[i].store(value, std::memory_order_relaxed);
+  return FP8_OK;
+}
+fp8_status_t fp8_get_knob(const char* name, int* value) {
+  const int i = knob_index(name);
+  if (i < 0) return fail(FP8_EINVAL, "unknown knob '%s'", name ? name : "(null)");
+  if (!value) return fail(FP8_EINVAL, "value: null pointer");
+  *value = g_knobs[i].load(std::memory_order_relaxed);
+  return FP8_OK;
+}
+void fp8_reset_knobs(void) {
+  for (int i = 0; i < KNOB_COUNT; ++i) g_knobs[i].store(kKnobs[i].def, std::memory_order_relaxed);
+}
 const char* fp8_last_error(void) { return g_err.c_str(); }
 uint64_t fp8_launch_count(void) { return g_launches.load(); }
 
@@ -465,7 +519,7 @@ fp8_status_t check_w_fp8(const fp8_linear_cfg_t* cfg, const fp8_tensor_t* w_fp8,
   }
   if (cfg->recipe != FP8_RECIPE_MXFP8) return fail(FP8_EUNSUPPORTED, "w_fp8 needs the tensorwise or mxfp8 recipe");
   if (w_fp8->gran != (mx_transposed() ? FP8_GRAN_MX32 : FP8_GRAN_MX32_RM))
-    return fail(FP8_EINVAL, "w_fp8->gran must be FP8_GRAN_MX32_RM (FP8_GRAN_MX32 with FP8T_MX_TRANSPOSED=1)");
+    return fail(FP8_EINVAL, "w_fp8->gran must be FP8_GRAN_MX32_RM (FP8_GRAN_MX32 with knob mx_transposed = 1)");
   if (!bwd_dx) {
     FP8T_TRY(check_ptr(w_fp8->q, "w_fp8->q"));
     if (!w_fp8->scale) return fail(FP8_EINVAL, "w_fp8->scale: null pointer");
@@ -526,7 +580,13 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
   const int ff = cfg->fmt_fwd;
   const int of32 = cfg->out_dtype == FP8_DT_F32;
   uint32_t* yam = reinterpret_cast<uint32_t*>(y_amax);
-  if (yam) FP8T_CUDA(cudaMemsetAsync(yam, 0, 4, st), "memset y_amax");
+  // y_amax is zeroed right before the forward GEMM, after every cast has read x_amax, so a caller
+  // chaining layers through one buffer (x_amax == y_amax) gets X cast with the incoming amax
+  auto fwd_gemm = [&](const GemmProblem& p) -> fp8_status_t {
+    if (yam) FP8T_CUDA(cudaMemsetAsync(yam, 0, 4, st), "memset y_amax");
+    FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+    return FP8_OK;
+  };
 
   if (!saved) {
     // forward-only FP8 (inference / float8 dynamic activation + weight, PAPER.md:470-471, 636:
@@ -551,7 +611,7 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
                   "cast w");
       }
       GemmProblem p{iw.xq, wq, ff, ff, 0, 0, iw.sx, swp, 0, M, N, K, K, K, y, of32, N, 0, yam};
-      FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+      FP8T_TRY(fwd_gemm(p));
     } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {   // PerRow
       float* axr = iw.amax;
       float* awr = axr + M;
@@ -563,7 +623,7 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
       FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 0, awr, awr, iw.wq, nullptr, (float*)iw.sw, nullptr, st),
                 "cast w");
       GemmProblem p{iw.xq, iw.wq, ff, ff, 0, 0, iw.sx, iw.sw, 1, M, N, K, K, K, y, of32, N, 0, yam};
-      FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+      FP8T_TRY(fwd_gemm(p));
     } else {   // MXFP8: dim0 only
       const bool rc = cfg->mx_round == FP8_MX_RCEIL;
       FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, iw.xq, (uint8_t*)iw.sx, nullptr, nullptr, st), "mx x");
@@ -572,7 +632,7 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
       const uint8_t* wq = w_fp8 ? w_fp8->q : iw.wq;
       const void* swp = w_fp8 ? w_fp8->scale : iw.sw;
       GemmProblem p{iw.xq, wq, ff, ff, 0, 0, iw.sx, swp, 2, M, N, K, K, K, y, of32, N, 0, yam};
-      FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+      FP8T_TRY(fwd_gemm(p));
     }
     return FP8_OK;
   }
@@ -588,10 +648,9 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
     const float* axp = x_amax ? x_amax : fw.amax;
     const uint8_t* wq = sv.wT;
     // amax X and W by one launch, then X and W cast by one launch (measured on c2: casts 0.165 ->
-    // 0.158 ms per step); FP8T_TW_DUAL=0 keeps four launches (X's cast right after its amax).
+    // 0.158 ms per step); knob tw_dual = 0 keeps four launches (X's cast right after its amax).
     // x_amax: amax(X) precomputed by X's producer (e.g. the previous layer's epilogue) -> no amax pass
-    const char* twd = getenv("FP8T_TW_DUAL");
-    const bool tw_dual = !(twd && twd[0] == '0');
+    const bool tw_dual = knob(KNOB_TW_DUAL) == 1;
     if (tw_dual && !w_fp8 && xb == wb) {
       cudaError_t e = cudaErrorNotSupported;
       if (!x_amax && x.ld == K && w.ld == K)
@@ -623,7 +682,7 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
       }
     }
     GemmProblem p{sv.xT, wq, ff, ff, 0, 0, sv.sx, sv.sw, 0, M, N, K, K, K, y, of32, N, 0, yam};
-    FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+    FP8T_TRY(fwd_gemm(p));
   } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {
     const bool gw_hp = cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;   // X's column-scaled copy unused
     float* axr = fw.amax;
@@ -663,7 +722,7 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
                 "cast w");
     }
     GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N, 0, yam};
-    FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+    FP8T_TRY(fwd_gemm(p));
   } else {
     const bool rc = cfg->mx_round == FP8_MX_RCEIL, tr = mx_transposed();
     FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, fw.xq, fw.sfx, sv.xT, (uint8_t*)sv.sx, st, tr),
@@ -676,7 +735,7 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
     const uint8_t* wq = w_fp8 ? w_fp8->q : fw.wq;
     const void* swp = w_fp8 ? w_fp8->scale : fw.sfw;
     GemmProblem p{fw.xq, wq, ff, ff, 0, 0, fw.sfx, swp, 2, M, N, K, K, K, y, of32, N, 0, yam};
-    FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+    FP8T_TRY(fwd_gemm(p));
   }
   return FP8_OK;
 }
@@ -811,7 +870,7 @@ gemms:
   } else {
     const uint8_t* w1 = w_fp8 ? w_fp8->q_t : sv.wT;
     const void* s1 = w_fp8 ? w_fp8->scale_t : sv.sw;
-    // MXFP8 with transposed dim1 copies (FP8T_MX_TRANSPOSED=1), all operands K-major
+    // MXFP8 with transposed dim1 copies (knob mx_transposed = 1), all operands K-major
     // dX[M,K] = dY[M,N] . W  : A = dY (K-major over N), B = W^T [K,N]
     if (dx) ps[n++] = GemmProblem{bw.g, w1, fg, ff, 0, 0, bw.sg, s1, mode, M, K, N, N, N, dx, of32, K, 0, dxam};
     // dW[N,K] = dY^T[N,M] . X : A = dY^T [N,M], B = X^T [K,M]

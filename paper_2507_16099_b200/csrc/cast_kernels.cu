@@ -960,22 +960,15 @@ __global__ void __launch_bounds__(256) transpose_u8_kernel(const uint8_t* __rest
 // ---------------------------------------------------------------------------
 // Host launchers
 // ---------------------------------------------------------------------------
-static int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+static int sm_count() { return device_sm_count(); }
 static inline dim3 tile_grid(int64_t R, int64_t C) { return dim3((unsigned)((C + 127) / 128), (unsigned)((R + 127) / 128)); }
 
-// FP8T_AMAX_TILE=0 selects the register-only amax_tile_kernel (A/B comparisons).
-static bool amax_tile_use_tma() {
-  const char* e = getenv("FP8T_AMAX_TILE");
-  return !(e && e[0] == '0');
+// knob amax_tile_tma = 0 selects the register-only amax_tile_kernel (A/B comparisons).
+static bool amax_tile_use_tma() { return knob(KNOB_AMAX_TILE_TMA) == 1; }
+// knob cast_grid > 0 caps a persistent grid (tests: many tiles per CTA)
+static int64_t cap_grid(int64_t cap) {
+  const int g = knob(KNOB_CAST_GRID);
+  return (g > 0 && g < cap) ? g : cap;
 }
 
 template <int MODE>
@@ -985,12 +978,9 @@ static cudaError_t amax_tma_go(const CUtensorMap& m, int64_t R, int64_t C, int64
   constexpr int ST = 3;
   constexpr int smem = ST * 128 * 256 + 8 * 128 * 4 + 64 + ST * 8;
   auto kern = amax_tile_tma_kernel<MODE, ST>;
-  // once per instantiation (thread-safe static initialisation)
-  static const cudaError_t attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const cudaError_t attr_err = ensure_smem<amax_tile_tma_kernel<MODE, ST>>(smem);
   if (attr_err != cudaSuccess) return attr_err;
-  int64_t cap = (int64_t)sm_count() * 2;
-  const char* g = getenv("FP8T_CAST_GRID");   // tests: cap the persistent grid (many tiles per CTA)
-  if (g && atoi(g) > 0 && atoi(g) < cap) cap = atoi(g);
+  const int64_t cap = cap_grid((int64_t)sm_count() * 2);
   if (!m1) {
     d = AmaxSecond{};
     d.tiles0 = (int)tiles;
@@ -1008,11 +998,10 @@ static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
   const T* p = static_cast<const T*>(x);
   if (mode == 1 && ld == C) {
     const int64_t n16 = R * C * (int64_t)sizeof(T) / 16;
-    // tuning knob FP8T_AMAX_CFG = "<blocks per SM><loads/thread: 4,8,C=12,G=16>"; default "88" (measured
-    // 5.2 TB/s pure read on C2's dY, vs 6.45 TB/s for a read+write copy and 3.0 for torch.amax)
-    const char* e = getenv("FP8T_AMAX_CFG");
-    const int bps = (e && e[0] >= '1' && e[0] <= '9') ? e[0] - '0' : 8;
-    const int u = (e && e[1] == 'C') ? 12 : (e && e[1] == 'G') ? 16 : (e && e[1] == '4') ? 4 : 8;
+    // tuning knobs amax_blocks_per_sm / amax_loads (16-byte loads per thread: 4, 8, 12, 16); default
+    // 8 / 8 (measured 5.2 TB/s pure read on C2's dY, vs 6.45 TB/s for a read+write copy and 3.0 for torch.amax)
+    const int bps = knob(KNOB_AMAX_BLOCKS_PER_SM);
+    const int u = knob(KNOB_AMAX_LOADS);
     const int64_t cap = (int64_t)sm_count() * bps;
     const int64_t want = (n16 + 255) / 256;
     const unsigned g = (unsigned)(want < cap ? want : cap);
@@ -1205,13 +1194,10 @@ static cudaError_t mx_tma_go(const CUtensorMap& m, int64_t R, int64_t C, uint8_t
                              uint8_t* sf1, cudaStream_t s) {
   auto kern = mx_cast_tma_kernel<FMT, RC, D0, D1, TR, ST>;
   constexpr int smem = MxSmem<ST, TR>::BYTES;
-  // once per instantiation (thread-safe static initialisation)
-  static const cudaError_t attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const cudaError_t attr_err = ensure_smem<mx_cast_tma_kernel<FMT, RC, D0, D1, TR, ST>>(smem);
   if (attr_err != cudaSuccess) return attr_err;
   const int64_t tiles = (R >> 7) * (C >> 7);
-  int64_t cap = (int64_t)sm_count() * (TR ? 1 : 2);
-  const char* g = getenv("FP8T_CAST_GRID");   // tests: cap the persistent grid (many tiles per CTA)
-  if (g && atoi(g) > 0 && atoi(g) < cap) cap = atoi(g);
+  const int64_t cap = cap_grid((int64_t)sm_count() * (TR ? 1 : 2));
   LaunchScope ls(K_MX, s);
   kern<<<(unsigned)(tiles < cap ? tiles : cap), 256, smem, s>>>(m, R, C, q0, sf0, q1, sf1);
   return cudaGetLastError();
@@ -1240,11 +1226,8 @@ static cudaError_t mx_tma_launch_t(const void* x, int64_t R, int64_t C, int64_t 
   return mx_tma_go<FMT, RC, false, true, false, 3>(m, R, C, q0, sf0, q1, sf1, s);
 }
 
-// FP8T_MX_CAST=0 selects the register-only mx_cast_kernel (A/B comparisons; fp32 inputs always use it).
-static bool mx_use_tma() {
-  const char* e = getenv("FP8T_MX_CAST");
-  return !(e && e[0] == '0');
-}
+// knob mx_cast_tma = 0 selects the register-only mx_cast_kernel (A/B comparisons; fp32 inputs always use it).
+static bool mx_use_tma() { return knob(KNOB_MX_CAST_TMA) == 1; }
 
 cudaError_t launch_mx_cast(const void* x, bool bf16, int fmt, bool rceil, int64_t R, int64_t C, int64_t ld,
                            uint8_t* q0, uint8_t* sf0, uint8_t* q1, uint8_t* sf1, cudaStream_t s, bool tr1) {

@@ -19,7 +19,7 @@
 // KS = 2 K atoms (256-deep K, 64 KB per CTA, 3 stages): 8 MMAs per full/empty barrier round
 // trip, which halves the per-MMA synchronisation overhead of the single-atom ring (measured
 // +10-25% on the C2 shapes).
-// CG = 1: a single CTA computes 128 x 256 (kept as a reference variant; FP8T_GEMM_CTA_GROUP=1).
+// CG = 1: a single CTA computes 128 x 256 (kept as a reference variant; knob gemm_cta_group = 1).
 // Accumulators are double-buffered in TMEM (2 x 256 columns) for the plain FP8 kinds so the
 // epilogue of tile i overlaps the mainloop of tile i+1; the MX kind keeps one accumulator
 // (256 columns) plus the scale-factor columns (E8M0 tiles loaded by TMA next to the operands,
@@ -885,23 +885,11 @@ static bool make_operand_map(CUtensorMap* m, const uint8_t* ptr, bool mn_major, 
   return r == CUDA_SUCCESS;
 }
 
-static int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+static int num_sms() { return device_sm_count(); }
 
-// CTA-pair mode for the plain FP8 kinds; FP8T_GEMM_CTA_GROUP=1 forces single-CTA tiles
+// CTA-pair mode for the plain FP8 kinds; knob gemm_cta_group = 1 forces single-CTA tiles
 // (used by the tests to cover both code paths).
-static int cta_group_for() {
-  const char* e = getenv("FP8T_GEMM_CTA_GROUP");
-  return (e && e[0] == '1') ? 1 : 2;
-}
+static int cta_group_for() { return knob(KNOB_GEMM_CTA_GROUP) == 1 ? 1 : 2; }
 
 // E8M0 blocked scale buffer of an MX operand with `rows` rows viewed as a 2-D u32 tensor
 // [rows/128 * K/128 tiles][128 words]; a box of KS consecutive tiles = KS K atoms.
@@ -975,16 +963,21 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
 // DESIGN.md §5).  Measured (bench, 1.97 GHz): c2 step GEMMs 1.963 ms row-major -> 1.925 ms (16); 8: 1.939,
 // 32: 2.02, 64: 2.16; c4 8.42-8.47 ms (8, 16) vs 9.09 (32), 9.78 (64); c3 layer step -1 to -3 %.
 // (Round r01c chose row-major when all of B fit ~80 MB of L2; with the dynamic scheduler the grouped
-// raster is as good or better for every shape measured.)  FP8T_GEMM_RASTER overrides (0 = row-major).
+// raster is as good or better for every shape measured.)  knob gemm_raster overrides (0 = row-major).
 static int choose_raster(const GemmProblem&, bool) { return GROUP_M; }
 
-// This launch's slot of g_sched on the current device (round robin over SCHED_SLOTS; launches under
-// stream capture use the graph region).
-static unsigned* sched_slot(cudaStream_t st) {
-  static std::atomic<unsigned*> base[64];
-  static std::atomic<unsigned> next_slot{0}, next_graph_slot{0};
+// This launch's slot of g_sched on the current device: eager launches round-robin over
+// [0, SCHED_SLOTS); a launch under stream capture takes the next unused slot of the graph region,
+// which is never recycled -- once it is used up (SCHED_SLOTS captured GEMMs on this device),
+// *exhausted is set and the caller falls back to the static round-robin schedule, so two graph
+// nodes never share a counter.  One captured node keeps its slot for every replay: replays of the
+// same graph (or of two execs instantiated from it) must not run concurrently (fp8train.h).
+static unsigned* sched_slot(cudaStream_t st, bool* exhausted) {
+  static std::atomic<unsigned*> base[MAX_DEVICES];
+  static std::atomic<unsigned> next_slot[MAX_DEVICES], next_graph_slot[MAX_DEVICES];
+  *exhausted = false;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (current_device(&dev) != cudaSuccess || dev >= MAX_DEVICES) return nullptr;
   unsigned* b = base[dev].load();
   if (!b) {
     void* p = nullptr;
@@ -994,19 +987,21 @@ static unsigned* sched_slot(cudaStream_t st) {
   }
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return nullptr;
-  if (cs == cudaStreamCaptureStatusActive) return b + 2 * (SCHED_SLOTS + next_graph_slot.fetch_add(1) % SCHED_SLOTS);
-  return b + 2 * (next_slot.fetch_add(1) % SCHED_SLOTS);
+  if (cs == cudaStreamCaptureStatusActive) {
+    const unsigned g = next_graph_slot[dev].fetch_add(1);
+    if (g >= (unsigned)SCHED_SLOTS) {
+      *exhausted = true;
+      return nullptr;
+    }
+    return b + 2 * (SCHED_SLOTS + g);
+  }
+  return b + 2 * (next_slot[dev].fetch_add(1) % SCHED_SLOTS);
 }
 
 template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bool E8 = false, int BNT = 256>
 static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   using L = Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8, BNT>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes);
-  });
+  const cudaError_t attr_err = ensure_smem<fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8, BNT>>(L::bytes);
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m0[4], m1[4];
   GemmArgs a{};
@@ -1029,21 +1024,21 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     a.num_tiles = a.t1;
   }
   {
-    const char* d = getenv("FP8T_GEMM_DEBUG");
-    a.debug = d ? atoi(d) : 0;
-    // FP8T_GEMM_SCHED=static: round-robin tiles (A/B); default: dynamic scheduler
-    const char* sc = getenv("FP8T_GEMM_SCHED");
-    if (!(sc && sc[0] == 's')) {
-      a.sched = sched_slot(st);
-      if (!a.sched) return cudaErrorInvalidValue;
+    a.debug = knob(KNOB_GEMM_DEBUG);
+    // knob gemm_sched = 0: round-robin tiles (A/B); default: dynamic scheduler.  A launch under
+    // stream capture whose graph slot region is exhausted also takes the static schedule (no slot
+    // is ever shared by two graph nodes).
+    if (knob(KNOB_GEMM_SCHED) == 1) {
+      bool exhausted = false;
+      a.sched = sched_slot(st, &exhausted);
+      if (!a.sched && !exhausted) return cudaErrorInvalidValue;
     }
-    const char* sf = getenv("FP8T_MX_SF_SPLIT");
-    a.sf_split = sf ? atoi(sf) : 1;
-    // raster per problem (choose_raster); FP8T_GEMM_RASTER overrides for every problem
-    const char* r = getenv("FP8T_GEMM_RASTER");
-    a.group_m = r ? atoi(r) : GROUP_M;
-    a.p0.raster = r ? a.group_m : choose_raster(ps[0], BF);
-    a.p1.raster = r ? a.group_m : (n > 1 ? choose_raster(ps[1], BF) : a.p0.raster);
+    a.sf_split = knob(KNOB_MX_SF_SPLIT);
+    // raster per problem (choose_raster); knob gemm_raster >= 0 overrides for every problem
+    const int r = knob(KNOB_GEMM_RASTER);
+    a.group_m = r >= 0 ? r : GROUP_M;
+    a.p0.raster = r >= 0 ? a.group_m : choose_raster(ps[0], BF);
+    a.p1.raster = r >= 0 ? a.group_m : (n > 1 ? choose_raster(ps[1], BF) : a.p0.raster);
   }
   const int slots = num_sms() / CG;
   // grouped: the tile count depends on the device-side offsets -> a full persistent grid
@@ -1093,27 +1088,26 @@ cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st) {
   const int cg = cta_group_for();
   if (ps[0].scale_mode == 2) {
     if (cg == 1) return launch_t<true, 1, 4, 1>(ps, n, st);
-    // FP8T_MX_N192=1 (K-major operands only): N = 192 tiles with double-buffered accumulators.  Measured
+    // knob mx_n192 = 1 (K-major operands only): N = 192 tiles with double-buffered accumulators.  Measured
     // 18 % fewer flop/clk/SM than N = 256 with one accumulator (c4 shape 10.5k vs 12.8k): the extra
     // operand traffic per flop costs more than the accumulator hand-over saves.  Kept as an option.
     bool kmaj = true;
     for (int i = 0; i < n; ++i) kmaj = kmaj && !ps[i].a_mn && !ps[i].b_mn;
-    const char* e = getenv("FP8T_MX_N192");
-    if (kmaj && e && e[0] == '1') return launch_t<true, 2, 3, 2, false, false, false, 192>(ps, n, st);
+    if (kmaj && knob(KNOB_MX_N192) == 1) return launch_t<true, 2, 3, 2, false, false, false, 192>(ps, n, st);
     return launch_t<true, 2, 3, 2>(ps, n, st);
   }
   if (cg == 1) return launch_t<false, 1, 4, 1>(ps, n, st);
   // default: 3 stages x 2 K atoms (64 KB per CTA per stage, 8 MMAs per barrier round trip);
-  // FP8T_GEMM_STAGES=6 selects 6 x 1 atom (4 MMAs per round trip) for comparison
-  const char* e = getenv("FP8T_GEMM_STAGES");
-  if (e && e[0] == '6') return launch_t<false, 2, 6, 1>(ps, n, st);
-  if (e && e[0] == '4') return launch_t<false, 2, 4, 1>(ps, n, st);
+  // knob gemm_stages = 6 selects 6 x 1 atom (4 MMAs per round trip) for comparison
+  const int stages = knob(KNOB_GEMM_STAGES);
+  if (stages == 6) return launch_t<false, 2, 6, 1>(ps, n, st);
+  if (stages == 4) return launch_t<false, 2, 4, 1>(ps, n, st);
   // short-K launches (tiles of <= 1024-deep K) are epilogue-bound: 8 epilogue warps (measured: K = 1024
   // 7.5k -> 8.6k flop/clk/SM; K = 2048 10.6k with 4 warps vs 9.9k with 8)
   bool short_k = false;
   for (int i = 0; i < n; ++i) short_k = short_k || ps[i].K <= 1024;
-  const char* ew = getenv("FP8T_GEMM_EPI");
-  if (ew) short_k = ew[0] == '8';
+  const int epi = knob(KNOB_GEMM_EPI);
+  if (epi) short_k = epi == 8;
   return short_k ? launch_t<false, 2, 3, 2, false, false, true>(ps, n, st) : launch_t<false, 2, 3, 2>(ps, n, st);
 }
 

@@ -4,10 +4,53 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <mutex>
 
 namespace fp8t {
 
 void count_launch();
+
+// ---- kernel-variant knobs (fp8_set_knob / fp8_get_knob) ----
+// The defaults are the product path; the other values are A/B variants the tests and tools/
+// select explicitly.  Read with relaxed atomics on the host per launch -- never from the process
+// environment, so results cannot depend on the caller's environment.
+enum Knob {
+  KNOB_AMAX_TILE_TMA = 0,   // 1: TMA-ring row/col amax strip kernel; 0: register-only tile kernel
+  KNOB_CAST_GRID,           // >0: cap the persistent cast / amax / MX grids (tests: many tiles per CTA)
+  KNOB_AMAX_BLOCKS_PER_SM,  // flat tensorwise amax: resident CTAs per SM (1..9)
+  KNOB_AMAX_LOADS,          // flat tensorwise amax: 16-byte loads in flight per thread (4, 8, 12, 16)
+  KNOB_MX_CAST_TMA,         // 1: TMA-ring MX cast (bf16); 0: register-only MX cast
+  KNOB_GEMM_CTA_GROUP,      // 2: CTA-pair tcgen05 tiles; 1: single-CTA tiles
+  KNOB_GEMM_DEBUG,          // tools/gemm_bench.py pipeline-isolation modes (0 = off)
+  KNOB_GEMM_SCHED,          // 1: dynamic tile scheduler; 0: static round-robin tiles
+  KNOB_MX_SF_SPLIT,         // MX GEMM scale-factor copier split (1 = default)
+  KNOB_GEMM_RASTER,         // <0: per-problem raster (choose_raster); >=0: fixed group width for all
+  KNOB_MX_N192,             // 1: MX GEMM with N = 192 tiles, double-buffered accumulators
+  KNOB_GEMM_STAGES,         // 3: 3 stages x 2 K atoms; 4 / 6: 4 / 6 stages x 1 atom
+  KNOB_GEMM_EPI,            // 0: epilogue warps by K (8 for K <= 1024, else 4); 4 / 8: forced
+  KNOB_MX_TRANSPOSED,       // 1: MX dim1 copies written transposed, read K-major (fwd and bwd must agree)
+  KNOB_TW_DUAL,             // 1: tensorwise forward X/W amax and cast by one launch each; 0: four launches
+  KNOB_COUNT
+};
+int knob(Knob k);
+
+// Multiprocessor count of the current device (cached per device).
+int device_sm_count();
+// Once per (kernel, device): raise the dynamic shared-memory limit of `Kern` to `bytes`.  The
+// attribute is per device context, so a process driving several GPUs sets it on each.
+constexpr int MAX_DEVICES = 64;
+cudaError_t current_device(int* dev);
+template <auto Kern>
+cudaError_t ensure_smem(int bytes) {
+  static std::once_flag flags[MAX_DEVICES];
+  static cudaError_t errs[MAX_DEVICES];
+  int dev = 0;
+  cudaError_t e = current_device(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= MAX_DEVICES) return cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  std::call_once(flags[dev], [&] { errs[dev] = cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
+  return errs[dev];
+}
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (nullptr if unavailable).
 PFN_cuTensorMapEncodeTiled_v12000 get_encode();

@@ -252,3 +252,37 @@ class GroupedPlan:
 
 def launch_count():
     return int(L.lib.fp8_launch_count())
+
+
+def set_knob(name, value):
+    """fp8_set_knob: select a kernel variant (A/B experiments, tests); defaults are the product path."""
+    L.check(L.lib.fp8_set_knob(name.encode(), int(value)), "fp8_set_knob")
+
+
+def get_knob(name):
+    v = ctypes.c_int(0)
+    L.check(L.lib.fp8_get_knob(name.encode(), ctypes.byref(v)), "fp8_get_knob")
+    return v.value
+
+
+def reset_knobs():
+    L.lib.fp8_reset_knobs()
+
+
+class knobs:
+    """Context manager: ``with ops.knobs(gemm_sched=0): ...`` sets knobs and restores them on exit."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_knob(k)
+            set_knob(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            set_knob(k, v)
+        return False

@@ -29,3 +29,13 @@ def read_golden(name):
 @pytest.fixture
 def golden():
     return read_golden
+
+
+@pytest.fixture
+def knob():
+    """Select kernel variants through fp8_set_knob for one test; every knob is restored to the
+    product default afterwards (the library never reads the process environment)."""
+    from paper_2507_16099_b200 import ops
+    ops.reset_knobs()
+    yield ops.set_knob
+    ops.reset_knobs()

@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol(L):
 
 
 def test_abi_version(L):
-    assert L.lib.fp8_abi_version() == 5
+    assert L.lib.fp8_abi_version() == 6
 
 
 def test_sizes_host_only(L):

@@ -215,20 +215,16 @@ def _grid_operands(M, N, K, seed=0):
 
 @pytest.fixture(params=["2", "2e4", "2rr", "2s6", "1"],
                 ids=["cta_pair", "cta_pair_epi4", "cta_pair_roundrobin", "cta_pair_1atom", "single_cta"])
-def cta_group(request, monkeypatch):
+def cta_group(request, knob):
     """Run a GEMM test with each kernel variant: CTA pair (cta_group::2) with 2-atom stages
     (default: 8 epilogue warps at K <= 1024, dynamic tile scheduler), the same with 4 epilogue
     warps (the long-K default), with static round-robin tiles, CTA pair with 1-atom stages, single CTA."""
-    monkeypatch.setenv("FP8T_GEMM_CTA_GROUP", request.param[0])
-    monkeypatch.setenv("FP8T_GEMM_STAGES", "6" if request.param == "2s6" else "3")
+    knob("gemm_cta_group", int(request.param[0]))
+    knob("gemm_stages", 6 if request.param == "2s6" else 3)
     if request.param == "2e4":
-        monkeypatch.setenv("FP8T_GEMM_EPI", "4")
-    else:
-        monkeypatch.delenv("FP8T_GEMM_EPI", raising=False)
+        knob("gemm_epi", 4)
     if request.param == "2rr":   # static round-robin tiles instead of the dynamic scheduler
-        monkeypatch.setenv("FP8T_GEMM_SCHED", "static")
-    else:
-        monkeypatch.delenv("FP8T_GEMM_SCHED", raising=False)
+        knob("gemm_sched", 0)
     return request.param
 
 
@@ -297,10 +293,10 @@ def _block(codes_logical):
 @pytest.mark.parametrize("fa,fb", [(E4M3, E4M3), (E5M2, E4M3)])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 128), (256, 384, 512), (384, 640, 384)])
 @pytest.mark.parametrize("majors", ["KK", "KM", "MM", "MK"])
-def test_gemm_mx_tolerance(fa, fb, M, N, K, majors, cta_group, monkeypatch):
+def test_gemm_mx_tolerance(fa, fb, M, N, K, majors, cta_group, knob):
     # MN-major operands keep the same logical [rows, K/32] scale factors (blocked layout)
     if cta_group == "2rr" and majors == "KK":   # also cover the optional N = 192 MX tiles
-        monkeypatch.setenv("FP8T_MX_N192", "1")
+        knob("mx_n192", 1)
     a = synth.tensor_c4("x", (M, K), seed=6)
     b = synth.tensor_c4("w", (N, K), seed=6)
     qa, sa = omx.quantize_dim0(a, fa)
@@ -359,10 +355,10 @@ def test_linear_fwd_bwd(recipe, cfg, M, N, K):
 
 @pytest.mark.parametrize("transposed", ["0", "1"], ids=["dim1_rowmajor_mn", "dim1_transposed_k"])
 @pytest.mark.parametrize("mx_round", ["floor", "rceil"])
-def test_linear_mx_dim1_layouts(transposed, mx_round, monkeypatch):
+def test_linear_mx_dim1_layouts(transposed, mx_round, knob):
     """MXFP8 backward operands: dim1 codes kept row-major and read MN-major (default) or written
-    transposed and read K-major (FP8T_MX_TRANSPOSED=1): same results within the bound."""
-    monkeypatch.setenv("FP8T_MX_TRANSPOSED", transposed)
+    transposed and read K-major (knob mx_transposed = 1): same results within the bound."""
+    knob("mx_transposed", int(transposed))
     M, N, K = 384, 640, 256
     x, w, dy = synth.linear_inputs("c4", M, N, K, seed=2)
     y, yb, _ = olin.forward(x, w, "mxfp8", mx_mode=mx_round)
@@ -538,10 +534,10 @@ def test_amax_handover_chain():
 @pytest.mark.parametrize("grid", ["1", "3"])
 @pytest.mark.parametrize("gran", ["mx32", "mx32_rm"])
 @pytest.mark.parametrize("fmt,mode", [(E4M3, omx.FLOOR), (E5M2, omx.RCEIL)])
-def test_mx_cast_persistent_ring(grid, gran, fmt, mode, monkeypatch):
+def test_mx_cast_persistent_ring(grid, gran, fmt, mode, knob):
     # the TMA-pipelined MX cast walks many tiles per CTA when the grid is capped: every
     # shared-memory ring slot is refilled several times (mbarrier parity wrap-around)
-    monkeypatch.setenv("FP8T_CAST_GRID", grid)
+    knob("cast_grid", int(grid))
     R, C = 512, 1280   # 40 tiles
     x = synth.tensor_c4("x", (R, C), seed=5)
     q0, s0 = omx.quantize_dim0(x, fmt, mode)
@@ -558,10 +554,10 @@ def test_mx_cast_persistent_ring(grid, gran, fmt, mode, monkeypatch):
 
 
 @pytest.mark.parametrize("impl", ["0", "1"])
-def test_mx_cast_impls_agree_c4_sized(impl, monkeypatch):
-    # both MX cast kernels (register-only: FP8T_MX_CAST=0; TMA ring: default) on a C4-like
+def test_mx_cast_impls_agree_c4_sized(impl, knob):
+    # both MX cast kernels (register-only: knob mx_cast_tma = 0; TMA ring: default) on a C4-like
     # tensor with many tiles per CTA, sampled rows against the oracle
-    monkeypatch.setenv("FP8T_MX_CAST", impl)
+    knob("mx_cast_tma", int(impl))
     R, C = 2048, 8192
     x = synth.tensor_c4("x", (R, C), seed=7)
     out = ops.cast(_dev(x, torch.bfloat16), "e4m3", "mx32_rm", want_q=True, want_qt=True)
@@ -817,12 +813,11 @@ def test_grouped_single_expert_equals_linear():
 
 @pytest.mark.parametrize("grid", ["0", "1", "5"])
 @pytest.mark.parametrize("impl", ["1", "0"])
-def test_amax_tile_strips(grid, impl, monkeypatch):
-    """Row / column / dual amax on 128-multiple shapes (the TMA strip kernel, FP8T_AMAX_TILE=1, and the
+def test_amax_tile_strips(grid, impl, knob):
+    """Row / column / dual amax on 128-multiple shapes (the TMA strip kernel, knob amax_tile_tma = 1, and the
     register kernel), with capped persistent grids so CTAs cross row strips: bit-exact vs the oracle."""
-    if grid != "0":
-        monkeypatch.setenv("FP8T_CAST_GRID", grid)
-    monkeypatch.setenv("FP8T_AMAX_TILE", impl)
+    knob("cast_grid", int(grid))
+    knob("amax_tile_tma", int(impl))
     x = synth.tensor_c3("x", (384, 1280), seed=9)
     X = _dev(x, torch.bfloat16)
     assert np.array_equal(_bits(_np(ops.amax(X, "row"))), _bits(fp8.amax(x, 1)))
@@ -932,13 +927,12 @@ def test_p2p_two_processes_ipc():
 
 
 @pytest.mark.parametrize("epi", ["8", "4"])
-def test_gemm_scheduler_long_launch_sequence(epi, monkeypatch):
+def test_gemm_scheduler_long_launch_sequence(epi, knob):
     """> 4096 back-to-back GEMM launches without a host sync (the dynamic tile scheduler's counter slots
     wrap around; slots are reset by each launch's last pair), mixing tensorwise, MXFP8 and two-problem
     launches: every launch's output stays bit-identical to the first one's (each tile is computed by
     one CTA pair in a fixed K order, so the bits do not depend on the schedule)."""
-    monkeypatch.setenv("FP8T_GEMM_EPI", epi)
-    monkeypatch.delenv("FP8T_GEMM_SCHED", raising=False)
+    knob("gemm_epi", int(epi))
     g = torch.Generator(device="cuda").manual_seed(3)
     M, N, K = 768, 1024, 512
     A = torch.randint(0, 0x70, (M, K), dtype=torch.uint8, device="cuda", generator=g)
@@ -1012,13 +1006,12 @@ def test_linear_cuda_graph_replay(recipe):
 
 
 @pytest.mark.parametrize("grid", ["3", "7", "0"])
-def test_linear_rowwise_dual_launch_straddle(grid, monkeypatch):
+def test_linear_rowwise_dual_launch_straddle(grid, knob):
     """Rowwise forward with X and W amax'd by one persistent TMA launch (capped grids make CTA tile
     ranges straddle the X -> W boundary, so a row strip of W follows one of X in the same CTA) and cast
     by one launch: the forward codes, scales and outputs match the oracle; the saved column-scaled
     copies drive a backward in tolerance."""
-    if grid != "0":
-        monkeypatch.setenv("FP8T_CAST_GRID", grid)
+    knob("cast_grid", int(grid))
     M, N, K = 640, 384, 512
     x, w, dy = synth.linear_inputs("c3", M, N, K, seed=5)
     y, yb, _ = olin.forward(x, w, "rowwise")
@@ -1035,10 +1028,10 @@ def test_linear_rowwise_dual_launch_straddle(grid, monkeypatch):
 
 
 @pytest.mark.parametrize("dual", ["1", "0"], ids=["xw_one_cast_launch", "separate_casts"])
-def test_linear_tensorwise_cast_launches(dual, monkeypatch):
+def test_linear_tensorwise_cast_launches(dual, knob):
     """Tensorwise forward with X and W cast by one launch (default) or separately: identical bytes,
     scales and outputs (bit-identical GEMM results), both in tolerance of the oracle."""
-    monkeypatch.setenv("FP8T_TW_DUAL", dual)
+    knob("tw_dual", int(dual))
     M, N, K = 640, 384, 512
     x, w, dy = synth.linear_inputs("c2", M, N, K, seed=6)
     y, yb, _ = olin.forward(x, w, "tensorwise")

@@ -1,5 +1,5 @@
 """Microbenchmark of the per-row / per-column amax pass (rowwise recipe) on C2/C3-sized tensors:
-TMA-ring strip kernel (default) vs the register-only kernel (FP8T_AMAX_TILE=0).  GB/s = 2 B read per
+TMA-ring strip kernel (default) vs the register-only kernel (knob amax_tile_tma = 0).  GB/s = 2 B read per
 element / time, a 512 MiB buffer rewritten between calls (context for tuning)."""
 import ctypes
 import json
@@ -38,7 +38,7 @@ for R, C in ((16384, 14336), (16384, 4096), (14336, 4096)):
         if gran == "row_col":   # the rowwise recipe's dual amax through the cast entry (amax only timed via cast)
             continue
         for impl in ("1", "0"):
-            os.environ["FP8T_AMAX_TILE"] = impl
+            ops.set_knob("amax_tile_tma", int(impl))
 
             def f():
                 flush.zero_()
@@ -46,11 +46,11 @@ for R, C in ((16384, 14336), (16384, 4096), (14336, 4096)):
                                        ws.numel(), ops._stream()), "amax")
             ms = timeit(f) - t_flush
             row[f"{gran}_{'tma' if impl == '1' else 'regs'}_GBps"] = round(R * C * 2 / ms / 1e6)
-    os.environ.pop("FP8T_AMAX_TILE", None)
+    ops.reset_knobs()
     # dual row+col amax + dual cast (the rowwise recipe's X pass), end to end through fp8_cast_scaled
     for impl in ("1", "0"):
-        os.environ["FP8T_AMAX_TILE"] = impl
+        ops.set_knob("amax_tile_tma", int(impl))
         ms = timeit(lambda: (flush.zero_(), ops.cast(x, "e4m3", "row_col", want_q=True, want_qt=True))) - t_flush
         row[f"rowcol_amax+cast_{'tma' if impl == '1' else 'regs'}_GBps"] = round(R * C * 6 / ms / 1e6)
-    os.environ.pop("FP8T_AMAX_TILE", None)
+    ops.reset_knobs()
     print(json.dumps(row), flush=True)

@@ -22,7 +22,8 @@ dy = torch.randn((16384, 14336), device="cuda", dtype=torch.bfloat16)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 res = {}
 for cfg in ("44", "48", "4C", "4G", "84", "88", "8C", "28", "2G"):
-    os.environ["FP8T_AMAX_CFG"] = cfg
+    ops.set_knob("amax_blocks_per_sm", int(cfg[0]))
+    ops.set_knob("amax_loads", {"4": 4, "8": 8, "C": 12, "G": 16}[cfg[1]])
     def f():
         flush.zero_()
         ops.amax(dy)
@@ -30,7 +31,7 @@ for cfg in ("44", "48", "4C", "4G", "84", "88", "8C", "28", "2G"):
     ms = timeit(f) - t_flush
     res[cfg] = round(dy.numel() * 2 / ms / 1e6)
 print(json.dumps({"amax_flat_GBps": res}))
-os.environ.pop("FP8T_AMAX_CFG")
+ops.reset_knobs()
 ms = timeit(lambda: (flush.zero_(), ops.cast(dy, "e5m2", "tensor"))) - timeit(lambda: flush.zero_())
 print(json.dumps({"amax+cast tensorwise GB/s (alg 5 B/elem)": round(dy.numel() * 5 / ms / 1e6)}))
 # reference read bandwidth: torch reductions / copy on the same tensor

@@ -37,19 +37,19 @@ def main():
         flops = 2.0 * M * N * K
         row = {"M": M, "N": N, "K": K}
         for dbg in ("0", "1"):   # 1: epilogue stores skipped (mainloop-only upper bound)
-            os.environ["FP8T_GEMM_DEBUG"] = dbg
+            ops.set_knob("gemm_debug", int(dbg))
             ms = timeit(lambda: ops.gemm(A, "e4m3", s, B, "e4m3", s, "tensor"))
             row["ours" if dbg == "0" else "ours_nostore"] = round(flops / ms / 1e9)
-        os.environ["FP8T_GEMM_DEBUG"] = "0"
+        ops.set_knob("gemm_debug", int("0"))
         if M % 128 == 0 and N % 128 == 0 and K % 128 == 0:   # MXFP8 block-scaled kind, codes 127 (=1.0)
             sfa = torch.full((M * K // 32,), 127, dtype=torch.uint8, device="cuda")
             sfb = torch.full((N * K // 32,), 127, dtype=torch.uint8, device="cuda")
             for dbg in os.environ.get("GEMM_BENCH_MX_DBG", "0,2").split(","):
                 # 1: no epilogue stores; 2: no tcgen05.cp of scales; 4: no scale TMA loads
-                os.environ["FP8T_GEMM_DEBUG"] = dbg
+                ops.set_knob("gemm_debug", int(dbg))
                 ms = timeit(lambda: ops.gemm(A, "e4m3", sfa, B, "e4m3", sfb, "mx32"))
                 row["ours_mx" + ("" if dbg == "0" else "_dbg" + dbg)] = round(flops / ms / 1e9)
-            os.environ["FP8T_GEMM_DEBUG"] = "0"
+            ops.set_knob("gemm_debug", int("0"))
             # MN-major operands (the MXFP8 backward's layout): A stored [K,M], B stored [K,N]
             At, Bt = A.t().contiguous(), B.t().contiguous()
             ms = timeit(lambda: ops.gemm(At, "e4m3", sfa, Bt, "e4m3", sfb, "mx32", a_mn=True, b_mn=True))

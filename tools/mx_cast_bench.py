@@ -1,7 +1,7 @@
 """Microbenchmark of the MXFP8 dim0+dim1 cast on the C4 operand shapes (context for tuning).
 
 Compares the TMA-pipelined persistent kernel (default) with the register-only kernel
-(FP8T_MX_CAST=0), for the row-major dim1 layout (MX32_RM, the linear's default) and the
+(knob mx_cast_tma = 0), for the row-major dim1 layout (MX32_RM, the linear's default) and the
 transposed one (MX32).  GB/s = algorithmic bytes (2 read + 1 + 1 written + 2/32 scales per
 element) / time; inputs are larger than L2 and a 512 MiB buffer is rewritten between calls.
 """
@@ -52,10 +52,10 @@ def main():
                                               ops._stream()), "cast")
             row = {"R": R, "C": C, "gran": gran}
             for impl in ("1", "0"):
-                os.environ["FP8T_MX_CAST"] = impl
+                ops.set_knob("mx_cast_tma", int(impl))
                 ms = timeit(f) - t_flush
                 row["tma" if impl == "1" else "regs"] = {"ms": round(ms, 4), "GBps": round(alg / ms / 1e6)}
-            os.environ.pop("FP8T_MX_CAST")
+            ops.reset_knobs()
             res.append(row)
             print(json.dumps(row), flush=True)
         del x, q0, q1, s0, s1

@@ -1,7 +1,7 @@
 """GEMM efficiency probe normalised by the SM clock: runs each variant back to back for ~1.5 s while
 sampling NVML (SM clock, power) and reports TFLOP/s, median SM MHz and flop/cycle/SM
 (= TFLOP/s / (MHz x SMs)), which separates kernel design from the power-capped clock.
-Variants: our tensorwise FP8 GEMM, our MXFP8 GEMM (+ FP8T_* env experiments), cuBLASLt FP8 / MXFP8.
+Variants: our tensorwise FP8 GEMM, our MXFP8 GEMM (+ knob experiments, MX_PROBE_KNOBS="gemm_raster=0;mx_sf_split=2"), cuBLASLt FP8 / MXFP8.
 Context for tuning only; not part of the contract."""
 import json
 import os
@@ -61,7 +61,7 @@ def main():
     shapes = [tuple(int(v) for v in sh.split("x")) for sh in
               os.environ.get("MX_PROBE_SHAPES", "16384x28672x8192,16384x14336x4096").split(",")]
     variants = os.environ.get("MX_PROBE_VARIANTS", "fp8,mx,cublas_fp8,cublas_mx").split(",")
-    envs = [e for e in os.environ.get("MX_PROBE_ENVS", "").split(";") if e]   # e.g. "FP8T_MX_SF_AHEAD=1"
+    envs = [e for e in os.environ.get("MX_PROBE_KNOBS", "").split(";") if e]   # e.g. "gemm_raster=0"
     for M, N, K in shapes:
         g = torch.Generator(device="cuda").manual_seed(0)
         A = torch.randint(0, 0x70, (M, K), dtype=torch.uint8, device="cuda", generator=g)
@@ -73,12 +73,10 @@ def main():
         for v in variants:
             runs = [("", None)] + ([(e, e) for e in envs] if v in ("mx", "fp8") else [])
             for tag, env in runs:
-                saved = {}
                 if env:
                     for kv in env.split(","):
                         k, val = kv.split("=")
-                        saved[k] = os.environ.get(k)
-                        os.environ[k] = val
+                        ops.set_knob(k, int(val))
                 if v == "fp8":
                     fn = lambda: ops.gemm(A, "e4m3", s, B, "e4m3", s, "tensor")  # noqa: E731
                 elif v == "mx":
@@ -101,11 +99,7 @@ def main():
                     r = probe(fn, flops)
                 except Exception as e:  # noqa: BLE001
                     r = {"error": str(e)[:100]}
-                for k, val in saved.items():
-                    if val is None:
-                        os.environ.pop(k, None)
-                    else:
-                        os.environ[k] = val
+                ops.reset_knobs()
                 print(json.dumps({"shape": [M, N, K], "variant": v, "env": tag, **r}), flush=True)
         del A, B, sfa, sfb
         torch.cuda.empty_cache()
