@@ -243,6 +243,34 @@ fp8_status_t fp8_gemm(const uint8_t* A, fp8_format_t fmt_a, fp8_major_t major_a,
  *   fp8_linear_infer_workspace_bytes() bytes.
  * ------------------------------------------------------------------------- */
 size_t fp8_linear_saved_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K);
+
+/* Where one linear's FP8 operands live inside its `saved` and `ws` buffers (inspection: parity
+ * tests byte-check exactly what fp8_linear_fwd / fp8_linear_bwd wrote; checkpoint tooling).  Fills
+ * `out` with pointers into the caller's buffers (no device access, no launch); NULL entries are
+ * operands the recipe does not have.  Forward-workspace entries hold the forward's operands
+ * after fp8_linear_fwd until the next call using `ws` (the backward reuses it); backward entries
+ * hold the backward's dY operands after fp8_linear_bwd.  Layouts (R-c17, operand plan §2):
+ *   tensorwise: x_fwd = x_bwd = Xq [M,K], w_fwd = w_bwd = Wq [N,K], float[1] scales;
+ *     dy_dx = dy_dw = Gq [M,N], float[1];
+ *   rowwise (+_gw_hp): x_fwd [M,K] row-scaled (float[M]), w_fwd [N,K] row-scaled (float[N]),
+ *     x_bwd [M,K] column-scaled (float[K]; NULL for gw_hp), w_bwd [N,K] column-scaled (float[K]),
+ *     dy_dx [M,N] row-scaled (float[M]), dy_dw [M,N] column-scaled (float[N]; NULL for gw_hp);
+ *   mxfp8: x_fwd/w_fwd/dy_dx dim0 codes in the input layout with blocked E8M0 [rows, cols/32];
+ *     x_bwd [M,K], w_bwd [N,K], dy_dw [M,N] dim1 codes (blocks of 32 along the row index) in the
+ *     input layout -- or transposed ([K,M], [K,N], [N,M]) when knob mx_transposed = 1
+ *     (bwd_transposed) -- with blocked E8M0 [cols, rows/32].
+ *   amax_fwd: tensorwise [amax X, amax W]; rowwise [X rows M | X cols K | W rows N | W cols K];
+ *   amax_bwd: tensorwise [amax dY]; rowwise [dY rows M | dY cols N]; mxfp8: NULL (per-block amax
+ *     is never stored). */
+typedef struct {
+  uint8_t* x_fwd; void* x_fwd_scale; uint8_t* w_fwd; void* w_fwd_scale;
+  uint8_t* x_bwd; void* x_bwd_scale; uint8_t* w_bwd; void* w_bwd_scale;
+  uint8_t* dy_dx; void* dy_dx_scale; uint8_t* dy_dw; void* dy_dw_scale;
+  float* amax_fwd; float* amax_bwd;
+  int bwd_transposed;
+} fp8_linear_buffers_t;
+fp8_status_t fp8_linear_buffers(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K, void* saved,
+                                void* ws, fp8_linear_buffers_t* out);
 size_t fp8_linear_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K);
 size_t fp8_linear_infer_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K);
 fp8_status_t fp8_linear_fwd(const fp8_linear_cfg_t* cfg, fp8_hp_t x, fp8_hp_t w,

@@ -34,6 +34,12 @@ class Tensor8(ctypes.Structure):
                 ("fmt", ctypes.c_int), ("gran", ctypes.c_int), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64)]
 
 
+class LinearBuffers(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in (
+        "x_fwd", "x_fwd_scale", "w_fwd", "w_fwd_scale", "x_bwd", "x_bwd_scale", "w_bwd", "w_bwd_scale",
+        "dy_dx", "dy_dx_scale", "dy_dw", "dy_dw_scale", "amax_fwd", "amax_bwd")] + [("bwd_transposed", ctypes.c_int)]
+
+
 class LinearCfg(ctypes.Structure):
     _fields_ = [("recipe", ctypes.c_int), ("fmt_fwd", ctypes.c_int), ("fmt_grad", ctypes.c_int),
                 ("mx_round", ctypes.c_int), ("out_dtype", ctypes.c_int)]
@@ -60,6 +66,8 @@ SIGNATURES = {
                             _c.c_void_p, _c.c_int, _c.c_int64, _c.c_int64, _c.c_int64, _c.c_int64, _c.c_int64,
                             _c.c_void_p, _c.c_int, _c.c_int64, _c.c_void_p]),
     "fp8_linear_saved_bytes": (_c.c_size_t, [_c.POINTER(LinearCfg), _c.c_int64, _c.c_int64, _c.c_int64]),
+    "fp8_linear_buffers": (_c.c_int, [_c.POINTER(LinearCfg), _c.c_int64, _c.c_int64, _c.c_int64, _c.c_void_p,
+                                      _c.c_void_p, _c.POINTER(LinearBuffers)]),
     "fp8_linear_workspace_bytes": (_c.c_size_t, [_c.POINTER(LinearCfg), _c.c_int64, _c.c_int64, _c.c_int64]),
     "fp8_linear_infer_workspace_bytes": (_c.c_size_t, [_c.POINTER(LinearCfg), _c.c_int64, _c.c_int64,
                                                        _c.c_int64]),

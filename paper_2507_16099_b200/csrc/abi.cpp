@@ -539,6 +539,41 @@ size_t fp8_linear_saved_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N,
   return b;
 }
 
+fp8_status_t fp8_linear_buffers(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K, void* saved,
+                                void* ws, fp8_linear_buffers_t* out) {
+  if (!out) return fail(FP8_EINVAL, "out: null pointer");
+  FP8T_TRY(check_cfg(cfg, M, N, K));
+  FP8T_TRY(check_ptr(saved, "saved"));
+  FP8T_TRY(check_ptr(ws, "ws"));
+  *out = fp8_linear_buffers_t{};
+  const Saved sv = carve_saved(cfg, M, N, K, saved, nullptr);
+  const FwdWs fw = carve_fwd(cfg, M, N, K, ws, nullptr);
+  const BwdWs bw = carve_bwd(cfg, M, N, ws, nullptr);
+  out->x_bwd = sv.xT; out->x_bwd_scale = sv.sx;
+  out->w_bwd = sv.wT; out->w_bwd_scale = sv.sw;
+  out->dy_dx = bw.g; out->dy_dx_scale = bw.sg;
+  out->dy_dw = bw.gT; out->dy_dw_scale = bw.sgT;
+  out->amax_fwd = fw.amax; out->amax_bwd = bw.amax;
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    out->x_fwd = sv.xT; out->x_fwd_scale = sv.sx;
+    out->w_fwd = sv.wT; out->w_fwd_scale = sv.sw;
+    out->dy_dw = bw.g; out->dy_dw_scale = bw.sg;
+  } else if (cfg->recipe == FP8_RECIPE_MXFP8) {
+    out->x_fwd = fw.xq; out->x_fwd_scale = fw.sfx;
+    out->w_fwd = fw.wq; out->w_fwd_scale = fw.sfw;
+    out->amax_fwd = out->amax_bwd = nullptr;
+    out->bwd_transposed = mx_transposed() ? 1 : 0;
+  } else {
+    out->x_fwd = fw.xq; out->x_fwd_scale = fw.sxr;
+    out->w_fwd = fw.wq; out->w_fwd_scale = fw.swr;
+    if (cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {
+      out->x_bwd = nullptr; out->x_bwd_scale = nullptr;
+      out->dy_dw = nullptr; out->dy_dw_scale = nullptr;
+    }
+  }
+  return FP8_OK;
+}
+
 size_t fp8_linear_infer_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K) {
   if (!cfg) return 0;
   size_t b = 0;

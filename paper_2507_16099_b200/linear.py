@@ -38,14 +38,23 @@ class _Float8LinearFn(torch.autograd.Function):
         x2d = x2d.contiguous()
         y = plan.forward(x2d, w.contiguous(), saved)
         ctx.plan, ctx.buf, ctx.wdtype = plan, saved, w.dtype
-        # rowwise_gw_hp keeps dL/dW in bf16: its dW GEMM reads the hp input
-        ctx.x = x2d if recipe == "rowwise_gw_hp" else None
+        # rowwise_gw_hp keeps dL/dW in bf16: its BF16 dW GEMM reads the hp input in
+        # bf16 (a bf16 copy when the activations are fp32; the forward casts still read x2d itself).
+        # Saved through save_for_backward, so an in-place change of x before backward raises.
+        ctx.gw_hp = recipe == "rowwise_gw_hp"
+        if ctx.gw_hp:
+            ctx.save_for_backward(x2d if x2d.dtype == torch.bfloat16 else x2d.to(torch.bfloat16))
         return y
 
     @staticmethod
     def backward(ctx, dy):
+        x_hp = None
+        if ctx.gw_hp:
+            (x_hp,) = ctx.saved_tensors
+            if dy.dtype != torch.bfloat16:
+                dy = dy.to(torch.bfloat16)
         dx, dw = ctx.plan.backward(dy.contiguous(), ctx.buf, want_dx=ctx.needs_input_grad[0],
-                                   want_dw=ctx.needs_input_grad[1], x=ctx.x)
+                                   want_dw=ctx.needs_input_grad[1], x=x_hp)
         if dw is not None and dw.dtype != ctx.wdtype:
             dw = dw.to(ctx.wdtype)
         return dx, dw, None

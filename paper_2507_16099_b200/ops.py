@@ -191,6 +191,57 @@ class LinearPlan:
                                         _ptr(ws), wsb, _stream(stream)), "fp8_linear_fwd_ex")
         return y
 
+    def buffers(self, saved):
+        """fp8_linear_buffers: uint8 / float32 views of the FP8 operands, scales and amaxes inside
+        `saved` and this plan's workspace (what the forward / backward wrote; see fp8train.h)."""
+        b = L.LinearBuffers()
+        L.check(L.lib.fp8_linear_buffers(ctypes.byref(self.cfg), self.M, self.N, self.K, _ptr(saved),
+                                         _ptr(self.ws), ctypes.byref(b)), "fp8_linear_buffers")
+        M, N, K = self.M, self.N, self.K
+        rec = self.cfg.recipe
+        mx = rec == L.RECIPE_MXFP8
+
+        def view(ptr, nbytes, dtype=torch.uint8, shape=None):
+            if not ptr:
+                return None
+            for base in (saved, self.ws):
+                off = ptr - base.data_ptr()
+                if 0 <= off and off + nbytes <= base.numel():
+                    t = base[off:off + nbytes]
+                    t = t.view(dtype) if dtype != torch.uint8 else t
+                    return t.view(shape) if shape is not None else t
+            raise RuntimeError("fp8_linear_buffers: pointer outside saved / ws")
+
+        def scale(ptr, n):   # n floats (tensorwise / rowwise) or n E8M0 bytes (mx)
+            return view(ptr, n, torch.uint8) if mx else view(ptr, 4 * n, torch.float32)
+
+        tw = rec == L.RECIPE_TENSORWISE
+        tr = bool(b.bwd_transposed)
+        out = {
+            "x_fwd": view(b.x_fwd, M * K, shape=(M, K)), "w_fwd": view(b.w_fwd, N * K, shape=(N, K)),
+            "x_bwd": view(b.x_bwd, M * K, shape=(K, M) if tr else (M, K)),
+            "w_bwd": view(b.w_bwd, N * K, shape=(K, N) if tr else (N, K)),
+            "dy_dx": view(b.dy_dx, M * N, shape=(M, N)),
+            "dy_dw": view(b.dy_dw, M * N, shape=(N, M) if tr else (M, N)),
+            "bwd_transposed": tr,
+        }
+        if mx:
+            out.update(x_fwd_scale=scale(b.x_fwd_scale, M * K // 32), w_fwd_scale=scale(b.w_fwd_scale, N * K // 32),
+                       x_bwd_scale=scale(b.x_bwd_scale, M * K // 32), w_bwd_scale=scale(b.w_bwd_scale, N * K // 32),
+                       dy_dx_scale=scale(b.dy_dx_scale, M * N // 32), dy_dw_scale=scale(b.dy_dw_scale, M * N // 32),
+                       amax_fwd=None, amax_bwd=None)
+        elif tw:
+            out.update(x_fwd_scale=scale(b.x_fwd_scale, 1), w_fwd_scale=scale(b.w_fwd_scale, 1),
+                       x_bwd_scale=scale(b.x_bwd_scale, 1), w_bwd_scale=scale(b.w_bwd_scale, 1),
+                       dy_dx_scale=scale(b.dy_dx_scale, 1), dy_dw_scale=scale(b.dy_dw_scale, 1),
+                       amax_fwd=scale(b.amax_fwd, 2), amax_bwd=scale(b.amax_bwd, 1))
+        else:
+            out.update(x_fwd_scale=scale(b.x_fwd_scale, M), w_fwd_scale=scale(b.w_fwd_scale, N),
+                       x_bwd_scale=scale(b.x_bwd_scale, K), w_bwd_scale=scale(b.w_bwd_scale, K),
+                       dy_dx_scale=scale(b.dy_dx_scale, M), dy_dw_scale=scale(b.dy_dw_scale, N),
+                       amax_fwd=scale(b.amax_fwd, M + K + N + K), amax_bwd=scale(b.amax_bwd, M + N))
+        return out
+
     def backward(self, dy, saved, dx=None, dw=None, want_dx=True, want_dw=True, w_fp8=None, x=None,
                  dy_amax=None, dx_amax=None, stream=None):
         """x: the forward input (read by rowwise_gw_hp's BF16 dW GEMM only); dy_amax / dx_amax: amax

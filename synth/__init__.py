@@ -138,10 +138,18 @@ def _outlier_channels(cfg, seed, K, count=8):
     return np.unique((u * K).astype(np.int64) % K)
 
 
-def tensor_c2(name, shape, seed, cfg="c2"):
+def _z(cfg, name, seed, shape, rows):
+    key = stream_key(cfg, name, seed, shape)
+    if rows is None:
+        return normal(key, shape)
+    return normal_rows(key, shape, rows[0], rows[1])
+
+
+def tensor_c2(name, shape, seed, cfg="c2", rows=None):
     """C2/C5 value structure (Llama linears, tensorwise):
-    X ~ N(0,1) with 8 outlier channels x20; W ~ N(0, 0.02^2); dY ~ N(0, 1e-3^2)."""
-    z = normal(stream_key(cfg, name, seed, shape), shape)
+    X ~ N(0,1) with 8 outlier channels x20; W ~ N(0, 0.02^2); dY ~ N(0, 1e-3^2).
+    rows=(r0, r1): only those rows of the same tensor (counter-based)."""
+    z = _z(cfg, name, seed, shape, rows)
     if name == "x":
         z[:, _outlier_channels(cfg, seed, shape[1])] *= 20.0
     elif name == "w":
@@ -151,10 +159,10 @@ def tensor_c2(name, shape, seed, cfg="c2"):
     return as_bf16_f32(z)
 
 
-def tensor_c3(name, shape, seed, cfg="c3"):
+def tensor_c3(name, shape, seed, cfg="c3", rows=None):
     """C3 (rowwise): C2 distributions, rows additionally scaled by 2^U(-8,8)
     (X, dY) or 2^U(-4,4) (W) so per-row scales differ."""
-    z = normal(stream_key(cfg, name, seed, shape), shape)
+    z = _z(cfg, name, seed, shape, rows)
     if name == "x":
         z[:, _outlier_channels(cfg, seed, shape[1])] *= 20.0
     elif name == "w":
@@ -163,22 +171,25 @@ def tensor_c3(name, shape, seed, cfg="c3"):
         z *= 1e-3
     span = 4.0 if name == "w" else 8.0
     u = uniform(stream_key(cfg, name + "_rowscale", seed, shape), (shape[0],))
+    if rows is not None:
+        u = u[rows[0]:rows[1]]
     z *= np.exp2((2.0 * u - 1.0) * span)[:, None]
     return as_bf16_f32(z)
 
 
-def tensor_c4(name, shape, seed, cfg="c4"):
+def tensor_c4(name, shape, seed, cfg="c4", rows=None):
     """C4 (MXFP8): per-32-block magnitude 2^U(-20,10) along rows; ~1% all-zero
     blocks; ~0.2% blocks at bf16-subnormal magnitude (2^-130)."""
     R, C = shape
-    z = normal(stream_key(cfg, name, seed, shape), shape).reshape(R, C // 32, 32)
-    u = uniform(stream_key(cfg, name + "_blk", seed, shape), (R, C // 32))
+    r0, r1 = rows if rows is not None else (0, R)
+    z = _z(cfg, name, seed, shape, rows).reshape(r1 - r0, C // 32, 32)
+    u = uniform(stream_key(cfg, name + "_blk", seed, shape), (R, C // 32))[r0:r1]
     mag = np.exp2(-20.0 + 30.0 * u)
-    v = uniform(stream_key(cfg, name + "_kind", seed, shape), (R, C // 32))
+    v = uniform(stream_key(cfg, name + "_kind", seed, shape), (R, C // 32))[r0:r1]
     mag = np.where(v < 0.01, 0.0, mag)
     mag = np.where((v >= 0.01) & (v < 0.012), 2.0 ** -130, mag)
     z = z * mag[:, :, None]
-    return as_bf16_f32(z.reshape(R, C))
+    return as_bf16_f32(z.reshape(r1 - r0, C))
 
 
 def tensor_c1(name, shape, seed, cfg="c1"):

@@ -1,9 +1,10 @@
-"""Full-size parity at BASELINE.json configs[1] (C2: M=16384, K=4096, N=14336, tensorwise), in the
-launch configuration bench.py times (fp8_linear_fwd / fp8_linear_bwd, bf16 in/out).
+"""Full-size parity at BASELINE.json configs[1..4] (C2 tensorwise, C3 rowwise at all seven layer shapes,
+C4 MXFP8, C5 FSDP tensorwise), in the launch configuration bench.py times (fp8_linear_fwd /
+fp8_linear_bwd, bf16 in/out), on the bytes the linear ITSELF writes (fp8_linear_buffers).
 
 The oracle cannot run the full GEMMs in reasonable time, so (SURVEY §4 "GPU integration"):
-  * amax and scales are checked over the full tensors, bit-exact;
-  * FP8 codes are checked bit-exact on sampled rows (cast entry point, same kernels);
+  * amax and scales (every row / column vector, every E8M0 code) over the full tensors, bit-exact;
+  * FP8 codes bit-exact on sampled rows / columns of the linear's own operand buffers;
   * Y and dX on 48 sampled rows x all columns, dW on 48 sampled rows x all columns, each computed
     by the oracle from its own casts (full-tensor scales) within the north-star tolerance.
 """
@@ -48,27 +49,31 @@ def test_c2_fullsize_tensorwise(c2):
     plan = ops.LinearPlan(M, N, K, recipe="tensorwise", out_dtype=bf)
     saved = plan.new_saved()
     Y = plan.forward(X, W, saved)
-    DX, DW = plan.backward(G, saved)
-    cx = ops.cast(X, "e4m3", "tensor")
-    cw = ops.cast(W, "e4m3", "tensor")
-    cg = ops.cast(G, "e5m2", "tensor")
     torch.cuda.synchronize()
+    fb = plan.buffers(saved)          # what the linear itself wrote (the dual X/W amax + cast launches)
+    f_amax = fb["amax_fwd"].cpu().numpy()
+    DX, DW = plan.backward(G, saved)
+    torch.cuda.synchronize()
+    bb = plan.buffers(saved)
 
     # full-tensor amax / scale (oracle), bit-exact
-    sx = fp8.scale_from_amax(fp8.amax(x), E4M3)
-    sw = fp8.scale_from_amax(fp8.amax(w), E4M3)
-    sg = fp8.scale_from_amax(fp8.amax(dy), E5M2)
-    for out, a, s in ((cx, fp8.amax(x), sx), (cw, fp8.amax(w), sw), (cg, fp8.amax(dy), sg)):
-        assert _bits(out["amax"].cpu().numpy())[0] == _bits(a).reshape(-1)[0]
-        assert _bits(out["scale"].cpu().numpy())[0] == _bits(s).reshape(-1)[0]
+    ax, aw, ag = fp8.amax(x), fp8.amax(w), fp8.amax(dy)
+    sx = fp8.scale_from_amax(ax, E4M3)
+    sw = fp8.scale_from_amax(aw, E4M3)
+    sg = fp8.scale_from_amax(ag, E5M2)
+    assert _bits(f_amax)[0] == _bits(ax).reshape(-1)[0] and _bits(f_amax)[1] == _bits(aw).reshape(-1)[0]
+    assert _bits(bb["amax_bwd"].cpu().numpy())[0] == _bits(ag).reshape(-1)[0]
+    for buf, s in ((bb["x_bwd_scale"], sx), (bb["w_bwd_scale"], sw), (bb["dy_dx_scale"], sg)):
+        assert _bits(buf.cpu().numpy())[0] == _bits(s).reshape(-1)[0]
 
     rng = np.random.default_rng(2024)
     rows_m = np.sort(rng.choice(M, 48, replace=False))
     rows_n = np.sort(rng.choice(N, 48, replace=False))
-    # sampled codes, bit-exact
-    assert np.array_equal(cx["q"][torch.from_numpy(rows_m).cuda()].cpu().numpy(), fp8.cast_scaled(x[rows_m], sx, E4M3))
-    assert np.array_equal(cw["q"][torch.from_numpy(rows_n).cuda()].cpu().numpy(), fp8.cast_scaled(w[rows_n], sw, E4M3))
-    assert np.array_equal(cg["q"][torch.from_numpy(rows_m).cuda()].cpu().numpy(), fp8.cast_scaled(dy[rows_m], sg, E5M2))
+    # sampled codes of the saved operands and the backward's dY operand, bit-exact
+    im, in_ = torch.from_numpy(rows_m).cuda(), torch.from_numpy(rows_n).cuda()
+    assert np.array_equal(bb["x_bwd"][im].cpu().numpy(), fp8.cast_scaled(x[rows_m], sx, E4M3))
+    assert np.array_equal(bb["w_bwd"][in_].cpu().numpy(), fp8.cast_scaled(w[rows_n], sw, E4M3))
+    assert np.array_equal(bb["dy_dx"][im].cpu().numpy(), fp8.cast_scaled(dy[rows_m], sg, E5M2))
 
     # oracle operands (its own casts with the full-tensor scales)
     wq = fp8.cast_scaled(w, sw, E4M3)                       # [N, K]
@@ -100,21 +105,85 @@ def _gpu_rows_cols(T, rows, cols):
     return T[r][:, c].float().cpu().numpy().astype(np.float64)
 
 
-def test_c3w1_fullsize_rowwise():
-    """BASELINE.json configs[2] (rowwise) at the Llama-3-8B w1 shape M=16384, N=14336, K=4096, bf16,
-    through fp8_linear_fwd / fp8_linear_bwd as bench.py runs it.  Every rowwise scaling unit is a row
-    or a column, so the oracle quantizes only the sampled rows / columns (P:597 operand plan, DESIGN
-    §2): Y, dX and dW on 48 x 48 sampled outputs, each a full-length contraction, within tolerance."""
+def _cpu(t):
+    return t.detach().cpu().numpy()
+
+
+def _eq_bits(name, got, want):
+    got, want = np.asarray(got), np.asarray(want)
+    if want.dtype == np.float32:
+        got, want = got.view(np.uint32), want.view(np.uint32)
+    assert got.shape == want.shape, (name, got.shape, want.shape)
+    bad = np.count_nonzero(got != want)
+    assert bad == 0, f"{name}: {bad} of {want.size} differ"
+
+
+def _unblock(buf, R, C):
+    """E8M0 blocked layout (fp8train.h) -> logical [R, C/32] codes (pure index permutation)."""
+    C32 = C // 32
+    b = _cpu(buf).reshape(R // 128, C32 // 4, 32, 4, 4)
+    return b.transpose(0, 3, 2, 1, 4).reshape(R, C32)
+
+
+C3_LINEARS = [("wq", 4096, 4096), ("wk", 1024, 4096), ("wv", 1024, 4096), ("wo", 4096, 4096),
+              ("w1", 14336, 4096), ("w3", 14336, 4096), ("w2", 4096, 14336)]
+
+
+@pytest.mark.parametrize("name,N3,K3", C3_LINEARS, ids=[c[0] for c in C3_LINEARS])
+def test_c3_fullsize_rowwise(name, N3, K3):
+    """BASELINE.json configs[2] (rowwise) at all seven Llama-3-8B layer shapes (M = 16384 tokens), bf16,
+    through fp8_linear_fwd / fp8_linear_bwd as bench.py runs them, checking what the linear ITSELF
+    wrote (fp8_linear_buffers):
+      * every row- and column-amax vector and every row / column scale vector over the FULL tensors
+        (X rows + cols, W rows + cols, dY rows + cols), bit-exact vs the oracle (P:597 operand plan);
+      * FP8 codes of 64 sampled rows of each row-scaled copy and 64 sampled columns of each
+        column-scaled copy, bit-exact;
+      * Y, dX, dW on 48 x 48 sampled outputs (full-length contractions) within tolerance."""
     from paper_2507_16099_b200 import ops
-    M3, N3, K3 = 16384, 14336, 4096
-    x, w, dy = synth.linear_inputs("c3", M3, N3, K3, seed=0)
+    M3 = 16384
+    seed = [c[0] for c in C3_LINEARS].index(name)
+    x, w, dy = synth.linear_inputs("c3", M3, N3, K3, seed=seed)
     bf = torch.bfloat16
     X, W, G = (torch.from_numpy(a).to(bf).cuda() for a in (x, w, dy))
     plan = ops.LinearPlan(M3, N3, K3, recipe="rowwise", out_dtype=bf)
     saved = plan.new_saved()
     Y = plan.forward(X, W, saved)
+    torch.cuda.synchronize()
+    pr_m, pr_n, pc_k, pc_n = _sample(M3, 64, 11), _sample(N3, 64, 12), _sample(K3, 64, 13), _sample(N3, 64, 14)
+    fb = plan.buffers(saved)
+    f_amax, f_sx, f_sw = _cpu(fb["amax_fwd"]), _cpu(fb["x_fwd_scale"]), _cpu(fb["w_fwd_scale"])
+    f_xrows = _cpu(fb["x_fwd"][torch.from_numpy(pr_m).cuda()])
+    f_wrows = _cpu(fb["w_fwd"][torch.from_numpy(pr_n).cuda()])
     DX, DW = plan.backward(G, saved)
     torch.cuda.synchronize()
+    bb = plan.buffers(saved)
+    ic_k, ic_n = torch.from_numpy(pc_k).cuda(), torch.from_numpy(pc_n).cuda()
+
+    # full amax / scale vectors
+    ax_r, ax_c = fp8.amax(x, axis=1), fp8.amax(x, axis=0)
+    aw_r, aw_c = fp8.amax(w, axis=1), fp8.amax(w, axis=0)
+    ag_r, ag_c = fp8.amax(dy, axis=1), fp8.amax(dy, axis=0)
+    _eq_bits("amax X rows", f_amax[:M3], ax_r)
+    _eq_bits("amax X cols", f_amax[M3:M3 + K3], ax_c)
+    _eq_bits("amax W rows", f_amax[M3 + K3:M3 + K3 + N3], aw_r)
+    _eq_bits("amax W cols", f_amax[M3 + K3 + N3:], aw_c)
+    _eq_bits("amax dY rows", _cpu(bb["amax_bwd"])[:M3], ag_r)
+    _eq_bits("amax dY cols", _cpu(bb["amax_bwd"])[M3:], ag_c)
+    _eq_bits("X row scales", f_sx, fp8.scale_from_amax(ax_r, E4M3))
+    _eq_bits("W row scales", f_sw, fp8.scale_from_amax(aw_r, E4M3))
+    _eq_bits("X col scales (saved)", _cpu(bb["x_bwd_scale"]), fp8.scale_from_amax(ax_c, E4M3))
+    _eq_bits("W col scales (saved)", _cpu(bb["w_bwd_scale"]), fp8.scale_from_amax(aw_c, E4M3))
+    _eq_bits("dY row scales", _cpu(bb["dy_dx_scale"]), fp8.scale_from_amax(ag_r, E5M2))
+    _eq_bits("dY col scales", _cpu(bb["dy_dw_scale"]), fp8.scale_from_amax(ag_c, E5M2))
+
+    # sampled codes from the linear's own buffers
+    _eq_bits("X row-scaled rows", f_xrows, fp8.cast_rowwise(x[pr_m], E4M3)[0])
+    _eq_bits("W row-scaled rows", f_wrows, fp8.cast_rowwise(w[pr_n], E4M3)[0])
+    _eq_bits("dY row-scaled rows", _cpu(bb["dy_dx"][torch.from_numpy(pr_m).cuda()]), fp8.cast_rowwise(dy[pr_m], E5M2)[0])
+    _eq_bits("X col-scaled cols (saved)", _cpu(bb["x_bwd"][:, ic_k]), fp8.cast_colwise(x[:, pc_k], E4M3)[0])
+    _eq_bits("W col-scaled cols (saved)", _cpu(bb["w_bwd"][:, ic_k]), fp8.cast_colwise(w[:, pc_k], E4M3)[0])
+    _eq_bits("dY col-scaled cols", _cpu(bb["dy_dw"][:, ic_n]), fp8.cast_colwise(dy[:, pc_n], E5M2)[0])
+
     rm, rn, rk = _sample(M3, 48, 1), _sample(N3, 48, 2), _sample(K3, 48, 3)
     # Y[m, n] = Xq_row[m] . Wq_row[n] / (sx[m] sw[n])
     xq, sx, _ = fp8.cast_rowwise(x[rm], E4M3)
@@ -133,12 +202,34 @@ def test_c3w1_fullsize_rowwise():
          ogemm.abs_bound(gcq.T, E5M2, sgc, xcq.T, E4M3, sxc))
 
 
+def _mx_codes_dim0(x, fmt):
+    """Full E8M0 code array of the dim0 copy (blocks along the row): the oracle's block amax + code."""
+    from oracle import mx as omx
+    out = np.empty((x.shape[0], x.shape[1] // 32), np.uint8)
+    for r0 in range(0, x.shape[0], 4096):
+        out[r0:r0 + 4096] = omx.scale_code(omx.block_amax(x[r0:r0 + 4096]), fmt)
+    return out
+
+
+def _mx_codes_dim1(x, fmt):
+    """Full E8M0 code array of the dim1 copy [C, R/32] (blocks along the column), chunked over columns."""
+    from oracle import mx as omx
+    out = np.empty((x.shape[1], x.shape[0] // 32), np.uint8)
+    for c0 in range(0, x.shape[1], 2048):
+        out[c0:c0 + 2048] = omx.scale_code(omx.block_amax(np.ascontiguousarray(x[:, c0:c0 + 2048].T)), fmt)
+    return out
+
+
 def test_c4_fullsize_mxfp8():
     """BASELINE.json configs[3] (MXFP8 block-32 E8M0, FLOOR) at the Llama-3-70B w1 shape M=16384,
     N=28672, K=8192, bf16, through fp8_linear_fwd / fp8_linear_bwd (the bench's launch configuration:
-    row-major dim1 codes read MN-major by the block-scaled GEMM).  A 32-block never leaves its row
-    (dim0) or column (dim1), so the oracle quantizes only the sampled rows / columns: Y, dX, dW on
-    48 x 48 sampled outputs, full-length contractions, within tolerance."""
+    row-major dim1 codes read MN-major by the block-scaled GEMM), checking what the linear ITSELF wrote
+    (fp8_linear_buffers):
+      * the FULL E8M0 code arrays of all six operand copies (X, W dim0; dY dim0; X, W, dY dim1), bit-exact
+        vs the oracle's block amax -> code (PAPER.md:735; R-c12);
+      * FP8 codes of 64 sampled rows of each dim0 copy and 64 sampled columns of each dim1 copy;
+      * Y, dX, dW on 48 x 48 sampled outputs, full-length contractions, within tolerance (a 32-block never
+        leaves its row (dim0) or column (dim1), so the oracle quantizes only the sampled rows / columns)."""
     from oracle import mx as omx
     from paper_2507_16099_b200 import ops
     M4, N4, K4 = 16384, 28672, 8192
@@ -148,8 +239,32 @@ def test_c4_fullsize_mxfp8():
     plan = ops.LinearPlan(M4, N4, K4, recipe="mxfp8", out_dtype=bf)
     saved = plan.new_saved()
     Y = plan.forward(X, W, saved)
+    torch.cuda.synchronize()
+    pr_m, pr_n, pc_k, pc_n = _sample(M4, 64, 21), _sample(N4, 64, 22), _sample(K4, 64, 23), _sample(N4, 64, 24)
+    fb = plan.buffers(saved)
+    assert not fb["bwd_transposed"]
+    f_sx, f_sw = _unblock(fb["x_fwd_scale"], M4, K4), _unblock(fb["w_fwd_scale"], N4, K4)
+    f_xrows = _cpu(fb["x_fwd"][torch.from_numpy(pr_m).cuda()])
+    f_wrows = _cpu(fb["w_fwd"][torch.from_numpy(pr_n).cuda()])
     DX, DW = plan.backward(G, saved)
     torch.cuda.synchronize()
+    bb = plan.buffers(saved)
+    ic_k, ic_n = torch.from_numpy(pc_k).cuda(), torch.from_numpy(pc_n).cuda()
+
+    _eq_bits("X E8M0 dim0", f_sx, _mx_codes_dim0(x, E4M3))
+    _eq_bits("W E8M0 dim0", f_sw, _mx_codes_dim0(w, E4M3))
+    _eq_bits("dY E8M0 dim0", _unblock(bb["dy_dx_scale"], M4, N4), _mx_codes_dim0(dy, E5M2))
+    _eq_bits("X E8M0 dim1 (saved)", _unblock(bb["x_bwd_scale"], K4, M4), _mx_codes_dim1(x, E4M3))
+    _eq_bits("W E8M0 dim1 (saved)", _unblock(bb["w_bwd_scale"], K4, N4), _mx_codes_dim1(w, E4M3))
+    _eq_bits("dY E8M0 dim1", _unblock(bb["dy_dw_scale"], N4, M4), _mx_codes_dim1(dy, E5M2))
+
+    _eq_bits("X dim0 rows", f_xrows, omx.quantize_dim0(x[pr_m], E4M3)[0])
+    _eq_bits("W dim0 rows", f_wrows, omx.quantize_dim0(w[pr_n], E4M3)[0])
+    _eq_bits("dY dim0 rows", _cpu(bb["dy_dx"][torch.from_numpy(pr_m).cuda()]), omx.quantize_dim0(dy[pr_m], E5M2)[0])
+    _eq_bits("X dim1 cols (saved)", _cpu(bb["x_bwd"][:, ic_k]).T, omx.quantize_dim1(x[:, pc_k], E4M3)[0])
+    _eq_bits("W dim1 cols (saved)", _cpu(bb["w_bwd"][:, ic_k]).T, omx.quantize_dim1(w[:, pc_k], E4M3)[0])
+    _eq_bits("dY dim1 cols", _cpu(bb["dy_dw"][:, ic_n]).T, omx.quantize_dim1(dy[:, pc_n], E5M2)[0])
+
     rm, rn, rk = _sample(M4, 48, 4), _sample(N4, 48, 5), _sample(K4, 48, 6)
     # Y = X dim0 . W dim0 (blocks along K)
     a, sa = omx.quantize_dim0(x[rm], E4M3)

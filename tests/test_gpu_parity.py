@@ -531,6 +531,66 @@ def test_amax_handover_chain():
     assert dx_amax.item() == DXb.float().abs().max().item()
 
 
+@pytest.mark.parametrize("recipe", ["tensorwise", "rowwise", "mxfp8", "rowwise_gw_hp"])
+def test_amax_handover_shared_buffer(recipe):
+    """x_amax and y_amax may be ONE buffer (a caller chaining layers through it): the forward reads the
+    incoming amax(|X|) for its casts before zeroing the buffer for the epilogue's amax(|Y|).  Results
+    equal the plain forward bit for bit, and the buffer ends holding amax(|Y|)."""
+    M, N, K = 512, 384, 256
+    x, w, _ = synth.linear_inputs("c2", M, N, K, seed=8)
+    X, W = _dev(x, torch.bfloat16), _dev(w, torch.bfloat16)
+    p = ops.LinearPlan(M, N, K, recipe=recipe)
+    Ya = p.forward(X, W, p.new_saved()).clone()
+    buf = X.float().abs().max().reshape(1).contiguous()
+    if recipe == "tensorwise":
+        Yb = p.forward(X, W, p.new_saved(), x_amax=buf, y_amax=buf)
+    else:   # x_amax is tensorwise-only; y_amax alone on the same path
+        Yb = p.forward(X, W, p.new_saved(), y_amax=buf)
+    torch.cuda.synchronize()
+    assert torch.equal(Ya, Yb)
+    assert buf.item() == Yb.float().abs().max().item()
+
+
+@pytest.mark.parametrize("recipe", ["tensorwise", "rowwise", "mxfp8", "rowwise_gw_hp"])
+def test_float8linear_fp32_module(recipe):
+    """Float8Linear on an fp32 model with fp32 activations, every recipe: forward casts read the fp32
+    inputs, rowwise_gw_hp's BF16 dW GEMM reads a saved bf16 copy of X (bf16 rounding, relative 2^-9, is
+    inside the 1e-2 bound); Y, dX, dW within tolerance of the oracle on the fp32 inputs."""
+    M, N, K = 256, 384, 256
+    x, w, dy = synth.linear_inputs("c2", M, N, K, seed=9)
+    x = x + synth.tensor_c1("x", (M, K), seed=9) * 1e-3   # not bf16-representable
+    x = x.astype(np.float32)
+    y, yb, _ = olin.forward(x, w, recipe)
+    dy_b = _np(_dev(dy, torch.bfloat16).float())          # the module's Y is bf16, so dY is bf16
+    dx, dxb, dw, dwb, _ = olin.backward(x, w, dy_b, recipe)
+    lin = torch.nn.Linear(K, N, bias=False).cuda()
+    with torch.no_grad():
+        lin.weight.copy_(_dev(w, torch.float32))
+    model = fp8t.convert(torch.nn.Sequential(lin), recipe)
+    X = _dev(x, torch.float32).requires_grad_(True)
+    Y = model(X)
+    Y.backward(_dev(dy_b, torch.bfloat16))
+    assert model[0].weight.grad.dtype == torch.float32 and X.grad.dtype == torch.float32   # autograd casts back
+    _tol_check(_np(Y.float()).astype(np.float64), y, yb)
+    _tol_check(_np(X.grad.float()).astype(np.float64), dx, dxb)
+    _tol_check(_np(model[0].weight.grad).astype(np.float64), dw, dwb)
+
+
+def test_float8linear_gw_hp_detects_inplace_input_change():
+    """rowwise_gw_hp keeps X for its BF16 dW GEMM through save_for_backward: changing X in place
+    between forward and backward raises instead of silently corrupting dW."""
+    M, N, K = 256, 256, 256
+    lin = torch.nn.Linear(K, N, bias=False).cuda().to(torch.bfloat16)
+    model = fp8t.convert(torch.nn.Sequential(lin), "rowwise_gw_hp")
+    X = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    Xl = X.clone().requires_grad_(True)
+    Xi = Xl * 1   # non-leaf so it can be modified in place
+    Y = model(Xi)
+    Xi.mul_(2)
+    with pytest.raises(RuntimeError):
+        Y.float().sum().backward()
+
+
 @pytest.mark.parametrize("grid", ["1", "3"])
 @pytest.mark.parametrize("gran", ["mx32", "mx32_rm"])
 @pytest.mark.parametrize("fmt,mode", [(E4M3, omx.FLOOR), (E5M2, omx.RCEIL)])
@@ -1009,8 +1069,9 @@ def test_linear_cuda_graph_replay(recipe):
 def test_linear_rowwise_dual_launch_straddle(grid, knob):
     """Rowwise forward with X and W amax'd by one persistent TMA launch (capped grids make CTA tile
     ranges straddle the X -> W boundary, so a row strip of W follows one of X in the same CTA) and cast
-    by one launch: the forward codes, scales and outputs match the oracle; the saved column-scaled
-    copies drive a backward in tolerance."""
+    by one launch: Y, dX and dW within tolerance of the oracle.  (The bytes these launches write are
+    checked bit-exact in test_linear_buffers_bit_exact and across variants in
+    test_linear_cast_launch_variants_identical.)"""
     knob("cast_grid", int(grid))
     M, N, K = 640, 384, 512
     x, w, dy = synth.linear_inputs("c3", M, N, K, seed=5)
@@ -1029,8 +1090,9 @@ def test_linear_rowwise_dual_launch_straddle(grid, knob):
 
 @pytest.mark.parametrize("dual", ["1", "0"], ids=["xw_one_cast_launch", "separate_casts"])
 def test_linear_tensorwise_cast_launches(dual, knob):
-    """Tensorwise forward with X and W cast by one launch (default) or separately: identical bytes,
-    scales and outputs (bit-identical GEMM results), both in tolerance of the oracle."""
+    """Tensorwise forward with X and W cast by one launch (default) or separately: Y, dX and dW within
+    tolerance of the oracle.  (Bytes and scales: test_linear_buffers_bit_exact; bit-identity across
+    the two settings: test_linear_cast_launch_variants_identical.)"""
     knob("tw_dual", int(dual))
     M, N, K = 640, 384, 512
     x, w, dy = synth.linear_inputs("c2", M, N, K, seed=6)
@@ -1071,3 +1133,168 @@ def test_linear_strided_inputs(recipe):
     torch.cuda.synchronize()
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+# ----------------------------------------------------------------------------- what the linear itself writes
+
+LINEAR_BUFFER_CASES = [
+    ("tensorwise", {}), ("tensorwise", {"tw_dual": 0}),
+    ("rowwise", {}), ("rowwise", {"cast_grid": 3}), ("rowwise", {"cast_grid": 7}), ("rowwise", {"amax_tile_tma": 0}),
+    ("rowwise_gw_hp", {}),
+    ("mxfp8", {}), ("mxfp8", {"cast_grid": 3}), ("mxfp8", {"mx_transposed": 1}), ("mxfp8", {"mx_cast_tma": 0}),
+]
+
+
+def _eq(name, got, want):
+    got = _np(got) if torch.is_tensor(got) else np.asarray(got)
+    want = np.asarray(want)
+    if want.dtype == np.float32:
+        got, want = got.view(np.uint32), want.view(np.uint32)
+    assert got.shape == want.shape, (name, got.shape, want.shape)
+    bad = np.argwhere(got != want)
+    assert bad.size == 0, f"{name}: {len(bad)} mismatches, first at {bad[:3].tolist()}"
+
+
+@pytest.mark.parametrize("shape", [(640, 384, 512), (400, 272, 528), (384, 640, 256)],
+                         ids=["multi_tile", "ragged", "wide"])
+@pytest.mark.parametrize("recipe,knobs", LINEAR_BUFFER_CASES,
+                         ids=[r + ("-" + "-".join(f"{k}{v}" for k, v in kn.items()) if kn else "") for r, kn in
+                              LINEAR_BUFFER_CASES])
+def test_linear_buffers_bit_exact(recipe, knobs, shape, knob):
+    """Byte-level parity of what fp8_linear_fwd / fp8_linear_bwd THEMSELVES write (not a separate
+    fp8_cast_scaled call): the forward GEMM operands in the workspace, the saved backward operands,
+    the backward's dY operands, their scales (fp32 bits or E8M0 codes) and the stored amaxes, for
+    every recipe and every launch variant of the casts (tensorwise X/W dual launches on and off;
+    rowwise dual amax/cast launches with capped grids whose CTA ranges straddle X -> W, and the
+    register amax kernel; MX TMA and register casts, capped grids, transposed dim1 copies) -- all
+    bit-exact vs the oracle's casts of the same seeded inputs."""
+    M, N, K = shape
+    if recipe == "mxfp8" and (M % 128 or N % 128 or K % 128):
+        pytest.skip("mxfp8 needs 128-multiples")
+    for k, v in knobs.items():
+        knob(k, v)
+    cfgname = {"tensorwise": "c2", "rowwise": "c3", "rowwise_gw_hp": "c3", "mxfp8": "c4"}[recipe]
+    x, w, dy = synth.linear_inputs(cfgname, M, N, K, seed=11)
+    plan = ops.LinearPlan(M, N, K, recipe=recipe)
+    saved = plan.new_saved()
+    X, W, G = _dev(x, torch.bfloat16), _dev(w, torch.bfloat16), _dev(dy, torch.bfloat16)
+    plan.forward(X, W, saved)
+    torch.cuda.synchronize()
+    fb = {k: (v.clone() if torch.is_tensor(v) else v) for k, v in plan.buffers(saved).items()}   # fwd ws
+    plan.backward(G, saved, x=X)
+    torch.cuda.synchronize()
+    bb = plan.buffers(saved)
+    _, _, so = olin.forward(x, w, recipe)
+    _, _, _, _, co = olin.backward(x, w, dy, recipe)
+    if recipe == "tensorwise":
+        _eq("x_fwd", fb["x_fwd"], so["xq"]); _eq("w_fwd", fb["w_fwd"], so["wq"])
+        _eq("sx", fb["x_fwd_scale"], np.float32(so["sx"]).reshape(1))
+        _eq("sw", fb["w_fwd_scale"], np.float32(so["sw"]).reshape(1))
+        _eq("amax_fwd", fb["amax_fwd"], np.array([so["amax_x"], so["amax_w"]], np.float32))
+        _eq("x_bwd (saved)", bb["x_bwd"], so["xq"]); _eq("w_bwd (saved)", bb["w_bwd"], so["wq"])
+        _eq("sx (saved)", bb["x_bwd_scale"], np.float32(so["sx"]).reshape(1))
+        _eq("dy", bb["dy_dx"], co["gq"]); _eq("sg", bb["dy_dx_scale"], np.float32(co["sg"]).reshape(1))
+        _eq("amax_bwd", bb["amax_bwd"], np.float32(co["amax_g"]).reshape(1))
+    elif recipe in ("rowwise", "rowwise_gw_hp"):
+        gw_hp = recipe == "rowwise_gw_hp"
+        _eq("x_fwd (row-scaled)", fb["x_fwd"], so["xq"]); _eq("sx rows", fb["x_fwd_scale"], so["sx"])
+        _eq("w_fwd (row-scaled)", fb["w_fwd"], so["wq"]); _eq("sw rows", fb["w_fwd_scale"], so["sw"])
+        xc, sxc, axc = fp8.cast_colwise(x, E4M3)
+        wc, swc, awc = fp8.cast_colwise(w, E4M3)
+        am = _np(fb["amax_fwd"])
+        _eq("amax X rows", am[:M], so["amax_x"])
+        if not gw_hp:
+            _eq("amax X cols", am[M:M + K], axc)
+        _eq("amax W rows", am[M + K:M + K + N], so["amax_w"])
+        _eq("amax W cols", am[M + K + N:], awc)
+        _eq("w_bwd (col-scaled, saved)", bb["w_bwd"], co["w_c"]); _eq("sw cols", bb["w_bwd_scale"], co["sw_c"])
+        assert np.array_equal(co["w_c"], wc)
+        _eq("dy_dx (row-scaled)", bb["dy_dx"], co["g_r"]); _eq("sg rows", bb["dy_dx_scale"], co["sg_r"])
+        gr, sgr, agr = fp8.cast_rowwise(dy, E5M2)
+        _eq("amax dY rows", _np(bb["amax_bwd"])[:M], agr)
+        if gw_hp:
+            assert bb["x_bwd"] is None and bb["dy_dw"] is None
+        else:
+            _eq("x_bwd (col-scaled, saved)", bb["x_bwd"], co["x_c"]); _eq("sx cols", bb["x_bwd_scale"], co["sx_c"])
+            _eq("dy_dw (col-scaled)", bb["dy_dw"], co["g_c"]); _eq("sg cols", bb["dy_dw_scale"], co["sg_c"])
+            _eq("amax dY cols", _np(bb["amax_bwd"])[M:], fp8.cast_colwise(dy, E5M2)[2])
+    else:
+        tr = bb["bwd_transposed"]
+        _eq("x_fwd dim0", fb["x_fwd"], so["xq"]); _eq("X E8M0 dim0", _unblock(fb["x_fwd_scale"], M, K), so["xsc"])
+        _eq("w_fwd dim0", fb["w_fwd"], so["wq"]); _eq("W E8M0 dim0", _unblock(fb["w_fwd_scale"], N, K), so["wsc"])
+        _eq("x_bwd dim1", bb["x_bwd"], co["x1"] if tr else co["x1"].T)
+        _eq("X E8M0 dim1", _unblock(bb["x_bwd_scale"], K, M), co["x1s"])
+        _eq("w_bwd dim1", bb["w_bwd"], co["w1"] if tr else co["w1"].T)
+        _eq("W E8M0 dim1", _unblock(bb["w_bwd_scale"], K, N), co["w1s"])
+        _eq("dy_dx dim0", bb["dy_dx"], co["g0"]); _eq("dY E8M0 dim0", _unblock(bb["dy_dx_scale"], M, N), co["g0s"])
+        _eq("dy_dw dim1", bb["dy_dw"], co["g1"] if tr else co["g1"].T)
+        _eq("dY E8M0 dim1", _unblock(bb["dy_dw_scale"], N, M), co["g1s"])
+
+
+@pytest.mark.parametrize("recipe,variants", [("tensorwise", [{}, {"tw_dual": 0}]),
+                                             ("rowwise", [{}, {"cast_grid": 3}, {"cast_grid": 7},
+                                                          {"amax_tile_tma": 0}])])
+def test_linear_cast_launch_variants_identical(recipe, variants, knob):
+    """The cast-launch variants of one recipe write identical bytes (saved buffers and forward
+    workspace) and give bit-identical Y, dX, dW (same codes -> same GEMM inputs)."""
+    M, N, K = 640, 384, 512
+    x, w, dy = synth.linear_inputs("c3", M, N, K, seed=12)
+    X, W, G = _dev(x, torch.bfloat16), _dev(w, torch.bfloat16), _dev(dy, torch.bfloat16)
+    runs = []
+    for v in variants:
+        fp8t.ops.reset_knobs()
+        for k, val in v.items():
+            knob(k, val)
+        plan = ops.LinearPlan(M, N, K, recipe=recipe)
+        saved = plan.new_saved()
+        saved.zero_()
+        plan.ws.zero_()   # alignment padding between regions is never written: make it equal
+        Y = plan.forward(X, W, saved)
+        fws = plan.ws.clone()
+        DX, DW = plan.backward(G, saved)
+        torch.cuda.synchronize()
+        runs.append((saved.clone(), fws, Y.clone(), DX.clone(), DW.clone()))
+    for r in runs[1:]:
+        for a, b, name in zip(runs[0], r, ("saved", "fwd ws", "Y", "dX", "dW")):
+            assert torch.equal(a, b), name
+
+
+# ----------------------------------------------------------------------------- exhaustive fp32 sweep
+
+@pytest.mark.parametrize("fmt", [E4M3, E5M2])
+def test_cast_all_fp32_patterns_scale_one(fmt):
+    """the cast over ALL 2^32 fp32 bit patterns at s = 1 (amax_in = fmax, so
+    s = fmax / fmax = 1 exactly and RN32(x * 1) = x, subnormals included) against the library
+    RNE-with-saturation routine clip(x, +-fmax) -> float8 (R-c1, R-c2).  That routine is the one the
+    oracle's encoder is pinned to on all 2^32 patterns on the CPU (tests/test_oracle_codecs.py,
+    FP8_EXHAUSTIVE=1); here it runs as torch's device conversion, and a random subsample of every
+    chunk re-checks it against ml_dtypes on the host.  NaN inputs (out of contract, R-c9): NaN class
+    only.  16 chunks of 2^28 patterns, each one fp8_cast_scaled launch of a [16384, 16384] fp32 tensor."""
+    import ml_dtypes
+    fmax = 448.0 if fmt == E4M3 else 57344.0
+    tdt = torch.float8_e4m3fn if fmt == E4M3 else torch.float8_e5m2
+    mdt = ml_dtypes.float8_e4m3fn if fmt == E4M3 else ml_dtypes.float8_e5m2
+    amax_in = torch.tensor([fmax], dtype=torch.float32, device="cuda")
+    chunk = 1 << 28
+    g = np.random.default_rng(99)
+    for c in range(1 << 32 >> 28):
+        bits = torch.arange(c * chunk, (c + 1) * chunk, dtype=torch.int64, device="cuda")
+        x = (bits - (1 << 32) * (bits >= (1 << 31))).to(torch.int32).view(torch.float32).view(16384, 16384)
+        del bits
+        out = ops.cast(x, FMTNAME[fmt], "tensor", want_q=True, amax_in=amax_in)
+        assert _np(out["scale"])[0] == 1.0
+        q = out["q"].view(-1)
+        xf = x.view(-1)
+        nan = torch.isnan(xf)
+        ref = xf.clamp(-fmax, fmax).to(tdt).view(torch.uint8)
+        ok = (q == ref) | nan
+        assert bool(ok.all()), f"chunk {c}: {int((~ok).sum())} mismatches"
+        qn = q[nan]
+        cls = (qn & 0x7F) == 0x7F if fmt == E4M3 else (((qn & 0x7C) == 0x7C) & ((qn & 3) != 0))
+        assert bool(cls.all()), f"chunk {c}: NaN input not encoded as NaN"
+        idx = torch.from_numpy(g.integers(0, chunk, 1 << 16)).cuda()
+        xs, rs = _np(xf[idx]), _np(ref[idx])
+        fin = ~np.isnan(xs)
+        want = np.clip(xs[fin], -fmax, fmax).astype(mdt).view(np.uint8)
+        assert np.array_equal(rs[fin], want), f"chunk {c}: device library cast != ml_dtypes"
+        del x, out, q, ref, nan, ok

@@ -1,6 +1,7 @@
 """The seeded input generator: determinism, row-addressability, bf16 rounding."""
 
 import numpy as np
+import pytest
 
 import synth
 
@@ -30,3 +31,30 @@ def test_bf16_rounding_is_rne_and_values_representable():
 def test_normal_moments():
     z = synth.normal(synth.stream_key("moments"), (200000,))
     assert abs(z.mean()) < 0.01 and abs(z.std() - 1) < 0.01
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
+def test_recipe_rows_match_full(cfg):
+    f = synth.RECIPES[cfg]
+    for name in ("x", "w", "dy"):
+        full = f(name, (96, 256), 4, cfg)
+        part = f(name, (96, 256), 4, cfg, rows=(37, 71))
+        assert np.array_equal(full[37:71].view(np.uint32), part.view(np.uint32)), (cfg, name)
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
+def test_device_port_matches_host_generator(cfg):
+    """synth.device (torch ops; bench.py's generator) reproduces synth bit for bit -- here with torch on
+    the CPU; tests/test_gpu_synth.py repeats it on the GPU at the full bench shapes."""
+    import torch
+    from synth import device as sd
+    f = synth.RECIPES[cfg]
+    for name, shape in (("x", (80, 256)), ("w", (64, 256)), ("dy", (80, 64 * 4))):
+        ref = f(name, shape, 2, cfg)
+        got = sd.tensor(cfg, name, shape, 2, "cpu").float().numpy()
+        assert np.array_equal(ref.view(np.uint32), got.view(np.uint32)), (cfg, name)
+        part = sd.tensor(cfg, name, shape, 2, "cpu", rows=(17, 50)).float().numpy()
+        assert np.array_equal(ref[17:50].view(np.uint32), part.view(np.uint32)), (cfg, name)
+    ws = synth.weight_shard_c5((64, 256), 1, 1, 4)
+    got = sd.weight_shard_c5((64, 256), 1, 1, 4, "cpu").float().numpy()
+    assert np.array_equal(ws.view(np.uint32), got.view(np.uint32))
