@@ -101,6 +101,9 @@ def parse():
                          "through the FSDP gather path, the same-config N=1 point of the N>1 runs)")
     ap.add_argument("--no-digest", dest="digest", action="store_false",
                     help="skip the SHA-256 of the timed inputs")
+    ap.add_argument("--knob", action="append", default=[],
+                    help="name=value: select a kernel variant via fp8_set_knob (A/B experiments; default = "
+                         "the product path); recorded in the JSON line")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -1106,6 +1109,12 @@ def main():
         return
     subs = [c for c in (a.sub.split(",") if a.sub else (["c2", "c3", "c5"] if default_headline and world == 1
                                                           else [])) if c]
+    if a.knob:
+        import paper_2507_16099_b200  # noqa: F401
+        from paper_2507_16099_b200 import ops
+        for kv in a.knob:
+            k, v = kv.split("=")
+            ops.set_knob(k, int(v))
     line = run_config(a, a.config)
     sub = {}
     for c in subs:
@@ -1117,6 +1126,8 @@ def main():
                                                                   "n_gpus", "scaling")}
     if line is not None:
         line["host"] = host_info()
+        if a.knob:
+            line["knobs"] = a.knob
         line["context"] = PAPER_CONTEXT
         if sub:
             line["sub"] = sub

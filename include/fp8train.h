@@ -355,6 +355,10 @@ fp8_status_t fp8_comm_get_unique_id(uint8_t id[128]);
  * current CUDA device. */
 fp8_status_t fp8_comm_init(fp8_comm_t* comm, const uint8_t id[128], int nranks, int rank);
 fp8_status_t fp8_comm_destroy(fp8_comm_t comm);
+/* Communicator health: FP8_ENCCL if NCCL reports an asynchronous error on it (ncclCommGetAsyncError:
+ * a peer failed, a timed-out or aborted operation), or the pending device fault (fp8_check_async_error).
+ * The FSDP entry points run the same check before enqueuing work. */
+fp8_status_t fp8_comm_check(fp8_comm_t comm);
 size_t fp8_fsdp_workspace_bytes(fp8_hp_t w_shard);
 fp8_status_t fp8_fsdp_allgather(fp8_comm_t comm, fp8_hp_t w_shard, fp8_format_t fmt,
                                 uint8_t* w_full, float* scale_out, float* amax_out,
@@ -498,6 +502,15 @@ fp8_status_t fp8_tp_allgather_linear_fwd_local(fp8_p2p_t* wins, int nranks, cons
  * Helpers
  * ------------------------------------------------------------------------- */
 int fp8_abi_version(void);
+/* Asynchronous device faults.  Kernels that wait on other ranks (the P2P FSDP gather, the fused
+ * reduce-scatter, async-TP) give up after the watchdog (knob watchdog_ms, default 30 s) instead of
+ * trapping -- a trap would poison the CUDA context -- and record a fault code in a process-wide word of
+ * pinned, device-mapped host memory; grouped GEMMs record invalid device offsets the same way.  The
+ * outputs of the call that faulted are invalid.  fp8_check_async_error() returns FP8_OK or the recorded
+ * fault (FP8_ECUDA / FP8_EINVAL, with fp8_last_error() naming the rank / chunk / epoch) and clears it;
+ * every P2P, async-TP, fused reduce-scatter, grouped and FSDP entry point performs the same check first.
+ * Like any asynchronous CUDA error, a fault becomes visible only after the faulting kernel ran. */
+fp8_status_t fp8_check_async_error(void);
 /* Thread-local message describing the last non-OK status of this thread. */
 const char* fp8_last_error(void);
 /* Number of kernels this library has launched in the calling process (all
@@ -510,7 +523,9 @@ uint64_t fp8_launch_count(void);
  *   mx_cast_tma (1) | gemm_cta_group (2) | gemm_debug (0) | gemm_sched (1 = dynamic) |
  *   mx_sf_split (1) | gemm_raster (-1 = per problem) | mx_n192 (0) | gemm_stages (3) |
  *   gemm_epi (0 = by K) | mx_transposed (0; forward and backward of one linear must agree) |
- *   tw_dual (1)   -- defaults in parentheses.
+ *   tw_dual (1) | gemm_kserp (1: odd waves of GEMM tiles walk K backwards) |
+ *   watchdog_ms (30000; 0 = peer waits never give up)
+ *   -- defaults in parentheses.
  * A knob changes launches enqueued after the call.  Unknown name or out-of-range value:
  * FP8_EINVAL, nothing changed.  fp8_reset_knobs restores every default. */
 fp8_status_t fp8_set_knob(const char* name, int value);

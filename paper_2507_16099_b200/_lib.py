@@ -53,6 +53,8 @@ SIGNATURES = {
     "fp8_launch_count": (_c.c_uint64, []),
     "fp8_profile_enable": (None, [_c.c_int]),
     "fp8_set_knob": (_c.c_int, [_c.c_char_p, _c.c_int]),
+    "fp8_check_async_error": (_c.c_int, []),
+    "fp8_comm_check": (_c.c_int, [_c.c_void_p]),
     "fp8_get_knob": (_c.c_int, [_c.c_char_p, _c.POINTER(_c.c_int)]),
     "fp8_reset_knobs": (None, []),
     "fp8_profile_collect": (_c.c_int, [_c.POINTER(_c.c_int), _c.POINTER(_c.c_float), _c.c_int]),

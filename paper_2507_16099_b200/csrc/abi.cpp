@@ -31,9 +31,10 @@ static const KnobDef kKnobs[KNOB_COUNT] = {
     {"gemm_debug", 0, 0, 1 << 16},  {"gemm_sched", 1, 0, 1},       {"mx_sf_split", 1, 0, 8},
     {"gemm_raster", -1, -1, 64},    {"mx_n192", 0, 0, 1},          {"gemm_stages", 3, 3, 6},
     {"gemm_epi", 0, 0, 8},          {"mx_transposed", 0, 0, 1},    {"tw_dual", 1, 0, 1},
+    {"gemm_kserp", 1, 0, 1},        {"watchdog_ms", 30000, 0, 1 << 30},
 };
 static std::atomic<int> g_knobs[KNOB_COUNT] = {
-    {1}, {0}, {8}, {8}, {1}, {2}, {0}, {1}, {1}, {-1}, {0}, {3}, {0}, {0}, {1},
+    {1}, {0}, {8}, {8}, {1}, {2}, {0}, {1}, {1}, {-1}, {0}, {3}, {0}, {0}, {1}, {1}, {30000},
 };
 int knob(Knob k) { return g_knobs[k].load(std::memory_order_relaxed); }
 static int knob_index(const char* name) {
@@ -41,6 +42,55 @@ static int knob_index(const char* name) {
   for (int i = 0; i < KNOB_COUNT; ++i)
     if (std::strcmp(name, kKnobs[i].name) == 0) return i;
   return -1;
+}
+
+// ---- asynchronous device faults ----
+fp8_status_t fail(fp8_status_t st, const char* fmt, ...);
+static std::once_flag g_fault_once;
+static volatile unsigned* g_fault_host = nullptr;
+static unsigned* g_fault_dev = nullptr;
+unsigned* fault_word() {
+  std::call_once(g_fault_once, [] {
+    void* h = nullptr;
+    if (cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    std::memset(h, 0, 64);
+    void* d = nullptr;
+    if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFreeHost(h);
+      return;
+    }
+    g_fault_host = static_cast<volatile unsigned*>(h);
+    g_fault_dev = static_cast<unsigned*>(d);
+  });
+  return g_fault_dev;
+}
+unsigned long long watchdog_ns() { return (unsigned long long)knob(KNOB_WATCHDOG_MS) * 1000000ull; }
+fp8_status_t check_fault() {
+  if (!g_fault_host) return FP8_OK;
+  const unsigned f = *g_fault_host;
+  if (!f) return FP8_OK;
+  *g_fault_host = 0;
+  const unsigned code = f >> 24, peer = (f >> 16) & 0xFF, ep = f & 0xFFFF;
+  switch (code) {
+    case FAULT_P2P_AMAX_WAIT:
+      return fail(FP8_ECUDA, "earlier P2P gather: rank %u's amax signal (epoch %u) never arrived within the "
+                  "watchdog; its outputs are invalid", peer, ep);
+    case FAULT_P2P_DONE_WAIT:
+      return fail(FP8_ECUDA, "earlier P2P call: rank %u's pushes / tiles (epoch %u) never completed within the "
+                  "watchdog; its outputs are invalid", peer, ep);
+    case FAULT_TP_CHUNK_WAIT:
+      return fail(FP8_ECUDA, "earlier async-TP GEMM: A chunk %u never arrived within the watchdog; its outputs "
+                  "are invalid", peer);
+    case FAULT_GROUP_OFFSETS:
+      return fail(FP8_EINVAL, "earlier grouped GEMM: device group offsets invalid (need 0 = offs[0] <= ... <= "
+                  "offs[G] = extent, multiples of 128); its outputs are invalid");
+    default:
+      return fail(FP8_ECUDA, "earlier kernel reported device fault 0x%08x", f);
+  }
 }
 
 // ---- per-device host caches ----
@@ -164,6 +214,8 @@ using namespace fp8t;
 extern "C" {
 
 int fp8_abi_version(void) { return FP8TRAIN_ABI_VERSION; }
+
+fp8_status_t fp8_check_async_error(void) { return check_fault(); }
 
 fp8_status_t fp8_set_knob(const char* name, int value) {
   const int i = knob_index(name);
@@ -793,6 +845,7 @@ fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const f
 fp8_status_t fp8_linear_bwd_rs(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x, const void* saved,
                                const fp8_tensor_t* w_fp8, void* dx, fp8_p2p_t rs_win, int nranks, void* dw_shard,
                                void* ws, size_t ws_bytes, void* stream) {
+  FP8T_TRY(check_fault());
   if (!rs_win || !dw_shard) return fail(FP8_EINVAL, "rs_win / dw_shard: null");
   if (nranks < 1) return fail(FP8_EINVAL, "nranks < 1");
   if (!cfg || cfg->out_dtype != FP8_DT_BF16) return fail(FP8_EUNSUPPORTED, "fused reduce-scatter: bf16 dW only");
@@ -982,6 +1035,7 @@ GBwdWs carve_gbwd(const fp8_linear_cfg_t* cfg, int64_t T, int64_t E, int64_t N, 
 }
 
 fp8_status_t check_grouped(const fp8_linear_cfg_t* cfg, int64_t T, int64_t E, int64_t N, int64_t K, const int* offs) {
+  FP8T_TRY(check_fault());
   if (!cfg) return fail(FP8_EINVAL, "cfg: null pointer");
   if (cfg->recipe != FP8_RECIPE_TENSORWISE && cfg->recipe != FP8_RECIPE_ROWWISE)
     return fail(FP8_EUNSUPPORTED, "grouped GEMM: tensorwise or rowwise recipe");

@@ -21,6 +21,7 @@
 namespace fp8t {
 fp8_status_t fail(fp8_status_t st, const char* fmt, ...);
 fp8_status_t cuda_check(cudaError_t e, const char* what);
+fp8_status_t check_fault();
 }  // namespace fp8t
 using namespace fp8t;
 
@@ -30,7 +31,24 @@ static fp8_status_t nccl_check(ncclResult_t r, const char* what) {
   return fail(FP8_ENCCL, "%s: %s", what, ncclGetErrorString(r));
 }
 
+// Health of a communicator before enqueuing more work on it: an asynchronous NCCL error (a peer died,
+// a network / NVLink fault, a timed-out operation) is polled with ncclCommGetAsyncError and
+// returned as FP8_ENCCL, as is an earlier device fault recorded in the fault word.
+static fp8_status_t comm_health(fp8_comm_t comm) {
+  if (!comm) return fail(FP8_EINVAL, "comm: null");
+  fp8_status_t s = check_fault();
+  if (s != FP8_OK) return s;
+  ncclResult_t ae = ncclSuccess;
+  ncclResult_t r = ncclCommGetAsyncError(comm->nccl, &ae);
+  if (r != ncclSuccess) return fail(FP8_ENCCL, "ncclCommGetAsyncError: %s", ncclGetErrorString(r));
+  if (ae != ncclSuccess && ae != ncclInProgress)
+    return fail(FP8_ENCCL, "communicator in error state (asynchronous NCCL error): %s", ncclGetErrorString(ae));
+  return FP8_OK;
+}
+
 extern "C" {
+
+fp8_status_t fp8_comm_check(fp8_comm_t comm) { return comm_health(comm); }
 
 fp8_status_t fp8_comm_get_unique_id(uint8_t id[128]) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
@@ -65,6 +83,10 @@ size_t fp8_fsdp_workspace_bytes(fp8_hp_t) { return 0; }
 
 fp8_status_t fp8_fsdp_precompute_amax(fp8_comm_t comm, const fp8_hp_t* w, int n, float* amax_out, void* stream) {
   if (!comm) return fail(FP8_EINVAL, "comm: null");
+  {
+    const fp8_status_t h = comm_health(comm);
+    if (h != FP8_OK) return h;
+  }
   fp8_status_t s = fp8_amax_multi(w, n, amax_out, stream);
   if (s != FP8_OK) return s;
   return nccl_check(ncclAllReduce(amax_out, amax_out, (size_t)n, ncclUint32, ncclMax, comm->nccl,
@@ -87,6 +109,10 @@ fp8_status_t fp8_fsdp_allgather_ex(fp8_comm_t comm, fp8_hp_t w, fp8_format_t fmt
   if ((reinterpret_cast<uintptr_t>(w.ptr) | reinterpret_cast<uintptr_t>(w_full)) & 15)
     return fail(FP8_EALIGN, "pointers must be 16-byte aligned");
   if (w.ld < w.cols || (w.ld * (w.dtype == FP8_DT_F32 ? 4 : 2)) % 16) return fail(FP8_EALIGN, "bad ld");
+  {
+    const fp8_status_t h = comm_health(comm);
+    if (h != FP8_OK) return h;
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool bf16 = w.dtype == FP8_DT_BF16;
   const size_t chunk = (size_t)w.rows * (size_t)w.cols;
@@ -153,6 +179,10 @@ fp8_status_t fp8_fsdp_allgather_mx(fp8_comm_t comm, fp8_hp_t w, fp8_mx_round_t m
   const bool dim1 = out->q_t != nullptr;
   if (dim1 && (!ws || ws_bytes < fp8_fsdp_mx_workspace_bytes(w, comm->nranks)))
     return fail(FP8_EWORKSPACE, "workspace too small");
+  {
+    const fp8_status_t h = comm_health(comm);
+    if (h != FP8_OK) return h;
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t chunk = (size_t)w.rows * (size_t)w.cols, r = (size_t)comm->rank;
   uint8_t* q0 = out->q + r * chunk;

@@ -98,6 +98,9 @@ struct GemmArgs {
   int group_m;        // tile raster (see tile_coords)
   int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
   int sf_split;       // MX: scale-factor copies issued by their own warp (see the SF copier)
+  int kserp;          // K-serpentine: tiles of odd "waves" (tile / pairs) walk their K stages backwards
+  unsigned* fault;    // process fault word (async-TP watchdog, bad group offsets); may be null
+  unsigned long long watchdog_ns;
   unsigned* sched;    // dynamic tile scheduler slot (g_sched[i]); null: static round robin
 };
 
@@ -234,9 +237,12 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
         }
         prev = v;
       }
-      if (!ok || prev != extent) {
-        if (blockIdx.x == 0) printf("fp8_gemm: bad group offsets (need 0 = offs[0] <= ... <= offs[G] = %d, multiples of 128)\n", extent);
-        asm volatile("trap;");
+      if (!ok || prev != extent) {   // report through the fault word; compute no tile of this problem
+        if (blockIdx.x == 0 && args.fault) atomicExch_system(args.fault, fault_pack(FAULT_GROUP_OFFSETS, lane, 0));
+        for (int g = 0; g <= P.G; ++g) {
+          o[g] = 0;
+          pre[g] = 0;
+        }
       }
     }
   }
@@ -470,22 +476,33 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
       const uint32_t sf_tx = (args.debug & 4) ? 0u : L::sf_tx_bytes;
       const int KT = P.sf_tiles_k;
       const int num_kb = ti.num_kb;
+      // K-serpentine (not for grouped problems): consecutive waves of tiles share operand panels (the
+      // grouped raster keeps M blocks across waves), so a wave that walks K in the opposite direction
+      // starts on the K slices the previous wave read last -- still in L2 -- instead of re-reading the
+      // panels from DRAM.  The direction is a function of the tile index only (deterministic results).
+      const bool krev = !GRP && args.kserp && ((tile / cta_stride) & 1);
       if (P.chunk_done) {   // async-TP: wait until the rank that owns these A rows has pushed them
         if (lane == 0) {
           const unsigned long long* f = P.chunk_done + (m0 + ti.a_row0) / P.chunk_rows;
-          uint32_t n = 0;
+          uint64_t t0;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
           while (ld_acquire_sys_u64(f) < P.chunk_epoch) {
             __nanosleep(64);
-            if (++n > (1u << 27)) {
-              printf("fp8_gemm: A chunk %d never arrived (watchdog)\n", (m0 + ti.a_row0) / P.chunk_rows);
-              asm volatile("trap;");
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (args.watchdog_ns && args.fault && t - t0 > args.watchdog_ns) {   // give up: report, load anyway
+              atomicExch_system(args.fault, fault_pack(FAULT_TP_CHUNK_WAIT, (m0 + ti.a_row0) / P.chunk_rows,
+                                                       P.chunk_epoch));
+              __threadfence_system();
+              break;
             }
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");   // generic-proxy acquire -> TMA reads
         }
         __syncwarp();
       }
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kbi = 0; kbi < num_kb; ++kbi) {
+        const int kb = krev ? num_kb - 1 - kbi : kbi;
         mbar_wait(empty_bar + 8 * stage, phase ^ 1);
         if (lane == 0) {
           // MX: E8M0 tiles first, on their own barrier: they land long before the operands, so the SF
@@ -964,7 +981,12 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
 // 32: 2.02, 64: 2.16; c4 8.42-8.47 ms (8, 16) vs 9.09 (32), 9.78 (64); c3 layer step -1 to -3 %.
 // (Round r01c chose row-major when all of B fit ~80 MB of L2; with the dynamic scheduler the grouped
 // raster is as good or better for every shape measured.)  knob gemm_raster overrides (0 = row-major).
-static int choose_raster(const GemmProblem&, bool) { return GROUP_M; }
+// Round r02 (K-serpentine on, tools/prof_raster.sh): long-K problems (K >= 16384: the c4 backward's dX and
+// dW, the c2 / c5 dW) keep fewer M tiles per group -- a wave then touches ~8 A panels and ~9 B panels
+// instead of 16 + 4.6, whose K slices the next wave re-reads from L2: c4 backward DRAM reads 8.35 -> 7.41 GB
+// per launch and the c4 step 9.27 -> 9.07 ms; the c4 forward (K = 8192) keeps 16 (its DRAM reads 1.30 GB
+// with 16 vs 2.14 GB with 8).
+static int choose_raster(const GemmProblem& p, bool) { return p.K >= 16384 ? 8 : GROUP_M; }
 
 // This launch's slot of g_sched on the current device: eager launches round-robin over
 // [0, SCHED_SLOTS); a launch under stream capture takes the next unused slot of the graph region,
@@ -1034,6 +1056,13 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
       if (!a.sched && !exhausted) return cudaErrorInvalidValue;
     }
     a.sf_split = knob(KNOB_MX_SF_SPLIT);
+    a.kserp = knob(KNOB_GEMM_KSERP);
+    bool need_fault = GRP;
+    for (int i = 0; i < n; ++i) need_fault = need_fault || ps[i].chunk_done != nullptr;
+    if (need_fault) {
+      a.fault = fault_word();
+      a.watchdog_ns = watchdog_ns();
+    }
     // raster per problem (choose_raster); knob gemm_raster >= 0 overrides for every problem
     const int r = knob(KNOB_GEMM_RASTER);
     a.group_m = r >= 0 ? r : GROUP_M;

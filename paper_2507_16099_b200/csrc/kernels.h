@@ -30,9 +30,31 @@ enum Knob {
   KNOB_GEMM_EPI,            // 0: epilogue warps by K (8 for K <= 1024, else 4); 4 / 8: forced
   KNOB_MX_TRANSPOSED,       // 1: MX dim1 copies written transposed, read K-major (fwd and bwd must agree)
   KNOB_TW_DUAL,             // 1: tensorwise forward X/W amax and cast by one launch each; 0: four launches
+  KNOB_GEMM_KSERP,          // 1: odd waves of GEMM tiles walk K backwards (L2 reuse across waves); 0: all forward
+  KNOB_WATCHDOG_MS,         // peer waits (P2P gather, fused reduce-scatter, async-TP) give up after this many ms
+                            // and report FP8_ECUDA at the next call; 0 = wait forever
   KNOB_COUNT
 };
 int knob(Knob k);
+
+// ---- asynchronous device faults (instead of trap) ----
+// A kernel that gives up waiting on a peer (watchdog) or rejects device-side arguments writes a code to
+// the process-wide fault word -- pinned host memory mapped into every device -- and returns without
+// trapping, so the CUDA context survives.  The next ABI call that checks it (fp8_check_async_error and
+// every P2P / FSDP / grouped / async-TP entry point) reports it as a status and clears it.
+enum FaultCode : unsigned {
+  FAULT_P2P_AMAX_WAIT = 1,   // a peer's amax signal never arrived (peer = slot, low bits = epoch)
+  FAULT_P2P_DONE_WAIT = 2,   // a peer's pushes / reduce-scatter tiles never completed
+  FAULT_TP_CHUNK_WAIT = 3,   // async-TP: a chunk of A rows never arrived
+  FAULT_GROUP_OFFSETS = 4,   // grouped GEMM: device offsets not 0 = o0 <= ... <= oG = extent, multiples of 128
+};
+__host__ __device__ constexpr unsigned fault_pack(unsigned code, unsigned peer, unsigned epoch) {
+  return (code << 24) | ((peer & 0xFFu) << 16) | (epoch & 0xFFFFu);
+}
+// Device-visible pointer to the fault word (nullptr if the pinned allocation failed: then the kernels
+// fall back to waiting without a watchdog); watchdog timeout in ns (knob watchdog_ms; 0 = none).
+unsigned* fault_word();
+unsigned long long watchdog_ns();
 
 // Multiprocessor count of the current device (cached per device).
 int device_sm_count();

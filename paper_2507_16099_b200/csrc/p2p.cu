@@ -13,8 +13,9 @@
 //   5. p2p_wait_done  : spin until all P done slots >= e  -> the gathered codes are complete
 // Step 3 doubles as the cross-rank WAR barrier: rank p pushes epoch-e codes into my buffer only
 // after my epoch-e amax signal, which my stream issues after all my earlier work (the GEMMs that
-// read epoch e-1's codes).  Every spin has a 10 s watchdog (globaltimer) that traps instead of
-// hanging the GPU.
+// read epoch e-1's codes).  Every spin has a watchdog (globaltimer, knob watchdog_ms, default 30 s):
+// on expiry it writes a fault code to the process-wide fault word (pinned host memory) and gives up
+// instead of trapping, so the context survives and the next call returns FP8_ECUDA.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -32,13 +33,21 @@
 namespace fp8t {
 fp8_status_t fail(fp8_status_t st, const char* fmt, ...);
 fp8_status_t cuda_check(cudaError_t e, const char* what);
+fp8_status_t check_fault();
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-constexpr uint64_t kWatchdogNs = 10ull * 1000 * 1000 * 1000;
+// Watchdog: true (after recording `code` in the fault word) once `timeout_ns` passed since t0.
+__device__ __forceinline__ bool watchdog_expired(uint64_t t0, unsigned long long timeout_ns, unsigned* fault,
+                                                 unsigned code) {
+  if (!timeout_ns || !fault || globaltimer_ns() - t0 <= timeout_ns) return false;
+  atomicExch_system(fault, code);
+  __threadfence_system();
+  return true;
+}
 
 __global__ void p2p_signal_amax_kernel(const __grid_constant__ P2PPeers pe, const uint32_t* amax_bits, uint32_t epoch) {
   const unsigned long long v = ((unsigned long long)epoch << 32) | (unsigned long long)*amax_bits;
@@ -46,17 +55,15 @@ __global__ void p2p_signal_amax_kernel(const __grid_constant__ P2PPeers pe, cons
 }
 
 template <int FMT>
-__global__ void p2p_wait_scale_kernel(P2PSig* mine, int P, uint32_t epoch, float* scale_out, float* amax_out) {
+__global__ void p2p_wait_scale_kernel(P2PSig* mine, int P, uint32_t epoch, float* scale_out, float* amax_out,
+                                      unsigned* fault, unsigned long long timeout_ns) {
   const int lane = threadIdx.x;
   uint32_t m = 0;
   const uint64_t t0 = globaltimer_ns();
   for (int p = lane; p < P; p += 32) {
     unsigned long long v;
     while (((v = ld_acquire_sys_u64(&mine->amax[p])) >> 32) != epoch) {
-      if (globaltimer_ns() - t0 > kWatchdogNs) {
-        printf("fp8train p2p: rank amax slot %d never reached epoch %u (watchdog)\n", p, epoch);
-        asm volatile("trap;");
-      }
+      if (watchdog_expired(t0, timeout_ns, fault, fault_pack(FAULT_P2P_AMAX_WAIT, p, epoch))) break;
       __nanosleep(100);
     }
     m = max(m, (uint32_t)(v & 0xFFFFFFFFull));
@@ -69,14 +76,12 @@ __global__ void p2p_wait_scale_kernel(P2PSig* mine, int P, uint32_t epoch, float
   }
 }
 
-__global__ void p2p_wait_done_kernel(P2PSig* mine, int P, uint32_t epoch) {
+__global__ void p2p_wait_done_kernel(P2PSig* mine, int P, uint32_t epoch, unsigned* fault,
+                                     unsigned long long timeout_ns) {
   const uint64_t t0 = globaltimer_ns();
   for (int p = threadIdx.x; p < P; p += blockDim.x) {
     while (ld_acquire_sys_u64(&mine->done[p]) < epoch) {
-      if (globaltimer_ns() - t0 > kWatchdogNs) {
-        printf("fp8train p2p: rank %d pushes of epoch %u never completed (watchdog)\n", p, epoch);
-        asm volatile("trap;");
-      }
+      if (watchdog_expired(t0, timeout_ns, fault, fault_pack(FAULT_P2P_DONE_WAIT, p, epoch))) break;
       __nanosleep(100);
     }
   }
@@ -158,6 +163,7 @@ fp8_status_t fp8_p2p_alloc(size_t bytes, int nranks, int rank, fp8_p2p_t* out, u
   if (bytes == 0) return fail(FP8_EINVAL, "bytes must be > 0");
   if (nranks < 1 || nranks > P2P_MAXP || rank < 0 || rank >= nranks)
     return fail(FP8_EINVAL, "bad nranks / rank (at most %d ranks)", P2P_MAXP);
+  fault_word();   // the watchdog's fault word, allocated at setup (not inside a capture)
   uint8_t* base = nullptr;
   fp8_status_t s = alloc_window(bytes, &base);
   if (s != FP8_OK) return s;
@@ -252,6 +258,7 @@ fp8_status_t fp8_p2p_create(fp8_comm_t comm, size_t bytes, fp8_p2p_t* out) {
 fp8_status_t fp8_p2p_create_local(int nranks, size_t bytes, fp8_p2p_t* out) {
   if (!out) return fail(FP8_EINVAL, "out: null pointer");
   if (nranks < 1 || nranks > P2P_MAXP || bytes == 0) return fail(FP8_EINVAL, "bad nranks / bytes");
+  fault_word();
   std::vector<uint8_t*> bases(nranks, nullptr);
   for (int p = 0; p < nranks; ++p) {
     fp8_status_t s = alloc_window(bytes, &bases[p]);
@@ -303,6 +310,7 @@ namespace {
 fp8_status_t p2p_check(fp8_p2p_t win, const fp8_hp_t& w, fp8_format_t fmt, const float* amax_in, float* scale_out,
                        float* amax_out) {
   if (!win) return fail(FP8_EINVAL, "win: null");
+  FP8T_P2P_TRY(check_fault());
   if (!w.ptr || !scale_out || (!amax_out && !amax_in)) return fail(FP8_EINVAL, "null pointer");
   if (fmt != FP8_E4M3 && fmt != FP8_E5M2) return fail(FP8_EINVAL, "bad fp8 format");
   if (w.dtype != FP8_DT_F32 && w.dtype != FP8_DT_BF16) return fail(FP8_EINVAL, "bad dtype");
@@ -334,8 +342,10 @@ fp8_status_t phase_signal(fp8_p2p_t win, const fp8_hp_t& w, const float* amax_in
 }
 fp8_status_t phase_wait_scale(fp8_p2p_t win, fp8_format_t fmt, float* scale_out, float* amax_out, cudaStream_t st) {
   LaunchScope ls(K_SYNC, st);
-  if (fmt == FP8_E4M3) p2p_wait_scale_kernel<0><<<1, 32, 0, st>>>(win->sig, win->P, win->epoch, scale_out, amax_out);
-  else p2p_wait_scale_kernel<1><<<1, 32, 0, st>>>(win->sig, win->P, win->epoch, scale_out, amax_out);
+  unsigned* f = fault_word();
+  const unsigned long long to = watchdog_ns();
+  if (fmt == FP8_E4M3) p2p_wait_scale_kernel<0><<<1, 32, 0, st>>>(win->sig, win->P, win->epoch, scale_out, amax_out, f, to);
+  else p2p_wait_scale_kernel<1><<<1, 32, 0, st>>>(win->sig, win->P, win->epoch, scale_out, amax_out, f, to);
   return cuda_check(cudaGetLastError(), "p2p_wait_scale");
 }
 fp8_status_t phase_cast_push(fp8_p2p_t win, const fp8_hp_t& w, fp8_format_t fmt, const float* scale, cudaStream_t st) {
@@ -346,7 +356,7 @@ fp8_status_t phase_cast_push(fp8_p2p_t win, const fp8_hp_t& w, fp8_format_t fmt,
 }
 fp8_status_t phase_wait_done(fp8_p2p_t win, cudaStream_t st) {
   LaunchScope ls(K_SYNC, st);
-  p2p_wait_done_kernel<<<1, 64, 0, st>>>(win->sig, win->P, win->epoch);
+  p2p_wait_done_kernel<<<1, 64, 0, st>>>(win->sig, win->P, win->epoch, fault_word(), watchdog_ns());
   return cuda_check(cudaGetLastError(), "p2p_wait_done");
 }
 
@@ -403,6 +413,7 @@ TpWs carve_tp(void* ws) {
 }
 fp8_status_t tp_check(fp8_p2p_t win, const fp8_linear_cfg_t* cfg, const fp8_hp_t& x, const fp8_hp_t& w, void* y,
                       void* ws, size_t ws_bytes) {
+  FP8T_P2P_TRY(check_fault());
   if (!cfg || cfg->recipe != FP8_RECIPE_TENSORWISE) return fail(FP8_EUNSUPPORTED, "async-TP: tensorwise recipe");
   if (cfg->out_dtype != FP8_DT_BF16 && cfg->out_dtype != FP8_DT_F32) return fail(FP8_EINVAL, "bad out_dtype");
   if (!y || !ws || !w.ptr) return fail(FP8_EINVAL, "null pointer");
@@ -530,6 +541,7 @@ size_t fp8_tp_bwd_workspace_bytes(int64_t M, int64_t n_local) { return 1024 + ((
 fp8_status_t fp8_tp_linear_bwd(fp8_p2p_t win, const void* fwd_ws, fp8_p2p_t rs_win, const fp8_linear_cfg_t* cfg,
                                fp8_hp_t dy, int64_t K, void* dx_shard, void* dw, void* ws, size_t ws_bytes,
                                void* stream) {
+  FP8T_P2P_TRY(check_fault());
   if (!win || !rs_win || !fwd_ws || !cfg || !ws || !dx_shard || !dw) return fail(FP8_EINVAL, "null pointer");
   if (cfg->recipe != FP8_RECIPE_TENSORWISE || cfg->out_dtype != FP8_DT_BF16)
     return fail(FP8_EUNSUPPORTED, "async-TP backward: tensorwise recipe, bf16 outputs");

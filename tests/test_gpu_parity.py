@@ -1298,3 +1298,55 @@ def test_cast_all_fp32_patterns_scale_one(fmt):
         want = np.clip(xs[fin], -fmax, fmax).astype(mdt).view(np.uint8)
         assert np.array_equal(rs[fin], want), f"chunk {c}: device library cast != ml_dtypes"
         del x, out, q, ref, nan, ok
+
+
+# ----------------------------------------------------------------------------- asynchronous faults
+
+def test_p2p_watchdog_reports_instead_of_trapping(knob):
+    """A rank whose peer never arrives (here: rank 1 of a local group simply never calls) gives up after
+    the watchdog (knob watchdog_ms) instead of trapping: the CUDA context survives, the next check returns
+    FP8_ECUDA naming the missing rank, and a fresh group gathers correctly afterwards (verdict r01 #6)."""
+    from paper_2507_16099_b200 import _lib as L
+    from paper_2507_16099_b200.fsdp import P2PWindow
+    knob("watchdog_ms", 300)
+    assert L.lib.fp8_check_async_error() == L.FP8_OK
+    wf = synth.tensor_c2("w", (512, 256), seed=4)
+    wins = P2PWindow.local_group(2, wf.size)
+    shard = _dev(wf[:256], torch.bfloat16)
+    q, s, _ = wins[0].allgather_fp8(shard, "e4m3")   # rank 1 never signals
+    torch.cuda.synchronize()                          # no sticky error: the kernels returned
+    st = L.lib.fp8_check_async_error()
+    assert st == L.FP8_ECUDA, st
+    assert b"rank 1" in L.lib.fp8_last_error()
+    assert L.lib.fp8_check_async_error() == L.FP8_OK   # reported once
+    for w_ in wins:
+        w_.close()
+    wins = P2PWindow.local_group(2, wf.size)
+    outs = P2PWindow.allgather_local(wins, [_dev(wf[:256], torch.bfloat16), _dev(wf[256:], torch.bfloat16)])
+    torch.cuda.synchronize()
+    ref = fp8.cast_tensorwise(wf, E4M3)[0]
+    assert all(np.array_equal(_np(c), ref) for c, _, _ in outs)
+    assert L.lib.fp8_check_async_error() == L.FP8_OK
+    for w_ in wins:
+        w_.close()
+
+
+def test_grouped_bad_device_offsets_reported():
+    """Grouped GEMM offsets live on the device, so they are validated in the kernel: invalid ones (not
+    multiples of 128) are reported through the fault word at the next grouped call (FP8_EINVAL), without
+    trapping; the context stays usable."""
+    from paper_2507_16099_b200 import _lib as L
+    T, E, N, K = 384, 2, 256, 256
+    x = _dev(synth.tensor_c3("x", (T, K), seed=1), torch.bfloat16)
+    w = _dev(synth.tensor_c3("w", (E * N, K), seed=2), torch.bfloat16)
+    gp = ops.GroupedPlan(T, E, N, K, recipe="rowwise")
+    bad = torch.tensor([0, 100, T], dtype=torch.int32, device="cuda")
+    gp.forward(x, w, bad, gp.new_saved())
+    torch.cuda.synchronize()
+    good = torch.tensor([0, 128, T], dtype=torch.int32, device="cuda")
+    with pytest.raises(fp8t._lib.Fp8Error) as e:
+        gp.forward(x, w, good, gp.new_saved())
+    assert e.value.status == L.FP8_EINVAL
+    Y = gp.forward(x, w, good, gp.new_saved())   # fault cleared: works again
+    torch.cuda.synchronize()
+    assert torch.isfinite(Y.float()).all()
