@@ -78,7 +78,7 @@ CONFIGS = {
 # few minutes) and for the cpu_baseline (one step of ~10-30 s of CPU work): same K and value
 # recipe, fewer rows
 CPU_SAMPLE = dict(M=128, N=2048)
-CPU_BASELINE_M = 512
+CPU_BASELINE_M = 1536   # tokens of the cpu_baseline sample: ~10-30 s of oracle work on the box's host cores
 # the MX oracle spends its time in the element codecs (decode / encode per element), so its sample keeps
 # fewer weight rows for the same few seconds per step
 

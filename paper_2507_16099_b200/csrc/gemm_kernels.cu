@@ -108,14 +108,22 @@ template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bo
   static constexpr int STAGES = ST;
   // MMA N of a tile.  256 everywhere except the MXFP8 N = 192 variant (K-major operands, CTA pair): two
   // 192-column accumulators + the scale-factor columns fit the 512 TMEM columns, 2 x 256 do not
+  // N = 512 (plain FP8 kinds, CTA pair, 1-atom stages): a 256 x 512 tile as two N = 256 MMAs per K step sharing
+  // A, i.e. 25 % fewer L2 -> SMEM operand bytes per flop than 256 x 256 (the measured limit at full clock,
+  // DESIGN.md §5); the two halves own TMEM columns [0, 256) and [256, 512) of one accumulator and are handed
+  // to the epilogue half by half (HALVES).
   static constexpr int BN = BNT;
-  static_assert(BN == 256 || (BN == 192 && MX && CG == 2), "N = 192 tiles: MX CTA-pair kernel only");
-  static constexpr int ACC = MX && BN == 256 ? 1 : 2;
+  static_assert(BN == 256 || (BN == 192 && MX && CG == 2) || (BN == 512 && !MX && !BF && !GRP && CG == 2 && KS == 1),
+                "N = 192 tiles: MX CTA-pair kernel only; N = 512: plain FP8 CTA-pair 1-atom kernel only");
+  static constexpr int HALVES = BN == 512 ? 2 : 1;
+  static constexpr int ACC = (MX && BN == 256) || BN == 512 ? 1 : 2;
+  static constexpr int NACC = ACC * HALVES;                   // tfull / tempty barriers
   static constexpr int EPI_WARPS = E8 || ACC == 1 ? 8 : 4;   // see the epilogue
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   // a stage holds KS 128-byte K atoms (16 KB sub-tiles of 128 rows each)
   static constexpr uint32_t A_STAGE = BM * BK * KS;         // 16 KB x KS
-  static constexpr uint32_t B_STAGE = (256 / CG) * BK * KS;  // 32 KB (CG=1) / 16 KB (CG=2) atom slots, x KS
+  static constexpr uint32_t B_ATOM = ((BN > 256 ? BN : 256) / CG) * BK;   // smem bytes of one B K atom
+  static constexpr uint32_t B_STAGE = B_ATOM * KS;  // 32 KB (CG=1, or N = 512) / 16 KB (CG=2) atom slots, x KS
   static constexpr uint32_t B_TX = (BN / CG) * BK * KS;     // bytes actually loaded (N = 192: 12 KB per atom)
   // MX scale factors per stage: SFA = this CTA's 128 rows x KS atoms; SFB = all 256 N rows x KS
   static constexpr uint32_t SFA_STAGE = MX ? KS * SF_CHUNK : 0;
@@ -129,9 +137,9 @@ template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bo
   // mbarriers (8 B each), in this order from off_bar; the kernel takes every address from these offsets
   static constexpr uint32_t off_full = off_bar;                                 // [STAGES]
   static constexpr uint32_t off_empty = off_full + 8 * STAGES;                  // [STAGES]
-  static constexpr uint32_t off_tfull = off_empty + 8 * STAGES;                 // [ACC]
-  static constexpr uint32_t off_tempty = off_tfull + 8 * ACC;                   // [ACC]
-  static constexpr uint32_t off_sf_bar = off_tempty + 8 * ACC;                  // [STAGES] (MX only)
+  static constexpr uint32_t off_tfull = off_empty + 8 * STAGES;                 // [NACC]
+  static constexpr uint32_t off_tempty = off_tfull + 8 * NACC;                  // [NACC]
+  static constexpr uint32_t off_sf_bar = off_tempty + 8 * NACC;                 // [STAGES] (MX only)
   static constexpr uint32_t off_sf_full = off_sf_bar + (MX ? 8 * STAGES : 0);   // [STAGES] (MX only)
   static constexpr uint32_t off_sched_full = off_sf_full + (MX ? 8 * STAGES : 0);   // [SD]
   static constexpr uint32_t off_sched_empty = off_sched_full + 8 * SD;         // [SD]
@@ -320,9 +328,9 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
       mbar_init(full_bar + 8 * s, CG);
       mbar_init(empty_bar + 8 * s, 1);
     }
-    for (int a = 0; a < L::ACC; ++a) {
+    for (int a = 0; a < L::NACC; ++a) {
       mbar_init(tfull_bar + 8 * a, 1);
-      mbar_init(tempty_bar + 8 * a, CG * L::EPI_WARPS);   // one arrival per epilogue warp
+      mbar_init(tempty_bar + 8 * a, CG * L::EPI_WARPS / L::HALVES);   // one arrival per epilogue warp (of the half)
     }
     if (MX)
       for (int s = 0; s < STAGES; ++s) {
@@ -554,7 +562,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
             const int k0 = BF ? (kb * KS + j) * 64 : (kb * KS + j) * BK;
             const int kmn = BF ? kb * 128 : k0;          // K row of an MN-major box
             const int am = BF ? m0 + 64 * j : m0, bn = BF ? n0 + 64 * j : n0;
-            const uint32_t da = sa_dst + j * 16384, db = sb_dst + j * 16384;
+            const uint32_t da = sa_dst + j * 16384, db = sb_dst + j * L::B_ATOM;
             if (CG == 2) {
               if (GRP) {   // grouped problems: per-group row / K offsets into the shared maps
                 tma_load_2d_2sm(da, tmA, a_mn ? am + ti.a_row0 : k0 + ti.a_k0,
@@ -564,6 +572,8 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
               } else {
                 tma_load_2d_2sm(da, tmA, a_mn ? am : k0, a_mn ? kmn : m0, fb);
                 tma_load_2d_2sm(db, tmB, b_mn ? bn : k0, b_mn ? kmn : n0, fb);
+                // N = 512: this CTA's 256 B rows are one 256-row K-major box or two 128-wide MN-major boxes
+                if (b_mn && L::BN / CG > 128) tma_load_2d_2sm(db + 16384, tmB, bn + 128, kmn, fb);
               }
             } else {
               tma_load_2d(da, tmA, a_mn ? m0 : k0, a_mn ? k0 : m0, fb, 0);
@@ -605,7 +615,10 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
         if (next < num_tiles) nti = locate(next);
         have_next = true;
       };
-      mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
+      // N = 512: the tile's two N = 256 halves are handed over separately -- half 1's columns are awaited
+      // only after half 0's MMAs of the first stage are queued, and half 0 is published to the epilogue
+      // before half 1's MMAs of the last stage -- so each hand-over overlaps the other half's MMAs
+      mbar_wait(tempty_bar + 8 * acc * L::HALVES, acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * L::BN;
       for (int kb = 0; kb < num_kb; ++kb) {
@@ -632,6 +645,21 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
           auto koff = [](int mn, int k) -> uint64_t {
             return mn ? (uint64_t)((BF ? 128 : 256) * k) : (uint64_t)(1024 * (k >> 2) + 2 * (k & 3));
           };
+          if constexpr (L::HALVES == 2) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (h == 1 && kb == 0) {
+                mbar_wait(tempty_bar + 8, acc_phase ^ 1);
+                tc_fence_after();
+              }
+              // half h: this CTA's B rows [128 h, 128 h + 128) (16 KB further in the stage), TMEM columns 256 h..
+              const uint64_t bdh = bdesc + (uint64_t)((16384 * h) >> 4);
+#pragma unroll
+              for (int k = 0; k < BK / 32; ++k)
+                mma_f8f6f4_cg2(d_tmem + 256 * h, adesc + koff(a_mn, k), bdh + koff(b_mn, k), idesc, (kb | k) != 0);
+              if (h == 0 && kb == num_kb - 1) mma_commit_cg2_mc(tfull_bar, 0x3);
+            }
+          } else
 #pragma unroll
           for (int k = 0; k < KS * BK / 32; ++k) {
             if (GRP && kb * KS + (k >> 2) >= ti.katoms) break;   // K-grouped: the group's last atom ends here
@@ -654,7 +682,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
           }
           if (CG == 2) {
             mma_commit_cg2_mc(empty_bar + 8 * stage, 0x3);
-            if (kb == num_kb - 1) mma_commit_cg2_mc(tfull_bar + 8 * acc, 0x3);
+            if (kb == num_kb - 1) mma_commit_cg2_mc(tfull_bar + 8 * (acc * L::HALVES + L::HALVES - 1), 0x3);
           } else {
             mma_commit(empty_bar + 8 * stage);
             if (kb == num_kb - 1) mma_commit(tfull_bar + 8 * acc);
@@ -798,15 +826,41 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
         __syncwarp();
       };
 
-      mbar_wait(tfull_bar + 8 * acc, acc_phase);
+      // this warp's accumulator barrier: per buffer, or per half of the N = 512 accumulator
+      const int ab = L::HALVES == 2 ? half : acc;
+      mbar_wait(tfull_bar + 8 * ab, acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * L::BN;
       if (args.debug & 8) {   // timing experiment (results invalid): release the accumulator untouched
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * acc);
-          else mbar_arrive(tempty_bar + 8 * acc);
+          if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * ab);
+          else mbar_arrive(tempty_bar + 8 * ab);
+        }
+      } else if (L::HALVES == 2) {
+        // N = 512: warps of half h drain TMEM columns [256 h, 256 h + 256) = the MMA of B rows 128 h.. of
+        // each CTA: column j < 128 is tile column 128 h + j (CTA 0's rows), j >= 128 is 256 + 128 h + j - 128
+        // (CTA 1's rows).  Chunk c + 1 is read from TMEM while chunk c is scaled and stored.
+        const uint32_t tb = tbase + 256 * half;
+        auto col = [&](int c) { return nb * L::BN + (c < 4 ? 128 * half + 32 * c : 256 + 128 * half + 32 * (c - 4)); };
+        uint32_t ra[32], rb[32];
+        tmem_ld_32x32b_x32(tb, ra);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 8; c += 2) {
+          tmem_ld_32x32b_x32(tb + 32 * (c + 1), rb);
+          process(ra, col(c));
+          tmem_wait_ld();
+          if (c + 2 < 8) tmem_ld_32x32b_x32(tb + 32 * (c + 2), ra);
+          process(rb, col(c + 1));
+          tmem_wait_ld();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * ab);
+          else mbar_arrive(tempty_bar + 8 * ab);
         }
       } else if (EPIW == 8) {
         constexpr int HC = L::BN / 64;   // 32-column chunks per half
@@ -1126,6 +1180,13 @@ cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st) {
     return launch_t<true, 2, 3, 2>(ps, n, st);
   }
   if (cg == 1) return launch_t<false, 1, 4, 1>(ps, n, st);
+  // 256 x 512 tiles (knob gemm_n512) when every problem's N is a multiple of 512: 4 stages x 1 atom
+  // (48 KB per CTA per stage: A 16 KB + B 32 KB)
+  if (knob(KNOB_GEMM_N512) == 1 && knob(KNOB_GEMM_STAGES) == 3) {
+    bool ok = true;
+    for (int i = 0; i < n; ++i) ok = ok && ps[i].N % 512 == 0 && !ps[i].grouped;
+    if (ok) return launch_t<false, 2, 4, 1, false, false, false, 512>(ps, n, st);
+  }
   // default: 3 stages x 2 K atoms (64 KB per CTA per stage, 8 MMAs per barrier round trip);
   // knob gemm_stages = 6 selects 6 x 1 atom (4 MMAs per round trip) for comparison
   const int stages = knob(KNOB_GEMM_STAGES);

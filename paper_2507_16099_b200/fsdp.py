@@ -109,6 +109,64 @@ class Comm:
             self._h = ctypes.c_void_p()
 
 
+class GatherPrefetcher:
+    """FSDP2-style forward prefetch of the FP8 weight gathers of a chain of linears.
+
+    Layer i's gather (amax -> all-reduce MAX -> cast into slot -> all-gather, `Comm.allgather_fp8`, or the
+    MXFP8 gather with mxfp8=True) is issued on a side stream and ordered with CUDA events, so gathering the
+    next layer's weight overlaps the current layer's GEMMs on the compute stream:
+
+        pf = GatherPrefetcher(comm, [w0_shard, w1_shard, ...])
+        pf.prefetch(0)
+        for i in range(L):
+            if i + 1 < L: pf.prefetch(i + 1)      # side stream, overlaps layer i
+            w_fp8 = pf.get(i)                    # compute stream waits for layer i's gather only
+            y = plans[i].forward(x, None, saved[i], w_fp8=w_fp8)
+
+    Each layer owns its gathered buffer (the backward reads the same FP8 weight, no re-gather).  A prefetch
+    first makes the side stream wait for everything already enqueued on the compute stream -- the shard's
+    last update (optimizer step) and every earlier read of the layer's buffer (the previous step's
+    backward) -- so only work enqueued after the prefetch call (the current layer's GEMMs) overlaps it.
+    Marshalling and stream ordering only: every byte is produced by the library's gather kernels / NCCL."""
+
+    def __init__(self, comm, shards, fmt="e4m3", mxfp8=False, stream=None):
+        self.comm, self.shards, self.fmt, self.mxfp8 = comm, list(shards), fmt, mxfp8
+        dev = self.shards[0].device
+        self.side = stream if stream is not None else torch.cuda.Stream(device=dev)
+        self.out = [None] * len(self.shards)
+        self.ready = [None] * len(self.shards)
+
+    def prefetch(self, i):
+        cur = torch.cuda.current_stream(self.shards[i].device)
+        self.side.wait_stream(cur)
+        with torch.cuda.stream(self.side):
+            if self.mxfp8:
+                self.out[i] = self.comm.allgather_mx(self.shards[i], self.fmt, out=self.out[i], stream=self.side)
+            else:
+                prev = self.out[i]
+                self.out[i] = self.comm.allgather_fp8(self.shards[i], self.fmt, out=prev[0] if prev else None,
+                                                      scale=prev[1] if prev else None,
+                                                      amax=prev[2] if prev else None, stream=self.side)
+            ev = torch.cuda.Event()
+            ev.record(self.side)
+            self.ready[i] = ev
+
+    def get(self, i):
+        """The gathered weight of layer i, in the form LinearPlan(w_fp8=...) takes; the compute stream waits
+        for its gather.  Gathers first (on the side stream) if it was not prefetched."""
+        if self.ready[i] is None:
+            self.prefetch(i)
+        cur = torch.cuda.current_stream(self.shards[i].device)
+        cur.wait_event(self.ready[i])
+        self.ready[i] = None
+        o = self.out[i]
+        # the gathered tensors are consumed on the compute stream: tell the caching allocator
+        for t in (o.values() if self.mxfp8 else o):
+            if t is not None:
+                t.record_stream(cur)
+        return o if self.mxfp8 else (o[0], o[1])
+
+
 def _tp_cfg(fmt, out_dtype, fmt_grad="e5m2"):
     return L.LinearCfg(L.RECIPE_TENSORWISE, FORMATS[fmt], FORMATS[fmt_grad], L.MX_FLOOR,
                        L.DT_F32 if out_dtype == torch.float32 else L.DT_BF16)

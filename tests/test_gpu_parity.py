@@ -1350,3 +1350,110 @@ def test_grouped_bad_device_offsets_reported():
     Y = gp.forward(x, w, good, gp.new_saved())   # fault cleared: works again
     torch.cuda.synchronize()
     assert torch.isfinite(Y.float()).all()
+
+
+# ----------------------------------------------------------------------------- 256 x 512 tiles (knob gemm_n512)
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 384), (640, 1024, 640), (272, 1536, 256), (1024, 2048, 1024)])
+@pytest.mark.parametrize("majors", ["KK", "KM", "MM", "MK"])
+@pytest.mark.parametrize("sched", [1, 0], ids=["dynamic", "roundrobin"])
+def test_gemm_n512_integer_grid_exact(M, N, K, majors, sched, knob):
+    """The 256 x 512 CTA-pair tile (two N = 256 MMAs sharing A, one 512-column accumulator handed to the
+    epilogue half by half, permuted column mapping, 256-row K-major / two 128-wide MN-major B boxes):
+    integer-grid operands give exact fp32 sums, so the result must equal X W^T bit for bit, for every
+    operand-major combination, ragged M, several tiles per CTA pair, K-serpentine tiles included."""
+    knob("gemm_n512", 1)
+    knob("gemm_sched", sched)
+    a, b = _grid_operands(M, N, K, seed=7)
+    qa, sa, _ = fp8.cast_tensorwise(a, E4M3)
+    qb, sb, _ = fp8.cast_tensorwise(b, E4M3)
+    want = a.astype(np.float64) @ b.astype(np.float64).T
+    a_mn, b_mn = majors[0] == "M", majors[1] == "M"
+    A = torch.from_numpy(np.ascontiguousarray(qa.T if a_mn else qa)).cuda()
+    B = torch.from_numpy(np.ascontiguousarray(qb.T if b_mn else qb)).cuda()
+    D = ops.gemm(A, "e4m3", torch.tensor([sa], device="cuda"), B, "e4m3", torch.tensor([sb], device="cuda"),
+                 "tensor", out_dtype=torch.float32, a_mn=a_mn, b_mn=b_mn)
+    assert np.array_equal(_np(D).astype(np.float64), want)
+
+
+@pytest.mark.parametrize("recipe", ["tensorwise", "rowwise"])
+def test_linear_n512_matches_default_tiles(recipe, knob):
+    """A Float8Linear whose N and K are multiples of 512 runs all three GEMMs (forward; dX + dW in one
+    launch) on 256 x 512 tiles: within tolerance of the oracle, and the FP8 operands are the same bytes."""
+    M, N, K = 768, 1024, 1536
+    x, w, dy = synth.linear_inputs("c3" if recipe == "rowwise" else "c2", M, N, K, seed=13)
+    y, yb, _ = olin.forward(x, w, recipe)
+    dx, dxb, dw, dwb, _ = olin.backward(x, w, dy, recipe)
+    X, W, G = _dev(x, torch.bfloat16), _dev(w, torch.bfloat16), _dev(dy, torch.bfloat16)
+    outs = []
+    for n512 in (0, 1):
+        knob("gemm_n512", n512)
+        plan = ops.LinearPlan(M, N, K, recipe=recipe, out_dtype=torch.float32)
+        saved = plan.new_saved()
+        Y = plan.forward(X, W, saved)
+        DX, DW = plan.backward(G, saved)
+        torch.cuda.synchronize()
+        _tol_check(_np(Y).astype(np.float64), y, yb)
+        _tol_check(_np(DX).astype(np.float64), dx, dxb)
+        _tol_check(_np(DW).astype(np.float64), dw, dwb)
+        outs.append((Y, DX, DW))
+    for a_, b_ in zip(outs[0], outs[1]):   # same operands, different fp32 summation trees: close, not equal
+        assert torch.allclose(a_, b_, rtol=1e-5, atol=1e-6 * float(a_.abs().max()))
+
+
+def test_fsdp_gather_prefetch_chain_bit_identical():
+    """GatherPrefetcher (FSDP2 forward prefetch): a 3-layer chain whose next layer's FP8 weight gather runs
+    on a side stream while the current layer's GEMMs run gives bit-identical activations and gradients to
+    gathering each weight right before its layer, for two steps with a weight update in between (the
+    prefetch of step 2 must see the updated shards and must not overwrite a buffer step 1's backward still
+    reads).  One NCCL rank (multi-rank data movement needs >= 2 GPUs)."""
+    import os
+    import torch.distributed as dist
+    from paper_2507_16099_b200.fsdp import Comm, GatherPrefetcher
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29543"
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = Comm()
+        M, dims = 512, [512, 768, 640, 512]
+        X0 = _dev(synth.tensor_c2("x", (M, dims[0]), seed=21), torch.bfloat16)
+        shards = [_dev(synth.tensor_c2("w", (dims[i + 1], dims[i]), seed=22 + i), torch.bfloat16) for i in range(3)]
+        G = _dev(synth.tensor_c2("dy", (M, dims[-1]), seed=25), torch.bfloat16)
+        plans = [ops.LinearPlan(M, dims[i + 1], dims[i], recipe="tensorwise") for i in range(3)]
+
+        def run(prefetch, shards_):
+            pf = GatherPrefetcher(comm, shards_)
+            saved = [p.new_saved() for p in plans]
+            outs = []
+            for step in range(2):
+                if step == 1:   # "optimizer step": update the shards in place on the compute stream
+                    for w_ in shards_:
+                        w_.mul_(0.5)
+                x = X0
+                wf = []
+                if prefetch:
+                    pf.prefetch(0)
+                acts = []
+                for i in range(3):
+                    if prefetch and i + 1 < 3:
+                        pf.prefetch(i + 1)
+                    wf.append(pf.get(i) if prefetch else comm.allgather_fp8(shards_[i], "e4m3")[:2])
+                    acts.append(x)
+                    x = plans[i].forward(x, None, saved[i], w_fp8=wf[i])
+                g = G
+                grads = []
+                for i in (2, 1, 0):
+                    g, dw = plans[i].backward(g, saved[i], w_fp8=wf[i])
+                    grads.append(dw.clone())
+                outs.append((x.clone(), g.clone(), *grads))
+            torch.cuda.synchronize()
+            return outs
+
+        a = run(False, [s.clone() for s in shards])
+        b = run(True, [s.clone() for s in shards])
+        for sa, sb in zip(a, b):
+            for ta, tb in zip(sa, sb):
+                assert torch.equal(ta, tb)
+        comm.close()
+    finally:
+        dist.destroy_process_group()

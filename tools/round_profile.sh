@@ -1,0 +1,15 @@
+# Round profile artefacts (run under gpurun; summarise here with tools/ncu_summary.py / ncu_traffic.py):
+#   launch lists of the headline (c4) and c2 steps, ncu --set full of their GEMM launches and cast kernels.
+# usage: bash tools/round_profile.sh <tag>
+T=${1:-r02}
+B="python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-bf16 --no-cpu-baseline --no-digest"
+for c in c4 c2; do
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches_$c.csv \
+    $B --config $c > gpurun_out/${T}_launches_$c.log 2>&1
+done
+B1="python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-bf16 --no-cpu-baseline --no-digest"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:fp8_gemm -s 6 -c 2 -o gpurun_out/${T}_gemm_c4 $B1 --config c4 > gpurun_out/${T}_gemm_c4.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:fp8_gemm -s 6 -c 2 -o gpurun_out/${T}_gemm_c2 $B1 --config c2 > gpurun_out/${T}_gemm_c2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:mx_cast -s 9 -c 3 -o gpurun_out/${T}_casts_c4 $B1 --config c4 > gpurun_out/${T}_casts_c4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"amax|cast" -s 12 -c 4 -o gpurun_out/${T}_casts_c2 $B1 --config c2 > gpurun_out/${T}_casts_c2.log 2>&1
+ls -la gpurun_out/${T}_*
