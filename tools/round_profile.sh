@@ -4,7 +4,7 @@
 T=${1:-r02}
 B="python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-bf16 --no-cpu-baseline --no-digest"
 for c in c4 c2; do
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches_$c.csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:fp8t:: --csv --log-file gpurun_out/${T}_launches_$c.csv \
     $B --config $c > gpurun_out/${T}_launches_$c.log 2>&1
 done
 B1="python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-bf16 --no-cpu-baseline --no-digest"
