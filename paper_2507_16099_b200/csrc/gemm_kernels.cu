@@ -63,6 +63,7 @@ struct Prob {
   const float* sa; const float* sb;
   void* D; int64_t ldd;
   int out_f32, row_scales;
+  int d_tma;          // N = 512 bf16 epilogue: D written by TMA stores through the map in the tSA slot
   int a_mn, b_mn;     // operand majors (MN-major: TMA boxes 128 MN x 128 K, K step 4 KB)
   uint32_t* out_amax; // optional: atomicMax of |D| bit patterns (amax of the stored output values)
   int raster;         // tile raster of this problem (see tile_coords / choose_raster)
@@ -132,8 +133,11 @@ template <bool MX, int CG, int ST, int KS, bool BF = false, bool GRP = false, bo
   static constexpr uint32_t off_b = off_a + STAGES * A_STAGE;
   static constexpr uint32_t off_sfa = off_b + STAGES * B_STAGE;
   static constexpr uint32_t off_sfb = off_sfa + STAGES * SFA_STAGE;
-  static constexpr uint32_t off_epi = off_sfb + STAGES * SFB_STAGE;   // 2 KB bf16 staging per epilogue warp
-  static constexpr uint32_t off_bar = off_epi + EPI_WARPS * 2048;
+  // per epilogue warp: 2 KB bf16 staging for the row-segment stores; N = 512: two 2 KB output chunks (32 rows
+  // x 32 bf16 columns, SWIZZLE_64B) written by TMA stores, double-buffered
+  static constexpr uint32_t EPI_BYTES = BN == 512 ? 4096 : 2048;
+  static constexpr uint32_t off_epi = off_sfb + STAGES * SFB_STAGE;
+  static constexpr uint32_t off_bar = off_epi + EPI_WARPS * EPI_BYTES;
   // mbarriers (8 B each), in this order from off_bar; the kernel takes every address from these offsets
   static constexpr uint32_t off_full = off_bar;                                 // [STAGES]
   static constexpr uint32_t off_empty = off_full + 8 * STAGES;                  // [STAGES]
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
     }
     for (int a = 0; a < L::NACC; ++a) {
       mbar_init(tfull_bar + 8 * a, 1);
-      mbar_init(tempty_bar + 8 * a, CG * L::EPI_WARPS / L::HALVES);   // one arrival per epilogue warp (of the half)
+      mbar_init(tempty_bar + 8 * a, CG * L::EPI_WARPS);   // one arrival per epilogue warp
     }
     if (MX)
       for (int s = 0; s < STAGES; ++s) {
@@ -740,7 +744,8 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
     int acc = 0;
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(tempty_bar, 0) : tempty_bar;
-    uint8_t* epi = gbase + L::off_epi + (warp - 4) * 2048;   // this warp's bf16 staging slot
+    uint8_t* epi = gbase + L::off_epi + (warp - 4) * L::EPI_BYTES;   // this warp's bf16 staging slot
+    const uint32_t epi_s = base + L::off_epi + (warp - 4) * L::EPI_BYTES;
     for (int sk = 0;;) {
       const int tile = seq_get(sk);
       if (tile >= num_tiles) break;
@@ -827,40 +832,98 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
       };
 
       // this warp's accumulator barrier: per buffer, or per half of the N = 512 accumulator
-      const int ab = L::HALVES == 2 ? half : acc;
-      mbar_wait(tfull_bar + 8 * ab, acc_phase);
-      tc_fence_after();
+      // (N = 512: the halves are awaited one by one below)
+      if (L::HALVES == 1) {
+        mbar_wait(tfull_bar + 8 * acc, acc_phase);
+        tc_fence_after();
+      }
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * L::BN;
       if (args.debug & 8) {   // timing experiment (results invalid): release the accumulator untouched
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * ab);
-          else mbar_arrive(tempty_bar + 8 * ab);
+        for (int h = 0; h < L::HALVES; ++h) {
+          const int ab = L::HALVES == 2 ? h : acc;
+          if (L::HALVES == 2) mbar_wait(tfull_bar + 8 * ab, acc_phase);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * ab);
+            else mbar_arrive(tempty_bar + 8 * ab);
+          }
         }
       } else if (L::HALVES == 2) {
-        // N = 512: warps of half h drain TMEM columns [256 h, 256 h + 256) = the MMA of B rows 128 h.. of
-        // each CTA: column j < 128 is tile column 128 h + j (CTA 0's rows), j >= 128 is 256 + 128 h + j - 128
-        // (CTA 1's rows).  Chunk c + 1 is read from TMEM while chunk c is scaled and stored.
-        const uint32_t tb = tbase + 256 * half;
-        auto col = [&](int c) { return nb * L::BN + (c < 4 ? 128 * half + 32 * c : 256 + 128 * half + 32 * (c - 4)); };
-        uint32_t ra[32], rb[32];
-        tmem_ld_32x32b_x32(tb, ra);
-        tmem_wait_ld();
+        // N = 512: the accumulator's halves h = 0, 1 (TMEM columns 256 h.., the MMA of B rows 128 h.. of each
+        // CTA) are drained in turn by all 8 warps: warp quarter `half` takes columns [128 half, +128) of the
+        // half, i.e. tile columns 128 h.. (half 0, CTA 0's B rows) or 256 + 128 h.. (half 1, CTA 1's rows).
+        // bf16 outputs are scaled into one of this warp's two 2 KB smem chunks and written by a TMA store each,
+        // so the warp never waits on global writes (which compete with the operand loads for L2) before it
+        // releases TMEM; a chunk buffer is reused once its previous store has been read out of smem.
+        const CUtensorMap* dmap = ti.pi ? &tSA1 : &tSA0;
+        const bool tma_out = P.d_tma;
+        const int row_base = mb * BM * CG + (int)crank * BM + q * 32;
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(tfull_bar + 8 * h, acc_phase);
+          tc_fence_after();
+          const uint32_t tb = tbase + 256 * h + 128 * half;
+          const int col0 = nb * L::BN + (half == 0 ? 128 * h : 256 + 128 * h);
+          // scale + convert 32 columns into chunk buffer c & 1 (SWIZZLE_64B rows of 64 B) and store it by TMA
+          auto stage = [&](const uint32_t (&r)[32], int c) {
+            if (!tma_out) {
+              process(r, col0 + 32 * c);
+              return;
+            }
+            float v[32];
+            if (row_scales) {
+              const float rcol = __frcp_rn(sb[col0 + 32 * c + (int)lane]);
 #pragma unroll
-        for (int c = 0; c < 8; c += 2) {
-          tmem_ld_32x32b_x32(tb + 32 * (c + 1), rb);
-          process(ra, col(c));
+              for (int j = 0; j < 32; ++j)
+                v[j] = __fmul_rn(__fmul_rn(__uint_as_float(r[j]), rs), __shfl_sync(0xffffffffu, rcol, j));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__uint_as_float(r[j]), rs);
+            }
+            uint32_t pk[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              __nv_bfloat162 hv = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+              pk[j] = *reinterpret_cast<uint32_t*>(&hv);
+            }
+            if (P.out_amax && rvalid) {
+              uint32_t m2 = 0;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) m2 = __vmaxu2(m2, pk[j] & 0x7FFF7FFFu);
+              dmax = max(dmax, max(m2 & 0xFFFFu, m2 >> 16) << 16);
+            }
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");   // buffer c & 1 free
+            __syncwarp();
+            uint8_t* buf = epi + (c & 1) * 2048 + lane * 64;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              *reinterpret_cast<uint4*>(buf + ((u ^ (int)((lane >> 1) & 3)) * 16)) =
+                  make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(dmap, epi_s + (c & 1) * 2048, col0 + 32 * c, (int)(ti.d_row0 + row_base));
+              bulk_commit_group();
+            }
+          };
+          uint32_t ra[32], rb[32];
+          tmem_ld_32x32b_x32(tb, ra);
           tmem_wait_ld();
-          if (c + 2 < 8) tmem_ld_32x32b_x32(tb + 32 * (c + 2), ra);
-          process(rb, col(c + 1));
-          tmem_wait_ld();
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * ab);
-          else mbar_arrive(tempty_bar + 8 * ab);
+#pragma unroll
+          for (int c = 0; c < 4; c += 2) {
+            tmem_ld_32x32b_x32(tb + 32 * (c + 1), rb);
+            stage(ra, c);
+            tmem_wait_ld();
+            if (c + 2 < 4) tmem_ld_32x32b_x32(tb + 32 * (c + 2), ra);
+            stage(rb, c + 1);
+            tmem_wait_ld();
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * h);
+            else mbar_arrive(tempty_bar + 8 * h);
+          }
         }
       } else if (EPIW == 8) {
         constexpr int HC = L::BN / 64;   // 32-column chunks per half
@@ -908,6 +971,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
       }
       if (++acc == L::ACC) { acc = 0; acc_phase ^= 1; }
     }
+    if (L::HALVES == 2 && lane == 0) bulk_wait_all0();   // this warp's TMA stores are complete
   }
 
   tc_fence_before();
@@ -987,8 +1051,20 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   if (MX) {
     if (!make_sf_map(&maps[2], p.sa, p.M, p.K, KS) || !make_sf_map(&maps[3], p.sb, p.N, p.K, KS)) return false;
   } else {
-    maps[2] = maps[0];   // unused by the plain FP8 kinds
+    maps[2] = maps[0];   // unused by the plain FP8 kinds (N = 512: the D map for the TMA-store epilogue)
     maps[3] = maps[1];
+  }
+  const bool d_tma = BNT == 512 && !p.out_f32 && !p.rs_bufs && !p.grouped;
+  if (d_tma) {   // D bf16 [M, N] (row stride ldd), boxes of 32 rows x 32 columns, SWIZZLE_64B
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)p.N, (cuuint64_t)p.M};
+    cuuint64_t strides[1] = {(cuuint64_t)p.ldd * 2};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc(&maps[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p.D, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
   }
   P = Prob{};
   P.M = (int)p.M; P.N = (int)p.N; P.K = (int)p.K;
@@ -1009,6 +1085,7 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
     P.row_scales = p.scale_mode == 1;
   }
   P.D = p.D; P.ldd = p.ldd; P.out_f32 = p.out_f32;
+  P.d_tma = d_tma ? 1 : 0;
   P.out_amax = p.out_amax;
   P.grouped = p.grouped;
   P.G = p.G;
@@ -1181,7 +1258,7 @@ cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st) {
   }
   if (cg == 1) return launch_t<false, 1, 4, 1>(ps, n, st);
   // 256 x 512 tiles (knob gemm_n512) when every problem's N is a multiple of 512: 4 stages x 1 atom
-  // (48 KB per CTA per stage: A 16 KB + B 32 KB)
+  // (48 KB per CTA per stage: A 16 KB + B 32 KB) + 4 KB of TMA-store output chunks per epilogue warp
   if (knob(KNOB_GEMM_N512) == 1 && knob(KNOB_GEMM_STAGES) == 3) {
     bool ok = true;
     for (int i = 0; i < n; ++i) ok = ok && ps[i].N % 512 == 0 && !ps[i].grouped;

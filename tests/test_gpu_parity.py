@@ -1357,7 +1357,8 @@ def test_grouped_bad_device_offsets_reported():
 @pytest.mark.parametrize("M,N,K", [(256, 512, 384), (640, 1024, 640), (272, 1536, 256), (1024, 2048, 1024)])
 @pytest.mark.parametrize("majors", ["KK", "KM", "MM", "MK"])
 @pytest.mark.parametrize("sched", [1, 0], ids=["dynamic", "roundrobin"])
-def test_gemm_n512_integer_grid_exact(M, N, K, majors, sched, knob):
+@pytest.mark.parametrize("out", [torch.float32, torch.bfloat16], ids=["f32_direct", "bf16_tma_store"])
+def test_gemm_n512_integer_grid_exact(M, N, K, majors, sched, out, knob):
     """The 256 x 512 CTA-pair tile (two N = 256 MMAs sharing A, one 512-column accumulator handed to the
     epilogue half by half, permuted column mapping, 256-row K-major / two 128-wide MN-major B boxes):
     integer-grid operands give exact fp32 sums, so the result must equal X W^T bit for bit, for every
@@ -1372,12 +1373,15 @@ def test_gemm_n512_integer_grid_exact(M, N, K, majors, sched, knob):
     A = torch.from_numpy(np.ascontiguousarray(qa.T if a_mn else qa)).cuda()
     B = torch.from_numpy(np.ascontiguousarray(qb.T if b_mn else qb)).cuda()
     D = ops.gemm(A, "e4m3", torch.tensor([sa], device="cuda"), B, "e4m3", torch.tensor([sb], device="cuda"),
-                 "tensor", out_dtype=torch.float32, a_mn=a_mn, b_mn=b_mn)
-    assert np.array_equal(_np(D).astype(np.float64), want)
+                 "tensor", out_dtype=out, a_mn=a_mn, b_mn=b_mn)
+    exp = want if out == torch.float32 else \
+        torch.from_numpy(want.astype(np.float32)).to(torch.bfloat16).float().numpy().astype(np.float64)
+    assert np.array_equal(_np(D.float()).astype(np.float64), exp)
 
 
+@pytest.mark.parametrize("out", [torch.float32, torch.bfloat16], ids=["f32", "bf16"])
 @pytest.mark.parametrize("recipe", ["tensorwise", "rowwise"])
-def test_linear_n512_matches_default_tiles(recipe, knob):
+def test_linear_n512_matches_default_tiles(recipe, out, knob):
     """A Float8Linear whose N and K are multiples of 512 runs all three GEMMs (forward; dX + dW in one
     launch) on 256 x 512 tiles: within tolerance of the oracle, and the FP8 operands are the same bytes."""
     M, N, K = 768, 1024, 1536
@@ -1388,17 +1392,20 @@ def test_linear_n512_matches_default_tiles(recipe, knob):
     outs = []
     for n512 in (0, 1):
         knob("gemm_n512", n512)
-        plan = ops.LinearPlan(M, N, K, recipe=recipe, out_dtype=torch.float32)
+        plan = ops.LinearPlan(M, N, K, recipe=recipe, out_dtype=out)
         saved = plan.new_saved()
-        Y = plan.forward(X, W, saved)
+        y_amax = torch.empty(1, device="cuda")
+        Y = plan.forward(X, W, saved, y_amax=y_amax)
         DX, DW = plan.backward(G, saved)
         torch.cuda.synchronize()
-        _tol_check(_np(Y).astype(np.float64), y, yb)
-        _tol_check(_np(DX).astype(np.float64), dx, dxb)
-        _tol_check(_np(DW).astype(np.float64), dw, dwb)
-        outs.append((Y, DX, DW))
+        _tol_check(_np(Y.float()).astype(np.float64), y, yb)
+        _tol_check(_np(DX.float()).astype(np.float64), dx, dxb)
+        _tol_check(_np(DW.float()).astype(np.float64), dw, dwb)
+        assert y_amax.item() == Y.float().abs().max().item()   # epilogue amax of the stored outputs
+        outs.append((Y.float(), DX.float(), DW.float()))
     for a_, b_ in zip(outs[0], outs[1]):   # same operands, different fp32 summation trees: close, not equal
-        assert torch.allclose(a_, b_, rtol=1e-5, atol=1e-6 * float(a_.abs().max()))
+        rt = 1e-5 if out == torch.float32 else 2 ** -7
+        assert torch.allclose(a_, b_, rtol=rt, atol=rt * float(a_.abs().max()))
 
 
 def test_fsdp_gather_prefetch_chain_bit_identical():

@@ -19,6 +19,8 @@ from paper_2507_16099_b200 import ops  # noqa: E402
 SHAPES = [tuple(int(v) for v in s.split("x")) for s in
           os.environ.get("PROBE_SHAPES", "16384x14336x4096,16384x4096x14336,16384x28672x8192").split(",")]
 MODES = [int(m) for m in os.environ.get("PROBE_MODES", "0,1,256,257").split(",")]
+KNOBS = [kv.split("=") for kv in os.environ.get("PROBE_KNOBS", "").split(",") if kv]   # e.g. gemm_n512=1
+KINDS = os.environ.get("PROBE_KINDS", "fp8,mx").split(",")
 
 
 class Clock:
@@ -72,8 +74,10 @@ def main():
         sfb = torch.full((N * K // 32,), 127, dtype=torch.uint8, device="cuda")
         flops = 2.0 * M * N * K
         iters = max(5, int(2e13 / flops))
-        for kind in ("fp8", "mx"):
+        for kind in KINDS:
             for mode in MODES:
+                for k, v in KNOBS:
+                    ops.set_knob(k, int(v))
                 ops.set_knob("gemm_debug", mode)
                 if kind == "fp8":
                     fn = lambda: ops.gemm(A, "e4m3", s, B, "e4m3", s, "tensor")  # noqa: E731
