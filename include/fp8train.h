@@ -524,6 +524,8 @@ uint64_t fp8_launch_count(void);
  *   mx_sf_split (1) | gemm_raster (-1 = per problem) | mx_n192 (0) | gemm_stages (3) |
  *   gemm_epi (0 = by K) | mx_transposed (0; forward and backward of one linear must agree) |
  *   tw_dual (1) | gemm_kserp (1: odd waves of GEMM tiles walk K backwards) |
+ *   gemm_n512 (2 = 256 x 512 tiles for plain FP8 launches whose problems all have N % 512 == 0 and
+ *   K >= 8192; 1 = whenever N % 512 == 0; 0 = never) |
  *   watchdog_ms (30000; 0 = peer waits never give up)
  *   -- defaults in parentheses.
  * A knob changes launches enqueued after the call.  Unknown name or out-of-range value:

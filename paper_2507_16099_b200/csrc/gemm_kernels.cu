@@ -1259,9 +1259,13 @@ cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st) {
   if (cg == 1) return launch_t<false, 1, 4, 1>(ps, n, st);
   // 256 x 512 tiles (knob gemm_n512) when every problem's N is a multiple of 512: 4 stages x 1 atom
   // (48 KB per CTA per stage: A 16 KB + B 32 KB) + 4 KB of TMA-store output chunks per epilogue warp
-  if (knob(KNOB_GEMM_N512) == 1 && knob(KNOB_GEMM_STAGES) == 3) {
+  // knob 1: whenever the shapes allow; 2 (auto): only when every problem also has K >= 8192 -- the single
+  // accumulator's per-tile hand-over costs more than the operand savings on short-K tiles (c3's wq/wk/wv/wo
+  // backward: -5 %), long-K launches gain 1-3 % (round-2 A/B)
+  const int n512 = knob(KNOB_GEMM_N512);
+  if (n512 && knob(KNOB_GEMM_STAGES) == 3) {
     bool ok = true;
-    for (int i = 0; i < n; ++i) ok = ok && ps[i].N % 512 == 0 && !ps[i].grouped;
+    for (int i = 0; i < n; ++i) ok = ok && ps[i].N % 512 == 0 && !ps[i].grouped && (n512 == 1 || ps[i].K >= 8192);
     if (ok) return launch_t<false, 2, 4, 1, false, false, false, 512>(ps, n, st);
   }
   // default: 3 stages x 2 K atoms (64 KB per CTA per stage, 8 MMAs per barrier round trip);

@@ -54,8 +54,20 @@ def main():
     for i in range(n):
         acc[i % per] += durs[i] / steps
     print(f"{name}: {per} launches per step, sum {sum(acc):.3f} ms")
+    # algorithmic bytes / flops per launch (rowwise: fwd amax X+W, fwd cast X+W (read 2 + two 1-B copies),
+    # GEMM, bwd amax dY, bwd cast dY, GEMM (dX + dW))
+    work = []
+    for u in units:
+        N, K = u["N"], u["K"]
+        xw = M * K + N * K
+        work += [("amax X,W", 2 * xw, "B"), ("cast X,W", 4 * xw, "B"), ("gemm fwd", 2 * M * N * K, "F"),
+                 ("amax dY", 2 * M * N, "B"), ("cast dY", 4 * M * N, "B"), ("gemm bwd", 4 * M * N * K, "F")]
     for i in range(per):
-        print(f"  {i:3d} {KIND.get(kinds[i], kinds[i]):10s} {acc[i] * 1e3:9.1f} us")
+        lab, w, kind = work[i] if per == len(work) else ("", 0, "B")
+        rate = (f"{w / (acc[i] * 1e-3) / 1e9:8.0f} GB/s" if kind == "B" else f"{w / (acc[i] * 1e-3) / 1e12:8.0f} TF/s") \
+            if w else ""
+        print(f"  {i:3d} {KIND.get(kinds[i], kinds[i]):10s} {acc[i] * 1e3:9.1f} us  {units[i // 6]['name'] if per == len(work) else '':4s}"
+              f" {lab:9s} {rate}")
 
 
 if __name__ == "__main__":
