@@ -526,6 +526,7 @@ uint64_t fp8_launch_count(void);
  *   tw_dual (1) | gemm_kserp (1: odd waves of GEMM tiles walk K backwards) |
  *   gemm_n512 (2 = 256 x 512 tiles for plain FP8 launches whose problems all have N % 512 == 0 and
  *   K >= 8192; 1 = whenever N % 512 == 0; 0 = never) |
+ *   gemm_l2pf (0 = off; d > 0: the GEMM producer prefetches operand boxes d stages ahead into L2) |
  *   watchdog_ms (30000; 0 = peer waits never give up)
  *   -- defaults in parentheses.
  * A knob changes launches enqueued after the call.  Unknown name or out-of-range value:

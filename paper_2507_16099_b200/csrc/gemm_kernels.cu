@@ -100,6 +100,7 @@ struct GemmArgs {
   int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
   int sf_split;       // MX: scale-factor copies issued by their own warp (see the SF copier)
   int kserp;          // K-serpentine: tiles of odd "waves" (tile / pairs) walk their K stages backwards
+  int l2pf;           // L2 prefetch distance of the operand boxes, in stages (0 = off)
   unsigned* fault;    // process fault word (async-TP watchdog, bad group offsets); may be null
   unsigned long long watchdog_ns;
   unsigned* sched;    // dynamic tile scheduler slot (g_sched[i]); null: static round robin
@@ -515,6 +516,18 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
       }
       for (int kbi = 0; kbi < num_kb; ++kbi) {
         const int kb = krev ? num_kb - 1 - kbi : kbi;
+        // knob gemm_l2pf = d > 0: before waiting for a free stage, ask L2 for the operand boxes d stages
+        // ahead, so a stage's TMA load finds its data in L2 (the operand fetch is latency-bound, §5)
+        if (!GRP && !BF && args.l2pf && lane == 0 && kbi + args.l2pf < num_kb && !(args.debug & 256)) {
+          const int kp = kbi + args.l2pf, kbp = krev ? num_kb - 1 - kp : kp;
+#pragma unroll
+          for (int j = 0; j < KS; ++j) {
+            const int k0 = (kbp * KS + j) * BK;
+            tma_prefetch_l2_2d(tmA, a_mn ? m0 : k0, a_mn ? k0 : m0);
+            tma_prefetch_l2_2d(tmB, b_mn ? n0 : k0, b_mn ? k0 : n0);
+            if (b_mn && L::BN / CG > 128) tma_prefetch_l2_2d(tmB, n0 + 128, k0);
+          }
+        }
         mbar_wait(empty_bar + 8 * stage, phase ^ 1);
         if (lane == 0) {
           // MX: E8M0 tiles first, on their own barrier: they land long before the operands, so the SF
@@ -1188,6 +1201,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     }
     a.sf_split = knob(KNOB_MX_SF_SPLIT);
     a.kserp = knob(KNOB_GEMM_KSERP);
+    a.l2pf = knob(KNOB_GEMM_L2PF);
     bool need_fault = GRP;
     for (int i = 0; i < n; ++i) need_fault = need_fault || ps[i].chunk_done != nullptr;
     if (need_fault) {

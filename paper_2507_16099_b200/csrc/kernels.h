@@ -31,7 +31,8 @@ enum Knob {
   KNOB_MX_TRANSPOSED,       // 1: MX dim1 copies written transposed, read K-major (fwd and bwd must agree)
   KNOB_TW_DUAL,             // 1: tensorwise forward X/W amax and cast by one launch each; 0: four launches
   KNOB_GEMM_KSERP,          // 1: odd waves of GEMM tiles walk K backwards (L2 reuse across waves); 0: all forward
-  KNOB_GEMM_N512,           // 1: plain FP8 GEMMs with every N % 512 == 0 use 256 x 512 CTA-pair tiles
+  KNOB_GEMM_N512,
+  KNOB_GEMM_L2PF,           // >0: the GEMM producer prefetches operand boxes this many stages ahead into L2           // 1: plain FP8 GEMMs with every N % 512 == 0 use 256 x 512 CTA-pair tiles
   KNOB_WATCHDOG_MS,         // peer waits (P2P gather, fused reduce-scatter, async-TP) give up after this many ms
                             // and report FP8_ECUDA at the next call; 0 = wait forever
   KNOB_COUNT

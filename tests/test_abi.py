@@ -143,3 +143,29 @@ def test_argument_errors_return_before_any_launch(L):
     t8 = L.Tensor8(A, A, A, A, None, None, L.E4M3, L.GRAN_MX32, 256, 256)
     assert L.lib.fp8_fsdp_allgather_mx(ctypes.c_void_p(A), hp(128, 256), L.MX_FLOOR, ctypes.byref(t8), ws, 1 << 20,
                                        None) == L.FP8_EUNSUPPORTED
+
+
+def test_knobs_host_only(L):
+    """fp8_set_knob / fp8_get_knob / fp8_reset_knobs (host-only, no GPU): every knob the header documents
+    exists with its documented default, out-of-range values and unknown names are rejected without
+    changing anything, and reset restores the defaults.  The library never reads the environment."""
+    import ctypes
+    import re
+    hdr = open(os.path.join(ROOT, "include", "fp8train.h")).read()
+    block = hdr[hdr.index("Kernel-variant knobs"):hdr.index("fp8_status_t fp8_set_knob")]
+    documented = dict((n, int(v)) for n, v in re.findall(r"([a-z0-9_]+) \((-?\d+)", block))
+    assert {"gemm_kserp", "gemm_n512", "watchdog_ms", "tw_dual", "mx_transposed"} <= set(documented)
+    L.lib.fp8_reset_knobs()
+    v = ctypes.c_int(0)
+    for name, default in documented.items():
+        assert L.lib.fp8_get_knob(name.encode(), ctypes.byref(v)) == L.FP8_OK, name
+        assert v.value == default, (name, v.value, default)
+    assert L.lib.fp8_set_knob(b"gemm_n512", 1) == L.FP8_OK
+    assert L.lib.fp8_set_knob(b"gemm_n512", 7) == L.FP8_EINVAL          # out of range: unchanged
+    L.lib.fp8_get_knob(b"gemm_n512", ctypes.byref(v))
+    assert v.value == 1
+    assert L.lib.fp8_set_knob(b"no_such_knob", 1) == L.FP8_EINVAL
+    L.lib.fp8_reset_knobs()
+    L.lib.fp8_get_knob(b"gemm_n512", ctypes.byref(v))
+    assert v.value == documented["gemm_n512"]
+    assert L.lib.fp8_check_async_error() == L.FP8_OK
