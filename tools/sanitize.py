@@ -47,4 +47,21 @@ ops.gemm(A8, "e4m3", one, B8, "e4m3", one, "tensor")
 slots = [ops.cast(W[r * 128:(r + 1) * 128].contiguous(), "e4m3", "mx32_rm", want_q=True, want_qt=True) for r in range(3)]
 ops.mx_scales_unshard(torch.cat([s["scale_t"] for s in slots]), 3, 128, K)
 torch.cuda.synchronize()
+# 256 x 512 GEMM tiles: bf16 output through the TMA-store epilogue, fp32 output through direct stores,
+# a two-problem launch (linear backward with N, K multiples of 512 and K >= 8192 -> the auto policy)
+ops.set_knob("gemm_n512", 1)
+A9 = torch.randint(0, 0x70, (512, 1024), dtype=torch.uint8, device="cuda")
+B9 = torch.randint(0, 0x70, (1024, 1024), dtype=torch.uint8, device="cuda")
+ops.gemm(A9, "e4m3", one, B9, "e4m3", one, "tensor")
+ops.gemm(A9, "e4m3", one, B9, "e4m3", one, "tensor", out_dtype=torch.float32)
+ops.set_knob("gemm_n512", 2)
+X9 = torch.randn((256, 8192), device="cuda").to(torch.bfloat16)
+W9 = (torch.randn((512, 8192), device="cuda") * 0.02).to(torch.bfloat16)
+G9 = (torch.randn((256, 512), device="cuda") * 1e-3).to(torch.bfloat16)
+p9 = ops.LinearPlan(256, 512, 8192, recipe="tensorwise")
+s9 = p9.new_saved()
+p9.forward(X9, W9, s9)
+p9.backward(G9, s9)
+ops.reset_knobs()
+torch.cuda.synchronize()
 print("ok")
