@@ -55,27 +55,35 @@ static int knob_index(const char* name) {
 
 // ---- asynchronous device faults ----
 fp8_status_t fail(fp8_status_t st, const char* fmt, ...);
-static std::once_flag g_fault_once;
+static std::mutex g_fault_mu;
+static std::atomic<unsigned*> g_fault_dev{nullptr};
 static volatile unsigned* g_fault_host = nullptr;
-static unsigned* g_fault_dev = nullptr;
-unsigned* fault_word() {
-  std::call_once(g_fault_once, [] {
-    void* h = nullptr;
-    if (cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
-      cudaGetLastError();
-      return;
-    }
-    std::memset(h, 0, 64);
-    void* d = nullptr;
-    if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) {
-      cudaGetLastError();
-      cudaFreeHost(h);
-      return;
-    }
-    g_fault_host = static_cast<volatile unsigned*>(h);
-    g_fault_dev = static_cast<unsigned*>(d);
-  });
-  return g_fault_dev;
+static bool g_fault_tried = false;
+unsigned* fault_word(cudaStream_t st) {
+  unsigned* d = g_fault_dev.load(std::memory_order_acquire);
+  if (d) return d;
+  // allocate lazily, but never while `st` is being captured into a CUDA graph (cudaHostAlloc is not a
+  // stream operation and would invalidate the capture): such a launch runs without fault reporting
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (st && (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)) return nullptr;
+  std::lock_guard<std::mutex> lk(g_fault_mu);
+  if (g_fault_tried) return g_fault_dev.load();
+  g_fault_tried = true;
+  void* h = nullptr;
+  if (cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::memset(h, 0, 64);
+  void* dp = nullptr;
+  if (cudaHostGetDevicePointer(&dp, h, 0) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFreeHost(h);
+    return nullptr;
+  }
+  g_fault_host = static_cast<volatile unsigned*>(h);
+  g_fault_dev.store(static_cast<unsigned*>(dp), std::memory_order_release);
+  return static_cast<unsigned*>(dp);
 }
 unsigned long long watchdog_ns() { return (unsigned long long)knob(KNOB_WATCHDOG_MS) * 1000000ull; }
 fp8_status_t check_fault() {

@@ -1205,7 +1205,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     bool need_fault = GRP;
     for (int i = 0; i < n; ++i) need_fault = need_fault || ps[i].chunk_done != nullptr;
     if (need_fault) {
-      a.fault = fault_word();
+      a.fault = fault_word(st);
       a.watchdog_ns = watchdog_ns();
     }
     // raster per problem (choose_raster); knob gemm_raster >= 0 overrides for every problem

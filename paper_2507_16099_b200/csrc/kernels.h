@@ -55,7 +55,7 @@ __host__ __device__ constexpr unsigned fault_pack(unsigned code, unsigned peer, 
 }
 // Device-visible pointer to the fault word (nullptr if the pinned allocation failed: then the kernels
 // fall back to waiting without a watchdog); watchdog timeout in ns (knob watchdog_ms; 0 = none).
-unsigned* fault_word();
+unsigned* fault_word(cudaStream_t st = nullptr);   // st: not allocated while st is capturing
 unsigned long long watchdog_ns();
 
 // Multiprocessor count of the current device (cached per device).

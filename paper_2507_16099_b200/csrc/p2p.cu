@@ -342,7 +342,7 @@ fp8_status_t phase_signal(fp8_p2p_t win, const fp8_hp_t& w, const float* amax_in
 }
 fp8_status_t phase_wait_scale(fp8_p2p_t win, fp8_format_t fmt, float* scale_out, float* amax_out, cudaStream_t st) {
   LaunchScope ls(K_SYNC, st);
-  unsigned* f = fault_word();
+  unsigned* f = fault_word(st);
   const unsigned long long to = watchdog_ns();
   if (fmt == FP8_E4M3) p2p_wait_scale_kernel<0><<<1, 32, 0, st>>>(win->sig, win->P, win->epoch, scale_out, amax_out, f, to);
   else p2p_wait_scale_kernel<1><<<1, 32, 0, st>>>(win->sig, win->P, win->epoch, scale_out, amax_out, f, to);
@@ -356,7 +356,7 @@ fp8_status_t phase_cast_push(fp8_p2p_t win, const fp8_hp_t& w, fp8_format_t fmt,
 }
 fp8_status_t phase_wait_done(fp8_p2p_t win, cudaStream_t st) {
   LaunchScope ls(K_SYNC, st);
-  p2p_wait_done_kernel<<<1, 64, 0, st>>>(win->sig, win->P, win->epoch, fault_word(), watchdog_ns());
+  p2p_wait_done_kernel<<<1, 64, 0, st>>>(win->sig, win->P, win->epoch, fault_word(st), watchdog_ns());
   return cuda_check(cudaGetLastError(), "p2p_wait_done");
 }
 
