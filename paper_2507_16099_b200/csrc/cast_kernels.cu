@@ -758,7 +758,8 @@ __device__ __forceinline__ uint2 cast8_bf16x2(const uint32_t (&w)[4], const floa
 }
 
 template <int FMT, bool RCEIL, bool DIM0, bool DIM1, bool TR1, int ST>
-__global__ void __launch_bounds__(256) mx_cast_tma_kernel(const __grid_constant__ CUtensorMap tmap, int64_t R,
+// ST == 2 (knob mx_cast_occ3): a 2-deep ring and <= 85 registers, so 3 CTAs (24 warps) share an SM
+__global__ void __launch_bounds__(256, (ST == 2 && !TR1) ? 3 : 1) mx_cast_tma_kernel(const __grid_constant__ CUtensorMap tmap, int64_t R,
                                                           int64_t C, uint8_t* __restrict__ q0,
                                                           uint8_t* __restrict__ sf0, uint8_t* __restrict__ q1,
                                                           uint8_t* __restrict__ sf1) {
@@ -1197,7 +1198,7 @@ static cudaError_t mx_tma_go(const CUtensorMap& m, int64_t R, int64_t C, uint8_t
   const cudaError_t attr_err = ensure_smem<mx_cast_tma_kernel<FMT, RC, D0, D1, TR, ST>>(smem);
   if (attr_err != cudaSuccess) return attr_err;
   const int64_t tiles = (R >> 7) * (C >> 7);
-  const int64_t cap = cap_grid((int64_t)sm_count() * (TR ? 1 : 2));
+  const int64_t cap = cap_grid((int64_t)sm_count() * (TR ? 1 : (ST == 2 ? 3 : 2)));
   LaunchScope ls(K_MX, s);
   kern<<<(unsigned)(tiles < cap ? tiles : cap), 256, smem, s>>>(m, R, C, q0, sf0, q1, sf1);
   return cudaGetLastError();
@@ -1219,6 +1220,7 @@ static cudaError_t mx_tma_launch_t(const void* x, int64_t R, int64_t C, int64_t 
     return cudaErrorInvalidValue;
   if (q0 && q1) {
     if (tr1) return mx_tma_go<FMT, RC, true, true, true, 4>(m, R, C, q0, sf0, q1, sf1, s);
+    if (knob(KNOB_MX_CAST_OCC3) == 1) return mx_tma_go<FMT, RC, true, true, false, 2>(m, R, C, q0, sf0, q1, sf1, s);
     return mx_tma_go<FMT, RC, true, true, false, 3>(m, R, C, q0, sf0, q1, sf1, s);
   }
   if (q0) return mx_tma_go<FMT, RC, true, false, false, 3>(m, R, C, q0, sf0, q1, sf1, s);

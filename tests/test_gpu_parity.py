@@ -1142,6 +1142,7 @@ LINEAR_BUFFER_CASES = [
     ("rowwise", {}), ("rowwise", {"cast_grid": 3}), ("rowwise", {"cast_grid": 7}), ("rowwise", {"amax_tile_tma": 0}),
     ("rowwise_gw_hp", {}),
     ("mxfp8", {}), ("mxfp8", {"cast_grid": 3}), ("mxfp8", {"mx_transposed": 1}), ("mxfp8", {"mx_cast_tma": 0}),
+    ("mxfp8", {"mx_cast_occ3": 1}), ("mxfp8", {"mx_cast_occ3": 1, "cast_grid": 5}),
 ]
 
 

@@ -43,13 +43,17 @@ def main(path):
             if k in hdr:
                 i = hdr.index(k)
                 print(f"  {label:45s} {r[i]:>18s} {units[i]}")
-        if "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg" in hdr and "sm__cycles_elapsed.avg" in hdr:
-            try:
-                a = float(r[hdr.index("sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg")])
-                e = float(r[hdr.index("sm__cycles_elapsed.avg")])
-                print(f"  {'tensor pipe active / elapsed':45s} {a / e * 100:>17.1f}%")
-            except ValueError:
-                pass
+        # tensor-pipe utilisation: the counter advances once per SM sub-partition (4 per SM), so active / (4 x
+        # elapsed); it agrees with achieved flop/clk / 16,384
+        for key in ("sm__pipe_tensor_cycles_active.avg", "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg"):
+            if key in hdr and "sm__cycles_elapsed.avg" in hdr:
+                try:
+                    a = float(r[hdr.index(key)])
+                    e = float(r[hdr.index("sm__cycles_elapsed.avg")])
+                    print(f"  {'tensor pipe active % (' + key.split('.')[0] + ')':45s} {a / (4 * e) * 100:>17.1f}%")
+                    break
+                except ValueError:
+                    pass
 
 
 if __name__ == "__main__":

@@ -8,8 +8,8 @@ for c in c4 c2; do
     $B --config $c > gpurun_out/${T}_launches_$c.log 2>&1
 done
 B1="python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-bf16 --no-cpu-baseline --no-digest"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:fp8_gemm -s 6 -c 2 -o gpurun_out/${T}_gemm_c4 $B1 --config c4 > gpurun_out/${T}_gemm_c4.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:fp8_gemm -s 6 -c 2 -o gpurun_out/${T}_gemm_c2 $B1 --config c2 > gpurun_out/${T}_gemm_c2.log 2>&1
+timeout 1200 ncu --set full --metrics sm__pipe_tensor_cycles_active.avg,sm__cycles_elapsed.avg --clock-control none --import-source on -k regex:fp8_gemm -s 6 -c 2 -o gpurun_out/${T}_gemm_c4 $B1 --config c4 > gpurun_out/${T}_gemm_c4.log 2>&1
+timeout 1200 ncu --set full --metrics sm__pipe_tensor_cycles_active.avg,sm__cycles_elapsed.avg --clock-control none --import-source on -k regex:fp8_gemm -s 6 -c 2 -o gpurun_out/${T}_gemm_c2 $B1 --config c2 > gpurun_out/${T}_gemm_c2.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:mx_cast -s 9 -c 3 -o gpurun_out/${T}_casts_c4 $B1 --config c4 > gpurun_out/${T}_casts_c4.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"amax|cast" -s 12 -c 4 -o gpurun_out/${T}_casts_c2 $B1 --config c2 > gpurun_out/${T}_casts_c2.log 2>&1
 ls -la gpurun_out/${T}_*
