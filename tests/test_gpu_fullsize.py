@@ -335,3 +335,65 @@ def test_c5_fullsize_fsdp_tensorwise():
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,recipe,shape", [("c2", "tensorwise", (16384, 14336, 4096)),
+                                              ("c3", "rowwise", (16384, 14336, 4096)),
+                                              ("c3", "rowwise", (16384, 4096, 14336)),
+                                              ("c4", "mxfp8", (16384, 28672, 8192))],
+                         ids=["c2-tensorwise", "c3w1-rowwise", "c3w2-rowwise", "c4-mxfp8"])
+def test_fullsize_power_of_two_invariance(cfg, recipe, shape):
+    """A property that holds at any size ("linearity in scales"; R-c3): scaling X by 2^3 scales
+    every amax over X by 8, every scale by 1/8 exactly (E8M0 codes by +3), and leaves every FP8 code of X
+    unchanged, so Y' = 8 Y, dX' = dX and dW' = 8 dW bit for bit (power-of-two factors are exact in fp32 and
+    bf16).  Checked over the FULL bench-size tensors and outputs, on the linear's own buffers.  MX: blocks
+    whose code is clamped (0 for the bf16-subnormal blocks of the c4 recipe, or > 251) are excluded from the
+    code check and Y is compared only on rows without a clamped nonzero block (all-zero blocks are fine)."""
+    from paper_2507_16099_b200 import ops
+    M, N, K = shape
+    from synth import device as sd
+    X = sd.tensor(cfg, "x", (M, K), 0, "cuda")
+    W = sd.tensor(cfg, "w", (N, K), 0, "cuda")
+    G = sd.tensor(cfg, "dy", (M, N), 0, "cuda")
+    X8 = X * 8   # exact in bf16 (exponent + 3; the recipes stay far below the bf16 maximum)
+    plan = ops.LinearPlan(M, N, K, recipe=recipe, out_dtype=torch.bfloat16)
+    runs = []
+    for x in (X, X8):
+        saved = plan.new_saved()
+        Y = plan.forward(x, W, saved)
+        torch.cuda.synchronize()
+        fb = {k: (v.clone() if torch.is_tensor(v) else v) for k, v in plan.buffers(saved).items()}
+        DX, DW = plan.backward(G, saved)
+        torch.cuda.synchronize()
+        runs.append((Y, DX, DW, fb, {k: (v.clone() if torch.is_tensor(v) else v) for k, v in plan.buffers(saved).items()}))
+    (Y, DX, DW, fb, bb), (Y8, DX8, DW8, fb8, bb8) = runs
+    if recipe != "mxfp8":
+        assert torch.equal(fb["x_fwd"], fb8["x_fwd"]) and torch.equal(bb["x_bwd"], bb8["x_bwd"])
+        for k_ in ("x_fwd_scale", "x_bwd_scale"):
+            assert torch.equal(fb[k_] if k_ == "x_fwd_scale" else bb[k_], 8 * (fb8[k_] if k_ == "x_fwd_scale" else bb8[k_]))
+        assert torch.equal(Y8.float(), 8 * Y.float())
+        assert torch.equal(DX8, DX)
+        assert torch.equal(DW8.float(), 8 * DW.float())
+        return
+    # MXFP8: E8M0 codes of X (dim0 along K, dim1 along M) shift by +3 wherever not clamped, element codes kept
+    for key_q, key_s in (("x_fwd", "x_fwd_scale"),):
+        s0 = fb[key_s].to(torch.int32)
+        s1 = fb8[key_s].to(torch.int32)
+        ok = (s0 >= 1) & (s0 <= 251)
+        assert torch.equal(s1[ok], s0[ok] + 3)
+    s0b = bb["x_bwd_scale"].to(torch.int32)
+    s1b = bb8["x_bwd_scale"].to(torch.int32)
+    okb = (s0b >= 1) & (s0b <= 251)
+    assert torch.equal(s1b[okb], s0b[okb] + 3)
+    # rows of X whose dim0 blocks are all unclamped: their codes match and Y' = 8 Y exactly there
+    # (the blocked E8M0 layout is a permutation; compare through the logical [M, K/32] view)
+    def unblock(buf, R, C):
+        C32 = C // 32
+        return buf.view(R // 128, C32 // 4, 32, 4, 4).permute(0, 3, 2, 1, 4).reshape(R, C32)
+    c0 = unblock(fb["x_fwd_scale"], M, K).to(torch.int32)
+    zero_blk = (X.view(M, K // 32, 32) == 0).all(dim=2)          # all-zero blocks contribute 0 either way
+    good_rows = (((c0 >= 1) & (c0 <= 251)) | zero_blk).all(dim=1)
+    assert int(good_rows.sum()) > M // 2
+    assert torch.equal(fb["x_fwd"][good_rows], fb8["x_fwd"][good_rows])
+    assert torch.equal(Y8[good_rows].float(), 8 * Y[good_rows].float())
+    assert torch.equal(DX8, DX)
