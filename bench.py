@@ -78,7 +78,7 @@ CONFIGS = {
 # few minutes) and for the cpu_baseline (one step of ~10-30 s of CPU work): same K and value
 # recipe, fewer rows
 CPU_SAMPLE = dict(M=128, N=2048)
-CPU_BASELINE_M = 1536   # tokens of the cpu_baseline sample: ~10-30 s of oracle work on the box's host cores
+CPU_BASELINE_M = 2560   # tokens of the cpu_baseline sample: ~10-30 s of oracle work on the box's host cores
 # the MX oracle spends its time in the element codecs (decode / encode per element), so its sample keeps
 # fewer weight rows for the same few seconds per step
 
@@ -97,8 +97,9 @@ def parse():
                          "configs[3]) at N=1 and c5 (the FSDP config, configs[4]) at N>1")
     ap.add_argument("--sub", default=None,
                     help="comma list of further configs measured in the same run and reported under 'sub' "
-                         "(no e2e / cpu_baseline); default at N=1 with the default headline: c2,c3,c5 (c5 "
-                         "through the FSDP gather path, the same-config N=1 point of the N>1 runs)")
+                         "(no e2e / cpu_baseline); default at N=1 with the default headline: c2,c3,c5,c3w1hp,moe "
+                         "(c5 through the FSDP gather path, the same-config N=1 point of the N>1 runs; c3w1hp the "
+                         "rowwise_gw_hp recipe; moe the scaled grouped GEMM)")
     ap.add_argument("--no-digest", dest="digest", action="store_false",
                     help="skip the SHA-256 of the timed inputs")
     ap.add_argument("--knob", action="append", default=[],
@@ -306,17 +307,13 @@ def input_digest(dev_tensors, seeds):
     """SHA-256 of the exact bytes of every timed input tensor (copied to the host once, outside the
     timed region) plus the generator and seeds that made them."""
     import hashlib
+    import torch
     out = {"generator": "synth.device (torch port of synth: splitmix64 -> Box-Muller fp64 -> recipe -> "
                         "RNE bf16), verified against synth by tests/test_gpu_synth.py", "seeds": seeds}
     for name, t in dev_tensors.items():
-        out["sha256_" + name] = hashlib.sha256(t.contiguous().view(-1).view(torch_uint8()).cpu().numpy()
+        out["sha256_" + name] = hashlib.sha256(t.contiguous().view(-1).view(torch.uint8).cpu().numpy()
                                                .tobytes()).hexdigest()
     return out
-
-
-def torch_uint8():
-    import torch
-    return torch.uint8
 
 
 def run_ours(a):
@@ -1107,8 +1104,8 @@ def main():
     if a.impl == "reference":
         run_reference(a)
         return
-    subs = [c for c in (a.sub.split(",") if a.sub else (["c2", "c3", "c5"] if default_headline and world == 1
-                                                          else [])) if c]
+    subs = [c for c in (a.sub.split(",") if a.sub else (["c2", "c3", "c5", "c3w1hp", "moe"]
+                                                          if default_headline and world == 1 else [])) if c]
     if a.knob:
         import paper_2507_16099_b200  # noqa: F401
         from paper_2507_16099_b200 import ops
