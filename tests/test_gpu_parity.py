@@ -1019,12 +1019,14 @@ def test_gemm_scheduler_long_launch_sequence(epi, knob):
         assert torch.equal(D.view(torch.int16), ref_m.view(torch.int16))
 
 
+@pytest.mark.parametrize("shape", [(512, 768, 512), (512, 1024, 8192)], ids=["small", "n512_auto"])
 @pytest.mark.parametrize("recipe", ["tensorwise", "rowwise", "mxfp8"])
-def test_linear_cuda_graph_replay(recipe):
+def test_linear_cuda_graph_replay(recipe, shape):
     """The whole fwd+bwd (amax, casts, GEMMs with the dynamic tile scheduler) captured into one CUDA graph
     (no host sync in any call) and replayed on new inputs copied into the static buffers: every replay is
-    bit-identical to the eager calls on the same inputs."""
-    M, N, K = 512, 768, 512
+    bit-identical to the eager calls on the same inputs.  n512_auto: the forward GEMM (N % 512 == 0,
+    K >= 8192) runs on 256 x 512 tiles with the TMA-store epilogue inside the graph."""
+    M, N, K = shape
     plan = ops.LinearPlan(M, N, K, recipe=recipe)
     saved = plan.new_saved()
     X = torch.empty((M, K), dtype=torch.bfloat16, device="cuda")
