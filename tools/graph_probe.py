@@ -23,7 +23,7 @@ def main():
     lin = cfg.get("linears") or [("w", cfg["N"], cfg["K"])]
     units = []
     for i, (nm, N, K) in enumerate(lin):
-        x, _, dy, w = bench.make_inputs(dict(cfg, N=N, K=K), M, N, K, 10 * i, 1, dev)
+        x, w, dy = bench.make_inputs(dict(cfg, N=N, K=K), M, N, K, 0, 1, dev, seed=i)
         plan = ops.LinearPlan(M, N, K, recipe=cfg["recipe"], out_dtype=torch.bfloat16, device=dev)
         units.append(dict(x=x, w=w, dy=dy, plan=plan, saved=plan.new_saved(dev),
                           y=torch.empty((M, N), dtype=torch.bfloat16, device=dev),
