@@ -1505,3 +1505,72 @@ def test_convert_training_tracks_high_precision(recipe):
     assert h[-1] < 0.05 * h[0] and f[-1] < 0.05 * f[0], (h[0], h[-1], f[0], f[-1])
     gap = max(abs(fk - hk) / hk for fk, hk in zip(f[:40], h[:40]))
     assert gap <= 0.1, (recipe, gap, [round(v, 4) for v in h[::8]], [round(v, 4) for v in f[::8]])
+
+
+# ----------------------------------------------------------------------------- randomized shapes and extremes
+
+def _fuzz_cases(n=24, seed=2025):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for i in range(n):
+        recipe = ["tensorwise", "rowwise", "rowwise_gw_hp", "mxfp8"][i % 4]
+        q = 128 if recipe == "mxfp8" else 16
+        M, N, K = (int(rng.integers(1, 1 + 1536 // q)) * q for _ in range(3))
+        cases.append((recipe, M, N, K, int(rng.integers(0, 1 << 30))))
+    return cases
+
+
+@pytest.mark.parametrize("recipe,M,N,K,seed", _fuzz_cases(), ids=lambda v: str(v))
+def test_linear_random_shapes(recipe, M, N, K, seed):
+    """Seeded random shapes (multiples of 16, of 128 for mxfp8, up to 1536 per dimension: one tile to several
+    waves, ragged tails in every dimension, N / K multiples of 512 included) for every recipe: the operand
+    bytes, scales and amaxes the linear writes bit-exact, Y / dX / dW within tolerance of the oracle."""
+    cfg = {"tensorwise": "c2", "rowwise": "c3", "rowwise_gw_hp": "c3", "mxfp8": "c4"}[recipe]
+    x, w, dy = synth.linear_inputs(cfg, M, N, K, seed=seed % 1000)
+    y, yb, so = olin.forward(x, w, recipe)
+    dx, dxb, dw, dwb, co = olin.backward(x, w, dy, recipe)
+    plan = ops.LinearPlan(M, N, K, recipe=recipe, out_dtype=torch.float32)
+    saved = plan.new_saved()
+    X, W, G = _dev(x, torch.bfloat16), _dev(w, torch.bfloat16), _dev(dy, torch.bfloat16)
+    Y = plan.forward(X, W, saved)
+    torch.cuda.synchronize()
+    fb = {k: (v.clone() if torch.is_tensor(v) else v) for k, v in plan.buffers(saved).items()}
+    DX, DW = plan.backward(G, saved, x=X)
+    torch.cuda.synchronize()
+    bb = plan.buffers(saved)
+    if recipe == "mxfp8":
+        _eq("x_fwd", fb["x_fwd"], so["xq"]); _eq("X E8M0", _unblock(fb["x_fwd_scale"], M, K), so["xsc"])
+        _eq("dy_dw", bb["dy_dw"], co["g1"].T); _eq("dY E8M0 dim1", _unblock(bb["dy_dw_scale"], N, M), co["g1s"])
+    else:
+        _eq("x_fwd", fb["x_fwd"], so["xq"]); _eq("sx", fb["x_fwd_scale"], np.asarray(so["sx"], np.float32).reshape(-1))
+        _eq("w_fwd", fb["w_fwd"], so["wq"])
+        key = "gq" if recipe == "tensorwise" else "g_r"
+        _eq("dy_dx", bb["dy_dx"], co[key])
+    _tol_check(_np(Y).astype(np.float64), y, yb)
+    _tol_check(_np(DX).astype(np.float64), dx, dxb)
+    _tol_check(_np(DW).astype(np.float64), dw, dwb)
+
+
+@pytest.mark.parametrize("recipe", ["tensorwise", "mxfp8"])
+def test_gemm_long_contraction(recipe):
+    """An extreme of the contraction length: K = 65536 (256 K stages per tile; the tolerance
+    1e-2 * sum|a||b| covers fp32 accumulation up to K ~ 128k), M = N = 256."""
+    M, N, K = 256, 256, 65536
+    cfg = "c4" if recipe == "mxfp8" else "c2"
+    a = synth.RECIPES[cfg]("x", (M, K), 3, cfg)
+    b = synth.RECIPES[cfg]("w", (N, K), 3, cfg)
+    if recipe == "mxfp8":
+        qa, sa = omx.quantize_dim0(a, E4M3)
+        qb, sb = omx.quantize_dim0(b, E4M3)
+        ref, bd = ogemm.mx_gemm_ref(qa, sa, E4M3, qb, sb, E4M3), ogemm.mx_abs_bound(qa, sa, E4M3, qb, sb, E4M3)
+        D = ops.gemm(torch.from_numpy(qa).cuda(), "e4m3", torch.from_numpy(_block(sa)).cuda(),
+                     torch.from_numpy(qb).cuda(), "e4m3", torch.from_numpy(_block(sb)).cuda(), "mx32",
+                     out_dtype=torch.float32)
+    else:
+        qa, sa, _ = fp8.cast_tensorwise(a, E4M3)
+        qb, sb, _ = fp8.cast_tensorwise(b, E4M3)
+        ref, bd = ogemm.gemm_ref(qa, E4M3, sa, qb, E4M3, sb), ogemm.abs_bound(qa, E4M3, sa, qb, E4M3, sb)
+        D = ops.gemm(torch.from_numpy(qa).cuda(), "e4m3", torch.tensor([sa], device="cuda"),
+                     torch.from_numpy(qb).cuda(), "e4m3", torch.tensor([sb], device="cuda"), "tensor",
+                     out_dtype=torch.float32)
+    _tol_check(_np(D).astype(np.float64), ref, bd)
