@@ -527,6 +527,7 @@ uint64_t fp8_launch_count(void);
  *   gemm_n512 (2 = 256 x 512 tiles for plain FP8 launches whose problems all have N % 512 == 0 and
  *   K >= 8192; 1 = whenever N % 512 == 0; 0 = never) |
  *   gemm_l2pf (0 = off; d > 0: the GEMM producer prefetches operand boxes d stages ahead into L2) |
+ *   mx_cast_occ3 (0) | amax_bulk (1: tensorwise amax of contiguous tensors by 1-D bulk copies; 0: register streaming) |
  *   watchdog_ms (30000; 0 = peer waits never give up)
  *   -- defaults in parentheses.
  * A knob changes launches enqueued after the call.  Unknown name or out-of-range value:

@@ -31,7 +31,7 @@ static const KnobDef kKnobs[KNOB_COUNT] = {
     {"gemm_debug", 0, 0, 1 << 16},  {"gemm_sched", 1, 0, 1},       {"mx_sf_split", 1, 0, 8},
     {"gemm_raster", -1, -1, 64},    {"mx_n192", 0, 0, 1},          {"gemm_stages", 3, 3, 6},
     {"gemm_epi", 0, 0, 8},          {"mx_transposed", 0, 0, 1},    {"tw_dual", 1, 0, 1},
-    {"gemm_kserp", 1, 0, 1},        {"gemm_n512", 2, 0, 2},        {"gemm_l2pf", 0, 0, 64},  {"mx_cast_occ3", 0, 0, 1},        {"watchdog_ms", 30000, 0, 1 << 30},
+    {"gemm_kserp", 1, 0, 1},        {"gemm_n512", 2, 0, 2},        {"gemm_l2pf", 0, 0, 64},  {"mx_cast_occ3", 0, 0, 1},      {"amax_bulk", 1, 0, 1},        {"watchdog_ms", 30000, 0, 1 << 30},
 };
 static std::atomic<int> g_knobs[KNOB_COUNT];
 // defaults come from the table (one source of truth); a table shorter than the enum leaves a null name

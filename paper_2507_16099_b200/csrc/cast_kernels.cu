@@ -993,10 +993,15 @@ static cudaError_t amax_tma_go(const CUtensorMap& m, int64_t R, int64_t C, int64
   return cudaGetLastError();
 }
 
+static cudaError_t amax_bulk_go(const void* x0, int64_t b0, uint32_t* out0, const void* x1, int64_t b1, uint32_t* out1,
+                                bool bf16, cudaStream_t st);
+
 template <typename T>
 static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, int mode, uint32_t* at,
                                  uint32_t* ar, uint32_t* ac, cudaStream_t st, const Seg& seg) {
   const T* p = static_cast<const T*>(x);
+  if (mode == 1 && ld == C && knob(KNOB_AMAX_BULK) == 1 && (R * C * (int64_t)sizeof(T)) % 16 == 0)
+    return amax_bulk_go(x, R * C * (int64_t)sizeof(T), at, nullptr, 0, nullptr, sizeof(T) == 2, st);
   if (mode == 1 && ld == C) {
     const int64_t n16 = R * C * (int64_t)sizeof(T) / 16;
     // tuning knobs amax_blocks_per_sm / amax_loads (16-byte loads per thread: 4, 8, 12, 16); default
@@ -1096,10 +1101,115 @@ cudaError_t launch_amax_multi(const AmaxMultiArgs& a, cudaStream_t st) {
 
 // Tensorwise amax of two contiguous tensors of one dtype in one launch (the forward's X and W): the
 // persistent grid is split between them in proportion to their sizes.
+// Tensorwise amax of one or two contiguous tensors through 1-D bulk copies (knob amax_bulk): 32 KB chunks
+// handed out interleaved over a persistent grid (CTA b: chunks b, b + G, ...; neighbouring chunks are read
+// at the same time), ST chunks in flight per CTA landing on mbarriers, |x| max on raw bit patterns, one
+// atomic per tensor per CTA.  Chunks [0, c0) belong to x0, [c0, c0 + c1) to x1.
+template <typename T, int ST>
+__global__ void __launch_bounds__(256) amax_bulk_kernel(const uint8_t* __restrict__ x0, int64_t b0, uint32_t* out0,
+                                                        const uint8_t* __restrict__ x1, int64_t b1, uint32_t* out1) {
+  constexpr int CH = 32768;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const uint32_t s0 = smem_u32(sm), bar0 = s0 + ST * CH;
+  const int t = threadIdx.x;
+  const int64_t c0 = (b0 + CH - 1) / CH, c1 = (b1 + CH - 1) / CH, total = c0 + c1;
+  const int64_t G = gridDim.x;
+  auto bytes_of = [&](int64_t id) -> uint32_t {
+    const int64_t off = id < c0 ? id * CH : (id - c0) * CH;
+    const int64_t n = id < c0 ? b0 : b1;
+    return (uint32_t)(n - off < CH ? n - off : CH);
+  };
+  auto issue = [&](int k) {
+    const int64_t id = blockIdx.x + (int64_t)k * G;
+    if (id < total) {
+      const uint32_t nb = bytes_of(id), bar = bar0 + 8 * (k % ST);
+      mbar_arrive_expect_tx(bar, nb);
+      bulk_load(s0 + (k % ST) * CH, id < c0 ? x0 + id * CH : x1 + (id - c0) * CH, nb, bar);
+    }
+  };
+  if (t == 0) {
+    for (int i = 0; i < ST; ++i) mbar_init(bar0 + 8 * i, 1);
+    fence_mbar_init();
+    for (int k = 0; k < ST; ++k) issue(k);
+  }
+  __syncthreads();
+  constexpr bool BF = sizeof(T) == 2;
+  const uint32_t mask = BF ? 0x7FFF7FFFu : 0x7FFFFFFFu;
+  uint32_t m0 = 0, m1 = 0;
+  for (int k = 0;; ++k) {
+    const int64_t id = blockIdx.x + (int64_t)k * G;
+    if (id >= total) break;
+    mbar_wait(bar0 + 8 * (k % ST), (uint32_t)(k / ST) & 1u);
+    const int nv = (int)(bytes_of(id) / 16);
+    const uint4* v = reinterpret_cast<const uint4*>(sm + (k % ST) * CH);
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < CH / 16 / 256; ++i) {
+      const int j = t + 256 * i;
+      if (j < nv) {
+        const uint4 q = v[j];
+        if (BF) {
+          m = __vmaxu2(m, q.x & mask); m = __vmaxu2(m, q.y & mask);
+          m = __vmaxu2(m, q.z & mask); m = __vmaxu2(m, q.w & mask);
+        } else {
+          m = max(m, q.x & mask); m = max(m, q.y & mask); m = max(m, q.z & mask); m = max(m, q.w & mask);
+        }
+      }
+    }
+    if (id < c0) m0 = BF ? __vmaxu2(m0, m) : max(m0, m);
+    else m1 = BF ? __vmaxu2(m1, m) : max(m1, m);
+    __syncthreads();   // stage consumed by every thread
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(k + ST);
+    }
+  }
+  if (BF) {   // packed bf16 pairs -> the larger half, as an fp32 bit pattern
+    m0 = max(m0 & 0xFFFFu, m0 >> 16) << 16;
+    m1 = max(m1 & 0xFFFFu, m1 >> 16) << 16;
+  }
+  __shared__ uint32_t red[2][8];
+  m0 = __reduce_max_sync(0xffffffffu, m0);
+  m1 = __reduce_max_sync(0xffffffffu, m1);
+  if ((t & 31) == 0) {
+    red[0][t >> 5] = m0;
+    red[1][t >> 5] = m1;
+  }
+  __syncthreads();
+  if (t == 0) {
+    uint32_t a = 0, b = 0;
+    for (int w = 0; w < 8; ++w) {
+      a = max(a, red[0][w]);
+      b = max(b, red[1][w]);
+    }
+    if (a) atomicMax(out0, a);
+    if (b && out1) atomicMax(out1, b);
+  }
+}
+
+static cudaError_t amax_bulk_go(const void* x0, int64_t b0, uint32_t* out0, const void* x1, int64_t b1, uint32_t* out1,
+                                bool bf16, cudaStream_t st) {
+  constexpr int ST = 4, CH = 32768;
+  constexpr int smem = ST * CH + ST * 8;
+  const cudaError_t e = bf16 ? ensure_smem<amax_bulk_kernel<__nv_bfloat16, ST>>(smem)
+                             : ensure_smem<amax_bulk_kernel<float, ST>>(smem);
+  if (e != cudaSuccess) return e;
+  const int64_t chunks = (b0 + CH - 1) / CH + (b1 + CH - 1) / CH;
+  const int64_t cap = cap_grid((int64_t)sm_count() * 1);
+  const unsigned g = (unsigned)(chunks < cap ? chunks : cap);
+  LaunchScope ls(K_AMAX, st);
+  const uint8_t* p0 = static_cast<const uint8_t*>(x0);
+  const uint8_t* p1 = static_cast<const uint8_t*>(x1);
+  if (bf16) amax_bulk_kernel<__nv_bfloat16, ST><<<g, 256, smem, st>>>(p0, b0, out0, p1, b1, out1);
+  else amax_bulk_kernel<float, ST><<<g, 256, smem, st>>>(p0, b0, out0, p1, b1, out1);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_amax_flat_dual(const void* x0, int64_t n0_elems, uint32_t* out0, const void* x1, int64_t n1_elems,
                                   uint32_t* out1, bool bf16, cudaStream_t st) {
   const int es = bf16 ? 2 : 4;
   if ((n0_elems * es) % 16 || (n1_elems * es) % 16 || n0_elems <= 0 || n1_elems <= 0) return cudaErrorNotSupported;
+  if (knob(KNOB_AMAX_BULK) == 1) return amax_bulk_go(x0, n0_elems * es, out0, x1, n1_elems * es, out1, bf16, st);
   const int64_t a16 = n0_elems * es / 16, b16 = n1_elems * es / 16;
   const int64_t cap = (int64_t)sm_count() * 8;
   const int64_t want = (a16 + b16 + 255) / 256;

@@ -33,7 +33,8 @@ enum Knob {
   KNOB_GEMM_KSERP,          // 1: odd waves of GEMM tiles walk K backwards (L2 reuse across waves); 0: all forward
   KNOB_GEMM_N512,
   KNOB_GEMM_L2PF,
-  KNOB_MX_CAST_OCC3,        // 1: MX cast (dim0 + dim1, row-major dim1) with a 2-deep ring at 3 CTAs per SM           // >0: the GEMM producer prefetches operand boxes this many stages ahead into L2           // 1: plain FP8 GEMMs with every N % 512 == 0 use 256 x 512 CTA-pair tiles
+  KNOB_MX_CAST_OCC3,
+  KNOB_AMAX_BULK,           // 1: tensorwise amax of contiguous tensors through 1-D bulk copies into a smem ring        // 1: MX cast (dim0 + dim1, row-major dim1) with a 2-deep ring at 3 CTAs per SM           // >0: the GEMM producer prefetches operand boxes this many stages ahead into L2           // 1: plain FP8 GEMMs with every N % 512 == 0 use 256 x 512 CTA-pair tiles
   KNOB_WATCHDOG_MS,         // peer waits (P2P gather, fused reduce-scatter, async-TP) give up after this many ms
                             // and report FP8_ECUDA at the next call; 0 = wait forever
   KNOB_COUNT

@@ -1140,7 +1140,8 @@ def test_linear_strided_inputs(recipe):
 # ----------------------------------------------------------------------------- what the linear itself writes
 
 LINEAR_BUFFER_CASES = [
-    ("tensorwise", {}), ("tensorwise", {"tw_dual": 0}),
+    ("tensorwise", {}), ("tensorwise", {"tw_dual": 0}), ("tensorwise", {"amax_bulk": 1}),
+    ("tensorwise", {"amax_bulk": 1, "tw_dual": 0}),
     ("rowwise", {}), ("rowwise", {"cast_grid": 3}), ("rowwise", {"cast_grid": 7}), ("rowwise", {"amax_tile_tma": 0}),
     ("rowwise_gw_hp", {}),
     ("mxfp8", {}), ("mxfp8", {"cast_grid": 3}), ("mxfp8", {"mx_transposed": 1}), ("mxfp8", {"mx_cast_tma": 0}),
@@ -1574,3 +1575,20 @@ def test_gemm_long_contraction(recipe):
                      torch.from_numpy(qb).cuda(), "e4m3", torch.tensor([sb], device="cuda"), "tensor",
                      out_dtype=torch.float32)
     _tol_check(_np(D).astype(np.float64), ref, bd)
+
+
+@pytest.mark.parametrize("bulk", [0, 1], ids=["streaming", "bulk_copy"])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("shape", [(16, 16), (272, 400), (1024, 4096), (4112, 1040), (16384, 512)])
+def test_amax_tensor_kernels(shape, dtype, bulk, knob):
+    """Tensorwise amax (the register-streaming kernel, or 1-D bulk copies into a smem ring with knob
+    amax_bulk): bit-exact vs the oracle for sizes from one 16-byte vector to many 32 KB chunks with a ragged
+    last chunk, bf16 and fp32, including an outlier placed in the last element."""
+    knob("amax_bulk", bulk)
+    x = synth.tensor_c2("x", shape, seed=3) if dtype == torch.bfloat16 else synth.tensor_c1("x", shape, seed=3)
+    x = x.copy()
+    x[-1, -1] = np.float32(-7777.0)
+    X = _dev(x, dtype)
+    got = ops.amax(X, "tensor")
+    torch.cuda.synchronize()
+    assert _bits(_np(got))[0] == _bits(fp8.amax(_np(X.float()))).reshape(-1)[0]
