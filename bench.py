@@ -66,6 +66,9 @@ CONFIGS = {
     "c3": dict(M=16384, K=4096, N=14336, recipe="rowwise", cfg="c3", kind="layer",
                linears=[("wq", 4096, 4096), ("wk", 1024, 4096), ("wv", 1024, 4096), ("wo", 4096, 4096),
                         ("w1", 14336, 4096), ("w3", 14336, 4096), ("w2", 4096, 14336)],
+               # linears that read the same input in a Llama layer (the attention norm's output, the MLP
+               # norm's output): one X per group, cast once (fp8_linear_fwd_shared)
+               shared=[("wq", "wk", "wv"), ("w1", "w3")],
                workload="c3: one Llama-3-8B layer's seven linears (attention wq/wk/wv/wo + MLP w1/w3/w2) fwd+bwd, "
                         "M=16384 tokens, rowwise scaling, bf16 in/out (BASELINE.json configs[2])"),
     "moe": dict(T=32768, E=8, N=14336, K=4096, recipe="rowwise", cfg="c3", kind="moe",
@@ -105,6 +108,9 @@ def parse():
     ap.add_argument("--knob", action="append", default=[],
                     help="name=value: select a kernel variant via fp8_set_knob (A/B experiments; default = "
                          "the product path); recorded in the JSON line")
+    ap.add_argument("--layer-separate", action="store_true",
+                    help="c3 layer: every linear casts its own input (default: wq/wk/wv and w1/w3 read one X, "
+                         "cast once through fp8_linear_fwd_shared)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -762,16 +768,44 @@ def run_layer(a):
     units = []
     for i, (name, N, K) in enumerate(cfg["linears"]):
         x, w, dy = make_inputs(dict(cfg, N=N, K=K), M, N, K, rank, 1, dev, seed=i)
-        plan = ops.LinearPlan(M, N, K, recipe=cfg["recipe"], out_dtype=torch.bfloat16, device=dev)
-        units.append(dict(name=name, N=N, K=K, x=x, w=w, dy=dy, plan=plan, saved=plan.new_saved(dev),
+        units.append(dict(name=name, N=N, K=K, x=x, w=w, dy=dy,
                           y=torch.empty((M, N), dtype=torch.bfloat16, device=dev),
                           dx=torch.empty((M, K), dtype=torch.bfloat16, device=dev),
                           dw=torch.empty((N, K), dtype=torch.bfloat16, device=dev)))
+    # groups of linears reading one X (the first member's); --layer-separate: every linear on its own
+    byname = {u["name"]: u for u in units}
+    groups = [] if a.layer_separate else [[byname[n] for n in g] for g in cfg.get("shared", [])]
+    grouped = {id(u) for g in groups for u in g}
+    groups += [[u] for u in units if id(u) not in grouped]
+    groups.sort(key=lambda g: units.index(g[0]))
+    for g in groups:
+        for u in g[1:]:
+            u["x"] = g[0]["x"]
+        if len(g) == 1:
+            u = g[0]
+            u["plan"] = ops.LinearPlan(M, u["N"], u["K"], recipe=cfg["recipe"], out_dtype=torch.bfloat16, device=dev)
+            u["saved"] = u["plan"].new_saved(dev)
+        else:
+            sp = ops.SharedInputPlan(M, [u["N"] for u in g], g[0]["K"], recipe=cfg["recipe"],
+                                     out_dtype=torch.bfloat16, device=dev)
+            sv = sp.new_saved(dev)
+            for u, t in zip(g, sv):
+                u["saved"] = t
+            g[0]["group_plan"] = sp
+
+    def run_group(g, xs, ws_, dys):
+        if len(g) == 1:
+            u = g[0]
+            u["plan"].forward(xs[0], ws_[0], u["saved"], y=u["y"])
+            u["plan"].backward(dys[0], u["saved"], dx=u["dx"], dw=u["dw"], x=xs[0])
+        else:
+            sp, sv = g[0]["group_plan"], [u["saved"] for u in g]
+            sp.forward(xs[0], ws_, sv, ys=[u["y"] for u in g])
+            sp.backward(dys, sv, dxs=[u["dx"] for u in g], dws=[u["dw"] for u in g], x=xs[0])
 
     def step():
-        for u in units:
-            u["plan"].forward(u["x"], u["w"], u["saved"], y=u["y"])
-            u["plan"].backward(u["dy"], u["saved"], dx=u["dx"], dw=u["dw"], x=u["x"])
+        for g in groups:
+            run_group(g, [g[0]["x"]], [u["w"] for u in g], [u["dy"] for u in g])
 
     for _ in range(max(a.warmup, 3)):
         step()
@@ -813,24 +847,28 @@ def run_layer(a):
     gemm_tflops = flops_step / (sum(gemm_ms) / a.steps / 1e3) / 1e12
     peaks = _peaks()
     fp8_peak = 2.0 * peaks["bf16"]
-    cast_bytes = sum((M * u["K"] + u["N"] * u["K"] + M * u["N"]) * 6 for u in units)   # rowwise: 6 B / element
+    # rowwise: 6 B / element (read for the amax, read for the cast, two 1-byte copies); X once per group
+    cast_bytes = sum((u["N"] * u["K"] + M * u["N"]) * 6 for u in units) + sum(M * g[0]["K"] * 6 for g in groups)
     cast_ms = sum(sum(by.get(k, [])) for k in (0, 1)) / a.steps
     e2e = None
     if a.e2e_steps > 0:
-        host = [dict(x=u["x"].cpu().pin_memory(), w=u["w"].cpu().pin_memory(), dy=u["dy"].cpu().pin_memory(),
-                     y=torch.empty_like(u["y"], device="cpu").pin_memory(),
-                     dx=torch.empty_like(u["dx"], device="cpu").pin_memory(),
-                     dw=torch.empty_like(u["dw"], device="cpu").pin_memory()) for u in units]
-        dbuf = [dict(x=torch.empty_like(u["x"]), w=torch.empty_like(u["w"]), dy=torch.empty_like(u["dy"])) for u in units]
+        host = {id(u): dict(x=u["x"].cpu().pin_memory() if u is g[0] else None, w=u["w"].cpu().pin_memory(),
+                            dy=u["dy"].cpu().pin_memory(), y=torch.empty_like(u["y"], device="cpu").pin_memory(),
+                            dx=torch.empty_like(u["dx"], device="cpu").pin_memory(),
+                            dw=torch.empty_like(u["dw"], device="cpu").pin_memory()) for g in groups for u in g}
+        dbuf = {id(u): dict(x=torch.empty_like(u["x"]) if u is g[0] else None, w=torch.empty_like(u["w"]),
+                            dy=torch.empty_like(u["dy"])) for g in groups for u in g}
 
         def e2e_step():
-            for u, h, d in zip(units, host, dbuf):
-                for k in ("x", "w", "dy"):
-                    d[k].copy_(h[k], non_blocking=True)
-                u["plan"].forward(d["x"], d["w"], u["saved"], y=u["y"])
-                u["plan"].backward(d["dy"], u["saved"], dx=u["dx"], dw=u["dw"], x=d["x"])
-                for k in ("y", "dx", "dw"):
-                    h[k].copy_(u[k], non_blocking=True)
+            for g in groups:
+                for u in g:
+                    for k in ("x", "w", "dy"):
+                        if host[id(u)][k] is not None:
+                            dbuf[id(u)][k].copy_(host[id(u)][k], non_blocking=True)
+                run_group(g, [dbuf[id(g[0])]["x"]], [dbuf[id(u)]["w"] for u in g], [dbuf[id(u)]["dy"] for u in g])
+                for u in g:
+                    for k in ("y", "dx", "dw"):
+                        host[id(u)][k].copy_(u[k], non_blocking=True)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -842,11 +880,12 @@ def run_layer(a):
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
         e2e = {"value": flops_step * a.e2e_steps * world / (ems / 1e3) / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": sum((u["x"].numel() + u["w"].numel() + u["dy"].numel()) * 2 for u in units),
+               "h2d_bytes_per_step": sum((u["w"].numel() + u["dy"].numel()) * 2 for u in units)
+                                     + sum(g[0]["x"].numel() * 2 for g in groups),
                "d2h_bytes_per_step": sum((u["y"].numel() + u["dx"].numel() + u["dw"].numel()) * 2 for u in units),
                "ms_per_step": ems / a.e2e_steps,
-               "path": "per linear: pinned host -> device X, W, dY + fp8_linear_fwd/bwd (C-ABI) + device -> host "
-                       "Y, dX, dW, every step, on the compute stream"}
+               "path": "per linear group: pinned host -> device X (once per group), W, dY + fp8_linear_fwd/bwd or "
+                       "fp8_linear_fwd/bwd_shared (C-ABI) + device -> host Y, dX, dW, every step, on the compute stream"}
     bf16 = None
     if not a.no_bf16:
         def bstep():
@@ -874,6 +913,7 @@ def run_layer(a):
             "vs_baseline": None, "dtype": "fp8 (e4m3 x e5m2 codes, fp32 accumulate, bf16 out)",
             "data": "synthetic (seeded synth generator run on the device, config value recipe; = the parity tests' inputs at rank 0)",
             "config": {"workload": cfg["workload"], "M_per_gpu": M, "linears": cfg["linears"], "recipe": cfg["recipe"],
+                       "shared_input_groups": [[u["name"] for u in g] for g in groups if len(g) > 1],
                        "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
                        "l2": "inputs larger than L2 (126 MB) for the MLP linears; no flush"},
             "roofline": {"bound": "tensor", "kernel": "fp8_gemm_kernel (tcgen05 kind::f8f6f4)",

@@ -80,7 +80,7 @@
 extern "C" {
 #endif
 
-#define FP8TRAIN_ABI_VERSION 6
+#define FP8TRAIN_ABI_VERSION 7
 
 typedef enum {
   FP8_OK = 0,
@@ -310,6 +310,31 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x
 fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
                                const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax,
                                void* dw, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Float8Linears sharing one input -- e.g. a Llama layer's wq / wk / wv (all read the attention
+ * norm's output) and w1 / w3 (the MLP norm's output).  Each member is the Float8Linear of
+ * fp8_linear_fwd / fp8_linear_bwd (Appendix A): X's scales depend on X alone
+ * (tensorwise amax over X; rowwise per row / per column of X; MX blocks of X), so its amax and
+ * FP8 copies are computed ONCE, by member 0, and read by every member's GEMMs.  Every output and
+ * every saved byte equals what n separate fp8_linear_fwd / fp8_linear_bwd calls write.
+ *   fwd: x [M,K]; w: HOST array of n weights [N_i, K] (same dtype as x); y: HOST array of n
+ *     outputs [M, N_i] (out_dtype, dense); saved: HOST array of n buffers of
+ *     fp8_linear_saved_bytes(cfg, M, N_i, K) bytes -- saved[0] holds X's backward operand,
+ *     saved[i > 0] only W_i's; ws >= fp8_linear_workspace_bytes(cfg, M, max N_i, K) bytes.
+ *   bwd: dy: HOST array of n [M, N_i]; x as for fp8_linear_bwd (data read by rowwise_gw_hp only);
+ *     saved: the same array the forward wrote (all n, saved[0] first); dx / dw: HOST arrays of n
+ *     outputs or NULL, entries may be NULL (dX_i is per member: summing the members' dX_i is the
+ *     caller's -- autograd's -- job, as for separate linears); ws as for the forward.
+ *   1 <= n <= FP8_SHARED_MAX.  No pre-cast weights (w_fp8) and no amax hand-over here.  All
+ *   arguments are validated before the first launch.
+ * ------------------------------------------------------------------------- */
+#define FP8_SHARED_MAX 8
+fp8_status_t fp8_linear_fwd_shared(const fp8_linear_cfg_t* cfg, fp8_hp_t x, int n, const fp8_hp_t* w,
+                                   void* const* y, void* const* saved, void* ws, size_t ws_bytes, void* stream);
+fp8_status_t fp8_linear_bwd_shared(const fp8_linear_cfg_t* cfg, int n, const fp8_hp_t* dy, fp8_hp_t x,
+                                   const void* const* saved, void* const* dx, void* const* dw, void* ws,
+                                   size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * MoE scaled grouped GEMM ("scaled_grouped_mm: differentiable scaled

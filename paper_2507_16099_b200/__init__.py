@@ -6,8 +6,8 @@ has not been built; there is no CPU fallback.
 """
 
 from . import _lib  # noqa: F401  (loads libfp8train.so or raises)
-from .ops import GroupedPlan, LinearPlan, amax, cast, gemm, launch_count  # noqa: F401
+from .ops import GroupedPlan, LinearPlan, SharedInputPlan, amax, cast, gemm, launch_count  # noqa: F401
 from .linear import Float8Linear, convert, scaled_grouped_mm  # noqa: F401
 
-__all__ = ["GroupedPlan", "LinearPlan", "amax", "cast", "gemm", "launch_count", "Float8Linear", "convert",
+__all__ = ["GroupedPlan", "LinearPlan", "SharedInputPlan", "amax", "cast", "gemm", "launch_count", "Float8Linear", "convert",
            "scaled_grouped_mm"]

@@ -601,6 +601,148 @@ fp8_status_t check_w_fp8(const fp8_linear_cfg_t* cfg, const fp8_tensor_t* w_fp8,
 
 }  // namespace
 
+}  // extern "C"
+
+// Training forward of one linear (fp8_linear_fwd_ex with `saved`, and each member of
+// fp8_linear_fwd_shared).  X's operands go to / come from `svx` (its backward copy) and `fw` (its
+// forward copy, row scales / E8M0), W's to `svw` and `fw`.  cast_x = false: X's amax and casts were
+// already written by the previous member of a shared-input group (same x, same fw / svx), so only
+// W is cast here -- the bytes are the ones a separate fp8_linear_fwd would write.
+static fp8_status_t linear_fwd_train(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const float* x_amax, fp8_hp_t w,
+                                     const fp8_tensor_t* w_fp8, void* y, float* y_amax, const Saved& svx,
+                                     const Saved& svw, const FwdWs& fw, bool cast_x, cudaStream_t st) {
+  const int64_t M = x.rows, K = x.cols, N = w.rows;
+  const bool xb = x.dtype == FP8_DT_BF16, wb = w.dtype == FP8_DT_BF16;
+  const int ff = cfg->fmt_fwd;
+  const int of32 = cfg->out_dtype == FP8_DT_F32;
+  uint32_t* yam = reinterpret_cast<uint32_t*>(y_amax);
+  auto fwd_gemm = [&](const GemmProblem& p) -> fp8_status_t {
+    if (yam) FP8T_CUDA(cudaMemsetAsync(yam, 0, 4, st), "memset y_amax");
+    FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
+    return FP8_OK;
+  };
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    // row-major codes only: the backward GEMMs read them MN-major (no transposed copies)
+    uint32_t* ax = reinterpret_cast<uint32_t*>(fw.amax);
+    uint32_t* aw = ax + 1;
+    const float* axp = x_amax ? x_amax : fw.amax;
+    const uint8_t* wq = svw.wT;
+    FP8T_CUDA(cudaMemsetAsync(cast_x ? ax : aw, 0, cast_x ? 8 : 4, st), "memset");
+    // amax X and W by one launch, then X and W cast by one launch (measured on c2: casts 0.165 ->
+    // 0.158 ms per step); knob tw_dual = 0 keeps four launches (X's cast right after its amax).
+    // x_amax: amax(X) precomputed by X's producer (e.g. the previous layer's epilogue) -> no amax pass
+    const bool tw_dual = knob(KNOB_TW_DUAL) == 1;
+    if (!cast_x) {
+      if (w_fp8) {
+        wq = w_fp8->q;
+        FP8T_CUDA(cudaMemcpyAsync(svw.sw, w_fp8->scale, 4, cudaMemcpyDeviceToDevice, st), "copy w scale");
+      } else {
+        FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 1, aw, nullptr, nullptr, st), "amax w");
+        FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 1, 0, fw.amax + 1, fw.amax + 1, svw.wT, nullptr,
+                              (float*)svw.sw, nullptr, st),
+                  "cast w");
+      }
+    } else if (tw_dual && !w_fp8 && xb == wb) {
+      cudaError_t e = cudaErrorNotSupported;
+      if (!x_amax && x.ld == K && w.ld == K)
+        e = launch_amax_flat_dual(x.ptr, M * K, ax, w.ptr, N * K, aw, xb, st);
+      if (e != cudaErrorNotSupported) {
+        FP8T_CUDA(e, "amax x, w");
+      } else {
+        if (!x_amax) FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
+        FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 1, aw, nullptr, nullptr, st), "amax w");
+      }
+      CastDual cd{};
+      cd.x[0] = x.ptr; cd.R[0] = M; cd.C[0] = K; cd.ld[0] = x.ld; cd.amax_q[0] = axp; cd.amax_t[0] = axp;
+      cd.q[0] = svx.xT; cd.scale_q[0] = (float*)svx.sx;
+      cd.x[1] = w.ptr; cd.R[1] = N; cd.C[1] = K; cd.ld[1] = w.ld; cd.amax_q[1] = fw.amax + 1;
+      cd.amax_t[1] = fw.amax + 1; cd.q[1] = svw.wT; cd.scale_q[1] = (float*)svw.sw;
+      FP8T_CUDA(launch_cast_dual(cd, xb, ff, 1, 0, st), "cast x, w");
+    } else {
+      if (!x_amax) FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
+      FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 1, 0, axp, axp, svx.xT, nullptr, (float*)svx.sx, nullptr, st),
+                "cast x");
+      if (w_fp8) {
+        wq = w_fp8->q;
+        FP8T_CUDA(cudaMemcpyAsync(svw.sw, w_fp8->scale, 4, cudaMemcpyDeviceToDevice, st), "copy w scale");
+      } else {
+        FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 1, aw, nullptr, nullptr, st), "amax w");
+        FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 1, 0, fw.amax + 1, fw.amax + 1, svw.wT, nullptr,
+                              (float*)svw.sw, nullptr, st),
+                  "cast w");
+      }
+    }
+    GemmProblem p{svx.xT, wq, ff, ff, 0, 0, svx.sx, svw.sw, 0, M, N, K, K, K, y, of32, N, 0, yam};
+    FP8T_TRY(fwd_gemm(p));
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {
+    const bool gw_hp = cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;   // X's column-scaled copy unused
+    float* axr = fw.amax;
+    float* axc = axr + M;
+    float* awr = axc + K;
+    float* awc = awr + N;
+    if (!cast_x) {   // X's row / column amax, codes and scales are already in fw / svx
+      FP8T_CUDA(cudaMemsetAsync(awr, 0, 4 * (N + K), st), "memset");
+      FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 6, nullptr, (uint32_t*)awr, (uint32_t*)awc, st), "amax w");
+      FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 5, awr, awc, fw.wq, svw.wT, fw.swr, (float*)svw.sw, st),
+                "cast w");
+      GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N, 0, yam};
+      return fwd_gemm(p);
+    }
+    FP8T_CUDA(cudaMemsetAsync(fw.amax, 0, 4 * (M + K + N + K), st), "memset");
+    // X and W in one amax launch and one cast launch where the shapes allow (the small weights of
+    // e.g. the wk/wv projections then cost no launch ramp and tail of their own); rowwise_gw_hp
+    // needs different scale modes for X and W, so it keeps separate launches
+    bool dual = false;
+    if (!gw_hp && xb && wb) {
+      const cudaError_t e = launch_amax_dual(x.ptr, M, K, x.ld, w.ptr, N, K, w.ld, 6, (uint32_t*)axr, (uint32_t*)axc,
+                                             (uint32_t*)awr, (uint32_t*)awc, st);
+      if (e != cudaErrorNotSupported) FP8T_CUDA(e, "amax x, w");
+      dual = e == cudaSuccess;
+    }
+    if (!dual) {
+      FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, gw_hp ? 2 : 6, nullptr, (uint32_t*)axr, (uint32_t*)axc, st),
+                "amax x");
+      FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 6, nullptr, (uint32_t*)awr, (uint32_t*)awc, st), "amax w");
+    }
+    // row-scaled codes for the forward GEMM; column-scaled codes written row-major for the
+    // backward GEMMs (read MN-major, no transposed copy)
+    if (!gw_hp && xb == wb) {
+      CastDual cd{};
+      cd.x[0] = x.ptr; cd.R[0] = M; cd.C[0] = K; cd.ld[0] = x.ld; cd.amax_q[0] = axr; cd.amax_t[0] = axc;
+      cd.q[0] = fw.xq; cd.qt[0] = svx.xT; cd.scale_q[0] = fw.sxr; cd.scale_t[0] = (float*)svx.sx;
+      cd.x[1] = w.ptr; cd.R[1] = N; cd.C[1] = K; cd.ld[1] = w.ld; cd.amax_q[1] = awr; cd.amax_t[1] = awc;
+      cd.q[1] = fw.wq; cd.qt[1] = svw.wT; cd.scale_q[1] = fw.swr; cd.scale_t[1] = (float*)svw.sw;
+      FP8T_CUDA(launch_cast_dual(cd, xb, ff, 2, 5, st), "cast x, w");
+    } else {
+      FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 2, gw_hp ? 0 : 5, axr, axc, fw.xq, gw_hp ? nullptr : svx.xT,
+                            fw.sxr, gw_hp ? nullptr : (float*)svx.sx, st),
+                "cast x");
+      FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 5, awr, awc, fw.wq, svw.wT, fw.swr, (float*)svw.sw, st),
+                "cast w");
+    }
+    GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N, 0, yam};
+    FP8T_TRY(fwd_gemm(p));
+  } else {
+    const bool rc = cfg->mx_round == FP8_MX_RCEIL, tr = mx_transposed();
+    if (cast_x)
+      FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, fw.xq, fw.sfx, svx.xT, (uint8_t*)svx.sx, st, tr),
+                "mx cast x");
+    // pre-gathered weight (fp8_fsdp_allgather_mx): its dim0 copy feeds this GEMM and its dim1 copy
+    // the backward, so nothing of W is cast or saved here
+    if (!w_fp8)
+      FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, fw.wq, fw.sfw, svw.wT, (uint8_t*)svw.sw, st, tr),
+                "mx cast w");
+    const uint8_t* wq = w_fp8 ? w_fp8->q : fw.wq;
+    const void* swp = w_fp8 ? w_fp8->scale : fw.sfw;
+    GemmProblem p{fw.xq, wq, ff, ff, 0, 0, fw.sfx, swp, 2, M, N, K, K, K, y, of32, N, 0, yam};
+    FP8T_TRY(fwd_gemm(p));
+  }
+  return FP8_OK;
+}
+
+
+extern "C" {
+
 size_t fp8_linear_saved_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t N, int64_t K) {
   if (!cfg) return 0;
   size_t b = 0;
@@ -741,107 +883,9 @@ fp8_status_t fp8_linear_fwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const fl
     return FP8_OK;
   }
 
-  Saved sv = carve_saved(cfg, M, N, K, saved, nullptr);
-  FwdWs fw = carve_fwd(cfg, M, N, K, ws, nullptr);
-
-  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
-    // row-major codes only: the backward GEMMs read them MN-major (no transposed copies)
-    uint32_t* ax = reinterpret_cast<uint32_t*>(fw.amax);
-    uint32_t* aw = ax + 1;
-    FP8T_CUDA(cudaMemsetAsync(ax, 0, 8, st), "memset");
-    const float* axp = x_amax ? x_amax : fw.amax;
-    const uint8_t* wq = sv.wT;
-    // amax X and W by one launch, then X and W cast by one launch (measured on c2: casts 0.165 ->
-    // 0.158 ms per step); knob tw_dual = 0 keeps four launches (X's cast right after its amax).
-    // x_amax: amax(X) precomputed by X's producer (e.g. the previous layer's epilogue) -> no amax pass
-    const bool tw_dual = knob(KNOB_TW_DUAL) == 1;
-    if (tw_dual && !w_fp8 && xb == wb) {
-      cudaError_t e = cudaErrorNotSupported;
-      if (!x_amax && x.ld == K && w.ld == K)
-        e = launch_amax_flat_dual(x.ptr, M * K, ax, w.ptr, N * K, aw, xb, st);
-      if (e != cudaErrorNotSupported) {
-        FP8T_CUDA(e, "amax x, w");
-      } else {
-        if (!x_amax) FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
-        FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 1, aw, nullptr, nullptr, st), "amax w");
-      }
-      CastDual cd{};
-      cd.x[0] = x.ptr; cd.R[0] = M; cd.C[0] = K; cd.ld[0] = x.ld; cd.amax_q[0] = axp; cd.amax_t[0] = axp;
-      cd.q[0] = sv.xT; cd.scale_q[0] = (float*)sv.sx;
-      cd.x[1] = w.ptr; cd.R[1] = N; cd.C[1] = K; cd.ld[1] = w.ld; cd.amax_q[1] = fw.amax + 1;
-      cd.amax_t[1] = fw.amax + 1; cd.q[1] = sv.wT; cd.scale_q[1] = (float*)sv.sw;
-      FP8T_CUDA(launch_cast_dual(cd, xb, ff, 1, 0, st), "cast x, w");
-    } else {
-      if (!x_amax) FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, 1, ax, nullptr, nullptr, st), "amax x");
-      FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 1, 0, axp, axp, sv.xT, nullptr, (float*)sv.sx, nullptr, st),
-                "cast x");
-      if (w_fp8) {
-        wq = w_fp8->q;
-        FP8T_CUDA(cudaMemcpyAsync(sv.sw, w_fp8->scale, 4, cudaMemcpyDeviceToDevice, st), "copy w scale");
-      } else {
-        FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 1, aw, nullptr, nullptr, st), "amax w");
-        FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 1, 0, fw.amax + 1, fw.amax + 1, sv.wT, nullptr,
-                              (float*)sv.sw, nullptr, st),
-                  "cast w");
-      }
-    }
-    GemmProblem p{sv.xT, wq, ff, ff, 0, 0, sv.sx, sv.sw, 0, M, N, K, K, K, y, of32, N, 0, yam};
-    FP8T_TRY(fwd_gemm(p));
-  } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {
-    const bool gw_hp = cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;   // X's column-scaled copy unused
-    float* axr = fw.amax;
-    float* axc = axr + M;
-    float* awr = axc + K;
-    float* awc = awr + N;
-    FP8T_CUDA(cudaMemsetAsync(fw.amax, 0, 4 * (M + K + N + K), st), "memset");
-    // X and W in one amax launch and one cast launch where the shapes allow (the small weights of
-    // e.g. the wk/wv projections then cost no launch ramp and tail of their own); rowwise_gw_hp
-    // needs different scale modes for X and W, so it keeps separate launches
-    bool dual = false;
-    if (!gw_hp && xb && wb) {
-      const cudaError_t e = launch_amax_dual(x.ptr, M, K, x.ld, w.ptr, N, K, w.ld, 6, (uint32_t*)axr, (uint32_t*)axc,
-                                             (uint32_t*)awr, (uint32_t*)awc, st);
-      if (e != cudaErrorNotSupported) FP8T_CUDA(e, "amax x, w");
-      dual = e == cudaSuccess;
-    }
-    if (!dual) {
-      FP8T_CUDA(launch_amax(x.ptr, xb, M, K, x.ld, gw_hp ? 2 : 6, nullptr, (uint32_t*)axr, (uint32_t*)axc, st),
-                "amax x");
-      FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 6, nullptr, (uint32_t*)awr, (uint32_t*)awc, st), "amax w");
-    }
-    // row-scaled codes for the forward GEMM; column-scaled codes written row-major for the
-    // backward GEMMs (read MN-major, no transposed copy)
-    if (!gw_hp && xb == wb) {
-      CastDual cd{};
-      cd.x[0] = x.ptr; cd.R[0] = M; cd.C[0] = K; cd.ld[0] = x.ld; cd.amax_q[0] = axr; cd.amax_t[0] = axc;
-      cd.q[0] = fw.xq; cd.qt[0] = sv.xT; cd.scale_q[0] = fw.sxr; cd.scale_t[0] = (float*)sv.sx;
-      cd.x[1] = w.ptr; cd.R[1] = N; cd.C[1] = K; cd.ld[1] = w.ld; cd.amax_q[1] = awr; cd.amax_t[1] = awc;
-      cd.q[1] = fw.wq; cd.qt[1] = sv.wT; cd.scale_q[1] = fw.swr; cd.scale_t[1] = (float*)sv.sw;
-      FP8T_CUDA(launch_cast_dual(cd, xb, ff, 2, 5, st), "cast x, w");
-    } else {
-      FP8T_CUDA(launch_cast(x.ptr, xb, ff, M, K, x.ld, 2, gw_hp ? 0 : 5, axr, axc, fw.xq, gw_hp ? nullptr : sv.xT,
-                            fw.sxr, gw_hp ? nullptr : (float*)sv.sx, st),
-                "cast x");
-      FP8T_CUDA(launch_cast(w.ptr, wb, ff, N, K, w.ld, 2, 5, awr, awc, fw.wq, sv.wT, fw.swr, (float*)sv.sw, st),
-                "cast w");
-    }
-    GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N, 0, yam};
-    FP8T_TRY(fwd_gemm(p));
-  } else {
-    const bool rc = cfg->mx_round == FP8_MX_RCEIL, tr = mx_transposed();
-    FP8T_CUDA(launch_mx_cast(x.ptr, xb, ff, rc, M, K, x.ld, fw.xq, fw.sfx, sv.xT, (uint8_t*)sv.sx, st, tr),
-              "mx cast x");
-    // pre-gathered weight (fp8_fsdp_allgather_mx): its dim0 copy feeds this GEMM and its dim1 copy
-    // the backward, so nothing of W is cast or saved here
-    if (!w_fp8)
-      FP8T_CUDA(launch_mx_cast(w.ptr, wb, ff, rc, N, K, w.ld, fw.wq, fw.sfw, sv.wT, (uint8_t*)sv.sw, st, tr),
-                "mx cast w");
-    const uint8_t* wq = w_fp8 ? w_fp8->q : fw.wq;
-    const void* swp = w_fp8 ? w_fp8->scale : fw.sfw;
-    GemmProblem p{fw.xq, wq, ff, ff, 0, 0, fw.sfx, swp, 2, M, N, K, K, K, y, of32, N, 0, yam};
-    FP8T_TRY(fwd_gemm(p));
-  }
-  return FP8_OK;
+  const Saved sv = carve_saved(cfg, M, N, K, saved, nullptr);
+  const FwdWs fw = carve_fwd(cfg, M, N, K, ws, nullptr);
+  return linear_fwd_train(cfg, x, x_amax, w, w_fp8, y, y_amax, sv, sv, fw, true, st);
 }
 
 fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x, const void* saved,
@@ -851,7 +895,65 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x
 
 static fp8_status_t linear_bwd_impl(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
                                     const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax, void* dw,
-                                    void* ws, size_t ws_bytes, void* stream, fp8_p2p_t rs_win, int rs_nranks);
+                                    void* ws, size_t ws_bytes, void* stream, fp8_p2p_t rs_win, int rs_nranks,
+                                    const void* saved_x = nullptr, int64_t n_x = 0);
+
+// Linears sharing one input (see fp8train.h): X is cast once by member 0, members 1..n-1 cast W only.
+fp8_status_t fp8_linear_fwd_shared(const fp8_linear_cfg_t* cfg, fp8_hp_t x, int n, const fp8_hp_t* w, void* const* y,
+                                   void* const* saved, void* ws, size_t ws_bytes, void* stream) {
+  FP8T_TRY(check_hp(x, "x"));
+  if (n < 1 || n > FP8_SHARED_MAX) return fail(FP8_EINVAL, "n must be in [1, %d]", FP8_SHARED_MAX);
+  if (!w || !y || !saved) return fail(FP8_EINVAL, "w / y / saved: null array");
+  const int64_t M = x.rows, K = x.cols;
+  int64_t nmax = 0;
+  for (int i = 0; i < n; ++i) {   // every argument is checked before the first launch
+    FP8T_TRY(check_hp(w[i], "w[i]"));
+    if (w[i].cols != K) return fail(FP8_EINVAL, "w[%d].cols != x.cols", i);
+    if (w[i].dtype != x.dtype) return fail(FP8_EINVAL, "w[%d].dtype != x.dtype", i);
+    FP8T_TRY(check_cfg(cfg, M, w[i].rows, K));
+    FP8T_TRY(check_ptr(y[i], "y[i]"));
+    FP8T_TRY(check_ptr(saved[i], "saved[i]"));
+    nmax = w[i].rows > nmax ? w[i].rows : nmax;
+  }
+  FP8T_TRY(check_ptr(ws, "ws"));
+  const size_t need = fp8_linear_workspace_bytes(cfg, M, nmax, K);
+  if (ws_bytes < need) return fail(FP8_EWORKSPACE, "workspace too small (%zu < %zu)", ws_bytes, need);
+  cudaStream_t st = S(stream);
+  // one carve of ws for the whole group (sized for the widest member): X's forward codes and row
+  // scales / E8M0 stay where member 0 wrote them; W's forward operand is rewritten per member
+  // (stream order: member i's GEMM has read it before member i+1's cast runs)
+  const FwdWs fw = carve_fwd(cfg, M, nmax, K, ws, nullptr);
+  const Saved sv0 = carve_saved(cfg, M, w[0].rows, K, saved[0], nullptr);
+  for (int i = 0; i < n; ++i) {
+    const Saved svi = i ? carve_saved(cfg, M, w[i].rows, K, saved[i], nullptr) : sv0;
+    FP8T_TRY(linear_fwd_train(cfg, x, nullptr, w[i], nullptr, y[i], nullptr, sv0, svi, fw, i == 0, st));
+  }
+  return FP8_OK;
+}
+
+fp8_status_t fp8_linear_bwd_shared(const fp8_linear_cfg_t* cfg, int n, const fp8_hp_t* dy, fp8_hp_t x,
+                                   const void* const* saved, void* const* dx, void* const* dw, void* ws,
+                                   size_t ws_bytes, void* stream) {
+  if (n < 1 || n > FP8_SHARED_MAX) return fail(FP8_EINVAL, "n must be in [1, %d]", FP8_SHARED_MAX);
+  if (!dy || !saved) return fail(FP8_EINVAL, "dy / saved: null array");
+  const bool gw_hp = cfg && cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;
+  for (int i = 0; i < n; ++i) {   // every argument is checked before the first launch
+    FP8T_TRY(check_hp(dy[i], "dy[i]"));
+    if (dy[i].rows != x.rows || dy[i].dtype != dy[0].dtype) return fail(FP8_EINVAL, "dy[%d]: rows / dtype differ", i);
+    FP8T_TRY(check_cfg(cfg, x.rows, dy[i].cols, x.cols));
+    FP8T_TRY(check_ptr(saved[i], "saved[i]"));
+    if (dx && dx[i]) FP8T_TRY(check_ptr(dx[i], "dx[i]"));
+    if (dw && dw[i]) FP8T_TRY(check_ptr(dw[i], "dw[i]"));
+    if (ws_bytes < fp8_linear_workspace_bytes(cfg, x.rows, dy[i].cols, x.cols))
+      return fail(FP8_EWORKSPACE, "workspace too small for member %d", i);
+  }
+  FP8T_TRY(check_hp(x, "x", gw_hp && dw));
+  for (int i = 0; i < n; ++i)
+    FP8T_TRY(linear_bwd_impl(cfg, dy[i], nullptr, x, saved[i], nullptr, dx ? dx[i] : nullptr, nullptr,
+                             dw ? dw[i] : nullptr, ws, ws_bytes, stream, nullptr, 1, saved[0], dy[0].cols));
+  return FP8_OK;
+}
+
 
 fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
                                const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax, void* dw,
@@ -871,7 +973,8 @@ fp8_status_t fp8_linear_bwd_rs(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_
 
 static fp8_status_t linear_bwd_impl(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
                                     const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax, void* dw,
-                                    void* ws, size_t ws_bytes, void* stream, fp8_p2p_t rs_win, int rs_nranks) {
+                                    void* ws, size_t ws_bytes, void* stream, fp8_p2p_t rs_win, int rs_nranks,
+                                    const void* saved_x, int64_t n_x) {
   FP8T_TRY(check_hp(dy, "dy"));
   const int64_t M = dy.rows, N = dy.cols, K = x.cols;
   const bool gw_hp = cfg && cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;
@@ -896,6 +999,11 @@ static fp8_status_t linear_bwd_impl(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, co
   const int ff = cfg->fmt_fwd, fg = cfg->fmt_grad;
   uint32_t* dxam = dx ? reinterpret_cast<uint32_t*>(dx_amax) : nullptr;
   Saved sv = carve_saved(cfg, M, N, K, const_cast<void*>(saved), nullptr);
+  if (saved_x) {   // shared-input group: X's backward operand lives in the first member's buffer
+    const Saved s0 = carve_saved(cfg, M, n_x, K, const_cast<void*>(saved_x), nullptr);
+    sv.xT = s0.xT;
+    sv.sx = s0.sx;
+  }
   BwdWs bw = carve_bwd(cfg, M, N, ws, nullptr);
   const int of32 = cfg->out_dtype == FP8_DT_F32;
   int mode;

@@ -260,6 +260,56 @@ class LinearPlan:
         return dx, dw
 
 
+class SharedInputPlan:
+    """Float8Linears that read the same input X (fp8_linear_fwd_shared / _bwd_shared): e.g. wq/wk/wv
+    or w1/w3 of a Llama layer.  X is cast once; outputs and saved bytes equal those of separate
+    LinearPlan calls.  One workspace for the group (sized for the widest member)."""
+
+    def __init__(self, M, Ns, K, recipe="tensorwise", fmt_fwd="e4m3", fmt_grad="e5m2", mx_round="floor",
+                 out_dtype=torch.bfloat16, device="cuda"):
+        self.M, self.Ns, self.K = M, list(Ns), K
+        self.out_dtype = out_dtype
+        self.cfg = L.LinearCfg(RECIPES[recipe], FORMATS[fmt_fwd], FORMATS[fmt_grad], MX_ROUND[mx_round],
+                               L.DT_F32 if out_dtype == torch.float32 else L.DT_BF16)
+        self.saved_bytes = [L.lib.fp8_linear_saved_bytes(ctypes.byref(self.cfg), M, N, K) for N in self.Ns]
+        self.ws_bytes = L.lib.fp8_linear_workspace_bytes(ctypes.byref(self.cfg), M, max(self.Ns), K)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
+
+    def new_saved(self, device="cuda"):
+        return [torch.empty(b, dtype=torch.uint8, device=device) for b in self.saved_bytes]
+
+    @staticmethod
+    def _ptrs(ts):
+        return (ctypes.c_void_p * len(ts))(*[_ptr(t) for t in ts])
+
+    def forward(self, x, ws_, saved, ys=None, stream=None):
+        """x [M,K]; ws_: list of weights [N_i, K]; saved: list from new_saved(); returns the list of Y_i."""
+        n = len(self.Ns)
+        if ys is None:
+            ys = [torch.empty((self.M, N), dtype=self.out_dtype, device=x.device) for N in self.Ns]
+        whs = (L.HP * n)(*[hp(w) for w in ws_])
+        L.check(L.lib.fp8_linear_fwd_shared(ctypes.byref(self.cfg), hp(x), n, whs, self._ptrs(ys), self._ptrs(saved),
+                                            _ptr(self.ws), self.ws_bytes, _stream(stream)), "fp8_linear_fwd_shared")
+        return ys
+
+    def backward(self, dys, saved, dxs=None, dws=None, x=None, want_dx=True, want_dw=True, stream=None):
+        """dys: list of dY_i [M, N_i]; returns (list of dX_i [M,K], list of dW_i [N_i,K]) -- the caller
+        sums the dX_i (as autograd does for separate linears)."""
+        n = len(self.Ns)
+        dev = dys[0].device
+        if want_dx and dxs is None:
+            dxs = [torch.empty((self.M, self.K), dtype=self.out_dtype, device=dev) for _ in range(n)]
+        if want_dw and dws is None:
+            dws = [torch.empty((N, self.K), dtype=self.out_dtype, device=dev) for N in self.Ns]
+        dyh = (L.HP * n)(*[hp(d) for d in dys])
+        xh = hp(x) if x is not None else L.HP(None, L.DT_BF16, self.M, self.K, self.K)
+        L.check(L.lib.fp8_linear_bwd_shared(ctypes.byref(self.cfg), n, dyh, xh, self._ptrs(saved),
+                                            self._ptrs(dxs) if want_dx else None,
+                                            self._ptrs(dws) if want_dw else None, _ptr(self.ws), self.ws_bytes,
+                                            _stream(stream)), "fp8_linear_bwd_shared")
+        return dxs, dws
+
+
 class GroupedPlan:
     """MoE scaled grouped GEMM (fp8_grouped_linear_fwd / _bwd): E experts with
     weights stacked [E*N, K], tokens [T, K] sorted by expert, device int32 offsets [E+1]."""

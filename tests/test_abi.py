@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol(L):
 
 
 def test_abi_version(L):
-    assert L.lib.fp8_abi_version() == 6
+    assert L.lib.fp8_abi_version() == 7
 
 
 def test_sizes_host_only(L):
@@ -143,6 +143,22 @@ def test_argument_errors_return_before_any_launch(L):
     t8 = L.Tensor8(A, A, A, A, None, None, L.E4M3, L.GRAN_MX32, 256, 256)
     assert L.lib.fp8_fsdp_allgather_mx(ctypes.c_void_p(A), hp(128, 256), L.MX_FLOOR, ctypes.byref(t8), ws, 1 << 20,
                                        None) == L.FP8_EUNSUPPORTED
+    # shared-input linears: member count, a member whose K differs, a too-small workspace (sized for
+    # the widest member), a dY whose rows differ -- each caught before the first launch
+    cfg.recipe = L.RECIPE_ROWWISE
+    ptrs = (ctypes.c_void_p * 3)(A, A, A)
+    ws3 = (L.HP * 3)(hp(256, 128), hp(512, 128), hp(128, 128))
+    fwd = lambda n, w, wsb: L.lib.fp8_linear_fwd_shared(ctypes.byref(cfg), hp(256, 128), n, w, ptrs, ptrs, ws, wsb,  # noqa: E731
+                                                        None)
+    assert fwd(0, ws3, 1 << 40) == L.FP8_EINVAL
+    assert fwd(9, ws3, 1 << 40) == L.FP8_EINVAL
+    assert fwd(3, (L.HP * 3)(hp(256, 128), hp(512, 144), hp(128, 128)), 1 << 40) == L.FP8_EINVAL
+    need = L.lib.fp8_linear_workspace_bytes(ctypes.byref(cfg), 256, 512, 128)
+    assert need > L.lib.fp8_linear_workspace_bytes(ctypes.byref(cfg), 256, 256, 128)
+    assert fwd(3, ws3, need - 1) == L.FP8_EWORKSPACE
+    dys = (L.HP * 2)(hp(256, 256), hp(272, 512))
+    assert L.lib.fp8_linear_bwd_shared(ctypes.byref(cfg), 2, dys, hp(256, 128), ptrs, ptrs, ptrs, ws, 1 << 40,
+                                       None) == L.FP8_EINVAL
 
 
 def test_knobs_host_only(L):

@@ -1592,3 +1592,61 @@ def test_amax_tensor_kernels(shape, dtype, bulk, knob):
     got = ops.amax(X, "tensor")
     torch.cuda.synchronize()
     assert _bits(_np(got))[0] == _bits(fp8.amax(_np(X.float()))).reshape(-1)[0]
+
+
+SHARED_CASES = [("tensorwise", {}), ("tensorwise", {"tw_dual": 0}), ("rowwise", {}), ("rowwise", {"amax_tile_tma": 0}),
+                ("rowwise_gw_hp", {}), ("mxfp8", {}), ("mxfp8", {"mx_transposed": 1})]
+
+
+@pytest.mark.parametrize("M,K,Ns", [(384, 512, (640, 128, 256)), (256, 384, (128, 512)), (384, 256, (384,)),
+                                    (400, 528, (272, 400, 144))], ids=["qkv", "w13", "single", "ragged"])
+@pytest.mark.parametrize("recipe,knobs", SHARED_CASES,
+                         ids=[r + ("-" + "-".join(f"{k}{v}" for k, v in kn.items()) if kn else "") for r, kn in
+                              SHARED_CASES])
+def test_linear_shared_input_matches_separate(recipe, knobs, M, K, Ns, knob):
+    """fp8_linear_fwd_shared / _bwd_shared (linears reading one X: wq/wk/wv, w1/w3) write exactly what
+    separate fp8_linear_fwd / fp8_linear_bwd calls write: Y_i, dX_i, dW_i bit-identical, X's saved
+    backward operand (member 0's buffer) and every member's W operand byte-identical -- X's scales
+    depend on X alone (Appendix A), so casting it once changes nothing.  Widest
+    member first and not first, ragged sizes; Y_i also within the oracle's bound."""
+    if recipe == "mxfp8" and (M % 128 or K % 128 or any(n % 128 for n in Ns)):
+        pytest.skip("mxfp8 needs 128-multiples")
+    for k, v in knobs.items():
+        knob(k, v)
+    cfgname = {"tensorwise": "c2", "rowwise": "c3", "rowwise_gw_hp": "c3", "mxfp8": "c4"}[recipe]
+    x = synth.linear_inputs(cfgname, M, Ns[0], K, seed=21)[0]
+    ws_, dys = [], []
+    for i, N in enumerate(Ns):
+        _, w, dy = synth.linear_inputs(cfgname, M, N, K, seed=31 + i)
+        ws_.append(w)
+        dys.append(dy)
+    X = _dev(x, torch.bfloat16)
+    W = [_dev(w, torch.bfloat16) for w in ws_]
+    G = [_dev(d, torch.bfloat16) for d in dys]
+    # separate linears
+    sep = []
+    for i, N in enumerate(Ns):
+        plan = ops.LinearPlan(M, N, K, recipe=recipe)
+        saved = plan.new_saved()
+        y = plan.forward(X, W[i], saved)
+        dx, dw = plan.backward(G[i], saved, x=X)
+        torch.cuda.synchronize()
+        b = plan.buffers(saved)
+        sep.append(dict(y=y, dx=dx, dw=dw, b={k: (v.clone() if torch.is_tensor(v) else v) for k, v in b.items()}))
+    # one shared-input group
+    sp = ops.SharedInputPlan(M, Ns, K, recipe=recipe)
+    saved = sp.new_saved()
+    ys = sp.forward(X, W, saved)
+    dxs, dws = sp.backward(G, saved, x=X)
+    torch.cuda.synchronize()
+    for i, N in enumerate(Ns):
+        _eq(f"y[{i}]", ys[i].view(torch.int16), _np(sep[i]["y"].view(torch.int16)))
+        _eq(f"dx[{i}]", dxs[i].view(torch.int16), _np(sep[i]["dx"].view(torch.int16)))
+        _eq(f"dw[{i}]", dws[i].view(torch.int16), _np(sep[i]["dw"].view(torch.int16)))
+        b = ops.LinearPlan(M, N, K, recipe=recipe).buffers(saved[i])
+        for key in ("w_bwd", "w_bwd_scale") + (("x_bwd", "x_bwd_scale") if i == 0 else ()):
+            if sep[i]["b"][key] is not None:
+                _eq(f"saved[{i}].{key}", b[key], _np(sep[i]["b"][key]))
+        yo, bd, _ = olin.forward(x, ws_[i], recipe)
+        err = np.abs(_np(ys[i].float()).astype(np.float64) - yo)
+        assert np.all(err <= 1e-2 * bd + 1e-30), f"y[{i}]: max err/bound {np.max(err / (bd + 1e-30)):.3e}"
