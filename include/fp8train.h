@@ -321,15 +321,21 @@ fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const f
  *   fwd: x [M,K]; w: HOST array of n weights [N_i, K] (same dtype as x); y: HOST array of n
  *     outputs [M, N_i] (out_dtype, dense); saved: HOST array of n buffers of
  *     fp8_linear_saved_bytes(cfg, M, N_i, K) bytes -- saved[0] holds X's backward operand,
- *     saved[i > 0] only W_i's; ws >= fp8_linear_workspace_bytes(cfg, M, max N_i, K) bytes.
+ *     saved[i > 0] only W_i's; ws >= fp8_linear_shared_workspace_bytes(cfg, M, K, n, N) bytes (every
+ *     member's forward W operand and backward dY operands side by side: the members' GEMMs -- Y_i in
+ *     the forward, dX_i and dW_i in the backward -- run as ONE persistent launch per pass, up to 6
+ *     problems per launch, so the small members (wk, wv) have no wave tail of their own).
  *   bwd: dy: HOST array of n [M, N_i]; x as for fp8_linear_bwd (data read by rowwise_gw_hp only);
  *     saved: the same array the forward wrote (all n, saved[0] first); dx / dw: HOST arrays of n
  *     outputs or NULL, entries may be NULL (dX_i is per member: summing the members' dX_i is the
- *     caller's -- autograd's -- job, as for separate linears); ws as for the forward.
+ *     caller's -- autograd's -- job, as for separate linears); ws as for the forward (the same buffer
+ *     may serve both passes).
  *   1 <= n <= FP8_SHARED_MAX.  No pre-cast weights (w_fp8) and no amax hand-over here.  All
  *   arguments are validated before the first launch.
  * ------------------------------------------------------------------------- */
 #define FP8_SHARED_MAX 8
+/* N: HOST int64[n], the members' output widths N_i.  0 for bad arguments. */
+size_t fp8_linear_shared_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t K, int n, const int64_t* N);
 fp8_status_t fp8_linear_fwd_shared(const fp8_linear_cfg_t* cfg, fp8_hp_t x, int n, const fp8_hp_t* w,
                                    void* const* y, void* const* saved, void* ws, size_t ws_bytes, void* stream);
 fp8_status_t fp8_linear_bwd_shared(const fp8_linear_cfg_t* cfg, int n, const fp8_hp_t* dy, fp8_hp_t x,

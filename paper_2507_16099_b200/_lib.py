@@ -81,6 +81,8 @@ SIGNATURES = {
                                      _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
     "fp8_linear_bwd_ex": (_c.c_int, [_c.POINTER(LinearCfg), HP, _c.c_void_p, HP, _c.c_void_p, _c.POINTER(Tensor8),
                                      _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
+    "fp8_linear_shared_workspace_bytes": (_c.c_size_t, [_c.POINTER(LinearCfg), _c.c_int64, _c.c_int64, _c.c_int,
+                                                        _c.POINTER(_c.c_int64)]),
     "fp8_linear_fwd_shared": (_c.c_int, [_c.POINTER(LinearCfg), HP, _c.c_int, _c.POINTER(HP), _c.POINTER(_c.c_void_p),
                                          _c.POINTER(_c.c_void_p), _c.c_void_p, _c.c_size_t, _c.c_void_p]),
     "fp8_linear_bwd_shared": (_c.c_int, [_c.POINTER(LinearCfg), _c.c_int, _c.POINTER(HP), HP, _c.POINTER(_c.c_void_p),

@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -607,16 +608,24 @@ fp8_status_t check_w_fp8(const fp8_linear_cfg_t* cfg, const fp8_tensor_t* w_fp8,
 // fp8_linear_fwd_shared).  X's operands go to / come from `svx` (its backward copy) and `fw` (its
 // forward copy, row scales / E8M0), W's to `svw` and `fw`.  cast_x = false: X's amax and casts were
 // already written by the previous member of a shared-input group (same x, same fw / svx), so only
-// W is cast here -- the bytes are the ones a separate fp8_linear_fwd would write.
+// W is cast here -- the bytes are the ones a separate fp8_linear_fwd would write.  W's forward
+// operand goes to fw.wq / fw.swr / fw.sfw (a group passes each member its own slice) and its amax to
+// the fw.amax slots after X's (reused member after member: each W amax is consumed by W's cast).
 static fp8_status_t linear_fwd_train(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const float* x_amax, fp8_hp_t w,
                                      const fp8_tensor_t* w_fp8, void* y, float* y_amax, const Saved& svx,
-                                     const Saved& svw, const FwdWs& fw, bool cast_x, cudaStream_t st) {
+                                     const Saved& svw, const FwdWs& fw, bool cast_x, cudaStream_t st,
+                                     GemmProblem* defer = nullptr) {
   const int64_t M = x.rows, K = x.cols, N = w.rows;
   const bool xb = x.dtype == FP8_DT_BF16, wb = w.dtype == FP8_DT_BF16;
   const int ff = cfg->fmt_fwd;
   const int of32 = cfg->out_dtype == FP8_DT_F32;
   uint32_t* yam = reinterpret_cast<uint32_t*>(y_amax);
+  // defer: hand the GEMM back to the caller (a shared-input group launches its members' GEMMs together)
   auto fwd_gemm = [&](const GemmProblem& p) -> fp8_status_t {
+    if (defer) {
+      *defer = p;
+      return FP8_OK;
+    }
     if (yam) FP8T_CUDA(cudaMemsetAsync(yam, 0, 4, st), "memset y_amax");
     FP8T_CUDA(launch_gemm(p, st), "gemm fwd");
     return FP8_OK;
@@ -896,39 +905,141 @@ fp8_status_t fp8_linear_bwd(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_t x
 static fp8_status_t linear_bwd_impl(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
                                     const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax, void* dw,
                                     void* ws, size_t ws_bytes, void* stream, fp8_p2p_t rs_win, int rs_nranks,
-                                    const void* saved_x = nullptr, int64_t n_x = 0);
+                                    const void* saved_x = nullptr, int64_t n_x = 0, const BwdWs* bw_in = nullptr,
+                                    std::vector<GemmProblem>* defer = nullptr);
 
-// Linears sharing one input (see fp8train.h): X is cast once by member 0, members 1..n-1 cast W only.
+// Linears sharing one input (see fp8train.h): X is cast once by member 0, members 1..n-1 cast W only;
+// every member's GEMMs run in one persistent launch (up to GEMM_MAX_PROBS problems per launch).
+namespace {
+
+struct SharedDims {
+  int64_t M = 0, K = 0, nsum = 0, nmax = 0;
+  int64_t pre[FP8_SHARED_MAX + 1] = {};   // prefix sums of N_i
+};
+
+// Group backward workspace: every member's dY operands side by side (they must all be resident when the
+// group's GEMMs run); the amax scratch is reused member after member (each dY amax feeds its own cast).
+struct BwdGroupWs {
+  uint8_t* g; uint8_t* gT;   // [M, nsum] each, member i at column block pre[i] (as M x N_i arrays)
+  float* amax;               // tensorwise [1] | rowwise [M + nmax]
+  void* sg; void* sgT;       // tensorwise float[n] | rowwise float[n * M], float[nsum] | mx E8M0 [M * nsum / 32] x 2
+};
+BwdGroupWs carve_bwd_group(const fp8_linear_cfg_t* cfg, const SharedDims& d, int n, void* base, size_t* bytes) {
+  Carve c(base);
+  BwdGroupWs w{};
+  const int64_t M = d.M, S = d.nsum;
+  w.g = c.take<uint8_t>((size_t)M * S);
+  w.gT = cfg->recipe == FP8_RECIPE_TENSORWISE ? nullptr : c.take<uint8_t>((size_t)M * S);
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    w.amax = c.take<float>(4);
+    w.sg = c.take<float>(4 * n);
+    w.sgT = w.sg;
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {
+    w.amax = c.take<float>(4 * (M + d.nmax));
+    w.sg = c.take<float>(4 * (size_t)n * M);
+    w.sgT = c.take<float>(4 * S);
+  } else {
+    w.sg = c.take<uint8_t>((size_t)M * S / 32);
+    w.sgT = c.take<uint8_t>((size_t)M * S / 32);
+  }
+  if (bytes) *bytes = c.off;
+  return w;
+}
+BwdWs bwd_member(const fp8_linear_cfg_t* cfg, const BwdGroupWs& w, const SharedDims& d, int i) {
+  const int64_t M = d.M, off = d.pre[i];
+  BwdWs b{};
+  b.g = w.g + M * off;
+  b.gT = w.gT ? w.gT + M * off : nullptr;
+  b.amax = w.amax;
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
+    b.sg = b.sgT = static_cast<float*>(w.sg) + i;
+  } else if (cfg->recipe == FP8_RECIPE_ROWWISE || cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP) {
+    b.sg = static_cast<float*>(w.sg) + (size_t)i * M;
+    b.sgT = static_cast<float*>(w.sgT) + off;
+  } else {
+    b.sg = static_cast<uint8_t*>(w.sg) + M * off / 32;
+    b.sgT = static_cast<uint8_t*>(w.sgT) + M * off / 32;
+  }
+  return b;
+}
+// Group forward workspace = carve_fwd for N = nsum: X's operands once, W_i's forward operands at row pre[i].
+FwdWs fwd_member(const fp8_linear_cfg_t* cfg, const FwdWs& f, const SharedDims& d, int i) {
+  FwdWs m = f;
+  const int64_t off = d.pre[i];
+  if (cfg->recipe == FP8_RECIPE_TENSORWISE) return m;   // W's codes and scale live in its saved buffer
+  m.wq = f.wq + off * d.K;
+  if (cfg->recipe == FP8_RECIPE_MXFP8) m.sfw = f.sfw + off * d.K / 32;
+  else m.swr = f.swr + off;
+  return m;
+}
+size_t shared_ws_bytes(const fp8_linear_cfg_t* cfg, const SharedDims& d, int n) {
+  size_t f = 0, b = 0;
+  carve_fwd(cfg, d.M, d.nsum, d.K, nullptr, &f);
+  carve_bwd_group(cfg, d, n, nullptr, &b);
+  return f > b ? f : b;
+}
+// Launch a group's GEMM problems: FP8 and BF16 (rowwise_gw_hp dW) kinds apart, GEMM_MAX_PROBS per launch.
+fp8_status_t launch_group(const std::vector<GemmProblem>& ps, cudaStream_t st) {
+  for (int bf = 0; bf < 2; ++bf) {
+    std::vector<GemmProblem> q;
+    for (const GemmProblem& p : ps)
+      if (p.bf16_in == bf) q.push_back(p);
+    for (size_t i = 0; i < q.size(); i += GEMM_MAX_PROBS) {
+      const int n = (int)std::min(q.size() - i, (size_t)GEMM_MAX_PROBS);
+      FP8T_CUDA(launch_gemms(q.data() + i, n, st), "shared-input group gemms");
+    }
+  }
+  return FP8_OK;
+}
+
+}  // namespace
+
+size_t fp8_linear_shared_workspace_bytes(const fp8_linear_cfg_t* cfg, int64_t M, int64_t K, int n, const int64_t* N) {
+  if (!cfg || !N || n < 1 || n > FP8_SHARED_MAX) return 0;
+  SharedDims d;
+  d.M = M;
+  d.K = K;
+  for (int i = 0; i < n; ++i) {
+    d.pre[i + 1] = d.pre[i] + N[i];
+    d.nmax = N[i] > d.nmax ? N[i] : d.nmax;
+  }
+  d.nsum = d.pre[n];
+  return shared_ws_bytes(cfg, d, n);
+}
+
 fp8_status_t fp8_linear_fwd_shared(const fp8_linear_cfg_t* cfg, fp8_hp_t x, int n, const fp8_hp_t* w, void* const* y,
                                    void* const* saved, void* ws, size_t ws_bytes, void* stream) {
   FP8T_TRY(check_hp(x, "x"));
   if (n < 1 || n > FP8_SHARED_MAX) return fail(FP8_EINVAL, "n must be in [1, %d]", FP8_SHARED_MAX);
   if (!w || !y || !saved) return fail(FP8_EINVAL, "w / y / saved: null array");
-  const int64_t M = x.rows, K = x.cols;
-  int64_t nmax = 0;
+  SharedDims d;
+  d.M = x.rows;
+  d.K = x.cols;
   for (int i = 0; i < n; ++i) {   // every argument is checked before the first launch
     FP8T_TRY(check_hp(w[i], "w[i]"));
-    if (w[i].cols != K) return fail(FP8_EINVAL, "w[%d].cols != x.cols", i);
+    if (w[i].cols != d.K) return fail(FP8_EINVAL, "w[%d].cols != x.cols", i);
     if (w[i].dtype != x.dtype) return fail(FP8_EINVAL, "w[%d].dtype != x.dtype", i);
-    FP8T_TRY(check_cfg(cfg, M, w[i].rows, K));
+    FP8T_TRY(check_cfg(cfg, d.M, w[i].rows, d.K));
     FP8T_TRY(check_ptr(y[i], "y[i]"));
     FP8T_TRY(check_ptr(saved[i], "saved[i]"));
-    nmax = w[i].rows > nmax ? w[i].rows : nmax;
+    d.pre[i + 1] = d.pre[i] + w[i].rows;
+    d.nmax = w[i].rows > d.nmax ? w[i].rows : d.nmax;
   }
+  d.nsum = d.pre[n];
   FP8T_TRY(check_ptr(ws, "ws"));
-  const size_t need = fp8_linear_workspace_bytes(cfg, M, nmax, K);
+  const size_t need = shared_ws_bytes(cfg, d, n);
   if (ws_bytes < need) return fail(FP8_EWORKSPACE, "workspace too small (%zu < %zu)", ws_bytes, need);
   cudaStream_t st = S(stream);
-  // one carve of ws for the whole group (sized for the widest member): X's forward codes and row
-  // scales / E8M0 stay where member 0 wrote them; W's forward operand is rewritten per member
-  // (stream order: member i's GEMM has read it before member i+1's cast runs)
-  const FwdWs fw = carve_fwd(cfg, M, nmax, K, ws, nullptr);
-  const Saved sv0 = carve_saved(cfg, M, w[0].rows, K, saved[0], nullptr);
+  // X's forward codes and row scales / E8M0 stay where member 0 wrote them; W_i's go to its slice
+  const FwdWs fw = carve_fwd(cfg, d.M, d.nsum, d.K, ws, nullptr);
+  const Saved sv0 = carve_saved(cfg, d.M, w[0].rows, d.K, saved[0], nullptr);
+  std::vector<GemmProblem> ps(n);
   for (int i = 0; i < n; ++i) {
-    const Saved svi = i ? carve_saved(cfg, M, w[i].rows, K, saved[i], nullptr) : sv0;
-    FP8T_TRY(linear_fwd_train(cfg, x, nullptr, w[i], nullptr, y[i], nullptr, sv0, svi, fw, i == 0, st));
+    const Saved svi = i ? carve_saved(cfg, d.M, w[i].rows, d.K, saved[i], nullptr) : sv0;
+    FP8T_TRY(linear_fwd_train(cfg, x, nullptr, w[i], nullptr, y[i], nullptr, sv0, svi, fwd_member(cfg, fw, d, i),
+                              i == 0, st, &ps[i]));
   }
-  return FP8_OK;
+  return launch_group(ps, st);
 }
 
 fp8_status_t fp8_linear_bwd_shared(const fp8_linear_cfg_t* cfg, int n, const fp8_hp_t* dy, fp8_hp_t x,
@@ -937,6 +1048,9 @@ fp8_status_t fp8_linear_bwd_shared(const fp8_linear_cfg_t* cfg, int n, const fp8
   if (n < 1 || n > FP8_SHARED_MAX) return fail(FP8_EINVAL, "n must be in [1, %d]", FP8_SHARED_MAX);
   if (!dy || !saved) return fail(FP8_EINVAL, "dy / saved: null array");
   const bool gw_hp = cfg && cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;
+  SharedDims d;
+  d.M = x.rows;
+  d.K = x.cols;
   for (int i = 0; i < n; ++i) {   // every argument is checked before the first launch
     FP8T_TRY(check_hp(dy[i], "dy[i]"));
     if (dy[i].rows != x.rows || dy[i].dtype != dy[0].dtype) return fail(FP8_EINVAL, "dy[%d]: rows / dtype differ", i);
@@ -944,16 +1058,23 @@ fp8_status_t fp8_linear_bwd_shared(const fp8_linear_cfg_t* cfg, int n, const fp8
     FP8T_TRY(check_ptr(saved[i], "saved[i]"));
     if (dx && dx[i]) FP8T_TRY(check_ptr(dx[i], "dx[i]"));
     if (dw && dw[i]) FP8T_TRY(check_ptr(dw[i], "dw[i]"));
-    if (ws_bytes < fp8_linear_workspace_bytes(cfg, x.rows, dy[i].cols, x.cols))
-      return fail(FP8_EWORKSPACE, "workspace too small for member %d", i);
+    d.pre[i + 1] = d.pre[i] + dy[i].cols;
+    d.nmax = dy[i].cols > d.nmax ? dy[i].cols : d.nmax;
   }
+  d.nsum = d.pre[n];
   FP8T_TRY(check_hp(x, "x", gw_hp && dw));
-  for (int i = 0; i < n; ++i)
+  FP8T_TRY(check_ptr(ws, "ws"));
+  const size_t need = shared_ws_bytes(cfg, d, n);
+  if (ws_bytes < need) return fail(FP8_EWORKSPACE, "workspace too small (%zu < %zu)", ws_bytes, need);
+  const BwdGroupWs gw = carve_bwd_group(cfg, d, n, ws, nullptr);
+  std::vector<GemmProblem> ps;
+  for (int i = 0; i < n; ++i) {
+    const BwdWs bi = bwd_member(cfg, gw, d, i);
     FP8T_TRY(linear_bwd_impl(cfg, dy[i], nullptr, x, saved[i], nullptr, dx ? dx[i] : nullptr, nullptr,
-                             dw ? dw[i] : nullptr, ws, ws_bytes, stream, nullptr, 1, saved[0], dy[0].cols));
-  return FP8_OK;
+                             dw ? dw[i] : nullptr, ws, ws_bytes, stream, nullptr, 1, saved[0], dy[0].cols, &bi, &ps));
+  }
+  return launch_group(ps, S(stream));
 }
-
 
 fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
                                const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax, void* dw,
@@ -974,7 +1095,8 @@ fp8_status_t fp8_linear_bwd_rs(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, fp8_hp_
 static fp8_status_t linear_bwd_impl(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
                                     const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax, void* dw,
                                     void* ws, size_t ws_bytes, void* stream, fp8_p2p_t rs_win, int rs_nranks,
-                                    const void* saved_x, int64_t n_x) {
+                                    const void* saved_x, int64_t n_x, const BwdWs* bw_in,
+                                    std::vector<GemmProblem>* defer) {
   FP8T_TRY(check_hp(dy, "dy"));
   const int64_t M = dy.rows, N = dy.cols, K = x.cols;
   const bool gw_hp = cfg && cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;
@@ -987,7 +1109,7 @@ static fp8_status_t linear_bwd_impl(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, co
   FP8T_TRY(check_ptr(ws, "ws"));
   if (dx) FP8T_TRY(check_ptr(dx, "dx"));
   if (dw) FP8T_TRY(check_ptr(dw, "dw"));
-  if (ws_bytes < fp8_linear_workspace_bytes(cfg, M, N, K)) return fail(FP8_EWORKSPACE, "workspace too small");
+  if (!bw_in && ws_bytes < fp8_linear_workspace_bytes(cfg, M, N, K)) return fail(FP8_EWORKSPACE, "workspace too small");
   if (w_fp8) FP8T_TRY(check_w_fp8(cfg, w_fp8, N, K, dx != nullptr));
   if (dy_amax && cfg->recipe != FP8_RECIPE_TENSORWISE)
     return fail(FP8_EUNSUPPORTED, "dy_amax (precomputed tensor amax) needs the tensorwise recipe");
@@ -1004,7 +1126,8 @@ static fp8_status_t linear_bwd_impl(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, co
     sv.xT = s0.xT;
     sv.sx = s0.sx;
   }
-  BwdWs bw = carve_bwd(cfg, M, N, ws, nullptr);
+  // bw_in: a shared-input group's slice for this member (its dY operands stay until the group's GEMMs)
+  BwdWs bw = bw_in ? *bw_in : carve_bwd(cfg, M, N, ws, nullptr);
   const int of32 = cfg->out_dtype == FP8_DT_F32;
   int mode;
   if (cfg->recipe == FP8_RECIPE_TENSORWISE) {
@@ -1044,11 +1167,16 @@ gemms:
     // high-precision operands (both row-major [M, .] -> MN-major)
     if (dx) {
       GemmProblem p{bw.g, sv.wT, fg, ff, 0, 1, bw.sg, sv.sw, 1, M, K, N, N, K, dx, of32, K, 0, dxam};
-      FP8T_CUDA(launch_gemm(p, st), "gemm dx");
+      if (defer) defer->push_back(p);
+      else FP8T_CUDA(launch_gemm(p, st), "gemm dx");
     }
     if (dw) {
       GemmProblem p{static_cast<const uint8_t*>(dy.ptr), static_cast<const uint8_t*>(x.ptr), 0, 0, 1, 1, nullptr,
                     nullptr, 0, N, K, M, dy.ld, x.ld, dw, of32, K, 1};
+      if (defer) {
+        defer->push_back(p);
+        return FP8_OK;
+      }
       if (rs_win) FP8T_TRY(p2p_rs_begin(rs_win, rs_rows, K, st, p));
       FP8T_CUDA(launch_gemm(p, st), "gemm dw bf16");
       if (rs_win) FP8T_TRY(p2p_rs_end(rs_win, rs_rows, K, dw, K, st));
@@ -1088,6 +1216,10 @@ gemms:
     if (dx) ps[n++] = GemmProblem{bw.g, w1, fg, ff, 0, 0, bw.sg, s1, mode, M, K, N, N, N, dx, of32, K, 0, dxam};
     // dW[N,K] = dY^T[N,M] . X : A = dY^T [N,M], B = X^T [K,M]
     if (dw) ps[n++] = GemmProblem{bw.gT, sv.xT, fg, ff, 0, 0, bw.sgT, sv.sx, mode, N, K, M, M, M, dw, of32, K};
+  }
+  if (defer) {
+    defer->insert(defer->end(), ps, ps + n);
+    return FP8_OK;
   }
   if (rs_win && dw) FP8T_TRY(p2p_rs_begin(rs_win, rs_rows, K, st, ps[n - 1]));   // dW is the last problem
   FP8T_CUDA(launch_gemms(ps, n, st), "gemm dx/dw");

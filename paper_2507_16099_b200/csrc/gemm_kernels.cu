@@ -32,6 +32,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 
@@ -91,12 +92,18 @@ struct Prob {
   int rs_rank, rs_chunk_rows, rs_expect;
   unsigned rs_epoch;
 };
-// A launch processes the tiles of p0 ([0, t1)) then p1 ([t1, num_tiles)) on one persistent grid:
-// the backward's dX and dW GEMMs share one launch, so neither has its own wave-quantisation tail.
+// A launch processes the tiles of p[0] ([tstart[0] = 0, tstart[1])), then p[1], ... p[np - 1] (up to
+// tstart[np] = num_tiles) on one persistent grid: the backward's dX and dW GEMMs share one launch (and a
+// shared-input group's members all theirs), so no problem has its own wave-quantisation tail.  Grouped
+// (MoE) launches carry at most two problems, whose tile counts are known on the device only.
+constexpr int MAXP = GEMM_MAX_PROBS;
+struct alignas(64) GemmMaps {
+  CUtensorMap m[MAXP][4];   // per problem: A, B, SFA (N = 512 bf16: the D map), SFB
+};
 struct GemmArgs {
-  Prob p0, p1;
-  int t1, num_tiles;
-  int group_m;        // tile raster (see tile_coords)
+  Prob p[MAXP];
+  int tstart[MAXP + 1];
+  int np, num_tiles;
   int debug;          // bit 0: skip the epilogue's global stores (mainloop-only timing)
   int sf_split;       // MX: scale-factor copies issued by their own warp (see the SF copier)
   int kserp;          // K-serpentine: tiles of odd "waves" (tile / pairs) walk their K stages backwards
@@ -193,11 +200,7 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 
 template <bool MX, int CG, int ST, int KS, bool BF, bool GRP, bool E8, int BNT>
 __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THREADS, 1)
-    fp8_gemm_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tB0,
-                    const __grid_constant__ CUtensorMap tSA0, const __grid_constant__ CUtensorMap tSB0,
-                    const __grid_constant__ CUtensorMap tA1, const __grid_constant__ CUtensorMap tB1,
-                    const __grid_constant__ CUtensorMap tSA1, const __grid_constant__ CUtensorMap tSB1,
-                    const __grid_constant__ GemmArgs args) {
+    fp8_gemm_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ GemmArgs args) {
   static_assert(KS == 1 || CG == 2, "multi-atom stages need the CTA-pair kernel");
   static_assert(!BF || (CG == 2 && KS == 2 && !MX), "BF16 operands: CTA-pair, 2-atom stages");
   static_assert(!GRP || (!MX && !BF), "grouped problems: plain FP8 kinds");
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
   int* goffs = reinterpret_cast<int*>(gbase + L::off_grp);   // [2][GMAX + 1]
   int* gpre = goffs + 2 * (GMAX + 1);                         // [2][GMAX + 1]
   if (GRP && warp == 3 && lane < 2) {
-    const Prob& P = lane ? args.p1 : args.p0;
+    const Prob& P = args.p[lane];
     int* o = goffs + lane * (GMAX + 1);
     int* pre = gpre + lane * (GMAX + 1);
     if (P.grouped) {
@@ -265,12 +268,18 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
     if (P.grouped == 1) return gpre[pi * (GMAX + 1) + P.G] * P.tiles_n;
     return P.G * P.tiles_m * P.tiles_n;
   };
-  int t1 = args.t1, num_tiles = args.num_tiles;   // (grouped: known after the setup barrier)
+  int t1 = args.tstart[1], num_tiles = args.num_tiles;   // (grouped: known after the setup barrier)
   auto locate = [&](int tile) -> TileInfo {
     TileInfo ti{};
-    ti.pi = tile >= t1 ? 1 : 0;
-    const Prob& P = ti.pi ? args.p1 : args.p0;
-    const int local = ti.pi ? tile - t1 : tile;
+    int pi = 0;
+    if (GRP) {
+      pi = tile >= t1 ? 1 : 0;
+    } else {
+      while (pi + 1 < args.np && tile >= args.tstart[pi + 1]) ++pi;
+    }
+    ti.pi = pi;
+    const Prob& P = args.p[pi];
+    const int local = tile - (GRP ? (pi ? t1 : 0) : args.tstart[pi]);
     ti.m_valid = P.M;
     ti.num_kb = P.num_kb;
     ti.katoms = 1 << 30;
@@ -315,18 +324,12 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
   };
 
   if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tA0);
-    tma_prefetch_desc(&tB0);
-    if (args.t1 < args.num_tiles) {
-      tma_prefetch_desc(&tA1);
-      tma_prefetch_desc(&tB1);
-    }
-    if (MX) {
-      tma_prefetch_desc(&tSA0);
-      tma_prefetch_desc(&tSB0);
-      if (args.t1 < args.num_tiles) {
-        tma_prefetch_desc(&tSA1);
-        tma_prefetch_desc(&tSB1);
+    for (int i = 0; i < args.np; ++i) {
+      tma_prefetch_desc(&maps.m[i][0]);
+      tma_prefetch_desc(&maps.m[i][1]);
+      if (MX) {
+        tma_prefetch_desc(&maps.m[i][2]);
+        tma_prefetch_desc(&maps.m[i][3]);
       }
     }
     for (int s = 0; s < STAGES; ++s) {
@@ -366,8 +369,8 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (GRP) {
-    t1 = count(args.p0, 0);
-    num_tiles = t1 + (args.num_tiles > args.t1 ? count(args.p1, 1) : 0);
+    t1 = count(args.p[0], 0);
+    num_tiles = t1 + (args.np > 1 ? count(args.p[1], 1) : 0);
   }
 
   // MX: copy a stage's E8M0 tiles smem -> TMEM (tcgen05.cp; 3 copies of 512 B per K atom, each
@@ -475,11 +478,11 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
       }
       const TileInfo ti = locate(tile);
       const int pi = ti.pi, mb = ti.mb, nb = ti.nb;
-      const Prob& P = pi ? args.p1 : args.p0;
-      const CUtensorMap* tmA = pi ? &tA1 : &tA0;
-      const CUtensorMap* tmB = pi ? &tB1 : &tB0;
-      const CUtensorMap* tmSFA = pi ? &tSA1 : &tSA0;
-      const CUtensorMap* tmSFB = pi ? &tSB1 : &tSB0;
+      const Prob& P = args.p[pi];
+      const CUtensorMap* tmA = &maps.m[pi][0];
+      const CUtensorMap* tmB = &maps.m[pi][1];
+      const CUtensorMap* tmSFA = &maps.m[pi][2];
+      const CUtensorMap* tmSFB = &maps.m[pi][3];
       const int a_mn = P.a_mn, b_mn = P.b_mn;
       const int m0 = mb * BM * CG + (int)crank * BM;
       const int n0 = nb * L::BN + (int)crank * (L::BN / CG);
@@ -621,7 +624,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
     TileInfo ti{};
     if (tile < num_tiles) ti = locate(tile);
     while (tile < num_tiles) {
-      const Prob& P = ti.pi ? args.p1 : args.p0;
+      const Prob& P = args.p[ti.pi];
       const int a_mn = P.a_mn, b_mn = P.b_mn, num_kb = ti.num_kb;
       const uint32_t idesc = P.idesc;
       int next = 0;
@@ -764,7 +767,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
       if (tile >= num_tiles) break;
       const TileInfo ti = locate(tile);
       const int mb = ti.mb, nb = ti.nb;
-      const Prob& P = ti.pi ? args.p1 : args.p0;
+      const Prob& P = args.p[ti.pi];
       const int N = P.N, row_scales = P.row_scales, out_f32 = P.out_f32;
       const float* sb = P.sb + ti.sb_off;
       const int row = mb * BM * CG + (int)crank * BM + q * 32 + (int)lane;   // row within the problem / group
@@ -869,7 +872,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
         // bf16 outputs are scaled into one of this warp's two 2 KB smem chunks and written by a TMA store each,
         // so the warp never waits on global writes (which compete with the operand loads for L2) before it
         // releases TMEM; a chunk buffer is reused once its previous store has been read out of smem.
-        const CUtensorMap* dmap = ti.pi ? &tSA1 : &tSA0;
+        const CUtensorMap* dmap = &maps.m[ti.pi][2];
         const bool tma_out = P.d_tma;
         const int row_base = mb * BM * CG + (int)crank * BM + q * 32;
         for (int h = 0; h < 2; ++h) {
@@ -1169,26 +1172,24 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
   using L = Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>;
   const cudaError_t attr_err = ensure_smem<fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8, BNT>>(L::bytes);
   if (attr_err != cudaSuccess) return attr_err;
-  CUtensorMap m0[4], m1[4];
+  if (n < 1 || n > MAXP || (GRP && n > 2)) return cudaErrorInvalidValue;
+  static_assert(sizeof(GemmMaps) + sizeof(GemmArgs) <= 32000, "kernel parameter space");
+  GemmMaps maps;
   GemmArgs a{};
-  // longer-K problem first: the dynamic scheduler then hands out the long tiles before the short ones
-  GemmProblem q[2];
-  q[0] = ps[0];
-  if (n > 1) {
-    q[1] = ps[1];
-    if (!GRP && ps[1].K > ps[0].K) { q[0] = ps[1]; q[1] = ps[0]; }
-  }
+  // longer-K problems first (stable): the dynamic scheduler then hands out the long tiles before the short ones
+  GemmProblem q[MAXP];
+  for (int i = 0; i < n; ++i) q[i] = ps[i];
+  if (!GRP)
+    std::stable_sort(q, q + n, [](const GemmProblem& x, const GemmProblem& y) { return x.K > y.K; });
   ps = q;
-  if (!setup_prob<MX, CG, ST, KS, BF, GRP, E8, BNT>(ps[0], a.p0, m0)) return cudaErrorInvalidValue;
-  a.t1 = a.p0.tiles_m * a.p0.tiles_n;
-  if (n > 1) {
-    if (!setup_prob<MX, CG, ST, KS, BF, GRP, E8, BNT>(ps[1], a.p1, m1)) return cudaErrorInvalidValue;
-    a.num_tiles = a.t1 + a.p1.tiles_m * a.p1.tiles_n;
-  } else {
-    a.p1 = a.p0;
-    for (int i = 0; i < 4; ++i) m1[i] = m0[i];
-    a.num_tiles = a.t1;
+  a.np = n;
+  a.tstart[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!setup_prob<MX, CG, ST, KS, BF, GRP, E8, BNT>(ps[i], a.p[i], maps.m[i])) return cudaErrorInvalidValue;
+    a.tstart[i + 1] = a.tstart[i] + a.p[i].tiles_m * a.p[i].tiles_n;
   }
+  for (int i = n; i <= MAXP; ++i) a.tstart[i] = a.tstart[n];
+  a.num_tiles = a.tstart[n];
   {
     a.debug = knob(KNOB_GEMM_DEBUG);
     // knob gemm_sched = 0: round-robin tiles (A/B); default: dynamic scheduler.  A launch under
@@ -1210,17 +1211,14 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     }
     // raster per problem (choose_raster); knob gemm_raster >= 0 overrides for every problem
     const int r = knob(KNOB_GEMM_RASTER);
-    a.group_m = r >= 0 ? r : GROUP_M;
-    a.p0.raster = r >= 0 ? a.group_m : choose_raster(ps[0], BF);
-    a.p1.raster = r >= 0 ? a.group_m : (n > 1 ? choose_raster(ps[1], BF) : a.p0.raster);
+    for (int i = 0; i < n; ++i) a.p[i].raster = r >= 0 ? r : choose_raster(ps[i], BF);
   }
   const int slots = num_sms() / CG;
   // grouped: the tile count depends on the device-side offsets -> a full persistent grid
   const int grid = GRP ? CG * slots : CG * (a.num_tiles < slots ? a.num_tiles : slots);
   LaunchScope ls(MX ? K_GEMM_MX : (BF ? K_GEMM_BF16 : K_GEMM), st);
   if (CG == 1) {
-    fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8, BNT><<<grid, L::THREADS, L::bytes, st>>>(m0[0], m0[1], m0[2], m0[3], m1[0], m1[1],
-                                                                      m1[2], m1[3], a);
+    fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8, BNT><<<grid, L::THREADS, L::bytes, st>>>(maps, a);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -1234,8 +1232,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8, BNT>, m0[0], m0[1], m0[2], m0[3], m1[0],
-                                       m1[1], m1[2], m1[3], a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fp8_gemm_kernel<MX, CG, ST, KS, BF, GRP, E8, BNT>, maps, a);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
@@ -1243,7 +1240,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
 
 // One or two problems of the same kind (scale mode) on one persistent launch.
 cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st) {
-  if (n < 1 || n > 2) return cudaErrorInvalidValue;
+  if (n < 1 || n > MAXP) return cudaErrorInvalidValue;
   bool grp = false;
   for (int i = 0; i < n; ++i) {
     if (ps[i].grouped) {
@@ -1253,7 +1250,8 @@ cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st) {
     }
   }
   if (grp) return launch_t<false, 2, 3, 2, false, true>(ps, n, st);
-  if (n == 2 && ((ps[0].scale_mode == 2) != (ps[1].scale_mode == 2))) return cudaErrorInvalidValue;
+  for (int i = 1; i < n; ++i)
+    if ((ps[i].scale_mode == 2) != (ps[0].scale_mode == 2)) return cudaErrorInvalidValue;
   if (ps[0].bf16_in) {
     for (int i = 1; i < n; ++i)
       if (!ps[i].bf16_in) return cudaErrorInvalidValue;

@@ -210,8 +210,9 @@ struct GemmProblem {
   unsigned rs_epoch = 0;
 };
 constexpr int GEMM_MAX_GROUPS = 256;
+constexpr int GEMM_MAX_PROBS = 6;   // problems per persistent launch (grouped MoE launches: 2)
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t st);
-// Two problems of the same kind on one persistent launch (tiles of ps[0] then ps[1]).
+// Up to GEMM_MAX_PROBS problems of the same kind (scale mode) on one persistent launch, longest K first.
 cudaError_t launch_gemms(const GemmProblem* ps, int n, cudaStream_t st);
 
 }  // namespace fp8t

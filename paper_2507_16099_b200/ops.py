@@ -263,7 +263,8 @@ class LinearPlan:
 class SharedInputPlan:
     """Float8Linears that read the same input X (fp8_linear_fwd_shared / _bwd_shared): e.g. wq/wk/wv
     or w1/w3 of a Llama layer.  X is cast once; outputs and saved bytes equal those of separate
-    LinearPlan calls.  One workspace for the group (sized for the widest member)."""
+    LinearPlan calls.  One workspace for the group (fp8_linear_shared_workspace_bytes); the members'
+    GEMMs run as one launch per pass."""
 
     def __init__(self, M, Ns, K, recipe="tensorwise", fmt_fwd="e4m3", fmt_grad="e5m2", mx_round="floor",
                  out_dtype=torch.bfloat16, device="cuda"):
@@ -272,7 +273,8 @@ class SharedInputPlan:
         self.cfg = L.LinearCfg(RECIPES[recipe], FORMATS[fmt_fwd], FORMATS[fmt_grad], MX_ROUND[mx_round],
                                L.DT_F32 if out_dtype == torch.float32 else L.DT_BF16)
         self.saved_bytes = [L.lib.fp8_linear_saved_bytes(ctypes.byref(self.cfg), M, N, K) for N in self.Ns]
-        self.ws_bytes = L.lib.fp8_linear_workspace_bytes(ctypes.byref(self.cfg), M, max(self.Ns), K)
+        ns = (ctypes.c_int64 * len(self.Ns))(*self.Ns)
+        self.ws_bytes = L.lib.fp8_linear_shared_workspace_bytes(ctypes.byref(self.cfg), M, K, len(self.Ns), ns)
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
 
     def new_saved(self, device="cuda"):

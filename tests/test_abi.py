@@ -153,8 +153,9 @@ def test_argument_errors_return_before_any_launch(L):
     assert fwd(0, ws3, 1 << 40) == L.FP8_EINVAL
     assert fwd(9, ws3, 1 << 40) == L.FP8_EINVAL
     assert fwd(3, (L.HP * 3)(hp(256, 128), hp(512, 144), hp(128, 128)), 1 << 40) == L.FP8_EINVAL
-    need = L.lib.fp8_linear_workspace_bytes(ctypes.byref(cfg), 256, 512, 128)
-    assert need > L.lib.fp8_linear_workspace_bytes(ctypes.byref(cfg), 256, 256, 128)
+    need = L.lib.fp8_linear_shared_workspace_bytes(ctypes.byref(cfg), 256, 128, 3, (ctypes.c_int64 * 3)(256, 512, 128))
+    assert need >= L.lib.fp8_linear_workspace_bytes(ctypes.byref(cfg), 256, 896, 128) > 0   # every member's operands
+    assert L.lib.fp8_linear_shared_workspace_bytes(ctypes.byref(cfg), 256, 128, 0, (ctypes.c_int64 * 3)()) == 0
     assert fwd(3, ws3, need - 1) == L.FP8_EWORKSPACE
     dys = (L.HP * 2)(hp(256, 256), hp(272, 512))
     assert L.lib.fp8_linear_bwd_shared(ctypes.byref(cfg), 2, dys, hp(256, 128), ptrs, ptrs, ptrs, ws, 1 << 40,

@@ -1599,7 +1599,8 @@ SHARED_CASES = [("tensorwise", {}), ("tensorwise", {"tw_dual": 0}), ("rowwise", 
 
 
 @pytest.mark.parametrize("M,K,Ns", [(384, 512, (640, 128, 256)), (256, 384, (128, 512)), (384, 256, (384,)),
-                                    (400, 528, (272, 400, 144))], ids=["qkv", "w13", "single", "ragged"])
+                                    (400, 528, (272, 400, 144)), (256, 256, (128, 256, 128, 384, 128, 256, 128))],
+                         ids=["qkv", "w13", "single", "ragged", "seven"])
 @pytest.mark.parametrize("recipe,knobs", SHARED_CASES,
                          ids=[r + ("-" + "-".join(f"{k}{v}" for k, v in kn.items()) if kn else "") for r, kn in
                               SHARED_CASES])
@@ -1607,8 +1608,10 @@ def test_linear_shared_input_matches_separate(recipe, knobs, M, K, Ns, knob):
     """fp8_linear_fwd_shared / _bwd_shared (linears reading one X: wq/wk/wv, w1/w3) write exactly what
     separate fp8_linear_fwd / fp8_linear_bwd calls write: Y_i, dX_i, dW_i bit-identical, X's saved
     backward operand (member 0's buffer) and every member's W operand byte-identical -- X's scales
-    depend on X alone (Appendix A), so casting it once changes nothing.  Widest
-    member first and not first, ragged sizes; Y_i also within the oracle's bound."""
+    depend on X alone (Appendix A), so casting it once changes nothing.  The members'
+    GEMMs share persistent launches (up to 6 problems each; "seven": 14 backward problems = 3 launches,
+    rowwise_gw_hp: FP8 dX and BF16 dW launches apart).  Widest member first and not first, ragged
+    sizes; Y_i also within the oracle's bound."""
     if recipe == "mxfp8" and (M % 128 or K % 128 or any(n % 128 for n in Ns)):
         pytest.skip("mxfp8 needs 128-multiples")
     for k, v in knobs.items():
