@@ -318,7 +318,7 @@ fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const f
  * (tensorwise amax over X; rowwise per row / per column of X; MX blocks of X), so its amax and
  * FP8 copies are computed ONCE, by member 0, and read by every member's GEMMs.  Every output and
  * every saved byte equals what n separate fp8_linear_fwd / fp8_linear_bwd calls write.
- *   fwd: x [M,K]; w: HOST array of n weights [N_i, K] (same dtype as x); y: HOST array of n
+ *   fwd: x [M,K]; w: HOST array of n weights [N_i, K] (fp32 or bf16 each); y: HOST array of n
  *     outputs [M, N_i] (out_dtype, dense); saved: HOST array of n buffers of
  *     fp8_linear_saved_bytes(cfg, M, N_i, K) bytes -- saved[0] holds X's backward operand,
  *     saved[i > 0] only W_i's; ws >= fp8_linear_shared_workspace_bytes(cfg, M, K, n, N) bytes (every

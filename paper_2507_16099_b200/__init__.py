@@ -7,7 +7,7 @@ has not been built; there is no CPU fallback.
 
 from . import _lib  # noqa: F401  (loads libfp8train.so or raises)
 from .ops import GroupedPlan, LinearPlan, SharedInputPlan, amax, cast, gemm, launch_count  # noqa: F401
-from .linear import Float8Linear, convert, scaled_grouped_mm  # noqa: F401
+from .linear import Float8Linear, convert, scaled_grouped_mm, shared_input_linears  # noqa: F401
 
 __all__ = ["GroupedPlan", "LinearPlan", "SharedInputPlan", "amax", "cast", "gemm", "launch_count", "Float8Linear", "convert",
-           "scaled_grouped_mm"]
+           "scaled_grouped_mm", "shared_input_linears"]

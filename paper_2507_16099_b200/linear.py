@@ -11,7 +11,7 @@ amax -> scale -> saturating RNE cast -> tcgen05 scaled GEMM, for Y, dX and dW.
 import torch
 from torch import nn
 
-from .ops import GroupedPlan, LinearPlan
+from .ops import GroupedPlan, LinearPlan, SharedInputPlan
 
 
 class _Plans:
@@ -108,6 +108,72 @@ def convert(model, recipe="tensorwise", module_filter_fn=None):
         else:
             convert(child, recipe, module_filter_fn)
     return model
+
+
+# ------------------------------------------------------------------ shared-input linears
+
+class _SharedPlans:
+    def __init__(self):
+        self._p = {}
+
+    def get(self, M, Ns, K, recipe, device):
+        key = (M, tuple(Ns), K, recipe, str(device))
+        if key not in self._p:
+            self._p[key] = SharedInputPlan(M, Ns, K, recipe=recipe, out_dtype=torch.bfloat16, device=device)
+        return self._p[key]
+
+
+_SPLANS = _SharedPlans()
+
+
+class _SharedInputFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x2d, recipe, *ws):
+        M, K = x2d.shape
+        plan = _SPLANS.get(M, [w.shape[0] for w in ws], K, recipe, x2d.device)
+        saved = plan.new_saved(x2d.device)
+        x2d = x2d.contiguous()
+        ys = plan.forward(x2d, [w.contiguous() for w in ws], saved)
+        ctx.plan, ctx.buf, ctx.wdtypes = plan, saved, [w.dtype for w in ws]
+        ctx.gw_hp = recipe == "rowwise_gw_hp"
+        if ctx.gw_hp:
+            ctx.save_for_backward(x2d if x2d.dtype == torch.bfloat16 else x2d.to(torch.bfloat16))
+        return tuple(ys)
+
+    @staticmethod
+    def backward(ctx, *dys):
+        x_hp = None
+        if ctx.gw_hp:
+            (x_hp,) = ctx.saved_tensors
+        dys = [d.to(torch.bfloat16).contiguous() for d in dys]   # (unused outputs arrive as zeros)
+        want_dw = any(ctx.needs_input_grad[2:])
+        dxs, dws = ctx.plan.backward(dys, ctx.buf, x=x_hp, want_dx=ctx.needs_input_grad[0], want_dw=want_dw)
+        dx = None
+        if dxs is not None:   # X feeds every member: its gradient is the members' sum (in member order)
+            dx = dxs[0]
+            for d in dxs[1:]:
+                dx = dx + d
+        grads = [None] * len(ctx.wdtypes)
+        if dws is not None:
+            grads = [dw if dw.dtype == t else dw.to(t) for dw, t in zip(dws, ctx.wdtypes)]
+        return (dx, None, *grads)
+
+
+def shared_input_linears(x, linears):
+    """Y_i = Float8Linear_i(x) for linears that read the same x (a layer's wq/wk/wv, w1/w3): X's amax
+    and FP8 copies are computed once and the members' GEMMs run as one launch per pass
+    (fp8_linear_fwd_shared / _bwd_shared).  Each Y_i, dW_i and dX_i is bit-identical to the separate
+    Float8Linear's; dX = sum of the dX_i in member order.  `linears`: Float8Linear modules with one
+    recipe and no bias.  Returns a tuple of outputs shaped like x with the last dim N_i."""
+    recipe = linears[0].recipe
+    if any(lin.recipe != recipe or lin.bias is not None for lin in linears):
+        raise ValueError("shared_input_linears: one recipe, no bias")
+    shp = x.shape
+    x2d = x.reshape(-1, shp[-1])
+    if x2d.dtype != torch.bfloat16 and x2d.dtype != torch.float32:
+        x2d = x2d.to(torch.bfloat16)
+    ys = _SharedInputFn.apply(x2d, recipe, *[lin.weight for lin in linears])
+    return tuple(y.reshape(*shp[:-1], y.shape[-1]) for y in ys)
 
 
 # ----------------------------------------------------------------------------- MoE

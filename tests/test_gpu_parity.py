@@ -1653,3 +1653,46 @@ def test_linear_shared_input_matches_separate(recipe, knobs, M, K, Ns, knob):
         yo, bd, _ = olin.forward(x, ws_[i], recipe)
         err = np.abs(_np(ys[i].float()).astype(np.float64) - yo)
         assert np.all(err <= 1e-2 * bd + 1e-30), f"y[{i}]: max err/bound {np.max(err / (bd + 1e-30)):.3e}"
+
+
+@pytest.mark.parametrize("recipe", ["tensorwise", "rowwise", "mxfp8", "rowwise_gw_hp"])
+@pytest.mark.parametrize("wdtype", [torch.bfloat16, torch.float32], ids=["bf16_params", "fp32_params"])
+def test_shared_input_linears_module(recipe, wdtype):
+    """fp8t.shared_input_linears (a layer's q/k/v reading one X) against the same Float8Linear modules
+    called separately: every Y_i and weight gradient bit-identical, X's gradient equal to the members'
+    dX_i summed in member order (separate modules' autograd sums the same dX_i, in its own order:
+    within one bf16 rounding per add); bf16 activations with bf16 or fp32 parameters."""
+    M, K, Ns = 256, 256, (384, 128, 128)
+    x = synth.linear_inputs("c3", M, Ns[0], K, seed=41)[0]
+    lins = []
+    for i, N in enumerate(Ns):
+        w = synth.linear_inputs("c3", M, N, K, seed=42 + i)[1]
+        lin = torch.nn.Linear(K, N, bias=False).cuda().to(wdtype)
+        with torch.no_grad():
+            lin.weight.copy_(_dev(w, wdtype))
+        lins.append(fp8t.Float8Linear.from_linear(lin, recipe))
+    dys = [_dev(synth.linear_inputs("c3", M, N, K, seed=50 + i)[2], torch.bfloat16) for i, N in enumerate(Ns)]
+    X1 = _dev(x, torch.bfloat16).requires_grad_(True)
+    ys = fp8t.shared_input_linears(X1, lins)
+    torch.autograd.backward(ys, dys)
+    g_shared = [lin.weight.grad.clone() for lin in lins]
+    for lin in lins:
+        lin.weight.grad = None
+    X2 = _dev(x, torch.bfloat16).requires_grad_(True)
+    ys2 = [lin(X2) for lin in lins]
+    torch.autograd.backward(ys2, dys)
+    for i in range(len(Ns)):
+        assert torch.equal(ys[i], ys2[i]), i
+        assert torch.equal(g_shared[i], lins[i].weight.grad), i
+    # the members' dX_i through the plan, summed in member order, is what the shared path returns
+    plans = [ops.LinearPlan(M, N, K, recipe=recipe) for N in Ns]
+    dxs = []
+    for p, lin, dy in zip(plans, lins, dys):
+        sv = p.new_saved()
+        p.forward(X2.detach(), lin.weight.detach(), sv)
+        dxs.append(p.backward(dy, sv, x=X2.detach(), want_dw=False)[0])
+    want = dxs[0] + dxs[1] + dxs[2]
+    assert torch.equal(X1.grad, want)
+    # each order rounds twice to bf16 (unit roundoff 2^-8) partial sums bounded by sum |dX_i|
+    bound = 4 * 2 ** -8 * sum(d.float().abs() for d in dxs)
+    assert torch.all((X1.grad.float() - X2.grad.float()).abs() <= bound)
