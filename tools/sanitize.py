@@ -63,5 +63,15 @@ s9 = p9.new_saved()
 p9.forward(X9, W9, s9)
 p9.backward(G9, s9)
 ops.reset_knobs()
+# shared-input groups: multi-problem GEMM launches (6 problems in the backward), FP8 + BF16 kinds apart
+for recipe in ("rowwise", "mxfp8", "rowwise_gw_hp", "tensorwise"):
+    Ns = [256, 128, 128]
+    sp = ops.SharedInputPlan(256, Ns, 256, recipe=recipe)
+    sv = sp.new_saved()
+    Xs = torch.randn((256, 256), device="cuda").to(torch.bfloat16)
+    Ws = [(torch.randn((n, 256), device="cuda") * 0.02).to(torch.bfloat16) for n in Ns]
+    Gs = [(torch.randn((256, n), device="cuda") * 1e-3).to(torch.bfloat16) for n in Ns]
+    sp.forward(Xs, Ws, sv)
+    sp.backward(Gs, sv, x=Xs)
 torch.cuda.synchronize()
 print("ok")
