@@ -559,6 +559,9 @@ uint64_t fp8_launch_count(void);
  *   K >= 8192; 1 = whenever N % 512 == 0; 0 = never) |
  *   gemm_l2pf (0 = off; d > 0: the GEMM producer prefetches operand boxes d stages ahead into L2) |
  *   mx_cast_occ3 (0) | amax_bulk (1: tensorwise amax of contiguous tensors by 1-D bulk copies; 0: register streaming) |
+ *   amax_rc (1: row / column amax by the multi-tensor warp-specialised kernel; 0: amax_tile_tma's choice) |
+ *   amax_rc_debug (0; A/B probes only) | group_batch (1: a rowwise shared-input group's amax and cast launches
+ *   batched over X and every W_i, and over every dY_i; 0: per member) |
  *   watchdog_ms (30000; 0 = peer waits never give up)
  *   -- defaults in parentheses.
  * A knob changes launches enqueued after the call.  Unknown name or out-of-range value:

@@ -32,7 +32,10 @@ static const KnobDef kKnobs[KNOB_COUNT] = {
     {"gemm_debug", 0, 0, 1 << 16},  {"gemm_sched", 1, 0, 1},       {"mx_sf_split", 1, 0, 8},
     {"gemm_raster", -1, -1, 64},    {"mx_n192", 0, 0, 1},          {"gemm_stages", 3, 3, 6},
     {"gemm_epi", 0, 0, 8},          {"mx_transposed", 0, 0, 1},    {"tw_dual", 1, 0, 1},
-    {"gemm_kserp", 1, 0, 1},        {"gemm_n512", 2, 0, 2},        {"gemm_l2pf", 0, 0, 64},  {"mx_cast_occ3", 0, 0, 1},      {"amax_bulk", 1, 0, 1},        {"watchdog_ms", 30000, 0, 1 << 30},
+    {"gemm_kserp", 1, 0, 1},        {"gemm_n512", 2, 0, 2},        {"gemm_l2pf", 0, 0, 64},
+    {"mx_cast_occ3", 0, 0, 1},      {"amax_bulk", 1, 0, 1},        {"amax_rc", 1, 0, 1},
+    {"amax_rc_debug", 0, 0, 3},     {"group_batch", 1, 0, 1},
+    {"watchdog_ms", 30000, 0, 1 << 30},
 };
 static std::atomic<int> g_knobs[KNOB_COUNT];
 // defaults come from the table (one source of truth); a table shorter than the enum leaves a null name
@@ -614,7 +617,7 @@ fp8_status_t check_w_fp8(const fp8_linear_cfg_t* cfg, const fp8_tensor_t* w_fp8,
 static fp8_status_t linear_fwd_train(const fp8_linear_cfg_t* cfg, fp8_hp_t x, const float* x_amax, fp8_hp_t w,
                                      const fp8_tensor_t* w_fp8, void* y, float* y_amax, const Saved& svx,
                                      const Saved& svw, const FwdWs& fw, bool cast_x, cudaStream_t st,
-                                     GemmProblem* defer = nullptr) {
+                                     GemmProblem* defer = nullptr, bool cast_done = false) {
   const int64_t M = x.rows, K = x.cols, N = w.rows;
   const bool xb = x.dtype == FP8_DT_BF16, wb = w.dtype == FP8_DT_BF16;
   const int ff = cfg->fmt_fwd;
@@ -689,6 +692,10 @@ static fp8_status_t linear_fwd_train(const fp8_linear_cfg_t* cfg, fp8_hp_t x, co
     float* axc = axr + M;
     float* awr = axc + K;
     float* awc = awr + N;
+    if (cast_done) {   // a shared-input group cast X and every W_i by one amax and one cast launch
+      GemmProblem p{fw.xq, fw.wq, ff, ff, 0, 0, fw.sxr, fw.swr, 1, M, N, K, K, K, y, of32, N, 0, yam};
+      return fwd_gemm(p);
+    }
     if (!cast_x) {   // X's row / column amax, codes and scales are already in fw / svx
       FP8T_CUDA(cudaMemsetAsync(awr, 0, 4 * (N + K), st), "memset");
       FP8T_CUDA(launch_amax(w.ptr, wb, N, K, w.ld, 6, nullptr, (uint32_t*)awr, (uint32_t*)awc, st), "amax w");
@@ -906,7 +913,7 @@ static fp8_status_t linear_bwd_impl(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, co
                                     const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax, void* dw,
                                     void* ws, size_t ws_bytes, void* stream, fp8_p2p_t rs_win, int rs_nranks,
                                     const void* saved_x = nullptr, int64_t n_x = 0, const BwdWs* bw_in = nullptr,
-                                    std::vector<GemmProblem>* defer = nullptr);
+                                    std::vector<GemmProblem>* defer = nullptr, bool cast_done = false);
 
 // Linears sharing one input (see fp8train.h): X is cast once by member 0, members 1..n-1 cast W only;
 // every member's GEMMs run in one persistent launch (up to GEMM_MAX_PROBS problems per launch).
@@ -972,11 +979,36 @@ FwdWs fwd_member(const fp8_linear_cfg_t* cfg, const FwdWs& f, const SharedDims& 
   else m.swr = f.swr + off;
   return m;
 }
+// Batched group casts (rowwise; knob group_batch): X and every W_i (forward), every member's dY (backward)
+// go through ONE amax launch and ONE cast launch, so each tensor needs its own row / column amax slots
+// while the launch runs: forward [M + K] for X then [N_i + K] per W_i, backward [M + N_i] per dY_i,
+// placed after the forward / backward workspace regions.
+bool group_batchable(const fp8_linear_cfg_t* cfg, int n) {
+  return cfg->recipe == FP8_RECIPE_ROWWISE && n + 1 <= AMAX_RC_MAX && n + 1 <= CAST_MULTI_MAX;
+}
+size_t group_fwd_amax_floats(const fp8_linear_cfg_t* cfg, const SharedDims& d, int n) {
+  return group_batchable(cfg, n) ? (size_t)(d.M + d.K + d.nsum + (int64_t)n * d.K) : 0;
+}
+size_t group_bwd_amax_floats(const fp8_linear_cfg_t* cfg, const SharedDims& d, int n) {
+  return group_batchable(cfg, n) ? (size_t)((int64_t)n * d.M + d.nsum) : 0;
+}
 size_t shared_ws_bytes(const fp8_linear_cfg_t* cfg, const SharedDims& d, int n) {
   size_t f = 0, b = 0;
   carve_fwd(cfg, d.M, d.nsum, d.K, nullptr, &f);
   carve_bwd_group(cfg, d, n, nullptr, &b);
+  f += al(4 * group_fwd_amax_floats(cfg, d, n));
+  b += al(4 * group_bwd_amax_floats(cfg, d, n));
   return f > b ? f : b;
+}
+float* group_fwd_amax(const fp8_linear_cfg_t* cfg, const SharedDims& d, void* ws) {
+  size_t f = 0;
+  carve_fwd(cfg, d.M, d.nsum, d.K, nullptr, &f);
+  return reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + f);
+}
+float* group_bwd_amax(const fp8_linear_cfg_t* cfg, const SharedDims& d, int n, void* ws) {
+  size_t b = 0;
+  carve_bwd_group(cfg, d, n, nullptr, &b);
+  return reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + b);
 }
 // Launch a group's GEMM problems: FP8 and BF16 (rowwise_gw_hp dW) kinds apart, GEMM_MAX_PROBS per launch.
 fp8_status_t launch_group(const std::vector<GemmProblem>& ps, cudaStream_t st) {
@@ -1032,11 +1064,46 @@ fp8_status_t fp8_linear_fwd_shared(const fp8_linear_cfg_t* cfg, fp8_hp_t x, int 
   // X's forward codes and row scales / E8M0 stay where member 0 wrote them; W_i's go to its slice
   const FwdWs fw = carve_fwd(cfg, d.M, d.nsum, d.K, ws, nullptr);
   const Saved sv0 = carve_saved(cfg, d.M, w[0].rows, d.K, saved[0], nullptr);
+  // rowwise: X's and every W_i's row / column amax by one launch, their row-scaled forward codes and
+  // column-scaled backward copies by one cast launch (the bytes separate linears write)
+  bool batched = false;
+  bool all_bf16 = x.dtype == FP8_DT_BF16;
+  for (int i = 0; i < n; ++i) all_bf16 = all_bf16 && w[i].dtype == FP8_DT_BF16;
+  if (group_batchable(cfg, n) && all_bf16 && knob(KNOB_GROUP_BATCH) == 1) {
+    float* am = group_fwd_amax(cfg, d, ws);
+    FP8T_CUDA(cudaMemsetAsync(am, 0, 4 * group_fwd_amax_floats(cfg, d, n), st), "memset group amax");
+    AmaxRCTensor ts[AMAX_RC_MAX];
+    CastMulti cm{};
+    cm.n = n + 1;
+    float* p = am;
+    for (int k = 0; k <= n; ++k) {
+      const fp8_hp_t& t = k ? w[k - 1] : x;
+      float* ar = p;
+      float* ac = p + t.rows;
+      p = ac + d.K;
+      ts[k] = AmaxRCTensor{t.ptr, t.rows, t.cols, t.ld, reinterpret_cast<uint32_t*>(ar), reinterpret_cast<uint32_t*>(ac)};
+      cm.x[k] = t.ptr; cm.R[k] = t.rows; cm.C[k] = t.cols; cm.ld[k] = t.ld;
+      cm.amax_q[k] = ar; cm.amax_t[k] = ac;
+      if (k == 0) {
+        cm.q[k] = fw.xq; cm.qt[k] = sv0.xT; cm.scale_q[k] = fw.sxr; cm.scale_t[k] = static_cast<float*>(sv0.sx);
+      } else {
+        const FwdWs fm = fwd_member(cfg, fw, d, k - 1);
+        const Saved svk = carve_saved(cfg, d.M, t.rows, d.K, saved[k - 1], nullptr);
+        cm.q[k] = fm.wq; cm.qt[k] = svk.wT; cm.scale_q[k] = fm.swr; cm.scale_t[k] = static_cast<float*>(svk.sw);
+      }
+    }
+    const cudaError_t e = launch_amax_rc(ts, n + 1, 6, st);
+    if (e != cudaErrorNotSupported) {
+      FP8T_CUDA(e, "group amax");
+      FP8T_CUDA(launch_cast_dual(cm, true, cfg->fmt_fwd, 2, 5, st), "group cast");
+      batched = true;
+    }
+  }
   std::vector<GemmProblem> ps(n);
   for (int i = 0; i < n; ++i) {
     const Saved svi = i ? carve_saved(cfg, d.M, w[i].rows, d.K, saved[i], nullptr) : sv0;
     FP8T_TRY(linear_fwd_train(cfg, x, nullptr, w[i], nullptr, y[i], nullptr, sv0, svi, fwd_member(cfg, fw, d, i),
-                              i == 0, st, &ps[i]));
+                              i == 0, st, &ps[i], batched));
   }
   return launch_group(ps, st);
 }
@@ -1066,13 +1133,46 @@ fp8_status_t fp8_linear_bwd_shared(const fp8_linear_cfg_t* cfg, int n, const fp8
   const size_t need = shared_ws_bytes(cfg, d, n);
   if (ws_bytes < need) return fail(FP8_EWORKSPACE, "workspace too small (%zu < %zu)", ws_bytes, need);
   const BwdGroupWs gw = carve_bwd_group(cfg, d, n, ws, nullptr);
+  cudaStream_t st = S(stream);
+  // rowwise with dX and dW for every member: every dY_i's row / column amax by one launch, its
+  // row-scaled (dX) and column-scaled (dW) codes by one cast launch
+  bool batched = false;
+  bool full = dx && dw && dy[0].dtype == FP8_DT_BF16;
+  for (int i = 0; full && i < n; ++i) full = dx[i] && dw[i];
+  if (group_batchable(cfg, n) && full && knob(KNOB_GROUP_BATCH) == 1) {
+    float* am = group_bwd_amax(cfg, d, n, ws);
+    FP8T_CUDA(cudaMemsetAsync(am, 0, 4 * group_bwd_amax_floats(cfg, d, n), st), "memset group amax");
+    AmaxRCTensor ts[AMAX_RC_MAX];
+    CastMulti cm{};
+    cm.n = n;
+    float* p = am;
+    for (int i = 0; i < n; ++i) {
+      const BwdWs bi = bwd_member(cfg, gw, d, i);
+      float* ar = p;
+      float* ac = p + d.M;
+      p = ac + dy[i].cols;
+      ts[i] = AmaxRCTensor{dy[i].ptr, d.M, dy[i].cols, dy[i].ld, reinterpret_cast<uint32_t*>(ar),
+                           reinterpret_cast<uint32_t*>(ac)};
+      cm.x[i] = dy[i].ptr; cm.R[i] = d.M; cm.C[i] = dy[i].cols; cm.ld[i] = dy[i].ld;
+      cm.amax_q[i] = ar; cm.amax_t[i] = ac;
+      cm.q[i] = bi.g; cm.qt[i] = bi.gT;
+      cm.scale_q[i] = static_cast<float*>(bi.sg); cm.scale_t[i] = static_cast<float*>(bi.sgT);
+    }
+    const cudaError_t e = launch_amax_rc(ts, n, 6, st);
+    if (e != cudaErrorNotSupported) {
+      FP8T_CUDA(e, "group amax dy");
+      FP8T_CUDA(launch_cast_dual(cm, true, cfg->fmt_grad, 2, 5, st), "group cast dy");
+      batched = true;
+    }
+  }
   std::vector<GemmProblem> ps;
   for (int i = 0; i < n; ++i) {
     const BwdWs bi = bwd_member(cfg, gw, d, i);
     FP8T_TRY(linear_bwd_impl(cfg, dy[i], nullptr, x, saved[i], nullptr, dx ? dx[i] : nullptr, nullptr,
-                             dw ? dw[i] : nullptr, ws, ws_bytes, stream, nullptr, 1, saved[0], dy[0].cols, &bi, &ps));
+                             dw ? dw[i] : nullptr, ws, ws_bytes, stream, nullptr, 1, saved[0], dy[0].cols, &bi, &ps,
+                             batched));
   }
-  return launch_group(ps, S(stream));
+  return launch_group(ps, st);
 }
 
 fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const float* dy_amax, fp8_hp_t x,
@@ -1095,7 +1195,7 @@ static fp8_status_t linear_bwd_impl(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, co
                                     const void* saved, const fp8_tensor_t* w_fp8, void* dx, float* dx_amax, void* dw,
                                     void* ws, size_t ws_bytes, void* stream, fp8_p2p_t rs_win, int rs_nranks,
                                     const void* saved_x, int64_t n_x, const BwdWs* bw_in,
-                                    std::vector<GemmProblem>* defer) {
+                                    std::vector<GemmProblem>* defer, bool cast_done) {
   FP8T_TRY(check_hp(dy, "dy"));
   const int64_t M = dy.rows, N = dy.cols, K = x.cols;
   const bool gw_hp = cfg && cfg->recipe == FP8_RECIPE_ROWWISE_GW_HP;
@@ -1143,6 +1243,7 @@ static fp8_status_t linear_bwd_impl(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, co
     float* ar = bw.amax;
     float* ac = ar + M;
     const bool colcopy = dw && !gw_hp;   // gw_hp: dW is a BF16 GEMM on the hp dY
+    if (cast_done) goto gemms;           // a shared-input group cast every member's dY by one launch pair
     if (!dx && !colcopy) goto gemms;
     FP8T_CUDA(cudaMemsetAsync(bw.amax, 0, 4 * (M + N), st), "memset");
     FP8T_CUDA(launch_amax(dy.ptr, gb, M, N, dy.ld, colcopy ? (dx ? 6 : 4) : 2, nullptr, (uint32_t*)ar,

@@ -394,6 +394,152 @@ __global__ void __launch_bounds__(256) amax_tile_tma_kernel(const __grid_constan
   }
 }
 
+// ---------------------------------------------------------------------------
+// amax_rc: row / column amax of up to AMAX_RC_MAX bf16 tensors in one launch (knob amax_rc; the
+// product path for row / column amax).  Same outputs as amax_tile_tma_kernel, without a CTA-wide
+// barrier per tile:
+//   * one producer warp streams each 128 x 128 tile as two 64-column TMA boxes (SWIZZLE_128B) into an
+//     ST-deep ring (full barrier: TMA bytes; empty barrier: one arrival per consumer warp);
+//   * consumer warp w owns the 16 columns [16w, 16w + 16) of every tile, lane l reads 8 of them
+//     (16 bytes) on rows l % 16 + 16 i -- with the 128-byte swizzle the 8 lanes of a shared-memory
+//     phase hit 8 different bank groups.  A warp releases the stage right after its loads;
+//   * column maxima: a 16-lane shuffle reduction per tile, then one atomicMax per column (the 8 lanes
+//     of each half-warp holding the 8 columns);
+//   * row maxima stay in registers while the CTA's contiguous tile range walks a 128-row strip and are
+//     flushed (xor-16 shuffle + one atomicMax per row and warp) when the strip changes.
+// Tensors are numbered consecutively: tiles [tstart[k], tstart[k+1]) belong to tensor k, row-major over
+// its tile grid.  seg (grouped recipe) applies to tensor 0's column outputs.
+// ---------------------------------------------------------------------------
+template <int MODE, int ST>
+__global__ void __launch_bounds__(288) amax_rc_kernel(const __grid_constant__ AmaxRCArgs a) {
+  constexpr int STAGE = 128 * 256, BOX = STAGE / 2;
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  const uint32_t raw0 = smem_u32(sm_raw);
+  const uint32_t base = (raw0 + 1023u) & ~1023u;   // SWIZZLE_128B boxes need 1024-byte alignment
+  const uint8_t* smp = sm_raw + (base - raw0);
+  const uint32_t full0 = base + ST * STAGE, empty0 = full0 + 8 * ST;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int total = a.tstart[a.n];
+  // dbg bit 1 (A/B only): tiles handed out interleaved (CTA b: b, b + G, ...) instead of contiguous ranges
+  const bool ilv = a.dbg & 2;
+  const int per = ilv ? 1 : (total + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int first = ilv ? (int)blockIdx.x : (int)blockIdx.x * per;
+  const int last = ilv ? total : min(first + per, total);
+  const int step = ilv ? (int)gridDim.x : 1;
+  if (t == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(full0 + 8 * i, 1);
+      mbar_init(empty0 + 8 * i, 8);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto where = [&](int id, int& k, int& rt, int& ct) {
+    k = 0;
+    while (k + 1 < a.n && id >= a.tstart[k + 1]) ++k;
+    const int local = id - a.tstart[k];
+    rt = local / a.tiles_x[k];
+    ct = local - rt * a.tiles_x[k];
+  };
+  if (warp == 8) {   // producer
+    if (lane == 0) {
+      for (int i = 0; i < a.n; ++i) tma_prefetch_desc(&a.map[i]);
+      const uint64_t pol = l2_policy_evict_first();
+      for (int k = 0; first + k * step < last; ++k) {
+        const int s = k % ST;
+        if (k >= ST) {
+          mbar_wait(empty0 + 8 * s, (uint32_t)(k / ST - 1) & 1u);
+          fence_proxy_async_smem();
+        }
+        int kk, rt, ct;
+        where(first + k * step, kk, rt, ct);
+        mbar_arrive_expect_tx(full0 + 8 * s, STAGE);
+        tma_load_2d(base + s * STAGE, &a.map[kk], ct * 128, rt * 128, full0 + 8 * s, pol);
+        tma_load_2d(base + s * STAGE + BOX, &a.map[kk], ct * 128 + 64, rt * 128, full0 + 8 * s, pol);
+      }
+    }
+    return;
+  }
+  const int r16 = lane & 15;
+  const int ch = (warp & 3) * 2 + (lane >> 4);   // 16-byte chunk of the 128-byte box row
+  const uint32_t off = (uint32_t)(warp >> 2) * BOX + r16 * 128 + ((ch ^ (r16 & 7)) << 4);
+  const int colw = (warp >> 2) * 64 + (warp & 3) * 16 + (lane >> 4) * 8;   // first column of the thread's 8
+  uint32_t rm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int strip = -1, fk = 0, frt = 0;
+  auto flush_rows = [&]() {
+    uint32_t* rowp = a.row[fk] + (int64_t)frt * 128;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t m = max(rm[i], __shfl_xor_sync(0xffffffffu, rm[i], 16));
+      if (lane < 16 && m) atomicMax(rowp + lane + 16 * i, m);
+      rm[i] = 0;
+    }
+  };
+  for (int k = 0; first + k * step < last; ++k) {
+    int kk, rt, ct;
+    where(first + k * step, kk, rt, ct);
+    if (a.dbg & 1) {   // A/B only: consume nothing (the TMA stream alone), results invalid
+      const int s = k % ST;
+      mbar_wait(full0 + 8 * s, (uint32_t)(k / ST) & 1u);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * s);
+      continue;
+    }
+    if (MODE & 2) {
+      const int skey = a.strip0[kk] + rt;
+      if (skey != strip) {
+        if (strip >= 0) flush_rows();
+        strip = skey;
+        fk = kk;
+        frt = rt;
+      }
+    }
+    const int s = k % ST;
+    mbar_wait(full0 + 8 * s, (uint32_t)(k / ST) & 1u);
+    uint4 raw[8];
+    const uint8_t* sp = smp + s * STAGE + off;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) raw[i] = *reinterpret_cast<const uint4*>(sp + i * 16 * 128);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * s);
+    uint32_t cm[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t a0 = raw[i].x & 0x7FFF7FFFu, a1 = raw[i].y & 0x7FFF7FFFu;
+      const uint32_t a2 = raw[i].z & 0x7FFF7FFFu, a3 = raw[i].w & 0x7FFF7FFFu;
+      if (MODE & 4) {
+        cm[0] = __vmaxu2(cm[0], a0); cm[1] = __vmaxu2(cm[1], a1);
+        cm[2] = __vmaxu2(cm[2], a2); cm[3] = __vmaxu2(cm[3], a3);
+      }
+      if (MODE & 2) {
+        const uint32_t m2 = __vmaxu2(__vmaxu2(a0, a1), __vmaxu2(a2, a3));
+        rm[i] = max(rm[i], max(m2 & 0xFFFFu, m2 >> 16) << 16);
+      }
+    }
+    if (MODE & 4) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        cm[j] = __vmaxu2(cm[j], __shfl_xor_sync(0xffffffffu, cm[j], 1));
+        cm[j] = __vmaxu2(cm[j], __shfl_xor_sync(0xffffffffu, cm[j], 2));
+        cm[j] = __vmaxu2(cm[j], __shfl_xor_sync(0xffffffffu, cm[j], 4));
+        cm[j] = __vmaxu2(cm[j], __shfl_xor_sync(0xffffffffu, cm[j], 8));
+      }
+      if (r16 < 8) {   // lane r16 of each half-warp: column colw + r16 (word r16 / 2, high half if odd)
+        const int j = r16 >> 1;
+        const uint32_t w = j == 0 ? cm[0] : j == 1 ? cm[1] : j == 2 ? cm[2] : cm[3];
+        const uint32_t v = (r16 & 1) ? (w & 0xFFFF0000u) : (w << 16);
+        int64_t cbase = 0;
+        if (kk == 0 && (a.seg.offs || a.seg.seg_rows > 0)) {
+          int64_t sstart;
+          cbase = (int64_t)seg_of(a.seg, (int64_t)rt * 128, sstart) * a.C[0];
+        }
+        if (v) atomicMax(a.col[kk] + cbase + (int64_t)ct * 128 + colw + r16, v);
+      }
+    }
+  }
+  if ((MODE & 2) && strip >= 0) flush_rows();
+}
+
 // Tensorwise amax of a contiguous tensor: persistent grid-stride stream of 16-byte vectors,
 // 8 independent loads in flight per thread, |x| max on raw bit patterns (bf16: two 16-bit
 // lanes per word via __vmaxu2), one atomicMax per CTA.
@@ -596,15 +742,16 @@ __global__ void __launch_bounds__(256) cast_tile_kernel(const T* __restrict__ x,
                                   rtile % (int)gridDim.x, rtile / (int)gridDim.x);
 }
 
-// Two tensors (the forward's X and W) cast by one launch: a 1-D grid over the tiles of both, walked in
-// decreasing order over [X tiles, W tiles] (the reverse of the dual amax launch), so the small weight
-// costs no launch ramp and tail of its own.
+// Several tensors (the forward's X and W; a shared-input group's X and every W_i, or every member's dY)
+// cast by one launch: a 1-D grid over the tiles of all, walked in decreasing order over
+// [tensor 0 tiles, tensor 1 tiles, ...] (the reverse of the multi-tensor amax launch), so the small
+// tensors cost no launch ramp and tail of their own.
 template <typename T, int FMT, int QM, int TM_>
-__global__ void __launch_bounds__(256) cast_tile_dual_kernel(const CastDual a) {
-  const int total = a.tiles[0] + a.tiles[1];
-  int id = total - 1 - (int)blockIdx.x;
-  const int k = id >= a.tiles[0] ? 1 : 0;
-  if (k) id -= a.tiles[0];
+__global__ void __launch_bounds__(256) cast_tile_dual_kernel(const __grid_constant__ CastMulti a) {
+  int id = a.tstart[a.n] - 1 - (int)blockIdx.x;
+  int k = 0;
+  while (k + 1 < a.n && id >= a.tstart[k + 1]) ++k;
+  id -= a.tstart[k];
   const int tx = (int)((a.C[k] + 127) / 128);
   cast_tile_body<T, FMT, QM, TM_>(static_cast<const T*>(a.x[k]), a.R[k], a.C[k], a.ld[k], a.amax_q[k], a.amax_t[k],
                                   a.q[k], a.qt[k], a.scale_q[k], a.scale_t[k], Seg{}, id % tx, id / tx);
@@ -993,6 +1140,61 @@ static cudaError_t amax_tma_go(const CUtensorMap& m, int64_t R, int64_t C, int64
   return cudaGetLastError();
 }
 
+// Row / column amax of n bf16 tensors by one amax_rc launch (outputs pre-zeroed).  cudaErrorNotSupported
+// when a shape does not fit the TMA path (rows or columns not multiples of 128, unaligned rows).
+cudaError_t launch_amax_rc(const AmaxRCTensor* ts, int n, int mode, cudaStream_t st, const Seg& seg) {
+  auto enc = get_encode();
+  if (!enc || n < 1 || n > AMAX_RC_MAX || (mode != 2 && mode != 4 && mode != 6)) return cudaErrorNotSupported;
+  AmaxRCArgs a{};
+  a.n = n;
+  a.seg = seg;
+  a.dbg = knob(KNOB_AMAX_RC_DEBUG);
+  for (int k = 0; k < n; ++k) {
+    const AmaxRCTensor& x = ts[k];
+    if (x.R <= 0 || x.C <= 0 || x.R % 128 || x.C % 128 || (x.ld * 2) % 16 || (reinterpret_cast<uintptr_t>(x.x) & 15))
+      return cudaErrorNotSupported;
+    cuuint64_t dims[2] = {(cuuint64_t)x.C, (cuuint64_t)x.R};
+    cuuint64_t strides[1] = {(cuuint64_t)x.ld * 2};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc(&a.map[k], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x.x), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorNotSupported;
+    const int64_t tr = x.R / 128, tc = x.C / 128;
+    if ((int64_t)a.tstart[k] + tr * tc > (int64_t)INT32_MAX) return cudaErrorNotSupported;
+    a.tstart[k + 1] = a.tstart[k] + (int)(tr * tc);
+    a.tiles_x[k] = (int)tc;
+    a.strip0[k] = k ? a.strip0[k - 1] + (int)(ts[k - 1].R / 128) : 0;
+    a.C[k] = x.C;
+    a.row[k] = x.row;
+    a.col[k] = x.col;
+    if (((mode & 2) && !x.row) || ((mode & 4) && !x.col)) return cudaErrorInvalidValue;
+  }
+  constexpr int ST = 3;
+  constexpr int smem = ST * 128 * 256 + 1024 + 16 * ST;
+  const int64_t all = a.tstart[n];
+  const int64_t cap = cap_grid((int64_t)sm_count() * 2);
+  const unsigned g = (unsigned)(all < cap ? all : cap);
+  cudaError_t e = cudaSuccess;
+  LaunchScope ls(K_AMAX, st);
+  switch (mode) {
+    case 2:
+      if ((e = ensure_smem<amax_rc_kernel<2, ST>>(smem)) != cudaSuccess) return e;
+      amax_rc_kernel<2, ST><<<g, 288, smem, st>>>(a);
+      break;
+    case 4:
+      if ((e = ensure_smem<amax_rc_kernel<4, ST>>(smem)) != cudaSuccess) return e;
+      amax_rc_kernel<4, ST><<<g, 288, smem, st>>>(a);
+      break;
+    default:
+      if ((e = ensure_smem<amax_rc_kernel<6, ST>>(smem)) != cudaSuccess) return e;
+      amax_rc_kernel<6, ST><<<g, 288, smem, st>>>(a);
+      break;
+  }
+  return cudaGetLastError();
+}
+
 static cudaError_t amax_bulk_go(const void* x0, int64_t b0, uint32_t* out0, const void* x1, int64_t b1, uint32_t* out1,
                                 bool bf16, cudaStream_t st);
 
@@ -1021,6 +1223,11 @@ static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
     return cudaGetLastError();
   }
   const int64_t tiles = ((R + 127) / 128) * ((C + 127) / 128);
+  if (sizeof(T) == 2 && mode != 1 && knob(KNOB_AMAX_RC) == 1) {
+    const AmaxRCTensor one{x, R, C, ld, ar, ac};
+    const cudaError_t e = launch_amax_rc(&one, 1, mode, st, seg);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (sizeof(T) == 2 && R % 128 == 0 && C % 128 == 0 && mode != 1 && amax_tile_use_tma()) {
     auto enc = get_encode();
     CUtensorMap m;
@@ -1058,6 +1265,10 @@ static cudaError_t amax_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
 cudaError_t launch_amax_dual(const void* x0, int64_t R0, int64_t C0, int64_t ld0, const void* x1, int64_t R1, int64_t C1,
                              int64_t ld1, int mode, uint32_t* ar0, uint32_t* ac0, uint32_t* ar1, uint32_t* ac1,
                              cudaStream_t st) {
+  if (knob(KNOB_AMAX_RC) == 1) {
+    const AmaxRCTensor two[2] = {{x0, R0, C0, ld0, ar0, ac0}, {x1, R1, C1, ld1, ar1, ac1}};
+    return launch_amax_rc(two, 2, mode, st);
+  }
   auto enc = get_encode();
   if (!enc || !amax_tile_use_tma() || (mode != 2 && mode != 4 && mode != 6)) return cudaErrorNotSupported;
   const void* xs[2] = {x0, x1};
@@ -1252,8 +1463,9 @@ static cudaError_t cast_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
 }
 
 template <typename T, int FMT>
-static cudaError_t cast_dual_launch_t(const CastDual& a, int qm, int tm, cudaStream_t s) {
-  const unsigned g = (unsigned)(a.tiles[0] + a.tiles[1]);
+static cudaError_t cast_dual_launch_t(const CastMulti& a, int qm, int tm, cudaStream_t s) {
+  const unsigned g = (unsigned)a.tstart[a.n];
+  if (g == 0) return cudaSuccess;
 #define FP8T_CAST2(QM, TM)                                                          \
   if (qm == QM && tm == TM) {                                                       \
     LaunchScope ls(K_CAST, s);                                                      \
@@ -1265,8 +1477,15 @@ static cudaError_t cast_dual_launch_t(const CastDual& a, int qm, int tm, cudaStr
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_cast_dual(CastDual a, bool bf16, int fmt, int qm, int tm, cudaStream_t s) {
-  for (int k = 0; k < 2; ++k) a.tiles[k] = (int)(((a.R[k] + 127) / 128) * ((a.C[k] + 127) / 128));
+cudaError_t launch_cast_dual(CastMulti a, bool bf16, int fmt, int qm, int tm, cudaStream_t s) {
+  if (a.n == 0) a.n = 2;
+  if (a.n < 1 || a.n > CAST_MULTI_MAX) return cudaErrorInvalidValue;
+  a.tstart[0] = 0;
+  for (int k = 0; k < a.n; ++k) {
+    const int64_t tiles = ((a.R[k] + 127) / 128) * ((a.C[k] + 127) / 128);
+    if (a.tstart[k] + tiles > (int64_t)INT32_MAX) return cudaErrorInvalidValue;
+    a.tstart[k + 1] = a.tstart[k] + (int)tiles;
+  }
   if (bf16)
     return fmt == 0 ? cast_dual_launch_t<__nv_bfloat16, 0>(a, qm, tm, s) : cast_dual_launch_t<__nv_bfloat16, 1>(a, qm, tm, s);
   return fmt == 0 ? cast_dual_launch_t<float, 0>(a, qm, tm, s) : cast_dual_launch_t<float, 1>(a, qm, tm, s);

@@ -31,10 +31,13 @@ enum Knob {
   KNOB_MX_TRANSPOSED,       // 1: MX dim1 copies written transposed, read K-major (fwd and bwd must agree)
   KNOB_TW_DUAL,             // 1: tensorwise forward X/W amax and cast by one launch each; 0: four launches
   KNOB_GEMM_KSERP,          // 1: odd waves of GEMM tiles walk K backwards (L2 reuse across waves); 0: all forward
-  KNOB_GEMM_N512,
-  KNOB_GEMM_L2PF,
-  KNOB_MX_CAST_OCC3,
-  KNOB_AMAX_BULK,           // 1: tensorwise amax of contiguous tensors through 1-D bulk copies into a smem ring        // 1: MX cast (dim0 + dim1, row-major dim1) with a 2-deep ring at 3 CTAs per SM           // >0: the GEMM producer prefetches operand boxes this many stages ahead into L2           // 1: plain FP8 GEMMs with every N % 512 == 0 use 256 x 512 CTA-pair tiles
+  KNOB_GEMM_N512,           // 1: plain FP8 GEMMs with every N % 512 == 0 use 256 x 512 CTA-pair tiles (2: auto, K >= 8192)
+  KNOB_GEMM_L2PF,           // >0: the GEMM producer prefetches operand boxes this many stages ahead into L2
+  KNOB_MX_CAST_OCC3,        // 1: MX cast (dim0 + dim1, row-major dim1) with a 2-deep ring at 3 CTAs per SM
+  KNOB_AMAX_BULK,           // 1: tensorwise amax of contiguous tensors through 1-D bulk copies into a smem ring
+  KNOB_AMAX_RC,             // 1: row / column amax by amax_rc_kernel (no CTA barrier per tile, multi-tensor)
+  KNOB_AMAX_RC_DEBUG,       // A/B only: bit 0 consumers skip the tile (results invalid), bit 1 interleaved tile order
+  KNOB_GROUP_BATCH,         // 1: a rowwise shared-input group's amax / cast launches batched over X + every W_i (fwd), every dY_i (bwd)
   KNOB_WATCHDOG_MS,         // peer waits (P2P gather, fused reduce-scatter, async-TP) give up after this many ms
                             // and report FP8_ECUDA at the next call; 0 = wait forever
   KNOB_COUNT
@@ -113,21 +116,48 @@ cudaError_t launch_amax_dual(const void* x0, int64_t R0, int64_t C0, int64_t ld0
                              int64_t ld1, int mode, uint32_t* ar0, uint32_t* ac0, uint32_t* ar1, uint32_t* ac1,
                              cudaStream_t st);
 // Tensorwise amax of two contiguous tensors (same dtype) in one launch; outputs pre-zeroed.
+// Row (mode 2) / column (4) / row+column (6) amax of up to AMAX_RC_MAX bf16 tensors in one launch
+// (amax_rc_kernel); outputs pre-zeroed; cudaErrorNotSupported if a shape does not fit the TMA path.
+constexpr int AMAX_RC_MAX = 9;   // X + FP8_SHARED_MAX weights
+struct AmaxRCTensor {
+  const void* x;
+  int64_t R, C, ld;
+  uint32_t* row;   // [R] (mode & 2)
+  uint32_t* col;   // [C] (mode & 4; [G][C] for tensor 0 with a Seg)
+};
+struct AmaxRCArgs {
+  CUtensorMap map[AMAX_RC_MAX];
+  int n;
+  int tstart[AMAX_RC_MAX + 1];
+  int tiles_x[AMAX_RC_MAX];
+  int strip0[AMAX_RC_MAX];
+  int64_t C[AMAX_RC_MAX];
+  uint32_t* row[AMAX_RC_MAX];
+  uint32_t* col[AMAX_RC_MAX];
+  Seg seg;
+  int dbg;   // knob amax_rc_debug (A/B experiments only)
+};
+cudaError_t launch_amax_rc(const AmaxRCTensor* ts, int n, int mode, cudaStream_t st, const Seg& seg = Seg{});
 cudaError_t launch_amax_flat_dual(const void* x0, int64_t n0_elems, uint32_t* out0, const void* x1, int64_t n1_elems,
                                   uint32_t* out1, bool bf16, cudaStream_t st);
 // Two tensors (same format and scale modes) cast by one launch; tiles[] is filled by the launcher.
-struct CastDual {
-  const void* x[2];
-  int64_t R[2], C[2], ld[2];
-  const float* amax_q[2];
-  const float* amax_t[2];
-  uint8_t* q[2];
-  uint8_t* qt[2];
-  float* scale_q[2];
-  float* scale_t[2];
-  int tiles[2];
+// Up to CAST_MULTI_MAX tensors (same format and scale modes) cast by one launch: tensor k's tiles follow
+// tensor k-1's; n = 0 is read as 2 (the forward's X and W); tstart[] is filled by the launcher.
+constexpr int CAST_MULTI_MAX = 9;
+struct CastMulti {
+  const void* x[CAST_MULTI_MAX];
+  int64_t R[CAST_MULTI_MAX], C[CAST_MULTI_MAX], ld[CAST_MULTI_MAX];
+  const float* amax_q[CAST_MULTI_MAX];
+  const float* amax_t[CAST_MULTI_MAX];
+  uint8_t* q[CAST_MULTI_MAX];
+  uint8_t* qt[CAST_MULTI_MAX];
+  float* scale_q[CAST_MULTI_MAX];
+  float* scale_t[CAST_MULTI_MAX];
+  int n;
+  int tstart[CAST_MULTI_MAX + 1];
 };
-cudaError_t launch_cast_dual(CastDual a, bool bf16, int fmt, int qm, int tm, cudaStream_t s);
+using CastDual = CastMulti;
+cudaError_t launch_cast_dual(CastMulti a, bool bf16, int fmt, int qm, int tm, cudaStream_t s);
 // Tensorwise amax of n <= AMAX_MULTI_MAX tensors in one launch; out[t] (u32 bit patterns of
 // non-negative floats) must be zeroed by the caller.  chunk_start[t] = first warp chunk of
 // tensor t (chunks of 256 16-byte vectors within one row), chunk_start[n] = total.

@@ -871,13 +871,18 @@ def test_grouped_single_expert_equals_linear():
     assert torch.equal(y1, y2) and torch.equal(dx1, dx2) and torch.equal(dw1, dw2)
 
 
+AMAX_IMPLS = {"rc": {"amax_rc": 1}, "tma": {"amax_rc": 0, "amax_tile_tma": 1}, "regs": {"amax_rc": 0, "amax_tile_tma": 0}}
+
+
 @pytest.mark.parametrize("grid", ["0", "1", "5"])
-@pytest.mark.parametrize("impl", ["1", "0"])
+@pytest.mark.parametrize("impl", list(AMAX_IMPLS))
 def test_amax_tile_strips(grid, impl, knob):
-    """Row / column / dual amax on 128-multiple shapes (the TMA strip kernel, knob amax_tile_tma = 1, and the
-    register kernel), with capped persistent grids so CTAs cross row strips: bit-exact vs the oracle."""
+    """Row / column / dual amax on 128-multiple shapes (the multi-tensor warp-specialised kernel, knob
+    amax_rc = 1; the TMA strip kernel; the register kernel), with capped persistent grids so CTAs cross
+    row strips: bit-exact vs the oracle."""
     knob("cast_grid", int(grid))
-    knob("amax_tile_tma", int(impl))
+    for k, v in AMAX_IMPLS[impl].items():
+        knob(k, v)
     x = synth.tensor_c3("x", (384, 1280), seed=9)
     X = _dev(x, torch.bfloat16)
     assert np.array_equal(_bits(_np(ops.amax(X, "row"))), _bits(fp8.amax(x, 1)))
@@ -1142,7 +1147,8 @@ def test_linear_strided_inputs(recipe):
 LINEAR_BUFFER_CASES = [
     ("tensorwise", {}), ("tensorwise", {"tw_dual": 0}), ("tensorwise", {"amax_bulk": 1}),
     ("tensorwise", {"amax_bulk": 1, "tw_dual": 0}),
-    ("rowwise", {}), ("rowwise", {"cast_grid": 3}), ("rowwise", {"cast_grid": 7}), ("rowwise", {"amax_tile_tma": 0}),
+    ("rowwise", {}), ("rowwise", {"cast_grid": 3}), ("rowwise", {"cast_grid": 7}), ("rowwise", {"amax_rc": 0}),
+    ("rowwise", {"amax_rc": 0, "amax_tile_tma": 0}), ("rowwise", {"amax_rc": 1, "cast_grid": 5}),
     ("rowwise_gw_hp", {}),
     ("mxfp8", {}), ("mxfp8", {"cast_grid": 3}), ("mxfp8", {"mx_transposed": 1}), ("mxfp8", {"mx_cast_tma": 0}),
     ("mxfp8", {"mx_cast_occ3": 1}), ("mxfp8", {"mx_cast_occ3": 1, "cast_grid": 5}),
@@ -1236,8 +1242,8 @@ def test_linear_buffers_bit_exact(recipe, knobs, shape, knob):
 
 
 @pytest.mark.parametrize("recipe,variants", [("tensorwise", [{}, {"tw_dual": 0}]),
-                                             ("rowwise", [{}, {"cast_grid": 3}, {"cast_grid": 7},
-                                                          {"amax_tile_tma": 0}])])
+                                             ("rowwise", [{}, {"cast_grid": 3}, {"cast_grid": 7}, {"amax_rc": 0},
+                                                          {"amax_rc": 0, "amax_tile_tma": 0}])])
 def test_linear_cast_launch_variants_identical(recipe, variants, knob):
     """The cast-launch variants of one recipe write identical bytes (saved buffers and forward
     workspace) and give bit-identical Y, dX, dW (same codes -> same GEMM inputs)."""
@@ -1594,8 +1600,8 @@ def test_amax_tensor_kernels(shape, dtype, bulk, knob):
     assert _bits(_np(got))[0] == _bits(fp8.amax(_np(X.float()))).reshape(-1)[0]
 
 
-SHARED_CASES = [("tensorwise", {}), ("tensorwise", {"tw_dual": 0}), ("rowwise", {}), ("rowwise", {"amax_tile_tma": 0}),
-                ("rowwise_gw_hp", {}), ("mxfp8", {}), ("mxfp8", {"mx_transposed": 1})]
+SHARED_CASES = [("tensorwise", {}), ("tensorwise", {"tw_dual": 0}), ("rowwise", {}), ("rowwise", {"amax_rc": 0, "amax_tile_tma": 0}),
+                ("rowwise", {"cast_grid": 5}), ("rowwise", {"group_batch": 0}), ("rowwise_gw_hp", {}), ("mxfp8", {}), ("mxfp8", {"mx_transposed": 1})]
 
 
 @pytest.mark.parametrize("M,K,Ns", [(384, 512, (640, 128, 256)), (256, 384, (128, 512)), (384, 256, (384,)),

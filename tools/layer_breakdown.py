@@ -1,7 +1,7 @@
 """Per-launch device times of one c3 (7-linear layer) step, in-step (not serialised like ncu): which
 amax / cast / GEMM launches lose time against their algorithmic bytes or flops.  Tuning context only.
 
-    python tools/layer_breakdown.py [config] [steps] [--separate]
+    python tools/layer_breakdown.py [config] [steps] [--separate] [--knob=name=value ...]
 """
 import ctypes
 import os
@@ -25,6 +25,10 @@ def main():
     torch.cuda.set_device(dev)
     M = cfg["M"]
     shared = "--separate" not in sys.argv
+    for a in sys.argv[1:]:
+        if a.startswith("--knob="):
+            k, v = a[len("--knob="):].split("=")
+            ops.set_knob(k, int(v))
     units = []
     for i, (nm, N, K) in enumerate(cfg["linears"]):
         x, w, dy = bench.make_inputs(dict(cfg, N=N, K=K), M, N, K, 0, 1, dev, seed=i)
@@ -38,6 +42,7 @@ def main():
     grouped = {id(u) for g in groups for u in g}
     groups += [[u] for u in units if id(u) not in grouped]
     groups.sort(key=lambda g: units.index(g[0]))
+    batched = cfg["recipe"] == "rowwise" and ops.get_knob("group_batch") == 1
     work = []   # (label, algorithmic bytes or flops, "B" / "F") per launch, in launch order
     for g in groups:
         K = g[0]["K"]
@@ -55,6 +60,14 @@ def main():
                 u["saved"] = t
             g[0]["group_plan"] = sp
         # amax: read 2 B / element; cast: read 2 + two 1-B copies
+        if batched and len(g) > 1:   # rowwise group: one amax + one cast launch over X and every W_i / dY_i
+            xw = M * K + sum(u["N"] * K for u in g)
+            work += [("amax X,W " + names, 2 * xw, "B"), ("cast X,W " + names, 4 * xw, "B")]
+            work += [("gemm fwd " + names, sum(2 * M * u["N"] * K for u in g), "F")]
+            gy = sum(M * u["N"] for u in g)
+            work += [("amax dY " + names, 2 * gy, "B"), ("cast dY " + names, 4 * gy, "B")]
+            work += [("gemm bwd " + names, sum(4 * M * u["N"] * K for u in g), "F")]
+            continue
         for j, u in enumerate(g):
             xw = (M * K if j == 0 else 0) + u["N"] * K
             lab = ("X," if j == 0 else "") + "W " + u["name"]
