@@ -576,6 +576,39 @@ def test_float8linear_fp32_module(recipe):
     _tol_check(_np(model[0].weight.grad).astype(np.float64), dw, dwb)
 
 
+@pytest.mark.parametrize("recipe", ["tensorwise", "rowwise", "rowwise_gw_hp", "mxfp8"])
+def test_linear_first_cuda_call_on_fresh_thread(recipe):
+    """A LinearPlan forward + backward whose launches are the first CUDA work of a new host thread (as in
+    PyTorch's autograd worker): the tensor-map encodes are driver-API calls that need a current context,
+    which the library binds itself.  Results equal the same calls on the main thread."""
+    import threading
+    M, N, K = 256, 384, 512
+    x, w, dy = synth.linear_inputs("c4", M, N, K, seed=17)
+    X, W, G = _dev(x, torch.bfloat16), _dev(w, torch.bfloat16), _dev(dy, torch.bfloat16)
+    plan = ops.LinearPlan(M, N, K, recipe=recipe)
+    ref_saved = plan.new_saved()
+    y0 = plan.forward(X, W, ref_saved).clone()
+    dx0, dw0 = (t.clone() for t in plan.backward(G, ref_saved, x=X))
+    saved = plan.new_saved()
+    torch.cuda.synchronize()
+    out, err = {}, []
+
+    def work():
+        try:
+            y = plan.forward(X, W, saved)
+            dx, dw = plan.backward(G, saved, x=X)
+            torch.cuda.synchronize()
+            out.update(y=y, dx=dx, dw=dw)
+        except Exception as e:   # reported on the main thread
+            err.append(e)
+
+    th = threading.Thread(target=work)
+    th.start()
+    th.join()
+    assert not err, err
+    assert torch.equal(out["y"], y0) and torch.equal(out["dx"], dx0) and torch.equal(out["dw"], dw0)
+
+
 def test_float8linear_gw_hp_detects_inplace_input_change():
     """rowwise_gw_hp keeps X for its BF16 dW GEMM through save_for_backward: changing X in place
     between forward and backward raises instead of silently corrupting dW."""
@@ -591,13 +624,16 @@ def test_float8linear_gw_hp_detects_inplace_input_change():
         Y.float().sum().backward()
 
 
+@pytest.mark.parametrize("ws", ["1", "0"])
 @pytest.mark.parametrize("grid", ["1", "3"])
 @pytest.mark.parametrize("gran", ["mx32", "mx32_rm"])
 @pytest.mark.parametrize("fmt,mode", [(E4M3, omx.FLOOR), (E5M2, omx.RCEIL)])
-def test_mx_cast_persistent_ring(grid, gran, fmt, mode, knob):
-    # the TMA-pipelined MX cast walks many tiles per CTA when the grid is capped: every
-    # shared-memory ring slot is refilled several times (mbarrier parity wrap-around)
+def test_mx_cast_persistent_ring(grid, gran, fmt, mode, ws, knob):
+    # the TMA-pipelined MX casts (warp-specialised kernel, knob mx_cast_ws = 1; the ring kernel) walk
+    # many tiles per CTA when the grid is capped: every shared-memory ring slot and E8M0 staging buffer
+    # is refilled several times (mbarrier parity wrap-around)
     knob("cast_grid", int(grid))
+    knob("mx_cast_ws", int(ws))
     R, C = 512, 1280   # 40 tiles
     x = synth.tensor_c4("x", (R, C), seed=5)
     q0, s0 = omx.quantize_dim0(x, fmt, mode)
@@ -613,11 +649,12 @@ def test_mx_cast_persistent_ring(grid, gran, fmt, mode, knob):
     assert np.array_equal(_np(out["q_t"]), q1.T if gran == "mx32_rm" else q1)
 
 
-@pytest.mark.parametrize("impl", ["0", "1"])
+@pytest.mark.parametrize("impl", ["0", "1", "ring"])
 def test_mx_cast_impls_agree_c4_sized(impl, knob):
-    # both MX cast kernels (register-only: knob mx_cast_tma = 0; TMA ring: default) on a C4-like
-    # tensor with many tiles per CTA, sampled rows against the oracle
-    knob("mx_cast_tma", int(impl))
+    # the MX cast kernels (register-only: knob mx_cast_tma = 0; TMA ring: mx_cast_ws = 0; warp-specialised:
+    # default) on a C4-like tensor with many tiles per CTA, sampled rows against the oracle
+    knob("mx_cast_tma", 0 if impl == "0" else 1)
+    knob("mx_cast_ws", 0 if impl == "ring" else 1)
     R, C = 2048, 8192
     x = synth.tensor_c4("x", (R, C), seed=7)
     out = ops.cast(_dev(x, torch.bfloat16), "e4m3", "mx32_rm", want_q=True, want_qt=True)
@@ -1150,7 +1187,7 @@ LINEAR_BUFFER_CASES = [
     ("rowwise", {}), ("rowwise", {"cast_grid": 3}), ("rowwise", {"cast_grid": 7}), ("rowwise", {"amax_rc": 0}),
     ("rowwise", {"amax_rc": 0, "amax_tile_tma": 0}), ("rowwise", {"amax_rc": 1, "cast_grid": 5}),
     ("rowwise_gw_hp", {}),
-    ("mxfp8", {}), ("mxfp8", {"cast_grid": 3}), ("mxfp8", {"mx_transposed": 1}), ("mxfp8", {"mx_cast_tma": 0}),
+    ("mxfp8", {}), ("mxfp8", {"cast_grid": 3}), ("mxfp8", {"mx_transposed": 1}), ("mxfp8", {"mx_cast_tma": 0}), ("mxfp8", {"mx_cast_ws": 0}),
     ("mxfp8", {"mx_cast_occ3": 1}), ("mxfp8", {"mx_cast_occ3": 1, "cast_grid": 5}),
 ]
 
