@@ -108,6 +108,8 @@ struct GemmArgs {
   int sf_split;       // MX: scale-factor copies issued by their own warp (see the SF copier)
   int kserp;          // K-serpentine: tiles of odd "waves" (tile / pairs) walk their K stages backwards
   int l2pf;           // L2 prefetch distance of the operand boxes, in stages (0 = off)
+  int st_ef;          // bf16 outputs stored with an L2 evict-first hint (written back during the GEMM, so the
+                      // next memory-bound kernel does not pay for evicting them)
   unsigned* fault;    // process fault word (async-TP watchdog, bad group offsets); may be null
   unsigned long long watchdog_ns;
   unsigned* sched;    // dynamic tile scheduler slot (g_sched[i]); null: static round robin
@@ -762,6 +764,8 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(tempty_bar, 0) : tempty_bar;
     uint8_t* epi = gbase + L::off_epi + (warp - 4) * L::EPI_BYTES;   // this warp's bf16 staging slot
     const uint32_t epi_s = base + L::off_epi + (warp - 4) * L::EPI_BYTES;
+    const bool st_ef = args.st_ef != 0;
+    const uint64_t st_pol = l2_policy_evict_first();
     for (int sk = 0;;) {
       const int tile = seq_get(sk);
       if (tile >= num_tiles) break;
@@ -840,9 +844,11 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
           const int rr = 8 * i + ((int)lane >> 2), j = lane & 3;
           const uint4 val = *reinterpret_cast<const uint4*>(epi + rr * 64 + ((j ^ ((rr >> 1) & 3)) * 16));
           const int grow = row - (int)lane + rr;
-          if (grow < ti.m_valid && 8 * j < nvalid)
-            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(Dbase) + (int64_t)grow * P.ldd + col0 + 8 * j) =
-                val;
+          if (grow < ti.m_valid && 8 * j < nvalid) {
+            uint4* dp = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(Dbase) + (int64_t)grow * P.ldd + col0 + 8 * j);
+            if (st_ef) st_global_v4_hint(dp, val, st_pol);
+            else *dp = val;
+          }
         }
         __syncwarp();
       };
@@ -918,7 +924,8 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(dmap, epi_s + (c & 1) * 2048, col0 + 32 * c, (int)(ti.d_row0 + row_base));
+              if (st_ef) tma_store_2d_hint(dmap, epi_s + (c & 1) * 2048, col0 + 32 * c, (int)(ti.d_row0 + row_base), st_pol);
+              else tma_store_2d(dmap, epi_s + (c & 1) * 2048, col0 + 32 * c, (int)(ti.d_row0 + row_base));
               bulk_commit_group();
             }
           };
@@ -1212,6 +1219,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     a.sf_split = knob(KNOB_MX_SF_SPLIT);
     a.kserp = knob(KNOB_GEMM_KSERP);
     a.l2pf = knob(KNOB_GEMM_L2PF);
+    a.st_ef = knob(KNOB_GEMM_ST_EF);
     bool need_fault = GRP;
     for (int i = 0; i < n; ++i) need_fault = need_fault || ps[i].chunk_done != nullptr;
     if (need_fault) {

@@ -40,6 +40,7 @@ enum Knob {
   KNOB_GROUP_BATCH,         // 1: a rowwise shared-input group's amax / cast launches batched over X + every W_i (fwd), every dY_i (bwd)
   KNOB_MX_CAST_DEBUG,       // A/B only: bit 0 the MX TMA cast skips its code stores (results invalid)
   KNOB_MX_CAST_WS,          // 1: bf16 MX casts with row-major dim1 copies by the warp-specialised kernel
+  KNOB_GEMM_ST_EF,          // 1: GEMM bf16 outputs stored with an L2 evict-first hint
   KNOB_WATCHDOG_MS,         // peer waits (P2P gather, fused reduce-scatter, async-TP) give up after this many ms
                             // and report FP8_ECUDA at the next call; 0 = wait forever
   KNOB_COUNT
