@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(288) amax_rc_kernel(const __grid_constant__ Am
       for (int k = 0; first + k * step < last; ++k) {
         const int s = k % ST;
         if (k >= ST) {
-          mbar_wait(empty0 + 8 * s, (uint32_t)(k / ST - 1) & 1u);
+          mbar_wait_opt(empty0 + 8 * s, (uint32_t)(k / ST - 1) & 1u, a.sleep);
           fence_proxy_async_smem();
         }
         int kk, rt, ct;
@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(288) amax_rc_kernel(const __grid_constant__ Am
     where(first + k * step, kk, rt, ct);
     if (a.dbg & 1) {   // A/B only: consume nothing (the TMA stream alone), results invalid
       const int s = k % ST;
-      mbar_wait(full0 + 8 * s, (uint32_t)(k / ST) & 1u);
+      mbar_wait_opt(full0 + 8 * s, (uint32_t)(k / ST) & 1u, a.sleep);
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8 * s);
       continue;
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(288) amax_rc_kernel(const __grid_constant__ Am
       }
     }
     const int s = k % ST;
-    mbar_wait(full0 + 8 * s, (uint32_t)(k / ST) & 1u);
+    mbar_wait_opt(full0 + 8 * s, (uint32_t)(k / ST) & 1u, a.sleep);
     uint4 raw[8];
     const uint8_t* sp = smp + s * STAGE + off;
 #pragma unroll
@@ -1041,7 +1041,7 @@ template <int FMT, bool RCEIL, bool DIM0, bool DIM1, int ST>
 __global__ void __launch_bounds__(288, 2) mx_cast_ws_kernel(const __grid_constant__ CUtensorMap tmap, int64_t R,
                                                           int64_t C, uint8_t* __restrict__ q0,
                                                           uint8_t* __restrict__ sf0, uint8_t* __restrict__ q1,
-                                                          uint8_t* __restrict__ sf1) {
+                                                          uint8_t* __restrict__ sf1, int sleep) {
   constexpr int STAGE = 128 * 256;
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* sfb = sm + ST * STAGE;                       // [2][1024]: dim0 tile (512 B) + dim1 tile (512 B)
@@ -1067,7 +1067,7 @@ __global__ void __launch_bounds__(288, 2) mx_cast_ws_kernel(const __grid_constan
         if (id >= num_tiles) break;
         const int s = k % ST;
         if (k >= ST) {
-          mbar_wait(empty0 + 8 * s, (uint32_t)(k / ST - 1) & 1u);
+          mbar_wait_opt(empty0 + 8 * s, (uint32_t)(k / ST - 1) & 1u, sleep);
           fence_proxy_async_smem();
         }
         mbar_arrive_expect_tx(full0 + 8 * s, STAGE);
@@ -1097,7 +1097,7 @@ __global__ void __launch_bounds__(288, 2) mx_cast_ws_kernel(const __grid_constan
     if (id >= num_tiles) break;
     const int s = k % ST;
     const int64_t r0 = (int64_t)(id / tiles_x) * 128, c0 = (int64_t)(id % tiles_x) * 128;
-    mbar_wait(full0 + 8 * s, (uint32_t)(k / ST) & 1u);
+    mbar_wait_opt(full0 + 8 * s, (uint32_t)(k / ST) & 1u, sleep);
     uint4 raw[8];
     const uint8_t* sp = sm + s * STAGE + rl * 256 + cl * 2;
 #pragma unroll
@@ -1287,6 +1287,7 @@ cudaError_t launch_amax_rc(const AmaxRCTensor* ts, int n, int mode, cudaStream_t
   a.n = n;
   a.seg = seg;
   a.dbg = knob(KNOB_AMAX_RC_DEBUG);
+  a.sleep = (knob(KNOB_WAIT_SLEEP) & 1) != 0;
   for (int k = 0; k < n; ++k) {
     const AmaxRCTensor& x = ts[k];
     if (x.R <= 0 || x.C <= 0 || x.R % 128 || x.C % 128 || (x.ld * 2) % 16 || (reinterpret_cast<uintptr_t>(x.x) & 15))
@@ -1681,7 +1682,8 @@ static cudaError_t mx_ws_go(const CUtensorMap& m, int64_t R, int64_t C, uint8_t*
   const int64_t tiles = (R >> 7) * (C >> 7);
   const int64_t cap = cap_grid((int64_t)sm_count() * 2);
   LaunchScope ls(K_MX, s);
-  mx_cast_ws_kernel<FMT, RC, D0, D1, ST><<<(unsigned)(tiles < cap ? tiles : cap), 288, smem, s>>>(m, R, C, q0, sf0, q1, sf1);
+  mx_cast_ws_kernel<FMT, RC, D0, D1, ST><<<(unsigned)(tiles < cap ? tiles : cap), 288, smem, s>>>(m, R, C, q0, sf0, q1, sf1,
+                                                                                          knob(KNOB_WAIT_SLEEP) & 1);
   return cudaGetLastError();
 }
 

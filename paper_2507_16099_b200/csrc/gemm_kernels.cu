@@ -108,6 +108,8 @@ struct GemmArgs {
   int sf_split;       // MX: scale-factor copies issued by their own warp (see the SF copier)
   int kserp;          // K-serpentine: tiles of odd "waves" (tile / pairs) walk their K stages backwards
   int l2pf;           // L2 prefetch distance of the operand boxes, in stages (0 = off)
+  int wsleep;         // knob wait_sleep: bit 1 epilogue waits, bit 2 producer / scheduler waits, bit 3 MMA / SF waits
+                      // use the suspend-time-hint try_wait (waiting warps sleep instead of spinning)
   int st_ef;          // bf16 outputs stored with an L2 evict-first hint (written back during the GEMM, so the
                       // next memory-bound kernel does not pay for evicting them)
   unsigned* fault;    // process fault word (async-TP watchdog, bad group offsets); may be null
@@ -427,7 +429,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
     const int slot = k & (SD - 1);
     const uint32_t ph = (uint32_t)(k / SD) & 1u;
     ++k;
-    mbar_wait(sched_empty + 8 * slot, ph ^ 1u);
+    mbar_wait_opt(sched_empty + 8 * slot, ph ^ 1u, args.wsleep & 4);
     if (lane == 0) {
       asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(ring + 4 * slot), "r"(t) : "memory");
       if (CG == 2) {
@@ -533,7 +535,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
             if (b_mn && L::BN / CG > 128) tma_prefetch_l2_2d(tmB, n0 + 128, k0);
           }
         }
-        mbar_wait(empty_bar + 8 * stage, phase ^ 1);
+        mbar_wait_opt(empty_bar + 8 * stage, phase ^ 1, args.wsleep & 4);
         if (lane == 0) {
           // MX: E8M0 tiles first, on their own barrier: they land long before the operands, so the SF
           // copier has them in TMEM by the time the MMA warp sees full_bar
@@ -640,14 +642,14 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
       // N = 512: the tile's two N = 256 halves are handed over separately -- half 1's columns are awaited
       // only after half 0's MMAs of the first stage are queued, and half 0 is published to the epilogue
       // before half 1's MMAs of the last stage -- so each hand-over overlaps the other half's MMAs
-      mbar_wait(tempty_bar + 8 * acc * L::HALVES, acc_phase ^ 1);
+      mbar_wait_opt(tempty_bar + 8 * acc * L::HALVES, acc_phase ^ 1, args.wsleep & 8);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * L::BN;
       for (int kb = 0; kb < num_kb; ++kb) {
         if (!have_next && kb + 2 >= num_kb) fetch_next();
-        mbar_wait(full_bar + 8 * stage, phase);
-        if (sf_split) mbar_wait(sf_bar + 8 * stage, phase);
-        else if (MX) mbar_wait(sf_full + 8 * stage, phase);
+        mbar_wait_opt(full_bar + 8 * stage, phase, args.wsleep & 8);
+        if (sf_split) mbar_wait_opt(sf_bar + 8 * stage, phase, args.wsleep & 8);
+        else if (MX) mbar_wait_opt(sf_full + 8 * stage, phase, args.wsleep & 8);
         tc_fence_after();
         if (lane == 0) {
           // debug bits 16/32/64 (timing experiments only; results invalid): duplicate every stage's
@@ -736,7 +738,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
       if (tile >= num_tiles) break;
       const int num_kb = locate(tile).num_kb;
       for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(sf_full + 8 * stage, phase);
+        mbar_wait_opt(sf_full + 8 * stage, phase, args.wsleep & 8);
         tc_fence_after();
         if (lane == 0) {
           copy_sf(stage, tmem_base);
@@ -856,14 +858,14 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
       // this warp's accumulator barrier: per buffer, or per half of the N = 512 accumulator
       // (N = 512: the halves are awaited one by one below)
       if (L::HALVES == 1) {
-        mbar_wait(tfull_bar + 8 * acc, acc_phase);
+        mbar_wait_opt(tfull_bar + 8 * acc, acc_phase, args.wsleep & 2);
         tc_fence_after();
       }
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * L::BN;
       if (args.debug & 8) {   // timing experiment (results invalid): release the accumulator untouched
         for (int h = 0; h < L::HALVES; ++h) {
           const int ab = L::HALVES == 2 ? h : acc;
-          if (L::HALVES == 2) mbar_wait(tfull_bar + 8 * ab, acc_phase);
+          if (L::HALVES == 2) mbar_wait_opt(tfull_bar + 8 * ab, acc_phase, args.wsleep & 2);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -882,7 +884,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
         const bool tma_out = P.d_tma;
         const int row_base = mb * BM * CG + (int)crank * BM + q * 32;
         for (int h = 0; h < 2; ++h) {
-          mbar_wait(tfull_bar + 8 * h, acc_phase);
+          mbar_wait_opt(tfull_bar + 8 * h, acc_phase, args.wsleep & 2);
           tc_fence_after();
           const uint32_t tb = tbase + 256 * h + 128 * half;
           const int col0 = nb * L::BN + (half == 0 ? 128 * h : 256 + 128 * h);
@@ -1220,6 +1222,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     a.kserp = knob(KNOB_GEMM_KSERP);
     a.l2pf = knob(KNOB_GEMM_L2PF);
     a.st_ef = knob(KNOB_GEMM_ST_EF);
+    a.wsleep = knob(KNOB_WAIT_SLEEP);
     bool need_fault = GRP;
     for (int i = 0; i < n; ++i) need_fault = need_fault || ps[i].chunk_done != nullptr;
     if (need_fault) {

@@ -41,6 +41,8 @@ enum Knob {
   KNOB_MX_CAST_DEBUG,       // A/B only: bit 0 the MX TMA cast skips its code stores (results invalid)
   KNOB_MX_CAST_WS,          // 1: bf16 MX casts with row-major dim1 copies by the warp-specialised kernel
   KNOB_GEMM_ST_EF,          // 1: GEMM bf16 outputs stored with an L2 evict-first hint
+  KNOB_WAIT_SLEEP,          // barrier waits with a suspend-time hint: bit 0 amax_rc / MX ws casts, bit 1 GEMM epilogue,
+                            // bit 2 GEMM producer, bit 3 GEMM MMA + SF copier
   KNOB_WATCHDOG_MS,         // peer waits (P2P gather, fused reduce-scatter, async-TP) give up after this many ms
                             // and report FP8_ECUDA at the next call; 0 = wait forever
   KNOB_COUNT
@@ -139,6 +141,7 @@ struct AmaxRCArgs {
   uint32_t* col[AMAX_RC_MAX];
   Seg seg;
   int dbg;   // knob amax_rc_debug (A/B experiments only)
+  int sleep; // knob wait_sleep bit 0: barrier waits sleep instead of spinning
 };
 cudaError_t launch_amax_rc(const AmaxRCTensor* ts, int n, int mode, cudaStream_t st, const Seg& seg = Seg{});
 cudaError_t launch_amax_flat_dual(const void* x0, int64_t n0_elems, uint32_t* out0, const void* x1, int64_t n1_elems,

@@ -54,6 +54,31 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
+// Wait with a suspend-time hint: a thread whose phase is not complete sleeps (NANOSLEEP.SYNCS, woken by the
+// barrier) instead of spinning, so waiting warps do not take issue slots (and power) from working ones.
+__device__ __forceinline__ uint32_t mbar_try_wait_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(1000u)
+      : "memory");
+  return ok;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t n = 0;
+  while (!mbar_try_wait_sleep(bar, parity)) {
+    if (++n > (1u << 24)) asm volatile("trap;");
+  }
+}
+// sleep = false: the spinning wait (A/B)
+__device__ __forceinline__ void mbar_wait_opt(uint32_t bar, uint32_t parity, bool sleep) {
+  if (sleep) mbar_wait_sleep(bar, parity);
+  else mbar_wait(bar, parity);
+}
+
 // ----------------------------------------------------------------------------
 // TMA / bulk copies
 // ----------------------------------------------------------------------------

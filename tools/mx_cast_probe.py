@@ -39,7 +39,8 @@ s0 = torch.empty(R * C // 32, dtype=torch.uint8, device="cuda")
 s1 = torch.empty(R * C // 32, dtype=torch.uint8, device="cuda")
 h = ops.hp(x)
 res = {"R": R, "C": C}
-for name, kn, a0, a1 in (("default", {}, True, True), ("ring", {"mx_cast_ws": 0}, True, True),
+for name, kn, a0, a1 in (("default", {}, True, True), ("sleep", {"wait_sleep": 1}, True, True),
+                         ("ring", {"mx_cast_ws": 0}, True, True),
                          ("ring_nostores", {"mx_cast_debug": 1}, True, True),
                          ("occ3", {"mx_cast_occ3": 1}, True, True), ("dim0_only", {}, True, False),
                          ("dim1_only", {}, False, True)):

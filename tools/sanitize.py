@@ -73,5 +73,15 @@ for recipe in ("rowwise", "mxfp8", "rowwise_gw_hp", "tensorwise"):
     Gs = [(torch.randn((256, n), device="cuda") * 1e-3).to(torch.bfloat16) for n in Ns]
     sp.forward(Xs, Ws, sv)
     sp.backward(Gs, sv, x=Xs)
+# ring wrap-around of the warp-specialised amax / MX cast kernels (capped grid), and the previous kernels
+ops.set_knob("cast_grid", 3)
+ops.amax(X, "row"), ops.amax(X, "col")
+ops.cast(X, "e5m2", "mx32_rm", want_q=True, want_qt=True)
+ops.reset_knobs()
+ops.set_knob("amax_rc", 0)
+ops.set_knob("mx_cast_ws", 0)
+ops.amax(X, "row"), ops.amax(X, "col")
+ops.cast(X, "e5m2", "mx32_rm", want_q=True, want_qt=True)
+ops.reset_knobs()
 torch.cuda.synchronize()
 print("ok")
