@@ -562,7 +562,7 @@ uint64_t fp8_launch_count(void);
  *   amax_rc (1: row / column amax by the multi-tensor warp-specialised kernel; 0: amax_tile_tma's choice) |
  *   amax_rc_debug (0; A/B probes only) | group_batch (1: a rowwise shared-input group's amax and cast launches
  *   batched over X and every W_i, and over every dY_i; 0: per member) |
- *   mx_cast_ws (1: bf16 MX casts with row-major dim1 copies by the warp-specialised kernel) | mx_cast_debug (0) |
+ *   mx_cast_ws (0; 1 = bf16 MX casts with row-major dim1 copies by the warp-specialised kernel) | mx_cast_debug (0) |
  *   gemm_st_ef (0: 1 = GEMM bf16 outputs stored with an L2 evict-first hint) | wait_sleep (0; bit mask: barrier waits
  *   sleep with a suspend-time hint -- 1 amax_rc / MX casts, 2 GEMM epilogue, 4 GEMM producer, 8 GEMM MMA) |
  *   watchdog_ms (30000; 0 = peer waits never give up)

@@ -769,8 +769,8 @@ __global__ void __launch_bounds__(256) cast_tile_dual_kernel(const __grid_consta
 // ---------------------------------------------------------------------------
 template <int FMT, bool RCEIL>
 __device__ __forceinline__ uint32_t e8m0_code(uint32_t amax_bits) {
+  // E == 0 (zero or subnormal amax) needs no branch: E - emax (+ 1) < 0 clamps to code 0
   const int E = (int)(amax_bits >> 23);
-  if (E == 0) return 0;
   int c = E - kEmax<FMT>();
   if (RCEIL && (amax_bits & 0x7FFFFFu) > 0x600000u) c += 1;
   return (uint32_t)min(max(c, 0), 254);
@@ -904,6 +904,18 @@ __device__ __forceinline__ uint2 cast8_bf16x2(const uint32_t (&w)[4], const floa
   return make_uint2(b[0] | (b[1] << 16), b[2] | (b[3] << 16));
 }
 
+// 8 fp32 values (pairs) -> 8 FP8 codes of x * mult.
+template <int FMT>
+__device__ __forceinline__ uint2 cast8_f32x2(const float2 (&f)[4], const float2 (&m)[4]) {
+  uint32_t b[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 p = __fmul2_rn(f[q], m[q]);
+    b[q] = FMT == 0 ? cvt_e4m3x2(p.y, p.x) : cvt_e5m2x2(p.y, p.x);
+  }
+  return make_uint2(b[0] | (b[1] << 16), b[2] | (b[3] << 16));
+}
+
 template <int FMT, bool RCEIL, bool DIM0, bool DIM1, bool TR1, int ST>
 // ST == 2 (knob mx_cast_occ3): a 2-deep ring and <= 85 registers, so 3 CTAs (24 warps) share an SM
 __global__ void __launch_bounds__(256, (ST == 2 && !TR1) ? 3 : 1) mx_cast_tma_kernel(const __grid_constant__ CUtensorMap tmap, int64_t R,
@@ -954,33 +966,36 @@ __global__ void __launch_bounds__(256, (ST == 2 && !TR1) ? 3 : 1) mx_cast_tma_ke
       issue(k + ST);
     }
 
-    // one pass over the 8 rows: dim0 block codes + casts, packed dim1 column maxima
+    // pass 1 over the raw words: packed |x| maxima per row (dim0, this thread's 8 columns) and per column
+    // (dim1, this thread's 8 rows)
     uint32_t cmw[4] = {0, 0, 0, 0};
+    uint32_t rmx[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
-      uint32_t a[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        a[j] = w[j] & 0x7FFF7FFFu;
-        if (DIM1) cmw[j] = __vmaxu2(cmw[j], a[j]);
+      const uint32_t a0 = raw[i].x & 0x7FFF7FFFu, a1 = raw[i].y & 0x7FFF7FFFu;
+      const uint32_t a2 = raw[i].z & 0x7FFF7FFFu, a3 = raw[i].w & 0x7FFF7FFFu;
+      if (DIM1) {
+        cmw[0] = __vmaxu2(cmw[0], a0); cmw[1] = __vmaxu2(cmw[1], a1);
+        cmw[2] = __vmaxu2(cmw[2], a2); cmw[3] = __vmaxu2(cmw[3], a3);
       }
-      if (DIM0) {
-        const uint32_t m2 = __vmaxu2(__vmaxu2(a[0], a[1]), __vmaxu2(a[2], a[3]));
-        uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
+      if (DIM0) rmx[i] = __vmaxu2(__vmaxu2(a0, a1), __vmaxu2(a2, a3));
+    }
+    // dim0 block codes (4 lanes per 32-column block; all 4 store the same byte)
+    float mu0[8];
+    if (DIM0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t m = max(rmx[i] & 0xFFFFu, rmx[i] >> 16);
         m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
         m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
         const uint32_t code = e8m0_code<FMT, RCEIL>(m << 16);
-        const float mu = e8m0_mult(code);
-        const float2 mm[4] = {make_float2(mu, mu), make_float2(mu, mu), make_float2(mu, mu), make_float2(mu, mu)};
-        const uint2 b0 = cast8_bf16x2<FMT>(w, mm);
-        if (!(dbg & 1)) *reinterpret_cast<uint2*>(q0 + (r0 + rbase + i) * C + c0 + cc) = b0;
-        else if (b0.x == 0x12345678u) q0[0] = 0;   // A/B probe (no stores): keep the cast alive
+        mu0[i] = e8m0_mult(code);
         const int rr = rbase + i;
-        if ((t & 3) == 0) s_sf0[(rr & 31) * 16 + (rr >> 5) * 4 + (cc >> 5)] = (uint8_t)code;
+        s_sf0[(rr & 31) * 16 + (rr >> 5) * 4 + (cc >> 5)] = (uint8_t)code;
       }
     }
     const int64_t base0 = ((r0 >> 7) * (C >> 7) + (c0 >> 7)) * 512;
+    float2 mu[4];
     if (DIM1) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) cmw[j] = __vmaxu2(cmw[j], __shfl_xor_sync(0xffffffffu, cmw[j], 16));
@@ -1004,16 +1019,35 @@ __global__ void __launch_bounds__(256, (ST == 2 && !TR1) ? 3 : 1) mx_cast_tma_ke
       const int j = t >> 6;                // all 8 rows of this thread lie in 32-row block j
       const float4 ma = *reinterpret_cast<const float4*>(&mult1[j][cc]);
       const float4 mb = *reinterpret_cast<const float4*>(&mult1[j][cc + 4]);
-      const float2 mu[4] = {make_float2(ma.x, ma.y), make_float2(ma.z, ma.w), make_float2(mb.x, mb.y),
-                            make_float2(mb.z, mb.w)};
+      mu[0] = make_float2(ma.x, ma.y); mu[1] = make_float2(ma.z, ma.w);
+      mu[2] = make_float2(mb.x, mb.y); mu[3] = make_float2(mb.z, mb.w);
+    }
+    // pass 2: each row unpacked once and cast with both multipliers
+    uint8_t* o0 = q0 + (r0 + rbase) * C + c0 + cc;
+    uint8_t* o1 = q1 + (r0 + rbase) * C + c0 + cc;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
-        const uint2 b = cast8_bf16x2<FMT>(w, mu);
+    for (int i = 0; i < 8; ++i) {
+      float2 f[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t w = q == 0 ? raw[i].x : q == 1 ? raw[i].y : q == 2 ? raw[i].z : raw[i].w;
+        f[q] = make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+      }
+      if (DIM0) {
+        const float2 mm[4] = {make_float2(mu0[i], mu0[i]), make_float2(mu0[i], mu0[i]), make_float2(mu0[i], mu0[i]),
+                              make_float2(mu0[i], mu0[i])};
+        const uint2 b0 = cast8_f32x2<FMT>(f, mm);
+        if (!(dbg & 1)) *reinterpret_cast<uint2*>(o0 + i * C) = b0;
+        else if (b0.x == 0x12345678u) q0[0] = 0;   // A/B probe (no stores): keep the cast alive
+      }
+      if (DIM1) {
+        const uint2 b = cast8_f32x2<FMT>(f, mu);
         if (TR1) *reinterpret_cast<uint2*>(&tile[swz(rbase + i, cc >> 2)]) = b;
-        else if (!(dbg & 1)) *reinterpret_cast<uint2*>(q1 + (r0 + rbase + i) * C + c0 + cc) = b;
+        else if (!(dbg & 1)) *reinterpret_cast<uint2*>(o1 + i * C) = b;
         else if (b.x == 0x12345678u) q1[0] = 0;
       }
+    }
+    if (DIM1) {
       if (TR1) {
         __syncthreads();                   // (4)
         store_transposed(tile, q1, R, r0, c0, 128, 128);
@@ -1109,47 +1143,63 @@ __global__ void __launch_bounds__(288, 2) mx_cast_ws_kernel(const __grid_constan
     asm volatile("bar.sync 1, 256;" ::: "memory");
     if (k > 0) store_sf((k - 1) & 1, pr0, pc0);
     uint8_t* sb = sfb + (k & 1) * 1024;
+    // pass 1 over the raw words: packed |x| maxima -- per row (dim0, over the lane's 8 columns) and per
+    // column (dim1, over the lane's 8 rows)
+    uint32_t rmx[8];
     uint32_t cm[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
-      uint32_t a[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a[q] = w[q] & 0x7FFF7FFFu;
-        if (DIM1) cm[q] = __vmaxu2(cm[q], a[q]);
+      const uint32_t a0 = raw[i].x & 0x7FFF7FFFu, a1 = raw[i].y & 0x7FFF7FFFu;
+      const uint32_t a2 = raw[i].z & 0x7FFF7FFFu, a3 = raw[i].w & 0x7FFF7FFFu;
+      if (DIM1) {
+        cm[0] = __vmaxu2(cm[0], a0); cm[1] = __vmaxu2(cm[1], a1);
+        cm[2] = __vmaxu2(cm[2], a2); cm[3] = __vmaxu2(cm[3], a3);
       }
-      if (DIM0) {
-        const uint32_t m2 = __vmaxu2(__vmaxu2(a[0], a[1]), __vmaxu2(a[2], a[3]));
-        uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
-        m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
-        m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
-        const uint32_t code = e8m0_code<FMT, RCEIL>(m << 16);
-        const float mu = e8m0_mult(code);
-        const float2 mm[4] = {make_float2(mu, mu), make_float2(mu, mu), make_float2(mu, mu), make_float2(mu, mu)};
-        *reinterpret_cast<uint2*>(q0 + (r0 + rl + i) * C + c0 + cl) = cast8_bf16x2<FMT>(w, mm);
-        if ((lane & 3) == 0) sb[p0 + 16 * i] = (uint8_t)code;
-      }
+      if (DIM0) rmx[i] = __vmaxu2(__vmaxu2(a0, a1), __vmaxu2(a2, a3));
     }
+    // dim1 block codes (all lanes of a column hold the same maxima after the shuffles, so every lane stores
+    // its codes: identical bytes to identical addresses, no divergent branch)
+    float2 mu1[4];
     if (DIM1) {
-      float2 mu[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         cm[q] = __vmaxu2(cm[q], __shfl_xor_sync(0xffffffffu, cm[q], 8));
         cm[q] = __vmaxu2(cm[q], __shfl_xor_sync(0xffffffffu, cm[q], 16));
         const uint32_t clo = e8m0_code<FMT, RCEIL>(cm[q] << 16), chi = e8m0_code<FMT, RCEIL>(cm[q] & 0xFFFF0000u);
-        mu[q] = make_float2(e8m0_mult(clo), e8m0_mult(chi));
-        if (lane < 8) {   // columns cl + 2q, cl + 2q + 1 of dim1 block j
-          const int c = cl + 2 * q;
-          sb[512 + (c & 31) * 16 + (c >> 5) * 4 + j] = (uint8_t)clo;
-          sb[512 + ((c + 1) & 31) * 16 + ((c + 1) >> 5) * 4 + j] = (uint8_t)chi;
-        }
+        mu1[q] = make_float2(e8m0_mult(clo), e8m0_mult(chi));
+        const int c = cl + 2 * q;   // columns c, c + 1 of dim1 block j
+        sb[512 + (c & 31) * 16 + (c >> 5) * 4 + j] = (uint8_t)clo;
+        sb[512 + ((c + 1) & 31) * 16 + ((c + 1) >> 5) * 4 + j] = (uint8_t)chi;
       }
+    }
+    // dim0 block codes: 4 lanes per 32-column block (the 4 lanes store the same byte)
+    float mu0[8];
+    if (DIM0) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
-        *reinterpret_cast<uint2*>(q1 + (r0 + rl + i) * C + c0 + cl) = cast8_bf16x2<FMT>(w, mu);
+        uint32_t m = max(rmx[i] & 0xFFFFu, rmx[i] >> 16);
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+        const uint32_t code = e8m0_code<FMT, RCEIL>(m << 16);
+        mu0[i] = e8m0_mult(code);
+        sb[p0 + 16 * i] = (uint8_t)code;
       }
+    }
+    // pass 2: each row unpacked once, cast with both multipliers
+    uint8_t* o0 = DIM0 ? q0 + (r0 + rl) * C + c0 + cl : nullptr;
+    uint8_t* o1 = DIM1 ? q1 + (r0 + rl) * C + c0 + cl : nullptr;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float2 f[4];
+      const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) f[q] = make_float2(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xFFFF0000u));
+      if (DIM0) {
+        const float2 mm[4] = {make_float2(mu0[i], mu0[i]), make_float2(mu0[i], mu0[i]), make_float2(mu0[i], mu0[i]),
+                              make_float2(mu0[i], mu0[i])};
+        *reinterpret_cast<uint2*>(o0 + i * C) = cast8_f32x2<FMT>(f, mm);
+      }
+      if (DIM1) *reinterpret_cast<uint2*>(o1 + i * C) = cast8_f32x2<FMT>(f, mu1);
     }
     pr0 = r0;
     pc0 = c0;

@@ -39,7 +39,7 @@ enum Knob {
   KNOB_AMAX_RC_DEBUG,       // A/B only: bit 0 consumers skip the tile (results invalid), bit 1 interleaved tile order
   KNOB_GROUP_BATCH,         // 1: a rowwise shared-input group's amax / cast launches batched over X + every W_i (fwd), every dY_i (bwd)
   KNOB_MX_CAST_DEBUG,       // A/B only: bit 0 the MX TMA cast skips its code stores (results invalid)
-  KNOB_MX_CAST_WS,          // 1: bf16 MX casts with row-major dim1 copies by the warp-specialised kernel
+  KNOB_MX_CAST_WS,          // 1: bf16 MX casts with row-major dim1 copies by the warp-specialised kernel (0: the ring kernel)
   KNOB_GEMM_ST_EF,          // 1: GEMM bf16 outputs stored with an L2 evict-first hint
   KNOB_WAIT_SLEEP,          // barrier waits with a suspend-time hint: bit 0 amax_rc / MX ws casts, bit 1 GEMM epilogue,
                             // bit 2 GEMM producer, bit 3 GEMM MMA + SF copier

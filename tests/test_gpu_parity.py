@@ -629,7 +629,7 @@ def test_float8linear_gw_hp_detects_inplace_input_change():
 @pytest.mark.parametrize("gran", ["mx32", "mx32_rm"])
 @pytest.mark.parametrize("fmt,mode", [(E4M3, omx.FLOOR), (E5M2, omx.RCEIL)])
 def test_mx_cast_persistent_ring(grid, gran, fmt, mode, ws, knob):
-    # the TMA-pipelined MX casts (warp-specialised kernel, knob mx_cast_ws = 1; the ring kernel) walk
+    # the TMA-pipelined MX casts (the ring kernel; the warp-specialised kernel, knob mx_cast_ws = 1) walk
     # many tiles per CTA when the grid is capped: every shared-memory ring slot and E8M0 staging buffer
     # is refilled several times (mbarrier parity wrap-around)
     knob("cast_grid", int(grid))
@@ -651,8 +651,8 @@ def test_mx_cast_persistent_ring(grid, gran, fmt, mode, ws, knob):
 
 @pytest.mark.parametrize("impl", ["0", "1", "ring"])
 def test_mx_cast_impls_agree_c4_sized(impl, knob):
-    # the MX cast kernels (register-only: knob mx_cast_tma = 0; TMA ring: mx_cast_ws = 0; warp-specialised:
-    # default) on a C4-like tensor with many tiles per CTA, sampled rows against the oracle
+    # the MX cast kernels (register-only: knob mx_cast_tma = 0; TMA ring: default; warp-specialised:
+    # mx_cast_ws = 1) on a C4-like tensor with many tiles per CTA, sampled rows against the oracle
     knob("mx_cast_tma", 0 if impl == "0" else 1)
     knob("mx_cast_ws", 0 if impl == "ring" else 1)
     R, C = 2048, 8192
@@ -1187,7 +1187,7 @@ LINEAR_BUFFER_CASES = [
     ("rowwise", {}), ("rowwise", {"cast_grid": 3}), ("rowwise", {"cast_grid": 7}), ("rowwise", {"amax_rc": 0}),
     ("rowwise", {"amax_rc": 0, "amax_tile_tma": 0}), ("rowwise", {"amax_rc": 1, "cast_grid": 5}),
     ("rowwise_gw_hp", {}),
-    ("mxfp8", {}), ("mxfp8", {"cast_grid": 3}), ("mxfp8", {"mx_transposed": 1}), ("mxfp8", {"mx_cast_tma": 0}), ("mxfp8", {"mx_cast_ws": 0}),
+    ("mxfp8", {}), ("mxfp8", {"cast_grid": 3}), ("mxfp8", {"mx_transposed": 1}), ("mxfp8", {"mx_cast_tma": 0}), ("mxfp8", {"mx_cast_ws": 1}),
     ("mxfp8", {"mx_cast_occ3": 1}), ("mxfp8", {"mx_cast_occ3": 1, "cast_grid": 5}),
 ]
 

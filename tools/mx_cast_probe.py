@@ -1,6 +1,6 @@
 """A/B probe of the MXFP8 dim0 + dim1 TMA cast on the c4 dY shape (larger than L2, no flush): the product
-kernel (warp-specialised), the ring kernel (mx_cast_ws = 0), the ring kernel without its code stores (knob
-mx_cast_debug = 1: results invalid), the occupancy-3 variant, dim0 only and dim1 only.  Rate = algorithmic bytes (2 read + 1 + 1 written + 2/32 scales per element for dim0 +
+kernel (the TMA ring), the warp-specialised kernel (mx_cast_ws = 1), the ring kernel without its code stores
+(knob mx_cast_debug = 1: results invalid), the occupancy-3 variant, dim0 only and dim1 only.  Rate = algorithmic bytes (2 read + 1 + 1 written + 2/32 scales per element for dim0 +
 dim1) / time.  Tuning context only.
 
     python tools/mx_cast_probe.py [R] [C]
@@ -40,7 +40,7 @@ s1 = torch.empty(R * C // 32, dtype=torch.uint8, device="cuda")
 h = ops.hp(x)
 res = {"R": R, "C": C}
 for name, kn, a0, a1 in (("default", {}, True, True), ("sleep", {"wait_sleep": 1}, True, True),
-                         ("ring", {"mx_cast_ws": 0}, True, True),
+                         ("ws", {"mx_cast_ws": 1}, True, True),
                          ("ring_nostores", {"mx_cast_debug": 1}, True, True),
                          ("occ3", {"mx_cast_occ3": 1}, True, True), ("dim0_only", {}, True, False),
                          ("dim1_only", {}, False, True)):
