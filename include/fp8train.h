@@ -316,8 +316,10 @@ fp8_status_t fp8_linear_bwd_ex(const fp8_linear_cfg_t* cfg, fp8_hp_t dy, const f
  * norm's output) and w1 / w3 (the MLP norm's output).  Each member is the Float8Linear of
  * fp8_linear_fwd / fp8_linear_bwd (Appendix A): X's scales depend on X alone
  * (tensorwise amax over X; rowwise per row / per column of X; MX blocks of X), so its amax and
- * FP8 copies are computed ONCE, by member 0, and read by every member's GEMMs.  Every output and
- * every saved byte equals what n separate fp8_linear_fwd / fp8_linear_bwd calls write.
+ * FP8 copies are computed ONCE and read by every member's GEMMs (rowwise: X's and every W_i's row /
+ * column amax by one launch and their FP8 copies by one cast launch; the backward likewise for every
+ * dY_i; knob group_batch = 0 casts member by member).  Every output and every saved byte equals what
+ * n separate fp8_linear_fwd / fp8_linear_bwd calls write.
  *   fwd: x [M,K]; w: HOST array of n weights [N_i, K] (fp32 or bf16 each); y: HOST array of n
  *     outputs [M, N_i] (out_dtype, dense); saved: HOST array of n buffers of
  *     fp8_linear_saved_bytes(cfg, M, N_i, K) bytes -- saved[0] holds X's backward operand,
@@ -351,8 +353,9 @@ fp8_status_t fp8_linear_bwd_shared(const fp8_linear_cfg_t* cfg, int n, const fp8
  *   offs: DEVICE int32[E+1], offs[0] = 0 <= offs[1] <= ... <= offs[E] = T, every entry
  *   a multiple of 128 (MoE token groups padded to 128 rows); expert g owns token rows
  *   [offs[g], offs[g+1]); empty experts allowed (dW_g = 0).  The offsets are validated
- *   on the device: a violation traps the kernel (reported as FP8_ECUDA at the next
- *   sync) -- the call never reads them on the host, so it never synchronises.
+ *   on the device: a violation makes the GEMM compute no tile of that problem and sets the
+ *   process fault word, reported as FP8_ECUDA by fp8_check_async_error (and by the next
+ *   grouped call) -- the call never reads them on the host, so it never synchronises.
  *   Recipes: tensorwise (one scale per X, W, dY) or rowwise (per token row, per expert
  *   weight row / column, per (expert, column) over the expert's tokens for dW).
  *   T, N multiples of 128; K multiple of 16; 1 <= E <= 256.
