@@ -508,6 +508,29 @@ def run_ours(a):
         gather_info = {"impl": gather_impl, "reduce_scatter": rs_impl, "ms": gms, "recv_bytes_per_rank": recv,
                        "busbw_GBps": recv / (gms / 1e3) / 1e9 if world > 1 else None,
                        "nvlink_peak_GBps": 900.0}
+        if world > 1:
+            # context: the BF16 all-gather of the same shard over NCCL, as FSDP2 without FP8 gathers
+            try:
+                full_bf16 = torch.empty((w_shard.shape[0] * world, w_shard.shape[1]), dtype=w_shard.dtype, device=dev)
+                for _ in range(3):
+                    dist.all_gather_into_tensor(full_bf16, w_shard)
+                torch.cuda.synchronize()
+                barrier()
+                b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                b0.record(stream)
+                for _ in range(a.steps):
+                    dist.all_gather_into_tensor(full_bf16, w_shard)
+                b1.record(stream)
+                torch.cuda.synchronize()
+                bms = b0.elapsed_time(b1) / a.steps
+                t = torch.tensor([bms], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                bms = float(t.item())
+                gather_info["bf16_allgather_ms"] = bms
+                gather_info["fp8_vs_bf16_gather_speedup"] = bms / gms if gms > 0 else None
+                del full_bf16
+            except Exception as e:   # context only: never lose the line over it
+                gather_info["bf16_allgather_error"] = str(e)[:200]
 
     flops_step = 6.0 * M * N * K            # three GEMMs of 2*M*N*K each (per rank)
     total_flops = flops_step * a.steps * world

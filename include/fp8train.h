@@ -354,7 +354,7 @@ fp8_status_t fp8_linear_bwd_shared(const fp8_linear_cfg_t* cfg, int n, const fp8
  *   a multiple of 128 (MoE token groups padded to 128 rows); expert g owns token rows
  *   [offs[g], offs[g+1]); empty experts allowed (dW_g = 0).  The offsets are validated
  *   on the device: a violation makes the GEMM compute no tile of that problem and sets the
- *   process fault word, reported as FP8_ECUDA by fp8_check_async_error (and by the next
+ *   process fault word, reported as FP8_EINVAL by fp8_check_async_error (and by the next
  *   grouped call) -- the call never reads them on the host, so it never synchronises.
  *   Recipes: tensorwise (one scale per X, W, dY) or rowwise (per token row, per expert
  *   weight row / column, per (expert, column) over the expert's tokens for dW).
