@@ -110,6 +110,8 @@ struct GemmArgs {
   int l2pf;           // L2 prefetch distance of the operand boxes, in stages (0 = off)
   int wsleep;         // knob wait_sleep: bit 1 epilogue waits, bit 2 producer / scheduler waits, bit 3 MMA / SF waits
                       // use the suspend-time-hint try_wait (waiting warps sleep instead of spinning)
+  int l2hint;         // knob gemm_l2hint (A/B): 1 A panels evict_last (the grouped raster reuses them across the
+                      // group's N sweep), 2 + B evict_first, 3 A evict_last with B explicitly evict_normal
   int st_ef;          // bf16 outputs stored with an L2 evict-first hint (written back during the GEMM, so the
                       // next memory-bound kernel does not pay for evicting them)
   unsigned* fault;    // process fault word (async-TP watchdog, bad group offsets); may be null
@@ -461,6 +463,8 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
+    const uint64_t polA = l2_policy_evict_last();
+    const uint64_t polB = args.l2hint == 2 ? l2_policy_evict_first() : l2_policy_evict_normal();
     int stage = 0;
     uint32_t phase = 0;
     int sk = 0;
@@ -593,6 +597,10 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
                                 a_mn ? kmn + ti.a_k0 : m0 + ti.a_row0, fb);
                 tma_load_2d_2sm(db, tmB, b_mn ? bn + ti.b_row0 : k0 + ti.b_k0,
                                 b_mn ? kmn + ti.b_k0 : n0 + ti.b_row0, fb);
+              } else if (args.l2hint) {
+                tma_load_2d_2sm_hint(da, tmA, a_mn ? am : k0, a_mn ? kmn : m0, fb, polA);
+                tma_load_2d_2sm_hint(db, tmB, b_mn ? bn : k0, b_mn ? kmn : n0, fb, polB);
+                if (b_mn && L::BN / CG > 128) tma_load_2d_2sm_hint(db + 16384, tmB, bn + 128, kmn, fb, polB);
               } else {
                 tma_load_2d_2sm(da, tmA, a_mn ? am : k0, a_mn ? kmn : m0, fb);
                 tma_load_2d_2sm(db, tmB, b_mn ? bn : k0, b_mn ? kmn : n0, fb);
@@ -1223,6 +1231,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     a.l2pf = knob(KNOB_GEMM_L2PF);
     a.st_ef = knob(KNOB_GEMM_ST_EF);
     a.wsleep = knob(KNOB_WAIT_SLEEP);
+    a.l2hint = knob(KNOB_GEMM_L2HINT);
     bool need_fault = GRP;
     for (int i = 0; i < n; ++i) need_fault = need_fault || ps[i].chunk_done != nullptr;
     if (need_fault) {
