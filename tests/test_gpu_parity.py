@@ -1642,8 +1642,9 @@ SHARED_CASES = [("tensorwise", {}), ("tensorwise", {"tw_dual": 0}), ("rowwise", 
 
 
 @pytest.mark.parametrize("M,K,Ns", [(384, 512, (640, 128, 256)), (256, 384, (128, 512)), (384, 256, (384,)),
-                                    (400, 528, (272, 400, 144)), (256, 256, (128, 256, 128, 384, 128, 256, 128))],
-                         ids=["qkv", "w13", "single", "ragged", "seven"])
+                                    (400, 528, (272, 400, 144)), (256, 256, (128, 256, 128, 384, 128, 256, 128)),
+                                    (256, 384, (128, 256, 128, 128, 384, 128, 256, 128))],
+                         ids=["qkv", "w13", "single", "ragged", "seven", "eight"])
 @pytest.mark.parametrize("recipe,knobs", SHARED_CASES,
                          ids=[r + ("-" + "-".join(f"{k}{v}" for k, v in kn.items()) if kn else "") for r, kn in
                               SHARED_CASES])
