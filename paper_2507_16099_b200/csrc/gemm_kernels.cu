@@ -110,6 +110,7 @@ struct GemmArgs {
   int l2pf;           // L2 prefetch distance of the operand boxes, in stages (0 = off)
   int wsleep;         // knob wait_sleep: bit 1 epilogue waits, bit 2 producer / scheduler waits, bit 3 MMA / SF waits
                       // use the suspend-time-hint try_wait (waiting warps sleep instead of spinning)
+  int afill;          // knob gemm_afill: N = 512 tiles issue both halves' MMAs per K step with A kept in the collector
   int l2hint;         // knob gemm_l2hint (A/B): 1 A panels evict_last (the grouped raster reuses them across the
                       // group's N sweep), 2 + B evict_first, 3 A evict_last with B explicitly evict_normal
   int st_ef;          // bf16 outputs stored with an L2 evict-first hint (written back during the GEMM, so the
@@ -678,6 +679,23 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
             return mn ? (uint64_t)((BF ? 128 : 256) * k) : (uint64_t)(1024 * (k >> 2) + 2 * (k & 3));
           };
           if constexpr (L::HALVES == 2) {
+            if (args.afill) {
+              // knob gemm_afill: per K step both halves' MMAs back to back, A held in the collector buffer
+              // (read from smem once for the two MMAs); half 1 is awaited after half 0's first MMA is queued
+              // and half 0 is published before half 1's last MMA, as below
+#pragma unroll
+              for (int k = 0; k < BK / 32; ++k) {
+                const uint64_t ad = adesc + koff(a_mn, k);
+                mma_f8f6f4_cg2_afill(d_tmem, ad, bdesc + koff(b_mn, k), idesc, (kb | k) != 0);
+                if (k == 0 && kb == 0) {
+                  mbar_wait(tempty_bar + 8, acc_phase ^ 1);
+                  tc_fence_after();
+                }
+                if (k == BK / 32 - 1 && kb == num_kb - 1) mma_commit_cg2_mc(tfull_bar, 0x3);
+                mma_f8f6f4_cg2_alastuse(d_tmem + 256, ad, bdesc + (uint64_t)(16384 >> 4) + koff(b_mn, k), idesc,
+                                        (kb | k) != 0);
+              }
+            } else
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               if (h == 1 && kb == 0) {
@@ -1232,6 +1250,7 @@ static cudaError_t launch_t(const GemmProblem* ps, int n, cudaStream_t st) {
     a.st_ef = knob(KNOB_GEMM_ST_EF);
     a.wsleep = knob(KNOB_WAIT_SLEEP);
     a.l2hint = knob(KNOB_GEMM_L2HINT);
+    a.afill = knob(KNOB_GEMM_AFILL);
     bool need_fault = GRP;
     for (int i = 0; i < n; ++i) need_fault = need_fault || ps[i].chunk_done != nullptr;
     if (need_fault) {

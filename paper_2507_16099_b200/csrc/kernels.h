@@ -44,6 +44,7 @@ enum Knob {
   KNOB_WAIT_SLEEP,          // barrier waits with a suspend-time hint: bit 0 amax_rc / MX ws casts, bit 1 GEMM epilogue,
                             // bit 2 GEMM producer, bit 3 GEMM MMA + SF copier
   KNOB_GEMM_L2HINT,         // A/B: L2 eviction hints on the GEMM operand loads (1 A evict_last, 2 + B evict_first, 3 + B normal)
+  KNOB_GEMM_AFILL,          // 1: 256 x 512 tiles: per K step both N halves' MMAs, A kept in the tensor core's collector
   KNOB_WATCHDOG_MS,         // peer waits (P2P gather, fused reduce-scatter, async-TP) give up after this many ms
                             // and report FP8_ECUDA at the next call; 0 = wait forever
   KNOB_COUNT

@@ -1405,13 +1405,16 @@ def test_grouped_bad_device_offsets_reported():
 @pytest.mark.parametrize("majors", ["KK", "KM", "MM", "MK"])
 @pytest.mark.parametrize("sched", [1, 0], ids=["dynamic", "roundrobin"])
 @pytest.mark.parametrize("out", [torch.float32, torch.bfloat16], ids=["f32_direct", "bf16_tma_store"])
-def test_gemm_n512_integer_grid_exact(M, N, K, majors, sched, out, knob):
+@pytest.mark.parametrize("afill", [0, 1], ids=["a_per_mma", "a_collector"])
+def test_gemm_n512_integer_grid_exact(M, N, K, majors, sched, out, afill, knob):
     """The 256 x 512 CTA-pair tile (two N = 256 MMAs sharing A, one 512-column accumulator handed to the
     epilogue half by half, permuted column mapping, 256-row K-major / two 128-wide MN-major B boxes):
     integer-grid operands give exact fp32 sums, so the result must equal X W^T bit for bit, for every
-    operand-major combination, ragged M, several tiles per CTA pair, K-serpentine tiles included."""
+    operand-major combination, ragged M, several tiles per CTA pair, K-serpentine tiles included; also with
+    both halves' MMAs issued per K step and A kept in the tensor core's collector (knob gemm_afill)."""
     knob("gemm_n512", 1)
     knob("gemm_sched", sched)
+    knob("gemm_afill", afill)
     a, b = _grid_operands(M, N, K, seed=7)
     qa, sa, _ = fp8.cast_tensorwise(a, E4M3)
     qb, sb, _ = fp8.cast_tensorwise(b, E4M3)
