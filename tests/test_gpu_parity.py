@@ -1306,6 +1306,37 @@ def test_linear_cast_launch_variants_identical(recipe, variants, knob):
             assert torch.equal(a, b), name
 
 
+SCHEDULE_VARIANTS = [{}, {"wait_sleep": 15}, {"gemm_l2hint": 1}, {"gemm_l2hint": 2}, {"gemm_st_ef": 1}]
+
+
+@pytest.mark.parametrize("recipe", ["tensorwise", "rowwise", "mxfp8"])
+def test_linear_schedule_knobs_bit_identical(recipe, knob):
+    """Knobs that change only how the kernels wait or hint the caches (sleeping barrier waits in the casts and
+    in every GEMM role; L2 eviction hints on the GEMM operand loads and output stores) leave every byte the
+    same: saved buffers, forward workspace, Y, dX, dW bit-identical to the default schedule (long-K N = 512 and
+    MX launches included)."""
+    M, N, K = 512, 1024, 8192
+    x, w, dy = synth.linear_inputs({"tensorwise": "c2", "rowwise": "c3", "mxfp8": "c4"}[recipe], M, N, K, seed=19)
+    X, W, G = _dev(x, torch.bfloat16), _dev(w, torch.bfloat16), _dev(dy, torch.bfloat16)
+    runs = []
+    for v in SCHEDULE_VARIANTS:
+        fp8t.ops.reset_knobs()
+        for k, val in v.items():
+            knob(k, val)
+        plan = ops.LinearPlan(M, N, K, recipe=recipe)
+        saved = plan.new_saved()
+        saved.zero_()
+        plan.ws.zero_()
+        Y = plan.forward(X, W, saved)
+        fws = plan.ws.clone()
+        DX, DW = plan.backward(G, saved)
+        torch.cuda.synchronize()
+        runs.append((saved.clone(), fws, Y.clone(), DX.clone(), DW.clone()))
+    for v, r in zip(SCHEDULE_VARIANTS[1:], runs[1:]):
+        for a, b, name in zip(runs[0], r, ("saved", "fwd ws", "Y", "dX", "dW")):
+            assert torch.equal(a, b), (v, name)
+
+
 # ----------------------------------------------------------------------------- exhaustive fp32 sweep
 
 @pytest.mark.parametrize("fmt", [E4M3, E5M2])
