@@ -1023,8 +1023,8 @@ __global__ void __launch_bounds__(256, (ST == 2 && !TR1) ? 3 : 1) mx_cast_tma_ke
       mu[2] = make_float2(mb.x, mb.y); mu[3] = make_float2(mb.z, mb.w);
     }
     // pass 2: each row unpacked once and cast with both multipliers
-    uint8_t* o0 = q0 + (r0 + rbase) * C + c0 + cc;
-    uint8_t* o1 = q1 + (r0 + rbase) * C + c0 + cc;
+    uint8_t* o0 = DIM0 ? q0 + (r0 + rbase) * C + c0 + cc : nullptr;
+    uint8_t* o1 = DIM1 && !TR1 ? q1 + (r0 + rbase) * C + c0 + cc : nullptr;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       float2 f[4];
