@@ -112,7 +112,9 @@ def parse():
                     help="c3 layer: every linear casts its own input (default: wq/wk/wv and w1/w3 read one X, "
                          "cast once through fp8_linear_fwd_shared)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    # 24 streamed steps: the first input copy and the last output copy (not overlapped with any compute) are
+    # inside the timed region, so fewer steps would mostly measure that pipeline fill and drain
+    ap.add_argument("--e2e-steps", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bf16", action="store_true")
     ap.add_argument("--gather", default="auto", choices=["auto", "p2p", "nccl"],
