@@ -916,12 +916,18 @@ __device__ __forceinline__ uint2 cast8_f32x2(const float2 (&f)[4], const float2 
   return make_uint2(b[0] | (b[1] << 16), b[2] | (b[3] << 16));
 }
 
-template <int FMT, bool RCEIL, bool DIM0, bool DIM1, bool TR1, int ST>
+// TS (knob mx_cast_tstore; dim0 + row-major dim1 only): the codes are written into the tile's own ring stage
+// (its bf16 data is in registers by then) and leave as two 16 KB TMA tensor stores; the stage is refilled
+// one tile later, once the stores have read it.
+template <int FMT, bool RCEIL, bool DIM0, bool DIM1, bool TR1, int ST, bool TS = false>
 // ST == 2 (knob mx_cast_occ3): a 2-deep ring and <= 85 registers, so 3 CTAs (24 warps) share an SM
 __global__ void __launch_bounds__(256, (ST == 2 && !TR1) ? 3 : 1) mx_cast_tma_kernel(const __grid_constant__ CUtensorMap tmap, int64_t R,
                                                           int64_t C, uint8_t* __restrict__ q0,
                                                           uint8_t* __restrict__ sf0, uint8_t* __restrict__ q1,
-                                                          uint8_t* __restrict__ sf1, int dbg) {
+                                                          uint8_t* __restrict__ sf1, int dbg,
+                                                          const __grid_constant__ CUtensorMap tq0,
+                                                          const __grid_constant__ CUtensorMap tq1) {
+  static_assert(!TS || (DIM0 && DIM1 && !TR1), "TMA-store variant: dim0 + row-major dim1 only");
   using L = MxSmem<ST, TR1>;
   extern __shared__ __align__(1024) uint8_t sm[];
   uint32_t(*red)[64] = reinterpret_cast<uint32_t(*)[64]>(sm + L::RED);
@@ -963,7 +969,12 @@ __global__ void __launch_bounds__(256, (ST == 2 && !TR1) ? 3 : 1) mx_cast_tma_ke
     __syncthreads();                       // (1) stage consumed by every thread
     if (t == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(k + ST);
+      if (!TS) {
+        issue(k + ST);
+      } else if (k > 0) {   // tile k-1's stores have been issued from its stage: refill it once they read it
+        bulk_wait_read0();
+        issue(k - 1 + ST);
+      }
     }
 
     // pass 1 over the raw words: packed |x| maxima per row (dim0, this thread's 8 columns) and per column
@@ -1037,14 +1048,26 @@ __global__ void __launch_bounds__(256, (ST == 2 && !TR1) ? 3 : 1) mx_cast_tma_ke
         const float2 mm[4] = {make_float2(mu0[i], mu0[i]), make_float2(mu0[i], mu0[i]), make_float2(mu0[i], mu0[i]),
                               make_float2(mu0[i], mu0[i])};
         const uint2 b0 = cast8_f32x2<FMT>(f, mm);
-        if (!(dbg & 1)) *reinterpret_cast<uint2*>(o0 + i * C) = b0;
+        if (TS) *reinterpret_cast<uint2*>(sm + (k % ST) * L::STAGE + (rbase + i) * 128 + cc) = b0;
+        else if (!(dbg & 1)) *reinterpret_cast<uint2*>(o0 + i * C) = b0;
         else if (b0.x == 0x12345678u) q0[0] = 0;   // A/B probe (no stores): keep the cast alive
       }
       if (DIM1) {
         const uint2 b = cast8_f32x2<FMT>(f, mu);
         if (TR1) *reinterpret_cast<uint2*>(&tile[swz(rbase + i, cc >> 2)]) = b;
+        else if (TS) *reinterpret_cast<uint2*>(sm + (k % ST) * L::STAGE + 16384 + (rbase + i) * 128 + cc) = b;
         else if (!(dbg & 1)) *reinterpret_cast<uint2*>(o1 + i * C) = b;
         else if (b.x == 0x12345678u) q1[0] = 0;
+      }
+    }
+    if (TS) {   // both 128 x 128 code tiles of this tile -> global by TMA
+      fence_proxy_async_smem();
+      __syncthreads();                     // (4)
+      if (t == 0) {
+        const uint32_t st_s = stage0 + (k % ST) * L::STAGE;
+        tma_store_2d(&tq0, st_s, (int)c0, (int)r0);
+        tma_store_2d(&tq1, st_s + 16384, (int)c0, (int)r0);
+        bulk_commit_group();
       }
     }
     if (DIM1) {
@@ -1057,6 +1080,7 @@ __global__ void __launch_bounds__(256, (ST == 2 && !TR1) ? 3 : 1) mx_cast_tma_ke
       if (t < 32) *reinterpret_cast<uint4*>(sf0 + base0 + t * 16) = *reinterpret_cast<const uint4*>(s_sf0 + t * 16);
     }
   }
+  if (TS && t == 0) bulk_wait_all0();   // the stores have read shared memory and completed before the CTA exits
 }
 
 // ---------------------------------------------------------------------------
@@ -1708,17 +1732,33 @@ static cudaError_t mx_launch_t(const void* x, int64_t R, int64_t C, int64_t ld, 
   return cudaGetLastError();
 }
 
-template <int FMT, bool RC, bool D0, bool D1, bool TR, int ST>
+template <int FMT, bool RC, bool D0, bool D1, bool TR, int ST, bool TS = false>
 static cudaError_t mx_tma_go(const CUtensorMap& m, int64_t R, int64_t C, uint8_t* q0, uint8_t* sf0, uint8_t* q1,
                              uint8_t* sf1, cudaStream_t s) {
-  auto kern = mx_cast_tma_kernel<FMT, RC, D0, D1, TR, ST>;
+  auto kern = mx_cast_tma_kernel<FMT, RC, D0, D1, TR, ST, TS>;
   constexpr int smem = MxSmem<ST, TR>::BYTES;
-  const cudaError_t attr_err = ensure_smem<mx_cast_tma_kernel<FMT, RC, D0, D1, TR, ST>>(smem);
+  const cudaError_t attr_err = ensure_smem<mx_cast_tma_kernel<FMT, RC, D0, D1, TR, ST, TS>>(smem);
   if (attr_err != cudaSuccess) return attr_err;
+  CUtensorMap mq0 = m, mq1 = m;
+  if (TS) {   // u8 [R, C] code maps, 128 x 128 boxes
+    auto enc = get_encode();
+    if (!enc) return cudaErrorNotSupported;
+    uint8_t* qs[2] = {q0, q1};
+    CUtensorMap* ms[2] = {&mq0, &mq1};
+    for (int j = 0; j < 2; ++j) {
+      cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)R};
+      cuuint64_t strides[1] = {(cuuint64_t)C};
+      cuuint32_t box[2] = {128, 128};
+      cuuint32_t estr[2] = {1, 1};
+      if (enc(ms[j], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, qs[j], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
+  }
   const int64_t tiles = (R >> 7) * (C >> 7);
   const int64_t cap = cap_grid((int64_t)sm_count() * (TR ? 1 : (ST == 2 ? 3 : 2)));
   LaunchScope ls(K_MX, s);
-  kern<<<(unsigned)(tiles < cap ? tiles : cap), 256, smem, s>>>(m, R, C, q0, sf0, q1, sf1, knob(KNOB_MX_CAST_DEBUG));
+  kern<<<(unsigned)(tiles < cap ? tiles : cap), 256, smem, s>>>(m, R, C, q0, sf0, q1, sf1, knob(KNOB_MX_CAST_DEBUG), mq0, mq1);
   return cudaGetLastError();
 }
 
@@ -1759,6 +1799,9 @@ static cudaError_t mx_tma_launch_t(const void* x, int64_t R, int64_t C, int64_t 
   if (q0 && q1) {
     if (tr1) return mx_tma_go<FMT, RC, true, true, true, 4>(m, R, C, q0, sf0, q1, sf1, s);
     if (knob(KNOB_MX_CAST_OCC3) == 1) return mx_tma_go<FMT, RC, true, true, false, 2>(m, R, C, q0, sf0, q1, sf1, s);
+    if (knob(KNOB_MX_CAST_TSTORE) == 1 && knob(KNOB_MX_CAST_DEBUG) == 0 && (reinterpret_cast<uintptr_t>(q0) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(q1) & 15) == 0 && C % 16 == 0)
+      return mx_tma_go<FMT, RC, true, true, false, 3, true>(m, R, C, q0, sf0, q1, sf1, s);
     return mx_tma_go<FMT, RC, true, true, false, 3>(m, R, C, q0, sf0, q1, sf1, s);
   }
   if (q0) return mx_tma_go<FMT, RC, true, false, false, 3>(m, R, C, q0, sf0, q1, sf1, s);

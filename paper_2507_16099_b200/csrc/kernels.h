@@ -45,6 +45,7 @@ enum Knob {
                             // bit 2 GEMM producer, bit 3 GEMM MMA + SF copier
   KNOB_GEMM_L2HINT,         // A/B: L2 eviction hints on the GEMM operand loads (1 A evict_last, 2 + B evict_first, 3 + B normal)
   KNOB_GEMM_AFILL,          // 1: 256 x 512 tiles: per K step both N halves' MMAs, A kept in the tensor core's collector
+  KNOB_MX_CAST_TSTORE,      // 1 (default): the MX ring cast (dim0 + row-major dim1) writes its codes by TMA tensor stores
   KNOB_WATCHDOG_MS,         // peer waits (P2P gather, fused reduce-scatter, async-TP) give up after this many ms
                             // and report FP8_ECUDA at the next call; 0 = wait forever
   KNOB_COUNT

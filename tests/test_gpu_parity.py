@@ -624,7 +624,7 @@ def test_float8linear_gw_hp_detects_inplace_input_change():
         Y.float().sum().backward()
 
 
-@pytest.mark.parametrize("ws", ["1", "0"])
+@pytest.mark.parametrize("ws", ["1", "0", "tstore"])
 @pytest.mark.parametrize("grid", ["1", "3"])
 @pytest.mark.parametrize("gran", ["mx32", "mx32_rm"])
 @pytest.mark.parametrize("fmt,mode", [(E4M3, omx.FLOOR), (E5M2, omx.RCEIL)])
@@ -633,7 +633,8 @@ def test_mx_cast_persistent_ring(grid, gran, fmt, mode, ws, knob):
     # many tiles per CTA when the grid is capped: every shared-memory ring slot and E8M0 staging buffer
     # is refilled several times (mbarrier parity wrap-around)
     knob("cast_grid", int(grid))
-    knob("mx_cast_ws", int(ws))
+    knob("mx_cast_ws", 1 if ws == "1" else 0)
+    knob("mx_cast_tstore", 1 if ws == "tstore" else 0)   # tstore: codes leave by TMA tensor stores (the default)
     R, C = 512, 1280   # 40 tiles
     x = synth.tensor_c4("x", (R, C), seed=5)
     q0, s0 = omx.quantize_dim0(x, fmt, mode)
@@ -1187,7 +1188,8 @@ LINEAR_BUFFER_CASES = [
     ("rowwise", {}), ("rowwise", {"cast_grid": 3}), ("rowwise", {"cast_grid": 7}), ("rowwise", {"amax_rc": 0}),
     ("rowwise", {"amax_rc": 0, "amax_tile_tma": 0}), ("rowwise", {"amax_rc": 1, "cast_grid": 5}),
     ("rowwise_gw_hp", {}),
-    ("mxfp8", {}), ("mxfp8", {"cast_grid": 3}), ("mxfp8", {"mx_transposed": 1}), ("mxfp8", {"mx_cast_tma": 0}), ("mxfp8", {"mx_cast_ws": 1}),
+    ("mxfp8", {}), ("mxfp8", {"cast_grid": 3}), ("mxfp8", {"mx_transposed": 1}), ("mxfp8", {"mx_cast_tma": 0}), ("mxfp8", {"mx_cast_ws": 1}), ("mxfp8", {"mx_cast_tstore": 0}),
+    ("mxfp8", {"mx_cast_tstore": 0, "cast_grid": 3}),
     ("mxfp8", {"mx_cast_occ3": 1}), ("mxfp8", {"mx_cast_occ3": 1, "cast_grid": 5}),
 ]
 

@@ -41,6 +41,7 @@ h = ops.hp(x)
 res = {"R": R, "C": C}
 for name, kn, a0, a1 in (("default", {}, True, True), ("sleep", {"wait_sleep": 1}, True, True),
                          ("ws", {"mx_cast_ws": 1}, True, True),
+                         ("tstore", {"mx_cast_tstore": 1}, True, True),
                          ("ring_nostores", {"mx_cast_debug": 1}, True, True),
                          ("occ3", {"mx_cast_occ3": 1}, True, True), ("dim0_only", {}, True, False),
                          ("dim1_only", {}, False, True)):
