@@ -571,6 +571,8 @@ uint64_t fp8_launch_count(void);
  *   gemm_l2hint (0; A/B: 1 = GEMM A operand loads evict_last, 2 = + B evict_first) |
  *   gemm_afill (0; 1 = 256 x 512 tiles issue both halves' MMAs per K step with A held in the collector) |
  *   mx_cast_tstore (1: the MX ring cast writes its dim0 / row-major dim1 codes by TMA tensor stores; 0: st.global) |
+ *   cast_rc_tma (1: rowwise casts of launches up to 12288 tiles by the persistent TMA kernel with TMA stores;
+ *   2: always; 0: never) |
  *   watchdog_ms (30000; 0 = peer waits never give up)
  *   -- defaults in parentheses.
  * A knob changes launches enqueued after the call.  Unknown name or out-of-range value:

@@ -758,6 +758,109 @@ __global__ void __launch_bounds__(256) cast_tile_dual_kernel(const __grid_consta
 }
 
 // ---------------------------------------------------------------------------
+// Rowwise casts, persistent TMA variant (bf16, rows and columns multiples of 128; knob cast_rc_tma): the
+// same arithmetic and bytes as cast_tile_kernel<bf16, FMT, 2, 5> (row-scaled codes q and column-scaled codes
+// qt, both row-major), for up to CAST_MULTI_MAX tensors per launch.  CTA b walks tiles total-1-b,
+// total-1-b-G, ... (the reverse of the amax launch's order, so the first reads find the amax's last tiles
+// in L2); thread 0 streams the bf16 tiles into a 3-deep ring; per tile the 128 row and 128 column scales
+// are computed into smem, every thread casts 8 rows x 8 columns twice, writes both code tiles into the
+// tile's own ring stage, and thread 0 sends them out by two TMA tensor stores (the stage is refilled one
+// tile later, after the stores have read it).
+// ---------------------------------------------------------------------------
+template <int FMT, int ST>
+__global__ void __launch_bounds__(256, 1) cast_rc_tma_kernel(const __grid_constant__ CastRCArgs a) {
+  constexpr int STAGE = 128 * 256;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  float* srow = reinterpret_cast<float*>(sm + ST * STAGE);
+  float* scol = srow + 128;
+  const uint32_t stage0 = smem_u32(sm), bar0 = smem_u32(sm + ST * STAGE + 1024);
+  const int t = threadIdx.x;
+  const int total = a.tstart[a.n];
+  const int G = (int)gridDim.x;
+  auto where = [&](int id, int& k, int& rt, int& ct) {
+    k = 0;
+    while (k + 1 < a.n && id >= a.tstart[k + 1]) ++k;
+    const int local = id - a.tstart[k];
+    rt = local / a.tiles_x[k];
+    ct = local - rt * a.tiles_x[k];
+  };
+  auto issue = [&](int k) {   // thread 0: the k-th tile of this CTA into stage k % ST
+    const int j = (int)blockIdx.x + k * G;
+    if (j < total) {
+      int kk, rt, ct;
+      where(total - 1 - j, kk, rt, ct);
+      const uint32_t bar = bar0 + 8 * (k % ST);
+      mbar_arrive_expect_tx(bar, STAGE);
+      tma_load_2d(stage0 + (k % ST) * STAGE, &a.in[kk], ct * 128, rt * 128, bar, l2_policy_evict_first());
+    }
+  };
+  if (t == 0) {
+    for (int i = 0; i < a.n; ++i) tma_prefetch_desc(&a.in[i]);
+    for (int i = 0; i < ST; ++i) mbar_init(bar0 + 8 * i, 1);
+    fence_mbar_init();
+    for (int k = 0; k < ST; ++k) issue(k);
+  }
+  __syncthreads();
+  const int cc = (t & 15) * 8, rbase = 8 * (t >> 4);
+  for (int k = 0;; ++k) {
+    const int j = (int)blockIdx.x + k * G;
+    if (j >= total) break;
+    int kk, rt, ct;
+    where(total - 1 - j, kk, rt, ct);
+    const int64_t r0 = (int64_t)rt * 128, c0 = (int64_t)ct * 128;
+    const int s = k % ST;
+    // this tile's scales (row t for t < 128, column t - 128 otherwise); the scale outputs are written by the
+    // tiles of the first tile column (rows) / first tile row (columns), as cast_tile_kernel does
+    if (t < 128) {
+      const float sc = scale_of<FMT>(a.amax_q[kk][r0 + t]);
+      srow[t] = sc;
+      if (ct == 0 && a.scale_q[kk]) a.scale_q[kk][r0 + t] = sc;
+    } else {
+      const float sc = scale_of<FMT>(a.amax_t[kk][c0 + t - 128]);
+      scol[t - 128] = sc;
+      if (rt == 0 && a.scale_t[kk]) a.scale_t[kk][c0 + t - 128] = sc;
+    }
+    mbar_wait(bar0 + 8 * s, (uint32_t)(k / ST) & 1u);
+    uint4 raw[8];
+    const uint8_t* sp = sm + s * STAGE + rbase * 256 + cc * 2;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) raw[i] = *reinterpret_cast<const uint4*>(sp + i * 256);
+    __syncthreads();                       // (1) stage read by every thread, scales visible
+    if (t == 0) {
+      fence_proxy_async_smem();
+      if (k > 0) {   // tile k-1's code stores were issued from its stage: refill it once they have read it
+        bulk_wait_read0();
+        issue(k - 1 + ST);
+      }
+    }
+    float sv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sv[q] = scol[cc + q];
+    uint8_t* dst = sm + s * STAGE;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float v[8];
+      const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        v[2 * q] = __uint_as_float(w[q] << 16);
+        v[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+      }
+      *reinterpret_cast<uint2*>(dst + (rbase + i) * 128 + cc) = cast8<FMT>(v, srow[rbase + i]);
+      *reinterpret_cast<uint2*>(dst + 16384 + (rbase + i) * 128 + cc) = cast8v<FMT>(v, sv);
+    }
+    fence_proxy_async_smem();
+    __syncthreads();                       // (2) both code tiles written; scales free for the next tile
+    if (t == 0) {
+      tma_store_2d(&a.oq[kk], stage0 + s * STAGE, (int)c0, (int)r0);
+      tma_store_2d(&a.ot[kk], stage0 + s * STAGE + 16384, (int)c0, (int)r0);
+      bulk_commit_group();
+    }
+  }
+  if (t == 0) bulk_wait_all0();
+}
+
+// ---------------------------------------------------------------------------
 // MXFP8 cast, dim0 (blocks of 32 along columns, row-major out) and dim1 (blocks
 // of 32 along rows, transposed out) from one read of a 128 x 128 tile.
 // E8M0 codes by integer exponent arithmetic (R-c12):
@@ -1675,6 +1778,67 @@ static cudaError_t cast_launch_t(const void* x, int64_t R, int64_t C, int64_t ld
   return cudaErrorInvalidValue;
 }
 
+// Rowwise (qm 2, tm 5) casts of bf16 tensors by cast_rc_tma_kernel; cudaErrorNotSupported when a tensor does
+// not fit the TMA path (the caller then launches the tile kernel).
+// Policy (knob cast_rc_tma): 1 = auto, launches of at most 12288 tiles (c3: every cast but the w1/w3 dY and the w2
+// X, W ones -- with two loads in flight per CTA the persistent kernel streams large tensors slower than the
+// 8-CTAs-per-SM tile kernel, but it saves the small launches' ramp and tail); 2 = always; 0 = never.
+static cudaError_t cast_rc_tma_launch(const CastMulti& m, int fmt, cudaStream_t s) {
+  auto enc = get_encode();
+  const int pol = knob(KNOB_CAST_RC_TMA);
+  if (!enc || pol == 0) return cudaErrorNotSupported;
+  if (pol == 1) {
+    int64_t tiles = 0;
+    for (int k = 0; k < m.n; ++k) tiles += ((m.R[k] + 127) / 128) * ((m.C[k] + 127) / 128);
+    if (tiles > 12288) return cudaErrorNotSupported;
+  }
+  CastRCArgs a{};
+  a.n = m.n;
+  for (int k = 0; k < m.n; ++k) {
+    const int64_t R = m.R[k], C = m.C[k], ld = m.ld[k];
+    if (R <= 0 || C <= 0 || R % 128 || C % 128 || (ld * 2) % 16 || !m.q[k] || !m.qt[k] ||
+        (reinterpret_cast<uintptr_t>(m.x[k]) & 15) || (reinterpret_cast<uintptr_t>(m.q[k]) & 15) ||
+        (reinterpret_cast<uintptr_t>(m.qt[k]) & 15))
+      return cudaErrorNotSupported;
+    cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)R};
+    cuuint64_t sin[1] = {(cuuint64_t)ld * 2}, sout[1] = {(cuuint64_t)C};
+    cuuint32_t box[2] = {128, 128};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc(&a.in[k], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(m.x[k]), dims, sin, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        enc(&a.oq[k], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, m.q[k], dims, sout, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        enc(&a.ot[k], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, m.qt[k], dims, sout, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorNotSupported;
+    const int64_t tiles = (R / 128) * (C / 128);
+    if ((int64_t)a.tstart[k] + tiles > (int64_t)INT32_MAX) return cudaErrorNotSupported;
+    a.tstart[k + 1] = a.tstart[k] + (int)tiles;
+    a.tiles_x[k] = (int)(C / 128);
+    a.amax_q[k] = m.amax_q[k];
+    a.amax_t[k] = m.amax_t[k];
+    a.scale_q[k] = m.scale_q[k];
+    a.scale_t[k] = m.scale_t[k];
+  }
+  constexpr int ST = 3;
+  constexpr int smem = ST * 128 * 256 + 1024 + 8 * ST;
+  const int64_t all = a.tstart[a.n];
+  if (all == 0) return cudaSuccess;
+  const int64_t cap = cap_grid((int64_t)sm_count() * 2);
+  const unsigned g = (unsigned)(all < cap ? all : cap);
+  cudaError_t e;
+  LaunchScope ls(K_CAST, s);
+  if (fmt == 0) {
+    if ((e = ensure_smem<cast_rc_tma_kernel<0, ST>>(smem)) != cudaSuccess) return e;
+    cast_rc_tma_kernel<0, ST><<<g, 256, smem, s>>>(a);
+  } else {
+    if ((e = ensure_smem<cast_rc_tma_kernel<1, ST>>(smem)) != cudaSuccess) return e;
+    cast_rc_tma_kernel<1, ST><<<g, 256, smem, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
 template <typename T, int FMT>
 static cudaError_t cast_dual_launch_t(const CastMulti& a, int qm, int tm, cudaStream_t s) {
   const unsigned g = (unsigned)a.tstart[a.n];
@@ -1699,6 +1863,10 @@ cudaError_t launch_cast_dual(CastMulti a, bool bf16, int fmt, int qm, int tm, cu
     if (a.tstart[k] + tiles > (int64_t)INT32_MAX) return cudaErrorInvalidValue;
     a.tstart[k + 1] = a.tstart[k] + (int)tiles;
   }
+  if (bf16 && qm == 2 && tm == 5) {
+    const cudaError_t e = cast_rc_tma_launch(a, fmt, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (bf16)
     return fmt == 0 ? cast_dual_launch_t<__nv_bfloat16, 0>(a, qm, tm, s) : cast_dual_launch_t<__nv_bfloat16, 1>(a, qm, tm, s);
   return fmt == 0 ? cast_dual_launch_t<float, 0>(a, qm, tm, s) : cast_dual_launch_t<float, 1>(a, qm, tm, s);
@@ -1707,6 +1875,14 @@ cudaError_t launch_cast_dual(CastMulti a, bool bf16, int fmt, int qm, int tm, cu
 cudaError_t launch_cast(const void* x, bool bf16, int fmt, int64_t R, int64_t C, int64_t ld, int qm, int tm,
                         const float* aq, const float* at, uint8_t* q, uint8_t* qt, float* sq, float* st,
                         cudaStream_t s, const Seg& seg) {
+  if (bf16 && qm == 2 && tm == 5 && !seg.offs && seg.seg_rows <= 0) {
+    CastMulti m{};
+    m.n = 1;
+    m.x[0] = x; m.R[0] = R; m.C[0] = C; m.ld[0] = ld; m.amax_q[0] = aq; m.amax_t[0] = at;
+    m.q[0] = q; m.qt[0] = qt; m.scale_q[0] = sq; m.scale_t[0] = st;
+    const cudaError_t e = cast_rc_tma_launch(m, fmt, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (bf16)
     return fmt == 0 ? cast_launch_t<__nv_bfloat16, 0>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s, seg)
                     : cast_launch_t<__nv_bfloat16, 1>(x, R, C, ld, qm, tm, aq, at, q, qt, sq, st, s, seg);

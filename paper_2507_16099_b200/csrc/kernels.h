@@ -46,6 +46,7 @@ enum Knob {
   KNOB_GEMM_L2HINT,         // A/B: L2 eviction hints on the GEMM operand loads (1 A evict_last, 2 + B evict_first, 3 + B normal)
   KNOB_GEMM_AFILL,          // 1: 256 x 512 tiles: per K step both N halves' MMAs, A kept in the tensor core's collector
   KNOB_MX_CAST_TSTORE,      // 1 (default): the MX ring cast (dim0 + row-major dim1) writes its codes by TMA tensor stores
+  KNOB_CAST_RC_TMA,         // rowwise casts of bf16 128-multiple tensors by the TMA-ring kernel with TMA stores: 1 auto (<= 12288 tiles), 2 always
   KNOB_WATCHDOG_MS,         // peer waits (P2P gather, fused reduce-scatter, async-TP) give up after this many ms
                             // and report FP8_ECUDA at the next call; 0 = wait forever
   KNOB_COUNT
@@ -166,6 +167,20 @@ struct CastMulti {
   int tstart[CAST_MULTI_MAX + 1];
 };
 using CastDual = CastMulti;
+// Rowwise casts (row-scaled codes + column-scaled codes, both row-major) of up to CAST_MULTI_MAX bf16 tensors by
+// the persistent TMA kernel (TMA loads and stores); filled by launch_cast_dual / launch_cast.
+struct CastRCArgs {
+  CUtensorMap in[CAST_MULTI_MAX];   // bf16 [R, C], 128 x 128 boxes
+  CUtensorMap oq[CAST_MULTI_MAX];   // u8 [R, C] row-scaled codes
+  CUtensorMap ot[CAST_MULTI_MAX];   // u8 [R, C] column-scaled codes
+  int n;
+  int tstart[CAST_MULTI_MAX + 1];
+  int tiles_x[CAST_MULTI_MAX];
+  const float* amax_q[CAST_MULTI_MAX];
+  const float* amax_t[CAST_MULTI_MAX];
+  float* scale_q[CAST_MULTI_MAX];
+  float* scale_t[CAST_MULTI_MAX];
+};
 cudaError_t launch_cast_dual(CastMulti a, bool bf16, int fmt, int qm, int tm, cudaStream_t s);
 // Tensorwise amax of n <= AMAX_MULTI_MAX tensors in one launch; out[t] (u32 bit patterns of
 // non-negative floats) must be zeroed by the caller.  chunk_start[t] = first warp chunk of

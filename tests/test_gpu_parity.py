@@ -1187,6 +1187,7 @@ LINEAR_BUFFER_CASES = [
     ("tensorwise", {"amax_bulk": 1, "tw_dual": 0}),
     ("rowwise", {}), ("rowwise", {"cast_grid": 3}), ("rowwise", {"cast_grid": 7}), ("rowwise", {"amax_rc": 0}),
     ("rowwise", {"amax_rc": 0, "amax_tile_tma": 0}), ("rowwise", {"amax_rc": 1, "cast_grid": 5}),
+    ("rowwise", {"cast_rc_tma": 0}), ("rowwise", {"cast_rc_tma": 2, "cast_grid": 3}),
     ("rowwise_gw_hp", {}),
     ("mxfp8", {}), ("mxfp8", {"cast_grid": 3}), ("mxfp8", {"mx_transposed": 1}), ("mxfp8", {"mx_cast_tma": 0}), ("mxfp8", {"mx_cast_ws": 1}), ("mxfp8", {"mx_cast_tstore": 0}),
     ("mxfp8", {"mx_cast_tstore": 0, "cast_grid": 3}),
@@ -1282,7 +1283,8 @@ def test_linear_buffers_bit_exact(recipe, knobs, shape, knob):
 
 @pytest.mark.parametrize("recipe,variants", [("tensorwise", [{}, {"tw_dual": 0}]),
                                              ("rowwise", [{}, {"cast_grid": 3}, {"cast_grid": 7}, {"amax_rc": 0},
-                                                          {"amax_rc": 0, "amax_tile_tma": 0}])])
+                                                          {"amax_rc": 0, "amax_tile_tma": 0}, {"cast_rc_tma": 0},
+                                                          {"cast_rc_tma": 0, "group_batch": 0}, {"cast_rc_tma": 2}])])
 def test_linear_cast_launch_variants_identical(recipe, variants, knob):
     """The cast-launch variants of one recipe write identical bytes (saved buffers and forward
     workspace) and give bit-identical Y, dX, dW (same codes -> same GEMM inputs)."""
@@ -1674,7 +1676,8 @@ def test_amax_tensor_kernels(shape, dtype, bulk, knob):
 
 
 SHARED_CASES = [("tensorwise", {}), ("tensorwise", {"tw_dual": 0}), ("rowwise", {}), ("rowwise", {"amax_rc": 0, "amax_tile_tma": 0}),
-                ("rowwise", {"cast_grid": 5}), ("rowwise", {"group_batch": 0}), ("rowwise_gw_hp", {}), ("mxfp8", {}), ("mxfp8", {"mx_transposed": 1})]
+                ("rowwise", {"cast_grid": 5}), ("rowwise", {"group_batch": 0}), ("rowwise", {"cast_rc_tma": 0}),
+                ("rowwise_gw_hp", {}), ("mxfp8", {}), ("mxfp8", {"mx_transposed": 1})]
 
 
 @pytest.mark.parametrize("M,K,Ns", [(384, 512, (640, 128, 256)), (256, 384, (128, 512)), (384, 256, (384,)),
