@@ -162,6 +162,22 @@ def test_argument_errors_return_before_any_launch(L):
                                        None) == L.FP8_EINVAL
 
 
+def test_shared_workspace_holds_batched_amax_scratch(L):
+    """Rowwise shared-input groups cast X and every W_i (and every dY_i) in one batched launch, so their
+    workspace holds, beside the members' FP8 operands, a row and a column amax slot per tensor:
+    forward M + K + sum(N_i) + n K floats, backward n M + sum(N_i) floats (host-only size query)."""
+    cfg = L.LinearCfg(L.RECIPE_ROWWISE, L.E4M3, L.E5M2, L.MX_FLOOR, L.DT_BF16)
+    M, K, Ns = 1024, 512, (384, 128, 256)
+    n, S = len(Ns), sum(Ns)
+    need = L.lib.fp8_linear_shared_workspace_bytes(ctypes.byref(cfg), M, K, n, (ctypes.c_int64 * n)(*Ns))
+    fwd_codes = M * K + S * K                      # X's and every W_i's forward codes
+    bwd_codes = 2 * M * S                          # every dY_i's row- and column-scaled codes
+    assert need >= fwd_codes + 4 * (M + K + S + n * K)
+    assert need >= bwd_codes + 4 * (n * M + S)
+    cfg.recipe = L.RECIPE_TENSORWISE               # no batched rowwise scratch for the other recipes
+    assert L.lib.fp8_linear_shared_workspace_bytes(ctypes.byref(cfg), M, K, n, (ctypes.c_int64 * n)(*Ns)) < need
+
+
 def test_knobs_host_only(L):
     """fp8_set_knob / fp8_get_knob / fp8_reset_knobs (host-only, no GPU): every knob the header documents
     exists with its documented default, out-of-range values and unknown names are rejected without
