@@ -92,18 +92,27 @@ __device__ __forceinline__ int seg_of(const Seg& sg, int64_t r0, int64_t& start)
 }
 __device__ __forceinline__ uint32_t abs_bits(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
 
+// x * s rounded to fp32 (IEEE RN, R-c4) two lanes per instruction (__fmul2_rn), then satRNE to FP8.
 template <int FMT>
 __device__ __forceinline__ uint2 cast8(const float (&v)[8], float s) {
   float p[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) p[i] = __fmul_rn(v[i], s);
+  for (int i = 0; i < 8; i += 2) {
+    const float2 q = __fmul2_rn(make_float2(v[i], v[i + 1]), make_float2(s, s));
+    p[i] = q.x;
+    p[i + 1] = q.y;
+  }
   return make_uint2(cvt_x4<FMT>(p[0], p[1], p[2], p[3]), cvt_x4<FMT>(p[4], p[5], p[6], p[7]));
 }
 template <int FMT>
 __device__ __forceinline__ uint2 cast8v(const float (&v)[8], const float* s) {
   float p[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) p[i] = __fmul_rn(v[i], s[i]);
+  for (int i = 0; i < 8; i += 2) {
+    const float2 q = __fmul2_rn(make_float2(v[i], v[i + 1]), make_float2(s[i], s[i + 1]));
+    p[i] = q.x;
+    p[i + 1] = q.y;
+  }
   return make_uint2(cvt_x4<FMT>(p[0], p[1], p[2], p[3]), cvt_x4<FMT>(p[4], p[5], p[6], p[7]));
 }
 
