@@ -701,12 +701,18 @@ __device__ __forceinline__ void cast_tile_body(const T* __restrict__ x, int64_t 
   };
   const int cc = (t & 15) * 8;
   const bool cvalid = cc < vcols;
+  // row (t >> 4) of the tile; row (t >> 4) + 16 i is 16 i rows further (64-bit products formed once)
+  // (32-bit row offsets: 7 x 16 rows x ld elements stays far below 2^32 for any tensor the library accepts)
+  const T* xrow = x + (r0 + (t >> 4)) * ld + c0 + cc;
+  const uint32_t xstep = 16u * (uint32_t)ld;
   Raw8<T> raw[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int rr = (t >> 4) + 16 * i;
-    if (cvalid && rr < vrows) raw[i].load(x + (r0 + rr) * ld + c0 + cc);
+    if (cvalid && rr < vrows) raw[i].load(xrow + (uint32_t)i * xstep);
   }
+  const int64_t orow = (r0 + (t >> 4)) * C + c0 + cc;
+  const uint32_t ostep = 16u * (uint32_t)C;
   fill(QM, amax_q, sq, scale_q);
   fill(TM, amax_t, st, scale_t);
   __syncthreads();
@@ -722,14 +728,14 @@ __device__ __forceinline__ void cast_tile_body(const T* __restrict__ x, int64_t 
       if (QM == 1) bq = cast8<FMT>(v, sq[0]);
       if (QM == 2) bq = cast8<FMT>(v, sq[rr]);
       if (QM == 3) bq = cast8v<FMT>(v, &sq[cc]);
-      *reinterpret_cast<uint2*>(q + (r0 + rr) * C + c0 + cc) = bq;
+      *reinterpret_cast<uint2*>(q + orow + (uint32_t)i * ostep) = bq;
     }
     if (TM != 0) {
       if (TM == QM) bt = bq;
       else if (TM == 1) bt = cast8<FMT>(v, st[0]);
       else if (TM == 2) bt = cast8<FMT>(v, st[rr]);
       else bt = cast8v<FMT>(v, &st[cc]);
-      if (TRM) *reinterpret_cast<uint2*>(qt + (r0 + rr) * C + c0 + cc) = bt;
+      if (TRM) *reinterpret_cast<uint2*>(qt + orow + (uint32_t)i * ostep) = bt;
       else *reinterpret_cast<uint2*>(&tile[swz(rr, cc >> 2)]) = bt;
     }
   }
@@ -776,8 +782,9 @@ __global__ void __launch_bounds__(256) cast_tile_dual_kernel(const __grid_consta
 // tile's own ring stage, and thread 0 sends them out by two TMA tensor stores (the stage is refilled one
 // tile later, after the stores have read it).
 // ---------------------------------------------------------------------------
-template <int FMT, int ST>
-__global__ void __launch_bounds__(256, 1) cast_rc_tma_kernel(const __grid_constant__ CastRCArgs a) {
+template <int FMT, int ST, int NT>   // NT threads: 256 (2 CTAs per SM) or 512 (1 CTA per SM, deeper ring)
+__global__ void __launch_bounds__(NT, 1) cast_rc_tma_kernel(const __grid_constant__ CastRCArgs a) {
+  constexpr int RPT = 2048 / NT;   // rows per thread (8 columns each)
   constexpr int STAGE = 128 * 256;
   extern __shared__ __align__(1024) uint8_t sm[];
   float* srow = reinterpret_cast<float*>(sm + ST * STAGE);
@@ -810,7 +817,7 @@ __global__ void __launch_bounds__(256, 1) cast_rc_tma_kernel(const __grid_consta
     for (int k = 0; k < ST; ++k) issue(k);
   }
   __syncthreads();
-  const int cc = (t & 15) * 8, rbase = 8 * (t >> 4);
+  const int cc = (t & 15) * 8, rbase = RPT * (t >> 4);
   for (int k = 0;; ++k) {
     const int j = (int)blockIdx.x + k * G;
     if (j >= total) break;
@@ -824,16 +831,16 @@ __global__ void __launch_bounds__(256, 1) cast_rc_tma_kernel(const __grid_consta
       const float sc = scale_of<FMT>(a.amax_q[kk][r0 + t]);
       srow[t] = sc;
       if (ct == 0 && a.scale_q[kk]) a.scale_q[kk][r0 + t] = sc;
-    } else {
+    } else if (t < 256) {
       const float sc = scale_of<FMT>(a.amax_t[kk][c0 + t - 128]);
       scol[t - 128] = sc;
       if (rt == 0 && a.scale_t[kk]) a.scale_t[kk][c0 + t - 128] = sc;
     }
     mbar_wait(bar0 + 8 * s, (uint32_t)(k / ST) & 1u);
-    uint4 raw[8];
+    uint4 raw[RPT];
     const uint8_t* sp = sm + s * STAGE + rbase * 256 + cc * 2;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) raw[i] = *reinterpret_cast<const uint4*>(sp + i * 256);
+    for (int i = 0; i < RPT; ++i) raw[i] = *reinterpret_cast<const uint4*>(sp + i * 256);
     __syncthreads();                       // (1) stage read by every thread, scales visible
     if (t == 0) {
       fence_proxy_async_smem();
@@ -847,7 +854,7 @@ __global__ void __launch_bounds__(256, 1) cast_rc_tma_kernel(const __grid_consta
     for (int q = 0; q < 8; ++q) sv[q] = scol[cc + q];
     uint8_t* dst = sm + s * STAGE;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < RPT; ++i) {
       float v[8];
       const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
 #pragma unroll
@@ -1830,20 +1837,34 @@ static cudaError_t cast_rc_tma_launch(const CastMulti& m, int fmt, cudaStream_t 
     a.scale_q[k] = m.scale_q[k];
     a.scale_t[k] = m.scale_t[k];
   }
-  constexpr int ST = 3;
-  constexpr int smem = ST * 128 * 256 + 1024 + 8 * ST;
   const int64_t all = a.tstart[a.n];
   if (all == 0) return cudaSuccess;
-  const int64_t cap = cap_grid((int64_t)sm_count() * 2);
-  const unsigned g = (unsigned)(all < cap ? all : cap);
   cudaError_t e;
   LaunchScope ls(K_CAST, s);
+  if (knob(KNOB_CAST_RC_WIDE) == 1) {   // 1 CTA of 512 threads per SM, 5-deep ring (four loads in flight)
+    constexpr int ST = 5;
+    constexpr int smem = ST * 128 * 256 + 1024 + 8 * ST;
+    const int64_t cap = cap_grid((int64_t)sm_count());
+    const unsigned g = (unsigned)(all < cap ? all : cap);
+    if (fmt == 0) {
+      if ((e = ensure_smem<cast_rc_tma_kernel<0, ST, 512>>(smem)) != cudaSuccess) return e;
+      cast_rc_tma_kernel<0, ST, 512><<<g, 512, smem, s>>>(a);
+    } else {
+      if ((e = ensure_smem<cast_rc_tma_kernel<1, ST, 512>>(smem)) != cudaSuccess) return e;
+      cast_rc_tma_kernel<1, ST, 512><<<g, 512, smem, s>>>(a);
+    }
+    return cudaGetLastError();
+  }
+  constexpr int ST = 3;
+  constexpr int smem = ST * 128 * 256 + 1024 + 8 * ST;
+  const int64_t cap = cap_grid((int64_t)sm_count() * 2);
+  const unsigned g = (unsigned)(all < cap ? all : cap);
   if (fmt == 0) {
-    if ((e = ensure_smem<cast_rc_tma_kernel<0, ST>>(smem)) != cudaSuccess) return e;
-    cast_rc_tma_kernel<0, ST><<<g, 256, smem, s>>>(a);
+    if ((e = ensure_smem<cast_rc_tma_kernel<0, ST, 256>>(smem)) != cudaSuccess) return e;
+    cast_rc_tma_kernel<0, ST, 256><<<g, 256, smem, s>>>(a);
   } else {
-    if ((e = ensure_smem<cast_rc_tma_kernel<1, ST>>(smem)) != cudaSuccess) return e;
-    cast_rc_tma_kernel<1, ST><<<g, 256, smem, s>>>(a);
+    if ((e = ensure_smem<cast_rc_tma_kernel<1, ST, 256>>(smem)) != cudaSuccess) return e;
+    cast_rc_tma_kernel<1, ST, 256><<<g, 256, smem, s>>>(a);
   }
   return cudaGetLastError();
 }

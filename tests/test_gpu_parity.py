@@ -1188,6 +1188,7 @@ LINEAR_BUFFER_CASES = [
     ("rowwise", {}), ("rowwise", {"cast_grid": 3}), ("rowwise", {"cast_grid": 7}), ("rowwise", {"amax_rc": 0}),
     ("rowwise", {"amax_rc": 0, "amax_tile_tma": 0}), ("rowwise", {"amax_rc": 1, "cast_grid": 5}),
     ("rowwise", {"cast_rc_tma": 0}), ("rowwise", {"cast_rc_tma": 2, "cast_grid": 3}),
+    ("rowwise", {"cast_rc_tma": 2, "cast_rc_wide": 1}), ("rowwise", {"cast_rc_tma": 2, "cast_rc_wide": 1, "cast_grid": 2}),
     ("rowwise_gw_hp", {}),
     ("mxfp8", {}), ("mxfp8", {"cast_grid": 3}), ("mxfp8", {"mx_transposed": 1}), ("mxfp8", {"mx_cast_tma": 0}), ("mxfp8", {"mx_cast_ws": 1}), ("mxfp8", {"mx_cast_tstore": 0}),
     ("mxfp8", {"mx_cast_tstore": 0, "cast_grid": 3}),
