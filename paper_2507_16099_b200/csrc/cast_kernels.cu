@@ -429,12 +429,9 @@ __global__ void __launch_bounds__(288) amax_rc_kernel(const __grid_constant__ Am
   const uint32_t full0 = base + ST * STAGE, empty0 = full0 + 8 * ST;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int total = a.tstart[a.n];
-  // dbg bit 1 (A/B only): tiles handed out interleaved (CTA b: b, b + G, ...) instead of contiguous ranges
-  const bool ilv = a.dbg & 2;
-  const int per = ilv ? 1 : (total + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int first = ilv ? (int)blockIdx.x : (int)blockIdx.x * per;
-  const int last = ilv ? total : min(first + per, total);
-  const int step = ilv ? (int)gridDim.x : 1;
+  const int per = (total + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int first = (int)blockIdx.x * per;
+  const int last = min(first + per, total);
   if (t == 0) {
     for (int i = 0; i < ST; ++i) {
       mbar_init(full0 + 8 * i, 1);
@@ -443,25 +440,43 @@ __global__ void __launch_bounds__(288) amax_rc_kernel(const __grid_constant__ Am
     fence_mbar_init();
   }
   __syncthreads();
-  auto where = [&](int id, int& k, int& rt, int& ct) {
-    k = 0;
-    while (k + 1 < a.n && id >= a.tstart[k + 1]) ++k;
-    const int local = id - a.tstart[k];
-    rt = local / a.tiles_x[k];
-    ct = local - rt * a.tiles_x[k];
+  // The CTA's tiles [first, last) in row-major order over each tensor's tile grid, tensor after tensor: one
+  // division to place the first tile, then a cursor (no per-tile division or search).
+  struct Cursor {
+    int k, rt, ct, id;
+  };
+  auto start = [&](int id) {
+    Cursor c{0, 0, 0, id};
+    while (c.k + 1 < a.n && id >= a.tstart[c.k + 1]) ++c.k;
+    const int local = id - a.tstart[c.k];
+    c.rt = local / a.tiles_x[c.k];
+    c.ct = local - c.rt * a.tiles_x[c.k];
+    return c;
+  };
+  auto advance = [&](Cursor& c) {
+    ++c.id;
+    if (++c.ct == a.tiles_x[c.k]) {
+      c.ct = 0;
+      ++c.rt;
+    }
+    if (c.k + 1 < a.n && c.id == a.tstart[c.k + 1]) {
+      ++c.k;
+      c.rt = 0;
+      c.ct = 0;
+    }
   };
   if (warp == 8) {   // producer
     if (lane == 0) {
       for (int i = 0; i < a.n; ++i) tma_prefetch_desc(&a.map[i]);
       const uint64_t pol = l2_policy_evict_first();
-      for (int k = 0; first + k * step < last; ++k) {
+      Cursor cur = start(first);
+      for (int k = 0; first + k < last; ++k, advance(cur)) {
         const int s = k % ST;
         if (k >= ST) {
           mbar_wait_opt(empty0 + 8 * s, (uint32_t)(k / ST - 1) & 1u, a.sleep);
           fence_proxy_async_smem();
         }
-        int kk, rt, ct;
-        where(first + k * step, kk, rt, ct);
+        const int kk = cur.k, rt = cur.rt, ct = cur.ct;
         mbar_arrive_expect_tx(full0 + 8 * s, STAGE);
         tma_load_2d(base + s * STAGE, &a.map[kk], ct * 128, rt * 128, full0 + 8 * s, pol);
         tma_load_2d(base + s * STAGE + BOX, &a.map[kk], ct * 128 + 64, rt * 128, full0 + 8 * s, pol);
@@ -484,16 +499,18 @@ __global__ void __launch_bounds__(288) amax_rc_kernel(const __grid_constant__ Am
       rm[i] = 0;
     }
   };
-  for (int k = 0; first + k * step < last; ++k) {
-    int kk, rt, ct;
-    where(first + k * step, kk, rt, ct);
-    if (a.dbg & 1) {   // A/B only: consume nothing (the TMA stream alone), results invalid
+  if (a.dbg & 1) {   // A/B only: consume nothing (the TMA stream alone), results invalid
+    for (int k = 0; first + k < last; ++k) {
       const int s = k % ST;
       mbar_wait_opt(full0 + 8 * s, (uint32_t)(k / ST) & 1u, a.sleep);
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8 * s);
-      continue;
     }
+    return;
+  }
+  Cursor cur = start(first);
+  for (int k = 0; first + k < last; ++k, advance(cur)) {
+    const int kk = cur.k, rt = cur.rt, ct = cur.ct;
     if (MODE & 2) {
       const int skey = a.strip0[kk] + rt;
       if (skey != strip) {

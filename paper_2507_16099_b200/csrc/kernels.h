@@ -36,7 +36,7 @@ enum Knob {
   KNOB_MX_CAST_OCC3,        // 1: MX cast (dim0 + dim1, row-major dim1) with a 2-deep ring at 3 CTAs per SM
   KNOB_AMAX_BULK,           // 1: tensorwise amax of contiguous tensors through 1-D bulk copies into a smem ring
   KNOB_AMAX_RC,             // 1: row / column amax by amax_rc_kernel (no CTA barrier per tile, multi-tensor)
-  KNOB_AMAX_RC_DEBUG,       // A/B only: bit 0 consumers skip the tile (results invalid), bit 1 interleaved tile order
+  KNOB_AMAX_RC_DEBUG,       // A/B only: bit 0 consumers skip the tile (results invalid)
   KNOB_GROUP_BATCH,         // 1: a rowwise shared-input group's amax / cast launches batched over X + every W_i (fwd), every dY_i (bwd)
   KNOB_MX_CAST_DEBUG,       // A/B only: bit 0 the MX TMA cast skips its code stores (results invalid)
   KNOB_MX_CAST_WS,          // 1: bf16 MX casts with row-major dim1 copies by the warp-specialised kernel (0: the ring kernel)
