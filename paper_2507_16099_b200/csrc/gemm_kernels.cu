@@ -822,14 +822,24 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = 0.f;
         } else if (row_scales) {
-          // lane j computes 1/sb for column col0 + j once; the warp shares them by shuffles
+          // lane j computes 1/sb for column col0 + j once; the warp shares them by shuffles.  Two columns per
+          // __fmul2_rn (IEEE RN per lane: the same roundings, in the same order, as two __fmul_rn)
           const float rcol = __frcp_rn(sb[min(col0 + (int)lane, N - 1)]);
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            v[j] = __fmul_rn(__fmul_rn(__uint_as_float(r[j]), rs), __shfl_sync(0xffffffffu, rcol, j));
+          for (int j = 0; j < 32; j += 2) {
+            const float2 a2 = __fmul2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), make_float2(rs, rs));
+            const float2 c2 = make_float2(__shfl_sync(0xffffffffu, rcol, j), __shfl_sync(0xffffffffu, rcol, j + 1));
+            const float2 p2 = __fmul2_rn(a2, c2);
+            v[j] = p2.x;
+            v[j + 1] = p2.y;
+          }
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__uint_as_float(r[j]), rs);
+          for (int j = 0; j < 32; j += 2) {
+            const float2 p2 = __fmul2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), make_float2(rs, rs));
+            v[j] = p2.x;
+            v[j + 1] = p2.y;
+          }
         }
         const int nvalid = min(32, N - col0);  // 16 or 32 (N % 16 == 0)
         if (out_f32) {
@@ -924,11 +934,19 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
             if (row_scales) {
               const float rcol = __frcp_rn(sb[col0 + 32 * c + (int)lane]);
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                v[j] = __fmul_rn(__fmul_rn(__uint_as_float(r[j]), rs), __shfl_sync(0xffffffffu, rcol, j));
+              for (int j = 0; j < 32; j += 2) {
+                const float2 a2 = __fmul2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), make_float2(rs, rs));
+                const float2 p2 = __fmul2_rn(a2, make_float2(__shfl_sync(0xffffffffu, rcol, j), __shfl_sync(0xffffffffu, rcol, j + 1)));
+                v[j] = p2.x;
+                v[j + 1] = p2.y;
+              }
             } else {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__uint_as_float(r[j]), rs);
+              for (int j = 0; j < 32; j += 2) {
+                const float2 p2 = __fmul2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), make_float2(rs, rs));
+                v[j] = p2.x;
+                v[j + 1] = p2.y;
+              }
             }
             uint32_t pk[16];
 #pragma unroll
