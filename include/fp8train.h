@@ -573,6 +573,7 @@ uint64_t fp8_launch_count(void);
  *   mx_cast_tstore (1: the MX ring cast writes its dim0 / row-major dim1 codes by TMA tensor stores; 0: st.global) |
  *   cast_rc_tma (1: rowwise casts of launches up to 12288 tiles by the persistent TMA kernel with TMA stores;
  *   2: always; 0: never) |
+ *   cast_rc_wide (0; A/B) | gemm_epi_tma (0; 1 = 256-wide GEMM tiles write bf16 outputs by TMA stores) |
  *   watchdog_ms (30000; 0 = peer waits never give up)
  *   -- defaults in parentheses.
  * A knob changes launches enqueued after the call.  Unknown name or out-of-range value:

@@ -36,7 +36,7 @@ static const KnobDef kKnobs[KNOB_COUNT] = {
     {"mx_cast_occ3", 0, 0, 1},      {"amax_bulk", 1, 0, 1},        {"amax_rc", 1, 0, 1},
     {"amax_rc_debug", 0, 0, 1},     {"group_batch", 1, 0, 1},
     {"mx_cast_debug", 0, 0, 1},     {"mx_cast_ws", 0, 0, 1},        {"gemm_st_ef", 0, 0, 1},
-    {"wait_sleep", 0, 0, 15},       {"gemm_l2hint", 0, 0, 3},       {"gemm_afill", 0, 0, 1},        {"mx_cast_tstore", 1, 0, 1},     {"cast_rc_tma", 1, 0, 2},        {"cast_rc_wide", 0, 0, 1},
+    {"wait_sleep", 0, 0, 15},       {"gemm_l2hint", 0, 0, 3},       {"gemm_afill", 0, 0, 1},        {"mx_cast_tstore", 1, 0, 1},     {"cast_rc_tma", 1, 0, 2},        {"cast_rc_wide", 0, 0, 1},       {"gemm_epi_tma", 0, 0, 1},
     {"watchdog_ms", 30000, 0, 1 << 30},
 };
 static std::atomic<int> g_knobs[KNOB_COUNT];

@@ -64,7 +64,8 @@ struct Prob {
   const float* sa; const float* sb;
   void* D; int64_t ldd;
   int out_f32, row_scales;
-  int d_tma;          // N = 512 bf16 epilogue: D written by TMA stores through the map in the tSA slot
+  int d_tma;          // bf16 epilogue writing D by TMA stores through map slot 4 (N = 512 tiles; 256-wide tiles with
+                      // knob gemm_epi_tma)
   int a_mn, b_mn;     // operand majors (MN-major: TMA boxes 128 MN x 128 K, K step 4 KB)
   uint32_t* out_amax; // optional: atomicMax of |D| bit patterns (amax of the stored output values)
   int raster;         // tile raster of this problem (see tile_coords / choose_raster)
@@ -98,7 +99,7 @@ struct Prob {
 // (MoE) launches carry at most two problems, whose tile counts are known on the device only.
 constexpr int MAXP = GEMM_MAX_PROBS;
 struct alignas(64) GemmMaps {
-  CUtensorMap m[MAXP][4];   // per problem: A, B, SFA (N = 512 bf16: the D map), SFB
+  CUtensorMap m[MAXP][5];   // per problem: A, B, SFA, SFB, D (bf16 output map of the TMA-store epilogue)
 };
 struct GemmArgs {
   Prob p[MAXP];
@@ -891,6 +892,45 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
         __syncwarp();
       };
 
+      // 256-wide tiles with knob gemm_epi_tma: a 32-column chunk of this warp's 32 rows is scaled into the warp's
+      // single 2 KB smem buffer (SWIZZLE_64B rows of 64 B) and leaves by one TMA store; the buffer is reused once
+      // the previous store has read it
+      const int row_base_w = mb * BM * CG + (int)crank * BM + q * 32;
+      auto tma_chunk = [&](const uint32_t (&r)[32], int colc) {
+        if (colc >= N || (args.debug & 1)) return;   // warp-uniform
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // buffer free
+        __syncwarp();
+        const float rcol = row_scales ? __frcp_rn(sb[min(colc + (int)lane, N - 1)]) : 1.f;
+        const int nvalid = min(32, N - colc);
+        uint32_t m2 = 0;
+        uint8_t* buf = epi + lane * 64;
+        // 8 columns at a time: scale (two per __fmul2_rn), convert, one 16-byte smem store -- few live registers
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint32_t w[4];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int jc = 8 * u + 2 * jj;
+            float2 p2 = __fmul2_rn(make_float2(__uint_as_float(r[jc]), __uint_as_float(r[jc + 1])), make_float2(rs, rs));
+            if (row_scales)
+              p2 = __fmul2_rn(p2, make_float2(__shfl_sync(0xffffffffu, rcol, jc), __shfl_sync(0xffffffffu, rcol, jc + 1)));
+            __nv_bfloat162 hv = __floats2bfloat162_rn(p2.x, p2.y);
+            w[jj] = *reinterpret_cast<uint32_t*>(&hv);
+            if (P.out_amax && jc < nvalid) m2 = __vmaxu2(m2, w[jj] & 0x7FFF7FFFu);
+          }
+          *reinterpret_cast<uint4*>(buf + ((u ^ (int)((lane >> 1) & 3)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        if (P.out_amax && rvalid) dmax = max(dmax, max(m2 & 0xFFFFu, m2 >> 16) << 16);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const CUtensorMap* dm = &maps.m[ti.pi][4];
+          if (st_ef) tma_store_2d_hint(dm, epi_s, colc, (int)(ti.d_row0 + row_base_w), st_pol);
+          else tma_store_2d(dm, epi_s, colc, (int)(ti.d_row0 + row_base_w));
+          bulk_commit_group();
+        }
+      };
+
       // this warp's accumulator barrier: per buffer, or per half of the N = 512 accumulator
       // (N = 512: the halves are awaited one by one below)
       if (L::HALVES == 1) {
@@ -916,7 +956,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
         // bf16 outputs are scaled into one of this warp's two 2 KB smem chunks and written by a TMA store each,
         // so the warp never waits on global writes (which compete with the operand loads for L2) before it
         // releases TMEM; a chunk buffer is reused once its previous store has been read out of smem.
-        const CUtensorMap* dmap = &maps.m[ti.pi][2];
+        const CUtensorMap* dmap = &maps.m[ti.pi][4];
         const bool tma_out = P.d_tma;
         const int row_base = mb * BM * CG + (int)crank * BM + q * 32;
         for (int h = 0; h < 2; ++h) {
@@ -1006,15 +1046,21 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
           if (CG == 2) mbar_arrive_cluster(tempty_leader + 8 * acc);
           else mbar_arrive(tempty_bar + 8 * acc);
         }
+        if (L::HALVES == 1 && P.d_tma) {
 #pragma unroll
-        for (int c = 0; c < HC; ++c) process(r[c], nb * L::BN + half * (L::BN / 2) + c * 32);
+          for (int c = 0; c < HC; ++c) tma_chunk(r[c], nb * L::BN + half * (L::BN / 2) + c * 32);
+        } else {
+#pragma unroll
+          for (int c = 0; c < HC; ++c) process(r[c], nb * L::BN + half * (L::BN / 2) + c * 32);
+        }
       } else {
 #pragma unroll 1
         for (int c = 0; c < L::BN / 32; ++c) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(tbase + c * 32, r);
           tmem_wait_ld();
-          process(r, nb * L::BN + c * 32);
+          if (L::HALVES == 1 && P.d_tma) tma_chunk(r, nb * L::BN + c * 32);
+          else process(r, nb * L::BN + c * 32);
         }
         tc_fence_before();
         __syncwarp();
@@ -1040,7 +1086,7 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
       }
       if (++acc == L::ACC) { acc = 0; acc_phase ^= 1; }
     }
-    if (L::HALVES == 2 && lane == 0) bulk_wait_all0();   // this warp's TMA stores are complete
+    if (lane == 0) bulk_wait_all0();   // this warp's TMA stores (if any) are complete
   }
 
   tc_fence_before();
@@ -1119,7 +1165,7 @@ static bool make_sf_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K
 }
 
 template <bool MX, int CG, int ST, int KS, bool BF, bool GRP, bool E8, int BNT>
-static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
+static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[5]) {
   // grouped 1: B holds G experts (K-major: G*N rows; MN-major: G*K contraction rows)
   const int64_t bN = p.grouped == 1 && !p.b_mn ? p.G * p.N : p.N;
   const int64_t bK = p.grouped == 1 && p.b_mn ? p.G * p.K : p.K;
@@ -1129,10 +1175,12 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
   if (MX) {
     if (!make_sf_map(&maps[2], p.sa, p.M, p.K, KS) || !make_sf_map(&maps[3], p.sb, p.N, p.K, KS)) return false;
   } else {
-    maps[2] = maps[0];   // unused by the plain FP8 kinds (N = 512: the D map for the TMA-store epilogue)
+    maps[2] = maps[0];   // unused by the plain FP8 kinds
     maps[3] = maps[1];
   }
-  const bool d_tma = BNT == 512 && !p.out_f32 && !p.rs_bufs && !p.grouped;
+  maps[4] = maps[0];
+  const bool d_tma = (BNT == 512 || knob(KNOB_GEMM_EPI_TMA) == 1) && !p.out_f32 && !p.rs_bufs && !p.grouped &&
+                     p.ldd % 8 == 0 && (reinterpret_cast<uintptr_t>(p.D) & 15) == 0;
   if (d_tma) {   // D bf16 [M, N] (row stride ldd), boxes of 32 rows x 32 columns, SWIZZLE_64B
     auto enc = get_encode();
     if (!enc) return false;
@@ -1140,7 +1188,7 @@ static bool setup_prob(const GemmProblem& p, Prob& P, CUtensorMap maps[4]) {
     cuuint64_t strides[1] = {(cuuint64_t)p.ldd * 2};
     cuuint32_t box[2] = {32, 32};
     cuuint32_t estr[2] = {1, 1};
-    if (enc(&maps[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p.D, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    if (enc(&maps[4], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p.D, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
   }

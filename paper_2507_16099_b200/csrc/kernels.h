@@ -48,6 +48,7 @@ enum Knob {
   KNOB_MX_CAST_TSTORE,      // 1 (default): the MX ring cast (dim0 + row-major dim1) writes its codes by TMA tensor stores
   KNOB_CAST_RC_TMA,         // rowwise casts of bf16 128-multiple tensors by the TMA-ring kernel with TMA stores: 1 auto (<= 12288 tiles), 2 always
   KNOB_CAST_RC_WIDE,        // A/B: the rowwise TMA cast as 1 CTA of 512 threads per SM with a 5-deep ring
+  KNOB_GEMM_EPI_TMA,        // 1: 256-wide GEMM tiles with bf16 outputs store them by TMA (one 2 KB chunk buffer per warp)
   KNOB_WATCHDOG_MS,         // peer waits (P2P gather, fused reduce-scatter, async-TP) give up after this many ms
                             // and report FP8_ECUDA at the next call; 0 = wait forever
   KNOB_COUNT

@@ -213,15 +213,19 @@ def _grid_operands(M, N, K, seed=0):
     return a, b
 
 
-@pytest.fixture(params=["2", "2e4", "2rr", "2s6", "1"],
-                ids=["cta_pair", "cta_pair_epi4", "cta_pair_roundrobin", "cta_pair_1atom", "single_cta"])
+@pytest.fixture(params=["2", "2e4", "2rr", "2s6", "1", "2tma", "2e4tma"],
+                ids=["cta_pair", "cta_pair_epi4", "cta_pair_roundrobin", "cta_pair_1atom", "single_cta",
+                     "cta_pair_tma_store", "cta_pair_epi4_tma_store"])
 def cta_group(request, knob):
     """Run a GEMM test with each kernel variant: CTA pair (cta_group::2) with 2-atom stages
     (default: 8 epilogue warps at K <= 1024, dynamic tile scheduler), the same with 4 epilogue
-    warps (the long-K default), with static round-robin tiles, CTA pair with 1-atom stages, single CTA."""
+    warps (the long-K default), with static round-robin tiles, CTA pair with 1-atom stages, single CTA,
+    and the CTA pair with bf16 outputs written by TMA stores (knob gemm_epi_tma; 8 and 4 epilogue warps)."""
     knob("gemm_cta_group", int(request.param[0]))
     knob("gemm_stages", 6 if request.param == "2s6" else 3)
-    if request.param == "2e4":
+    if request.param.endswith("tma"):
+        knob("gemm_epi_tma", 1)
+    if request.param in ("2e4", "2e4tma"):
         knob("gemm_epi", 4)
     if request.param == "2rr":   # static round-robin tiles instead of the dynamic scheduler
         knob("gemm_sched", 0)
