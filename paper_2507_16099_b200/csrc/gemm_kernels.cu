@@ -1104,11 +1104,13 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
 // The tensor-map encode is a driver-API call and fails with CUDA_ERROR_INVALID_CONTEXT on a thread that
 // has no current context yet -- e.g. PyTorch's autograd worker when an MX backward is its first CUDA work
 // (the runtime binds the device's primary context to a thread only at its first context-using call).
-// One cheap runtime call per thread binds it.
+// cudaSetDevice on the thread's current device binds it (CUDA 12: it initialises and makes current the
+// primary context; unlike cudaFree it is not a memory operation, so it is harmless inside a stream capture).
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   thread_local bool bound = false;
   if (!bound) {
-    cudaFree(nullptr);
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaSetDevice(dev);
     bound = true;
   }
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
