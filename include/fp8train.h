@@ -118,7 +118,8 @@ typedef enum {
   FP8_RECIPE_ROWWISE_GW_HP = 3   /* rowwise, but dL/dW stays in bfloat16 */
 } fp8_recipe_t;
 
-/* High-precision input matrix: row-major, `ld` in elements (>= cols). */
+/* High-precision input matrix: row-major, `ld` in elements (cols <= ld <= 2^25; rows, cols multiples of 16
+ * in [16, 2^31]; 16-byte aligned pointer and ld * elem_size; FP8_EINVAL / FP8_EALIGN otherwise). */
 typedef struct {
   const void* ptr;
   fp8_dtype_t dtype;

@@ -205,6 +205,8 @@ static fp8_status_t check_hp(const fp8_hp_t& x, const char* name, bool need_ptr 
   if (x.ld < x.cols) return fail(FP8_EINVAL, "%s: ld < cols", name);
   if ((x.ld * (int64_t)esize(x.dtype)) % 16) return fail(FP8_EALIGN, "%s: ld*elem_size must be a multiple of 16", name);
   if (x.rows > (int64_t)1 << 31 || x.cols > (int64_t)1 << 31) return fail(FP8_EINVAL, "%s: dims too large", name);
+  // the tile casts address the rows of a 128-row tile by 32-bit offsets from the tile's first row
+  if (x.ld > (int64_t)1 << 25) return fail(FP8_EINVAL, "%s: ld too large (> 2^25 elements)", name);
   if (need_ptr && !x.ptr) return fail(FP8_EINVAL, "%s: null pointer", name);
   if (x.ptr && !aligned16(x.ptr)) return fail(FP8_EALIGN, "%s: pointer not 16-byte aligned", name);
   return FP8_OK;

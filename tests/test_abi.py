@@ -73,6 +73,11 @@ def test_validation_returns_before_launch(L):
     # bad format
     t = L.Tensor8(16, None, 32, None, None, None, 7, L.GRAN_TENSOR, 128, 96)
     assert L.lib.fp8_cast_scaled(L.HP(16, L.DT_BF16, 128, 96, 96), 0, None, ctypes.byref(t), None, 0, None) == L.FP8_EINVAL
+    # ld beyond 2^25 elements (the tile casts' 32-bit row offsets) -> FP8_EINVAL before any launch
+    t = L.Tensor8(16, None, 32, None, None, None, L.E4M3, L.GRAN_TENSOR, 128, 96)
+    assert L.lib.fp8_cast_scaled(L.HP(16, L.DT_BF16, 128, 96, (1 << 25) + 8), 0, None, ctypes.byref(t), None, 0,
+                                 None) == L.FP8_EINVAL
+    assert b"ld too large" in L.lib.fp8_last_error()
     # amax gran ROW_COL is not an amax unit
     assert L.lib.fp8_amax(L.HP(16, L.DT_BF16, 128, 96, 96), L.GRAN_ROW_COL, 16, None, 0, None) == L.FP8_EINVAL
     # GEMM K not multiple of 16
