@@ -823,17 +823,22 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = 0.f;
         } else if (row_scales) {
-          // lane j computes 1/sb for column col0 + j once; the warp shares them by shuffles.  Two columns per
+          // lane j computes 1/sb for column col0 + j once and parks it in the warp's (free) staging buffer; every
+          // lane reads the 32 values back as 8 broadcast 16-byte loads (instead of 32 shuffles).  Two columns per
           // __fmul2_rn (IEEE RN per lane: the same roundings, in the same order, as two __fmul_rn)
-          const float rcol = __frcp_rn(sb[min(col0 + (int)lane, N - 1)]);
+          reinterpret_cast<float*>(epi)[lane] = __frcp_rn(sb[min(col0 + (int)lane, N - 1)]);
+          __syncwarp();
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const float2 a2 = __fmul2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), make_float2(rs, rs));
-            const float2 c2 = make_float2(__shfl_sync(0xffffffffu, rcol, j), __shfl_sync(0xffffffffu, rcol, j + 1));
-            const float2 p2 = __fmul2_rn(a2, c2);
-            v[j] = p2.x;
-            v[j + 1] = p2.y;
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const float4 c4 = reinterpret_cast<const float4*>(epi)[q4];
+            const int j = 4 * q4;
+            const float2 a0 = __fmul2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), make_float2(rs, rs));
+            const float2 a1 = __fmul2_rn(make_float2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])), make_float2(rs, rs));
+            const float2 p0 = __fmul2_rn(a0, make_float2(c4.x, c4.y));
+            const float2 p1 = __fmul2_rn(a1, make_float2(c4.z, c4.w));
+            v[j] = p0.x; v[j + 1] = p0.y; v[j + 2] = p1.x; v[j + 3] = p1.y;
           }
+          __syncwarp();   // every lane has read the scales before the staging writes below reuse the buffer
         } else {
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
@@ -971,15 +976,23 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
               return;
             }
             float v[32];
-            if (row_scales) {
-              const float rcol = __frcp_rn(sb[col0 + 32 * c + (int)lane]);
+            if (row_scales) {   // column scales through the chunk buffer (broadcast loads), as in process()
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");   // buffer c & 1 free
+              __syncwarp();
+              float* rcb = reinterpret_cast<float*>(epi + (c & 1) * 2048);
+              rcb[lane] = __frcp_rn(sb[col0 + 32 * c + (int)lane]);
+              __syncwarp();
 #pragma unroll
-              for (int j = 0; j < 32; j += 2) {
-                const float2 a2 = __fmul2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), make_float2(rs, rs));
-                const float2 p2 = __fmul2_rn(a2, make_float2(__shfl_sync(0xffffffffu, rcol, j), __shfl_sync(0xffffffffu, rcol, j + 1)));
-                v[j] = p2.x;
-                v[j + 1] = p2.y;
+              for (int q4 = 0; q4 < 8; ++q4) {
+                const float4 c4 = reinterpret_cast<const float4*>(rcb)[q4];
+                const int j = 4 * q4;
+                const float2 a0 = __fmul2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), make_float2(rs, rs));
+                const float2 a1 = __fmul2_rn(make_float2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])), make_float2(rs, rs));
+                const float2 p0 = __fmul2_rn(a0, make_float2(c4.x, c4.y));
+                const float2 p1 = __fmul2_rn(a1, make_float2(c4.z, c4.w));
+                v[j] = p0.x; v[j + 1] = p0.y; v[j + 2] = p1.x; v[j + 3] = p1.y;
               }
+              __syncwarp();
             } else {
 #pragma unroll
               for (int j = 0; j < 32; j += 2) {
