@@ -883,13 +883,17 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
           *reinterpret_cast<uint4*>(epi + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16)) =
               make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         __syncwarp();
+        // row 8 i + (lane >> 2) of the warp's 32: one 64-bit base per chunk, 8 rows further per store
+        const int jq = lane & 3;
+        const int grow0 = row - (int)lane + ((int)lane >> 2);
+        __nv_bfloat16* dq = reinterpret_cast<__nv_bfloat16*>(Dbase) + (int64_t)grow0 * P.ldd + col0 + 8 * jq;
+        const int64_t dstep = 8 * P.ldd;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int rr = 8 * i + ((int)lane >> 2), j = lane & 3;
-          const uint4 val = *reinterpret_cast<const uint4*>(epi + rr * 64 + ((j ^ ((rr >> 1) & 3)) * 16));
-          const int grow = row - (int)lane + rr;
-          if (grow < ti.m_valid && 8 * j < nvalid) {
-            uint4* dp = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(Dbase) + (int64_t)grow * P.ldd + col0 + 8 * j);
+          const int rr = 8 * i + ((int)lane >> 2);
+          const uint4 val = *reinterpret_cast<const uint4*>(epi + rr * 64 + ((jq ^ ((rr >> 1) & 3)) * 16));
+          if (grow0 + 8 * i < ti.m_valid && 8 * jq < nvalid) {
+            uint4* dp = reinterpret_cast<uint4*>(dq + i * dstep);
             if (st_ef) st_global_v4_hint(dp, val, st_pol);
             else *dp = val;
           }
