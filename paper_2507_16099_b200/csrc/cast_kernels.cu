@@ -1093,10 +1093,17 @@ __global__ void __launch_bounds__(256, (ST == 2 && !TR1) ? 3 : 1) mx_cast_tma_ke
   }
   __syncthreads();
   const int cc = (t & 15) * 8, rbase = 8 * (t >> 4);
-  for (int k = 0;; ++k) {
+  // tiles b, b + G, b + 2G, ...: (row, column) tile by a cursor -- G = gq * tiles_x + gr, one compare per step
+  const int gq = G / tiles_x, gr = G - gq * tiles_x;
+  int trow = (int)blockIdx.x / tiles_x, tcol = (int)blockIdx.x - trow * tiles_x;
+  for (int k = 0;; ++k, trow += gq, tcol += gr) {
+    if (tcol >= tiles_x) {
+      tcol -= tiles_x;
+      ++trow;
+    }
     const int id = (int)blockIdx.x + k * G;
     if (id >= num_tiles) break;
-    const int64_t r0 = (int64_t)(id / tiles_x) * 128, c0 = (int64_t)(id % tiles_x) * 128;
+    const int64_t r0 = (int64_t)trow * 128, c0 = (int64_t)tcol * 128;
     mbar_wait(bar0 + 8 * (k % ST), (uint32_t)(k / ST) & 1u);
     uint4 raw[8];
     const uint8_t* sp = sm + (k % ST) * L::STAGE + rbase * 256 + cc * 2;
