@@ -692,27 +692,29 @@ __device__ __forceinline__ void cast_tile_body(const T* __restrict__ x, int64_t 
   const int64_t r0 = (int64_t)by * 128, c0 = (int64_t)bx * 128;
   const int vrows = imin128(R - r0), vcols = imin128(C - c0);
 
-  // Per-tile scale vectors (and the scale outputs).
-  auto fill = [&](int mode, const float* amax, float* sv, float* out) {
+  // Per-tile scale vectors (and the scale outputs).  `u` is the filling thread's index: with per-row AND
+  // per-column vectors the rows are filled by threads 0..127 and the columns by threads 128..255, in parallel.
+  auto fill = [&](int mode, const float* amax, float* sv, float* out, int u) {
+    if (u < 0) return;
     if (mode == 1) {
-      if (t == 0) {
+      if (u == 0) {
         const float s = scale_of<FMT>(amax[0]);
         sv[0] = s;
         if (out && bx == 0 && by == 0) out[0] = s;
       }
     } else if (mode == 2) {
-      if (t < vrows) {
-        const float s = scale_of<FMT>(amax[r0 + t]);
-        sv[t] = s;
-        if (out && bx == 0) out[r0 + t] = s;
+      if (u < vrows) {
+        const float s = scale_of<FMT>(amax[r0 + u]);
+        sv[u] = s;
+        if (out && bx == 0) out[r0 + u] = s;
       }
     } else if (mode == 3) {   // per column (per segment of rows in the grouped recipe)
-      if (t < vcols) {
+      if (u < vcols) {
         int64_t sstart;
         const int64_t cbase = (int64_t)seg_of(seg, r0, sstart) * C;
-        const float s = scale_of<FMT>(amax[cbase + c0 + t]);
-        sv[t] = s;
-        if (out && r0 == sstart) out[cbase + c0 + t] = s;
+        const float s = scale_of<FMT>(amax[cbase + c0 + u]);
+        sv[u] = s;
+        if (out && r0 == sstart) out[cbase + c0 + u] = s;
       }
     }
   };
@@ -730,8 +732,14 @@ __device__ __forceinline__ void cast_tile_body(const T* __restrict__ x, int64_t 
   }
   const int64_t orow = (r0 + (t >> 4)) * C + c0 + cc;
   const uint32_t ostep = 16u * (uint32_t)C;
-  fill(QM, amax_q, sq, scale_q);
-  fill(TM, amax_t, st, scale_t);
+  constexpr bool split = QM >= 2 && TM >= 2 && QM != TM;   // a row and a column vector: one half of the CTA each
+  if (split) {
+    if (t < 128) fill(QM, amax_q, sq, scale_q, t);
+    else fill(TM, amax_t, st, scale_t, t - 128);
+  } else {
+    fill(QM, amax_q, sq, scale_q, t);
+    fill(TM, amax_t, st, scale_t, t);
+  }
   __syncthreads();
 
 #pragma unroll
