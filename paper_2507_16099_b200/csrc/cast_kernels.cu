@@ -1117,14 +1117,12 @@ __global__ void __launch_bounds__(256, (ST == 2 && !TR1) ? 3 : 1) mx_cast_tma_ke
     const uint8_t* sp = sm + (k % ST) * L::STAGE + rbase * 256 + cc * 2;
 #pragma unroll
     for (int i = 0; i < 8; ++i) raw[i] = *reinterpret_cast<const uint4*>(sp + i * 256);
-    __syncthreads();                       // (1) stage consumed by every thread
-    if (t == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (!TS) {
+    if (!TS) {   // TS: the stage is overwritten by this tile's codes only after barrier (2), which every thread
+                 // reaches after its loads above -- no barrier of its own
+      __syncthreads();                     // (1) stage consumed by every thread
+      if (t == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(k + ST);
-      } else if (k > 0) {   // tile k-1's stores have been issued from its stage: refill it once they read it
-        bulk_wait_read0();
-        issue(k - 1 + ST);
       }
     }
 
@@ -1163,6 +1161,11 @@ __global__ void __launch_bounds__(256, (ST == 2 && !TR1) ? 3 : 1) mx_cast_tma_ke
       for (int j = 0; j < 4; ++j) cmw[j] = __vmaxu2(cmw[j], __shfl_xor_sync(0xffffffffu, cmw[j], 16));
       if (lane < 16) *reinterpret_cast<uint4*>(&red[warp][cc >> 1]) = make_uint4(cmw[0], cmw[1], cmw[2], cmw[3]);
       __syncthreads();                     // (2)
+      if (TS && t == 0 && k > 0) {   // tile k-1's code stores were issued from its stage: refill it once read
+        bulk_wait_read0();
+        fence_proxy_async_smem();
+        issue(k - 1 + ST);
+      }
       {
         const int j = t >> 6, wp = t & 63;   // 32-row block j, columns 2wp, 2wp+1
         const uint32_t m2 = __vmaxu2(red[2 * j][wp], red[2 * j + 1][wp]);

@@ -6,7 +6,7 @@ CMD="$*"
 L=paper_2507_16099_b200/libfp8train.so
 cp $L /tmp/_new_lib.so
 for r in $(seq 1 $R); do
-  for tag in new old; do
+  for tag in ${ORDER:-new old}; do
     if [ $tag = old ]; then cp _old_lib.so $L; else cp /tmp/_new_lib.so $L; fi
     c=${CMD//\{tag\}/$tag}; c=${c//\{r\}/$r}
     bash -c "$c"
