@@ -818,6 +818,20 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
       // scale + convert + store 32 columns [col0, col0 + 32) of this thread's row
       auto process = [&](const uint32_t (&r)[32], int col0) {
         if (col0 >= N || (args.debug & 1)) return;   // warp-uniform
+        const int nvalid = min(32, N - col0);  // 16 or 32 (N % 16 == 0)
+        uint32_t pk[16];
+        bool packed = false;
+        if constexpr (MX) {   // block scales are applied inside the MMA (rs = 1, exact): convert straight from TMEM
+          if (!out_f32) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            packed = true;
+          }
+        }
+        if (!packed) {
         float v[32];
         if (kzero) {
 #pragma unroll
@@ -847,7 +861,6 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
             v[j + 1] = p2.y;
           }
         }
-        const int nvalid = min(32, N - col0);  // 16 or 32 (N % 16 == 0)
         if (out_f32) {
           if (!rvalid) return;
           float* dst = reinterpret_cast<float*>(Dbase) + (int64_t)row * P.ldd + col0;
@@ -862,11 +875,11 @@ __global__ void __launch_bounds__(Layout<MX, CG, ST, KS, BF, GRP, E8, BNT>::THRE
               reinterpret_cast<float4*>(dst)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           return;
         }
-        uint32_t pk[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
           pk[j] = *reinterpret_cast<uint32_t*>(&h);
+        }
         }
         if (P.out_amax && rvalid) {   // amax of the bf16-rounded outputs (what a consumer reads)
           uint32_t m2 = 0;
